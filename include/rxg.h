@@ -1,0 +1,188 @@
+/*
+ * rxg.h — C ABI of the B200 lockstep regular-expression matcher.
+ *
+ * This is the drop-in boundary for the reference's matcher API
+ * (arxiv/paper_1108_3126, proj/include/rx). Plain pointers and sizes only; no
+ * C++ or torch types. Every entry point returns an int status (RXG_OK = 0);
+ * rxg_last_error() gives a thread-local detail string for the last failure.
+ *
+ * Reference interface each entry point replaces (file:line under proj/):
+ *   rxg_parse_compile       rx::parse (include/rx/regex.hpp:60, src/regex.cpp:186-194)
+ *                           + rx::compile (include/rx/heap.hpp:43, src/heap.cpp:13-72)
+ *   rxg_dump / rxg_parse_dump  rx::dump / rx::parse_dump (include/rx/heap.hpp:68-69)
+ *   rxg_check_knode         rx::check_knode (include/rx/heap.hpp:52, src/heap.cpp:106-128)
+ *   rxg_heap_create         (new) uploads a compiled rx::Heap {nodes, knodes}
+ *                           (include/rx/heap.hpp:28-37) and its derived tables to a GPU
+ *   rxg_match_one           rx::lockstep_accepts(const Heap&, InputView, LockstepStats*)
+ *                           (include/rx/lockstep.hpp:43, src/lockstep.cpp:75-82);
+ *                           engine RXG_ENGINE_ROUNDS / PERNODE reproduce rx::par_accepts
+ *                           (include/rx/parallel.hpp:102, src/parallel.cpp:192-195)
+ *   rxg_match_batch*        rx::lockstep_accepts over every line of a buffer, the loop of
+ *                           `rxvm match` (tools/rxvm.cpp:100-112, std::getline semantics)
+ *   rxg_match_batch_multi   the same, sharded over several GPUs with one count all-reduce
+ *
+ * Symbols are bytes. For patterns whose literals are all ASCII (< 0x80) this
+ * is exact for any valid UTF-8 input: a multi-byte sequence decodes to one
+ * scalar that no position matches, and feeding its bytes kills the active set
+ * just the same. Patterns with non-ASCII literals are rejected with
+ * RXG_EUNSUPPORTED by the byte-level matchers.
+ */
+#ifndef RXG_H
+#define RXG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes */
+#define RXG_OK 0
+#define RXG_EINVAL 1        /* bad argument (null pointer, bad size, misaligned buffer) */
+#define RXG_EPARSE 2        /* pattern syntax error; rx::ParseError (regex.hpp:50-54) */
+#define RXG_EUTF8 3         /* malformed UTF-8 pattern; decode_utf8 (utf8.cpp:32-41) */
+#define RXG_EUNSUPPORTED 4  /* pattern literal >= 0x80 on a byte-level matcher */
+#define RXG_ECUDA 5         /* CUDA runtime error */
+#define RXG_ENOMEM 6        /* allocation failed */
+#define RXG_ETOOBIG 7       /* memoized step table exceeds the shared-memory budget */
+#define RXG_ENCCL 8         /* NCCL unavailable or failed */
+#define RXG_EHEAP 9         /* malformed heap table */
+#define RXG_ENODEV 10       /* handle has no device tables (created with device < 0) */
+
+/* node kinds, rx::Node::Kind order (heap.hpp:18) */
+#define RXG_NODE_EPS 0
+#define RXG_NODE_CHR 1
+#define RXG_NODE_ALT 2
+#define RXG_NODE_SEQ 3
+#define RXG_NODE_STAR 4
+
+/* single-string engines (rxg_match_one*) */
+#define RXG_ENGINE_AUTO 0     /* fastest available */
+#define RXG_ENGINE_DFA_SEQ 1  /* one thread walks the memoized step table */
+#define RXG_ENGINE_PERNODE 2  /* K1: paper §8 thread-per-node lockstep, bitset form, one CTA */
+#define RXG_ENGINE_ROUNDS 3   /* literal §8 protocol: one thread per heap node, c/n stamps, rounds */
+#define RXG_ENGINE_CHUNKED 4  /* chunk-parallel walk of the step table (all SMs) */
+
+/* Byte layout identical to rx::Node (heap.hpp:17-23): 16 bytes. */
+typedef struct rxg_node {
+    uint8_t kind;
+    uint8_t pad[3];
+    uint32_t sym;
+    int32_t left;
+    int32_t right;
+} rxg_node;
+
+typedef struct rxg_heap rxg_heap;
+
+typedef struct rxg_heap_info {
+    int32_t nodes;         /* N */
+    int32_t positions;     /* |C| (Chr nodes) */
+    int32_t words;         /* W = ceil((|C|+1)/32) */
+    int32_t classes;       /* byte classes (class 0 = matches nothing) */
+    int32_t dfa_states;    /* memoized E sets (0 if over the cap) */
+    int32_t byte_symbols;  /* 1 if every literal is ASCII */
+    int32_t device;        /* CUDA device, or -1 for a host-only handle */
+    int32_t nullable;      /* root eps-reaches null: the empty string matches */
+    uint32_t line_table_bytes;   /* shared-memory image for '\n' lines (0 if none) */
+    uint32_t plain_table_bytes;  /* shared-memory image for single strings / fixed stride */
+} rxg_heap_info;
+
+const char* rxg_strerror(int status);
+const char* rxg_last_error(void);
+const char* rxg_version(void);
+
+/* ── front end (host only; no GPU needed) ─────────────────────────────── */
+
+/* Parse + compile. Writes min(n, cap) nodes/knodes; *n_out = N. On
+ * RXG_EPARSE / RXG_EUTF8, *err_pos is the scalar / byte offset. */
+int rxg_parse_compile(const char* pattern, size_t len, rxg_node* nodes, int32_t* knodes,
+                      int32_t cap, int32_t* n_out, size_t* err_pos);
+
+/* Canonical printer (rx::print, regex.hpp:65). Writes a NUL-terminated string. */
+int rxg_print(const char* pattern, size_t len, char* out, size_t cap, size_t* out_len);
+
+/* Heap dump text (three tab-separated columns per address). */
+int rxg_dump(const rxg_node* nodes, const int32_t* knodes, int32_t n, char* out, size_t cap,
+             size_t* out_len);
+int rxg_parse_dump(const char* text, size_t len, rxg_node* nodes, int32_t* knodes, int32_t cap,
+                   int32_t* n_out);
+int rxg_check_knode(const rxg_node* nodes, const int32_t* knodes, int32_t n, int32_t* ok);
+
+/* ── compiled heap handle ─────────────────────────────────────────────── */
+
+/* device >= 0: upload tables to that GPU. device < 0: host-only handle
+ * (front end, derived tables and DFA; no kernels). */
+int rxg_heap_create(const rxg_node* nodes, const int32_t* knodes, int32_t n, int device,
+                    rxg_heap** out);
+int rxg_heap_create_pattern(const char* pattern, size_t len, int device, rxg_heap** out);
+void rxg_heap_destroy(rxg_heap* h);
+int rxg_heap_info_get(const rxg_heap* h, rxg_heap_info* info);
+
+/* Derived tables of the position form, for tests/tools.
+ * pos_addr: |C| heap addresses; follow: (|C|+1)*W words; init: W words. */
+int rxg_heap_tables(const rxg_heap* h, int32_t* pos_addr, uint32_t* follow, uint32_t* init);
+
+/* Host walk of the memoized step (no GPU): E sets after each symbol.
+ * sets_out: (len+1)*W words (row 0 = E_0), may be null; *accept set. */
+int rxg_host_walk(const rxg_heap* h, const uint8_t* bytes, uint64_t len, uint32_t* sets_out,
+                  int32_t* accept);
+
+/* Host emulation of the batch kernels (same table image, same chunk
+ * ownership / SKIP / tail rules), for CPU tests of the device logic.
+ * chunk: bytes per chain (multiple of 16; 0 = default). */
+int rxg_host_emulate_batch(const rxg_heap* h, const uint8_t* text, uint64_t len, int32_t delimiter,
+                           uint32_t stride, uint32_t chunk, uint64_t* count, uint8_t* results);
+
+/* ── matching ─────────────────────────────────────────────────────────── */
+
+/* One string, host buffer (synchronous). */
+int rxg_match_one(rxg_heap* h, const uint8_t* bytes, uint64_t len, int engine, int32_t* accept);
+
+/* One string, device buffer, asynchronous on `stream` (cudaStream_t or NULL).
+ * d_accept is a device int32. */
+int rxg_match_one_device(rxg_heap* h, const uint8_t* d_bytes, uint64_t len, int engine,
+                         int32_t* d_accept, void* stream);
+
+/* Batch over a device buffer, asynchronous on `stream`.
+ *   delimiter in [0,255]: strings are the lines of the buffer split on that
+ *     byte (the delimiter is not part of a string; a final unterminated
+ *     segment is a string, a trailing delimiter does not open one);
+ *   delimiter < 0: fixed stride, strings text[i*stride, (i+1)*stride).
+ * d_count (device u64) receives the number of matching strings (it is
+ * overwritten). d_results (device, nullable) receives one 0/1 byte per
+ * string; it needs room for (#delimiters + 1) bytes in line mode. d_text
+ * must be 16-byte aligned. */
+int rxg_match_batch(rxg_heap* h, const uint8_t* d_text, uint64_t len, int32_t delimiter,
+                    uint32_t stride, unsigned long long* d_count, uint8_t* d_results,
+                    void* stream);
+
+/* Same, host buffers; copies in and out inside the call (synchronous). */
+int rxg_match_batch_host(rxg_heap* h, const uint8_t* text, uint64_t len, int32_t delimiter,
+                         uint32_t stride, uint64_t* count, uint8_t* results);
+
+/* Byte-balanced sharding of a host buffer over `ndev` GPUs (split at string
+ * boundaries), one stream per device, and one NCCL all-reduce of the int64
+ * match count across the devices (the only inter-GPU traffic). */
+int rxg_match_batch_multi(const int* devices, int ndev, const char* pattern, size_t plen,
+                          const uint8_t* text, uint64_t len, int32_t delimiter, uint32_t stride,
+                          uint64_t* count, uint8_t* results);
+
+/* Shard boundaries used by rxg_match_batch_multi: offsets[0..ndev], split at
+ * delimiter boundaries (line mode) or stride multiples. Host only. */
+int rxg_shard_bounds(const uint8_t* text, uint64_t len, int32_t delimiter, uint32_t stride,
+                     int ndev, uint64_t* offsets);
+
+/* Number of kernels the last matching call on this thread launched. */
+int rxg_last_launch_count(void);
+
+/* ── synthetic workloads of SURVEY.md §8(d) (host only) ───────────────── */
+int rxg_synth_pattern(char config, char* out, size_t cap, size_t* out_len);
+uint64_t rxg_synth_input_size(char config);
+int rxg_synth_input(char config, uint64_t seed, uint8_t* out, uint64_t cap, uint64_t* written);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RXG_H */

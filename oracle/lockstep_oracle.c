@@ -1,0 +1,274 @@
+/*
+ * TEST INFRASTRUCTURE — CPU oracle for the B200 lockstep matcher.
+ *
+ * A plain-C restatement of the reference's sequential lockstep machine
+ * (arxiv/paper_1108_3126, proj/src/lockstep.cpp) over the compiled heap
+ * table {nodes, knodes} (proj/include/rx/heap.hpp:17-37). It is the checker
+ * the parity tests compare the CUDA kernels against, and the "port" kind of
+ * the bench's cpu_baseline. The product library never links or calls it.
+ *
+ * Pinned against the reference two ways (tests/test_oracle.py):
+ *   - the golden vectors of proj/tests/test_lockstep.cpp:15-58 and the
+ *     exhaustive small suite of test_lockstep.cpp:60-72 / acceptance
+ *     criterion 3 (acceptance_main.cpp:93-105), via tests/golden/;
+ *   - against oracle/_ref (the reference's own lockstep.cpp compiled from its
+ *     sources by oracle/Makefile) on seeded random cases.
+ *
+ * Function-by-function correspondence:
+ *   eps_successors     proj/src/pwpi.cpp:9-20
+ *   evolve             proj/src/lockstep.cpp:10-40   (FIFO worklist + seen)
+ *   eps_reaches_null   proj/src/lockstep.cpp:42-62
+ *   step_char          proj/src/lockstep.cpp:64-73
+ *   lockstep_accepts   proj/src/lockstep.cpp:75-82
+ */
+#include "lockstep_oracle.h"
+
+#include <pthread.h>
+#include <stdlib.h>
+#include <string.h>
+
+enum { EPS = 0, CHR = 1, ALT = 2, SEQ = 3, STAR = 4 };
+
+/* pwpi.cpp:9-20: unlabeled successors in fixed order; may contain null (-1). */
+static int eps_successors(const oracle_heap* h, int32_t p, int32_t out[2]) {
+    const oracle_node* n = &h->nodes[p];
+    switch (n->kind) {
+    case ALT: out[0] = n->left; out[1] = n->right; return 2;
+    case SEQ: out[0] = n->left; return 1;
+    case STAR: out[0] = n->left; out[1] = h->knodes[p]; return 2;
+    case EPS: out[0] = h->knodes[p]; return 1;
+    default: return 0;
+    }
+}
+
+void oracle_ws_init(oracle_ws* ws, int32_t n) {
+    ws->n = n;
+    ws->seen = (uint32_t*)calloc((size_t)n, sizeof(uint32_t));
+    ws->queue = (int32_t*)malloc((size_t)(n + 1) * sizeof(int32_t));
+    ws->epoch = 0;
+}
+
+void oracle_ws_free(oracle_ws* ws) {
+    free(ws->seen);
+    free(ws->queue);
+    ws->seen = NULL;
+    ws->queue = NULL;
+}
+
+static uint32_t next_epoch(oracle_ws* ws) {
+    if (++ws->epoch == 0) {
+        memset(ws->seen, 0, (size_t)ws->n * sizeof(uint32_t));
+        ws->epoch = 1;
+    }
+    return ws->epoch;
+}
+
+/* lockstep.cpp:10-35: the character nodes eps-reachable from s, FIFO order,
+ * each address enqueued at most once; null members ignored. `out` receives
+ * the Chr addresses in discovery order; returns their count. *enqueued (if
+ * non-null) is incremented like LockstepStats::enqueued. */
+int32_t oracle_evolve(const oracle_heap* h, oracle_ws* ws, const int32_t* s, int32_t ns, int32_t* out,
+                      uint64_t* enqueued) {
+    const uint32_t ep = next_epoch(ws);
+    int32_t head = 0, tail = 0, nout = 0;
+    for (int32_t i = 0; i < ns; ++i) {
+        const int32_t p = s[i];
+        if (p < 0 || ws->seen[p] == ep) continue;
+        ws->seen[p] = ep;
+        ws->queue[tail++] = p;
+        if (enqueued) ++*enqueued;
+    }
+    while (head < tail) {
+        const int32_t p = ws->queue[head++];
+        if (h->nodes[p].kind == CHR) {
+            out[nout++] = p;
+            continue;
+        }
+        int32_t succ[2];
+        const int k = eps_successors(h, p, succ);
+        for (int j = 0; j < k; ++j) {
+            const int32_t q = succ[j];
+            if (q < 0 || ws->seen[q] == ep) continue;
+            ws->seen[q] = ep;
+            ws->queue[tail++] = q;
+            if (enqueued) ++*enqueued;
+        }
+    }
+    return nout;
+}
+
+/* lockstep.cpp:42-62 */
+int oracle_eps_reaches_null(const oracle_heap* h, oracle_ws* ws, const int32_t* s, int32_t ns) {
+    for (int32_t i = 0; i < ns; ++i)
+        if (s[i] < 0) return 1;
+    const uint32_t ep = next_epoch(ws);
+    int32_t head = 0, tail = 0;
+    for (int32_t i = 0; i < ns; ++i) {
+        if (ws->seen[s[i]] == ep) continue;
+        ws->seen[s[i]] = ep;
+        ws->queue[tail++] = s[i];
+    }
+    while (head < tail) {
+        const int32_t p = ws->queue[head++];
+        int32_t succ[2];
+        const int k = eps_successors(h, p, succ);
+        for (int j = 0; j < k; ++j) {
+            const int32_t q = succ[j];
+            if (q < 0) return 1;
+            if (ws->seen[q] == ep) continue;
+            ws->seen[q] = ep;
+            ws->queue[tail++] = q;
+        }
+    }
+    return 0;
+}
+
+/* lockstep.cpp:64-73: knode of every Chr member labeled a (null skipped);
+ * set semantics: duplicates removed. Returns the count, or -1 when a member
+ * is neither null nor a Chr node (the reference throws invalid_argument). */
+int32_t oracle_step_char(const oracle_heap* h, oracle_ws* ws, const int32_t* e, int32_t ne, uint32_t a,
+                         int32_t* out) {
+    const uint32_t ep = next_epoch(ws);
+    int32_t nout = 0;
+    int have_null = 0;
+    for (int32_t i = 0; i < ne; ++i) {
+        const int32_t p = e[i];
+        if (p < 0) continue;
+        if (h->nodes[p].kind != CHR) return -1;
+        if (h->nodes[p].sym != a) continue;
+        const int32_t q = h->knodes[p];
+        if (q < 0) {
+            if (!have_null) out[nout++] = -1;
+            have_null = 1;
+        } else if (ws->seen[q] != ep) {
+            ws->seen[q] = ep;
+            out[nout++] = q;
+        }
+    }
+    return nout;
+}
+
+/* lockstep.cpp:75-82. Sets are kept as address lists; S holds at most n+1
+ * entries (every address plus null). */
+int oracle_lockstep_accepts(const oracle_heap* h, oracle_ws* ws, const uint32_t* w, uint64_t len,
+                            int32_t* buf_a, int32_t* buf_b, uint64_t* enqueued) {
+    int32_t* s = buf_a;
+    int32_t* e = buf_b;
+    int32_t ns = 1;
+    s[0] = 0;
+    for (uint64_t i = 0; i < len; ++i) {
+        const int32_t ne = oracle_evolve(h, ws, s, ns, e, enqueued);
+        ns = oracle_step_char(h, ws, e, ne, w[i], s);
+        if (ns <= 0) return 0;
+    }
+    return oracle_eps_reaches_null(h, ws, s, ns);
+}
+
+int oracle_accepts_bytes(const oracle_heap* h, const uint8_t* bytes, uint64_t len) {
+    oracle_ws ws;
+    oracle_ws_init(&ws, h->n);
+    int32_t* a = (int32_t*)malloc((size_t)(h->n + 1) * sizeof(int32_t));
+    int32_t* b = (int32_t*)malloc((size_t)(h->n + 1) * sizeof(int32_t));
+    uint32_t* w = (uint32_t*)malloc((len ? len : 1) * sizeof(uint32_t));
+    for (uint64_t i = 0; i < len; ++i) w[i] = bytes[i];
+    const int r = oracle_lockstep_accepts(h, &ws, w, len, a, b, NULL);
+    free(w);
+    free(a);
+    free(b);
+    oracle_ws_free(&ws);
+    return r;
+}
+
+/* ── batch driver (std::getline semantics of rxvm.cpp:100-112) ──────── */
+
+typedef struct {
+    const oracle_heap* h;
+    const uint8_t* text;
+    const uint64_t* starts;
+    const uint64_t* lens;
+    uint64_t nstr;
+    uint8_t* results;
+    int tid, nthreads;
+    uint64_t count;
+} job_t;
+
+static void* run_job(void* arg) {
+    job_t* j = (job_t*)arg;
+    oracle_ws ws;
+    oracle_ws_init(&ws, j->h->n);
+    int32_t* a = (int32_t*)malloc((size_t)(j->h->n + 1) * sizeof(int32_t));
+    int32_t* b = (int32_t*)malloc((size_t)(j->h->n + 1) * sizeof(int32_t));
+    uint64_t cap = 1024;
+    uint32_t* w = (uint32_t*)malloc(cap * sizeof(uint32_t));
+    /* static interleaved partition, crosscheck.cpp:121 */
+    for (uint64_t k = (uint64_t)j->tid; k < j->nstr; k += (uint64_t)j->nthreads) {
+        const uint64_t len = j->lens[k];
+        if (len > cap) {
+            cap = len * 2;
+            w = (uint32_t*)realloc(w, cap * sizeof(uint32_t));
+        }
+        const uint8_t* src = j->text + j->starts[k];
+        for (uint64_t i = 0; i < len; ++i) w[i] = src[i];
+        const int r = oracle_lockstep_accepts(j->h, &ws, w, len, a, b, NULL);
+        if (j->results) j->results[k] = (uint8_t)r;
+        j->count += (uint64_t)r;
+    }
+    free(w);
+    free(a);
+    free(b);
+    oracle_ws_free(&ws);
+    return NULL;
+}
+
+uint64_t oracle_split(const uint8_t* text, uint64_t len, int32_t delimiter, uint32_t stride, uint64_t* starts,
+                      uint64_t* lens) {
+    uint64_t n = 0;
+    if (delimiter < 0) {
+        for (uint64_t at = 0; at + stride <= len; at += stride) {
+            if (starts) {
+                starts[n] = at;
+                lens[n] = stride;
+            }
+            ++n;
+        }
+        return n;
+    }
+    uint64_t at = 0;
+    while (at < len) {
+        const uint8_t* hit = (const uint8_t*)memchr(text + at, delimiter, len - at);
+        const uint64_t end = hit ? (uint64_t)(hit - text) : len;
+        if (starts) {
+            starts[n] = at;
+            lens[n] = end - at;
+        }
+        ++n;
+        at = end + 1;
+    }
+    return n;
+}
+
+uint64_t oracle_match_batch(const oracle_heap* h, const uint8_t* text, uint64_t len, int32_t delimiter,
+                            uint32_t stride, uint8_t* results, int nthreads) {
+    const uint64_t n = oracle_split(text, len, delimiter, stride, NULL, NULL);
+    uint64_t* starts = (uint64_t*)malloc((n ? n : 1) * sizeof(uint64_t));
+    uint64_t* lens = (uint64_t*)malloc((n ? n : 1) * sizeof(uint64_t));
+    oracle_split(text, len, delimiter, stride, starts, lens);
+    if (nthreads < 1) nthreads = 1;
+    job_t* jobs = (job_t*)calloc((size_t)nthreads, sizeof(job_t));
+    pthread_t* th = (pthread_t*)calloc((size_t)nthreads, sizeof(pthread_t));
+    for (int t = 0; t < nthreads; ++t) {
+        jobs[t] = (job_t){h, text, starts, lens, n, results, t, nthreads, 0};
+        if (nthreads > 1) pthread_create(&th[t], NULL, run_job, &jobs[t]);
+    }
+    if (nthreads == 1) run_job(&jobs[0]);
+    uint64_t count = 0;
+    for (int t = 0; t < nthreads; ++t) {
+        if (nthreads > 1) pthread_join(th[t], NULL);
+        count += jobs[t].count;
+    }
+    free(jobs);
+    free(th);
+    free(starts);
+    free(lens);
+    return count;
+}

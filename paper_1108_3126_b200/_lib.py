@@ -1,0 +1,95 @@
+"""ctypes binding of the product library librxg.so (include/rxg.h).
+
+The library is built in-tree by ``paper_1108_3126_b200/build.py`` (or
+``__graft_entry__.build()``). There is no fallback: importing the binding
+without the built library raises immediately.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+LIB_PATH = Path(__file__).resolve().parent / "librxg.so"
+
+RXG_OK = 0
+RXG_EINVAL = 1
+RXG_EPARSE = 2
+RXG_EUTF8 = 3
+RXG_EUNSUPPORTED = 4
+RXG_ECUDA = 5
+RXG_ENOMEM = 6
+RXG_ETOOBIG = 7
+RXG_ENCCL = 8
+RXG_EHEAP = 9
+RXG_ENODEV = 10
+
+ENGINES = {"auto": 0, "dfa_seq": 1, "pernode": 2, "rounds": 3, "chunked": 4}
+
+
+class rxg_node(C.Structure):
+    _fields_ = [("kind", C.c_uint8), ("pad", C.c_uint8 * 3), ("sym", C.c_uint32),
+                ("left", C.c_int32), ("right", C.c_int32)]
+
+
+class rxg_heap_info(C.Structure):
+    _fields_ = [("nodes", C.c_int32), ("positions", C.c_int32), ("words", C.c_int32),
+                ("classes", C.c_int32), ("dfa_states", C.c_int32), ("byte_symbols", C.c_int32),
+                ("device", C.c_int32), ("nullable", C.c_int32),
+                ("line_table_bytes", C.c_uint32), ("plain_table_bytes", C.c_uint32)]
+
+
+# name -> (restype, argtypes). Every symbol declared in include/rxg.h.
+_P = C.c_void_p
+_SIG = {
+    "rxg_strerror": (C.c_char_p, [C.c_int]),
+    "rxg_last_error": (C.c_char_p, []),
+    "rxg_version": (C.c_char_p, []),
+    "rxg_parse_compile": (C.c_int, [C.c_char_p, C.c_size_t, C.POINTER(rxg_node), C.POINTER(C.c_int32),
+                                    C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_size_t)]),
+    "rxg_print": (C.c_int, [C.c_char_p, C.c_size_t, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]),
+    "rxg_dump": (C.c_int, [C.POINTER(rxg_node), C.POINTER(C.c_int32), C.c_int32, C.c_char_p, C.c_size_t,
+                           C.POINTER(C.c_size_t)]),
+    "rxg_parse_dump": (C.c_int, [C.c_char_p, C.c_size_t, C.POINTER(rxg_node), C.POINTER(C.c_int32), C.c_int32,
+                                 C.POINTER(C.c_int32)]),
+    "rxg_check_knode": (C.c_int, [C.POINTER(rxg_node), C.POINTER(C.c_int32), C.c_int32, C.POINTER(C.c_int32)]),
+    "rxg_heap_create": (C.c_int, [C.POINTER(rxg_node), C.POINTER(C.c_int32), C.c_int32, C.c_int, C.POINTER(_P)]),
+    "rxg_heap_create_pattern": (C.c_int, [C.c_char_p, C.c_size_t, C.c_int, C.POINTER(_P)]),
+    "rxg_heap_destroy": (None, [_P]),
+    "rxg_heap_info_get": (C.c_int, [_P, C.POINTER(rxg_heap_info)]),
+    "rxg_heap_tables": (C.c_int, [_P, _P, _P, _P]),
+    "rxg_host_walk": (C.c_int, [_P, _P, C.c_uint64, _P, C.POINTER(C.c_int32)]),
+    "rxg_host_emulate_batch": (C.c_int, [_P, _P, C.c_uint64, C.c_int32, C.c_uint32, C.c_uint32,
+                                         C.POINTER(C.c_uint64), _P]),
+    "rxg_match_one": (C.c_int, [_P, _P, C.c_uint64, C.c_int, C.POINTER(C.c_int32)]),
+    "rxg_match_one_device": (C.c_int, [_P, _P, C.c_uint64, C.c_int, _P, _P]),
+    "rxg_match_batch": (C.c_int, [_P, _P, C.c_uint64, C.c_int32, C.c_uint32, _P, _P, _P]),
+    "rxg_match_batch_host": (C.c_int, [_P, _P, C.c_uint64, C.c_int32, C.c_uint32, C.POINTER(C.c_uint64), _P]),
+    "rxg_match_batch_multi": (C.c_int, [C.POINTER(C.c_int), C.c_int, C.c_char_p, C.c_size_t, _P, C.c_uint64,
+                                        C.c_int32, C.c_uint32, C.POINTER(C.c_uint64), _P]),
+    "rxg_shard_bounds": (C.c_int, [_P, C.c_uint64, C.c_int32, C.c_uint32, C.c_int, C.POINTER(C.c_uint64)]),
+    "rxg_last_launch_count": (C.c_int, []),
+    "rxg_synth_pattern": (C.c_int, [C.c_char, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]),
+    "rxg_synth_input_size": (C.c_uint64, [C.c_char]),
+    "rxg_synth_input": (C.c_int, [C.c_char, C.c_uint64, _P, C.c_uint64, C.POINTER(C.c_uint64)]),
+}
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """The loaded product library; raises if it has not been built."""
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise ImportError(f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`")
+        l = C.CDLL(str(LIB_PATH))
+        for name, (res, args) in _SIG.items():
+            f = getattr(l, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = l
+    return _lib
+
+
+def declared_symbols() -> list[str]:
+    return list(_SIG)

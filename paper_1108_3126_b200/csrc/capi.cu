@@ -1,0 +1,750 @@
+// extern "C" boundary (include/rxg.h). Host C++ around the kernels: handle
+// lifetime, lazy per-delimiter table images, stream-ordered scratch, the
+// pipelined host-buffer path and the multi-GPU sharder.
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "rxg.h"
+#include "frontend.hpp"
+#include "launch.hpp"
+#include "program.hpp"
+#include "single.hpp"
+#include "synth.hpp"
+#include "tables.hpp"
+
+using namespace rxg;
+
+namespace {
+
+thread_local std::string g_err;
+thread_local int g_launches = 0;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+    return fail(RXG_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define RXG_CUDA(call)                                  \
+    do {                                                \
+        cudaError_t e_ = (call);                        \
+        if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
+    } while (0)
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        if (dev >= 0 && cudaGetDevice(&prev) == cudaSuccess && prev != dev) cudaSetDevice(dev);
+        else prev = -1;
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+struct TableSlot {
+    KTable host;
+    DevTable dev;
+    void* dptr = nullptr;
+};
+
+constexpr int32_t kMaxDfaStates = 16384;
+
+}  // namespace
+
+struct rxg_heap {
+    int device = -1;
+    Program prog;
+    bool dfa_ok = false;
+    Dfa dfa;
+    int smem_limit = 0;
+    std::mutex mu;
+    std::unique_ptr<TableSlot> plain;
+    std::map<int, std::unique_ptr<TableSlot>> lines;
+    // staging for host-buffer calls
+    uint8_t* d_stage[2] = {nullptr, nullptr};
+    size_t stage_bytes = 0;
+    unsigned long long* d_count = nullptr;
+    int32_t* d_accept = nullptr;
+    cudaStream_t stream = nullptr;
+    cudaStream_t copy_stream = nullptr;
+
+    ~rxg_heap() {
+        if (device < 0) return;
+        DeviceGuard g(device);
+        if (plain && plain->dptr) cudaFree(plain->dptr);
+        for (auto& kv : lines)
+            if (kv.second->dptr) cudaFree(kv.second->dptr);
+        for (auto* p : d_stage)
+            if (p) cudaFree(p);
+        if (d_count) cudaFree(d_count);
+        if (d_accept) cudaFree(d_accept);
+        if (stream) cudaStreamDestroy(stream);
+        if (copy_stream) cudaStreamDestroy(copy_stream);
+    }
+};
+
+namespace {
+
+int upload(rxg_heap* h, std::unique_ptr<TableSlot>& slot, KTable&& kt) {
+    if (static_cast<int>(kt.img.size()) > h->smem_limit)
+        return fail(RXG_ETOOBIG, "step table needs " + std::to_string(kt.img.size()) +
+                                     " B of shared memory, limit " + std::to_string(h->smem_limit));
+    auto s = std::make_unique<TableSlot>();
+    s->host = std::move(kt);
+    RXG_CUDA(cudaMalloc(&s->dptr, s->host.img.size()));
+    RXG_CUDA(cudaMemcpy(s->dptr, s->host.img.data(), s->host.img.size(), cudaMemcpyHostToDevice));
+    DevTable& d = s->dev;
+    const KTable& k = s->host;
+    d.img = s->dptr;
+    d.img_bytes = static_cast<uint32_t>(k.img.size());
+    d.cls = k.cls;
+    d.esize = k.esize;
+    d.row_bytes = k.row_bytes;
+    d.cls_off = k.cls_off;
+    d.ncols = static_cast<uint32_t>(k.ncols);
+    d.start = k.start;
+    d.dead = k.dead;
+    d.skip = k.skip;
+    d.acc_shift = k.acc_shift;
+    d.tail_delta = k.tail_delta;
+    d.term_acc = k.term_acc;
+    d.term_rej = k.term_rej;
+    d.delim_col = k.delim_col;
+    slot = std::move(s);
+    return RXG_OK;
+}
+
+int need_device(rxg_heap* h) {
+    if (!h) return fail(RXG_EINVAL, "null heap");
+    if (h->device < 0) return fail(RXG_ENODEV, "host-only heap handle");
+    if (!h->prog.byte_symbols)
+        return fail(RXG_EUNSUPPORTED, "pattern has a literal >= 0x80; byte-level matching needs ASCII literals");
+    if (!h->dfa_ok) return fail(RXG_ETOOBIG, "memoized step table exceeds " + std::to_string(kMaxDfaStates) + " states");
+    return RXG_OK;
+}
+
+int plain_table(rxg_heap* h, const DevTable** out) {
+    std::lock_guard<std::mutex> lk(h->mu);
+    if (!h->plain) {
+        const int rc = upload(h, h->plain, make_plain_table(h->prog, h->dfa));
+        if (rc) return rc;
+    }
+    *out = &h->plain->dev;
+    return RXG_OK;
+}
+
+int line_table(rxg_heap* h, int delim, const DevTable** out) {
+    std::lock_guard<std::mutex> lk(h->mu);
+    auto it = h->lines.find(delim);
+    if (it == h->lines.end()) {
+        std::unique_ptr<TableSlot> slot;
+        const int rc = upload(h, slot, make_line_table(h->prog, h->dfa, static_cast<uint8_t>(delim)));
+        if (rc) return rc;
+        it = h->lines.emplace(delim, std::move(slot)).first;
+    }
+    *out = &it->second->dev;
+    return RXG_OK;
+}
+
+uint32_t pick_chunk(const DevTable& t, uint64_t len) {
+    static const uint32_t env_chunk = [] {
+        const char* v = std::getenv("RXG_LINE_CHUNK");
+        return v ? static_cast<uint32_t>(std::strtoul(v, nullptr, 10)) : 0u;
+    }();
+    if (env_chunk >= 16 && env_chunk % 16 == 0) return env_chunk;
+    return lines_auto_chunk(t, len);
+}
+
+Heap heap_from_c(const rxg_node* nodes, const int32_t* knodes, int32_t n) {
+    Heap h;
+    h.nodes.resize(static_cast<size_t>(n));
+    std::memcpy(h.nodes.data(), nodes, static_cast<size_t>(n) * sizeof(rxg_node));
+    h.knodes.assign(knodes, knodes + n);
+    return h;
+}
+
+int make_heap(Heap&& hp, int device, rxg_heap** out) {
+    auto h = std::make_unique<rxg_heap>();
+    h->device = device;
+    h->prog = build_program(hp);
+    h->dfa_ok = build_dfa(h->prog, kMaxDfaStates, h->dfa);
+    if (device >= 0) {
+        DeviceGuard g(device);
+        int ndev = 0;
+        if (cudaGetDeviceCount(&ndev) != cudaSuccess || device >= ndev)
+            return fail(RXG_ECUDA, "no CUDA device " + std::to_string(device));
+        RXG_CUDA(cudaSetDevice(device));
+        RXG_CUDA(cudaDeviceGetAttribute(&h->smem_limit, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+        RXG_CUDA(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+        RXG_CUDA(cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking));
+        RXG_CUDA(cudaMalloc(&h->d_count, sizeof(unsigned long long)));
+        RXG_CUDA(cudaMalloc(&h->d_accept, sizeof(int32_t)));
+    }
+    *out = h.release();
+    return RXG_OK;
+}
+
+int ensure_stage(rxg_heap* h, size_t bytes) {
+    if (h->stage_bytes >= bytes) return RXG_OK;
+    for (auto*& p : h->d_stage) {
+        if (p) cudaFree(p);
+        p = nullptr;
+    }
+    h->stage_bytes = 0;
+    for (auto*& p : h->d_stage) RXG_CUDA(cudaMalloc(&p, bytes));
+    h->stage_bytes = bytes;
+    return RXG_OK;
+}
+
+int batch_device(rxg_heap* h, const uint8_t* d_text, uint64_t len, int32_t delimiter, uint32_t stride,
+                 unsigned long long* d_count, uint8_t* d_results, cudaStream_t st, bool zero_count) {
+    LaunchStats ls;
+    if (zero_count) RXG_CUDA(cudaMemsetAsync(d_count, 0, sizeof(unsigned long long), st));
+    if (delimiter >= 0) {
+        if (delimiter > 255) return fail(RXG_EINVAL, "delimiter must be a byte");
+        if (reinterpret_cast<uintptr_t>(d_text) & 15) return fail(RXG_EINVAL, "text must be 16-byte aligned");
+        const DevTable* t = nullptr;
+        if (int rc = line_table(h, delimiter, &t)) return rc;
+        const uint32_t chunk = pick_chunk(*t, len);
+        unsigned long long* scratch = nullptr;
+        size_t sbytes = 0;
+        if (d_results) {
+            sbytes = lines_scratch_bytes(len, chunk);
+            RXG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&scratch), sbytes, st));
+        }
+        const cudaError_t e = launch_lines(*t, d_text, len, static_cast<uint8_t>(delimiter), chunk, d_count,
+                                           d_results, scratch, sbytes, st, &ls);
+        if (scratch) cudaFreeAsync(scratch, st);
+        if (e != cudaSuccess) return cuda_fail(e, "launch_lines");
+    } else {
+        if (stride == 0 || len % stride) return fail(RXG_EINVAL, "fixed stride must divide the buffer length");
+        if (stride % 16 == 0 && (reinterpret_cast<uintptr_t>(d_text) & 15))
+            return fail(RXG_EINVAL, "text must be 16-byte aligned");
+        const DevTable* t = nullptr;
+        if (int rc = plain_table(h, &t)) return rc;
+        const cudaError_t e = launch_fixed(*t, d_text, len / stride, stride, d_count, d_results, st, &ls);
+        if (e != cudaSuccess) return cuda_fail(e, "launch_fixed");
+    }
+    g_launches = static_cast<int>(ls.kernels) + (zero_count ? 0 : 0);
+    return RXG_OK;
+}
+
+// Piece boundaries for the pipelined host path: pieces end just after a
+// delimiter (or at a stride multiple) so each piece holds whole strings.
+std::vector<uint64_t> pieces(const uint8_t* text, uint64_t len, int32_t delimiter, uint32_t stride, uint64_t target) {
+    std::vector<uint64_t> b{0};
+    uint64_t at = 0;
+    while (len - at > target) {
+        uint64_t cut = at + target;
+        if (delimiter >= 0) {
+            const void* hit = std::memchr(text + cut - 1, delimiter, len - (cut - 1));
+            if (!hit) break;
+            cut = static_cast<uint64_t>(static_cast<const uint8_t*>(hit) - text) + 1;
+            if (cut >= len) break;
+        } else {
+            cut -= cut % stride;
+            if (cut <= at) break;
+        }
+        b.push_back(cut);
+        at = cut;
+    }
+    b.push_back(len);
+    return b;
+}
+
+uint64_t count_strings(const uint8_t* text, uint64_t lo, uint64_t hi, int32_t delimiter, uint32_t stride) {
+    if (delimiter < 0) return (hi - lo) / stride;
+    uint64_t n = 0;
+    for (uint64_t i = lo; i < hi; ++i) n += text[i] == static_cast<uint8_t>(delimiter);
+    if (hi > lo && text[hi - 1] != static_cast<uint8_t>(delimiter)) ++n;
+    return n;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* rxg_strerror(int s) {
+    switch (s) {
+    case RXG_OK: return "ok";
+    case RXG_EINVAL: return "invalid argument";
+    case RXG_EPARSE: return "pattern syntax error";
+    case RXG_EUTF8: return "invalid UTF-8";
+    case RXG_EUNSUPPORTED: return "unsupported pattern for byte-level matching";
+    case RXG_ECUDA: return "CUDA error";
+    case RXG_ENOMEM: return "out of memory";
+    case RXG_ETOOBIG: return "step table too large";
+    case RXG_ENCCL: return "NCCL error";
+    case RXG_EHEAP: return "malformed heap";
+    case RXG_ENODEV: return "no device tables";
+    default: return "unknown status";
+    }
+}
+
+const char* rxg_last_error(void) { return g_err.c_str(); }
+const char* rxg_version(void) { return "rxg 0.1 sm_100a"; }
+int rxg_last_launch_count(void) { return g_launches; }
+
+int rxg_parse_compile(const char* pattern, size_t len, rxg_node* nodes, int32_t* knodes, int32_t cap,
+                      int32_t* n_out, size_t* err_pos) {
+    if (!pattern && len) return fail(RXG_EINVAL, "null pattern");
+    try {
+        const Heap h = compile(parse(std::string_view(pattern ? pattern : "", len)));
+        if (n_out) *n_out = h.size();
+        const int32_t n = std::min(cap, h.size());
+        if (nodes && n > 0) std::memcpy(nodes, h.nodes.data(), static_cast<size_t>(n) * sizeof(rxg_node));
+        if (knodes && n > 0) std::memcpy(knodes, h.knodes.data(), static_cast<size_t>(n) * sizeof(int32_t));
+        return RXG_OK;
+    } catch (const ParseError& e) {
+        if (err_pos) *err_pos = e.pos;
+        return fail(RXG_EPARSE, e.what());
+    } catch (const Utf8Error& e) {
+        if (err_pos) *err_pos = e.at;
+        return fail(RXG_EUTF8, e.what());
+    } catch (const std::exception& e) {
+        return fail(RXG_EINVAL, e.what());
+    }
+}
+
+int rxg_print(const char* pattern, size_t len, char* out, size_t cap, size_t* out_len) {
+    try {
+        const std::string s = print(parse(std::string_view(pattern ? pattern : "", len)));
+        if (out_len) *out_len = s.size();
+        if (out && cap) {
+            const size_t n = std::min(cap - 1, s.size());
+            std::memcpy(out, s.data(), n);
+            out[n] = '\0';
+        }
+        return RXG_OK;
+    } catch (const ParseError& e) {
+        return fail(RXG_EPARSE, e.what());
+    } catch (const Utf8Error& e) {
+        return fail(RXG_EUTF8, e.what());
+    }
+}
+
+int rxg_dump(const rxg_node* nodes, const int32_t* knodes, int32_t n, char* out, size_t cap, size_t* out_len) {
+    if (!nodes || !knodes || n <= 0) return fail(RXG_EINVAL, "empty heap");
+    const std::string s = dump(heap_from_c(nodes, knodes, n));
+    if (out_len) *out_len = s.size();
+    if (out && cap) {
+        const size_t k = std::min(cap - 1, s.size());
+        std::memcpy(out, s.data(), k);
+        out[k] = '\0';
+    }
+    return RXG_OK;
+}
+
+int rxg_parse_dump(const char* text, size_t len, rxg_node* nodes, int32_t* knodes, int32_t cap, int32_t* n_out) {
+    try {
+        const Heap h = parse_dump(std::string_view(text ? text : "", len));
+        if (n_out) *n_out = h.size();
+        const int32_t n = std::min(cap, h.size());
+        if (nodes && n > 0) std::memcpy(nodes, h.nodes.data(), static_cast<size_t>(n) * sizeof(rxg_node));
+        if (knodes && n > 0) std::memcpy(knodes, h.knodes.data(), static_cast<size_t>(n) * sizeof(int32_t));
+        return RXG_OK;
+    } catch (const std::exception& e) {
+        return fail(RXG_EHEAP, e.what());
+    }
+}
+
+int rxg_check_knode(const rxg_node* nodes, const int32_t* knodes, int32_t n, int32_t* ok) {
+    if (!nodes || !knodes || !ok || n < 0) return fail(RXG_EINVAL, "bad arguments");
+    *ok = n > 0 && check_knode(heap_from_c(nodes, knodes, n));
+    return RXG_OK;
+}
+
+int rxg_heap_create(const rxg_node* nodes, const int32_t* knodes, int32_t n, int device, rxg_heap** out) {
+    if (!nodes || !knodes || n <= 0 || !out) return fail(RXG_EINVAL, "bad arguments");
+    try {
+        Heap hp = heap_from_c(nodes, knodes, n);
+        const std::string bad = validate_heap(hp);
+        if (!bad.empty()) return fail(RXG_EHEAP, bad);
+        return make_heap(std::move(hp), device, out);
+    } catch (const std::bad_alloc&) {
+        return fail(RXG_ENOMEM, "host allocation failed");
+    } catch (const std::exception& e) {
+        return fail(RXG_EHEAP, e.what());
+    }
+}
+
+int rxg_heap_create_pattern(const char* pattern, size_t len, int device, rxg_heap** out) {
+    if (!out) return fail(RXG_EINVAL, "null out");
+    try {
+        return make_heap(compile(parse(std::string_view(pattern ? pattern : "", len))), device, out);
+    } catch (const ParseError& e) {
+        return fail(RXG_EPARSE, e.what());
+    } catch (const Utf8Error& e) {
+        return fail(RXG_EUTF8, e.what());
+    } catch (const std::bad_alloc&) {
+        return fail(RXG_ENOMEM, "host allocation failed");
+    } catch (const std::exception& e) {
+        return fail(RXG_EHEAP, e.what());
+    }
+}
+
+void rxg_heap_destroy(rxg_heap* h) { delete h; }
+
+int rxg_heap_info_get(const rxg_heap* h, rxg_heap_info* info) {
+    if (!h || !info) return fail(RXG_EINVAL, "bad arguments");
+    std::memset(info, 0, sizeof(*info));
+    info->nodes = h->prog.heap.size();
+    info->positions = h->prog.n_pos;
+    info->words = h->prog.W;
+    info->classes = h->prog.n_classes;
+    info->dfa_states = h->dfa_ok ? h->dfa.n_states : 0;
+    info->byte_symbols = h->prog.byte_symbols;
+    info->device = h->device;
+    info->nullable = h->prog.test(h->prog.init, h->prog.n_pos);
+    if (h->dfa_ok) {
+        info->line_table_bytes = static_cast<uint32_t>(make_line_table(h->prog, h->dfa, '\n').img.size());
+        info->plain_table_bytes = static_cast<uint32_t>(make_plain_table(h->prog, h->dfa).img.size());
+    }
+    return RXG_OK;
+}
+
+int rxg_heap_tables(const rxg_heap* h, int32_t* pos_addr, uint32_t* follow, uint32_t* init) {
+    if (!h) return fail(RXG_EINVAL, "null heap");
+    const Program& p = h->prog;
+    if (pos_addr) std::copy(p.pos_addr.begin(), p.pos_addr.end(), pos_addr);
+    if (follow) std::copy(p.follow.begin(), p.follow.end(), follow);
+    if (init) std::copy(p.init.begin(), p.init.end(), init);
+    return RXG_OK;
+}
+
+int rxg_host_walk(const rxg_heap* h, const uint8_t* bytes, uint64_t len, uint32_t* sets_out, int32_t* accept) {
+    if (!h || (!bytes && len)) return fail(RXG_EINVAL, "bad arguments");
+    const Program& p = h->prog;
+    const size_t W = static_cast<size_t>(p.W);
+    std::vector<uint32_t> cur(p.init), nxt(W);
+    if (sets_out) std::copy(cur.begin(), cur.end(), sets_out);
+    for (uint64_t i = 0; i < len; ++i) {
+        step_set(p, cur.data(), p.byte_class[bytes[i]], nxt.data());
+        cur.swap(nxt);
+        if (sets_out) std::copy(cur.begin(), cur.end(), sets_out + (i + 1) * W);
+    }
+    if (accept) *accept = p.test(cur, p.n_pos);
+    return RXG_OK;
+}
+
+int rxg_host_emulate_batch(const rxg_heap* h, const uint8_t* text, uint64_t len, int32_t delimiter, uint32_t stride,
+                           uint32_t chunk, uint64_t* count, uint8_t* results) {
+    if (!h || !count || (!text && len)) return fail(RXG_EINVAL, "bad arguments");
+    if (!h->dfa_ok) return fail(RXG_ETOOBIG, "no memoized step table");
+    uint64_t cnt = 0;
+    if (delimiter < 0) {
+        if (stride == 0 || len % stride) return fail(RXG_EINVAL, "fixed stride must divide the buffer length");
+        const KTable t = make_plain_table(h->prog, h->dfa);
+        for (uint64_t i = 0; i < len / stride; ++i) {
+            uint32_t s = t.start;
+            for (uint32_t k = 0; k < stride; ++k) s = ktable_step(t, s, text[i * stride + k]);
+            const uint32_t ok = ktable_accept(t, s);
+            if (results) results[i] = static_cast<uint8_t>(ok);
+            cnt += ok;
+        }
+        *count = cnt;
+        return RXG_OK;
+    }
+    if (delimiter > 255) return fail(RXG_EINVAL, "delimiter must be a byte");
+    if (chunk == 0) chunk = 1024;
+    if (chunk % 16) return fail(RXG_EINVAL, "chunk must be a multiple of 16");
+    const KTable t = make_line_table(h->prog, h->dfa, static_cast<uint8_t>(delimiter));
+    const uint8_t d = static_cast<uint8_t>(delimiter);
+    const uint64_t nchunks = (len + chunk - 1) / chunk;
+    uint64_t line_base = 0;
+    for (uint64_t c = 0; c < nchunks; ++c) {
+        const uint64_t c0 = c * chunk, c1 = std::min<uint64_t>(c0 + chunk, len);
+        uint64_t line = line_base;
+        for (uint64_t i = c0; i < c1; ++i) line_base += text[i] == d;
+        uint32_t s = (c0 == 0 || text[c0 - 1] == d) ? t.start : t.skip;
+        uint32_t last = 0;
+        for (uint64_t i = c0; i < c1; ++i) {
+            const uint32_t prev = s;
+            s = ktable_step(t, s, text[i]);
+            if (text[i] == d) {
+                if (prev != t.skip && results) results[line] = static_cast<uint8_t>(s >> t.acc_shift);
+                ++line;
+            }
+            cnt += s >> t.acc_shift;
+            last = text[i];
+        }
+        if (s != t.skip && last != d) {
+            s += t.tail_delta;
+            uint64_t pos = c1;
+            while (pos < len && s < t.term_acc) {
+                const uint64_t end = std::min<uint64_t>(pos + 16, len);
+                for (; pos < end; ++pos) s = ktable_step(t, s, text[pos]);
+            }
+            if (s < t.term_acc) s = ktable_step(t, s, d);
+            const uint32_t ok = s == t.term_acc;
+            if (results) results[line] = static_cast<uint8_t>(ok);
+            cnt += ok;
+        }
+    }
+    *count = cnt;
+    return RXG_OK;
+}
+
+int rxg_match_one_device(rxg_heap* h, const uint8_t* d_bytes, uint64_t len, int engine, int32_t* d_accept,
+                         void* stream) {
+    if (int rc = need_device(h)) return rc;
+    if (!d_accept || (!d_bytes && len)) return fail(RXG_EINVAL, "bad arguments");
+    DeviceGuard g(h->device);
+    const cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const DevTable* t = nullptr;
+    if (int rc = plain_table(h, &t)) return rc;
+    switch (engine) {
+    case RXG_ENGINE_AUTO:
+    case RXG_ENGINE_DFA_SEQ: {
+        const cudaError_t e = launch_seq(*t, d_bytes, len, d_accept, st);
+        if (e != cudaSuccess) return cuda_fail(e, "launch_seq");
+        g_launches = 1;
+        return RXG_OK;
+    }
+    default:
+        return fail(RXG_EUNSUPPORTED, "engine not available");
+    }
+}
+
+int rxg_match_one(rxg_heap* h, const uint8_t* bytes, uint64_t len, int engine, int32_t* accept) {
+    if (int rc = need_device(h)) return rc;
+    if (!accept || (!bytes && len)) return fail(RXG_EINVAL, "bad arguments");
+    DeviceGuard g(h->device);
+    if (int rc = ensure_stage(h, std::max<size_t>(len, 16))) return rc;
+    if (len) RXG_CUDA(cudaMemcpyAsync(h->d_stage[0], bytes, len, cudaMemcpyHostToDevice, h->stream));
+    if (int rc = rxg_match_one_device(h, h->d_stage[0], len, engine, h->d_accept, h->stream)) return rc;
+    RXG_CUDA(cudaMemcpyAsync(accept, h->d_accept, sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream));
+    RXG_CUDA(cudaStreamSynchronize(h->stream));
+    return RXG_OK;
+}
+
+int rxg_match_batch(rxg_heap* h, const uint8_t* d_text, uint64_t len, int32_t delimiter, uint32_t stride,
+                    unsigned long long* d_count, uint8_t* d_results, void* stream) {
+    if (int rc = need_device(h)) return rc;
+    if (!d_count || (!d_text && len)) return fail(RXG_EINVAL, "bad arguments");
+    DeviceGuard g(h->device);
+    return batch_device(h, d_text, len, delimiter, stride, d_count, d_results, static_cast<cudaStream_t>(stream), true);
+}
+
+int rxg_match_batch_host(rxg_heap* h, const uint8_t* text, uint64_t len, int32_t delimiter, uint32_t stride,
+                         uint64_t* count, uint8_t* results) {
+    if (int rc = need_device(h)) return rc;
+    if (!count || (!text && len)) return fail(RXG_EINVAL, "bad arguments");
+    if (delimiter < 0 && (stride == 0 || len % stride)) return fail(RXG_EINVAL, "fixed stride must divide the buffer length");
+    DeviceGuard g(h->device);
+    // Pipelined: piece k+1 is copied on copy_stream while piece k is matched.
+    constexpr uint64_t kPiece = 64ull << 20;
+    const std::vector<uint64_t> b = pieces(text, len, delimiter, stride, kPiece);
+    uint64_t maxp = 16;
+    for (size_t i = 0; i + 1 < b.size(); ++i) maxp = std::max(maxp, b[i + 1] - b[i]);
+    if (int rc = ensure_stage(h, (maxp + 15) & ~uint64_t(15))) return rc;
+    uint8_t* d_res = nullptr;
+    std::vector<uint64_t> res_base;
+    uint64_t nstr = 0;
+    if (results) {
+        res_base.resize(b.size());
+        for (size_t i = 0; i + 1 < b.size(); ++i) {
+            res_base[i] = nstr;
+            nstr += count_strings(text, b[i], b[i + 1], delimiter, stride);
+        }
+        RXG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_res), std::max<uint64_t>(nstr, 1) + 1, h->stream));
+    }
+    cudaEvent_t copied[2], consumed[2];
+    for (int i = 0; i < 2; ++i) {
+        cudaEventCreateWithFlags(&copied[i], cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&consumed[i], cudaEventDisableTiming);
+    }
+    RXG_CUDA(cudaMemsetAsync(h->d_count, 0, sizeof(unsigned long long), h->stream));
+    int rc = RXG_OK;
+    int launches = 1;
+    for (size_t i = 0; i + 1 < b.size() && rc == RXG_OK; ++i) {
+        const int k = static_cast<int>(i & 1);
+        const uint64_t n = b[i + 1] - b[i];
+        if (i >= 2) cudaStreamWaitEvent(h->copy_stream, consumed[k], 0);
+        cudaMemcpyAsync(h->d_stage[k], text + b[i], n, cudaMemcpyHostToDevice, h->copy_stream);
+        cudaEventRecord(copied[k], h->copy_stream);
+        cudaStreamWaitEvent(h->stream, copied[k], 0);
+        rc = batch_device(h, h->d_stage[k], n, delimiter, stride, h->d_count, results ? d_res + res_base[i] : nullptr,
+                          h->stream, false);
+        launches += g_launches;
+        cudaEventRecord(consumed[k], h->stream);
+    }
+    if (rc == RXG_OK) {
+        unsigned long long c = 0;
+        cudaMemcpyAsync(&c, h->d_count, sizeof(c), cudaMemcpyDeviceToHost, h->stream);
+        if (results && nstr) cudaMemcpyAsync(results, d_res, nstr, cudaMemcpyDeviceToHost, h->stream);
+        const cudaError_t e = cudaStreamSynchronize(h->stream);
+        if (e != cudaSuccess) rc = cuda_fail(e, "match_batch_host");
+        *count = c;
+    }
+    if (d_res) cudaFreeAsync(d_res, h->stream);
+    cudaStreamSynchronize(h->stream);
+    for (int i = 0; i < 2; ++i) {
+        cudaEventDestroy(copied[i]);
+        cudaEventDestroy(consumed[i]);
+    }
+    g_launches = launches;
+    return rc;
+}
+
+int rxg_shard_bounds(const uint8_t* text, uint64_t len, int32_t delimiter, uint32_t stride, int ndev,
+                     uint64_t* offsets) {
+    if (ndev <= 0 || !offsets || (!text && len)) return fail(RXG_EINVAL, "bad arguments");
+    if (delimiter < 0 && (stride == 0 || len % stride)) return fail(RXG_EINVAL, "fixed stride must divide the buffer length");
+    offsets[0] = 0;
+    const uint64_t nstr = delimiter < 0 ? len / stride : 0;
+    for (int k = 1; k < ndev; ++k) {
+        uint64_t cut;
+        if (delimiter < 0) {
+            cut = nstr * static_cast<uint64_t>(k) / static_cast<uint64_t>(ndev) * stride;
+        } else {
+            cut = len * static_cast<uint64_t>(k) / static_cast<uint64_t>(ndev);
+            if (cut > 0 && cut < len && text[cut - 1] != static_cast<uint8_t>(delimiter)) {
+                const void* hit = std::memchr(text + cut, delimiter, len - cut);
+                cut = hit ? static_cast<uint64_t>(static_cast<const uint8_t*>(hit) - text) + 1 : len;
+            }
+        }
+        offsets[k] = std::max(cut, offsets[k - 1]);
+    }
+    offsets[ndev] = len;
+    return RXG_OK;
+}
+
+int rxg_match_batch_multi(const int* devices, int ndev, const char* pattern, size_t plen, const uint8_t* text,
+                          uint64_t len, int32_t delimiter, uint32_t stride, uint64_t* count, uint8_t* results) {
+    if (!devices || ndev <= 0 || !count) return fail(RXG_EINVAL, "bad arguments");
+    std::vector<uint64_t> off(static_cast<size_t>(ndev) + 1);
+    if (int rc = rxg_shard_bounds(text, len, delimiter, stride, ndev, off.data())) return rc;
+    std::vector<rxg_heap*> hs(static_cast<size_t>(ndev), nullptr);
+    auto cleanup = [&] {
+        for (auto* x : hs) rxg_heap_destroy(x);
+    };
+    std::vector<uint8_t*> d_text(static_cast<size_t>(ndev), nullptr);
+    std::vector<uint8_t*> d_res(static_cast<size_t>(ndev), nullptr);
+    std::vector<uint64_t> res_base(static_cast<size_t>(ndev), 0);
+    uint64_t nstr = 0;
+    int rc = RXG_OK;
+    for (int k = 0; k < ndev && rc == RXG_OK; ++k) {
+        rc = rxg_heap_create_pattern(pattern, plen, devices[k], &hs[static_cast<size_t>(k)]);
+        if (rc) break;
+        rxg_heap* h = hs[static_cast<size_t>(k)];
+        if ((rc = need_device(h))) break;
+        DeviceGuard g(h->device);
+        const uint64_t n = off[static_cast<size_t>(k) + 1] - off[static_cast<size_t>(k)];
+        if (cudaMalloc(&d_text[static_cast<size_t>(k)], std::max<uint64_t>(n, 16)) != cudaSuccess) {
+            rc = fail(RXG_ENOMEM, "device allocation failed");
+            break;
+        }
+        if (results) {
+            res_base[static_cast<size_t>(k)] = nstr;
+            const uint64_t m = count_strings(text, off[static_cast<size_t>(k)], off[static_cast<size_t>(k) + 1], delimiter, stride);
+            nstr += m;
+            cudaMalloc(&d_res[static_cast<size_t>(k)], std::max<uint64_t>(m, 1) + 1);
+        }
+        cudaMemcpyAsync(d_text[static_cast<size_t>(k)], text + off[static_cast<size_t>(k)], n, cudaMemcpyHostToDevice, h->stream);
+        rc = batch_device(h, d_text[static_cast<size_t>(k)], n, delimiter, stride, h->d_count, d_res[static_cast<size_t>(k)],
+                          h->stream, true);
+    }
+    if (rc == RXG_OK && ndev > 1) {
+        // One all-reduce of the 8-byte count: the only inter-GPU traffic.
+        void* lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        auto init_all = lib ? reinterpret_cast<ncclResult_t (*)(ncclComm_t*, int, const int*)>(dlsym(lib, "ncclCommInitAll")) : nullptr;
+        auto allreduce = lib ? reinterpret_cast<ncclResult_t (*)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t)>(dlsym(lib, "ncclAllReduce")) : nullptr;
+        auto gstart = lib ? reinterpret_cast<ncclResult_t (*)()>(dlsym(lib, "ncclGroupStart")) : nullptr;
+        auto gend = lib ? reinterpret_cast<ncclResult_t (*)()>(dlsym(lib, "ncclGroupEnd")) : nullptr;
+        auto destroy = lib ? reinterpret_cast<ncclResult_t (*)(ncclComm_t)>(dlsym(lib, "ncclCommDestroy")) : nullptr;
+        if (!init_all || !allreduce || !gstart || !gend || !destroy) {
+            rc = fail(RXG_ENCCL, "libnccl.so.2 not loadable");
+        } else {
+            std::vector<ncclComm_t> comms(static_cast<size_t>(ndev));
+            if (init_all(comms.data(), ndev, devices) != ncclSuccess) {
+                rc = fail(RXG_ENCCL, "ncclCommInitAll failed");
+            } else {
+                gstart();
+                for (int k = 0; k < ndev; ++k) {
+                    rxg_heap* h = hs[static_cast<size_t>(k)];
+                    allreduce(h->d_count, h->d_count, 1, ncclUint64, ncclSum, comms[static_cast<size_t>(k)], h->stream);
+                }
+                if (gend() != ncclSuccess) rc = fail(RXG_ENCCL, "ncclAllReduce failed");
+                for (int k = 0; k < ndev; ++k) {
+                    DeviceGuard g(devices[k]);
+                    cudaStreamSynchronize(hs[static_cast<size_t>(k)]->stream);
+                }
+                for (auto c : comms) destroy(c);
+            }
+        }
+    }
+    if (rc == RXG_OK) {
+        rxg_heap* h0 = hs[0];
+        DeviceGuard g(h0->device);
+        unsigned long long c = 0;
+        cudaMemcpy(&c, h0->d_count, sizeof(c), cudaMemcpyDeviceToHost);
+        *count = c;
+        if (ndev == 1) *count = c;
+        if (results) {
+            for (int k = 0; k < ndev; ++k) {
+                DeviceGuard gk(devices[k]);
+                const uint64_t m = (k + 1 < ndev ? res_base[static_cast<size_t>(k) + 1] : nstr) - res_base[static_cast<size_t>(k)];
+                if (m) cudaMemcpy(results + res_base[static_cast<size_t>(k)], d_res[static_cast<size_t>(k)], m, cudaMemcpyDeviceToHost);
+            }
+        }
+    }
+    for (int k = 0; k < ndev; ++k) {
+        if (!hs[static_cast<size_t>(k)]) continue;
+        DeviceGuard g(devices[k]);
+        cudaDeviceSynchronize();
+        if (d_text[static_cast<size_t>(k)]) cudaFree(d_text[static_cast<size_t>(k)]);
+        if (d_res[static_cast<size_t>(k)]) cudaFree(d_res[static_cast<size_t>(k)]);
+    }
+    cleanup();
+    g_launches = ndev;
+    return rc;
+}
+
+int rxg_synth_pattern(char config, char* out, size_t cap, size_t* out_len) {
+    try {
+        const std::string s = synth_pattern(config);
+        if (out_len) *out_len = s.size();
+        if (out && cap) {
+            const size_t n = std::min(cap - 1, s.size());
+            std::memcpy(out, s.data(), n);
+            out[n] = '\0';
+        }
+        return RXG_OK;
+    } catch (const std::exception& e) {
+        return fail(RXG_EINVAL, e.what());
+    }
+}
+
+uint64_t rxg_synth_input_size(char config) {
+    try {
+        return synth_input_size(config);
+    } catch (...) {
+        return 0;
+    }
+}
+
+int rxg_synth_input(char config, uint64_t seed, uint8_t* out, uint64_t cap, uint64_t* written) {
+    if (!out && cap) return fail(RXG_EINVAL, "null buffer");
+    try {
+        const uint64_t n = synth_input(config, seed, out, cap);
+        if (written) *written = n;
+        return RXG_OK;
+    } catch (const std::exception& e) {
+        return fail(RXG_EINVAL, e.what());
+    }
+}
+
+}  // extern "C"

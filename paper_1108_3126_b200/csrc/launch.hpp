@@ -1,0 +1,45 @@
+// Host-side launch interface between the C ABI (capi.cu) and the kernels.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace rxg {
+
+// Device-resident shared-memory image plus the scalar offsets the kernels need.
+struct DevTable {
+    const void* img = nullptr;   // device copy of KTable::img
+    uint32_t img_bytes = 0;
+    bool cls = false;
+    int esize = 2;
+    uint32_t row_bytes = 0;
+    uint32_t cls_off = 0;
+    uint32_t ncols = 0;
+    uint32_t start = 0, dead = 0, skip = 0, acc_shift = 0, tail_delta = 0;
+    uint32_t term_acc = 0, term_rej = 0, delim_col = 0;
+};
+
+struct LaunchStats {
+    uint32_t kernels = 0;   // kernels launched by the last call
+};
+
+// K2, delimited batch. `count` (device u64) is accumulated (caller zeroes it).
+// `results` (device, one byte per line) and `line_base` are optional.
+cudaError_t launch_lines(const DevTable& t, const uint8_t* text, uint64_t len, uint8_t delim,
+                         uint32_t chunk, unsigned long long* count, uint8_t* results,
+                         unsigned long long* scratch, size_t scratch_bytes, cudaStream_t st,
+                         LaunchStats* ls);
+
+// Chunk (bytes per chain) that gives one wave of resident chains over len.
+uint32_t lines_auto_chunk(const DevTable& t, uint64_t len);
+
+// Bytes of scratch launch_lines needs when results != nullptr.
+size_t lines_scratch_bytes(uint64_t len, uint32_t chunk);
+
+// K2, fixed-stride batch: strings text[i*stride, (i+1)*stride), i < n.
+cudaError_t launch_fixed(const DevTable& t, const uint8_t* text, uint64_t n, uint32_t stride,
+                         unsigned long long* count, uint8_t* results, cudaStream_t st, LaunchStats* ls);
+
+int device_sm_count(int device);
+
+}  // namespace rxg

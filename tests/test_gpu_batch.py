@@ -1,0 +1,79 @@
+"""GPU parity of the batch kernels (K2) against the CPU oracle and the
+reference library, through the C ABI (rxg_match_batch_host / rxg_match_batch)."""
+import numpy as np
+import pytest
+
+from oracle_bind import Oracle, Ref, RefHeap
+from paper_1108_3126_b200 import rx
+
+pytestmark = pytest.mark.gpu
+
+
+def _oracle(pattern):
+    return Oracle(rx.compile(rx.parse(pattern)))
+
+
+@pytest.mark.parametrize("cfg,nbytes", [("c", 8 << 20), ("d", 8 << 20)])
+def test_lines_config_sample_matches_oracle(cfg, nbytes):
+    pattern = rx.synth_pattern(cfg)
+    text = rx.synth_input(cfg, nbytes)
+    m = rx.Matcher(pattern, device=0)
+    count, res = m.match_batch(text, delimiter=10, results=True)
+    ocount, ores = _oracle(pattern).match_batch(text, 10, 0)
+    assert count == ocount
+    assert np.array_equal(res, ores)
+    # count-only launch agrees with the results launch
+    c2, _ = m.match_batch(text, delimiter=10)
+    assert c2 == count
+
+
+def test_fixed_stride_cox_full_batch():
+    pattern = rx.synth_pattern("b")
+    text = rx.synth_input("b")
+    m = rx.Matcher(pattern, device=0)
+    count, res = m.match_batch(text, delimiter=-1, stride=32, results=True)
+    assert count == 1_000_000 and res.all()
+    # the reference itself on a slice
+    if Ref.available():
+        rc, rr = RefHeap(pattern.encode()).match_batch(text[: 32 * 2000], -1, 32)
+        assert rc == 2000 and rr.all()
+
+
+def test_lines_against_reference_library():
+    if not Ref.available():
+        pytest.skip("oracle/_ref not built")
+    pattern = rx.synth_pattern("c")
+    text = rx.synth_input("c", 2 << 20)
+    rc, rr = RefHeap(pattern.encode()).match_batch(text, 10, 0)
+    count, res = rx.Matcher(pattern, device=0).match_batch(text, delimiter=10, results=True)
+    assert count == rc and np.array_equal(res, rr)
+
+
+@pytest.mark.parametrize("chunk_text", [b"", b"\n", b"\n\n\n", b"ab", b"ab\n", b"\nab", b"a\nb\n\nab"])
+def test_edge_buffers(chunk_text):
+    for pattern in ["a*", "ab", "()", "(a|b)*abb", "a|()"]:
+        m = rx.Matcher(pattern, device=0)
+        o = _oracle(pattern)
+        text = np.frombuffer(chunk_text, np.uint8) if chunk_text else np.zeros(0, np.uint8)
+        count, res = m.match_batch(text, delimiter=10, results=True)
+        ocount, ores = o.match_batch(text, 10, 0)
+        assert count == ocount, (pattern, chunk_text)
+        assert np.array_equal(res, ores), (pattern, chunk_text)
+
+
+def test_enumerated_regexes_over_all_short_strings():
+    """Acceptance criterion 3 shape (acceptance_main.cpp:93-105) on the GPU:
+    every regex <= 5 nodes over {a,b} x every string <= 4, as one line buffer each."""
+    import itertools
+
+    strings = [""] + ["".join(t) for L in range(1, 5) for t in itertools.product("ab", repeat=L)]
+    text = np.frombuffer(("\n".join(strings) + "\n").encode(), np.uint8)
+    pats = Ref.enumerate_regexes(5, "ab") if Ref.available() else ["a**b", "(a|b)*a", "()", "a*b*"]
+    bad = []
+    for p in pats:
+        m = rx.Matcher(p, device=0)
+        _, res = m.match_batch(text, delimiter=10, results=True)
+        _, ores = _oracle(p).match_batch(text, 10, 0)
+        if not np.array_equal(res, ores):
+            bad.append(p)
+    assert not bad, bad[:10]
