@@ -134,6 +134,11 @@ int rxg_host_walk(const rxg_heap* h, const uint8_t* bytes, uint64_t len, uint32_
 int rxg_host_emulate_batch(const rxg_heap* h, const uint8_t* text, uint64_t len, int32_t delimiter,
                            uint32_t stride, uint32_t chunk, uint64_t* count, uint8_t* results);
 
+/* Same for the TMA-staged line kernel's layout and range partition
+ * (chunk: multiple of 32). RXG_ETOOBIG if the DFA does not fit that layout. */
+int rxg_host_emulate_lines_tma(const rxg_heap* h, const uint8_t* text, uint64_t len, int32_t delimiter,
+                               uint32_t chunk, uint64_t* count);
+
 /* ── matching ─────────────────────────────────────────────────────────── */
 
 /* One string, host buffer (synchronous). */

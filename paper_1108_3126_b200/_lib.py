@@ -60,6 +60,7 @@ _SIG = {
     "rxg_host_walk": (C.c_int, [_P, _P, C.c_uint64, _P, C.POINTER(C.c_int32)]),
     "rxg_host_emulate_batch": (C.c_int, [_P, _P, C.c_uint64, C.c_int32, C.c_uint32, C.c_uint32,
                                          C.POINTER(C.c_uint64), _P]),
+    "rxg_host_emulate_lines_tma": (C.c_int, [_P, _P, C.c_uint64, C.c_int32, C.c_uint32, C.POINTER(C.c_uint64)]),
     "rxg_match_one": (C.c_int, [_P, _P, C.c_uint64, C.c_int, C.POINTER(C.c_int32)]),
     "rxg_match_one_device": (C.c_int, [_P, _P, C.c_uint64, C.c_int, _P, _P]),
     "rxg_match_batch": (C.c_int, [_P, _P, C.c_uint64, C.c_int32, C.c_uint32, _P, _P, _P]),

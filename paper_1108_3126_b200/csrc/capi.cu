@@ -15,6 +15,7 @@
 #include "rxg.h"
 #include "frontend.hpp"
 #include "launch.hpp"
+#include "lines_tma.hpp"
 #include "program.hpp"
 #include "single.hpp"
 #include "synth.hpp"
@@ -57,6 +58,7 @@ struct TableSlot {
     KTable host;
     DevTable dev;
     void* dptr = nullptr;
+    LtTable lt;   // TMA line layout (delimited slots only; lt.ok false if it does not fit)
 };
 
 constexpr int32_t kMaxDfaStates = 16384;
@@ -84,8 +86,11 @@ struct rxg_heap {
         if (device < 0) return;
         DeviceGuard g(device);
         if (plain && plain->dptr) cudaFree(plain->dptr);
-        for (auto& kv : lines)
+        for (auto& kv : lines) {
             if (kv.second->dptr) cudaFree(kv.second->dptr);
+            if (kv.second->lt.d_lo) cudaFree(kv.second->lt.d_lo);
+            if (kv.second->lt.d_hi) cudaFree(kv.second->lt.d_hi);
+        }
         for (auto* p : d_stage)
             if (p) cudaFree(p);
         if (d_count) cudaFree(d_count);
@@ -145,26 +150,36 @@ int plain_table(rxg_heap* h, const DevTable** out) {
     return RXG_OK;
 }
 
-int line_table(rxg_heap* h, int delim, const DevTable** out) {
+int line_table(rxg_heap* h, int delim, TableSlot** out) {
     std::lock_guard<std::mutex> lk(h->mu);
     auto it = h->lines.find(delim);
     if (it == h->lines.end()) {
         std::unique_ptr<TableSlot> slot;
         const int rc = upload(h, slot, make_line_table(h->prog, h->dfa, static_cast<uint8_t>(delim)));
         if (rc) return rc;
+        static const bool no_tma = std::getenv("RXG_NO_TMA") != nullptr;
+        LtTable lt = make_lines_tma_table(h->prog, h->dfa, static_cast<uint8_t>(delim));
+        if (lt.ok && !no_tma && static_cast<int>(lt.smem_bytes) <= h->smem_limit) {
+            RXG_CUDA(cudaMalloc(&lt.d_lo, lt.lo.size()));
+            RXG_CUDA(cudaMalloc(&lt.d_hi, lt.hi.size()));
+            RXG_CUDA(cudaMemcpy(lt.d_lo, lt.lo.data(), lt.lo.size(), cudaMemcpyHostToDevice));
+            RXG_CUDA(cudaMemcpy(lt.d_hi, lt.hi.data(), lt.hi.size(), cudaMemcpyHostToDevice));
+        } else {
+            lt.ok = false;
+        }
+        slot->lt = std::move(lt);
         it = h->lines.emplace(delim, std::move(slot)).first;
     }
-    *out = &it->second->dev;
+    *out = it->second.get();
     return RXG_OK;
 }
 
-uint32_t pick_chunk(const DevTable& t, uint64_t len) {
-    static const uint32_t env_chunk = [] {
-        const char* v = std::getenv("RXG_LINE_CHUNK");
-        return v ? static_cast<uint32_t>(std::strtoul(v, nullptr, 10)) : 0u;
+uint32_t env_chunk() {
+    static const uint32_t v = [] {
+        const char* e = std::getenv("RXG_LINE_CHUNK");
+        return e ? static_cast<uint32_t>(std::strtoul(e, nullptr, 10)) : 0u;
     }();
-    if (env_chunk >= 16 && env_chunk % 16 == 0) return env_chunk;
-    return lines_auto_chunk(t, len);
+    return v;
 }
 
 Heap heap_from_c(const rxg_node* nodes, const int32_t* knodes, int32_t n) {
@@ -215,19 +230,30 @@ int batch_device(rxg_heap* h, const uint8_t* d_text, uint64_t len, int32_t delim
     if (delimiter >= 0) {
         if (delimiter > 255) return fail(RXG_EINVAL, "delimiter must be a byte");
         if (reinterpret_cast<uintptr_t>(d_text) & 15) return fail(RXG_EINVAL, "text must be 16-byte aligned");
-        const DevTable* t = nullptr;
-        if (int rc = line_table(h, delimiter, &t)) return rc;
-        const uint32_t chunk = pick_chunk(*t, len);
-        unsigned long long* scratch = nullptr;
-        size_t sbytes = 0;
-        if (d_results) {
-            sbytes = lines_scratch_bytes(len, chunk);
-            RXG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&scratch), sbytes, st));
+        TableSlot* slot = nullptr;
+        if (int rc = line_table(h, delimiter, &slot)) return rc;
+        if (!d_results && slot->lt.ok) {
+            uint32_t chunk = env_chunk();
+            if (chunk == 0 || chunk % kLtSlice) chunk = lines_tma_auto_chunk(slot->lt, len);
+            const cudaError_t e = launch_lines_tma(slot->lt, d_text, len, static_cast<uint8_t>(delimiter), chunk,
+                                                   d_count, st);
+            if (e != cudaSuccess) return cuda_fail(e, "launch_lines_tma");
+            ls.kernels = 1;
+        } else {
+            const DevTable* t = &slot->dev;
+            uint32_t chunk = env_chunk();
+            if (chunk == 0 || chunk % 16) chunk = lines_auto_chunk(*t, len);
+            unsigned long long* scratch = nullptr;
+            size_t sbytes = 0;
+            if (d_results) {
+                sbytes = lines_scratch_bytes(len, chunk);
+                RXG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&scratch), sbytes, st));
+            }
+            const cudaError_t e = launch_lines(*t, d_text, len, static_cast<uint8_t>(delimiter), chunk, d_count,
+                                               d_results, scratch, sbytes, st, &ls);
+            if (scratch) cudaFreeAsync(scratch, st);
+            if (e != cudaSuccess) return cuda_fail(e, "launch_lines");
         }
-        const cudaError_t e = launch_lines(*t, d_text, len, static_cast<uint8_t>(delimiter), chunk, d_count,
-                                           d_results, scratch, sbytes, st, &ls);
-        if (scratch) cudaFreeAsync(scratch, st);
-        if (e != cudaSuccess) return cuda_fail(e, "launch_lines");
     } else {
         if (stride == 0 || len % stride) return fail(RXG_EINVAL, "fixed stride must divide the buffer length");
         if (stride % 16 == 0 && (reinterpret_cast<uintptr_t>(d_text) & 15))
@@ -491,6 +517,46 @@ int rxg_host_emulate_batch(const rxg_heap* h, const uint8_t* text, uint64_t len,
             const uint32_t ok = s == t.term_acc;
             if (results) results[line] = static_cast<uint8_t>(ok);
             cnt += ok;
+        }
+    }
+    *count = cnt;
+    return RXG_OK;
+}
+
+int rxg_host_emulate_lines_tma(const rxg_heap* h, const uint8_t* text, uint64_t len, int32_t delimiter,
+                               uint32_t chunk, uint64_t* count) {
+    if (!h || !count || (!text && len) || delimiter < 0 || delimiter > 255) return fail(RXG_EINVAL, "bad arguments");
+    if (!h->dfa_ok) return fail(RXG_ETOOBIG, "no memoized step table");
+    const uint8_t d = static_cast<uint8_t>(delimiter);
+    const LtTable t = make_lines_tma_table(h->prog, h->dfa, d);
+    if (!t.ok) return fail(RXG_ETOOBIG, "DFA too large for the TMA line layout");
+    if (chunk == 0 || chunk % kLtSlice) return fail(RXG_EINVAL, "chunk must be a multiple of 32");
+    // same partition as launch_lines_tma: full rows, then remainder pieces
+    std::vector<std::pair<uint64_t, uint64_t>> ranges;
+    const uint64_t rows = len / chunk;
+    for (uint64_t r = 0; r < rows; ++r) ranges.emplace_back(r * chunk, (r + 1) * chunk);
+    const uint64_t rem = len - rows * chunk;
+    if (rem) {
+        uint64_t piece = ((rem + 31) / 32 + 15) & ~uint64_t(15);
+        if (piece < 16) piece = 16;
+        for (uint64_t c0 = rows * chunk; c0 < len; c0 += piece) ranges.emplace_back(c0, std::min(c0 + piece, len));
+    }
+    uint64_t cnt = 0;
+    for (const auto& [c0, c1] : ranges) {
+        uint32_t s = (c0 == 0 || text[c0 - 1] == d) ? t.start : t.skip;
+        for (uint64_t i = c0; i < c1; ++i) {
+            s = lt_step(t, s, text[i]);
+            cnt += s >> 15;
+        }
+        if (s != t.skip && text[c1 - 1] != d) {
+            s += t.tail_delta;
+            uint64_t pos = c1;
+            while (pos < len && s < t.term_acc) {
+                const uint64_t end = std::min<uint64_t>((pos / 16 + 1) * 16, len);
+                for (; pos < end; ++pos) s = lt_step(t, s, text[pos]);
+            }
+            if (s < t.term_acc) s = lt_step(t, s, d);
+            cnt += s == t.term_acc;
         }
     }
     *count = cnt;

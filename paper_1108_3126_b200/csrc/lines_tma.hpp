@@ -1,0 +1,46 @@
+// TMA-staged line kernel: constants, shared-memory layout and launch API.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+#include <vector>
+
+#include "program.hpp"
+
+namespace rxg {
+
+constexpr int kLtWarps = 8;                       // warps per CTA
+constexpr int kLtChains = 2;                      // ranges per lane
+constexpr int kLtRowsPerWarp = 32 * kLtChains;    // ranges per warp tile (TMA box rows)
+constexpr uint32_t kLtSlice = 32;                 // bytes per range per stage (TMA box width)
+constexpr int kLtStages = 4;
+constexpr uint32_t kLtStageBytes = kLtRowsPerWarp * kLtSlice;
+constexpr uint32_t kLtSmemBase = 0x400;           // dynamic shared window start (1 KB reserved)
+constexpr uint32_t kLtAccAddr = 0x8000;           // START_A row: the only main-loop row with bit 15
+constexpr uint32_t kLtRowBytes = 548;             // 256 u16 entries + pad; 137 words = 9 mod 32 banks
+
+// Host-built absolute-address layout of one line table (+ stage ring).
+struct LtTable {
+    bool ok = false;                 // false if the DFA is too large for this layout
+    std::vector<uint8_t> lo, hi;     // images of [lo_addr, +lo) main rows and [hi_addr, +hi) upper rows
+    uint32_t lo_addr = 0, hi_addr = 0;
+    uint32_t lo_bytes = 0, hi_bytes = 0;
+    uint32_t start = 0, skip = 0, void_row = 0, tail_delta = 0, term_acc = 0, term_rej = 0;
+    uint32_t stage_addr[kLtWarps * kLtStages] = {};
+    uint32_t bar_addr = 0;
+    uint32_t smem_bytes = 0;         // dynamic shared memory to request
+    // device copies
+    void* d_lo = nullptr;
+    void* d_hi = nullptr;
+};
+
+LtTable make_lines_tma_table(const Program& p, const Dfa& d, uint8_t delim);
+
+// Host emulation of the table walk (absolute addresses), for CPU tests.
+uint32_t lt_step(const LtTable& t, uint32_t s, uint8_t byte);
+
+cudaError_t launch_lines_tma(const LtTable& t, const uint8_t* text, uint64_t len, uint8_t delim, uint32_t chunk,
+                             unsigned long long* count, cudaStream_t st);
+uint32_t lines_tma_auto_chunk(const LtTable& t, uint64_t len);
+
+}  // namespace rxg

@@ -258,6 +258,13 @@ class Matcher:
                                               res.ctypes.data))
         return cnt.value, res[:nstr]
 
+    def emulate_lines_tma(self, text, delimiter: int = 10, chunk: int = 256) -> int:
+        """Host emulation of the TMA line kernel's table layout and partition -> count."""
+        p, n, keep = _ptr(text)
+        cnt = C.c_uint64(0)
+        _check(L.lib().rxg_host_emulate_lines_tma(self._h, p, n, delimiter, chunk, C.byref(cnt)))
+        return cnt.value
+
     def lockstep_accepts(self, w, engine: str = "auto") -> bool:
         p, n, keep = _ptr(w)
         acc = C.c_int32(0)
