@@ -249,6 +249,8 @@ def main():
     nbytes = len(text_np)
     units = count_units(text_np, delim, stride)
     m = rx.Matcher(pattern, device=dev)
+    if delim >= 0:
+        m.tune(text_np[: 1 << 20], delimiter=delim)   # planner: table bank placement from a 1 MiB sample
     info = m.info()
 
     host = torch.from_numpy(text_np).pin_memory()

@@ -119,6 +119,13 @@ int rxg_heap_create_pattern(const char* pattern, size_t len, int device, rxg_hea
 void rxg_heap_destroy(rxg_heap* h);
 int rxg_heap_info_get(const rxg_heap* h, rxg_heap_info* info);
 
+/* Planner hint: sample the state x byte visit frequencies of typical input
+ * for `delimiter`-separated lines and re-place the shared-memory table rows
+ * so concurrent lanes in different states hit different banks. Changes
+ * speed only, never results. rxg_match_batch_host tunes itself from the
+ * head of its buffer on first use. */
+int rxg_heap_tune(rxg_heap* h, const uint8_t* sample, uint64_t len, int32_t delimiter);
+
 /* Derived tables of the position form, for tests/tools.
  * pos_addr: |C| heap addresses; follow: (|C|+1)*W words; init: W words. */
 int rxg_heap_tables(const rxg_heap* h, int32_t* pos_addr, uint32_t* follow, uint32_t* init);

@@ -56,6 +56,7 @@ _SIG = {
     "rxg_heap_create_pattern": (C.c_int, [C.c_char_p, C.c_size_t, C.c_int, C.POINTER(_P)]),
     "rxg_heap_destroy": (None, [_P]),
     "rxg_heap_info_get": (C.c_int, [_P, C.POINTER(rxg_heap_info)]),
+    "rxg_heap_tune": (C.c_int, [_P, _P, C.c_uint64, C.c_int32]),
     "rxg_heap_tables": (C.c_int, [_P, _P, _P, _P]),
     "rxg_host_walk": (C.c_int, [_P, _P, C.c_uint64, _P, C.POINTER(C.c_int32)]),
     "rxg_host_emulate_batch": (C.c_int, [_P, _P, C.c_uint64, C.c_int32, C.c_uint32, C.c_uint32,

@@ -74,6 +74,7 @@ struct rxg_heap {
     std::mutex mu;
     std::unique_ptr<TableSlot> plain;
     std::map<int, std::unique_ptr<TableSlot>> lines;
+    std::map<int, std::vector<double>> line_freq;   // sampled state x byte counts per delimiter (rxg_heap_tune)
     // staging for host-buffer calls
     uint8_t* d_stage[2] = {nullptr, nullptr};
     size_t stage_bytes = 0;
@@ -150,6 +151,25 @@ int plain_table(rxg_heap* h, const DevTable** out) {
     return RXG_OK;
 }
 
+// (Re)build and upload the TMA line layout for `delim` (caller holds h->mu).
+int build_lt(rxg_heap* h, int delim, LtTable& out) {
+    auto f = h->line_freq.find(delim);
+    LtTable lt = make_lines_tma_table(h->prog, h->dfa, static_cast<uint8_t>(delim),
+                                      f == h->line_freq.end() ? nullptr : &f->second);
+    if (lt.ok && static_cast<int>(lt.smem_bytes) <= h->smem_limit) {
+        RXG_CUDA(cudaMalloc(&lt.d_lo, lt.lo.size()));
+        RXG_CUDA(cudaMalloc(&lt.d_hi, lt.hi.size()));
+        RXG_CUDA(cudaMemcpy(lt.d_lo, lt.lo.data(), lt.lo.size(), cudaMemcpyHostToDevice));
+        RXG_CUDA(cudaMemcpy(lt.d_hi, lt.hi.data(), lt.hi.size(), cudaMemcpyHostToDevice));
+    } else {
+        lt.ok = false;
+    }
+    if (out.d_lo) cudaFree(out.d_lo);
+    if (out.d_hi) cudaFree(out.d_hi);
+    out = std::move(lt);
+    return RXG_OK;
+}
+
 int line_table(rxg_heap* h, int delim, TableSlot** out) {
     std::lock_guard<std::mutex> lk(h->mu);
     auto it = h->lines.find(delim);
@@ -158,16 +178,8 @@ int line_table(rxg_heap* h, int delim, TableSlot** out) {
         const int rc = upload(h, slot, make_line_table(h->prog, h->dfa, static_cast<uint8_t>(delim)));
         if (rc) return rc;
         static const bool no_tma = std::getenv("RXG_NO_TMA") != nullptr;
-        LtTable lt = make_lines_tma_table(h->prog, h->dfa, static_cast<uint8_t>(delim));
-        if (lt.ok && !no_tma && static_cast<int>(lt.smem_bytes) <= h->smem_limit) {
-            RXG_CUDA(cudaMalloc(&lt.d_lo, lt.lo.size()));
-            RXG_CUDA(cudaMalloc(&lt.d_hi, lt.hi.size()));
-            RXG_CUDA(cudaMemcpy(lt.d_lo, lt.lo.data(), lt.lo.size(), cudaMemcpyHostToDevice));
-            RXG_CUDA(cudaMemcpy(lt.d_hi, lt.hi.data(), lt.hi.size(), cudaMemcpyHostToDevice));
-        } else {
-            lt.ok = false;
-        }
-        slot->lt = std::move(lt);
+        if (!no_tma)
+            if (int rc2 = build_lt(h, delim, slot->lt)) return rc2;
         it = h->lines.emplace(delim, std::move(slot)).first;
     }
     *out = it->second.get();
@@ -523,12 +535,26 @@ int rxg_host_emulate_batch(const rxg_heap* h, const uint8_t* text, uint64_t len,
     return RXG_OK;
 }
 
+int rxg_heap_tune(rxg_heap* h, const uint8_t* sample, uint64_t len, int32_t delimiter) {
+    if (!h || (!sample && len) || delimiter < 0 || delimiter > 255) return fail(RXG_EINVAL, "bad arguments");
+    if (!h->dfa_ok) return RXG_OK;
+    std::lock_guard<std::mutex> lk(h->mu);
+    h->line_freq[delimiter] = lt_sample_freq(h->prog, h->dfa, static_cast<uint8_t>(delimiter), sample, len);
+    auto it = h->lines.find(delimiter);
+    if (it != h->lines.end() && it->second->lt.ok && h->device >= 0) {
+        DeviceGuard g(h->device);
+        return build_lt(h, delimiter, it->second->lt);
+    }
+    return RXG_OK;
+}
+
 int rxg_host_emulate_lines_tma(const rxg_heap* h, const uint8_t* text, uint64_t len, int32_t delimiter,
                                uint32_t chunk, uint64_t* count) {
     if (!h || !count || (!text && len) || delimiter < 0 || delimiter > 255) return fail(RXG_EINVAL, "bad arguments");
     if (!h->dfa_ok) return fail(RXG_ETOOBIG, "no memoized step table");
     const uint8_t d = static_cast<uint8_t>(delimiter);
-    const LtTable t = make_lines_tma_table(h->prog, h->dfa, d);
+    auto f = h->line_freq.find(delimiter);
+    const LtTable t = make_lines_tma_table(h->prog, h->dfa, d, f == h->line_freq.end() ? nullptr : &f->second);
     if (!t.ok) return fail(RXG_ETOOBIG, "DFA too large for the TMA line layout");
     if (chunk == 0 || chunk % kLtSlice) return fail(RXG_EINVAL, "chunk must be a multiple of 32");
     // same partition as launch_lines_tma: full rows, then remainder pieces
@@ -610,6 +636,15 @@ int rxg_match_batch_host(rxg_heap* h, const uint8_t* text, uint64_t len, int32_t
     if (!count || (!text && len)) return fail(RXG_EINVAL, "bad arguments");
     if (delimiter < 0 && (stride == 0 || len % stride)) return fail(RXG_EINVAL, "fixed stride must divide the buffer length");
     DeviceGuard g(h->device);
+    if (delimiter >= 0 && delimiter <= 255) {
+        bool tuned;
+        {
+            std::lock_guard<std::mutex> lk(h->mu);
+            tuned = h->line_freq.count(delimiter) != 0;
+        }
+        if (!tuned)   // bank placement from the head of the buffer (speed only)
+            if (int rc = rxg_heap_tune(h, text, std::min<uint64_t>(len, 1u << 20), delimiter)) return rc;
+    }
     // Pipelined: piece k+1 is copied on copy_stream while piece k is matched.
     constexpr uint64_t kPiece = 64ull << 20;
     const std::vector<uint64_t> b = pieces(text, len, delimiter, stride, kPiece);

@@ -3,18 +3,20 @@
 //
 // Data path per warp: the warp owns 64 consecutive equal byte ranges
 // ("rows" of a 2-D view [rows][chunk] of the input) — two per lane. A TMA
-// tensor map streams 32-byte column slices of those 64 rows into a 4-stage
-// shared-memory ring (SWIZZLE_32B, so the per-lane 16-byte reads of 8
-// consecutive rows hit 8 distinct bank groups). One elected lane arms the
+// tensor map streams 16-byte column slices of those 64 rows into a 4-stage
+// shared-memory ring (rows 16 B apart, so the per-lane 16-byte reads of 8
+// consecutive rows fill one 128-byte wavefront). One elected lane arms the
 // stage mbarrier and issues the copy; all lanes wait on its phase.
 //
 // Step per input byte (the memoized lockstep macro step, see tables.hpp):
 //     b = PRMT(word, k)            extract byte
-//     s = LDS.U16 [s + 2b]         s and the entries are absolute shared addresses
+//     s = LDS.U16 [s + 4b]         s and the entries are absolute shared addresses
 //     n += hi32(s * 2^17)          START_A (the accepted-line-end row) is the only
 //                                  row at >= 0x8000 the main loop can enter
-// Rows are 548 B apart (137 words = 9 mod 32 banks), so lanes in different
-// states reading the same byte column land in different banks.
+// Columns are 4 B apart, so the bytes of one row map to banks (row + b) mod 32
+// (' ' and 'a' no longer collide); rows are 1060 B apart (265 words = 9 mod
+// 32), so lanes in different states reading the same byte land in
+// different banks.
 //
 // Line ownership (every line matched exactly once) is the rule of
 // kernels_batch.cu: a range owns the lines starting in it, enters in SKIP
@@ -64,7 +66,7 @@ __device__ __forceinline__ uint4 lds128(uint32_t addr) {
 }
 
 __device__ __forceinline__ uint32_t step(uint32_t s, uint32_t word, int k) {
-    return tab(s + (__byte_perm(word, 0, 0x4440 + k) << 1));
+    return tab(s + __byte_perm(word, 0, 0x4440 + k) * kLtColBytes);
 }
 
 __device__ __forceinline__ uint32_t word_of(const uint4& v, int w) {
@@ -104,11 +106,11 @@ __device__ uint32_t finish_line(const Args& a, uint32_t s, uint64_t pos) {
                 for (int k = 0; k < 4; ++k) s = step(s, word_of(v, w), k);
             pos += 16;
         } else {
-            for (; pos < a.len; ++pos) s = tab(s + (static_cast<uint32_t>(a.text[pos]) << 1));
+            for (; pos < a.len; ++pos) s = tab(s + static_cast<uint32_t>(a.text[pos]) * kLtColBytes);
         }
         if (s >= a.term_acc) return s;
     }
-    return tab(s + (a.delim << 1));
+    return tab(s + a.delim * kLtColBytes);
 }
 
 // A range processed entirely with direct loads (the remainder pieces).
@@ -129,7 +131,7 @@ __device__ void range_direct(const Args& a, uint64_t c0, uint64_t c1, uint32_t& 
     }
     for (; pos < c1; ++pos) {
         last = a.text[pos];
-        s = tab(s + (last << 1));
+        s = tab(s + last * kLtColBytes);
         cnt += __umulhi(s, 1u << 17);
     }
     if (s != a.skip && last != a.delim) cnt += finish_line(a, s + a.tail_delta, c1) == a.term_acc;
@@ -137,7 +139,7 @@ __device__ void range_direct(const Args& a, uint64_t c0, uint64_t c1, uint32_t& 
 
 __global__ void __launch_bounds__(kLtWarps * 32) k_lines_tma(const __grid_constant__ Args a,
                                                              const __grid_constant__ CUtensorMap map) {
-    extern __shared__ __align__(1024) uint8_t sm[];
+    extern __shared__ __align__(128) uint8_t sm[];
     const uint32_t base = static_cast<uint32_t>(__cvta_generic_to_shared(sm));
     if (base != kLtSmemBase) __trap();   // the table's absolute addresses assume this window
     {
@@ -198,7 +200,7 @@ __global__ void __launch_bounds__(kLtWarps * 32) k_lines_tma(const __grid_consta
 #pragma unroll
                 for (int j = 0; j < kLtChains; ++j) {
                     const uint32_t r = j * 32 + lane;
-                    v[j] = lds128(stage[st] + r * kLtSlice + ((g ^ ((r >> 2) & 1u)) << 4));
+                    v[j] = lds128(stage[st] + r * kLtSlice + g * 16u);
                 }
 #pragma unroll
                 for (int w = 0; w < 4; ++w)
@@ -284,7 +286,7 @@ cudaError_t launch_lines_tma(const LtTable& t, const uint8_t* text, uint64_t len
         const cuuint32_t box[2] = {kLtSlice, kLtRowsPerWarp};
         const cuuint32_t estr[2] = {1, 1};
         const CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(text), dims, strides, box,
-                               estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B,
+                               estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                                CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
     } else {

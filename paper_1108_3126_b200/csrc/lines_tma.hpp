@@ -9,15 +9,16 @@
 
 namespace rxg {
 
-constexpr int kLtWarps = 8;                       // warps per CTA
+constexpr int kLtWarps = 32;                      // warps per CTA (one CTA per SM)
 constexpr int kLtChains = 2;                      // ranges per lane
 constexpr int kLtRowsPerWarp = 32 * kLtChains;    // ranges per warp tile (TMA box rows)
-constexpr uint32_t kLtSlice = 32;                 // bytes per range per stage (TMA box width)
+constexpr uint32_t kLtSlice = 16;                 // bytes per range per stage (TMA box width)
 constexpr int kLtStages = 4;
 constexpr uint32_t kLtStageBytes = kLtRowsPerWarp * kLtSlice;
 constexpr uint32_t kLtSmemBase = 0x400;           // dynamic shared window start (1 KB reserved)
 constexpr uint32_t kLtAccAddr = 0x8000;           // START_A row: the only main-loop row with bit 15
-constexpr uint32_t kLtRowBytes = 548;             // 256 u16 entries + pad; 137 words = 9 mod 32 banks
+constexpr uint32_t kLtColBytes = 4;               // column stride: byte b of a row -> bank (row + b) mod 32
+constexpr uint32_t kLtRowBytes = 256 * kLtColBytes;
 
 // Host-built absolute-address layout of one line table (+ stage ring).
 struct LtTable {
@@ -34,7 +35,10 @@ struct LtTable {
     void* d_hi = nullptr;
 };
 
-LtTable make_lines_tma_table(const Program& p, const Dfa& d, uint8_t delim);
+// freq: (S+2) x 256 state-by-byte visit counts of a sample (lt_sample_freq);
+// null = default bank placement.
+LtTable make_lines_tma_table(const Program& p, const Dfa& d, uint8_t delim, const std::vector<double>* freq = nullptr);
+std::vector<double> lt_sample_freq(const Program& p, const Dfa& d, uint8_t delim, const uint8_t* sample, uint64_t len);
 
 // Host emulation of the table walk (absolute addresses), for CPU tests.
 uint32_t lt_step(const LtTable& t, uint32_t s, uint8_t byte);

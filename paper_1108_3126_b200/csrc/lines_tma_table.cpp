@@ -1,15 +1,24 @@
 // Absolute-address shared-memory layout for the TMA line kernel
-// (kernels_lines_tma.cu). Rows are raw-byte indexed u16 entries holding the
-// absolute shared address of the next row, so one IMAD + one LDS advance a
-// string by one byte.
+// (kernels_lines_tma.cu). Rows are raw-byte indexed u16 entries (4-byte
+// column stride) holding the absolute shared address of the next row, so one
+// IMAD + one LDS advance a string by one byte.
 //
-//   [0x400 .. lo_addr)        stage-ring slots (2 KB, 1 KB aligned)
+//   [0x400 .. lo_addr)        stage-ring slots (1 KB, 128 B aligned)
 //   [lo_addr .. 0x8000)       main rows: DFA states 0..S-1, SKIP, VOID (absorbing,
 //                             for lanes whose range lies past the input)
 //   [0x8000]                  START_A (copy of the start row, entered on an
 //                             accepted line end; bit 15 set)
-//   [0x8000 + 548 ..)         tail copies of states 0..S-1, TERM_A, TERM_R
+//   [main + tail_delta ..)    tail copies of states 0..S-1, then TERM_A, TERM_R
 //   [..]                      remaining stage slots, then the mbarriers
+//
+// Bank placement: byte b of a row at word offset o sits in bank (o + b) mod 32.
+// Each main row gets its own o (rows are addressed absolutely, so the choice
+// is free): greedily, hottest row first, the o that minimises the expected
+// number of lanes colliding with already placed rows under the sampled
+// state x byte frequencies (lt_sample_freq). Placement changes speed only,
+// never results.
+#include <algorithm>
+#include <array>
 #include <cstring>
 
 #include "lines_tma.hpp"
@@ -27,59 +36,128 @@ uint32_t align_up(uint32_t x, uint32_t a) { return (x + a - 1) / a * a; }
 
 }  // namespace
 
-LtTable make_lines_tma_table(const Program& p, const Dfa& d, uint8_t delim) {
+std::vector<double> lt_sample_freq(const Program& p, const Dfa& d, uint8_t delim, const uint8_t* sample,
+                                   uint64_t len) {
+    const size_t S = static_cast<size_t>(d.n_states);
+    std::vector<double> f((S + 2) * 256, 0.0);
+    int32_t s = d.start;
+    for (uint64_t i = 0; i < len; ++i) {
+        const uint8_t b = sample[i];
+        f[static_cast<size_t>(s) * 256 + b] += 1.0;
+        s = b == delim ? d.start : d.next[static_cast<size_t>(s) * static_cast<size_t>(d.n_classes) + p.byte_class[b]];
+    }
+    return f;
+}
+
+std::vector<uint32_t> lt_place_rows(const std::vector<double>& f, uint32_t nrows) {
+    // 32-bin bank histograms per row (byte b of a row sits in bank (offset + b) mod 32)
+    std::vector<std::array<double, 32>> H(nrows);
+    std::vector<double> tot(nrows, 0.0);
+    for (uint32_t r = 0; r < nrows; ++r) {
+        H[r].fill(0.0);
+        for (int b = 0; b < 256; ++b) {
+            const double x = r * 256u + static_cast<uint32_t>(b) < f.size() ? f[r * 256u + static_cast<uint32_t>(b)] : 0.0;
+            H[r][static_cast<size_t>(b & 31)] += x;
+            tot[r] += x;
+        }
+    }
+    std::vector<uint32_t> order(nrows);
+    for (uint32_t r = 0; r < nrows; ++r) order[r] = r;
+    std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return tot[a] > tot[b]; });
+    std::vector<uint32_t> off(nrows, 0);
+    std::vector<uint32_t> placed;
+    for (uint32_t r : order) {
+        if (tot[r] == 0.0) {
+            off[r] = (r * 9u) & 31u;
+            continue;
+        }
+        double best = -1.0;
+        uint32_t bo = 0;
+        for (uint32_t o = 0; o < 32; ++o) {
+            double c = 0.0;
+            for (uint32_t r2 : placed)
+                for (uint32_t k = 0; k < 32; ++k) c += H[r][k] * H[r2][(k + o + 32 - off[r2]) & 31u];
+            if (best < 0.0 || c < best) {
+                best = c;
+                bo = o;
+            }
+        }
+        off[r] = bo;
+        placed.push_back(r);
+    }
+    return off;
+}
+
+LtTable make_lines_tma_table(const Program& p, const Dfa& d, uint8_t delim, const std::vector<double>* freq) {
     LtTable t;
     const uint32_t S = static_cast<uint32_t>(d.n_states);
     const uint32_t R = kLtRowBytes;
-    const uint32_t main_bytes = (S + 2) * R;   // + SKIP + VOID
-    if (main_bytes + kLtSmemBase > kLtAccAddr) return t;
-    const uint32_t upper_bytes = (S + 3) * R;
-    if (kLtAccAddr + upper_bytes > 0x10000u) return t;
-    t.lo_addr = (kLtAccAddr - main_bytes) & ~15u;
+    const uint32_t slot = R + 128;   // worst case row + alignment pad
+    // main rows: states 0..S-1, SKIP (S), VOID (S+1), each at a chosen bank offset
+    std::vector<uint32_t> off;
+    if (freq) {
+        off = lt_place_rows(*freq, S + 2);
+    } else {
+        off.resize(S + 2);
+        for (uint32_t r = 0; r < S + 2; ++r) off[r] = (r * 9u) & 31u;
+    }
+    if ((S + 2) * slot + kLtSmemBase > kLtAccAddr) return t;
+    t.lo_addr = (kLtAccAddr - (S + 2) * slot) & ~127u;
+    std::vector<uint32_t> addr(S + 2);
+    uint32_t cur = t.lo_addr;
+    for (uint32_t r = 0; r < S + 2; ++r) {
+        const uint32_t want = off[r] * 4u;
+        addr[r] = cur + ((want + 128u - (cur & 127u)) & 127u);
+        cur = addr[r] + R;
+    }
+    if (cur > kLtAccAddr) return t;
+    // upper region: START_A at 0x8000, tail copies at main + tail_delta, TERM rows
+    t.tail_delta = align_up(kLtAccAddr + R - t.lo_addr, 128);
+    t.term_acc = align_up(cur + t.tail_delta, 4);
+    t.term_rej = t.term_acc + R;
+    const uint32_t hi_end = t.term_rej + R;
+    if (hi_end > 0x10000u) return t;
     t.lo_bytes = align_up(kLtAccAddr - t.lo_addr, 16);
     t.hi_addr = kLtAccAddr;
-    t.hi_bytes = align_up(upper_bytes, 16);
+    t.hi_bytes = align_up(hi_end - kLtAccAddr, 16);
     t.lo.assign(t.lo_bytes, 0);
     t.hi.assign(t.hi_bytes, 0);
-    auto main_row = [&](uint32_t s) { return t.lo_addr + s * R; };
-    auto tail_row = [&](uint32_t s) { return kLtAccAddr + R + s * R; };
+    auto main_row = [&](uint32_t s) { return addr[s]; };
+    auto tail_row = [&](uint32_t s) { return addr[s] + t.tail_delta; };
     t.start = main_row(static_cast<uint32_t>(d.start));
     t.skip = main_row(S);
     t.void_row = main_row(S + 1);
-    t.tail_delta = tail_row(0) - main_row(0);
-    t.term_acc = tail_row(S);
-    t.term_rej = tail_row(S + 1);
     auto next = [&](uint32_t s, int b) {
         return static_cast<uint32_t>(d.next[static_cast<size_t>(s) * static_cast<size_t>(d.n_classes) + p.byte_class[b]]);
     };
+    auto put_lo = [&](uint32_t row, int b, uint32_t v) { put16(t.lo, row - t.lo_addr + kLtColBytes * static_cast<uint32_t>(b), v); };
+    auto put_hi = [&](uint32_t row, int b, uint32_t v) { put16(t.hi, row - kLtAccAddr + kLtColBytes * static_cast<uint32_t>(b), v); };
     for (uint32_t s = 0; s < S; ++s) {
         const bool acc = d.accept[s] != 0;
         for (int b = 0; b < 256; ++b) {
-            const uint32_t mo = main_row(s) - t.lo_addr + 2u * static_cast<uint32_t>(b);
-            const uint32_t to = tail_row(s) - kLtAccAddr + 2u * static_cast<uint32_t>(b);
             if (b == delim) {
-                put16(t.lo, mo, acc ? kLtAccAddr : t.start);
-                put16(t.hi, to, acc ? t.term_acc : t.term_rej);
+                put_lo(main_row(s), b, acc ? kLtAccAddr : t.start);
+                put_hi(tail_row(s), b, acc ? t.term_acc : t.term_rej);
             } else {
-                put16(t.lo, mo, main_row(next(s, b)));
-                put16(t.hi, to, tail_row(next(s, b)));
+                put_lo(main_row(s), b, main_row(next(s, b)));
+                put_hi(tail_row(s), b, tail_row(next(s, b)));
             }
         }
     }
     for (int b = 0; b < 256; ++b) {
-        put16(t.lo, t.skip - t.lo_addr + 2u * static_cast<uint32_t>(b), b == delim ? t.start : t.skip);
-        put16(t.lo, t.void_row - t.lo_addr + 2u * static_cast<uint32_t>(b), t.void_row);
-        put16(t.hi, t.term_acc - kLtAccAddr + 2u * static_cast<uint32_t>(b), t.term_acc);
-        put16(t.hi, t.term_rej - kLtAccAddr + 2u * static_cast<uint32_t>(b), t.term_rej);
+        put_lo(t.skip, b, b == delim ? t.start : t.skip);
+        put_lo(t.void_row, b, t.void_row);
+        put_hi(t.term_acc, b, t.term_acc);
+        put_hi(t.term_rej, b, t.term_rej);
     }
     std::memcpy(&t.hi[0], &t.lo[t.start - t.lo_addr], R);   // START_A = start row
 
     // stage slots: first in the gap below the main rows, then after the upper rows
-    int slot = 0;
-    for (uint32_t a = kLtSmemBase; a + kLtStageBytes <= t.lo_addr && slot < kLtWarps * kLtStages; a += kLtStageBytes)
-        t.stage_addr[slot++] = a;
-    uint32_t a = align_up(kLtAccAddr + t.hi_bytes, 1024);
-    for (; slot < kLtWarps * kLtStages; ++slot, a += kLtStageBytes) t.stage_addr[slot] = a;
+    int k = 0;
+    for (uint32_t a = kLtSmemBase; a + kLtStageBytes <= t.lo_addr && k < kLtWarps * kLtStages; a += kLtStageBytes)
+        t.stage_addr[k++] = a;
+    uint32_t a = align_up(kLtAccAddr + t.hi_bytes, 128);
+    for (; k < kLtWarps * kLtStages; ++k, a += kLtStageBytes) t.stage_addr[k] = a;
     t.bar_addr = align_up(a, 8);
     t.smem_bytes = t.bar_addr + kLtWarps * kLtStages * 8 - kLtSmemBase;
     t.ok = true;
@@ -88,8 +166,8 @@ LtTable make_lines_tma_table(const Program& p, const Dfa& d, uint8_t delim) {
 
 uint32_t lt_step(const LtTable& t, uint32_t s, uint8_t byte) {
     uint16_t v;
-    if (s < kLtAccAddr) std::memcpy(&v, &t.lo[s - t.lo_addr + 2u * byte], 2);
-    else std::memcpy(&v, &t.hi[s - kLtAccAddr + 2u * byte], 2);
+    if (s < kLtAccAddr) std::memcpy(&v, &t.lo[s - t.lo_addr + kLtColBytes * byte], 2);
+    else std::memcpy(&v, &t.hi[s - kLtAccAddr + kLtColBytes * byte], 2);
     return v;
 }
 

@@ -229,6 +229,11 @@ class Matcher:
         _check(L.lib().rxg_heap_info_get(self._h, C.byref(i)))
         return {f: getattr(i, f) for f, _ in L.rxg_heap_info._fields_}
 
+    def tune(self, sample, delimiter: int = 10):
+        """Planner hint: place table rows for the state/byte mix of `sample` (speed only)."""
+        p, n, keep = _ptr(sample)
+        _check(L.lib().rxg_heap_tune(self._h, p, n, delimiter))
+
     def tables(self):
         """(pos_addr, follow[(|C|+1) x W], init[W]) of the position form."""
         inf = self.info()
