@@ -156,7 +156,7 @@ int build_lt(rxg_heap* h, int delim, LtTable& out) {
     auto f = h->line_freq.find(delim);
     LtTable lt = make_lines_tma_table(h->prog, h->dfa, static_cast<uint8_t>(delim),
                                       f == h->line_freq.end() ? nullptr : &f->second);
-    if (lt.ok && static_cast<int>(lt.smem_bytes) <= h->smem_limit) {
+    if (lt.ok && static_cast<int>(lt.smem_table_end - kLtSmemBase) + 96 * 1024 <= h->smem_limit) {
         RXG_CUDA(cudaMalloc(&lt.d_lo, lt.lo.size()));
         RXG_CUDA(cudaMalloc(&lt.d_hi, lt.hi.size()));
         RXG_CUDA(cudaMemcpy(lt.d_lo, lt.lo.data(), lt.lo.size(), cudaMemcpyHostToDevice));
@@ -187,11 +187,8 @@ int line_table(rxg_heap* h, int delim, TableSlot** out) {
 }
 
 uint32_t env_chunk() {
-    static const uint32_t v = [] {
-        const char* e = std::getenv("RXG_LINE_CHUNK");
-        return e ? static_cast<uint32_t>(std::strtoul(e, nullptr, 10)) : 0u;
-    }();
-    return v;
+    const char* e = std::getenv("RXG_LINE_CHUNK");   // tuning override (bytes per range)
+    return e ? static_cast<uint32_t>(std::strtoul(e, nullptr, 10)) : 0u;
 }
 
 Heap heap_from_c(const rxg_node* nodes, const int32_t* knodes, int32_t n) {
@@ -246,7 +243,7 @@ int batch_device(rxg_heap* h, const uint8_t* d_text, uint64_t len, int32_t delim
         if (int rc = line_table(h, delimiter, &slot)) return rc;
         if (!d_results && slot->lt.ok) {
             uint32_t chunk = env_chunk();
-            if (chunk == 0 || chunk % kLtSlice) chunk = lines_tma_auto_chunk(slot->lt, len);
+            if (chunk % lines_tma_slice()) chunk = 0;
             const cudaError_t e = launch_lines_tma(slot->lt, d_text, len, static_cast<uint8_t>(delimiter), chunk,
                                                    d_count, st);
             if (e != cudaSuccess) return cuda_fail(e, "launch_lines_tma");
@@ -556,7 +553,7 @@ int rxg_host_emulate_lines_tma(const rxg_heap* h, const uint8_t* text, uint64_t 
     auto f = h->line_freq.find(delimiter);
     const LtTable t = make_lines_tma_table(h->prog, h->dfa, d, f == h->line_freq.end() ? nullptr : &f->second);
     if (!t.ok) return fail(RXG_ETOOBIG, "DFA too large for the TMA line layout");
-    if (chunk == 0 || chunk % kLtSlice) return fail(RXG_EINVAL, "chunk must be a multiple of 32");
+    if (chunk == 0 || chunk % 16) return fail(RXG_EINVAL, "chunk must be a multiple of 16");
     // same partition as launch_lines_tma: full rows, then remainder pieces
     std::vector<std::pair<uint64_t, uint64_t>> ranges;
     const uint64_t rows = len / chunk;

@@ -3,10 +3,11 @@
 //
 // Data path per warp: the warp owns 64 consecutive equal byte ranges
 // ("rows" of a 2-D view [rows][chunk] of the input) — two per lane. A TMA
-// tensor map streams 16-byte column slices of those 64 rows into a 4-stage
-// shared-memory ring (rows 16 B apart, so the per-lane 16-byte reads of 8
-// consecutive rows fill one 128-byte wavefront). One elected lane arms the
-// stage mbarrier and issues the copy; all lanes wait on its phase.
+// tensor map streams 32-byte column slices of those 64 rows into a 3-stage
+// shared-memory ring (SWIZZLE_32B, so the per-lane 16-byte reads of 8
+// consecutive rows hit 8 distinct bank groups). One elected lane arms the
+// stage mbarrier and issues the copy; all lanes wait on its phase. 24 warps
+// per CTA, one CTA per SM (the table plus ring use ~188 KB of shared memory).
 //
 // Step per input byte (the memoized lockstep macro step, see tables.hpp):
 //     b = PRMT(word, k)            extract byte
@@ -25,6 +26,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <cstring>
 
 #include "launch.hpp"
@@ -34,12 +36,14 @@ namespace rxg {
 
 namespace {
 
+constexpr int kMaxSlots = 128;
+
 struct Args {
     const uint8_t* text;
     uint64_t len;
     uint64_t rows;         // full ranges covered by the tensor map
-    uint64_t tiles;        // ceil(rows / kRowsPerWarp)
-    uint32_t chunk;        // range width (multiple of kSlice)
+    uint64_t tiles;        // ceil(rows / rows per warp)
+    uint32_t chunk;        // range width (multiple of the slice)
     uint32_t rem_piece;    // remainder [rows*chunk, len) split in pieces (direct loads)
     uint32_t rem_pieces;
     const uint4* img_lo;
@@ -47,10 +51,18 @@ struct Args {
     const uint4* img_hi;
     uint32_t hi_addr, hi_words;
     uint32_t bar_addr;
-    uint32_t stage_addr[kLtWarps * kLtStages];
+    uint32_t stage_addr[kMaxSlots];
     uint32_t start, skip, void_row, tail_delta, term_acc;
     uint32_t delim;
     unsigned long long* count;
+};
+
+// Kernel shape: warps per CTA, ranges per lane, bytes per range per stage, ring depth.
+template <int W, int K, int SL, int ST>
+struct Shape {
+    static constexpr int warps = W, chains = K, slice = SL, stages = ST, rows = 32 * K;
+    static constexpr uint32_t stage_bytes = static_cast<uint32_t>(rows * SL);
+    static_assert(W * ST <= kMaxSlots, "stage table too small");
 };
 
 __device__ __forceinline__ uint32_t tab(uint32_t addr) {
@@ -87,12 +99,24 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
         : "memory");
 }
 
+template <uint32_t BYTES>
 __device__ __forceinline__ void tma_issue(const CUtensorMap* map, uint32_t dst, uint32_t bar, int32_t x, int32_t y) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "n"(kLtStageBytes) : "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "n"(BYTES) : "memory");
     asm volatile(
         "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
         "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar)
         : "memory");
+}
+
+// Physical 16-byte granule of logical granule g in row r of a stage: the
+// TMA swizzle (none / 32B / 64B / 128B by slice width) XORs the granule
+// index with row bits so 8 consecutive rows hit 8 distinct bank groups.
+template <int SL>
+__device__ __forceinline__ uint32_t granule(uint32_t r, uint32_t g) {
+    if constexpr (SL == 16) return 0;
+    else if constexpr (SL == 32) return g ^ ((r >> 2) & 1u);
+    else if constexpr (SL == 64) return g ^ ((r >> 1) & 3u);
+    else return g ^ (r & 7u);
 }
 
 // Finish the line straddling a range end with direct loads (tail copy rows).
@@ -137,9 +161,10 @@ __device__ void range_direct(const Args& a, uint64_t c0, uint64_t c1, uint32_t& 
     if (s != a.skip && last != a.delim) cnt += finish_line(a, s + a.tail_delta, c1) == a.term_acc;
 }
 
-__global__ void __launch_bounds__(kLtWarps * 32) k_lines_tma(const __grid_constant__ Args a,
+template <class C>
+__global__ void __launch_bounds__(C::warps * 32) k_lines_tma(const __grid_constant__ Args a,
                                                              const __grid_constant__ CUtensorMap map) {
-    extern __shared__ __align__(128) uint8_t sm[];
+    extern __shared__ __align__(1024) uint8_t sm[];
     const uint32_t base = static_cast<uint32_t>(__cvta_generic_to_shared(sm));
     if (base != kLtSmemBase) __trap();   // the table's absolute addresses assume this window
     {
@@ -149,9 +174,9 @@ __global__ void __launch_bounds__(kLtWarps * 32) k_lines_tma(const __grid_consta
         for (uint32_t i = threadIdx.x; i < a.hi_words; i += blockDim.x) hi[i] = a.img_hi[i];
     }
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t bar0 = a.bar_addr + warp * kLtStages * 8;
+    const uint32_t bar0 = a.bar_addr + warp * C::stages * 8;
     if (lane == 0) {
-        for (int st = 0; st < kLtStages; ++st) mbar_init(bar0 + st * 8, 1);
+        for (int st = 0; st < C::stages; ++st) mbar_init(bar0 + st * 8, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (threadIdx.x == 0) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map)) : "memory");
@@ -167,20 +192,21 @@ __global__ void __launch_bounds__(kLtWarps * 32) k_lines_tma(const __grid_consta
     }
 
     uint32_t phase = 0;   // bit st = parity of stage st's next completion
-    const uint32_t ncol = a.chunk / kLtSlice;
-    const uint32_t* stage = a.stage_addr + warp * kLtStages;
-    for (uint64_t tile = static_cast<uint64_t>(blockIdx.x) * kLtWarps + warp; tile < a.tiles;
-         tile += static_cast<uint64_t>(gridDim.x) * kLtWarps) {
-        const uint64_t row0 = tile * kLtRowsPerWarp;
+    const uint32_t ncol = a.chunk / C::slice;
+    const uint32_t* stage = a.stage_addr + warp * C::stages;
+    for (uint64_t tile = static_cast<uint64_t>(blockIdx.x) * C::warps + warp; tile < a.tiles;
+         tile += static_cast<uint64_t>(gridDim.x) * C::warps) {
+        const uint64_t row0 = tile * C::rows;
         if (lane == 0) {
-            const uint32_t pro = ncol < kLtStages ? ncol : kLtStages;
+            const uint32_t pro = ncol < C::stages ? ncol : C::stages;
             for (uint32_t st = 0; st < pro; ++st)
-                tma_issue(&map, stage[st], bar0 + st * 8, static_cast<int32_t>(st * kLtSlice), static_cast<int32_t>(row0));
+                tma_issue<C::stage_bytes>(&map, stage[st], bar0 + st * 8, static_cast<int32_t>(st * C::slice),
+                                          static_cast<int32_t>(row0));
         }
-        uint32_t s[kLtChains];
-        bool valid[kLtChains];
+        uint32_t s[C::chains];
+        bool valid[C::chains];
 #pragma unroll
-        for (int j = 0; j < kLtChains; ++j) {
+        for (int j = 0; j < C::chains; ++j) {
             const uint64_t row = row0 + j * 32 + lane;
             valid[j] = row < a.rows;
             s[j] = a.void_row;
@@ -189,40 +215,40 @@ __global__ void __launch_bounds__(kLtWarps * 32) k_lines_tma(const __grid_consta
                 s[j] = (c0 == 0 || a.text[c0 - 1] == a.delim) ? a.start : a.skip;
             }
         }
-        uint32_t last[kLtChains] = {};
+        uint32_t last[C::chains] = {};
         for (uint32_t col = 0; col < ncol; ++col) {
-            const uint32_t st = col % kLtStages;
+            const uint32_t st = col % C::stages;
             mbar_wait(bar0 + st * 8, (phase >> st) & 1u);
             phase ^= 1u << st;
 #pragma unroll
-            for (int g = 0; g < kLtSlice / 16; ++g) {
-                uint4 v[kLtChains];
+            for (int g = 0; g < C::slice / 16; ++g) {
+                uint4 v[C::chains];
 #pragma unroll
-                for (int j = 0; j < kLtChains; ++j) {
+                for (int j = 0; j < C::chains; ++j) {
                     const uint32_t r = j * 32 + lane;
-                    v[j] = lds128(stage[st] + r * kLtSlice + g * 16u);
+                    v[j] = lds128(stage[st] + r * C::slice + (granule<C::slice>(r, g) << 4));
                 }
 #pragma unroll
                 for (int w = 0; w < 4; ++w)
 #pragma unroll
                     for (int k = 0; k < 4; ++k)
 #pragma unroll
-                        for (int j = 0; j < kLtChains; ++j) {
+                        for (int j = 0; j < C::chains; ++j) {
                             s[j] = step(s[j], word_of(v[j], w), k);
                             cnt += __umulhi(s[j], 1u << 17);
                         }
 #pragma unroll
-                for (int j = 0; j < kLtChains; ++j) last[j] = v[j].w >> 24;
+                for (int j = 0; j < C::chains; ++j) last[j] = v[j].w >> 24;
             }
             __syncwarp();
-            if (lane == 0 && col + kLtStages < ncol) {
+            if (lane == 0 && col + C::stages < ncol) {
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                tma_issue(&map, stage[st], bar0 + st * 8, static_cast<int32_t>((col + kLtStages) * kLtSlice),
-                          static_cast<int32_t>(row0));
+                tma_issue<C::stage_bytes>(&map, stage[st], bar0 + st * 8, static_cast<int32_t>((col + C::stages) * C::slice),
+                                          static_cast<int32_t>(row0));
             }
         }
 #pragma unroll
-        for (int j = 0; j < kLtChains; ++j) {
+        for (int j = 0; j < C::chains; ++j) {
             if (valid[j] && s[j] != a.skip && last[j] != a.delim) {
                 const uint64_t row = row0 + j * 32 + lane;
                 cnt += finish_line(a, s[j] + a.tail_delta, (row + 1) * a.chunk) == a.term_acc;
@@ -245,18 +271,63 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     return fn;
 }
 
-}  // namespace
+uint32_t align_up(uint32_t x, uint32_t a) { return (x + a - 1) / a * a; }
 
-cudaError_t launch_lines_tma(const LtTable& t, const uint8_t* text, uint64_t len, uint8_t delim, uint32_t chunk,
-                             unsigned long long* count, cudaStream_t st) {
+// Stage slots: first the gap below the main rows, then after the upper rows.
+template <class C>
+uint32_t place_stages(const LtTable& t, Args& a) {
+    int k = 0;
+    for (uint32_t p = kLtSmemBase; p + C::stage_bytes <= t.lo_addr && k < C::warps * C::stages; p += C::stage_bytes)
+        a.stage_addr[k++] = p;
+    uint32_t p = align_up(kLtAccAddr + t.hi_bytes, 1024);
+    for (; k < C::warps * C::stages; ++k, p += C::stage_bytes) a.stage_addr[k] = p;
+    a.bar_addr = align_up(p, 8);
+    return a.bar_addr + C::warps * C::stages * 8 - kLtSmemBase;
+}
+
+CUtensorMapSwizzle swizzle_of(int slice) {
+    switch (slice) {
+    case 32: return CU_TENSOR_MAP_SWIZZLE_32B;
+    case 64: return CU_TENSOR_MAP_SWIZZLE_64B;
+    case 128: return CU_TENSOR_MAP_SWIZZLE_128B;
+    default: return CU_TENSOR_MAP_SWIZZLE_NONE;
+    }
+}
+
+template <class C>
+int per_sm_of(uint32_t smem) {
+    int per_sm = 0;
+    cudaFuncSetAttribute(k_lines_tma<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_lines_tma<C>, C::warps * 32, smem);
+    return per_sm < 1 ? 1 : per_sm;
+}
+
+template <class C>
+uint32_t auto_chunk(const LtTable& t, uint64_t len) {
+    Args a{};
+    const uint32_t smem = place_stages<C>(t, a);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const uint64_t rows = static_cast<uint64_t>(per_sm_of<C>(smem)) * device_sm_count(dev) * C::warps * C::rows;
+    uint64_t c = (len + rows - 1) / rows;
+    c = (c + C::slice - 1) / C::slice * C::slice;
+    if (c < 4u * C::slice) c = 4u * C::slice;
+    if (c > (1u << 20)) c = 1u << 20;
+    return static_cast<uint32_t>(c);
+}
+
+template <class C>
+cudaError_t launch(const LtTable& t, const uint8_t* text, uint64_t len, uint8_t delim, uint32_t chunk,
+                   unsigned long long* count, cudaStream_t st) {
     if (len == 0) return cudaSuccess;
-    if (chunk % kLtSlice) return cudaErrorInvalidValue;
+    if (chunk == 0) chunk = auto_chunk<C>(t, len);
+    if (chunk % C::slice) return cudaErrorInvalidValue;
     Args a{};
     a.text = text;
     a.len = len;
     a.chunk = chunk;
     a.rows = len / chunk;
-    a.tiles = (a.rows + kLtRowsPerWarp - 1) / kLtRowsPerWarp;
+    a.tiles = (a.rows + C::rows - 1) / C::rows;
     const uint64_t rem = len - a.rows * chunk;
     a.rem_piece = static_cast<uint32_t>(((rem + 31) / 32 + 15) & ~uint64_t(15));
     if (a.rem_piece < 16) a.rem_piece = 16;
@@ -267,8 +338,7 @@ cudaError_t launch_lines_tma(const LtTable& t, const uint8_t* text, uint64_t len
     a.img_hi = static_cast<const uint4*>(t.d_hi);
     a.hi_addr = t.hi_addr;
     a.hi_words = t.hi_bytes / 16;
-    a.bar_addr = t.bar_addr;
-    for (int i = 0; i < kLtWarps * kLtStages; ++i) a.stage_addr[i] = t.stage_addr[i];
+    const uint32_t smem = place_stages<C>(t, a);
     a.start = t.start;
     a.skip = t.skip;
     a.void_row = t.void_row;
@@ -278,48 +348,64 @@ cudaError_t launch_lines_tma(const LtTable& t, const uint8_t* text, uint64_t len
     a.count = count;
 
     CUtensorMap map;
+    std::memset(&map, 0, sizeof(map));
     if (a.rows > 0) {
         auto enc = encode_fn();
         if (!enc) return cudaErrorNotSupported;
         const cuuint64_t dims[2] = {chunk, a.rows};
         const cuuint64_t strides[1] = {chunk};
-        const cuuint32_t box[2] = {kLtSlice, kLtRowsPerWarp};
+        const cuuint32_t box[2] = {static_cast<cuuint32_t>(C::slice), static_cast<cuuint32_t>(C::rows)};
         const cuuint32_t estr[2] = {1, 1};
+        CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
+        if (const char* e = std::getenv("RXG_TMA_PROMO")) {   // tuning override
+            const int v = std::atoi(e);
+            promo = v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+                    : v == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                    : v == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+        }
         const CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(text), dims, strides, box,
-                               estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                               CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                               estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle_of(C::slice), promo,
+                               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
-    } else {
-        std::memset(&map, 0, sizeof(map));
     }
-    const uint32_t smem = t.smem_bytes;
-    cudaError_t e = cudaFuncSetAttribute(k_lines_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    if (e != cudaSuccess) return e;
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_lines_tma, kLtWarps * 32, smem);
-    if (per_sm < 1) per_sm = 1;
+    const int per_sm = per_sm_of<C>(smem);
     int dev = 0;
     cudaGetDevice(&dev);
     const uint64_t cap = static_cast<uint64_t>(per_sm) * device_sm_count(dev);
-    const uint64_t want = (a.tiles + kLtWarps - 1) / kLtWarps;
+    const uint64_t want = (a.tiles + C::warps - 1) / C::warps;
     const int grid = static_cast<int>(want == 0 ? 1 : (want < cap ? want : cap));
-    k_lines_tma<<<grid, kLtWarps * 32, smem, st>>>(a, map);
+    k_lines_tma<C><<<grid, C::warps * 32, smem, st>>>(a, map);
     return cudaGetLastError();
 }
 
-uint32_t lines_tma_auto_chunk(const LtTable& t, uint64_t len) {
-    int per_sm = 0;
-    cudaFuncSetAttribute(k_lines_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(t.smem_bytes));
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_lines_tma, kLtWarps * 32, t.smem_bytes);
-    if (per_sm < 1) per_sm = 1;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    const uint64_t rows = static_cast<uint64_t>(per_sm) * device_sm_count(dev) * kLtWarps * kLtRowsPerWarp;
-    uint64_t c = (len + rows - 1) / rows;
-    c = (c + kLtSlice - 1) / kLtSlice * kLtSlice;
-    if (c < 4 * kLtSlice) c = 4 * kLtSlice;
-    if (c > (1u << 20)) c = 1u << 20;
-    return static_cast<uint32_t>(c);
+// Kernel shapes (RXG_LT_SHAPE selects one for tuning runs; 0 is the default).
+// Measured on config (c), 1 GB, B200 (tools/ab_lines.py): 16-byte slices are
+// TMA-request bound (~3.3 TB/s); 32-byte slices with 24 warps x 2 ranges x 3
+// stages reach ~5.05 TB/s; 4 stages / 3 ranges per lane give the same.
+using S0 = Shape<24, 2, 32, 3>;
+using S1 = Shape<16, 2, 32, 4>;
+using S2 = Shape<24, 2, 32, 2>;
+using S3 = Shape<16, 3, 32, 3>;
+using S4 = Shape<32, 2, 16, 4>;
+
+int shape_id() {
+    const char* e = std::getenv("RXG_LT_SHAPE");
+    return e ? std::atoi(e) : 0;
 }
+
+}  // namespace
+
+cudaError_t launch_lines_tma(const LtTable& t, const uint8_t* text, uint64_t len, uint8_t delim, uint32_t chunk,
+                             unsigned long long* count, cudaStream_t st) {
+    switch (shape_id()) {
+    case 1: return launch<S1>(t, text, len, delim, chunk, count, st);
+    case 2: return launch<S2>(t, text, len, delim, chunk, count, st);
+    case 3: return launch<S3>(t, text, len, delim, chunk, count, st);
+    case 4: return launch<S4>(t, text, len, delim, chunk, count, st);
+    default: return launch<S0>(t, text, len, delim, chunk, count, st);
+    }
+}
+
+uint32_t lines_tma_slice() { return shape_id() == 4 ? 16 : 32; }
 
 }  // namespace rxg

@@ -9,12 +9,6 @@
 
 namespace rxg {
 
-constexpr int kLtWarps = 32;                      // warps per CTA (one CTA per SM)
-constexpr int kLtChains = 2;                      // ranges per lane
-constexpr int kLtRowsPerWarp = 32 * kLtChains;    // ranges per warp tile (TMA box rows)
-constexpr uint32_t kLtSlice = 16;                 // bytes per range per stage (TMA box width)
-constexpr int kLtStages = 4;
-constexpr uint32_t kLtStageBytes = kLtRowsPerWarp * kLtSlice;
 constexpr uint32_t kLtSmemBase = 0x400;           // dynamic shared window start (1 KB reserved)
 constexpr uint32_t kLtAccAddr = 0x8000;           // START_A row: the only main-loop row with bit 15
 constexpr uint32_t kLtColBytes = 4;               // column stride: byte b of a row -> bank (row + b) mod 32
@@ -27,9 +21,7 @@ struct LtTable {
     uint32_t lo_addr = 0, hi_addr = 0;
     uint32_t lo_bytes = 0, hi_bytes = 0;
     uint32_t start = 0, skip = 0, void_row = 0, tail_delta = 0, term_acc = 0, term_rej = 0;
-    uint32_t stage_addr[kLtWarps * kLtStages] = {};
-    uint32_t bar_addr = 0;
-    uint32_t smem_bytes = 0;         // dynamic shared memory to request
+    uint32_t smem_table_end = 0;     // end of the table regions (stage ring placed at launch)
     // device copies
     void* d_lo = nullptr;
     void* d_hi = nullptr;
@@ -43,8 +35,9 @@ std::vector<double> lt_sample_freq(const Program& p, const Dfa& d, uint8_t delim
 // Host emulation of the table walk (absolute addresses), for CPU tests.
 uint32_t lt_step(const LtTable& t, uint32_t s, uint8_t byte);
 
+// chunk = bytes per range (multiple of lines_tma_slice()), 0 = one wave of ranges.
 cudaError_t launch_lines_tma(const LtTable& t, const uint8_t* text, uint64_t len, uint8_t delim, uint32_t chunk,
                              unsigned long long* count, cudaStream_t st);
-uint32_t lines_tma_auto_chunk(const LtTable& t, uint64_t len);
+uint32_t lines_tma_slice();
 
 }  // namespace rxg

@@ -152,14 +152,7 @@ LtTable make_lines_tma_table(const Program& p, const Dfa& d, uint8_t delim, cons
     }
     std::memcpy(&t.hi[0], &t.lo[t.start - t.lo_addr], R);   // START_A = start row
 
-    // stage slots: first in the gap below the main rows, then after the upper rows
-    int k = 0;
-    for (uint32_t a = kLtSmemBase; a + kLtStageBytes <= t.lo_addr && k < kLtWarps * kLtStages; a += kLtStageBytes)
-        t.stage_addr[k++] = a;
-    uint32_t a = align_up(kLtAccAddr + t.hi_bytes, 128);
-    for (; k < kLtWarps * kLtStages; ++k, a += kLtStageBytes) t.stage_addr[k] = a;
-    t.bar_addr = align_up(a, 8);
-    t.smem_bytes = t.bar_addr + kLtWarps * kLtStages * 8 - kLtSmemBase;
+    t.smem_table_end = kLtAccAddr + t.hi_bytes;
     t.ok = true;
     return t;
 }
