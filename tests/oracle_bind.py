@@ -51,6 +51,13 @@ class Oracle:
                                                 C.c_void_p, C.c_int]
         self.lib.oracle_accepts_bytes.restype = C.c_int
         self.lib.oracle_accepts_bytes.argtypes = [C.POINTER(_Heap), C.c_void_p, C.c_uint64]
+        P = C.c_void_p
+        for fn, res, args in [("oracle_ws_init", None, [P, C.c_int32]), ("oracle_ws_free", None, [P]),
+                              ("oracle_evolve", C.c_int32, [C.POINTER(_Heap), P, P, C.c_int32, P, P]),
+                              ("oracle_step_char", C.c_int32, [C.POINTER(_Heap), P, P, C.c_int32, C.c_uint32, P]),
+                              ("oracle_eps_reaches_null", C.c_int, [C.POINTER(_Heap), P, P, C.c_int32])]:
+            getattr(self.lib, fn).restype = res
+            getattr(self.lib, fn).argtypes = args
         n = heap.size()
         self._nodes = (_Node * n)()
         for i, x in enumerate(heap.nodes):
@@ -62,6 +69,43 @@ class Oracle:
     def accepts(self, w: bytes) -> bool:
         buf = C.create_string_buffer(bytes(w), max(len(w), 1))
         return bool(self.lib.oracle_accepts_bytes(C.byref(self.h), buf, len(w)))
+
+    # set-level functions (lockstep.cpp:10-73), sets as Python sets of addresses (-1 = null)
+    def _ws(self):
+        class WS(C.Structure):
+            _fields_ = [("n", C.c_int32), ("seen", C.c_void_p), ("queue", C.c_void_p), ("epoch", C.c_uint32)]
+        ws = WS()
+        self.lib.oracle_ws_init(C.byref(ws), self.h.n)
+        return ws
+
+    def evolve(self, s) -> set:
+        k, out = self._evolve(s)
+        return set(out[:k].tolist())
+
+    def _evolve(self, s):
+        ws = self._ws()
+        a = np.array(sorted(s), np.int32)
+        out = np.zeros(2 * self.h.n + len(a) + 2, np.int32)
+        k = self.lib.oracle_evolve(C.byref(self.h), C.byref(ws), a.ctypes.data, len(a), out.ctypes.data, None)
+        self.lib.oracle_ws_free(C.byref(ws))
+        return k, out
+
+    def step_char(self, s, a: int) -> set:
+        ws = self._ws()
+        arr = np.array(sorted(s), np.int32)
+        out = np.zeros(2 * self.h.n + len(arr) + 2, np.int32)
+        k = self.lib.oracle_step_char(C.byref(self.h), C.byref(ws), arr.ctypes.data, len(arr), a, out.ctypes.data)
+        self.lib.oracle_ws_free(C.byref(ws))
+        if k < 0:
+            raise ValueError("step_char: unevolved member")
+        return set(out[:k].tolist())
+
+    def eps_reaches_null(self, s) -> bool:
+        ws = self._ws()
+        arr = np.array(sorted(s), np.int32)
+        r = self.lib.oracle_eps_reaches_null(C.byref(self.h), C.byref(ws), arr.ctypes.data, len(arr))
+        self.lib.oracle_ws_free(C.byref(ws))
+        return bool(r)
 
     def match_batch(self, text: np.ndarray, delimiter=10, stride=0, results=True, threads=None):
         a = np.ascontiguousarray(text, np.uint8)
