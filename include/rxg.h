@@ -156,6 +156,23 @@ int rxg_match_one(rxg_heap* h, const uint8_t* bytes, uint64_t len, int engine, i
 int rxg_match_one_device(rxg_heap* h, const uint8_t* d_bytes, uint64_t len, int engine,
                          int32_t* d_accept, void* stream);
 
+/* Per-engine options and instrumentation for rxg_match_one_ex (all optional;
+ * zero-initialise). Device pointers. */
+typedef struct rxg_one_opts {
+    uint32_t checkpoint_every;        /* PERNODE: E set (W words) after every k symbols ... */
+    uint32_t* d_checkpoints;          /* ... into (len / k) x W words (the chunk-parallel oracle check) */
+    unsigned long long* d_stats;      /* ROUNDS: claims, rounds, macro steps, max claims per node per step
+                                         (rx::ParStats, parallel.hpp:52-58) */
+    uint32_t* d_trace;                /* ROUNDS: per symbol the next schedule as (N+1)-bit rows, bit N = null;
+                                         zeroed by the caller (test_parallel.cpp:114-137) */
+    uint32_t chunk;                   /* CHUNKED: bytes per range (multiple of 64), 0 = auto */
+    uint32_t lookback;                /* CHUNKED: bytes walked before a range to guess its entry state (0 = 64) */
+    unsigned long long* d_repairs;    /* CHUNKED: ranges re-walked by the in-order repair pass */
+} rxg_one_opts;
+
+int rxg_match_one_ex(rxg_heap* h, const uint8_t* d_bytes, uint64_t len, int engine, int32_t* d_accept,
+                     const rxg_one_opts* opts, void* stream);
+
 /* Batch over a device buffer, asynchronous on `stream`.
  *   delimiter in [0,255]: strings are the lines of the buffer split on that
  *     byte (the delimiter is not part of a string; a final unterminated

@@ -38,6 +38,11 @@ class rxg_heap_info(C.Structure):
                 ("line_table_bytes", C.c_uint32), ("plain_table_bytes", C.c_uint32)]
 
 
+class rxg_one_opts(C.Structure):
+    _fields_ = [("checkpoint_every", C.c_uint32), ("d_checkpoints", C.c_void_p), ("d_stats", C.c_void_p),
+                ("d_trace", C.c_void_p), ("chunk", C.c_uint32), ("lookback", C.c_uint32), ("d_repairs", C.c_void_p)]
+
+
 # name -> (restype, argtypes). Every symbol declared in include/rxg.h.
 _P = C.c_void_p
 _SIG = {
@@ -63,6 +68,7 @@ _SIG = {
                                          C.POINTER(C.c_uint64), _P]),
     "rxg_host_emulate_lines_tma": (C.c_int, [_P, _P, C.c_uint64, C.c_int32, C.c_uint32, C.POINTER(C.c_uint64)]),
     "rxg_match_one": (C.c_int, [_P, _P, C.c_uint64, C.c_int, C.POINTER(C.c_int32)]),
+    "rxg_match_one_ex": (C.c_int, [_P, _P, C.c_uint64, C.c_int, _P, C.POINTER(rxg_one_opts), _P]),
     "rxg_match_one_device": (C.c_int, [_P, _P, C.c_uint64, C.c_int, _P, _P]),
     "rxg_match_batch": (C.c_int, [_P, _P, C.c_uint64, C.c_int32, C.c_uint32, _P, _P, _P]),
     "rxg_match_batch_host": (C.c_int, [_P, _P, C.c_uint64, C.c_int32, C.c_uint32, C.POINTER(C.c_uint64), _P]),

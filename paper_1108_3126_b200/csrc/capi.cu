@@ -18,6 +18,8 @@
 #include "lines_tma.hpp"
 #include "program.hpp"
 #include "single.hpp"
+#include "pernode.hpp"
+#include "chunked.hpp"
 #include "synth.hpp"
 #include "tables.hpp"
 
@@ -82,6 +84,11 @@ struct rxg_heap {
     int32_t* d_accept = nullptr;
     cudaStream_t stream = nullptr;
     cudaStream_t copy_stream = nullptr;
+    // lazily built tables of the thread-per-node engines
+    void* d_rounds = nullptr;
+    RoundsTables rounds;
+    void* d_pernode = nullptr;
+    PernodeTables pernode;
 
     ~rxg_heap() {
         if (device < 0) return;
@@ -98,6 +105,8 @@ struct rxg_heap {
         if (d_accept) cudaFree(d_accept);
         if (stream) cudaStreamDestroy(stream);
         if (copy_stream) cudaStreamDestroy(copy_stream);
+        if (d_rounds) cudaFree(d_rounds);
+        if (d_pernode) cudaFree(d_pernode);
     }
 };
 
@@ -132,12 +141,85 @@ int upload(rxg_heap* h, std::unique_ptr<TableSlot>& slot, KTable&& kt) {
     return RXG_OK;
 }
 
-int need_device(rxg_heap* h) {
+int need_device(rxg_heap* h, bool dfa = true) {
     if (!h) return fail(RXG_EINVAL, "null heap");
     if (h->device < 0) return fail(RXG_ENODEV, "host-only heap handle");
     if (!h->prog.byte_symbols)
         return fail(RXG_EUNSUPPORTED, "pattern has a literal >= 0x80; byte-level matching needs ASCII literals");
-    if (!h->dfa_ok) return fail(RXG_ETOOBIG, "memoized step table exceeds " + std::to_string(kMaxDfaStates) + " states");
+    if (dfa && !h->dfa_ok)
+        return fail(RXG_ETOOBIG, "memoized step table exceeds " + std::to_string(kMaxDfaStates) + " states");
+    return RXG_OK;
+}
+
+// Packs host arrays into one device allocation; returns device pointers in order.
+template <typename... Vs>
+int upload_pack(void** dbuf, std::vector<const void*>& dptrs, const Vs&... vs) {
+    std::vector<std::pair<const void*, size_t>> parts{{vs.data(), vs.size() * sizeof(vs[0])}...};
+    size_t total = 0;
+    for (auto& p : parts) total += (p.second + 255) & ~size_t(255);
+    RXG_CUDA(cudaMalloc(dbuf, std::max<size_t>(total, 256)));
+    size_t off = 0;
+    for (auto& p : parts) {
+        uint8_t* d = static_cast<uint8_t*>(*dbuf) + off;
+        if (p.second) RXG_CUDA(cudaMemcpy(d, p.first, p.second, cudaMemcpyHostToDevice));
+        dptrs.push_back(d);
+        off += (p.second + 255) & ~size_t(255);
+    }
+    return RXG_OK;
+}
+
+int rounds_tables(rxg_heap* h, const RoundsTables** out) {
+    std::lock_guard<std::mutex> lk(h->mu);
+    if (!h->d_rounds) {
+        const Heap& hp = h->prog.heap;
+        if (hp.size() > kRoundsMaxNodes) return fail(RXG_ETOOBIG, "heap too large for the one-CTA rounds engine");
+        std::vector<uint8_t> kind;
+        std::vector<uint32_t> sym;
+        std::vector<int32_t> left, right;
+        for (const HeapNode& n : hp.nodes) {
+            kind.push_back(n.kind);
+            sym.push_back(n.sym);
+            left.push_back(n.left);
+            right.push_back(n.right);
+        }
+        std::vector<const void*> p;
+        if (int rc = upload_pack(&h->d_rounds, p, kind, sym, left, right, hp.knodes)) return rc;
+        h->rounds.kind = static_cast<const uint8_t*>(p[0]);
+        h->rounds.sym = static_cast<const uint32_t*>(p[1]);
+        h->rounds.left = static_cast<const int32_t*>(p[2]);
+        h->rounds.right = static_cast<const int32_t*>(p[3]);
+        h->rounds.knode = static_cast<const int32_t*>(p[4]);
+        h->rounds.n = hp.size();
+    }
+    *out = &h->rounds;
+    return RXG_OK;
+}
+
+int pernode_tables(rxg_heap* h, const PernodeTables** out) {
+    std::lock_guard<std::mutex> lk(h->mu);
+    if (!h->d_pernode) {
+        const Program& pg = h->prog;
+        if (pg.W > 256) return fail(RXG_ETOOBIG, "more than 8191 positions for the one-warp K1 engine");
+        const BitsetPlan plan = build_bitset_plan(pg);
+        std::vector<uint8_t> cls(pg.byte_class, pg.byte_class + 256);
+        std::vector<const void*> p;
+        if (int rc = upload_pack(&h->d_pernode, p, cls, pg.class_mask, plan.shift, plan.has_group, plan.group,
+                                 plan.rows, pg.init))
+            return rc;
+        PernodeTables& t = h->pernode;
+        t.cls = static_cast<const uint8_t*>(p[0]);
+        t.cmask = static_cast<const uint32_t*>(p[1]);
+        t.shift = static_cast<const uint32_t*>(p[2]);
+        t.has_group = static_cast<const uint32_t*>(p[3]);
+        t.group = static_cast<const int32_t*>(p[4]);
+        t.rows = static_cast<const uint32_t*>(p[5]);
+        t.init = static_cast<const uint32_t*>(p[6]);
+        t.W = pg.W;
+        t.n_bits = pg.n_bits;
+        t.n_groups = plan.n_groups;
+        t.n_classes = pg.n_classes;
+    }
+    *out = &h->pernode;
     return RXG_OK;
 }
 
@@ -586,29 +668,69 @@ int rxg_host_emulate_lines_tma(const rxg_heap* h, const uint8_t* text, uint64_t 
     return RXG_OK;
 }
 
-int rxg_match_one_device(rxg_heap* h, const uint8_t* d_bytes, uint64_t len, int engine, int32_t* d_accept,
-                         void* stream) {
-    if (int rc = need_device(h)) return rc;
+int rxg_match_one_ex(rxg_heap* h, const uint8_t* d_bytes, uint64_t len, int engine, int32_t* d_accept,
+                     const rxg_one_opts* opts, void* stream) {
+    const bool dfa_engine = engine == RXG_ENGINE_AUTO || engine == RXG_ENGINE_DFA_SEQ || engine == RXG_ENGINE_CHUNKED;
+    if (int rc = need_device(h, dfa_engine)) return rc;
     if (!d_accept || (!d_bytes && len)) return fail(RXG_EINVAL, "bad arguments");
+    rxg_one_opts o{};
+    if (opts) o = *opts;
     DeviceGuard g(h->device);
     const cudaStream_t st = static_cast<cudaStream_t>(stream);
-    const DevTable* t = nullptr;
-    if (int rc = plain_table(h, &t)) return rc;
     switch (engine) {
-    case RXG_ENGINE_AUTO:
     case RXG_ENGINE_DFA_SEQ: {
+        const DevTable* t = nullptr;
+        if (int rc = plain_table(h, &t)) return rc;
         const cudaError_t e = launch_seq(*t, d_bytes, len, d_accept, st);
         if (e != cudaSuccess) return cuda_fail(e, "launch_seq");
         g_launches = 1;
         return RXG_OK;
     }
+    case RXG_ENGINE_AUTO:
+    case RXG_ENGINE_CHUNKED: {
+        const DevTable* t = nullptr;
+        if (int rc = plain_table(h, &t)) return rc;
+        uint32_t chunk = o.chunk ? o.chunk : chunked_auto_chunk(*t, len, h->device);
+        if (chunk % 64) return fail(RXG_EINVAL, "chunk must be a multiple of 64");
+        const uint32_t lookback = o.lookback ? o.lookback : 64;
+        void* scratch = nullptr;
+        RXG_CUDA(cudaMallocAsync(&scratch, chunked_scratch_bytes(len, chunk), st));
+        const cudaError_t e = launch_chunked(*t, d_bytes, len, chunk, lookback, scratch, d_accept, o.d_repairs,
+                                             h->device, st);
+        cudaFreeAsync(scratch, st);
+        if (e != cudaSuccess) return cuda_fail(e, "launch_chunked");
+        g_launches = 2;
+        return RXG_OK;
+    }
+    case RXG_ENGINE_PERNODE: {
+        const PernodeTables* t = nullptr;
+        if (int rc = pernode_tables(h, &t)) return rc;
+        if (o.checkpoint_every && !o.d_checkpoints) return fail(RXG_EINVAL, "checkpoint buffer missing");
+        const cudaError_t e = launch_pernode(*t, d_bytes, len, o.checkpoint_every, o.d_checkpoints, d_accept, st);
+        if (e != cudaSuccess) return cuda_fail(e, "launch_pernode");
+        g_launches = 1;
+        return RXG_OK;
+    }
+    case RXG_ENGINE_ROUNDS: {
+        const RoundsTables* t = nullptr;
+        if (int rc = rounds_tables(h, &t)) return rc;
+        const cudaError_t e = launch_rounds(*t, d_bytes, len, d_accept, o.d_stats, o.d_trace, st);
+        if (e != cudaSuccess) return cuda_fail(e, "launch_rounds");
+        g_launches = 1;
+        return RXG_OK;
+    }
     default:
-        return fail(RXG_EUNSUPPORTED, "engine not available");
+        return fail(RXG_EINVAL, "unknown engine");
     }
 }
 
+int rxg_match_one_device(rxg_heap* h, const uint8_t* d_bytes, uint64_t len, int engine, int32_t* d_accept,
+                         void* stream) {
+    return rxg_match_one_ex(h, d_bytes, len, engine, d_accept, nullptr, stream);
+}
+
 int rxg_match_one(rxg_heap* h, const uint8_t* bytes, uint64_t len, int engine, int32_t* accept) {
-    if (int rc = need_device(h)) return rc;
+    if (int rc = need_device(h, engine != RXG_ENGINE_PERNODE && engine != RXG_ENGINE_ROUNDS)) return rc;
     if (!accept || (!bytes && len)) return fail(RXG_EINVAL, "bad arguments");
     DeviceGuard g(h->device);
     if (int rc = ensure_stage(h, std::max<size_t>(len, 16))) return rc;

@@ -1,0 +1,18 @@
+// Launch interface of the chunk-parallel single-string walk (kernels_chunked.cu).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "launch.hpp"
+
+namespace rxg {
+
+size_t chunked_scratch_bytes(uint64_t len, uint32_t chunk);
+uint32_t chunked_auto_chunk(const DevTable& t, uint64_t len, int device);
+
+// scratch: chunked_scratch_bytes(len, chunk) device bytes. repairs: device u64 (nullable).
+cudaError_t launch_chunked(const DevTable& t, const uint8_t* text, uint64_t len, uint32_t chunk, uint32_t lookback,
+                           void* scratch, int32_t* accept, unsigned long long* repairs, int device, cudaStream_t st);
+
+}  // namespace rxg

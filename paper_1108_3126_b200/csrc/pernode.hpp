@@ -1,0 +1,42 @@
+// Launch interface of the thread-per-node engines (kernels_pernode.cu).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace rxg {
+
+// Heap table in SoA form for the literal §8 protocol (device pointers).
+struct RoundsTables {
+    const uint8_t* kind = nullptr;
+    const uint32_t* sym = nullptr;
+    const int32_t* left = nullptr;
+    const int32_t* right = nullptr;
+    const int32_t* knode = nullptr;
+    int32_t n = 0;
+};
+
+// Position-form bitset tables for K1 (device pointers).
+struct PernodeTables {
+    const uint8_t* cls = nullptr;
+    const uint32_t* cmask = nullptr;
+    const uint32_t* shift = nullptr;
+    const uint32_t* has_group = nullptr;
+    const int32_t* group = nullptr;
+    const uint32_t* rows = nullptr;
+    const uint32_t* init = nullptr;
+    int32_t W = 0, n_bits = 0, n_groups = 0, n_classes = 0;
+};
+
+constexpr int32_t kRoundsMaxNodes = 32 * 1024;   // one CTA of 1024 threads, <= 32 nodes each
+
+// stats (device, 4 x u64, nullable): claims, rounds, macro steps, max claims per node per step.
+// trace (device, zeroed, nullable): per symbol the next schedule as (N+1)-bit rows, bit N = null.
+cudaError_t launch_rounds(const RoundsTables& t, const uint8_t* text, uint64_t len, int32_t* accept,
+                          unsigned long long* stats, uint32_t* trace, cudaStream_t st);
+
+// every > 0: E after every `every` symbols into checkpoints ((len/every) x W words).
+cudaError_t launch_pernode(const PernodeTables& t, const uint8_t* text, uint64_t len, uint32_t every,
+                           uint32_t* checkpoints, int32_t* accept, cudaStream_t st);
+
+}  // namespace rxg

@@ -276,6 +276,16 @@ class Matcher:
         _check(L.lib().rxg_match_one(self._h, p, n, L.ENGINES[engine], C.byref(acc)))
         return bool(acc.value)
 
+    def match_one_ex(self, d_text, d_accept, engine: str = "auto", stream=None, nbytes: int | None = None, **opts):
+        """Async single-string match with engine options / instrumentation (device tensors):
+        checkpoint_every + d_checkpoints (pernode), d_stats / d_trace (rounds), chunk / lookback / d_repairs (chunked)."""
+        o = L.rxg_one_opts()
+        for k, v in opts.items():
+            setattr(o, k, v.data_ptr() if hasattr(v, "data_ptr") else v)
+        n = d_text.numel() if nbytes is None else nbytes
+        _check(L.lib().rxg_match_one_ex(self._h, d_text.data_ptr(), n, L.ENGINES[engine], d_accept.data_ptr(),
+                                        C.byref(o), _stream_ptr(stream)))
+
     def match_one_device(self, d_text, d_accept, engine: str = "auto", stream=None):
         """Async single-string match on device tensors (d_accept: int32 cuda tensor)."""
         _check(L.lib().rxg_match_one_device(self._h, d_text.data_ptr(), d_text.numel(), L.ENGINES[engine],

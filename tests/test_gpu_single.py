@@ -1,40 +1,138 @@
-"""GPU parity of the single-string engines against the oracle / reference."""
+"""GPU parity of the single-string engines (K1 thread-per-node, the literal
+§8 rounds protocol, the chunk-parallel walk, the sequential table walk)
+against the oracle and the reference library."""
 import numpy as np
 import pytest
+import torch
 
 from oracle_bind import Oracle, Ref, RefHeap
 from paper_1108_3126_b200 import rx
 
 pytestmark = pytest.mark.gpu
 
-ENGINES = ["dfa_seq", "auto"]
+ENGINES = ["dfa_seq", "chunked", "pernode", "rounds", "auto"]
+
+
+def O(p):
+    return Oracle(rx.compile(rx.parse(p)))
 
 
 @pytest.mark.parametrize("engine", ENGINES)
 def test_worked_examples(engine):
-    # test_lockstep.cpp:52-58
+    # test_lockstep.cpp:52-58, test_parallel.cpp:84-93
     assert rx.Matcher("a**b").lockstep_accepts(b"aab", engine)
     assert not rx.Matcher("a**b").lockstep_accepts(b"aa", engine)
     assert rx.Matcher("a**").lockstep_accepts(b"", engine)
     assert rx.Matcher("()").lockstep_accepts(b"", engine)
     assert not rx.Matcher("a").lockstep_accepts(b"", engine)
+    assert not rx.Matcher("a").lockstep_accepts(b"b", engine)
+    assert rx.Matcher("(a*)*b").lockstep_accepts(b"a" * 1000 + b"b", engine)
 
 
 @pytest.mark.parametrize("engine", ENGINES)
 def test_config_a_full(engine):
-    pattern = rx.synth_pattern("a")
-    m = rx.Matcher(pattern)
+    m = rx.Matcher(rx.synth_pattern("a"))
     assert m.lockstep_accepts(rx.synth_input("a").tobytes(), engine) is True
     assert m.lockstep_accepts(rx.synth_input("A").tobytes(), engine) is False
 
 
 @pytest.mark.parametrize("engine", ENGINES)
-def test_random_small(engine):
+def test_random_small_against_oracle(engine):
     rng = np.random.default_rng(5)
-    pats = Ref.random_regexes(40, 12, seed=9) if Ref.available() else ["(a|b)*abb", "a**b"]
+    pats = Ref.random_regexes(40, 14, seed=9) if Ref.available() else ["(a|b)*abb", "a**b", "(ab|a)*b"]
     for p in pats:
         m = rx.Matcher(p)
-        o = Oracle(rx.compile(rx.parse(p)))
-        for _ in range(10):
-            w = bytes(rng.choice([97, 98], size=int(rng.integers(0, 40))).astype(np.uint8))
+        o = O(p)
+        for _ in range(6):
+            w = bytes(rng.choice([97, 98], size=int(rng.integers(0, 300))).astype(np.uint8))
             assert m.lockstep_accepts(w, engine) == o.accepts(w), (p, w)
+
+
+def test_chunked_long_strings_with_small_ranges():
+    """Many ranges and repairs: parity on non-synchronizing automata too."""
+    rng = np.random.default_rng(2)
+    for p in ["(a|b)*abb", "(aa)*", "((a|b)(a|b))*", "(ab|ba)*a", "a*b*a*b*"]:
+        m = rx.Matcher(p)
+        o = O(p)
+        for n in (0, 1, 63, 64, 65, 5000, 100_000):
+            w = rng.choice([97, 98], size=n).astype(np.uint8)
+            if p == "(aa)*":
+                w[:] = 97
+            d = torch.from_numpy(w).cuda() if n else torch.zeros(1, dtype=torch.uint8, device="cuda")
+            acc = torch.zeros(1, dtype=torch.int32, device="cuda")
+            rep = torch.zeros(1, dtype=torch.int64, device="cuda")
+            m.match_one_ex(d, acc, "chunked", nbytes=n, chunk=256, lookback=16, d_repairs=rep)
+            torch.cuda.synchronize()
+            assert bool(acc.item()) == o.accepts(w.tobytes()), (p, n)
+
+
+def test_rounds_instrumentation_like_parallel_cpp():
+    """claims once per node per macro step, launches <= steps * N (test_parallel.cpp:95-112)."""
+    rng = np.random.default_rng(23)
+    pats = Ref.random_regexes(30, 8, seed=23) if Ref.available() else ["a**b", "(a|b)*a"]
+    for p in pats:
+        m = rx.Matcher(p)
+        h = rx.compile(rx.parse(p))
+        w = rng.choice([97, 98], size=int(rng.integers(0, 6))).astype(np.uint8)
+        d = torch.from_numpy(w).cuda() if len(w) else torch.zeros(1, dtype=torch.uint8, device="cuda")
+        acc = torch.zeros(1, dtype=torch.int32, device="cuda")
+        stats = torch.zeros(4, dtype=torch.int64, device="cuda")
+        m.match_one_ex(d, acc, "rounds", nbytes=len(w), d_stats=stats)
+        claims, rounds, steps, maxc = stats.tolist()
+        assert bool(acc.item()) == O(p).accepts(w.tobytes())
+        assert maxc <= 1
+        assert rounds <= steps * h.size()
+        if Ref.available():
+            ok, rs = RefHeap(p.encode()).par_accepts(w.tobytes(), workers=1, seed=1)
+            assert ok == bool(acc.item())
+            assert claims == rs["claims"]   # each node claimed once per step it is scheduled in
+
+
+def test_rounds_macro_boundaries_equal_lockstep_sets():
+    """test_parallel.cpp:114-137: the next schedule (null included) equals step_char(evolve(S), a)."""
+    rng = np.random.default_rng(31)
+    pats = Ref.random_regexes(30, 8, seed=31) if Ref.available() else ["a**b", "(a|b)*a"]
+    for p in pats:
+        h = rx.compile(rx.parse(p))
+        o = O(p)
+        m = rx.Matcher(p)
+        w = rng.choice([97, 98], size=int(rng.integers(1, 5))).astype(np.uint8)
+        words = (h.size() + 1 + 31) // 32
+        trace = torch.zeros(len(w) * words, dtype=torch.int32, device="cuda")
+        acc = torch.zeros(1, dtype=torch.int32, device="cuda")
+        m.match_one_ex(torch.from_numpy(w).cuda(), acc, "rounds", d_trace=trace)
+        rows = trace.cpu().numpy().view(np.uint32).reshape(len(w), words)
+        s = {0}
+        for i, a in enumerate(w):
+            s = o.step_char(o.evolve(s), int(a))
+            got = {q for q in range(h.size()) if (rows[i][q >> 5] >> (q & 31)) & 1}
+            if (rows[i][h.size() >> 5] >> (h.size() & 31)) & 1:
+                got.add(-1)
+            assert got == s, (p, w, i)
+            if not s:
+                break
+
+
+def test_pernode_checkpoints_equal_host_sets():
+    p = rx.synth_pattern("e")
+    m = rx.Matcher(p)
+    w = rx.synth_input("e", 4096)
+    W = m.info()["words"]
+    every = 256
+    ck = torch.zeros((4096 // every) * W, dtype=torch.int32, device="cuda")
+    acc = torch.zeros(1, dtype=torch.int32, device="cuda")
+    m.match_one_ex(torch.from_numpy(w).cuda(), acc, "pernode", checkpoint_every=every, d_checkpoints=ck)
+    got = ck.cpu().numpy().view(np.uint32).reshape(-1, W)
+    sets, hacc = rx.Matcher(p, device=-1).host_walk(w.tobytes())
+    for k in range(len(got)):
+        assert np.array_equal(got[k], sets[(k + 1) * every]), k
+    assert bool(acc.item()) == hacc
+
+
+@pytest.mark.parametrize("engine", ["chunked", "pernode", "dfa_seq"])
+def test_config_e_prefix(engine):
+    p = rx.synth_pattern("e")
+    m = rx.Matcher(p)
+    for n in (1 << 16, 1 << 20):
+        w = rx.synth_input("e", n)
+        assert m.lockstep_accepts(w.tobytes(), engine) == O(p).accepts(w.tobytes())
