@@ -204,7 +204,7 @@ int pernode_tables(rxg_heap* h, const PernodeTables** out) {
         std::vector<uint8_t> cls(pg.byte_class, pg.byte_class + 256);
         std::vector<const void*> p;
         if (int rc = upload_pack(&h->d_pernode, p, cls, pg.class_mask, plan.shift, plan.has_group, plan.group,
-                                 plan.rows, pg.init))
+                                 plan.rows, pg.init, plan.trigger))
             return rc;
         PernodeTables& t = h->pernode;
         t.cls = static_cast<const uint8_t*>(p[0]);
@@ -214,6 +214,7 @@ int pernode_tables(rxg_heap* h, const PernodeTables** out) {
         t.group = static_cast<const int32_t*>(p[4]);
         t.rows = static_cast<const uint32_t*>(p[5]);
         t.init = static_cast<const uint32_t*>(p[6]);
+        t.trig = static_cast<const uint32_t*>(p[7]);
         t.W = pg.W;
         t.n_bits = pg.n_bits;
         t.n_groups = plan.n_groups;

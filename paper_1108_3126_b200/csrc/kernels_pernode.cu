@@ -179,7 +179,8 @@ __global__ void __launch_bounds__(1024) k_rounds(const __grid_constant__ RoundsA
 
 // ── k_pernode (K1) ───────────────────────────────────────────────────────
 
-constexpr int kMaxSlots = 8;   // words per lane: W <= 256 (8191 positions)
+constexpr int kMaxSlots = 8;        // words per lane: W <= 256 (8191 positions)
+constexpr int kDenseGroups = 32;    // up to this many residual rows: vote per row, rows in smem
 
 struct PernodeArgs {
     const uint8_t* text;
@@ -190,61 +191,77 @@ struct PernodeArgs {
     const uint32_t* has_group; // W
     const int32_t* group;      // n_bits
     const uint32_t* rows;      // n_groups x W
+    const uint32_t* trig;      // n_groups x W : positions whose residual is row g
     const uint32_t* init;      // W
     int32_t W, n_bits, n_groups, n_classes;
+    int32_t byte_masks;        // 1: smem holds M per raw byte (256 x W), else per class
     uint32_t every;            // checkpoint period (0 = none)
     uint32_t* checkpoints;     // (len / every) x W words: E after every `every` symbols
     int32_t* accept;
 };
 
-template <int SLOTS>
-__global__ void __launch_bounds__(32) k_pernode(const __grid_constant__ PernodeArgs a) {
-    extern __shared__ __align__(16) uint32_t smp[];
+// One lockstep step of the warp-wide bitset. DENSE: <= 32 residual rows,
+// each tested by a warp vote; otherwise hit rows are marked in a shared
+// bitmap (claimed once per step) and OR-ed afterwards.
+template <int SLOTS, bool DENSE, int GREG>
+__device__ __forceinline__ void pernode_step(const PernodeArgs& a, const uint32_t (&Mw)[SLOTS], const uint32_t* TR,
+                                             const uint32_t* RR, uint32_t* hit, int hw, int lane,
+                                             uint32_t (&E)[SLOTS], const uint32_t (&SH)[SLOTS],
+                                             const uint32_t (&HG)[SLOTS], const uint32_t (&TRr)[GREG ? GREG : 1][SLOTS],
+                                             const uint32_t (&RRr)[GREG ? GREG : 1][SLOTS]) {
     const int W = a.W;
-    uint32_t* cm = smp;                                   // class masks
-    uint32_t* hit = cm + a.n_classes * W;                 // hit-group bitmap
-    const int hw = (a.n_groups + 31) / 32;
-    uint8_t* cls = reinterpret_cast<uint8_t*>(hit + hw);
-    const int lane = threadIdx.x;
-    for (int i = lane; i < a.n_classes * W; i += 32) cm[i] = a.cmask[i];
-    for (int i = lane; i < 256; i += 32) cls[i] = a.cls[i];
-    for (int i = lane; i < hw; i += 32) hit[i] = 0;
-    uint32_t E[SLOTS], SH[SLOTS], HG[SLOTS];
+    uint32_t fire[SLOTS], nx[SLOTS];
+    bool any_group = false;
 #pragma unroll
     for (int k = 0; k < SLOTS; ++k) {
-        const int w = lane + 32 * k;
-        E[k] = w < W ? a.init[w] : 0u;
-        SH[k] = w < W ? a.shift[w] : 0u;
-        HG[k] = w < W ? a.has_group[w] : 0u;
+        fire[k] = E[k] & Mw[k];
+        any_group |= (fire[k] & HG[k]) != 0u;
     }
-    __syncwarp();
-    uint64_t pos = 0;
-    for (; pos < a.len; ++pos) {
-        const uint32_t c = cls[a.text[pos]];
-        const uint32_t* M = cm + c * W;
-        uint32_t fire[SLOTS], nx[SLOTS];
-        bool any_group = false;
 #pragma unroll
-        for (int k = 0; k < SLOTS; ++k) {
-            const int w = lane + 32 * k;
-            fire[k] = w < W ? (E[k] & M[w]) : 0u;
-            // one-bit successor of consecutive literals; carry from word w-1
-            const uint32_t sh = fire[k] & SH[k];
-            uint32_t carry = __shfl_up_sync(0xFFFFFFFFu, sh >> 31, 1);
-            const uint32_t wrap = __shfl_sync(0xFFFFFFFFu, k > 0 ? (fire[k - 1] & SH[k - 1]) >> 31 : 0u, 31);
-            if (lane == 0) carry = wrap;
-            nx[k] = (sh << 1) | carry;
-            any_group |= (fire[k] & HG[k]) != 0u;
+    for (int k = 0; k < SLOTS; ++k) {
+        // one-bit successor of consecutive literals; carry from word w-1
+        const uint32_t sh = fire[k] & SH[k];
+        uint32_t carry = __shfl_up_sync(0xFFFFFFFFu, sh >> 31, 1);
+        const uint32_t wrap = __shfl_sync(0xFFFFFFFFu, k > 0 ? (fire[k - 1] & SH[k - 1]) >> 31 : 0u, 31);
+        if (lane == 0) carry = wrap;
+        nx[k] = (sh << 1) | carry;
+    }
+    if constexpr (GREG > 0) {
+        // few residual rows: triggers and rows live in registers, one vote each
+#pragma unroll
+        for (int g = 0; g < GREG; ++g) {
+            bool t = false;
+#pragma unroll
+            for (int k = 0; k < SLOTS; ++k) t |= (fire[k] & TRr[g][k]) != 0u;
+            const bool h = __any_sync(0xFFFFFFFFu, t);
+#pragma unroll
+            for (int k = 0; k < SLOTS; ++k) nx[k] |= h ? RRr[g][k] : 0u;
         }
-        // residual rows: mark each hit group once, then OR its row (dedup by row identity)
-        if (__any_sync(0xFFFFFFFFu, any_group)) {
+    } else if (__any_sync(0xFFFFFFFFu, any_group)) {
+        if constexpr (DENSE) {
+            for (int g = 0; g < a.n_groups; ++g) {
+                bool t = false;
+#pragma unroll
+                for (int k = 0; k < SLOTS; ++k) {
+                    const int w = lane + 32 * k;
+                    if (w < W) t |= (fire[k] & TR[g * W + w]) != 0u;
+                }
+                if (__any_sync(0xFFFFFFFFu, t)) {
+#pragma unroll
+                    for (int k = 0; k < SLOTS; ++k) {
+                        const int w = lane + 32 * k;
+                        if (w < W) nx[k] |= RR[g * W + w];
+                    }
+                }
+            }
+        } else {
 #pragma unroll
             for (int k = 0; k < SLOTS; ++k) {
                 uint32_t f = fire[k] & HG[k];
                 while (f) {
                     const int b = __ffs(f) - 1;
                     f &= f - 1;
-                    const int g = a.group[(lane + 32 * k) * 32 + b];
+                    const int g = __ldg(a.group + (lane + 32 * k) * 32 + b);
                     atomicOr(&hit[g >> 5], 1u << (g & 31));
                 }
             }
@@ -266,24 +283,95 @@ __global__ void __launch_bounds__(32) k_pernode(const __grid_constant__ PernodeA
             for (int i = lane; i < hw; i += 32) hit[i] = 0;
             __syncwarp();
         }
+    }
 #pragma unroll
-        for (int k = 0; k < SLOTS; ++k) E[k] = nx[k];
-        if (a.every && (pos + 1) % a.every == 0) {
-            uint32_t* out = a.checkpoints + ((pos + 1) / a.every - 1) * W;
+    for (int k = 0; k < SLOTS; ++k) E[k] = nx[k];
+}
+
+template <int SLOTS, bool DENSE, int GREG>
+__global__ void __launch_bounds__(32) k_pernode(const __grid_constant__ PernodeArgs a) {
+    extern __shared__ __align__(16) uint32_t smp[];
+    const int W = a.W;
+    const int lane = threadIdx.x;
+    // shared layout: masks (256 x W by byte, or n_classes x W by class), then
+    // the dense rows + triggers, or the sparse hit bitmap; then the class map
+    uint32_t* masks = smp;
+    const int mrows = a.byte_masks ? 256 : a.n_classes;
+    uint32_t* TR = masks + mrows * W;
+    uint32_t* RR = TR + (DENSE ? a.n_groups * W : 0);
+    uint32_t* hit = RR + (DENSE ? a.n_groups * W : 0);
+    const int hw = DENSE ? 0 : (a.n_groups + 31) / 32;
+    uint8_t* cls = reinterpret_cast<uint8_t*>(hit + hw);
+    for (int i = lane; i < 256; i += 32) cls[i] = a.cls[i];
+    __syncwarp();
+    for (int i = lane; i < mrows * W; i += 32)
+        masks[i] = a.byte_masks ? a.cmask[cls[i / W] * W + i % W] : a.cmask[i];
+    if (DENSE)
+        for (int i = lane; i < a.n_groups * W; i += 32) {
+            TR[i] = a.trig[i];
+            RR[i] = a.rows[i];
+        }
+    for (int i = lane; i < hw; i += 32) hit[i] = 0;
+    uint32_t E[SLOTS], SH[SLOTS], HG[SLOTS];
+    uint32_t TRr[GREG ? GREG : 1][SLOTS], RRr[GREG ? GREG : 1][SLOTS];
+#pragma unroll
+    for (int k = 0; k < SLOTS; ++k) {
+        const int w = lane + 32 * k;
+        E[k] = w < W ? a.init[w] : 0u;
+        SH[k] = w < W ? a.shift[w] : 0u;
+        HG[k] = w < W ? a.has_group[w] : 0u;
+#pragma unroll
+        for (int g = 0; g < (GREG ? GREG : 1); ++g) {
+            TRr[g][k] = (GREG && g < a.n_groups && w < W) ? a.trig[g * W + w] : 0u;
+            RRr[g][k] = (GREG && g < a.n_groups && w < W) ? a.rows[g * W + w] : 0u;
+        }
+    }
+    __syncwarp();
+    uint64_t pos = 0;
+    bool live = true;
+    // 16 input bytes per uniform load (every lane reads the same vector)
+    const uint64_t head = (16 - (reinterpret_cast<uintptr_t>(a.text) & 15)) & 15;
+    auto rowp = [&](uint32_t b) { return a.byte_masks ? masks + b * W : masks + cls[b] * W; };
+    auto one = [&](const uint32_t (&Mw)[SLOTS]) {
+        pernode_step<SLOTS, DENSE, GREG>(a, Mw, TR, RR, hit, hw, lane, E, SH, HG, TRr, RRr);
+        ++pos;
+        if (a.every && pos % a.every == 0) {
+            uint32_t* out = a.checkpoints + (pos / a.every - 1) * W;
 #pragma unroll
             for (int k = 0; k < SLOTS; ++k)
                 if (lane + 32 * k < W) out[lane + 32 * k] = E[k];
         }
-        if ((pos & 63) == 63) {   // the empty set is absorbing: stop early
-            bool live = false;
+    };
+    auto single = [&](uint32_t b) {
+        const uint32_t* M = rowp(b);
+        uint32_t Mw[SLOTS];
 #pragma unroll
-            for (int k = 0; k < SLOTS; ++k) live |= E[k] != 0u;
-            if (!__any_sync(0xFFFFFFFFu, live)) {
-                ++pos;
-                break;
-            }
+        for (int k = 0; k < SLOTS; ++k) Mw[k] = lane + 32 * k < W ? M[lane + 32 * k] : 0u;
+        one(Mw);
+    };
+    for (uint64_t i = 0; i < head && pos < a.len; ++i) single(a.text[pos]);
+    while (live && pos + 16 <= a.len) {
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(a.text + pos));
+        const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
+        // the 16 mask rows depend only on the input: load them all before the
+        // dependent chain of 16 steps starts
+        uint32_t Mw[16][SLOTS];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            const uint32_t* M = rowp((wv[i >> 2] >> (8 * (i & 3))) & 0xFFu);
+#pragma unroll
+            for (int k = 0; k < SLOTS; ++k) Mw[i][k] = lane + 32 * k < W ? M[lane + 32 * k] : 0u;
+        }
+#pragma unroll
+        for (int i = 0; i < 16; ++i) one(Mw[i]);
+        if ((pos & 63) == 0) {   // the empty set is absorbing: stop early
+            bool any = false;
+#pragma unroll
+            for (int k = 0; k < SLOTS; ++k) any |= E[k] != 0u;
+            live = __any_sync(0xFFFFFFFFu, any);
         }
     }
+    while (live && pos < a.len) single(a.text[pos]);
     const int A = a.n_bits - 1;   // accept bit
     uint32_t acc = 0;
 #pragma unroll
@@ -293,12 +381,20 @@ __global__ void __launch_bounds__(32) k_pernode(const __grid_constant__ PernodeA
     if (lane == 0) *a.accept = static_cast<int32_t>(acc);
 }
 
-template <int SLOTS>
+template <int SLOTS, bool DENSE, int GREG>
 cudaError_t run_pernode(const PernodeArgs& a, uint32_t smem, cudaStream_t st) {
-    cudaError_t e = cudaFuncSetAttribute(k_pernode<SLOTS>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaError_t e = cudaFuncSetAttribute(k_pernode<SLOTS, DENSE, GREG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
     if (e != cudaSuccess) return e;
-    k_pernode<SLOTS><<<1, 32, smem, st>>>(a);
+    k_pernode<SLOTS, DENSE, GREG><<<1, 32, smem, st>>>(a);
     return cudaGetLastError();
+}
+
+template <int SLOTS>
+cudaError_t run_pernode2(const PernodeArgs& a, uint32_t smem, bool dense, cudaStream_t st) {
+    if (a.n_groups <= 1) return run_pernode<SLOTS, true, 1>(a, smem, st);
+    if (a.n_groups <= 2) return run_pernode<SLOTS, true, 2>(a, smem, st);
+    return dense ? run_pernode<SLOTS, true, 0>(a, smem, st) : run_pernode<SLOTS, false, 0>(a, smem, st);
 }
 
 }  // namespace
@@ -336,6 +432,7 @@ cudaError_t launch_pernode(const PernodeTables& t, const uint8_t* text, uint64_t
     a.has_group = t.has_group;
     a.group = t.group;
     a.rows = t.rows;
+    a.trig = t.trig;
     a.init = t.init;
     a.W = t.W;
     a.n_bits = t.n_bits;
@@ -344,12 +441,18 @@ cudaError_t launch_pernode(const PernodeTables& t, const uint8_t* text, uint64_t
     a.every = every;
     a.checkpoints = checkpoints;
     a.accept = accept;
-    const uint32_t smem = static_cast<uint32_t>(t.n_classes * t.W + (t.n_groups + 31) / 32) * 4u + 256u;
+    const bool dense = t.n_groups <= kDenseGroups;
+    a.byte_masks = 256u * static_cast<uint32_t>(t.W) * 4u <= 128u * 1024u;
+    const uint32_t mrows = a.byte_masks ? 256u : static_cast<uint32_t>(t.n_classes);
+    const uint32_t group_words = dense ? 2u * static_cast<uint32_t>(t.n_groups * t.W)
+                                       : static_cast<uint32_t>((t.n_groups + 31) / 32);
+    const uint32_t smem = (mrows * static_cast<uint32_t>(t.W) + group_words) * 4u + 256u;
     const int slots = (t.W + 31) / 32;
-    if (slots <= 1) return run_pernode<1>(a, smem, st);
-    if (slots <= 2) return run_pernode<2>(a, smem, st);
-    if (slots <= 4) return run_pernode<4>(a, smem, st);
-    if (slots <= kMaxSlots) return run_pernode<kMaxSlots>(a, smem, st);
+    if (slots <= 1) return run_pernode2<1>(a, smem, dense, st);
+    if (slots <= 2) return run_pernode2<2>(a, smem, dense, st);
+    if (slots <= 3) return run_pernode2<3>(a, smem, dense, st);
+    if (slots <= 4) return run_pernode2<4>(a, smem, dense, st);
+    if (slots <= kMaxSlots) return run_pernode2<kMaxSlots>(a, smem, dense, st);
     return cudaErrorInvalidValue;
 }
 

@@ -24,6 +24,7 @@ struct PernodeTables {
     const uint32_t* has_group = nullptr;
     const int32_t* group = nullptr;
     const uint32_t* rows = nullptr;
+    const uint32_t* trig = nullptr;
     const uint32_t* init = nullptr;
     int32_t W = 0, n_bits = 0, n_groups = 0, n_classes = 0;
 };
