@@ -298,6 +298,13 @@ int make_heap(Heap&& hp, int device, rxg_heap** out) {
         RXG_CUDA(cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking));
         RXG_CUDA(cudaMalloc(&h->d_count, sizeof(unsigned long long)));
         RXG_CUDA(cudaMalloc(&h->d_accept, sizeof(int32_t)));
+        // keep stream-ordered scratch (results / chunked engines) cached in the
+        // device's default pool instead of returning it to the driver at every sync
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+            uint64_t keep = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
     }
     *out = h.release();
     return RXG_OK;

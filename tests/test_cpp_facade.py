@@ -1,0 +1,30 @@
+"""The header-only C++ facade (include/rx_b200.hpp) keeps the reference's
+rx:: call sites compiling and behaving the same; built with g++ against the
+in-tree librxg.so."""
+import subprocess
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parent.parent
+SRC = ROOT / "tests" / "cpp" / "facade_test.cpp"
+
+
+@pytest.fixture(scope="module")
+def binary(tmp_path_factory):
+    out = tmp_path_factory.mktemp("facade") / "facade_test"
+    lib = ROOT / "paper_1108_3126_b200"
+    subprocess.run(["g++", "-std=c++17", "-O1", f"-I{ROOT / 'include'}", str(SRC), f"-L{lib}", "-lrxg",
+                    f"-Wl,-rpath,{lib}", "-o", str(out)], check=True)
+    return out
+
+
+def test_facade_front_end(binary):
+    r = subprocess.run([str(binary), "cpu"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr + r.stdout
+
+
+@pytest.mark.gpu
+def test_facade_matching_on_gpu(binary):
+    r = subprocess.run([str(binary), "gpu"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr + r.stdout
