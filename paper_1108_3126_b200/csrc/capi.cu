@@ -239,7 +239,7 @@ int build_lt(rxg_heap* h, int delim, LtTable& out) {
     auto f = h->line_freq.find(delim);
     LtTable lt = make_lines_tma_table(h->prog, h->dfa, static_cast<uint8_t>(delim),
                                       f == h->line_freq.end() ? nullptr : &f->second);
-    if (lt.ok && static_cast<int>(lt.smem_table_end - kLtSmemBase) + 96 * 1024 <= h->smem_limit) {
+    if (lt.ok && static_cast<int>(lt.smem_table_end - kLtSmemBase) + 64 * 1024 <= h->smem_limit) {
         RXG_CUDA(cudaMalloc(&lt.d_lo, lt.lo.size()));
         RXG_CUDA(cudaMalloc(&lt.d_hi, lt.hi.size()));
         RXG_CUDA(cudaMemcpy(lt.d_lo, lt.lo.data(), lt.lo.size(), cudaMemcpyHostToDevice));
@@ -659,7 +659,7 @@ int rxg_host_emulate_lines_tma(const rxg_heap* h, const uint8_t* text, uint64_t 
         uint32_t s = (c0 == 0 || text[c0 - 1] == d) ? t.start : t.skip;
         for (uint64_t i = c0; i < c1; ++i) {
             s = lt_step(t, s, text[i]);
-            cnt += s >> 15;
+            cnt += lt_count(t, s);
         }
         if (s != t.skip && text[c1 - 1] != d) {
             s += t.tail_delta;

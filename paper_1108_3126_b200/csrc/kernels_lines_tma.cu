@@ -54,6 +54,7 @@ struct Args {
     uint32_t stage_addr[kMaxSlots];
     uint32_t start, skip, void_row, tail_delta, term_acc;
     uint32_t delim;
+    uint32_t row_bytes, cmap_addr, acc_shift;   // class layout
     unsigned long long* count;
 };
 
@@ -77,8 +78,30 @@ __device__ __forceinline__ uint4 lds128(uint32_t addr) {
     return v;
 }
 
-__device__ __forceinline__ uint32_t step(uint32_t s, uint32_t word, int k) {
-    return tab(s + __byte_perm(word, 0, 0x4440 + k) * kLtColBytes);
+__device__ __forceinline__ uint32_t lds32(uint32_t addr) {
+    uint32_t v;
+    asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+
+// One memoized step on byte b. Direct layout: s is an absolute row address.
+// Class layout: s is a row index, the class map gives the column address.
+template <bool CLS>
+__device__ __forceinline__ uint32_t step_b(const Args& a, uint32_t s, uint32_t b) {
+    if constexpr (CLS) return tab(s * a.row_bytes + lds32(a.cmap_addr + b * 4u));
+    else return tab(s + b * kLtColBytes);
+}
+
+template <bool CLS>
+__device__ __forceinline__ uint32_t step(const Args& a, uint32_t s, uint32_t word, int k) {
+    return step_b<CLS>(a, s, __byte_perm(word, 0, 0x4440 + k));
+}
+
+// 1 iff s is START_A (the accepted-line-end row).
+template <bool CLS>
+__device__ __forceinline__ uint32_t counted(const Args& a, uint32_t s) {
+    if constexpr (CLS) return s >> a.acc_shift;
+    else return __umulhi(s, 1u << 17);
 }
 
 __device__ __forceinline__ uint32_t word_of(const uint4& v, int w) {
@@ -120,6 +143,7 @@ __device__ __forceinline__ uint32_t granule(uint32_t r, uint32_t g) {
 }
 
 // Finish the line straddling a range end with direct loads (tail copy rows).
+template <bool CLS>
 __device__ uint32_t finish_line(const Args& a, uint32_t s, uint64_t pos) {
     while (pos < a.len) {
         if (pos + 16 <= a.len) {
@@ -127,17 +151,18 @@ __device__ uint32_t finish_line(const Args& a, uint32_t s, uint64_t pos) {
 #pragma unroll
             for (int w = 0; w < 4; ++w)
 #pragma unroll
-                for (int k = 0; k < 4; ++k) s = step(s, word_of(v, w), k);
+                for (int k = 0; k < 4; ++k) s = step<CLS>(a, s, word_of(v, w), k);
             pos += 16;
         } else {
-            for (; pos < a.len; ++pos) s = tab(s + static_cast<uint32_t>(a.text[pos]) * kLtColBytes);
+            for (; pos < a.len; ++pos) s = step_b<CLS>(a, s, a.text[pos]);
         }
         if (s >= a.term_acc) return s;
     }
-    return tab(s + a.delim * kLtColBytes);
+    return step_b<CLS>(a, s, a.delim);
 }
 
 // A range processed entirely with direct loads (the remainder pieces).
+template <bool CLS>
 __device__ void range_direct(const Args& a, uint64_t c0, uint64_t c1, uint32_t& cnt) {
     uint32_t s = (c0 == 0 || a.text[c0 - 1] == a.delim) ? a.start : a.skip;
     uint32_t last = 0;
@@ -148,20 +173,20 @@ __device__ void range_direct(const Args& a, uint64_t c0, uint64_t c1, uint32_t& 
         for (int w = 0; w < 4; ++w)
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-                s = step(s, word_of(v, w), k);
-                cnt += __umulhi(s, 1u << 17);
+                s = step<CLS>(a, s, word_of(v, w), k);
+                cnt += counted<CLS>(a, s);
             }
         last = v.w >> 24;
     }
     for (; pos < c1; ++pos) {
         last = a.text[pos];
-        s = tab(s + last * kLtColBytes);
-        cnt += __umulhi(s, 1u << 17);
+        s = step_b<CLS>(a, s, last);
+        cnt += counted<CLS>(a, s);
     }
-    if (s != a.skip && last != a.delim) cnt += finish_line(a, s + a.tail_delta, c1) == a.term_acc;
+    if (s != a.skip && last != a.delim) cnt += finish_line<CLS>(a, s + a.tail_delta, c1) == a.term_acc;
 }
 
-template <class C>
+template <class C, bool CLS>
 __global__ void __launch_bounds__(C::warps * 32) k_lines_tma(const __grid_constant__ Args a,
                                                              const __grid_constant__ CUtensorMap map) {
     extern __shared__ __align__(1024) uint8_t sm[];
@@ -187,7 +212,7 @@ __global__ void __launch_bounds__(C::warps * 32) k_lines_tma(const __grid_consta
         const uint64_t r0 = a.rows * a.chunk;
         for (uint32_t p = lane; p < a.rem_pieces; p += 32) {
             const uint64_t c0 = r0 + static_cast<uint64_t>(p) * a.rem_piece;
-            range_direct(a, c0, min(c0 + a.rem_piece, a.len), cnt);
+            range_direct<CLS>(a, c0, min(c0 + a.rem_piece, a.len), cnt);
         }
     }
 
@@ -234,8 +259,8 @@ __global__ void __launch_bounds__(C::warps * 32) k_lines_tma(const __grid_consta
                     for (int k = 0; k < 4; ++k)
 #pragma unroll
                         for (int j = 0; j < C::chains; ++j) {
-                            s[j] = step(s[j], word_of(v[j], w), k);
-                            cnt += __umulhi(s[j], 1u << 17);
+                            s[j] = step<CLS>(a, s[j], word_of(v[j], w), k);
+                            cnt += counted<CLS>(a, s[j]);
                         }
 #pragma unroll
                 for (int j = 0; j < C::chains; ++j) last[j] = v[j].w >> 24;
@@ -251,7 +276,7 @@ __global__ void __launch_bounds__(C::warps * 32) k_lines_tma(const __grid_consta
         for (int j = 0; j < C::chains; ++j) {
             if (valid[j] && s[j] != a.skip && last[j] != a.delim) {
                 const uint64_t row = row0 + j * 32 + lane;
-                cnt += finish_line(a, s[j] + a.tail_delta, (row + 1) * a.chunk) == a.term_acc;
+                cnt += finish_line<CLS>(a, s[j] + a.tail_delta, (row + 1) * a.chunk) == a.term_acc;
             }
         }
     }
@@ -277,9 +302,13 @@ uint32_t align_up(uint32_t x, uint32_t a) { return (x + a - 1) / a * a; }
 template <class C>
 uint32_t place_stages(const LtTable& t, Args& a) {
     int k = 0;
-    for (uint32_t p = kLtSmemBase; p + C::stage_bytes <= t.lo_addr && k < C::warps * C::stages; p += C::stage_bytes)
+    // free space inside the table image: below the main rows (direct layout)
+    // or the unused rows below START_A (class layout)
+    const uint32_t lo = t.cls ? align_up(t.hole_lo, 1024) : kLtSmemBase;
+    const uint32_t hi = t.cls ? t.hole_hi : t.lo_addr;
+    for (uint32_t p = lo; p + C::stage_bytes <= hi && k < C::warps * C::stages; p += C::stage_bytes)
         a.stage_addr[k++] = p;
-    uint32_t p = align_up(kLtAccAddr + t.hi_bytes, 1024);
+    uint32_t p = align_up(t.cls ? t.smem_table_end : kLtAccAddr + t.hi_bytes, 1024);
     for (; k < C::warps * C::stages; ++k, p += C::stage_bytes) a.stage_addr[k] = p;
     a.bar_addr = align_up(p, 8);
     return a.bar_addr + C::warps * C::stages * 8 - kLtSmemBase;
@@ -294,21 +323,21 @@ CUtensorMapSwizzle swizzle_of(int slice) {
     }
 }
 
-template <class C>
+template <class C, bool CLS>
 int per_sm_of(uint32_t smem) {
     int per_sm = 0;
-    cudaFuncSetAttribute(k_lines_tma<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_lines_tma<C>, C::warps * 32, smem);
+    cudaFuncSetAttribute(k_lines_tma<C, CLS>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_lines_tma<C, CLS>, C::warps * 32, smem);
     return per_sm < 1 ? 1 : per_sm;
 }
 
-template <class C>
+template <class C, bool CLS>
 uint32_t auto_chunk(const LtTable& t, uint64_t len) {
     Args a{};
     const uint32_t smem = place_stages<C>(t, a);
     int dev = 0;
     cudaGetDevice(&dev);
-    const uint64_t rows = static_cast<uint64_t>(per_sm_of<C>(smem)) * device_sm_count(dev) * C::warps * C::rows;
+    const uint64_t rows = static_cast<uint64_t>(per_sm_of<C, CLS>(smem)) * device_sm_count(dev) * C::warps * C::rows;
     uint64_t c = (len + rows - 1) / rows;
     c = (c + C::slice - 1) / C::slice * C::slice;
     if (c < 4u * C::slice) c = 4u * C::slice;
@@ -316,11 +345,11 @@ uint32_t auto_chunk(const LtTable& t, uint64_t len) {
     return static_cast<uint32_t>(c);
 }
 
-template <class C>
+template <class C, bool CLS>
 cudaError_t launch(const LtTable& t, const uint8_t* text, uint64_t len, uint8_t delim, uint32_t chunk,
                    unsigned long long* count, cudaStream_t st) {
     if (len == 0) return cudaSuccess;
-    if (chunk == 0) chunk = auto_chunk<C>(t, len);
+    if (chunk == 0) chunk = auto_chunk<C, CLS>(t, len);
     if (chunk % C::slice) return cudaErrorInvalidValue;
     Args a{};
     a.text = text;
@@ -345,6 +374,9 @@ cudaError_t launch(const LtTable& t, const uint8_t* text, uint64_t len, uint8_t 
     a.tail_delta = t.tail_delta;
     a.term_acc = t.term_acc;
     a.delim = delim;
+    a.row_bytes = t.row_bytes;
+    a.cmap_addr = t.cmap_addr;
+    a.acc_shift = t.acc_shift;
     a.count = count;
 
     CUtensorMap map;
@@ -368,13 +400,13 @@ cudaError_t launch(const LtTable& t, const uint8_t* text, uint64_t len, uint8_t 
                                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
     }
-    const int per_sm = per_sm_of<C>(smem);
+    const int per_sm = per_sm_of<C, CLS>(smem);
     int dev = 0;
     cudaGetDevice(&dev);
     const uint64_t cap = static_cast<uint64_t>(per_sm) * device_sm_count(dev);
     const uint64_t want = (a.tiles + C::warps - 1) / C::warps;
     const int grid = static_cast<int>(want == 0 ? 1 : (want < cap ? want : cap));
-    k_lines_tma<C><<<grid, C::warps * 32, smem, st>>>(a, map);
+    k_lines_tma<C, CLS><<<grid, C::warps * 32, smem, st>>>(a, map);
     return cudaGetLastError();
 }
 
@@ -393,16 +425,24 @@ int shape_id() {
     return e ? std::atoi(e) : 0;
 }
 
+
+template <class C>
+cudaError_t launch2(const LtTable& t, const uint8_t* text, uint64_t len, uint8_t delim, uint32_t chunk,
+                    unsigned long long* count, cudaStream_t st) {
+    return t.cls ? launch<C, true>(t, text, len, delim, chunk, count, st)
+                 : launch<C, false>(t, text, len, delim, chunk, count, st);
+}
+
 }  // namespace
 
 cudaError_t launch_lines_tma(const LtTable& t, const uint8_t* text, uint64_t len, uint8_t delim, uint32_t chunk,
                              unsigned long long* count, cudaStream_t st) {
     switch (shape_id()) {
-    case 1: return launch<S1>(t, text, len, delim, chunk, count, st);
-    case 2: return launch<S2>(t, text, len, delim, chunk, count, st);
-    case 3: return launch<S3>(t, text, len, delim, chunk, count, st);
-    case 4: return launch<S4>(t, text, len, delim, chunk, count, st);
-    default: return launch<S0>(t, text, len, delim, chunk, count, st);
+    case 1: return launch2<S1>(t, text, len, delim, chunk, count, st);
+    case 2: return launch2<S2>(t, text, len, delim, chunk, count, st);
+    case 3: return launch2<S3>(t, text, len, delim, chunk, count, st);
+    case 4: return launch2<S4>(t, text, len, delim, chunk, count, st);
+    default: return launch2<S0>(t, text, len, delim, chunk, count, st);
     }
 }
 

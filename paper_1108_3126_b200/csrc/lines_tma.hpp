@@ -15,8 +15,18 @@ constexpr uint32_t kLtColBytes = 4;               // column stride: byte b of a 
 constexpr uint32_t kLtRowBytes = 256 * kLtColBytes;
 
 // Host-built absolute-address layout of one line table (+ stage ring).
+// Two layouts:
+//   direct (cls = false): rows of 256 u16 entries at 4-byte column stride,
+//     entries and states are absolute shared addresses, START_A = 0x8000;
+//   class  (cls = true):  rows indexed by byte class, entries and states are
+//     row indices, a 256-entry u32 class map holds the absolute address of
+//     each byte's column in row 0 (addr = row * row_bytes + cmap[b]), and
+//     START_A is row 2^acc_shift (tail copies and TERM rows above it).
 struct LtTable {
     bool ok = false;                 // false if the DFA is too large for this layout
+    bool cls = false;
+    uint32_t row_bytes = 0, cmap_addr = 0, acc_shift = 15;
+    uint32_t hole_lo = 0, hole_hi = 0;   // unused rows inside the table (class layout): stage slots go here
     std::vector<uint8_t> lo, hi;     // images of [lo_addr, +lo) main rows and [hi_addr, +hi) upper rows
     uint32_t lo_addr = 0, hi_addr = 0;
     uint32_t lo_bytes = 0, hi_bytes = 0;
@@ -29,11 +39,16 @@ struct LtTable {
 
 // freq: (S+2) x 256 state-by-byte visit counts of a sample (lt_sample_freq);
 // null = default bank placement.
-LtTable make_lines_tma_table(const Program& p, const Dfa& d, uint8_t delim, const std::vector<double>* freq = nullptr);
+LtTable make_lines_tma_table(const Program& p, const Dfa& d, uint8_t delim, const std::vector<double>* freq = nullptr,
+                             bool force_class = false);
 std::vector<double> lt_sample_freq(const Program& p, const Dfa& d, uint8_t delim, const uint8_t* sample, uint64_t len);
 
-// Host emulation of the table walk (absolute addresses), for CPU tests.
+// Host emulation of the table walk, for CPU tests.
 uint32_t lt_step(const LtTable& t, uint32_t s, uint8_t byte);
+inline uint32_t lt_count(const LtTable& t, uint32_t s) { return s >> t.acc_shift; }
+
+// Largest DFA the direct layout takes; bigger ones use the class layout.
+constexpr int32_t kLtDirectMaxStates = 25;
 
 // chunk = bytes per range (multiple of lines_tma_slice()), 0 = one wave of ranges.
 cudaError_t launch_lines_tma(const LtTable& t, const uint8_t* text, uint64_t len, uint8_t delim, uint32_t chunk,

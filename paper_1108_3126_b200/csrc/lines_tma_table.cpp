@@ -88,7 +88,79 @@ std::vector<uint32_t> lt_place_rows(const std::vector<double>& f, uint32_t nrows
     return off;
 }
 
-LtTable make_lines_tma_table(const Program& p, const Dfa& d, uint8_t delim, const std::vector<double>* freq) {
+namespace {
+
+// Class layout (large DFAs): rows indexed by byte class, u16 row-index entries.
+LtTable make_class_table(const Program& p, const Dfa& d, uint8_t delim) {
+    LtTable t;
+    t.cls = true;
+    const uint32_t S = static_cast<uint32_t>(d.n_states);
+    const uint32_t ncols = static_cast<uint32_t>(p.n_classes) + 1;   // + the delimiter column
+    const uint32_t delim_col = ncols - 1;
+    uint32_t rb = align_up(ncols * 2u, 4u);
+    if (((rb / 4u) & 1u) == 0) rb += 4;   // odd word stride: consecutive rows rotate banks
+    t.row_bytes = rb;
+    uint32_t k = 0;
+    while ((1u << k) < S + 2) ++k;       // states, SKIP, VOID below START_A
+    t.acc_shift = k;
+    const uint32_t acc = 1u << k;
+    const uint32_t nrows = acc + 1 + S + 2;   // START_A, tail copies, TERM_A, TERM_R
+    if (nrows > 0xFFFFu) return t;
+    t.cmap_addr = kLtSmemBase;
+    const uint32_t rows_addr = kLtSmemBase + 1024;
+    t.lo_addr = kLtSmemBase;
+    t.lo_bytes = align_up(1024 + nrows * rb, 16);
+    if (kLtSmemBase + t.lo_bytes > 200u * 1024u) return t;
+    t.lo.assign(t.lo_bytes, 0);
+    t.hi_addr = kLtSmemBase + t.lo_bytes;
+    t.hi_bytes = 0;
+    t.hole_lo = align_up(rows_addr + (S + 2) * rb, 256);
+    t.hole_hi = rows_addr + acc * rb;
+    // class map: absolute address of each byte's column in row 0
+    for (int b = 0; b < 256; ++b) {
+        const uint32_t col = b == delim ? delim_col : p.byte_class[b];
+        const uint32_t v = rows_addr + col * 2u;
+        std::memcpy(&t.lo[static_cast<size_t>(b) * 4], &v, 4);
+    }
+    auto put = [&](uint32_t row, uint32_t col, uint32_t v) { put16(t.lo, 1024 + row * rb + col * 2u, v); };
+    const uint32_t skip = S, vd = S + 1, tail0 = acc + 1, term_a = acc + 1 + S, term_r = term_a + 1;
+    t.start = static_cast<uint32_t>(d.start);
+    t.skip = skip;
+    t.void_row = vd;
+    t.tail_delta = tail0;
+    t.term_acc = term_a;
+    t.term_rej = term_r;
+    for (uint32_t s = 0; s < S; ++s) {
+        const bool ac = d.accept[s] != 0;
+        for (uint32_t c = 0; c < ncols; ++c) {
+            if (c == delim_col) {
+                put(s, c, ac ? acc : t.start);
+                put(tail0 + s, c, ac ? term_a : term_r);
+            } else {
+                const uint32_t nx = static_cast<uint32_t>(d.next[static_cast<size_t>(s) * static_cast<size_t>(d.n_classes) + c]);
+                put(s, c, nx);
+                put(tail0 + s, c, tail0 + nx);
+            }
+        }
+    }
+    for (uint32_t c = 0; c < ncols; ++c) {
+        put(skip, c, c == delim_col ? t.start : skip);
+        put(vd, c, vd);
+        put(term_a, c, term_a);
+        put(term_r, c, term_r);
+        put(acc, c, 0);
+    }
+    std::memcpy(&t.lo[1024 + acc * rb], &t.lo[1024 + t.start * rb], rb);   // START_A = start row
+    t.smem_table_end = kLtSmemBase + t.lo_bytes;
+    t.ok = true;
+    return t;
+}
+
+}  // namespace
+
+LtTable make_lines_tma_table(const Program& p, const Dfa& d, uint8_t delim, const std::vector<double>* freq,
+                             bool force_class) {
+    if (force_class || d.n_states > kLtDirectMaxStates) return make_class_table(p, d, delim);
     LtTable t;
     const uint32_t S = static_cast<uint32_t>(d.n_states);
     const uint32_t R = kLtRowBytes;
@@ -159,6 +231,12 @@ LtTable make_lines_tma_table(const Program& p, const Dfa& d, uint8_t delim, cons
 
 uint32_t lt_step(const LtTable& t, uint32_t s, uint8_t byte) {
     uint16_t v;
+    if (t.cls) {
+        uint32_t colabs;
+        std::memcpy(&colabs, &t.lo[static_cast<size_t>(byte) * 4], 4);
+        std::memcpy(&v, &t.lo[s * t.row_bytes + colabs - t.lo_addr], 2);
+        return v;
+    }
     if (s < kLtAccAddr) std::memcpy(&v, &t.lo[s - t.lo_addr + kLtColBytes * byte], 2);
     else std::memcpy(&v, &t.hi[s - kLtAccAddr + kLtColBytes * byte], 2);
     return v;
