@@ -61,6 +61,8 @@ struct TableSlot {
     DevTable dev;
     void* dptr = nullptr;
     LtTable lt;   // TMA line layout (delimited slots only; lt.ok false if it does not fit)
+    DevTable abs;  // plain slot: entries rebased to absolute shared addresses (fixed-stride kernel)
+    void* d_abs = nullptr;
 };
 
 constexpr int32_t kMaxDfaStates = 16384;
@@ -94,6 +96,7 @@ struct rxg_heap {
         if (device < 0) return;
         DeviceGuard g(device);
         if (plain && plain->dptr) cudaFree(plain->dptr);
+        if (plain && plain->d_abs) cudaFree(plain->d_abs);
         for (auto& kv : lines) {
             if (kv.second->dptr) cudaFree(kv.second->dptr);
             if (kv.second->lt.d_lo) cudaFree(kv.second->lt.d_lo);
@@ -224,13 +227,31 @@ int pernode_tables(rxg_heap* h, const PernodeTables** out) {
     return RXG_OK;
 }
 
-int plain_table(rxg_heap* h, const DevTable** out) {
+int plain_table(rxg_heap* h, const DevTable** out, const DevTable** abs_out = nullptr) {
     std::lock_guard<std::mutex> lk(h->mu);
     if (!h->plain) {
         const int rc = upload(h, h->plain, make_plain_table(h->prog, h->dfa));
         if (rc) return rc;
+        const KTable& k = h->plain->host;
+        // rebased copy for k_fixed_abs: raw-byte u16 rows whose entries are
+        // absolute shared addresses (the dynamic window starts at 0x400)
+        if (!k.cls && k.esize == 2 && k.img.size() + 0x400 < 0x10000) {
+            std::vector<uint8_t> img = k.img;
+            for (uint32_t r = 0; r < static_cast<uint32_t>(k.n_states); ++r)
+                for (uint32_t c = 0; c < static_cast<uint32_t>(k.ncols); ++c) {
+                    uint16_t v;
+                    std::memcpy(&v, &img[r * k.row_bytes + c * 2u], 2);
+                    v = static_cast<uint16_t>(v + 0x400);
+                    std::memcpy(&img[r * k.row_bytes + c * 2u], &v, 2);
+                }
+            RXG_CUDA(cudaMalloc(&h->plain->d_abs, img.size()));
+            RXG_CUDA(cudaMemcpy(h->plain->d_abs, img.data(), img.size(), cudaMemcpyHostToDevice));
+            h->plain->abs = h->plain->dev;
+            h->plain->abs.img = h->plain->d_abs;
+        }
     }
     *out = &h->plain->dev;
+    if (abs_out) *abs_out = h->plain->d_abs ? &h->plain->abs : nullptr;
     return RXG_OK;
 }
 
@@ -358,8 +379,11 @@ int batch_device(rxg_heap* h, const uint8_t* d_text, uint64_t len, int32_t delim
         if (stride % 16 == 0 && (reinterpret_cast<uintptr_t>(d_text) & 15))
             return fail(RXG_EINVAL, "text must be 16-byte aligned");
         const DevTable* t = nullptr;
-        if (int rc = plain_table(h, &t)) return rc;
-        const cudaError_t e = launch_fixed(*t, d_text, len / stride, stride, d_count, d_results, st, &ls);
+        const DevTable* ta = nullptr;
+        if (int rc = plain_table(h, &t, &ta)) return rc;
+        const cudaError_t e = ta && stride % 16 == 0
+                                  ? launch_fixed_abs(*ta, d_text, len / stride, stride, d_count, d_results, st, &ls)
+                                  : launch_fixed(*t, d_text, len / stride, stride, d_count, d_results, st, &ls);
         if (e != cudaSuccess) return cuda_fail(e, "launch_fixed");
     }
     g_launches = static_cast<int>(ls.kernels) + (zero_count ? 0 : 0);

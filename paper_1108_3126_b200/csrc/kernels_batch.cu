@@ -213,8 +213,13 @@ __global__ void __launch_bounds__(kBlock) k_count_delims(const uint8_t* __restri
     out[c] = n;
 }
 
+// Fixed-stride strings: few large CTAs (one table copy per SM, not per 256
+// threads: the table can be as large as a small input), 4 strings per thread.
+constexpr int kFixedBlock = 1024;
+constexpr int kFixedChains = 4;
+
 template <typename E, bool CLS, int K, bool RES>
-__global__ void __launch_bounds__(kBlock) k_fixed(const __grid_constant__ FixedArgs a) {
+__global__ void __launch_bounds__(kFixedBlock) k_fixed(const __grid_constant__ FixedArgs a) {
     extern __shared__ __align__(16) uint8_t sm[];
     load_table(sm, a.img, a.img_words);
     uint32_t cnt = 0;
@@ -231,7 +236,28 @@ __global__ void __launch_bounds__(kBlock) k_fixed(const __grid_constant__ FixedA
         }
         if (vec) {
             const uint32_t nblk = a.stride / 16;
-            for (uint32_t i = 0; i < nblk; ++i) {
+            uint32_t i = 0;
+            // two 16-byte blocks of every string in flight before the dependent walk
+            for (; i + 2 <= nblk; i += 2) {
+                uint4 v[K][2];
+#pragma unroll
+                for (int j = 0; j < K; ++j)
+                    if (live[j]) {
+                        const uint8_t* p = a.text + (base + j * T + tid) * a.stride + i * 16u;
+                        v[j][0] = ldg16(p);
+                        v[j][1] = ldg16(p + 16);
+                    }
+#pragma unroll
+                for (int h = 0; h < 2; ++h)
+#pragma unroll
+                    for (int w = 0; w < 4; ++w)
+#pragma unroll
+                        for (int k = 0; k < 4; ++k)
+#pragma unroll
+                            for (int j = 0; j < K; ++j)
+                                if (live[j]) s[j] = step<E, CLS>(sm, a.cls_off, s[j], (word_of(v[j][h], w) >> (8 * k)) & 0xFFu);
+            }
+            for (; i < nblk; ++i) {
                 uint4 v[K];
 #pragma unroll
                 for (int j = 0; j < K; ++j)
@@ -293,8 +319,13 @@ cudaError_t run_fixed(const DevTable& t, const FixedArgs& a, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     int dev = 0;
     cudaGetDevice(&dev);
-    const int grid = grid_for(kern, smem, (a.n + K - 1) / K, dev);
-    kern<<<grid, kBlock, smem, st>>>(a);
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kFixedBlock, smem);
+    if (per_sm < 1) per_sm = 1;
+    const uint64_t cap = static_cast<uint64_t>(per_sm) * device_sm_count(dev);
+    const uint64_t want = (a.n + static_cast<uint64_t>(kFixedBlock) * K - 1) / (static_cast<uint64_t>(kFixedBlock) * K);
+    const int grid = static_cast<int>(want < cap ? (want ? want : 1) : cap);
+    kern<<<grid, kFixedBlock, smem, st>>>(a);
     return cudaGetLastError();
 }
 
@@ -310,10 +341,11 @@ cudaError_t dispatch_lines(const DevTable& t, const LinesArgs& a, cudaStream_t s
 
 template <bool RES>
 cudaError_t dispatch_fixed(const DevTable& t, const FixedArgs& a, cudaStream_t st) {
+    constexpr int K = kFixedChains;
     if (t.esize == 2) {
-        return t.cls ? run_fixed<uint16_t, true, kChains, RES>(t, a, st) : run_fixed<uint16_t, false, kChains, RES>(t, a, st);
+        return t.cls ? run_fixed<uint16_t, true, K, RES>(t, a, st) : run_fixed<uint16_t, false, K, RES>(t, a, st);
     }
-    return t.cls ? run_fixed<uint32_t, true, kChains, RES>(t, a, st) : run_fixed<uint32_t, false, kChains, RES>(t, a, st);
+    return t.cls ? run_fixed<uint32_t, true, K, RES>(t, a, st) : run_fixed<uint32_t, false, K, RES>(t, a, st);
 }
 
 template <typename E, bool CLS>
@@ -420,6 +452,132 @@ cudaError_t launch_fixed(const DevTable& t, const uint8_t* text, uint64_t n, uin
     a.results = results;
     if (ls) ls->kernels = 1;
     return results ? dispatch_fixed<true>(t, a, st) : dispatch_fixed<false>(t, a, st);
+}
+
+}  // namespace rxg
+
+// ── fixed stride, absolute-address variant ─────────────────────────────────
+//
+// Same walk as k_fixed, for raw-byte u16 tables (DFA <= ~120 states) whose
+// entries were rebased to absolute shared addresses (+0x400) on the host:
+// per byte PRMT + IMAD + LDS, no predication (lanes past the end walk string
+// 0 and are not counted), 4 strings per thread, both 16-byte blocks of a
+// 32-byte string loaded before the walk.
+namespace rxg {
+
+namespace {
+
+constexpr uint32_t kAbsBase = 0x400;
+
+struct FixedAbsArgs {
+    const uint8_t* text;
+    uint64_t n;
+    uint32_t stride;   // multiple of 16
+    uint32_t img_words;
+    const uint4* img;
+    uint32_t start;    // absolute
+    uint32_t acc_col;  // byte offset of the accept column
+    unsigned long long* count;
+    uint8_t* results;
+};
+
+__device__ __forceinline__ uint32_t tab16(uint32_t addr) {
+    uint16_t v;
+    asm("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(addr));
+    return v;
+}
+
+template <int K, bool RES>
+__global__ void __launch_bounds__(1024) k_fixed_abs(const __grid_constant__ FixedAbsArgs a) {
+    extern __shared__ __align__(16) uint8_t sm[];
+    if (static_cast<uint32_t>(__cvta_generic_to_shared(sm)) != kAbsBase) __trap();
+    for (uint32_t i = threadIdx.x; i < a.img_words; i += blockDim.x) reinterpret_cast<uint4*>(sm)[i] = a.img[i];
+    __syncthreads();
+    uint32_t cnt = 0;
+    const uint64_t T = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const uint32_t nblk = a.stride / 16;
+    for (uint64_t base = 0; base < a.n; base += T * K) {
+        uint32_t s[K];
+        uint64_t idx[K];
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+            idx[j] = base + j * T + tid;
+            s[j] = a.start;
+        }
+        for (uint32_t i = 0; i < nblk; i += 2) {
+            const bool two = i + 1 < nblk;
+            uint4 v[K][2];
+#pragma unroll
+            for (int j = 0; j < K; ++j) {
+                const uint8_t* p = a.text + (idx[j] < a.n ? idx[j] : 0) * a.stride + i * 16u;
+                v[j][0] = __ldg(reinterpret_cast<const uint4*>(p));
+                v[j][1] = two ? __ldg(reinterpret_cast<const uint4*>(p + 16)) : make_uint4(0, 0, 0, 0);
+            }
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                if (h == 1 && !two) break;
+#pragma unroll
+                for (int w = 0; w < 4; ++w) {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+#pragma unroll
+                        for (int j = 0; j < K; ++j) {
+                            const uint32_t word = w == 0 ? v[j][h].x : (w == 1 ? v[j][h].y : (w == 2 ? v[j][h].z : v[j][h].w));
+                            s[j] = tab16(s[j] + __byte_perm(word, 0, 0x4440 + k) * 2u);
+                        }
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+            if (idx[j] >= a.n) continue;
+            const uint32_t ok = tab16(s[j] + a.acc_col);
+            if (RES) a.results[idx[j]] = static_cast<uint8_t>(ok);
+            cnt += ok;
+        }
+    }
+    cnt = __reduce_add_sync(0xFFFFFFFFu, cnt);
+    if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(a.count, static_cast<unsigned long long>(cnt));
+}
+
+template <int K, bool RES>
+cudaError_t run_fixed_abs(const FixedAbsArgs& a, uint32_t smem, cudaStream_t st) {
+    auto kern = k_fixed_abs<K, RES>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 1024, smem);
+    if (per_sm < 1) per_sm = 1;
+    const uint64_t cap = static_cast<uint64_t>(per_sm) * device_sm_count(dev);
+    const uint64_t want = (a.n + 1024ull * K - 1) / (1024ull * K);
+    const int grid = static_cast<int>(want < cap ? (want ? want : 1) : cap);
+    kern<<<grid, 1024, smem, st>>>(a);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_fixed_abs(const DevTable& t, const uint8_t* text, uint64_t n, uint32_t stride,
+                             unsigned long long* count, uint8_t* results, cudaStream_t st, LaunchStats* ls) {
+    if (ls) ls->kernels = 0;
+    if (n == 0) return cudaSuccess;
+    if (t.cls || t.esize != 2 || stride % 16) return cudaErrorInvalidValue;
+    FixedAbsArgs a{};
+    a.text = text;
+    a.n = n;
+    a.stride = stride;
+    a.img = static_cast<const uint4*>(t.img);
+    a.img_words = t.img_bytes / 16;
+    a.start = t.start + kAbsBase;
+    a.acc_col = t.ncols * 2u;
+    a.count = count;
+    a.results = results;
+    if (ls) ls->kernels = 1;
+    return results ? run_fixed_abs<4, true>(a, t.img_bytes, st) : run_fixed_abs<4, false>(a, t.img_bytes, st);
 }
 
 }  // namespace rxg

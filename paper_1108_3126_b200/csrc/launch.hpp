@@ -40,6 +40,11 @@ size_t lines_scratch_bytes(uint64_t len, uint32_t chunk);
 cudaError_t launch_fixed(const DevTable& t, const uint8_t* text, uint64_t n, uint32_t stride,
                          unsigned long long* count, uint8_t* results, cudaStream_t st, LaunchStats* ls);
 
+// Same, on a raw-byte u16 table image whose entries were rebased by +0x400
+// (absolute shared addresses; stride must be a multiple of 16).
+cudaError_t launch_fixed_abs(const DevTable& t_abs, const uint8_t* text, uint64_t n, uint32_t stride,
+                             unsigned long long* count, uint8_t* results, cudaStream_t st, LaunchStats* ls);
+
 int device_sm_count(int device);
 
 }  // namespace rxg
