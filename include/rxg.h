@@ -186,6 +186,14 @@ int rxg_match_batch(rxg_heap* h, const uint8_t* d_text, uint64_t len, int32_t de
                     uint32_t stride, unsigned long long* d_count, uint8_t* d_results,
                     void* stream);
 
+/* Batch engines for rxg_match_batch_ex */
+#define RXG_BATCH_AUTO 0    /* memoized-step (DFA) kernels; bitset if the DFA is over the cap */
+#define RXG_BATCH_DFA 1     /* K2: one lane per byte range, memoized step in shared memory */
+#define RXG_BATCH_BITSET 2  /* K2b: one warp per line, bitset lockstep (line mode only) */
+
+int rxg_match_batch_ex(rxg_heap* h, const uint8_t* d_text, uint64_t len, int32_t delimiter, uint32_t stride,
+                       int engine, unsigned long long* d_count, uint8_t* d_results, void* stream);
+
 /* Same, host buffers; copies in and out inside the call (synchronous). */
 int rxg_match_batch_host(rxg_heap* h, const uint8_t* text, uint64_t len, int32_t delimiter,
                          uint32_t stride, uint64_t* count, uint8_t* results);

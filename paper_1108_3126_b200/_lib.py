@@ -24,6 +24,7 @@ RXG_EHEAP = 9
 RXG_ENODEV = 10
 
 ENGINES = {"auto": 0, "dfa_seq": 1, "pernode": 2, "rounds": 3, "chunked": 4}
+BATCH_ENGINES = {"auto": 0, "dfa": 1, "bitset": 2}
 
 
 class rxg_node(C.Structure):
@@ -71,6 +72,7 @@ _SIG = {
     "rxg_match_one_ex": (C.c_int, [_P, _P, C.c_uint64, C.c_int, _P, C.POINTER(rxg_one_opts), _P]),
     "rxg_match_one_device": (C.c_int, [_P, _P, C.c_uint64, C.c_int, _P, _P]),
     "rxg_match_batch": (C.c_int, [_P, _P, C.c_uint64, C.c_int32, C.c_uint32, _P, _P, _P]),
+    "rxg_match_batch_ex": (C.c_int, [_P, _P, C.c_uint64, C.c_int32, C.c_uint32, C.c_int, _P, _P, _P]),
     "rxg_match_batch_host": (C.c_int, [_P, _P, C.c_uint64, C.c_int32, C.c_uint32, C.POINTER(C.c_uint64), _P]),
     "rxg_match_batch_multi": (C.c_int, [C.POINTER(C.c_int), C.c_int, C.c_char_p, C.c_size_t, _P, C.c_uint64,
                                         C.c_int32, C.c_uint32, C.POINTER(C.c_uint64), _P]),

@@ -773,12 +773,32 @@ int rxg_match_one(rxg_heap* h, const uint8_t* bytes, uint64_t len, int engine, i
     return RXG_OK;
 }
 
-int rxg_match_batch(rxg_heap* h, const uint8_t* d_text, uint64_t len, int32_t delimiter, uint32_t stride,
-                    unsigned long long* d_count, uint8_t* d_results, void* stream) {
-    if (int rc = need_device(h)) return rc;
+int rxg_match_batch_ex(rxg_heap* h, const uint8_t* d_text, uint64_t len, int32_t delimiter, uint32_t stride,
+                       int engine, unsigned long long* d_count, uint8_t* d_results, void* stream) {
+    const bool bitset = engine == RXG_BATCH_BITSET || (engine == RXG_BATCH_AUTO && h && !h->dfa_ok);
+    if (int rc = need_device(h, !bitset)) return rc;
     if (!d_count || (!d_text && len)) return fail(RXG_EINVAL, "bad arguments");
     DeviceGuard g(h->device);
-    return batch_device(h, d_text, len, delimiter, stride, d_count, d_results, static_cast<cudaStream_t>(stream), true);
+    const cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (!bitset) return batch_device(h, d_text, len, delimiter, stride, d_count, d_results, st, true);
+    if (delimiter < 0 || delimiter > 255) return fail(RXG_EUNSUPPORTED, "the bitset batch engine takes delimited lines");
+    const PernodeTables* t = nullptr;
+    if (int rc = pernode_tables(h, &t)) return rc;
+    RXG_CUDA(cudaMemsetAsync(d_count, 0, sizeof(unsigned long long), st));
+    const size_t sb = lines_bitset_scratch_bytes(len);
+    void* scratch = nullptr;
+    RXG_CUDA(cudaMallocAsync(&scratch, sb, st));
+    const cudaError_t e = launch_lines_bitset(*t, d_text, len, static_cast<uint8_t>(delimiter), d_count, d_results,
+                                              scratch, sb, h->device, st);
+    cudaFreeAsync(scratch, st);
+    if (e != cudaSuccess) return cuda_fail(e, "launch_lines_bitset");
+    g_launches = len ? 4 : 0;
+    return RXG_OK;
+}
+
+int rxg_match_batch(rxg_heap* h, const uint8_t* d_text, uint64_t len, int32_t delimiter, uint32_t stride,
+                    unsigned long long* d_count, uint8_t* d_results, void* stream) {
+    return rxg_match_batch_ex(h, d_text, len, delimiter, stride, RXG_BATCH_AUTO, d_count, d_results, stream);
 }
 
 int rxg_match_batch_host(rxg_heap* h, const uint8_t* text, uint64_t len, int32_t delimiter, uint32_t stride,

@@ -22,6 +22,8 @@
 //             per step — the dedup-by-pointer-equality of the paper.
 #include <cstdint>
 
+#include <cub/device/device_scan.cuh>
+
 #include "pernode.hpp"
 
 namespace rxg {
@@ -181,6 +183,7 @@ __global__ void __launch_bounds__(1024) k_rounds(const __grid_constant__ RoundsA
 
 constexpr int kMaxSlots = 8;        // words per lane: W <= 256 (8191 positions)
 constexpr int kDenseGroups = 32;    // up to this many residual rows: vote per row, rows in smem
+constexpr uint32_t kBitsetChunk = 4096;   // delimiter-scan chunk of the K2b line index
 
 struct PernodeArgs {
     const uint8_t* text;
@@ -397,6 +400,166 @@ cudaError_t run_pernode2(const PernodeArgs& a, uint32_t smem, bool dense, cudaSt
     return dense ? run_pernode<SLOTS, true, 0>(a, smem, st) : run_pernode<SLOTS, false, 0>(a, smem, st);
 }
 
+// ── K2b: warp-per-line bitset lockstep for batches ───────────────────────
+//
+// The bitset variant of the batch path (no memoized DFA: works for patterns
+// whose DFA would explode). Every warp walks whole lines with the K1 step,
+// its lanes holding the ballot words of the active set; tables are shared by
+// the CTA's warps. Line boundaries come from a delimiter-position pass.
+
+struct BitsetLinesArgs {
+    PernodeArgs p;                       // tables (p.text / p.len unused)
+    const uint8_t* text;
+    uint64_t len;
+    const unsigned long long* dpos;      // positions of the delimiters, ascending
+    const unsigned long long* ndelim;    // device: number of delimiters
+    unsigned long long* count;
+    uint8_t* results;
+};
+
+template <int SLOTS, bool DENSE, int GREG>
+__global__ void __launch_bounds__(256) k_lines_bitset(const __grid_constant__ BitsetLinesArgs b) {
+    extern __shared__ __align__(16) uint32_t smp[];
+    const PernodeArgs& a = b.p;
+    const int W = a.W;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    uint32_t* masks = smp;
+    const int mrows = a.byte_masks ? 256 : a.n_classes;
+    uint32_t* TR = masks + mrows * W;
+    uint32_t* RR = TR + (DENSE ? a.n_groups * W : 0);
+    const int hw = DENSE ? 0 : (a.n_groups + 31) / 32;
+    uint32_t* hit_all = RR + (DENSE ? a.n_groups * W : 0);
+    uint8_t* cls = reinterpret_cast<uint8_t*>(hit_all + hw * nw);
+    uint32_t* hit = hit_all + hw * warp;
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) cls[i] = a.cls[i];
+    __syncthreads();
+    for (int i = threadIdx.x; i < mrows * W; i += blockDim.x)
+        masks[i] = a.byte_masks ? a.cmask[cls[i / W] * W + i % W] : a.cmask[i];
+    if (DENSE)
+        for (int i = threadIdx.x; i < a.n_groups * W; i += blockDim.x) {
+            TR[i] = a.trig[i];
+            RR[i] = a.rows[i];
+        }
+    for (int i = threadIdx.x; i < hw * nw; i += blockDim.x) hit_all[i] = 0;
+    uint32_t SH[SLOTS], HG[SLOTS], I0[SLOTS];
+    uint32_t TRr[GREG ? GREG : 1][SLOTS], RRr[GREG ? GREG : 1][SLOTS];
+#pragma unroll
+    for (int k = 0; k < SLOTS; ++k) {
+        const int w = lane + 32 * k;
+        I0[k] = w < W ? a.init[w] : 0u;
+        SH[k] = w < W ? a.shift[w] : 0u;
+        HG[k] = w < W ? a.has_group[w] : 0u;
+#pragma unroll
+        for (int g = 0; g < (GREG ? GREG : 1); ++g) {
+            TRr[g][k] = (GREG && g < a.n_groups && w < W) ? a.trig[g * W + w] : 0u;
+            RRr[g][k] = (GREG && g < a.n_groups && w < W) ? a.rows[g * W + w] : 0u;
+        }
+    }
+    __syncthreads();
+    const unsigned long long nd = *b.ndelim;
+    // a final segment after the last delimiter is a line (std::getline)
+    const unsigned long long nlines = nd + ((b.len > 0 && (nd == 0 || b.dpos[nd - 1] != b.len - 1)) ? 1ull : 0ull);
+    const int A = a.n_bits - 1;
+    uint32_t cnt = 0;
+    auto rowp = [&](uint32_t byte) { return a.byte_masks ? masks + byte * W : masks + cls[byte] * W; };
+    for (unsigned long long line = static_cast<unsigned long long>(blockIdx.x) * nw + warp; line < nlines;
+         line += static_cast<unsigned long long>(gridDim.x) * nw) {
+        const uint64_t lo = line == 0 ? 0 : b.dpos[line - 1] + 1;
+        const uint64_t hi = line < nd ? b.dpos[line] : b.len;
+        uint32_t E[SLOTS];
+#pragma unroll
+        for (int k = 0; k < SLOTS; ++k) E[k] = I0[k];
+        uint64_t pos = lo;
+        bool live = true;
+        while (live && pos + 16 <= hi) {
+            uint32_t by[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) by[i] = __ldg(b.text + pos + i);
+            uint32_t Mw[16][SLOTS];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                const uint32_t* M = rowp(by[i]);
+#pragma unroll
+                for (int k = 0; k < SLOTS; ++k) Mw[i][k] = lane + 32 * k < W ? M[lane + 32 * k] : 0u;
+            }
+#pragma unroll
+            for (int i = 0; i < 16; ++i) pernode_step<SLOTS, DENSE, GREG>(a, Mw[i], TR, RR, hit, hw, lane, E, SH, HG, TRr, RRr);
+            pos += 16;
+            bool any = false;
+#pragma unroll
+            for (int k = 0; k < SLOTS; ++k) any |= E[k] != 0u;
+            live = __any_sync(0xFFFFFFFFu, any);
+        }
+        for (; live && pos < hi; ++pos) {
+            const uint32_t* M = rowp(__ldg(b.text + pos));
+            uint32_t Mw[SLOTS];
+#pragma unroll
+            for (int k = 0; k < SLOTS; ++k) Mw[k] = lane + 32 * k < W ? M[lane + 32 * k] : 0u;
+            pernode_step<SLOTS, DENSE, GREG>(a, Mw, TR, RR, hit, hw, lane, E, SH, HG, TRr, RRr);
+        }
+        uint32_t acc = 0;
+#pragma unroll
+        for (int k = 0; k < SLOTS; ++k)
+            if (lane + 32 * k == (A >> 5)) acc = (E[k] >> (A & 31)) & 1u;
+        acc = __reduce_or_sync(0xFFFFFFFFu, acc);
+        if (lane == 0) {
+            if (b.results) b.results[line] = static_cast<uint8_t>(acc);
+            cnt += acc;
+        }
+    }
+    if (lane == 0 && cnt) atomicAdd(b.count, static_cast<unsigned long long>(cnt));
+}
+
+template <int SLOTS, bool DENSE, int GREG>
+cudaError_t run_lines_bitset(const BitsetLinesArgs& b, uint32_t smem, int device, cudaStream_t st) {
+    auto kern = k_lines_bitset<SLOTS, DENSE, GREG>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem);
+    if (per_sm < 1) per_sm = 1;
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    kern<<<per_sm * sms, 256, smem, st>>>(b);
+    return cudaGetLastError();
+}
+
+template <int SLOTS>
+cudaError_t run_lines_bitset2(const BitsetLinesArgs& b, uint32_t smem, bool dense, int device, cudaStream_t st) {
+    if (b.p.n_groups <= 1) return run_lines_bitset<SLOTS, true, 1>(b, smem, device, st);
+    if (b.p.n_groups <= 2) return run_lines_bitset<SLOTS, true, 2>(b, smem, device, st);
+    return dense ? run_lines_bitset<SLOTS, true, 0>(b, smem, device, st)
+                 : run_lines_bitset<SLOTS, false, 0>(b, smem, device, st);
+}
+
+// Delimiter positions: per chunk count -> scan (host side, cub) -> positions.
+__global__ void __launch_bounds__(256) k_delim_pos(const uint8_t* __restrict__ text, uint64_t len, uint32_t chunk,
+                                                   uint64_t nchunks, uint32_t delim,
+                                                   const unsigned long long* __restrict__ base,
+                                                   unsigned long long* __restrict__ dpos) {
+    const uint64_t c = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (c >= nchunks) return;
+    const uint64_t c0 = c * chunk, c1 = min(c0 + chunk, len);
+    unsigned long long k = base[c];
+    for (uint64_t p = c0; p < c1; ++p)
+        if (text[p] == delim) dpos[k++] = p;
+}
+
+__global__ void __launch_bounds__(256) k_delim_count(const uint8_t* __restrict__ text, uint64_t len, uint32_t chunk,
+                                                     uint64_t nchunks, uint32_t delim,
+                                                     unsigned long long* __restrict__ out) {
+    const uint64_t c = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (c > nchunks) return;
+    if (c == nchunks) {   // trailing zero so the exclusive scan yields the total at [nchunks]
+        out[c] = 0;
+        return;
+    }
+    const uint64_t c0 = c * chunk, c1 = min(c0 + chunk, len);
+    unsigned long long n = 0;
+    for (uint64_t p = c0; p < c1; ++p) n += text[p] == delim;
+    out[c] = n;
+}
+
 }  // namespace
 
 cudaError_t launch_rounds(const RoundsTables& t, const uint8_t* text, uint64_t len, int32_t* accept,
@@ -453,6 +616,65 @@ cudaError_t launch_pernode(const PernodeTables& t, const uint8_t* text, uint64_t
     if (slots <= 3) return run_pernode2<3>(a, smem, dense, st);
     if (slots <= 4) return run_pernode2<4>(a, smem, dense, st);
     if (slots <= kMaxSlots) return run_pernode2<kMaxSlots>(a, smem, dense, st);
+    return cudaErrorInvalidValue;
+}
+
+size_t lines_bitset_scratch_bytes(uint64_t len) {
+    const uint64_t nchunks = (len + kBitsetChunk - 1) / kBitsetChunk;
+    size_t temp = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, temp, static_cast<unsigned long long*>(nullptr),
+                                  static_cast<unsigned long long*>(nullptr), static_cast<int64_t>(nchunks + 1));
+    // counts, base, positions (at most one per byte), cub temp
+    return (2 * (nchunks + 1) + len + 1) * sizeof(unsigned long long) + temp + 256;
+}
+
+cudaError_t launch_lines_bitset(const PernodeTables& t, const uint8_t* text, uint64_t len, uint8_t delim,
+                                unsigned long long* count, uint8_t* results, void* scratch, size_t scratch_bytes,
+                                int device, cudaStream_t st) {
+    if (len == 0) return cudaSuccess;
+    const uint64_t nchunks = (len + kBitsetChunk - 1) / kBitsetChunk;
+    unsigned long long* counts = static_cast<unsigned long long*>(scratch);
+    unsigned long long* base = counts + nchunks + 1;
+    unsigned long long* dpos = base + nchunks + 1;
+    void* temp = dpos + len + 1;
+    size_t temp_bytes = scratch_bytes - (2 * (nchunks + 1) + len + 1) * sizeof(unsigned long long);
+    const unsigned g = static_cast<unsigned>((nchunks + 1 + 255) / 256);
+    k_delim_count<<<g, 256, 0, st>>>(text, len, kBitsetChunk, nchunks, delim, counts);
+    cudaError_t e = cub::DeviceScan::ExclusiveSum(temp, temp_bytes, counts, base, static_cast<int64_t>(nchunks + 1), st);
+    if (e != cudaSuccess) return e;
+    k_delim_pos<<<g, 256, 0, st>>>(text, len, kBitsetChunk, nchunks, delim, base, dpos);
+    BitsetLinesArgs b{};
+    PernodeArgs& a = b.p;
+    a.cls = t.cls;
+    a.cmask = t.cmask;
+    a.shift = t.shift;
+    a.has_group = t.has_group;
+    a.group = t.group;
+    a.rows = t.rows;
+    a.trig = t.trig;
+    a.init = t.init;
+    a.W = t.W;
+    a.n_bits = t.n_bits;
+    a.n_groups = t.n_groups;
+    a.n_classes = t.n_classes;
+    const bool dense = t.n_groups <= kDenseGroups;
+    a.byte_masks = 256u * static_cast<uint32_t>(t.W) * 4u <= 96u * 1024u;
+    b.text = text;
+    b.len = len;
+    b.dpos = dpos;
+    b.ndelim = base + nchunks;
+    b.count = count;
+    b.results = results;
+    const uint32_t mrows = a.byte_masks ? 256u : static_cast<uint32_t>(t.n_classes);
+    const uint32_t group_words = dense ? 2u * static_cast<uint32_t>(t.n_groups * t.W)
+                                       : 8u * static_cast<uint32_t>((t.n_groups + 31) / 32);
+    const uint32_t smem = (mrows * static_cast<uint32_t>(t.W) + group_words) * 4u + 256u;
+    const int slots = (t.W + 31) / 32;
+    if (slots <= 1) return run_lines_bitset2<1>(b, smem, dense, device, st);
+    if (slots <= 2) return run_lines_bitset2<2>(b, smem, dense, device, st);
+    if (slots <= 3) return run_lines_bitset2<3>(b, smem, dense, device, st);
+    if (slots <= 4) return run_lines_bitset2<4>(b, smem, dense, device, st);
+    if (slots <= kMaxSlots) return run_lines_bitset2<kMaxSlots>(b, smem, dense, device, st);
     return cudaErrorInvalidValue;
 }
 

@@ -90,8 +90,74 @@ std::vector<uint32_t> lt_place_rows(const std::vector<double>& f, uint32_t nrows
 
 namespace {
 
+// Row numbering for the class layout. Row r starts at word (base + r*rb/4)
+// with rb/4 odd, so its bank offset cycles through all 32 values as r does:
+// choosing a row index for a state chooses its bank offset. Hot states are
+// numbered greedily (hottest first) into the offset class that collides least
+// with the already numbered hot states under the sampled class frequencies.
+std::vector<uint32_t> number_states(const Program& p, const Dfa& d, uint8_t delim, const std::vector<double>* freq,
+                                    uint32_t nmain, uint32_t base_word, uint32_t rb_words, uint32_t delim_col) {
+    const uint32_t S = static_cast<uint32_t>(d.n_states);
+    std::vector<uint32_t> row(nmain);
+    for (uint32_t s = 0; s < nmain; ++s) row[s] = s;
+    if (!freq || freq->size() < static_cast<size_t>(S) * 256) return row;
+    auto off_of = [&](uint32_t r) { return (base_word + r * rb_words) & 31u; };
+    // bank histogram of each state in a row at offset 0: column c sits in word c/2
+    std::vector<std::array<double, 32>> H(S);
+    std::vector<double> tot(S, 0.0);
+    for (uint32_t s = 0; s < S; ++s) {
+        H[s].fill(0.0);
+        for (int b = 0; b < 256; ++b) {
+            const double x = (*freq)[static_cast<size_t>(s) * 256 + static_cast<size_t>(b)];
+            if (x == 0.0) continue;
+            const uint32_t c = b == delim ? delim_col : p.byte_class[b];
+            H[s][(c / 2) & 31u] += x;
+            tot[s] += x;
+        }
+    }
+    std::vector<uint32_t> order(S);
+    for (uint32_t s = 0; s < S; ++s) order[s] = s;
+    std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return tot[a] > tot[b]; });
+    // free rows per bank offset
+    std::array<std::vector<uint32_t>, 32> free_rows;
+    for (uint32_t r = nmain; r-- > 0;) free_rows[off_of(r)].push_back(r);   // pop_back yields the lowest
+    std::vector<uint32_t> hot_state, hot_off;
+    std::vector<bool> placed(nmain, false);
+    constexpr size_t kHot = 64;
+    for (uint32_t s : order) {
+        if (tot[s] == 0.0) break;
+        double best = -1.0;
+        uint32_t bo = 0;
+        for (uint32_t o = 0; o < 32; ++o) {
+            if (free_rows[o].empty()) continue;
+            double c = 0.0;
+            for (size_t i = 0; i < hot_state.size(); ++i)
+                for (uint32_t k = 0; k < 32; ++k) c += H[s][k] * H[hot_state[i]][(k + o + 32 - hot_off[i]) & 31u];
+            if (best < 0.0 || c < best) {
+                best = c;
+                bo = o;
+            }
+        }
+        row[s] = free_rows[bo].back();
+        free_rows[bo].pop_back();
+        placed[s] = true;
+        if (hot_state.size() < kHot) {
+            hot_state.push_back(s);
+            hot_off.push_back(bo);
+        }
+    }
+    // cold states, SKIP and VOID take the remaining rows in order
+    std::vector<uint32_t> rest;
+    for (auto& v : free_rows) rest.insert(rest.end(), v.begin(), v.end());
+    std::sort(rest.begin(), rest.end());
+    size_t k = 0;
+    for (uint32_t s = 0; s < nmain; ++s)
+        if (!placed[s]) row[s] = rest[k++];
+    return row;
+}
+
 // Class layout (large DFAs): rows indexed by byte class, u16 row-index entries.
-LtTable make_class_table(const Program& p, const Dfa& d, uint8_t delim) {
+LtTable make_class_table(const Program& p, const Dfa& d, uint8_t delim, const std::vector<double>* freq) {
     LtTable t;
     t.cls = true;
     const uint32_t S = static_cast<uint32_t>(d.n_states);
@@ -104,7 +170,7 @@ LtTable make_class_table(const Program& p, const Dfa& d, uint8_t delim) {
     while ((1u << k) < S + 2) ++k;       // states, SKIP, VOID below START_A
     t.acc_shift = k;
     const uint32_t acc = 1u << k;
-    const uint32_t nrows = acc + 1 + S + 2;   // START_A, tail copies, TERM_A, TERM_R
+    const uint32_t nrows = acc + 1 + (S + 2) + 2;   // START_A, tail copies of the S+2 main rows, TERM_A, TERM_R
     if (nrows > 0xFFFFu) return t;
     t.cmap_addr = kLtSmemBase;
     const uint32_t rows_addr = kLtSmemBase + 1024;
@@ -123,8 +189,9 @@ LtTable make_class_table(const Program& p, const Dfa& d, uint8_t delim) {
         std::memcpy(&t.lo[static_cast<size_t>(b) * 4], &v, 4);
     }
     auto put = [&](uint32_t row, uint32_t col, uint32_t v) { put16(t.lo, 1024 + row * rb + col * 2u, v); };
-    const uint32_t skip = S, vd = S + 1, tail0 = acc + 1, term_a = acc + 1 + S, term_r = term_a + 1;
-    t.start = static_cast<uint32_t>(d.start);
+    const std::vector<uint32_t> R = number_states(p, d, delim, freq, S + 2, rows_addr / 4u, rb / 4u, delim_col);
+    const uint32_t skip = R[S], vd = R[S + 1], tail0 = acc + 1, term_a = acc + 1 + S + 2, term_r = term_a + 1;
+    t.start = R[static_cast<uint32_t>(d.start)];
     t.skip = skip;
     t.void_row = vd;
     t.tail_delta = tail0;
@@ -132,14 +199,15 @@ LtTable make_class_table(const Program& p, const Dfa& d, uint8_t delim) {
     t.term_rej = term_r;
     for (uint32_t s = 0; s < S; ++s) {
         const bool ac = d.accept[s] != 0;
+        const uint32_t r = R[s];
         for (uint32_t c = 0; c < ncols; ++c) {
             if (c == delim_col) {
-                put(s, c, ac ? acc : t.start);
-                put(tail0 + s, c, ac ? term_a : term_r);
+                put(r, c, ac ? acc : t.start);
+                put(tail0 + r, c, ac ? term_a : term_r);
             } else {
-                const uint32_t nx = static_cast<uint32_t>(d.next[static_cast<size_t>(s) * static_cast<size_t>(d.n_classes) + c]);
-                put(s, c, nx);
-                put(tail0 + s, c, tail0 + nx);
+                const uint32_t nx = R[static_cast<uint32_t>(d.next[static_cast<size_t>(s) * static_cast<size_t>(d.n_classes) + c])];
+                put(r, c, nx);
+                put(tail0 + r, c, tail0 + nx);
             }
         }
     }
@@ -160,7 +228,7 @@ LtTable make_class_table(const Program& p, const Dfa& d, uint8_t delim) {
 
 LtTable make_lines_tma_table(const Program& p, const Dfa& d, uint8_t delim, const std::vector<double>* freq,
                              bool force_class) {
-    if (force_class || d.n_states > kLtDirectMaxStates) return make_class_table(p, d, delim);
+    if (force_class || d.n_states > kLtDirectMaxStates) return make_class_table(p, d, delim, freq);
     LtTable t;
     const uint32_t S = static_cast<uint32_t>(d.n_states);
     const uint32_t R = kLtRowBytes;

@@ -40,4 +40,10 @@ cudaError_t launch_rounds(const RoundsTables& t, const uint8_t* text, uint64_t l
 cudaError_t launch_pernode(const PernodeTables& t, const uint8_t* text, uint64_t len, uint32_t every,
                            uint32_t* checkpoints, int32_t* accept, cudaStream_t st);
 
+// K2b: warp-per-line bitset batch (line mode). scratch: lines_bitset_scratch_bytes(len).
+size_t lines_bitset_scratch_bytes(uint64_t len);
+cudaError_t launch_lines_bitset(const PernodeTables& t, const uint8_t* text, uint64_t len, uint8_t delim,
+                                unsigned long long* count, uint8_t* results, void* scratch, size_t scratch_bytes,
+                                int device, cudaStream_t st);
+
 }  // namespace rxg

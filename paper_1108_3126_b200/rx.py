@@ -292,12 +292,12 @@ class Matcher:
                                             d_accept.data_ptr(), _stream_ptr(stream)))
 
     def match_batch_device(self, d_text, d_count, d_results=None, delimiter: int = 10, stride: int = 0,
-                           stream=None, nbytes: int | None = None):
+                           stream=None, nbytes: int | None = None, engine: str = "auto"):
         """Async batch match on device tensors (d_count: int64 cuda tensor of 1)."""
         n = d_text.numel() if nbytes is None else nbytes
-        _check(L.lib().rxg_match_batch(self._h, d_text.data_ptr(), n, delimiter, stride, d_count.data_ptr(),
-                                       d_results.data_ptr() if d_results is not None else None,
-                                       _stream_ptr(stream)))
+        _check(L.lib().rxg_match_batch_ex(self._h, d_text.data_ptr(), n, delimiter, stride, L.BATCH_ENGINES[engine],
+                                          d_count.data_ptr(), d_results.data_ptr() if d_results is not None else None,
+                                          _stream_ptr(stream)))
 
     def match_batch(self, text, delimiter: int = 10, stride: int = 0, results: bool = False):
         """Synchronous batch match of a host buffer -> (count, results|None)."""

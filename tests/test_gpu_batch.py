@@ -77,3 +77,51 @@ def test_enumerated_regexes_over_all_short_strings():
         if not np.array_equal(res, ores):
             bad.append(p)
     assert not bad, bad[:10]
+
+
+def _device_batch(m, text, engine, delimiter=10):
+    import torch
+
+    d = torch.from_numpy(np.ascontiguousarray(text)).cuda() if len(text) else torch.zeros(16, dtype=torch.uint8, device="cuda")
+    n = len(text)
+    cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+    res = torch.zeros(max(rx.count_strings(text, delimiter, 0), 1) + 1, dtype=torch.uint8, device="cuda")
+    m.match_batch_device(d, cnt, res, delimiter=delimiter, nbytes=n, engine=engine)
+    torch.cuda.synchronize()
+    return int(cnt.item()), res.cpu().numpy()[: rx.count_strings(text, delimiter, 0)]
+
+
+@pytest.mark.parametrize("cfg", ["c", "d"])
+def test_bitset_batch_engine_matches_oracle(cfg):
+    pattern = rx.synth_pattern(cfg)
+    text = rx.synth_input(cfg, 2 << 20)
+    ocount, ores = _oracle(pattern).match_batch(text, 10, 0)
+    m = rx.Matcher(pattern, device=0)
+    c, r = _device_batch(m, text, "bitset")
+    assert c == ocount and np.array_equal(r, ores)
+    c2, r2 = _device_batch(m, text, "dfa")
+    assert c2 == ocount and np.array_equal(r2, ores)
+
+
+@pytest.mark.parametrize("chunk_text", [b"\n", b"\n\n\n", b"ab", b"ab\n", b"\nab", b"a\nb\n\nab", b"abb" * 40])
+def test_bitset_batch_edges(chunk_text):
+    for pattern in ["a*", "ab", "()", "(a|b)*abb", "a|()"]:
+        m = rx.Matcher(pattern, device=0)
+        text = np.frombuffer(chunk_text, np.uint8)
+        ocount, ores = _oracle(pattern).match_batch(text, 10, 0)
+        c, r = _device_batch(m, text, "bitset")
+        assert c == ocount and np.array_equal(r, ores), (pattern, chunk_text)
+
+
+def test_exploding_dfa_falls_back_to_bitset_engine():
+    """(a|b)*a(a|b)^17 needs 2^18 DFA states: the memoized path refuses it and
+    the batch entry point runs the warp-per-line bitset engine instead."""
+    pattern = "(a|b)*a" + "(a|b)" * 17
+    m = rx.Matcher(pattern, device=0)
+    assert m.info()["dfa_states"] == 0
+    rng = np.random.default_rng(4)
+    lines = [bytes(rng.choice([97, 98], size=int(rng.integers(0, 60))).astype(np.uint8)) for _ in range(3000)]
+    text = np.frombuffer(b"\n".join(lines) + b"\n", np.uint8)
+    ocount, ores = _oracle(pattern).match_batch(text, 10, 0)
+    c, r = _device_batch(m, text, "auto")
+    assert c == ocount and np.array_equal(r, ores)

@@ -18,16 +18,14 @@ for v in sys.argv[2:]:
     m = rx.Matcher(pat, device=0)
     if name == "tune":
         m.tune(text[: 1 << 20])
-    res = None
-    if name == "generic":
-        res = torch.zeros(1, dtype=torch.uint8, device=0)  # placeholder: results path not timed here
+    eng = "bitset" if name == "bitset" else "auto"
     for _ in range(3):
-        m.match_batch_device(d, cnt, nbytes=len(text))
+        m.match_batch_device(d, cnt, nbytes=len(text), engine=eng)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
     e0.record()
     for _ in range(10):
-        m.match_batch_device(d, cnt, nbytes=len(text))
+        m.match_batch_device(d, cnt, nbytes=len(text), engine=eng)
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / 10
