@@ -12,6 +12,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 OUT = PKG / "librxg.so"
+CLI = PKG / "rxgmatch"
 BUILD = ROOT / "build" / "rxg"
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -60,6 +61,11 @@ def build(verbose: bool = False, force: bool = False) -> Path:
     if force or not OUT.exists() or any(o.stat().st_mtime > OUT.stat().st_mtime for o in objs):
         cmd = [nvcc()] + ARCH + ["-shared", "-o", str(OUT)] + [str(o) for o in objs] + ["-ldl"]
         subprocess.run(cmd, check=True)
+    # the `rxvm match` front end on the batch path (links librxg.so)
+    cli_src = CSRC / "tools" / "rxgmatch.cpp"
+    if force or not CLI.exists() or cli_src.stat().st_mtime > CLI.stat().st_mtime or OUT.stat().st_mtime > CLI.stat().st_mtime:
+        subprocess.run(["g++", "-std=c++17", "-O2", f"-I{ROOT / 'include'}", str(cli_src), f"-L{PKG}", "-lrxg",
+                        "-Wl,-rpath,$ORIGIN", "-o", str(CLI)], check=True)
     return OUT
 
 
