@@ -67,11 +67,28 @@ namespace detail {
 inline void check(int rc) {
     if (rc != RXG_OK) raise(rc);
 }
-// Symbols to bytes: ASCII as is; a scalar >= 0x80 can match no literal of a
-// byte-level pattern, so it becomes a byte no position matches.
+// Symbols to the UTF-8 bytes the device matches (literals are expanded to
+// UTF-8 byte chains, so this is exact for every scalar).
 inline std::string narrow(InputView w) {
-    std::string s(w.size(), '\0');
-    for (size_t i = 0; i < w.size(); ++i) s[i] = w[i] < 0x80 ? static_cast<char>(w[i]) : static_cast<char>(0x80);
+    std::string s;
+    s.reserve(w.size());
+    for (char32_t cp : w) {
+        if (cp < 0x80) {
+            s += static_cast<char>(cp);
+        } else if (cp < 0x800) {
+            s += static_cast<char>(0xC0 | (cp >> 6));
+            s += static_cast<char>(0x80 | (cp & 0x3F));
+        } else if (cp < 0x10000) {
+            s += static_cast<char>(0xE0 | (cp >> 12));
+            s += static_cast<char>(0x80 | ((cp >> 6) & 0x3F));
+            s += static_cast<char>(0x80 | (cp & 0x3F));
+        } else {
+            s += static_cast<char>(0xF0 | (cp >> 18));
+            s += static_cast<char>(0x80 | ((cp >> 12) & 0x3F));
+            s += static_cast<char>(0x80 | ((cp >> 6) & 0x3F));
+            s += static_cast<char>(0x80 | (cp & 0x3F));
+        }
+    }
     return s;
 }
 }  // namespace detail
@@ -169,8 +186,12 @@ inline bool par_accepts(const Heap& h, InputView w, unsigned workers, uint64_t s
     (void)seed;
     const std::string b = detail::narrow(w);
     int32_t acc = 0;
-    detail::check(rxg_match_one(h.device_handle(), reinterpret_cast<const uint8_t*>(b.data()), b.size(),
-                                RXG_ENGINE_ROUNDS, &acc));
+    int rc = rxg_match_one(h.device_handle(), reinterpret_cast<const uint8_t*>(b.data()), b.size(), RXG_ENGINE_ROUNDS,
+                           &acc);
+    if (rc == RXG_EUNSUPPORTED)   // non-ASCII literals: the thread-per-node bitset form of the same scheme
+        rc = rxg_match_one(h.device_handle(), reinterpret_cast<const uint8_t*>(b.data()), b.size(), RXG_ENGINE_PERNODE,
+                           &acc);
+    detail::check(rc);
     if (stats) *stats = ParStats{};
     return acc != 0;
 }

@@ -21,11 +21,14 @@
  *                           `rxvm match` (tools/rxvm.cpp:100-112, std::getline semantics)
  *   rxg_match_batch_multi   the same, sharded over several GPUs with one count all-reduce
  *
- * Symbols are bytes. For patterns whose literals are all ASCII (< 0x80) this
- * is exact for any valid UTF-8 input: a multi-byte sequence decodes to one
- * scalar that no position matches, and feeding its bytes kills the active set
- * just the same. Patterns with non-ASCII literals are rejected with
- * RXG_EUNSUPPORTED by the byte-level matchers.
+ * Symbols are bytes: every literal is matched as the UTF-8 encoding of its
+ * scalar (a multi-byte literal is a chain of byte positions). UTF-8 is
+ * prefix-free and the lead byte fixes the length, so on valid UTF-8 input
+ * this is exactly the reference's match over decode_utf8 scalars. On invalid
+ * UTF-8 the reference throws; here the affected strings simply do not match
+ * (rxgmatch validates and exits 2 like rxvm). The literal rounds engine
+ * (RXG_ENGINE_ROUNDS) compares raw bytes with literals and needs ASCII
+ * literals (RXG_EUNSUPPORTED otherwise).
  */
 #ifndef RXG_H
 #define RXG_H
@@ -42,7 +45,7 @@ extern "C" {
 #define RXG_EINVAL 1        /* bad argument (null pointer, bad size, misaligned buffer) */
 #define RXG_EPARSE 2        /* pattern syntax error; rx::ParseError (regex.hpp:50-54) */
 #define RXG_EUTF8 3         /* malformed UTF-8 pattern; decode_utf8 (utf8.cpp:32-41) */
-#define RXG_EUNSUPPORTED 4  /* pattern literal >= 0x80 on a byte-level matcher */
+#define RXG_EUNSUPPORTED 4  /* engine cannot run this pattern / mode */
 #define RXG_ECUDA 5         /* CUDA runtime error */
 #define RXG_ENOMEM 6        /* allocation failed */
 #define RXG_ETOOBIG 7       /* memoized step table exceeds the shared-memory budget */

@@ -148,7 +148,7 @@ int need_device(rxg_heap* h, bool dfa = true) {
     if (!h) return fail(RXG_EINVAL, "null heap");
     if (h->device < 0) return fail(RXG_ENODEV, "host-only heap handle");
     if (!h->prog.byte_symbols)
-        return fail(RXG_EUNSUPPORTED, "pattern has a literal >= 0x80; byte-level matching needs ASCII literals");
+        return fail(RXG_EUNSUPPORTED, "pattern has a literal that is not a Unicode scalar value");
     if (dfa && !h->dfa_ok)
         return fail(RXG_ETOOBIG, "memoized step table exceeds " + std::to_string(kMaxDfaStates) + " states");
     return RXG_OK;
@@ -744,6 +744,7 @@ int rxg_match_one_ex(rxg_heap* h, const uint8_t* d_bytes, uint64_t len, int engi
         return RXG_OK;
     }
     case RXG_ENGINE_ROUNDS: {
+        if (h->prog.scalar_pos) return fail(RXG_EUNSUPPORTED, "the literal rounds engine compares bytes: ASCII literals only");
         const RoundsTables* t = nullptr;
         if (int rc = rounds_tables(h, &t)) return rc;
         const cudaError_t e = launch_rounds(*t, d_bytes, len, d_accept, o.d_stats, o.d_trace, st);

@@ -71,6 +71,73 @@ struct Closure {
     }
 };
 
+std::vector<uint8_t> utf8_bytes(uint32_t cp) {
+    std::vector<uint8_t> b;
+    if (cp < 0x80) {
+        b.push_back(static_cast<uint8_t>(cp));
+    } else if (cp < 0x800) {
+        b.push_back(static_cast<uint8_t>(0xC0 | (cp >> 6)));
+        b.push_back(static_cast<uint8_t>(0x80 | (cp & 0x3F)));
+    } else if (cp < 0x10000) {
+        b.push_back(static_cast<uint8_t>(0xE0 | (cp >> 12)));
+        b.push_back(static_cast<uint8_t>(0x80 | ((cp >> 6) & 0x3F)));
+        b.push_back(static_cast<uint8_t>(0x80 | (cp & 0x3F)));
+    } else {
+        b.push_back(static_cast<uint8_t>(0xF0 | (cp >> 18)));
+        b.push_back(static_cast<uint8_t>(0x80 | ((cp >> 12) & 0x3F)));
+        b.push_back(static_cast<uint8_t>(0x80 | ((cp >> 6) & 0x3F)));
+        b.push_back(static_cast<uint8_t>(0x80 | (cp & 0x3F)));
+    }
+    return b;
+}
+
+// Rewrites the scalar position form into the UTF-8 byte position form.
+void expand_utf8(Program& p) {
+    const int32_t n_old = p.n_pos;
+    const size_t W_old = static_cast<size_t>(p.W);
+    std::vector<int32_t> entry(static_cast<size_t>(n_old) + 1);
+    std::vector<std::vector<uint8_t>> bytes(static_cast<size_t>(n_old));
+    int32_t n_new = 0;
+    for (int32_t q = 0; q < n_old; ++q) {
+        entry[static_cast<size_t>(q)] = n_new;
+        bytes[static_cast<size_t>(q)] = utf8_bytes(p.pos_sym[static_cast<size_t>(q)]);
+        n_new += static_cast<int32_t>(bytes[static_cast<size_t>(q)].size());
+    }
+    entry[static_cast<size_t>(n_old)] = n_new;   // accept bit
+    const int32_t W_new = (n_new + 1 + 31) / 32;
+    auto remap = [&](const uint32_t* src, uint32_t* dst) {
+        for (int32_t q = 0; q <= n_old; ++q)
+            if ((src[q >> 5] >> (q & 31)) & 1u) set_bit(dst, entry[static_cast<size_t>(q)]);
+    };
+    std::vector<uint32_t> follow(static_cast<size_t>(n_new + 1) * static_cast<size_t>(W_new), 0u);
+    std::vector<uint32_t> init(static_cast<size_t>(W_new), 0u);
+    std::vector<uint32_t> sym(static_cast<size_t>(n_new));
+    std::vector<Addr> addr(static_cast<size_t>(n_new));
+    for (int32_t q = 0; q < n_old; ++q) {
+        const auto& b = bytes[static_cast<size_t>(q)];
+        const int32_t e = entry[static_cast<size_t>(q)];
+        for (size_t j = 0; j < b.size(); ++j) {
+            const int32_t np = e + static_cast<int32_t>(j);
+            sym[static_cast<size_t>(np)] = b[j];
+            addr[static_cast<size_t>(np)] = p.pos_addr[static_cast<size_t>(q)];
+            uint32_t* row = &follow[static_cast<size_t>(np) * static_cast<size_t>(W_new)];
+            if (j + 1 < b.size()) set_bit(row, np + 1);
+            else remap(&p.follow[static_cast<size_t>(q) * W_old], row);
+        }
+    }
+    remap(p.init.data(), init.data());
+    for (Addr a = 0; a < static_cast<Addr>(p.addr_pos.size()); ++a)
+        if (p.addr_pos[static_cast<size_t>(a)] >= 0) p.addr_pos[static_cast<size_t>(a)] = entry[static_cast<size_t>(p.addr_pos[static_cast<size_t>(a)])];
+    p.scalar_pos = n_old;
+    p.n_pos = n_new;
+    p.n_bits = n_new + 1;
+    p.W = W_new;
+    p.follow.swap(follow);
+    p.init.swap(init);
+    p.pos_sym.swap(sym);
+    p.pos_addr.swap(addr);
+}
+
 }  // namespace
 
 Program build_program(const Heap& h) {
@@ -79,6 +146,7 @@ Program build_program(const Heap& h) {
     Program p;
     p.heap = h;
     const int32_t N = h.size();
+    p.scalar_pos = 0;
     p.addr_pos.assign(static_cast<size_t>(N), -1);
 
     // Positions in left-to-right leaf order (pre-order walk, left child
@@ -118,7 +186,7 @@ Program build_program(const Heap& h) {
     p.n_pos = static_cast<int32_t>(p.pos_addr.size());
     p.n_bits = p.n_pos + 1;
     p.W = (p.n_bits + 31) / 32;
-    const size_t W = static_cast<size_t>(p.W);
+    size_t W = static_cast<size_t>(p.W);
     const int32_t A = p.n_pos;
 
     Closure cl(h, p.addr_pos);
@@ -131,11 +199,23 @@ Program build_program(const Heap& h) {
     p.init.assign(W, 0u);
     if (cl.run(0, p.init.data())) set_bit(p.init.data(), A);
 
+    // Symbols are matched as UTF-8 bytes. A literal whose scalar needs k > 1
+    // bytes becomes a chain of k byte positions (entry = first byte); every
+    // follow set that contained the literal now contains its entry. UTF-8 is
+    // prefix-free and the lead byte fixes the length, so on valid UTF-8 input
+    // the k byte steps reproduce the reference's one scalar step exactly
+    // (decode_utf8, utf8.cpp:16-46, then step_char).
+    bool valid = true, multi = false;
+    for (uint32_t s : p.pos_sym) {
+        if (s > 0x10FFFF || (s >= 0xD800 && s <= 0xDFFF)) valid = false;
+        if (s >= 0x80) multi = true;
+    }
+    p.byte_symbols = valid;
+    if (valid && multi) expand_utf8(p);
+
+    W = static_cast<size_t>(p.W);
     // Byte classes: bytes with the same matching position set share a class;
     // class 0 is the empty set (bytes no position matches).
-    p.byte_symbols = true;
-    for (uint32_t s : p.pos_sym)
-        if (s >= 0x80) p.byte_symbols = false;
     std::vector<std::vector<uint32_t>> masks(256, std::vector<uint32_t>(W, 0u));
     for (int32_t q = 0; q < p.n_pos; ++q) {
         const uint32_t s = p.pos_sym[static_cast<size_t>(q)];

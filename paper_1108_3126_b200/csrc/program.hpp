@@ -11,6 +11,8 @@
 //     E0             = evolve({root})     ∪ {A if eps_reaches_null({root})}
 //     E_{i+1}        = ∪ { F'(q) : q in E_i, sym(q) = a_i }      (A never matches)
 //     accept(w)      = A in E_|w|
+// Literals are then expanded to UTF-8 byte chains (expand_utf8) so that the
+// kernels step on bytes; for ASCII literals nothing changes.
 // evolve distributes over union, so E_i = evolve(S_i) ∪ {A iff S_i accepts}
 // at every step, and the early reject of the reference is the absorbing
 // empty set here. DFA states are memoized E sets of exactly this step.
@@ -34,7 +36,8 @@ struct Program {
     std::vector<uint32_t> pos_sym;  // position -> symbol
     std::vector<uint32_t> follow;   // n_bits x W ; row A is empty
     std::vector<uint32_t> init;     // W
-    bool byte_symbols = true;       // every Chr symbol < 0x80 (bytes == scalars for UTF-8 input)
+    bool byte_symbols = true;       // every literal is a Unicode scalar: matched as its UTF-8 bytes
+    int32_t scalar_pos = 0;         // Chr nodes before UTF-8 expansion (0 if every literal is ASCII)
     uint8_t byte_class[256] = {};   // byte -> class id; class 0 matches no position
     int32_t n_classes = 0;
     std::vector<uint32_t> class_mask;   // n_classes x W

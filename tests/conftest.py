@@ -16,11 +16,9 @@ def pytest_configure(config):
 @pytest.fixture(scope="session", autouse=True)
 def _built():
     """The product library and the CPU checkers must exist (no fallback)."""
-    from paper_1108_3126_b200 import _lib
+    from paper_1108_3126_b200 import _lib, build
 
-    if not _lib.LIB_PATH.exists():
-        from paper_1108_3126_b200 import build
-
+    if not _lib.LIB_PATH.exists() or not build.CLI.exists():
         build.build()
     import oracle_bind
 

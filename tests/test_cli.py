@@ -68,3 +68,10 @@ def test_invalid_utf8_line_is_an_error_after_earlier_matches():
     assert r.returncode == 2
     assert r.stdout == b"ab\nb\n"
     assert b"invalid UTF-8" in r.stderr
+
+
+@pytest.mark.gpu
+def test_unicode_pattern():
+    data = "é中\naé中\nb\n😀é\n".encode()
+    r = run(["(a|é)*中"], data)
+    assert r.returncode == 0 and r.stdout == "é中\naé中\n".encode()

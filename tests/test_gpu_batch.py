@@ -125,3 +125,30 @@ def test_exploding_dfa_falls_back_to_bitset_engine():
     ocount, ores = _oracle(pattern).match_batch(text, 10, 0)
     c, r = _device_batch(m, text, "auto")
     assert c == ocount and np.array_equal(r, ores)
+
+
+def test_unicode_literals_all_engines():
+    """Literals >= 0x80 are matched as UTF-8 byte chains; parity with the
+    reference's scalar matching (decode_utf8) on valid UTF-8 lines."""
+    import random
+
+    rng = random.Random(11)
+    alpha = ["a", "b", "é", "中", "😀", " "]
+    for pattern in ["(a|é)*中", "😀(a|b| )*é", "((é|b)*中)*", "(a|b|é|中|😀| )*😀(a|b|é|中|😀| )*"]:
+        lines = ["".join(rng.choice(alpha) for _ in range(rng.randint(0, 12))) for _ in range(2000)]
+        text = np.frombuffer(("\n".join(lines) + "\n").encode(), np.uint8)
+        if Ref.available():
+            rh = RefHeap(pattern.encode())
+            want = np.array([rh.accepts(l) for l in lines], np.uint8)
+        else:
+            want = rx.Matcher(pattern, device=-1).emulate_batch(text, 10, 0, 16)[1]
+        m = rx.Matcher(pattern, device=0)
+        for eng in ("dfa", "bitset"):
+            c, r = _device_batch(m, text, eng)
+            assert np.array_equal(r, want), (pattern, eng)
+            assert c == int(want.sum())
+        c, r = m.match_batch(text, delimiter=10, results=True)
+        assert np.array_equal(r, want)
+        for l, wv in list(zip(lines, want))[:40]:
+            for eng in ("chunked", "pernode", "dfa_seq"):
+                assert m.lockstep_accepts(l.encode(), eng) == bool(wv), (pattern, l, eng)

@@ -116,8 +116,27 @@ def test_non_matching_bytes_behave_like_unmatched_scalars():
             assert RefHeap(b"(a|b)*abb").accepts(w) == want
 
 
-def test_non_ascii_literals_are_flagged():
-    assert H("α*").info()["byte_symbols"] == 0
+def test_non_ascii_literals_match_as_utf8_chains():
+    """Literals >= 0x80 become UTF-8 byte chains: same answers as the reference
+    on decoded scalars, for valid UTF-8 inputs."""
+    import random
+
+    rng = random.Random(3)
+    alpha = ["a", "b", "é", "中", "😀"]
+    for p in ["é*", "(a|é)*中", "😀(a|b)*é", "a|é|中|😀", "(é中)*😀", "((é|b)*中)*"]:
+        m = H(p)
+        assert m.info()["byte_symbols"] == 1
+        want = RefHeap(p.encode()) if Ref.available() else None
+        for _ in range(150):
+            w = "".join(rng.choice(alpha) for _ in range(rng.randint(0, 8)))
+            _, acc = m.host_walk(w.encode())
+            if want is not None:
+                assert acc == want.accepts(w), (p, w)
+        # the emulated line kernels agree with the host walk on a UTF-8 line buffer
+        lines = ["".join(rng.choice(alpha) for _ in range(rng.randint(0, 8))) for _ in range(300)]
+        text = np.frombuffer("\n".join(lines).encode() + b"\n", np.uint8)
+        c, res = m.emulate_batch(text, 10, 0, 16)
+        assert list(res) == [int(m.host_walk(l.encode())[1]) for l in lines]
 
 
 def test_synth_generators_are_deterministic():
