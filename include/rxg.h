@@ -208,6 +208,16 @@ int rxg_match_batch_multi(const int* devices, int ndev, const char* pattern, siz
                           const uint8_t* text, uint64_t len, int32_t delimiter, uint32_t stride,
                           uint64_t* count, uint8_t* results);
 
+/* Every pattern against every string — the reference's crosscheck sweep
+ * shape (crosscheck.cpp:111-185) as one device call; a GPU `EngineId` for
+ * run_engine (engines.cpp:40-82) can answer from this. patterns: n_patterns
+ * NUL-terminated UTF-8 patterns back to back. Strings: the lines of text
+ * (delimiter >= 0) or fixed-stride pieces. results: n_patterns x n_strings
+ * bytes (row-major, 0/1). On a pattern error returns RXG_EPARSE/RXG_EUTF8 and
+ * *bad_pattern = its index. */
+int rxg_match_many(int device, const char* patterns, int32_t n_patterns, const uint8_t* text, uint64_t len,
+                   int32_t delimiter, uint32_t stride, uint8_t* results, uint64_t* n_strings, int32_t* bad_pattern);
+
 /* Shard boundaries used by rxg_match_batch_multi: offsets[0..ndev], split at
  * delimiter boundaries (line mode) or stride multiples. Host only. */
 int rxg_shard_bounds(const uint8_t* text, uint64_t len, int32_t delimiter, uint32_t stride,

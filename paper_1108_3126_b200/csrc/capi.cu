@@ -20,6 +20,7 @@
 #include "single.hpp"
 #include "pernode.hpp"
 #include "chunked.hpp"
+#include "many.hpp"
 #include "synth.hpp"
 #include "tables.hpp"
 
@@ -869,6 +870,96 @@ int rxg_match_batch_host(rxg_heap* h, const uint8_t* text, uint64_t len, int32_t
         cudaEventDestroy(consumed[i]);
     }
     g_launches = launches;
+    return rc;
+}
+
+int rxg_match_many(int device, const char* patterns, int32_t n_patterns, const uint8_t* text, uint64_t len,
+                   int32_t delimiter, uint32_t stride, uint8_t* results, uint64_t* n_strings, int32_t* bad_pattern) {
+    if (!patterns || n_patterns < 0 || (!text && len) || !results || !n_strings) return fail(RXG_EINVAL, "bad arguments");
+    if (delimiter > 255 || (delimiter < 0 && (stride == 0 || len % stride))) return fail(RXG_EINVAL, "bad string layout");
+    // strings
+    std::vector<uint64_t> off{0};
+    uint32_t sep = 0;
+    if (delimiter >= 0) {
+        sep = 1;
+        for (uint64_t at = 0; at < len;) {
+            const void* nl = std::memchr(text + at, delimiter, len - at);
+            at = nl ? static_cast<uint64_t>(static_cast<const uint8_t*>(nl) - text) + 1 : len + 1;
+            off.push_back(at);   // +1 past the delimiter; a final unterminated string ends at len (+1 virtual)
+        }
+    } else {
+        for (uint64_t at = stride; at <= len; at += stride) off.push_back(at);
+    }
+    const uint64_t ns = off.size() - 1;
+    *n_strings = ns;
+    // per-pattern tables (host: parse, compile, position form, memoized step)
+    std::vector<uint8_t> tables;
+    std::vector<uint64_t> toff{0};
+    std::vector<uint32_t> meta;
+    uint32_t max_bytes = 16;
+    const char* pp = patterns;
+    for (int32_t k = 0; k < n_patterns; ++k) {
+        const size_t pl = std::strlen(pp);
+        try {
+            const Program pg = build_program(compile(parse(std::string_view(pp, pl))));
+            Dfa d;
+            if (!pg.byte_symbols || !build_dfa(pg, 4096, d)) {
+                if (bad_pattern) *bad_pattern = k;
+                return fail(RXG_ETOOBIG, "pattern " + std::to_string(k) + ": memoized step table too large");
+            }
+            const uint32_t S = static_cast<uint32_t>(d.n_states), C = static_cast<uint32_t>(pg.n_classes);
+            const uint32_t acc_off = 256, rows_off = (256 + S + 15) & ~15u;
+            const uint32_t bytes = (rows_off + S * C * 2 + 15) & ~15u;
+            std::vector<uint8_t> img(bytes, 0);
+            std::memcpy(img.data(), pg.byte_class, 256);
+            for (uint32_t st = 0; st < S; ++st) {
+                img[acc_off + st] = d.accept[st];
+                for (uint32_t c = 0; c < C; ++c) {
+                    const uint16_t v = static_cast<uint16_t>(d.next[st * C + c]);
+                    std::memcpy(&img[rows_off + (st * C + c) * 2], &v, 2);
+                }
+            }
+            tables.insert(tables.end(), img.begin(), img.end());
+            toff.push_back(tables.size());
+            meta.insert(meta.end(), {S, C, static_cast<uint32_t>(d.start), acc_off, rows_off});
+            max_bytes = std::max(max_bytes, bytes);
+        } catch (const ParseError& e) {
+            if (bad_pattern) *bad_pattern = k;
+            return fail(RXG_EPARSE, "pattern " + std::to_string(k) + ": " + e.what());
+        } catch (const Utf8Error& e) {
+            if (bad_pattern) *bad_pattern = k;
+            return fail(RXG_EUTF8, "pattern " + std::to_string(k) + ": " + e.what());
+        }
+        pp += pl + 1;
+    }
+    if (max_bytes > 200u * 1024u) return fail(RXG_ETOOBIG, "a pattern table exceeds shared memory");
+    if (n_patterns == 0 || ns == 0) return RXG_OK;
+    DeviceGuard g(device);
+    // one device buffer: tables | table offsets | meta | text | string offsets | results
+    auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+    const size_t b0 = al(tables.size()), b1 = al(toff.size() * 8), b2 = al(meta.size() * 4), b3 = al(len + 16),
+                 b4 = al(off.size() * 8), b5 = al(static_cast<size_t>(n_patterns) * ns);
+    uint8_t* d = nullptr;
+    RXG_CUDA(cudaMalloc(&d, b0 + b1 + b2 + b3 + b4 + b5));
+    int rc = RXG_OK;
+    cudaError_t e = cudaSuccess;
+    ManyDev md;
+    md.tables = d;
+    md.table_off = reinterpret_cast<const uint64_t*>(d + b0);
+    md.meta = reinterpret_cast<const uint32_t*>(d + b0 + b1);
+    md.text = d + b0 + b1 + b2;
+    md.str_off = reinterpret_cast<const uint64_t*>(d + b0 + b1 + b2 + b3);
+    uint8_t* dres = d + b0 + b1 + b2 + b3 + b4;
+    if ((e = cudaMemcpy(d, tables.data(), tables.size(), cudaMemcpyHostToDevice)) == cudaSuccess &&
+        (e = cudaMemcpy(d + b0, toff.data(), toff.size() * 8, cudaMemcpyHostToDevice)) == cudaSuccess &&
+        (e = cudaMemcpy(d + b0 + b1, meta.data(), meta.size() * 4, cudaMemcpyHostToDevice)) == cudaSuccess &&
+        (!len || (e = cudaMemcpy(d + b0 + b1 + b2, text, len, cudaMemcpyHostToDevice)) == cudaSuccess) &&
+        (e = cudaMemcpy(d + b0 + b1 + b2 + b3, off.data(), off.size() * 8, cudaMemcpyHostToDevice)) == cudaSuccess &&
+        (e = launch_many(md, static_cast<uint64_t>(n_patterns), ns, sep, dres, max_bytes, device, nullptr)) == cudaSuccess)
+        e = cudaMemcpy(results, dres, static_cast<size_t>(n_patterns) * ns, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) rc = cuda_fail(e, "rxg_match_many");
+    cudaFree(d);
+    g_launches = 1;
     return rc;
 }
 

@@ -343,6 +343,19 @@ def match_batch_multi(devices, pattern, text, delimiter: int = 10, stride: int =
     return cnt.value, (res[:nstr] if res is not None else None)
 
 
+def match_many(patterns, text, delimiter: int = 10, stride: int = 0, device: int = 0) -> np.ndarray:
+    """Every pattern against every string (the crosscheck sweep shape) -> [n_patterns, n_strings] 0/1."""
+    blob = b"".join(_b(p) + b"\0" for p in patterns)
+    p, n, keep = _ptr(text)
+    nstr = count_strings(text, delimiter, stride) if delimiter >= 0 else n // stride
+    res = np.zeros(max(len(patterns) * nstr, 1), np.uint8)
+    ns = C.c_uint64(0)
+    bad = C.c_int32(-1)
+    _check(L.lib().rxg_match_many(device, blob, len(patterns), p, n, delimiter, stride, res.ctypes.data,
+                                  C.byref(ns), C.byref(bad)))
+    return res[: len(patterns) * ns.value].reshape(len(patterns), ns.value)
+
+
 def shard_bounds(text, ndev: int, delimiter: int = 10, stride: int = 0) -> list[int]:
     p, n, keep = _ptr(text)
     off = (C.c_uint64 * (ndev + 1))()

@@ -152,3 +152,23 @@ def test_unicode_literals_all_engines():
         for l, wv in list(zip(lines, want))[:40]:
             for eng in ("chunked", "pernode", "dfa_seq"):
                 assert m.lockstep_accepts(l.encode(), eng) == bool(wv), (pattern, l, eng)
+
+
+def test_crosscheck_sweep_acceptance_criterion_3():
+    """Acceptance criterion 3 shape (acceptance_main.cpp:93-105, crosscheck.cpp:111-185):
+    every regex <= 8 AST nodes over {a,b} x every string <= 6, on the GPU in one
+    multi-heap call, against the oracle (pinned to the reference)."""
+    import itertools
+
+    if not Ref.available():
+        pytest.skip("oracle/_ref not built (regex enumeration comes from the reference)")
+    pats = Ref.enumerate_regexes(8, "ab")
+    strings = [""] + ["".join(t) for L in range(1, 7) for t in itertools.product("ab", repeat=L)]
+    text = np.frombuffer(("\n".join(strings) + "\n").encode(), np.uint8)
+    got = rx.match_many(pats, text, delimiter=10)
+    assert got.shape == (len(pats), len(strings))
+    # oracle on a deterministic sample of 4000 regexes (all 39k take ~1 min on CPU)
+    rng = np.random.default_rng(0)
+    for k in rng.choice(len(pats), size=4000, replace=False):
+        _, want = _oracle(pats[k]).match_batch(text, 10, 0, threads=1)
+        assert np.array_equal(got[k], want), pats[k]
