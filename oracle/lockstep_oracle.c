@@ -164,6 +164,30 @@ int oracle_lockstep_accepts(const oracle_heap* h, oracle_ws* ws, const uint32_t*
     return oracle_eps_reaches_null(h, ws, s, ns);
 }
 
+/* lockstep.cpp:77-80 from an arbitrary start set: S <- step_char(evolve(S), a)
+ * for each byte, stopping early on the empty set. s_io holds the start set on
+ * entry (n_io entries, null allowed) and the final set on exit; capacity n+1.
+ * Used to verify a long single-string run chunk by chunk from checkpoints
+ * (SURVEY.md §8(c) parity plan item 2). */
+int32_t oracle_walk_from(const oracle_heap* h, int32_t* s_io, int32_t n_io, const uint8_t* bytes, uint64_t len) {
+    oracle_ws ws;
+    oracle_ws_init(&ws, h->n);
+    int32_t* e = (int32_t*)malloc((size_t)(h->n + 1) * sizeof(int32_t));
+    int32_t* t = (int32_t*)malloc((size_t)(h->n + 1) * sizeof(int32_t));
+    int32_t ns = n_io;
+    memcpy(t, s_io, (size_t)ns * sizeof(int32_t));
+    for (uint64_t i = 0; i < len && ns > 0; ++i) {
+        const int32_t ne = oracle_evolve(h, &ws, t, ns, e, NULL);
+        ns = oracle_step_char(h, &ws, e, ne, bytes[i], t);
+        if (ns < 0) ns = 0;
+    }
+    memcpy(s_io, t, (size_t)ns * sizeof(int32_t));
+    free(e);
+    free(t);
+    oracle_ws_free(&ws);
+    return ns;
+}
+
 int oracle_accepts_bytes(const oracle_heap* h, const uint8_t* bytes, uint64_t len) {
     oracle_ws ws;
     oracle_ws_init(&ws, h->n);

@@ -40,6 +40,7 @@ int32_t oracle_step_char(const oracle_heap* h, oracle_ws* ws, const int32_t* e, 
 int oracle_lockstep_accepts(const oracle_heap* h, oracle_ws* ws, const uint32_t* w, uint64_t len,
                             int32_t* buf_a, int32_t* buf_b, uint64_t* enqueued);
 int oracle_accepts_bytes(const oracle_heap* h, const uint8_t* bytes, uint64_t len);
+int32_t oracle_walk_from(const oracle_heap* h, int32_t* s_io, int32_t n_io, const uint8_t* bytes, uint64_t len);
 uint64_t oracle_split(const uint8_t* text, uint64_t len, int32_t delimiter, uint32_t stride, uint64_t* starts,
                       uint64_t* lens);
 uint64_t oracle_match_batch(const oracle_heap* h, const uint8_t* text, uint64_t len, int32_t delimiter,

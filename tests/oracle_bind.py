@@ -70,6 +70,17 @@ class Oracle:
         buf = C.create_string_buffer(bytes(w), max(len(w), 1))
         return bool(self.lib.oracle_accepts_bytes(C.byref(self.h), buf, len(w)))
 
+    def walk_from(self, s, w: bytes) -> set:
+        """S after stepping through w from start set s (lockstep.cpp:77-80)."""
+        self.lib.oracle_walk_from.restype = C.c_int32
+        self.lib.oracle_walk_from.argtypes = [C.POINTER(_Heap), C.c_void_p, C.c_int32, C.c_void_p, C.c_uint64]
+        io = np.zeros(self.h.n + 2, np.int32)
+        arr = sorted(s)
+        io[: len(arr)] = arr
+        buf = C.create_string_buffer(bytes(w), max(len(w), 1))
+        k = self.lib.oracle_walk_from(C.byref(self.h), io.ctypes.data, len(arr), buf, len(w))
+        return set(io[:k].tolist())
+
     # set-level functions (lockstep.cpp:10-73), sets as Python sets of addresses (-1 = null)
     def _ws(self):
         class WS(C.Structure):
@@ -115,6 +126,35 @@ class Oracle:
         cnt = self.lib.oracle_match_batch(C.byref(self.h), a.ctypes.data, a.nbytes, delimiter, stride,
                                           res.ctypes.data if res is not None else None, threads)
         return int(cnt), (res[:nstr] if res is not None else None)
+
+
+def verify_checkpoints(heap, pos_addr, n_pos, checkpoints, text, every, threads=None):
+    """Chunk-parallel check of a long single-string run.
+    checkpoints[k] is the position-form set E after (k+1)*every symbols: the
+    Chr addresses of evolve(S) plus the accept bit n_pos. Chunk k is re-run by
+    the oracle from the Chr addresses of checkpoint k-1 (evolve(E) = E for Chr
+    sets; {root} for k = 0) and must end in a set S with evolve(S) equal to
+    checkpoint k's Chr addresses and accepts(S) equal to its accept bit.
+    Returns the number of chunks verified; raises AssertionError on a mismatch."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    o = Oracle(heap)
+
+    def chr_set(row):
+        return {int(pos_addr[q]) for q in range(n_pos) if (row[q >> 5] >> (q & 31)) & 1}
+
+    def acc_bit(row):
+        return bool((row[n_pos >> 5] >> (n_pos & 31)) & 1)
+
+    def check(k):
+        start = {0} if k == 0 else chr_set(checkpoints[k - 1])
+        s = o.walk_from(start, bytes(text[k * every:(k + 1) * every]))
+        assert o.evolve(s) == chr_set(checkpoints[k]), f"chunk {k}: evolved set differs"
+        assert (-1 in s or o.eps_reaches_null(s)) == acc_bit(checkpoints[k]), f"chunk {k}: accept differs"
+        return True
+
+    with ThreadPoolExecutor(threads or os.cpu_count() or 1) as ex:
+        return sum(ex.map(check, range(len(checkpoints))))
 
 
 def _count_strings(a, delimiter, stride):

@@ -136,3 +136,23 @@ def test_config_e_prefix(engine):
     for n in (1 << 16, 1 << 20):
         w = rx.synth_input("e", n)
         assert m.lockstep_accepts(w.tobytes(), engine) == O(p).accepts(w.tobytes())
+
+
+def test_config_e_k1_checkpoints_verified_chunk_parallel():
+    """SURVEY.md §8(c) parity plan item 2: K1 (thread-per-node) emits its active
+    set every 256 KiB of a 4 MiB prefix of config (e); each chunk is re-run by
+    the oracle from the previous checkpoint on all host cores."""
+    from oracle_bind import verify_checkpoints
+
+    p = rx.synth_pattern("e")
+    m = rx.Matcher(p)
+    n, every = 4 << 20, 256 << 10
+    w = rx.synth_input("e", n)
+    W = m.info()["words"]
+    ck = torch.zeros((n // every) * W, dtype=torch.int32, device="cuda")
+    acc = torch.zeros(1, dtype=torch.int32, device="cuda")
+    m.match_one_ex(torch.from_numpy(w).cuda(), acc, "pernode", checkpoint_every=every, d_checkpoints=ck)
+    rows = ck.cpu().numpy().view(np.uint32).reshape(-1, W)
+    pos_addr, _, _ = rx.Matcher(p, device=-1).tables()
+    assert verify_checkpoints(rx.compile(rx.parse(p)), pos_addr, len(pos_addr), rows, w, every) == n // every
+    assert bool(acc.item()) == bool((rows[-1][len(pos_addr) >> 5] >> (len(pos_addr) & 31)) & 1)
