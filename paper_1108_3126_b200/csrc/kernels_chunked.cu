@@ -37,6 +37,8 @@ struct ChunkArgs {
     uint32_t* mid;       // nranges x (chunk / kMid)
     int32_t* accept;
     unsigned long long* repairs;   // ranges re-walked (instrumentation, nullable)
+    unsigned int* ticket;          // zeroed before the walk: CTAs finished
+    unsigned long long* first_bad; // set to ~0 before the walk: first range whose entry guess is wrong
 };
 
 __device__ __forceinline__ uint32_t word_of(const uint4& v, int w) {
@@ -89,6 +91,24 @@ __global__ void __launch_bounds__(256) k_chunk_walk(const __grid_constant__ Chun
         }
         a.e[j] = s;
     }
+    // The last CTA to finish checks every range boundary in parallel, so the
+    // in-order repair pass only starts where a guess was actually wrong.
+    __shared__ bool last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        last = atomicAdd(a.ticket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    unsigned long long bad = ~0ull;
+    for (uint64_t j = 1 + threadIdx.x; j < a.nranges; j += blockDim.x)
+        if (a.g[j] != a.e[j - 1]) {
+            bad = j;
+            break;
+        }
+    if (bad != ~0ull) atomicMin(a.first_bad, bad);
 }
 
 // Phase 2: one warp repairs the entry states in order; lane 0 walks, the warp
@@ -100,8 +120,10 @@ __global__ void __launch_bounds__(32) k_chunk_fix(const __grid_constant__ ChunkA
     const uint32_t lane = threadIdx.x;
     const uint32_t per = a.chunk / kMid;
     unsigned long long repairs = 0;
-    uint32_t exact = a.nranges ? a.e[0] : a.start;   // range 0 starts at the true start
-    for (uint64_t base = 1; base < a.nranges; base += 32) {
+    const unsigned long long fb = *a.first_bad;
+    // ranges before the first wrong guess chain exactly (range 0 starts at the true start)
+    uint32_t exact = a.nranges == 0 ? a.start : (fb == ~0ull ? a.e[a.nranges - 1] : a.e[fb - 1]);
+    for (uint64_t base = fb == ~0ull ? a.nranges : fb; base < a.nranges; base += 32) {
         // ranges base..base+31: find mismatches in order; after a repair the
         // exact exit may change, so re-scan from the repaired range.
         uint64_t j = base;
@@ -171,7 +193,7 @@ cudaError_t run(const DevTable& t, const ChunkArgs& a, int device, cudaStream_t 
 
 size_t chunked_scratch_bytes(uint64_t len, uint32_t chunk) {
     const uint64_t n = (len + chunk - 1) / chunk;
-    return (2 * n + n * (chunk / kMid)) * sizeof(uint32_t) + 64;
+    return 16 + (2 * n + n * (chunk / kMid)) * sizeof(uint32_t) + 64;
 }
 
 uint32_t chunked_auto_chunk(const DevTable& t, uint64_t len, int device) {
@@ -198,13 +220,20 @@ cudaError_t launch_chunked(const DevTable& t, const uint8_t* text, uint64_t len,
     a.start = t.start;
     a.dead = t.dead;
     a.acc_col = t.ncols * static_cast<uint32_t>(t.esize);
-    uint32_t* sc = static_cast<uint32_t*>(scratch);
+    a.ticket = static_cast<unsigned int*>(scratch);
+    a.first_bad = reinterpret_cast<unsigned long long*>(static_cast<uint8_t*>(scratch) + 8);
+    uint32_t* sc = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(scratch) + 16);
     a.g = sc;
     a.e = sc + a.nranges;
     a.mid = sc + 2 * a.nranges;
     a.accept = accept;
     a.repairs = repairs;
     if (chunk == 0 || chunk % kMid) return cudaErrorInvalidValue;
+    {
+        const unsigned long long init[2] = {0ull, ~0ull};   // ticket (low word) | first_bad
+        cudaError_t e = cudaMemcpyAsync(scratch, init, sizeof(init), cudaMemcpyHostToDevice, st);
+        if (e != cudaSuccess) return e;
+    }
     if (t.esize == 2) return t.cls ? run<uint16_t, true>(t, a, device, st) : run<uint16_t, false>(t, a, device, st);
     return t.cls ? run<uint32_t, true>(t, a, device, st) : run<uint32_t, false>(t, a, device, st);
 }
