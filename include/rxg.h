@@ -126,7 +126,8 @@ int rxg_heap_info_get(const rxg_heap* h, rxg_heap_info* info);
  * for `delimiter`-separated lines and re-place the shared-memory table rows
  * so concurrent lanes in different states hit different banks. Changes
  * speed only, never results. rxg_match_batch_host tunes itself from the
- * head of its buffer on first use. */
+ * head of its buffer on first use. delimiter = -1: the sample is one long
+ * string (placement of the chunk-parallel single-string table). */
 int rxg_heap_tune(rxg_heap* h, const uint8_t* sample, uint64_t len, int32_t delimiter);
 
 /* Derived tables of the position form, for tests/tools.
@@ -168,7 +169,7 @@ typedef struct rxg_one_opts {
                                          (rx::ParStats, parallel.hpp:52-58) */
     uint32_t* d_trace;                /* ROUNDS: per symbol the next schedule as (N+1)-bit rows, bit N = null;
                                          zeroed by the caller (test_parallel.cpp:114-137) */
-    uint32_t chunk;                   /* CHUNKED: bytes per range (multiple of 64), 0 = auto */
+    uint32_t chunk;                   /* CHUNKED: bytes per range (multiple of 256), 0 = auto */
     uint32_t lookback;                /* CHUNKED: bytes walked before a range to guess its entry state (0 = 64) */
     unsigned long long* d_repairs;    /* CHUNKED: ranges re-walked by the in-order repair pass */
 } rxg_one_opts;

@@ -64,6 +64,8 @@ struct TableSlot {
     LtTable lt;   // TMA line layout (delimited slots only; lt.ok false if it does not fit)
     DevTable abs;  // plain slot: entries rebased to absolute shared addresses (fixed-stride kernel)
     void* d_abs = nullptr;
+    LtTable chunk_lt;   // plain slot: TMA chunk-parallel layout (chunk_lt.ok false if it does not fit)
+    void* d_chunk = nullptr;
 };
 
 constexpr int32_t kMaxDfaStates = 16384;
@@ -98,6 +100,7 @@ struct rxg_heap {
         DeviceGuard g(device);
         if (plain && plain->dptr) cudaFree(plain->dptr);
         if (plain && plain->d_abs) cudaFree(plain->d_abs);
+        if (plain && plain->d_chunk) cudaFree(plain->d_chunk);
         for (auto& kv : lines) {
             if (kv.second->dptr) cudaFree(kv.second->dptr);
             if (kv.second->lt.d_lo) cudaFree(kv.second->lt.d_lo);
@@ -228,6 +231,23 @@ int pernode_tables(rxg_heap* h, const PernodeTables** out) {
     return RXG_OK;
 }
 
+// (Re)build the TMA chunk-parallel table of the plain slot (caller holds h->mu).
+int build_chunk_lt(rxg_heap* h) {
+    auto f = h->line_freq.find(-1);
+    LtTable lt = make_chunk_tma_table(h->prog, h->dfa, f == h->line_freq.end() ? nullptr : &f->second);
+    void* d = nullptr;
+    if (lt.ok && static_cast<int>(lt.smem_table_end - kLtSmemBase) + 150 * 1024 <= h->smem_limit) {
+        RXG_CUDA(cudaMalloc(&d, lt.lo.size()));
+        RXG_CUDA(cudaMemcpy(d, lt.lo.data(), lt.lo.size(), cudaMemcpyHostToDevice));
+    } else {
+        lt.ok = false;
+    }
+    if (h->plain->d_chunk) cudaFree(h->plain->d_chunk);
+    h->plain->d_chunk = d;
+    h->plain->chunk_lt = std::move(lt);
+    return RXG_OK;
+}
+
 int plain_table(rxg_heap* h, const DevTable** out, const DevTable** abs_out = nullptr) {
     std::lock_guard<std::mutex> lk(h->mu);
     if (!h->plain) {
@@ -250,6 +270,7 @@ int plain_table(rxg_heap* h, const DevTable** out, const DevTable** abs_out = nu
             h->plain->abs = h->plain->dev;
             h->plain->abs.img = h->plain->d_abs;
         }
+        if (int rc = build_chunk_lt(h)) return rc;
     }
     *out = &h->plain->dev;
     if (abs_out) *abs_out = h->plain->d_abs ? &h->plain->abs : nullptr;
@@ -648,9 +669,17 @@ int rxg_host_emulate_batch(const rxg_heap* h, const uint8_t* text, uint64_t len,
 }
 
 int rxg_heap_tune(rxg_heap* h, const uint8_t* sample, uint64_t len, int32_t delimiter) {
-    if (!h || (!sample && len) || delimiter < 0 || delimiter > 255) return fail(RXG_EINVAL, "bad arguments");
+    if (!h || (!sample && len) || delimiter < -1 || delimiter > 255) return fail(RXG_EINVAL, "bad arguments");
     if (!h->dfa_ok) return RXG_OK;
     std::lock_guard<std::mutex> lk(h->mu);
+    if (delimiter < 0) {   // one long string: placement of the chunk-parallel table
+        h->line_freq[-1] = lt_sample_freq_plain(h->prog, h->dfa, sample, len);
+        if (h->plain && h->device >= 0) {
+            DeviceGuard g(h->device);
+            return build_chunk_lt(h);
+        }
+        return RXG_OK;
+    }
     h->line_freq[delimiter] = lt_sample_freq(h->prog, h->dfa, static_cast<uint8_t>(delimiter), sample, len);
     auto it = h->lines.find(delimiter);
     if (it != h->lines.end() && it->second->lt.ok && h->device >= 0) {
@@ -723,6 +752,20 @@ int rxg_match_one_ex(rxg_heap* h, const uint8_t* d_bytes, uint64_t len, int engi
     case RXG_ENGINE_CHUNKED: {
         const DevTable* t = nullptr;
         if (int rc = plain_table(h, &t)) return rc;
+        static const bool no_tma = std::getenv("RXG_NO_TMA") != nullptr;
+        if (h->plain->chunk_lt.ok && !no_tma) {
+            uint32_t chunk = o.chunk ? o.chunk : chunked_tma_auto_chunk(len, h->device);
+            if (chunk % 256) return fail(RXG_EINVAL, "chunk must be a multiple of 256 on the TMA path");
+            void* scratch = nullptr;
+            RXG_CUDA(cudaMallocAsync(&scratch, chunked_tma_scratch_bytes(len, chunk), st));
+            const cudaError_t e = launch_chunked_tma(h->plain->chunk_lt, h->plain->d_chunk, d_bytes, len, chunk,
+                                                     o.lookback ? o.lookback : 64, scratch, d_accept, o.d_repairs,
+                                                     h->device, st);
+            cudaFreeAsync(scratch, st);
+            if (e != cudaSuccess) return cuda_fail(e, "launch_chunked_tma");
+            g_launches = 2;
+            return RXG_OK;
+        }
         uint32_t chunk = o.chunk ? o.chunk : chunked_auto_chunk(*t, len, h->device);
         if (chunk % 64) return fail(RXG_EINVAL, "chunk must be a multiple of 64");
         const uint32_t lookback = o.lookback ? o.lookback : 64;

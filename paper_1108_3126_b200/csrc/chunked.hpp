@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include "launch.hpp"
+#include "lines_tma.hpp"
 
 namespace rxg {
 
@@ -14,5 +15,12 @@ uint32_t chunked_auto_chunk(const DevTable& t, uint64_t len, int device);
 // scratch: chunked_scratch_bytes(len, chunk) device bytes. repairs: device u64 (nullable).
 cudaError_t launch_chunked(const DevTable& t, const uint8_t* text, uint64_t len, uint32_t chunk, uint32_t lookback,
                            void* scratch, int32_t* accept, unsigned long long* repairs, int device, cudaStream_t st);
+
+// TMA-staged variant (tables from make_chunk_tma_table; d_img = device copy of t.lo).
+uint32_t chunked_tma_auto_chunk(uint64_t len, int device);
+size_t chunked_tma_scratch_bytes(uint64_t len, uint32_t chunk);
+cudaError_t launch_chunked_tma(const LtTable& t, const void* d_img, const uint8_t* text, uint64_t len, uint32_t chunk,
+                               uint32_t lookback, void* scratch, int32_t* accept, unsigned long long* repairs,
+                               int device, cudaStream_t st);
 
 }  // namespace rxg

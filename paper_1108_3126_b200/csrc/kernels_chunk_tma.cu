@@ -1,0 +1,362 @@
+// Chunk-parallel walk of one long string on the TMA-staged data path
+// (RXG_ENGINE_CHUNKED; the algorithm of kernels_chunked.cu, the data path of
+// kernels_lines_tma.cu).
+//
+// The string is viewed as [rows][chunk]; lane-owned rows ("ranges") stream
+// through a 3-stage shared-memory ring of 32-byte column slices (2-D TMA,
+// SWIZZLE_32B). Each range first guesses its entry state by walking the
+// `lookback` bytes before it from the start state (direct loads), then walks
+// its own bytes from the ring, recording the state every kMidT bytes and at
+// its end. The last CTA to finish checks every range boundary in parallel;
+// an in-order repair pass (one warp) re-walks only ranges whose guess was
+// wrong, stopping as soon as the re-walk meets the recorded trajectory.
+// Exact for every pattern.
+#include <cstdlib>
+#include <cstring>
+
+#include "chunked.hpp"
+#include "tma_common.cuh"
+
+namespace rxg {
+
+namespace tma {
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return static_cast<PFN_cuTensorMapEncodeTiled_v12000>(nullptr);
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }();
+    return fn;
+}
+
+CUresult make_map(CUtensorMap* map, const uint8_t* text, uint64_t rows, uint32_t chunk, uint32_t slice,
+                  uint32_t box_rows) {
+    auto enc = encode_fn();
+    if (!enc) return CUDA_ERROR_NOT_SUPPORTED;
+    const cuuint64_t dims[2] = {chunk, rows};
+    const cuuint64_t strides[1] = {chunk};
+    const cuuint32_t box[2] = {slice, box_rows};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUtensorMapSwizzle sw = slice == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                  : slice == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                  : slice == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE;
+    return enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(text), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+}
+
+}  // namespace tma
+
+namespace {
+
+constexpr int kWarps = 24, kChains = 2, kRows = 32 * kChains, kStages = 3;
+constexpr uint32_t kSlice = 32, kStageBytes = kRows * kSlice;
+constexpr uint32_t kMidT = 256;   // trajectory checkpoint period (bytes)
+
+struct Args {
+    const uint8_t* text;
+    uint64_t len;
+    uint64_t rows;      // full ranges in the tensor map; range `rows` (if any) is the remainder
+    uint64_t nranges;
+    uint64_t tiles;
+    uint32_t chunk;
+    uint32_t lookback;
+    const uint4* img;
+    uint32_t img_words;
+    uint32_t bar_addr;
+    uint32_t stage_addr[kWarps * kStages];
+    uint32_t start, row_bytes, cmap_addr, acc_off;
+    uint32_t* g;
+    uint32_t* e;
+    uint32_t* mid;      // nranges x (chunk / kMidT)
+    unsigned int* ticket;
+    unsigned long long* first_bad;
+    int32_t* accept;
+    unsigned long long* repairs;
+};
+
+template <bool CLS>
+__device__ __forceinline__ uint32_t stepb(const Args& a, uint32_t s, uint32_t b) {
+    return tma::step<CLS>(s, b, a.row_bytes, a.cmap_addr);
+}
+
+// Walk [lo, hi) with direct loads.
+template <bool CLS>
+__device__ uint32_t walk(const Args& a, uint32_t s, uint64_t lo, uint64_t hi) {
+    uint64_t p = lo;
+    for (; p < hi && (p & 15); ++p) s = stepb<CLS>(a, s, a.text[p]);
+    for (; p + 16 <= hi; p += 16) {
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(a.text + p));
+#pragma unroll
+        for (int w = 0; w < 4; ++w)
+#pragma unroll
+            for (int k = 0; k < 4; ++k) s = stepb<CLS>(a, s, __byte_perm(tma::word_of(v, w), 0, 0x4440 + k));
+    }
+    for (; p < hi; ++p) s = stepb<CLS>(a, s, a.text[p]);
+    return s;
+}
+
+__device__ __forceinline__ void load_image(const Args& a, uint8_t* sm) {
+    for (uint32_t i = threadIdx.x; i < a.img_words; i += blockDim.x) reinterpret_cast<uint4*>(sm)[i] = a.img[i];
+}
+
+template <bool CLS>
+__device__ uint32_t entry_guess(const Args& a, uint64_t r) {
+    const uint64_t c0 = r * a.chunk;
+    return r == 0 ? a.start : walk<CLS>(a, a.start, c0 > a.lookback ? c0 - a.lookback : 0, c0);
+}
+
+template <bool CLS>
+__global__ void __launch_bounds__(kWarps * 32) k_chunk_tma(const __grid_constant__ Args a,
+                                                           const __grid_constant__ CUtensorMap map) {
+    extern __shared__ __align__(1024) uint8_t sm[];
+    if (static_cast<uint32_t>(__cvta_generic_to_shared(sm)) != kLtSmemBase) __trap();
+    load_image(a, sm);
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t bar0 = a.bar_addr + warp * kStages * 8;
+    if (lane == 0) {
+        for (int st = 0; st < kStages; ++st) tma::mbar_init(bar0 + st * 8, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const uint32_t per = a.chunk / kMidT;
+    // the remainder range (past the last full row) walks with direct loads
+    if (blockIdx.x == 0 && threadIdx.x == 0 && a.nranges > a.rows) {
+        const uint64_t r = a.rows, c0 = r * a.chunk;
+        uint32_t s = entry_guess<CLS>(a, r);
+        a.g[r] = s;
+        uint32_t k = 0;
+        for (uint64_t p = c0; p < a.len; p += kMidT, ++k) {
+            s = walk<CLS>(a, s, p, min(p + kMidT, a.len));
+            a.mid[r * per + k] = s;
+        }
+        a.e[r] = s;
+    }
+    uint32_t phase = 0;
+    const uint32_t ncol = a.chunk / kSlice;
+    const uint32_t* stage = a.stage_addr + warp * kStages;
+    for (uint64_t tile = static_cast<uint64_t>(blockIdx.x) * kWarps + warp; tile < a.tiles;
+         tile += static_cast<uint64_t>(gridDim.x) * kWarps) {
+        const uint64_t row0 = tile * kRows;
+        if (lane == 0) {
+            const uint32_t pro = ncol < kStages ? ncol : kStages;
+            for (uint32_t st = 0; st < pro; ++st)
+                tma::issue<kStageBytes>(&map, stage[st], bar0 + st * 8, static_cast<int32_t>(st * kSlice),
+                                        static_cast<int32_t>(row0));
+        }
+        uint32_t s[kChains];
+        bool valid[kChains];
+#pragma unroll
+        for (int j = 0; j < kChains; ++j) {
+            const uint64_t r = row0 + j * 32 + lane;
+            valid[j] = r < a.rows;
+            s[j] = valid[j] ? entry_guess<CLS>(a, r) : a.start;
+            if (valid[j]) a.g[r] = s[j];
+        }
+        for (uint32_t col = 0; col < ncol; ++col) {
+            const uint32_t st = col % kStages;
+            tma::mbar_wait(bar0 + st * 8, (phase >> st) & 1u);
+            phase ^= 1u << st;
+#pragma unroll
+            for (int g = 0; g < 2; ++g) {
+                uint4 v[kChains];
+#pragma unroll
+                for (int j = 0; j < kChains; ++j) {
+                    const uint32_t r = j * 32 + lane;
+                    v[j] = tma::lds128(stage[st] + r * kSlice + (tma::granule<kSlice>(r, g) << 4));
+                }
+#pragma unroll
+                for (int w = 0; w < 4; ++w)
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+#pragma unroll
+                        for (int j = 0; j < kChains; ++j)
+                            s[j] = stepb<CLS>(a, s[j], __byte_perm(tma::word_of(v[j], w), 0, 0x4440 + k));
+            }
+            __syncwarp();
+            if (lane == 0 && col + kStages < ncol) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                tma::issue<kStageBytes>(&map, stage[st], bar0 + st * 8, static_cast<int32_t>((col + kStages) * kSlice),
+                                        static_cast<int32_t>(row0));
+            }
+            if (((col + 1) * kSlice) % kMidT == 0) {
+#pragma unroll
+                for (int j = 0; j < kChains; ++j)
+                    if (valid[j]) a.mid[(row0 + j * 32 + lane) * per + ((col + 1) * kSlice) / kMidT - 1] = s[j];
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < kChains; ++j)
+            if (valid[j]) a.e[row0 + j * 32 + lane] = s[j];
+    }
+    // last CTA: parallel boundary check (flag word after the mbarriers: no
+    // static shared memory, which would move the dynamic window off 0x400)
+    uint32_t* last = reinterpret_cast<uint32_t*>(sm + (a.bar_addr + kWarps * kStages * 8 - kLtSmemBase));
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        *last = atomicAdd(a.ticket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!*last) return;
+    __threadfence();
+    unsigned long long bad = ~0ull;
+    for (uint64_t j = 1 + threadIdx.x; j < a.nranges; j += blockDim.x)
+        if (a.g[j] != a.e[j - 1]) {
+            bad = j;
+            break;
+        }
+    if (bad != ~0ull) atomicMin(a.first_bad, bad);
+}
+
+// In-order repair from the first wrong guess (one warp), then the answer.
+template <bool CLS>
+__global__ void __launch_bounds__(32) k_chunk_tma_fix(const __grid_constant__ Args a) {
+    extern __shared__ __align__(1024) uint8_t sm[];
+    if (static_cast<uint32_t>(__cvta_generic_to_shared(sm)) != kLtSmemBase) __trap();
+    const unsigned long long fb0 = *a.first_bad;
+    if (fb0 == ~0ull) {   // every guess was right: the answer is the last range's exit state
+        if (threadIdx.x == 0) {
+            const uint32_t s = a.nranges ? a.e[a.nranges - 1] : a.start;
+            const uint32_t off = CLS ? 1024 + s * a.row_bytes + a.acc_off : s - kLtSmemBase + a.acc_off;
+            *a.accept = reinterpret_cast<const uint16_t*>(reinterpret_cast<const uint8_t*>(a.img) + off)[0];
+            if (a.repairs) *a.repairs = 0;
+        }
+        return;
+    }
+    load_image(a, sm);
+    __syncwarp();
+    const uint32_t lane = threadIdx.x;
+    const uint32_t per = a.chunk / kMidT;
+    unsigned long long repairs = 0;
+    const unsigned long long fb = *a.first_bad;
+    uint32_t exact = a.nranges == 0 ? a.start : (fb == ~0ull ? a.e[a.nranges - 1] : a.e[fb - 1]);
+    for (uint64_t base = fb == ~0ull ? a.nranges : fb; base < a.nranges; base += 32) {
+        uint64_t j = base;
+        while (j < a.nranges && j < base + 32) {
+            const uint64_t jj = j + lane;
+            const bool ok = jj >= a.nranges || jj >= base + 32 || (jj == j ? a.g[jj] == exact : a.g[jj] == a.e[jj - 1]);
+            const uint32_t bad = __ballot_sync(0xFFFFFFFFu, !ok);
+            if (!bad) {
+                const uint64_t lastr = min(base + 32, a.nranges) - 1;
+                exact = a.e[lastr];
+                j = lastr + 1;
+                break;
+            }
+            const uint64_t r = j + (__ffs(bad) - 1);
+            const uint32_t entry = r == j ? exact : a.e[r - 1];
+            uint32_t s = entry;
+            if (lane == 0) {
+                const uint64_t c0 = r * a.chunk, c1 = min(c0 + a.chunk, a.len);
+                uint32_t* mid = a.mid + r * per;
+                uint32_t k = 0;
+                for (uint64_t p = c0; p < c1; p += kMidT, ++k) {
+                    s = walk<CLS>(a, s, p, min(p + kMidT, c1));
+                    if (s == mid[k]) {
+                        s = a.e[r];
+                        break;
+                    }
+                    mid[k] = s;
+                }
+                a.g[r] = entry;
+                a.e[r] = s;
+                ++repairs;
+            }
+            __syncwarp();
+            exact = __shfl_sync(0xFFFFFFFFu, s, 0);
+            j = r + 1;
+        }
+    }
+    if (lane == 0) {
+        const uint32_t acc_addr = CLS ? kLtSmemBase + 1024 + exact * a.row_bytes + a.acc_off : exact + a.acc_off;
+        *a.accept = static_cast<int32_t>(tma::lds16(acc_addr));
+        if (a.repairs) *a.repairs = repairs;
+    }
+}
+
+uint32_t align_up(uint32_t x, uint32_t a) { return (x + a - 1) / a * a; }
+
+template <bool CLS>
+cudaError_t run(const LtTable& t, Args& a, int device, cudaStream_t st) {
+    // stage ring after the table image, mbarriers after the ring
+    uint32_t p = align_up(t.smem_table_end, 1024);
+    for (int k = 0; k < kWarps * kStages; ++k, p += kStageBytes) a.stage_addr[k] = p;
+    a.bar_addr = align_up(p, 8);
+    const uint32_t smem = a.bar_addr + kWarps * kStages * 8 + 16 - kLtSmemBase;
+    const uint32_t fix_smem = t.lo_bytes;
+    CUtensorMap map;
+    std::memset(&map, 0, sizeof(map));
+    if (a.rows > 0 && tma::make_map(&map, a.text, a.rows, a.chunk, kSlice, kRows) != CUDA_SUCCESS)
+        return cudaErrorInvalidValue;
+    cudaError_t e = cudaFuncSetAttribute(k_chunk_tma<CLS>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(k_chunk_tma_fix<CLS>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(fix_smem));
+    if (e != cudaSuccess) return e;
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    const uint64_t want = (a.tiles + kWarps - 1) / kWarps;
+    const int grid = static_cast<int>(want == 0 ? 1 : (want < static_cast<uint64_t>(sms) ? want : sms));
+    k_chunk_tma<CLS><<<grid, kWarps * 32, smem, st>>>(a, map);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    k_chunk_tma_fix<CLS><<<1, 32, fix_smem, st>>>(a);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+uint32_t chunked_tma_auto_chunk(uint64_t len, int device) {
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    const uint64_t ranges = static_cast<uint64_t>(sms) * kWarps * kRows;
+    uint64_t c = (len + ranges - 1) / ranges;
+    c = (c + kMidT - 1) / kMidT * kMidT;
+    if (c < kMidT) c = kMidT;
+    return static_cast<uint32_t>(c);
+}
+
+size_t chunked_tma_scratch_bytes(uint64_t len, uint32_t chunk) {
+    const uint64_t n = (len + chunk - 1) / chunk;
+    return 16 + (2 * n + n * (chunk / kMidT)) * sizeof(uint32_t) + 64;
+}
+
+cudaError_t launch_chunked_tma(const LtTable& t, const void* d_img, const uint8_t* text, uint64_t len, uint32_t chunk,
+                               uint32_t lookback, void* scratch, int32_t* accept, unsigned long long* repairs,
+                               int device, cudaStream_t st) {
+    if (chunk == 0 || chunk % kMidT) return cudaErrorInvalidValue;
+    Args a{};
+    a.text = text;
+    a.len = len;
+    a.chunk = chunk;
+    a.lookback = lookback;
+    a.rows = len / chunk;
+    a.nranges = (len + chunk - 1) / chunk;
+    a.tiles = (a.rows + kRows - 1) / kRows;
+    a.img = static_cast<const uint4*>(d_img);
+    a.img_words = t.lo_bytes / 16;
+    a.start = t.start;
+    a.row_bytes = t.row_bytes;
+    a.cmap_addr = t.cmap_addr;
+    a.acc_off = t.acc_off;
+    a.ticket = static_cast<unsigned int*>(scratch);
+    a.first_bad = reinterpret_cast<unsigned long long*>(static_cast<uint8_t*>(scratch) + 8);
+    uint32_t* sc = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(scratch) + 16);
+    a.g = sc;
+    a.e = sc + a.nranges;
+    a.mid = sc + 2 * a.nranges;
+    a.accept = accept;
+    a.repairs = repairs;
+    const unsigned long long init[2] = {0ull, ~0ull};   // ticket | first_bad
+    cudaError_t e = cudaMemcpyAsync(scratch, init, sizeof(init), cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return e;
+    if (len == 0) {
+        // empty string: accept iff the start state accepts; reuse the repair kernel with no ranges
+        return t.cls ? run<true>(t, a, device, st) : run<false>(t, a, device, st);
+    }
+    return t.cls ? run<true>(t, a, device, st) : run<false>(t, a, device, st);
+}
+
+}  // namespace rxg

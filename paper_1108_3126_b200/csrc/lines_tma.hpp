@@ -27,6 +27,7 @@ struct LtTable {
     bool cls = false;
     uint32_t row_bytes = 0, cmap_addr = 0, acc_shift = 15;
     uint32_t hole_lo = 0, hole_hi = 0;   // unused rows inside the table (class layout): stage slots go here
+    uint32_t acc_off = 0;                // plain (chunk) tables: byte offset of a row's accept flag
     std::vector<uint8_t> lo, hi;     // images of [lo_addr, +lo) main rows and [hi_addr, +hi) upper rows
     uint32_t lo_addr = 0, hi_addr = 0;
     uint32_t lo_bytes = 0, hi_bytes = 0;
@@ -42,6 +43,15 @@ struct LtTable {
 LtTable make_lines_tma_table(const Program& p, const Dfa& d, uint8_t delim, const std::vector<double>* freq = nullptr,
                              bool force_class = false);
 std::vector<double> lt_sample_freq(const Program& p, const Dfa& d, uint8_t delim, const uint8_t* sample, uint64_t len);
+// Same for one long string (no delimiter): S x 256 counts.
+std::vector<double> lt_sample_freq_plain(const Program& p, const Dfa& d, const uint8_t* sample, uint64_t len);
+
+// Plain table (no delimiter) for the chunk-parallel single-string kernel:
+// direct layout (accept flag in the high half of column 0) for small DFAs,
+// class layout (accept flag in an extra column) otherwise. freq: S x 256
+// state-by-byte counts of a sample (nullable). Rows start at 0x400; the
+// stage ring goes after smem_table_end.
+LtTable make_chunk_tma_table(const Program& p, const Dfa& d, const std::vector<double>* freq = nullptr);
 
 // Host emulation of the table walk, for CPU tests.
 uint32_t lt_step(const LtTable& t, uint32_t s, uint8_t byte);

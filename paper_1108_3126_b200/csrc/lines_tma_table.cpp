@@ -49,6 +49,16 @@ std::vector<double> lt_sample_freq(const Program& p, const Dfa& d, uint8_t delim
     return f;
 }
 
+std::vector<double> lt_sample_freq_plain(const Program& p, const Dfa& d, const uint8_t* sample, uint64_t len) {
+    std::vector<double> f(static_cast<size_t>(d.n_states) * 256, 0.0);
+    int32_t s = d.start;
+    for (uint64_t i = 0; i < len; ++i) {
+        f[static_cast<size_t>(s) * 256 + sample[i]] += 1.0;
+        s = d.next[static_cast<size_t>(s) * static_cast<size_t>(d.n_classes) + p.byte_class[sample[i]]];
+    }
+    return f;
+}
+
 std::vector<uint32_t> lt_place_rows(const std::vector<double>& f, uint32_t nrows) {
     // 32-bin bank histograms per row (byte b of a row sits in bank (offset + b) mod 32)
     std::vector<std::array<double, 32>> H(nrows);
@@ -293,6 +303,72 @@ LtTable make_lines_tma_table(const Program& p, const Dfa& d, uint8_t delim, cons
     std::memcpy(&t.hi[0], &t.lo[t.start - t.lo_addr], R);   // START_A = start row
 
     t.smem_table_end = kLtAccAddr + t.hi_bytes;
+    t.ok = true;
+    return t;
+}
+
+LtTable make_chunk_tma_table(const Program& p, const Dfa& d, const std::vector<double>* freq) {
+    LtTable t;
+    const uint32_t S = static_cast<uint32_t>(d.n_states);
+    auto next = [&](uint32_t s, uint32_t c) {
+        return static_cast<uint32_t>(d.next[static_cast<size_t>(s) * static_cast<size_t>(d.n_classes) + c]);
+    };
+    t.lo_addr = kLtSmemBase;
+    if (S <= kLtDirectMaxStates) {
+        // direct: rows of 256 four-byte columns at chosen bank offsets
+        const uint32_t R = kLtRowBytes;
+        std::vector<uint32_t> off;
+        if (freq) off = lt_place_rows(*freq, S);
+        else for (uint32_t r = 0; r < S; ++r) off.push_back((r * 9u) & 31u);
+        std::vector<uint32_t> addr(S);
+        uint32_t cur = kLtSmemBase;
+        for (uint32_t r = 0; r < S; ++r) {
+            addr[r] = cur + ((off[r] * 4u + 128u - (cur & 127u)) & 127u);
+            cur = addr[r] + R;
+        }
+        if (cur > 0x10000u) return t;
+        t.lo_bytes = align_up(cur - kLtSmemBase, 16);
+        t.lo.assign(t.lo_bytes, 0);
+        for (uint32_t s = 0; s < S; ++s) {
+            for (int b = 0; b < 256; ++b)
+                put16(t.lo, addr[s] - kLtSmemBase + kLtColBytes * static_cast<uint32_t>(b), addr[next(s, p.byte_class[b])]);
+            put16(t.lo, addr[s] - kLtSmemBase + 2u, d.accept[s]);   // high half of column 0
+        }
+        t.start = addr[static_cast<uint32_t>(d.start)];
+        t.acc_off = 2;
+    } else {
+        t.cls = true;
+        const uint32_t ncols = static_cast<uint32_t>(p.n_classes) + 1;   // + the accept column
+        uint32_t rb = align_up(ncols * 2u, 4u);
+        if (((rb / 4u) & 1u) == 0) rb += 4;
+        t.row_bytes = rb;
+        t.cmap_addr = kLtSmemBase;
+        const uint32_t rows_addr = kLtSmemBase + 1024;
+        t.lo_bytes = align_up(1024 + S * rb, 16);
+        if (kLtSmemBase + t.lo_bytes > 160u * 1024u || S > 0xFFFFu) return t;
+        t.lo.assign(t.lo_bytes, 0);
+        for (int b = 0; b < 256; ++b) {
+            const uint32_t v = rows_addr + static_cast<uint32_t>(p.byte_class[b]) * 2u;
+            std::memcpy(&t.lo[static_cast<size_t>(b) * 4], &v, 4);
+        }
+        std::vector<uint32_t> R(S);
+        if (freq) {
+            std::vector<double> f2(static_cast<size_t>(S) * 256);
+            std::copy(freq->begin(), freq->begin() + static_cast<std::ptrdiff_t>(f2.size()), f2.begin());
+            R = number_states(p, d, 0xFF, &f2, S, rows_addr / 4u, rb / 4u, ncols);   // no delimiter column used
+        } else {
+            for (uint32_t s = 0; s < S; ++s) R[s] = s;
+        }
+        for (uint32_t s = 0; s < S; ++s) {
+            for (uint32_t c = 0; c + 1 < ncols; ++c) put16(t.lo, 1024 + R[s] * rb + c * 2u, R[next(s, c)]);
+            put16(t.lo, 1024 + R[s] * rb + (ncols - 1) * 2u, d.accept[s]);
+        }
+        t.start = R[static_cast<uint32_t>(d.start)];
+        t.acc_off = (ncols - 1) * 2u;
+    }
+    t.hi_addr = kLtSmemBase + t.lo_bytes;
+    t.hi_bytes = 0;
+    t.smem_table_end = kLtSmemBase + t.lo_bytes;
     t.ok = true;
     return t;
 }
