@@ -349,8 +349,9 @@ cudaError_t launch_chunked_tma(const LtTable& t, const void* d_img, const uint8_
     a.mid = sc + 2 * a.nranges;
     a.accept = accept;
     a.repairs = repairs;
-    const unsigned long long init[2] = {0ull, ~0ull};   // ticket | first_bad
-    cudaError_t e = cudaMemcpyAsync(scratch, init, sizeof(init), cudaMemcpyHostToDevice, st);
+    // ticket = 0, first_bad = ~0 (device-side memsets: no host staging)
+    cudaError_t e = cudaMemsetAsync(scratch, 0, 8, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(static_cast<uint8_t*>(scratch) + 8, 0xFF, 8, st);
     if (e != cudaSuccess) return e;
     if (len == 0) {
         // empty string: accept iff the start state accepts; reuse the repair kernel with no ranges

@@ -410,7 +410,7 @@ cudaError_t launch(const LtTable& t, const uint8_t* text, uint64_t len, uint8_t 
     return cudaGetLastError();
 }
 
-// Kernel shapes (RXG_LT_SHAPE selects one for tuning runs; 0 is the default).
+// Kernel shapes (RXG_LT_SHAPE selects one for tuning runs; unset = per-layout default).
 // Measured on config (c), 1 GB, B200 (tools/ab_lines.py): 16-byte slices are
 // TMA-request bound (~3.3 TB/s); 32-byte slices with 24 warps x 2 ranges x 3
 // stages reach ~5.05 TB/s; 4 stages / 3 ranges per lane give the same.
@@ -419,10 +419,14 @@ using S1 = Shape<16, 2, 32, 4>;
 using S2 = Shape<24, 2, 32, 2>;
 using S3 = Shape<16, 3, 32, 3>;
 using S4 = Shape<32, 2, 16, 4>;
+using S5 = Shape<16, 4, 32, 2>;
+using S6 = Shape<24, 3, 32, 2>;
+using S7 = Shape<20, 3, 32, 2>;
+using S8 = Shape<12, 4, 32, 3>;
 
 int shape_id() {
     const char* e = std::getenv("RXG_LT_SHAPE");
-    return e ? std::atoi(e) : 0;
+    return e ? std::atoi(e) : -1;
 }
 
 
@@ -433,16 +437,30 @@ cudaError_t launch2(const LtTable& t, const uint8_t* text, uint64_t len, uint8_t
                  : launch<C, false>(t, text, len, delim, chunk, count, st);
 }
 
+// Default shape per layout (measured, config c / d): the direct layout (one
+// LDS per byte) gains from a third range per lane, the class layout (two LDS
+// per byte, ~225 KB with its ring) does not fit it.
+cudaError_t launch_default(const LtTable& t, const uint8_t* text, uint64_t len, uint8_t delim, uint32_t chunk,
+                           unsigned long long* count, cudaStream_t st) {
+    return t.cls ? launch<S0, true>(t, text, len, delim, chunk, count, st)
+                 : launch<S6, false>(t, text, len, delim, chunk, count, st);
+}
+
 }  // namespace
 
 cudaError_t launch_lines_tma(const LtTable& t, const uint8_t* text, uint64_t len, uint8_t delim, uint32_t chunk,
                              unsigned long long* count, cudaStream_t st) {
     switch (shape_id()) {
+    case 0: return launch2<S0>(t, text, len, delim, chunk, count, st);
     case 1: return launch2<S1>(t, text, len, delim, chunk, count, st);
     case 2: return launch2<S2>(t, text, len, delim, chunk, count, st);
     case 3: return launch2<S3>(t, text, len, delim, chunk, count, st);
     case 4: return launch2<S4>(t, text, len, delim, chunk, count, st);
-    default: return launch2<S0>(t, text, len, delim, chunk, count, st);
+    case 5: return launch2<S5>(t, text, len, delim, chunk, count, st);
+    case 6: return launch2<S6>(t, text, len, delim, chunk, count, st);
+    case 7: return launch2<S7>(t, text, len, delim, chunk, count, st);
+    case 8: return launch2<S8>(t, text, len, delim, chunk, count, st);
+    default: return launch_default(t, text, len, delim, chunk, count, st);
     }
 }
 
