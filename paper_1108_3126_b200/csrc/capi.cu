@@ -79,6 +79,7 @@ struct rxg_heap {
     Dfa dfa;
     int smem_limit = 0;
     std::mutex mu;
+    std::mutex host_mu;   // host-buffer calls share the staging buffers and streams
     std::unique_ptr<TableSlot> plain;
     std::map<int, std::unique_ptr<TableSlot>> lines;
     std::map<int, std::vector<double>> line_freq;   // sampled state x byte counts per delimiter (rxg_heap_tune)
@@ -119,6 +120,14 @@ struct rxg_heap {
 
 namespace {
 
+// Pageable H2D cudaMemcpy may return before the DMA lands; the heaps' kernels
+// run on non-blocking streams, so table uploads wait for completion.
+cudaError_t h2d(void* dst, const void* src, size_t n) {
+    cudaError_t e = cudaMemcpy(dst, src, n, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(cudaStreamLegacy);
+    return e;
+}
+
 int upload(rxg_heap* h, std::unique_ptr<TableSlot>& slot, KTable&& kt) {
     if (static_cast<int>(kt.img.size()) > h->smem_limit)
         return fail(RXG_ETOOBIG, "step table needs " + std::to_string(kt.img.size()) +
@@ -126,7 +135,7 @@ int upload(rxg_heap* h, std::unique_ptr<TableSlot>& slot, KTable&& kt) {
     auto s = std::make_unique<TableSlot>();
     s->host = std::move(kt);
     RXG_CUDA(cudaMalloc(&s->dptr, s->host.img.size()));
-    RXG_CUDA(cudaMemcpy(s->dptr, s->host.img.data(), s->host.img.size(), cudaMemcpyHostToDevice));
+    RXG_CUDA(h2d(s->dptr, s->host.img.data(), s->host.img.size()));
     DevTable& d = s->dev;
     const KTable& k = s->host;
     d.img = s->dptr;
@@ -168,7 +177,7 @@ int upload_pack(void** dbuf, std::vector<const void*>& dptrs, const Vs&... vs) {
     size_t off = 0;
     for (auto& p : parts) {
         uint8_t* d = static_cast<uint8_t*>(*dbuf) + off;
-        if (p.second) RXG_CUDA(cudaMemcpy(d, p.first, p.second, cudaMemcpyHostToDevice));
+        if (p.second) RXG_CUDA(h2d(d, p.first, p.second));
         dptrs.push_back(d);
         off += (p.second + 255) & ~size_t(255);
     }
@@ -238,7 +247,7 @@ int build_chunk_lt(rxg_heap* h) {
     void* d = nullptr;
     if (lt.ok && static_cast<int>(lt.smem_table_end - kLtSmemBase) + 150 * 1024 <= h->smem_limit) {
         RXG_CUDA(cudaMalloc(&d, lt.lo.size()));
-        RXG_CUDA(cudaMemcpy(d, lt.lo.data(), lt.lo.size(), cudaMemcpyHostToDevice));
+        RXG_CUDA(h2d(d, lt.lo.data(), lt.lo.size()));
     } else {
         lt.ok = false;
     }
@@ -266,7 +275,7 @@ int plain_table(rxg_heap* h, const DevTable** out, const DevTable** abs_out = nu
                     std::memcpy(&img[r * k.row_bytes + c * 2u], &v, 2);
                 }
             RXG_CUDA(cudaMalloc(&h->plain->d_abs, img.size()));
-            RXG_CUDA(cudaMemcpy(h->plain->d_abs, img.data(), img.size(), cudaMemcpyHostToDevice));
+            RXG_CUDA(h2d(h->plain->d_abs, img.data(), img.size()));
             h->plain->abs = h->plain->dev;
             h->plain->abs.img = h->plain->d_abs;
         }
@@ -285,8 +294,8 @@ int build_lt(rxg_heap* h, int delim, LtTable& out) {
     if (lt.ok && static_cast<int>(lt.smem_table_end - kLtSmemBase) + 64 * 1024 <= h->smem_limit) {
         RXG_CUDA(cudaMalloc(&lt.d_lo, lt.lo.size()));
         RXG_CUDA(cudaMalloc(&lt.d_hi, lt.hi.size()));
-        RXG_CUDA(cudaMemcpy(lt.d_lo, lt.lo.data(), lt.lo.size(), cudaMemcpyHostToDevice));
-        RXG_CUDA(cudaMemcpy(lt.d_hi, lt.hi.data(), lt.hi.size(), cudaMemcpyHostToDevice));
+        RXG_CUDA(h2d(lt.d_lo, lt.lo.data(), lt.lo.size()));
+        RXG_CUDA(h2d(lt.d_hi, lt.hi.data(), lt.hi.size()));
     } else {
         lt.ok = false;
     }
@@ -809,6 +818,7 @@ int rxg_match_one_device(rxg_heap* h, const uint8_t* d_bytes, uint64_t len, int 
 int rxg_match_one(rxg_heap* h, const uint8_t* bytes, uint64_t len, int engine, int32_t* accept) {
     if (int rc = need_device(h, engine != RXG_ENGINE_PERNODE && engine != RXG_ENGINE_ROUNDS)) return rc;
     if (!accept || (!bytes && len)) return fail(RXG_EINVAL, "bad arguments");
+    std::lock_guard<std::mutex> host_lock(h->host_mu);
     DeviceGuard g(h->device);
     if (int rc = ensure_stage(h, std::max<size_t>(len, 16))) return rc;
     if (len) RXG_CUDA(cudaMemcpyAsync(h->d_stage[0], bytes, len, cudaMemcpyHostToDevice, h->stream));
@@ -818,18 +828,18 @@ int rxg_match_one(rxg_heap* h, const uint8_t* bytes, uint64_t len, int engine, i
     return RXG_OK;
 }
 
-int rxg_match_batch_ex(rxg_heap* h, const uint8_t* d_text, uint64_t len, int32_t delimiter, uint32_t stride,
-                       int engine, unsigned long long* d_count, uint8_t* d_results, void* stream) {
-    const bool bitset = engine == RXG_BATCH_BITSET || (engine == RXG_BATCH_AUTO && h && !h->dfa_ok);
-    if (int rc = need_device(h, !bitset)) return rc;
-    if (!d_count || (!d_text && len)) return fail(RXG_EINVAL, "bad arguments");
-    DeviceGuard g(h->device);
-    const cudaStream_t st = static_cast<cudaStream_t>(stream);
-    if (!bitset) return batch_device(h, d_text, len, delimiter, stride, d_count, d_results, st, true);
+namespace {
+
+// Batch on device buffers with engine selection; zero_count = overwrite the
+// count (false: accumulate, for the pieces of the pipelined host path).
+int batch_any(rxg_heap* h, const uint8_t* d_text, uint64_t len, int32_t delimiter, uint32_t stride, int engine,
+              unsigned long long* d_count, uint8_t* d_results, cudaStream_t st, bool zero_count) {
+    const bool bitset = engine == RXG_BATCH_BITSET || (engine == RXG_BATCH_AUTO && !h->dfa_ok);
+    if (!bitset) return batch_device(h, d_text, len, delimiter, stride, d_count, d_results, st, zero_count);
     if (delimiter < 0 || delimiter > 255) return fail(RXG_EUNSUPPORTED, "the bitset batch engine takes delimited lines");
     const PernodeTables* t = nullptr;
     if (int rc = pernode_tables(h, &t)) return rc;
-    RXG_CUDA(cudaMemsetAsync(d_count, 0, sizeof(unsigned long long), st));
+    if (zero_count) RXG_CUDA(cudaMemsetAsync(d_count, 0, sizeof(unsigned long long), st));
     const size_t sb = lines_bitset_scratch_bytes(len);
     void* scratch = nullptr;
     RXG_CUDA(cudaMallocAsync(&scratch, sb, st));
@@ -841,6 +851,18 @@ int rxg_match_batch_ex(rxg_heap* h, const uint8_t* d_text, uint64_t len, int32_t
     return RXG_OK;
 }
 
+}  // namespace
+
+int rxg_match_batch_ex(rxg_heap* h, const uint8_t* d_text, uint64_t len, int32_t delimiter, uint32_t stride,
+                       int engine, unsigned long long* d_count, uint8_t* d_results, void* stream) {
+    const bool bitset = engine == RXG_BATCH_BITSET || (engine == RXG_BATCH_AUTO && h && !h->dfa_ok);
+    if (int rc = need_device(h, !bitset)) return rc;
+    if (!d_count || (!d_text && len)) return fail(RXG_EINVAL, "bad arguments");
+    DeviceGuard g(h->device);
+    return batch_any(h, d_text, len, delimiter, stride, engine, d_count, d_results, static_cast<cudaStream_t>(stream),
+                     true);
+}
+
 int rxg_match_batch(rxg_heap* h, const uint8_t* d_text, uint64_t len, int32_t delimiter, uint32_t stride,
                     unsigned long long* d_count, uint8_t* d_results, void* stream) {
     return rxg_match_batch_ex(h, d_text, len, delimiter, stride, RXG_BATCH_AUTO, d_count, d_results, stream);
@@ -848,11 +870,13 @@ int rxg_match_batch(rxg_heap* h, const uint8_t* d_text, uint64_t len, int32_t de
 
 int rxg_match_batch_host(rxg_heap* h, const uint8_t* text, uint64_t len, int32_t delimiter, uint32_t stride,
                          uint64_t* count, uint8_t* results) {
-    if (int rc = need_device(h)) return rc;
+    if (int rc = need_device(h, false)) return rc;
+    if (!h->dfa_ok && delimiter < 0) return fail(RXG_ETOOBIG, "memoized step table over the cap (fixed stride needs it)");
+    std::lock_guard<std::mutex> host_lock(h->host_mu);
     if (!count || (!text && len)) return fail(RXG_EINVAL, "bad arguments");
     if (delimiter < 0 && (stride == 0 || len % stride)) return fail(RXG_EINVAL, "fixed stride must divide the buffer length");
     DeviceGuard g(h->device);
-    if (delimiter >= 0 && delimiter <= 255) {
+    if (delimiter >= 0 && delimiter <= 255 && h->dfa_ok) {
         bool tuned;
         {
             std::lock_guard<std::mutex> lk(h->mu);
@@ -893,8 +917,8 @@ int rxg_match_batch_host(rxg_heap* h, const uint8_t* text, uint64_t len, int32_t
         cudaMemcpyAsync(h->d_stage[k], text + b[i], n, cudaMemcpyHostToDevice, h->copy_stream);
         cudaEventRecord(copied[k], h->copy_stream);
         cudaStreamWaitEvent(h->stream, copied[k], 0);
-        rc = batch_device(h, h->d_stage[k], n, delimiter, stride, h->d_count, results ? d_res + res_base[i] : nullptr,
-                          h->stream, false);
+        rc = batch_any(h, h->d_stage[k], n, delimiter, stride, RXG_BATCH_AUTO, h->d_count,
+                       results ? d_res + res_base[i] : nullptr, h->stream, false);
         launches += g_launches;
         cudaEventRecord(consumed[k], h->stream);
     }
@@ -1047,7 +1071,11 @@ int rxg_match_batch_multi(const int* devices, int ndev, const char* pattern, siz
         rc = rxg_heap_create_pattern(pattern, plen, devices[k], &hs[static_cast<size_t>(k)]);
         if (rc) break;
         rxg_heap* h = hs[static_cast<size_t>(k)];
-        if ((rc = need_device(h))) break;
+        if ((rc = need_device(h, false))) break;
+        if (!h->dfa_ok && delimiter < 0) {
+            rc = fail(RXG_ETOOBIG, "memoized step table over the cap (fixed stride needs it)");
+            break;
+        }
         DeviceGuard g(h->device);
         const uint64_t n = off[static_cast<size_t>(k) + 1] - off[static_cast<size_t>(k)];
         if (cudaMalloc(&d_text[static_cast<size_t>(k)], std::max<uint64_t>(n, 16)) != cudaSuccess) {
@@ -1060,9 +1088,20 @@ int rxg_match_batch_multi(const int* devices, int ndev, const char* pattern, siz
             nstr += m;
             cudaMalloc(&d_res[static_cast<size_t>(k)], std::max<uint64_t>(m, 1) + 1);
         }
-        cudaMemcpyAsync(d_text[static_cast<size_t>(k)], text + off[static_cast<size_t>(k)], n, cudaMemcpyHostToDevice, h->stream);
-        rc = batch_device(h, d_text[static_cast<size_t>(k)], n, delimiter, stride, h->d_count, d_res[static_cast<size_t>(k)],
-                          h->stream, true);
+        if (results && !d_res[static_cast<size_t>(k)]) {
+            rc = fail(RXG_ENOMEM, "device allocation failed");
+            break;
+        }
+        if (n) {
+            const cudaError_t e = cudaMemcpyAsync(d_text[static_cast<size_t>(k)], text + off[static_cast<size_t>(k)], n,
+                                                  cudaMemcpyHostToDevice, h->stream);
+            if (e != cudaSuccess) {
+                rc = cuda_fail(e, "shard upload");
+                break;
+            }
+        }
+        rc = batch_any(h, d_text[static_cast<size_t>(k)], n, delimiter, stride, RXG_BATCH_AUTO, h->d_count,
+                       d_res[static_cast<size_t>(k)], h->stream, true);
     }
     if (rc == RXG_OK && ndev > 1) {
         // One all-reduce of the 8-byte count: the only inter-GPU traffic.
@@ -1094,19 +1133,21 @@ int rxg_match_batch_multi(const int* devices, int ndev, const char* pattern, siz
         }
     }
     if (rc == RXG_OK) {
-        rxg_heap* h0 = hs[0];
-        DeviceGuard g(h0->device);
+        // the heaps' streams are non-blocking: read back on them, then wait
         unsigned long long c = 0;
-        cudaMemcpy(&c, h0->d_count, sizeof(c), cudaMemcpyDeviceToHost);
-        *count = c;
-        if (ndev == 1) *count = c;
-        if (results) {
-            for (int k = 0; k < ndev; ++k) {
-                DeviceGuard gk(devices[k]);
-                const uint64_t m = (k + 1 < ndev ? res_base[static_cast<size_t>(k) + 1] : nstr) - res_base[static_cast<size_t>(k)];
-                if (m) cudaMemcpy(results + res_base[static_cast<size_t>(k)], d_res[static_cast<size_t>(k)], m, cudaMemcpyDeviceToHost);
-            }
+        cudaError_t e = cudaSuccess;
+        for (int k = 0; k < ndev && e == cudaSuccess; ++k) {
+            rxg_heap* h = hs[static_cast<size_t>(k)];
+            DeviceGuard gk(h->device);
+            if (k == 0) e = cudaMemcpyAsync(&c, h->d_count, sizeof(c), cudaMemcpyDeviceToHost, h->stream);
+            const uint64_t m = results ? (k + 1 < ndev ? res_base[static_cast<size_t>(k) + 1] : nstr) - res_base[static_cast<size_t>(k)] : 0;
+            if (e == cudaSuccess && m)
+                e = cudaMemcpyAsync(results + res_base[static_cast<size_t>(k)], d_res[static_cast<size_t>(k)], m,
+                                    cudaMemcpyDeviceToHost, h->stream);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
         }
+        if (e != cudaSuccess) rc = cuda_fail(e, "rxg_match_batch_multi readback");
+        *count = c;
     }
     for (int k = 0; k < ndev; ++k) {
         if (!hs[static_cast<size_t>(k)]) continue;

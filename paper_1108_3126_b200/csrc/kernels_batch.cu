@@ -491,50 +491,69 @@ template <int K, bool RES>
 __global__ void __launch_bounds__(1024) k_fixed_abs(const __grid_constant__ FixedAbsArgs a) {
     extern __shared__ __align__(16) uint8_t sm[];
     if (static_cast<uint32_t>(__cvta_generic_to_shared(sm)) != kAbsBase) __trap();
-    for (uint32_t i = threadIdx.x; i < a.img_words; i += blockDim.x) reinterpret_cast<uint4*>(sm)[i] = a.img[i];
-    __syncthreads();
-    uint32_t cnt = 0;
     const uint64_t T = static_cast<uint64_t>(gridDim.x) * blockDim.x;
     const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     const uint32_t nblk = a.stride / 16;
-    for (uint64_t base = 0; base < a.n; base += T * K) {
-        uint32_t s[K];
-        uint64_t idx[K];
+    // first 32 bytes of the K strings of a pass (lanes past the end read string 0)
+    auto fetch = [&](uint64_t base, uint4 (&v)[K][2]) {
 #pragma unroll
         for (int j = 0; j < K; ++j) {
-            idx[j] = base + j * T + tid;
-            s[j] = a.start;
+            const uint64_t idx = base + j * T + tid;
+            const uint8_t* p = a.text + (idx < a.n ? idx : 0) * a.stride;
+            v[j][0] = __ldg(reinterpret_cast<const uint4*>(p));
+            v[j][1] = nblk > 1 ? __ldg(reinterpret_cast<const uint4*>(p + 16)) : make_uint4(0, 0, 0, 0);
         }
-        for (uint32_t i = 0; i < nblk; i += 2) {
-            const bool two = i + 1 < nblk;
+    };
+    // the first pass's input is in flight while the table is copied in
+    uint4 nxt[K][2];
+    fetch(0, nxt);
+    for (uint32_t i = threadIdx.x; i < a.img_words; i += blockDim.x) reinterpret_cast<uint4*>(sm)[i] = a.img[i];
+    __syncthreads();
+    uint32_t cnt = 0;
+    auto walk = [&](uint32_t (&s)[K], const uint4 (&v)[K][2], int halves) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            if (h >= halves) break;
+#pragma unroll
+            for (int w = 0; w < 4; ++w)
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+#pragma unroll
+                    for (int j = 0; j < K; ++j) {
+                        const uint32_t word = w == 0 ? v[j][h].x : (w == 1 ? v[j][h].y : (w == 2 ? v[j][h].z : v[j][h].w));
+                        s[j] = tab16(s[j] + __byte_perm(word, 0, 0x4440 + k) * 2u);
+                    }
+        }
+    };
+    for (uint64_t base = 0; base < a.n; base += T * K) {
+        uint4 cur[K][2];
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+            cur[j][0] = nxt[j][0];
+            cur[j][1] = nxt[j][1];
+        }
+        if (base + T * K < a.n) fetch(base + T * K, nxt);   // next pass in flight during this one
+        uint32_t s[K];
+#pragma unroll
+        for (int j = 0; j < K; ++j) s[j] = a.start;
+        walk(s, cur, nblk > 1 ? 2 : 1);
+        for (uint32_t i = 2; i < nblk; i += 2) {   // strings longer than 32 bytes
             uint4 v[K][2];
 #pragma unroll
             for (int j = 0; j < K; ++j) {
-                const uint8_t* p = a.text + (idx[j] < a.n ? idx[j] : 0) * a.stride + i * 16u;
+                const uint64_t idx = base + j * T + tid;
+                const uint8_t* p = a.text + (idx < a.n ? idx : 0) * a.stride + i * 16u;
                 v[j][0] = __ldg(reinterpret_cast<const uint4*>(p));
-                v[j][1] = two ? __ldg(reinterpret_cast<const uint4*>(p + 16)) : make_uint4(0, 0, 0, 0);
+                v[j][1] = i + 1 < nblk ? __ldg(reinterpret_cast<const uint4*>(p + 16)) : make_uint4(0, 0, 0, 0);
             }
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                if (h == 1 && !two) break;
-#pragma unroll
-                for (int w = 0; w < 4; ++w) {
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-#pragma unroll
-                        for (int j = 0; j < K; ++j) {
-                            const uint32_t word = w == 0 ? v[j][h].x : (w == 1 ? v[j][h].y : (w == 2 ? v[j][h].z : v[j][h].w));
-                            s[j] = tab16(s[j] + __byte_perm(word, 0, 0x4440 + k) * 2u);
-                        }
-                    }
-                }
-            }
+            walk(s, v, i + 1 < nblk ? 2 : 1);
         }
 #pragma unroll
         for (int j = 0; j < K; ++j) {
-            if (idx[j] >= a.n) continue;
+            const uint64_t idx = base + j * T + tid;
+            if (idx >= a.n) continue;
             const uint32_t ok = tab16(s[j] + a.acc_col);
-            if (RES) a.results[idx[j]] = static_cast<uint8_t>(ok);
+            if (RES) a.results[idx] = static_cast<uint8_t>(ok);
             cnt += ok;
         }
     }
@@ -577,7 +596,7 @@ cudaError_t launch_fixed_abs(const DevTable& t, const uint8_t* text, uint64_t n,
     a.count = count;
     a.results = results;
     if (ls) ls->kernels = 1;
-    return results ? run_fixed_abs<4, true>(a, t.img_bytes, st) : run_fixed_abs<4, false>(a, t.img_bytes, st);
+    return results ? run_fixed_abs<2, true>(a, t.img_bytes, st) : run_fixed_abs<2, false>(a, t.img_bytes, st);
 }
 
 }  // namespace rxg

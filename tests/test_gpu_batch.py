@@ -125,6 +125,19 @@ def test_exploding_dfa_falls_back_to_bitset_engine():
     ocount, ores = _oracle(pattern).match_batch(text, 10, 0)
     c, r = _device_batch(m, text, "auto")
     assert c == ocount and np.array_equal(r, ores)
+    # the host-buffer entry point (pipelined pieces) takes the same fallback
+    c, r = m.match_batch(text, delimiter=10, results=True)
+    assert c == ocount and np.array_equal(r, ores)
+
+
+def test_multi_device_entry_single_gpu():
+    """rxg_match_batch_multi over devices=[0]: the sharded entry point with one
+    shard equals the single-heap batch (and the oracle)."""
+    pattern = rx.synth_pattern("c")
+    text = rx.synth_input("c", 4 << 20)
+    ocount, ores = _oracle(pattern).match_batch(text, 10, 0)
+    c, r = rx.match_batch_multi([0], pattern, text, delimiter=10, results=True)
+    assert c == ocount and np.array_equal(r, ores)
 
 
 def test_unicode_literals_all_engines():
