@@ -202,6 +202,29 @@ int rxg_match_batch_ex(rxg_heap* h, const uint8_t* d_text, uint64_t len, int32_t
 int rxg_match_batch_host(rxg_heap* h, const uint8_t* text, uint64_t len, int32_t delimiter,
                          uint32_t stride, uint64_t* count, uint8_t* results);
 
+/* rxg_match_batch_host plus, when utf8_first_bad is non-null, the device
+ * UTF-8 check of every string (rxg_utf8_check) fused into the same pipelined
+ * pass: *utf8_first_bad = offset of the first byte at which rx::decode_utf8
+ * would throw on its string, or UINT64_MAX. This is the whole per-line loop
+ * of `rxvm match` (tools/rxvm.cpp:100-112: getline, decode_utf8, lockstep). */
+int rxg_match_batch_host_ex(rxg_heap* h, const uint8_t* text, uint64_t len, int32_t delimiter,
+                            uint32_t stride, uint64_t* count, uint8_t* results,
+                            uint64_t* utf8_first_bad);
+
+/* Device UTF-8 decode check, exactly rx::decode_utf8 (src/utf8.cpp:16-46)
+ * applied to every string of the buffer (delimiter in [0,127] or -1 with a
+ * fixed stride, as rxg_match_batch; delimiter -1 and stride 0 = the whole
+ * buffer is one string): *d_first_bad (device u64) receives the byte offset
+ * the reference's runtime_error "invalid UTF-8 at byte N" names for the
+ * first failing string (N + the string's offset), or UINT64_MAX when every
+ * string decodes. Asynchronous on `stream`; any alignment. */
+int rxg_utf8_check(int device, const uint8_t* d_text, uint64_t len, int32_t delimiter,
+                   uint32_t stride, uint64_t* d_first_bad, void* stream);
+
+/* Same on a host buffer (synchronous). */
+int rxg_utf8_check_host(int device, const uint8_t* text, uint64_t len, int32_t delimiter,
+                        uint32_t stride, uint64_t* first_bad);
+
 /* Byte-balanced sharding of a host buffer over `ndev` GPUs (split at string
  * boundaries), one stream per device, and one NCCL all-reduce of the int64
  * match count across the devices (the only inter-GPU traffic). */

@@ -296,3 +296,56 @@ uint64_t oracle_match_batch(const oracle_heap* h, const uint8_t* text, uint64_t 
     free(lens);
     return count;
 }
+
+/* rx::decode_utf8 (proj/src/utf8.cpp:16-46) restated: the index of the byte
+ * named by its "invalid UTF-8 at byte N" error, or -1 when it decodes.
+ * Checks in the reference's order: lead class, truncation, continuation
+ * bytes, then overlong / surrogate / > U+10FFFF. */
+int64_t oracle_decode_utf8_error(const uint8_t* s, uint64_t n) {
+    static const uint32_t min_for_len[5] = {0, 0, 0x80, 0x800, 0x10000};
+    uint64_t i = 0;
+    while (i < n) {
+        const uint32_t b0 = s[i];
+        if (b0 < 0x80) {
+            ++i;
+            continue;
+        }
+        uint32_t len, cp;
+        if ((b0 & 0xE0) == 0xC0) { len = 2; cp = b0 & 0x1F; }
+        else if ((b0 & 0xF0) == 0xE0) { len = 3; cp = b0 & 0x0F; }
+        else if ((b0 & 0xF8) == 0xF0) { len = 4; cp = b0 & 0x07; }
+        else return (int64_t)i;
+        if (i + len > n) return (int64_t)i;
+        for (uint32_t k = 1; k < len; ++k) {
+            const uint32_t b = s[i + k];
+            if ((b & 0xC0) != 0x80) return (int64_t)(i + k);
+            cp = (cp << 6) | (b & 0x3F);
+        }
+        if (cp < min_for_len[len]) return (int64_t)i;
+        if (cp > 0x10FFFF || (cp >= 0xD800 && cp <= 0xDFFF)) return (int64_t)i;
+        i += len;
+    }
+    return -1;
+}
+
+/* decode_utf8 over every string of a buffer (the `rxvm match` getline loop,
+ * rxvm.cpp:100-112): global offset of the first failing byte, or UINT64_MAX.
+ * delimiter < 0 with stride 0: the whole buffer is one string. */
+uint64_t oracle_utf8_first_bad(const uint8_t* text, uint64_t len, int32_t delimiter, uint32_t stride) {
+    if (delimiter < 0 && stride == 0) {
+        const int64_t e = oracle_decode_utf8_error(text, len);
+        return e < 0 ? UINT64_MAX : (uint64_t)e;
+    }
+    const uint64_t n = oracle_split(text, len, delimiter, stride, NULL, NULL);
+    uint64_t* starts = (uint64_t*)malloc((n ? n : 1) * sizeof(uint64_t));
+    uint64_t* lens = (uint64_t*)malloc((n ? n : 1) * sizeof(uint64_t));
+    oracle_split(text, len, delimiter, stride, starts, lens);
+    uint64_t bad = UINT64_MAX;
+    for (uint64_t k = 0; k < n && bad == UINT64_MAX; ++k) {
+        const int64_t e = oracle_decode_utf8_error(text + starts[k], lens[k]);
+        if (e >= 0) bad = starts[k] + (uint64_t)e;
+    }
+    free(starts);
+    free(lens);
+    return bad;
+}

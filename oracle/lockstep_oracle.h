@@ -45,6 +45,8 @@ uint64_t oracle_split(const uint8_t* text, uint64_t len, int32_t delimiter, uint
                       uint64_t* lens);
 uint64_t oracle_match_batch(const oracle_heap* h, const uint8_t* text, uint64_t len, int32_t delimiter,
                             uint32_t stride, uint8_t* results, int nthreads);
+int64_t oracle_decode_utf8_error(const uint8_t* s, uint64_t n);
+uint64_t oracle_utf8_first_bad(const uint8_t* text, uint64_t len, int32_t delimiter, uint32_t stride);
 
 #ifdef __cplusplus
 }

@@ -216,4 +216,17 @@ int ref_random_regexes(int count, int max_nodes, const char* alphabet, uint64_t 
     return put_str(s, out, cap);
 }
 
+// rx::decode_utf8 (utf8.cpp:16-46): -1 when it decodes, else N from its
+// runtime_error "invalid UTF-8 at byte N".
+int64_t ref_decode_utf8_error(const uint8_t* s, size_t n) {
+    try {
+        (void)rx::decode_utf8(std::string_view(reinterpret_cast<const char*>(s), n));
+        return -1;
+    } catch (const std::runtime_error& e) {
+        const std::string m = e.what();
+        const size_t at = m.rfind(' ');
+        return at == std::string::npos ? -2 : static_cast<int64_t>(std::stoull(m.substr(at + 1)));
+    }
+}
+
 }  // extern "C"

@@ -74,6 +74,10 @@ _SIG = {
     "rxg_match_batch": (C.c_int, [_P, _P, C.c_uint64, C.c_int32, C.c_uint32, _P, _P, _P]),
     "rxg_match_batch_ex": (C.c_int, [_P, _P, C.c_uint64, C.c_int32, C.c_uint32, C.c_int, _P, _P, _P]),
     "rxg_match_batch_host": (C.c_int, [_P, _P, C.c_uint64, C.c_int32, C.c_uint32, C.POINTER(C.c_uint64), _P]),
+    "rxg_match_batch_host_ex": (C.c_int, [_P, _P, C.c_uint64, C.c_int32, C.c_uint32, C.POINTER(C.c_uint64), _P,
+                                          C.POINTER(C.c_uint64)]),
+    "rxg_utf8_check": (C.c_int, [C.c_int, _P, C.c_uint64, C.c_int32, C.c_uint32, _P, _P]),
+    "rxg_utf8_check_host": (C.c_int, [C.c_int, _P, C.c_uint64, C.c_int32, C.c_uint32, C.POINTER(C.c_uint64)]),
     "rxg_match_batch_multi": (C.c_int, [C.POINTER(C.c_int), C.c_int, C.c_char_p, C.c_size_t, _P, C.c_uint64,
                                         C.c_int32, C.c_uint32, C.POINTER(C.c_uint64), _P]),
     "rxg_match_many": (C.c_int, [C.c_int, C.c_char_p, C.c_int32, _P, C.c_uint64, C.c_int32, C.c_uint32, _P,

@@ -18,6 +18,7 @@
 #include "lines_tma.hpp"
 #include "program.hpp"
 #include "single.hpp"
+#include "utf8.hpp"
 #include "pernode.hpp"
 #include "chunked.hpp"
 #include "many.hpp"
@@ -154,6 +155,13 @@ int upload(rxg_heap* h, std::unique_ptr<TableSlot>& slot, KTable&& kt) {
     d.term_rej = k.term_rej;
     d.delim_col = k.delim_col;
     slot = std::move(s);
+    return RXG_OK;
+}
+
+int ensure_cuda(int device) {
+    int ndev = 0;
+    if (device < 0 || cudaGetDeviceCount(&ndev) != cudaSuccess || device >= ndev)
+        return fail(RXG_ECUDA, "no CUDA device " + std::to_string(device));
     return RXG_OK;
 }
 
@@ -870,7 +878,13 @@ int rxg_match_batch(rxg_heap* h, const uint8_t* d_text, uint64_t len, int32_t de
 
 int rxg_match_batch_host(rxg_heap* h, const uint8_t* text, uint64_t len, int32_t delimiter, uint32_t stride,
                          uint64_t* count, uint8_t* results) {
+    return rxg_match_batch_host_ex(h, text, len, delimiter, stride, count, results, nullptr);
+}
+
+int rxg_match_batch_host_ex(rxg_heap* h, const uint8_t* text, uint64_t len, int32_t delimiter, uint32_t stride,
+                            uint64_t* count, uint8_t* results, uint64_t* utf8_first_bad) {
     if (int rc = need_device(h, false)) return rc;
+    if (utf8_first_bad && delimiter > 127) return fail(RXG_EINVAL, "UTF-8 check needs an ASCII delimiter");
     if (!h->dfa_ok && delimiter < 0) return fail(RXG_ETOOBIG, "memoized step table over the cap (fixed stride needs it)");
     std::lock_guard<std::mutex> host_lock(h->host_mu);
     if (!count || (!text && len)) return fail(RXG_EINVAL, "bad arguments");
@@ -908,6 +922,11 @@ int rxg_match_batch_host(rxg_heap* h, const uint8_t* text, uint64_t len, int32_t
         cudaEventCreateWithFlags(&consumed[i], cudaEventDisableTiming);
     }
     RXG_CUDA(cudaMemsetAsync(h->d_count, 0, sizeof(unsigned long long), h->stream));
+    unsigned long long* d_bad = nullptr;
+    if (utf8_first_bad) {
+        RXG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_bad), sizeof(unsigned long long), h->stream));
+        RXG_CUDA(cudaMemsetAsync(d_bad, 0xFF, sizeof(unsigned long long), h->stream));
+    }
     int rc = RXG_OK;
     int launches = 1;
     for (size_t i = 0; i + 1 < b.size() && rc == RXG_OK; ++i) {
@@ -920,23 +939,69 @@ int rxg_match_batch_host(rxg_heap* h, const uint8_t* text, uint64_t len, int32_t
         rc = batch_any(h, h->d_stage[k], n, delimiter, stride, RXG_BATCH_AUTO, h->d_count,
                        results ? d_res + res_base[i] : nullptr, h->stream, false);
         launches += g_launches;
+        if (rc == RXG_OK && d_bad) {   // strings never straddle pieces, so per-piece checks are exact
+            const cudaError_t e = launch_utf8_check(h->d_stage[k], n, delimiter, delimiter < 0 ? stride : 0, b[i], d_bad,
+                                                    h->device, h->stream);
+            if (e != cudaSuccess) rc = cuda_fail(e, "launch_utf8_check");
+            launches += n ? 1 : 0;
+        }
         cudaEventRecord(consumed[k], h->stream);
     }
     if (rc == RXG_OK) {
         unsigned long long c = 0;
         cudaMemcpyAsync(&c, h->d_count, sizeof(c), cudaMemcpyDeviceToHost, h->stream);
         if (results && nstr) cudaMemcpyAsync(results, d_res, nstr, cudaMemcpyDeviceToHost, h->stream);
+        unsigned long long bad = ~0ull;
+        if (d_bad) cudaMemcpyAsync(&bad, d_bad, sizeof(bad), cudaMemcpyDeviceToHost, h->stream);
         const cudaError_t e = cudaStreamSynchronize(h->stream);
         if (e != cudaSuccess) rc = cuda_fail(e, "match_batch_host");
         *count = c;
+        if (utf8_first_bad) *utf8_first_bad = bad;
     }
     if (d_res) cudaFreeAsync(d_res, h->stream);
+    if (d_bad) cudaFreeAsync(d_bad, h->stream);
     cudaStreamSynchronize(h->stream);
     for (int i = 0; i < 2; ++i) {
         cudaEventDestroy(copied[i]);
         cudaEventDestroy(consumed[i]);
     }
     g_launches = launches;
+    return rc;
+}
+
+int rxg_utf8_check(int device, const uint8_t* d_text, uint64_t len, int32_t delimiter, uint32_t stride,
+                   uint64_t* d_first_bad, void* stream) {
+    if (!d_first_bad || (!d_text && len) || delimiter > 127) return fail(RXG_EINVAL, "bad arguments");
+    if (delimiter < 0 && stride && len % stride) return fail(RXG_EINVAL, "fixed stride must divide the buffer length");
+    if (int rc = ensure_cuda(device)) return rc;
+    DeviceGuard g(device);
+    const cudaStream_t st = static_cast<cudaStream_t>(stream);
+    auto* out = reinterpret_cast<unsigned long long*>(d_first_bad);
+    RXG_CUDA(cudaMemsetAsync(out, 0xFF, sizeof(unsigned long long), st));
+    const cudaError_t e = launch_utf8_check(d_text, len, delimiter, delimiter < 0 ? stride : 0, 0, out, device, st);
+    if (e != cudaSuccess) return cuda_fail(e, "launch_utf8_check");
+    g_launches = len ? 1 : 0;
+    return RXG_OK;
+}
+
+int rxg_utf8_check_host(int device, const uint8_t* text, uint64_t len, int32_t delimiter, uint32_t stride,
+                        uint64_t* first_bad) {
+    if (!first_bad || (!text && len) || delimiter > 127) return fail(RXG_EINVAL, "bad arguments");
+    if (int rc = ensure_cuda(device)) return rc;
+    DeviceGuard g(device);
+    uint8_t* d = nullptr;
+    RXG_CUDA(cudaMalloc(&d, len + 16));
+    cudaError_t e = len ? cudaMemcpy(d + 8, text, len, cudaMemcpyHostToDevice) : cudaSuccess;
+    int rc = RXG_OK;
+    if (e == cudaSuccess) rc = rxg_utf8_check(device, d + 8, len, delimiter, stride, reinterpret_cast<uint64_t*>(d), nullptr);
+    else rc = cuda_fail(e, "upload");
+    if (rc == RXG_OK) {
+        unsigned long long bad = ~0ull;
+        e = cudaMemcpy(&bad, d, sizeof(bad), cudaMemcpyDeviceToHost);
+        if (e != cudaSuccess) rc = cuda_fail(e, "readback");
+        *first_bad = bad;
+    }
+    cudaFree(d);
     return rc;
 }
 

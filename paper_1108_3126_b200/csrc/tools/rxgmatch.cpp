@@ -7,9 +7,12 @@
 // Without: every stdin line (std::getline: '\n' stripped, '\r' kept, a final
 // unterminated line counts) is a candidate; matching lines are echoed in
 // order; same exit codes. Lines are matched in one device pass
-// (rxg_match_batch_host) instead of one engine call per line. As in the
-// reference, a line that is not valid UTF-8 is an error (exit 2) after the
-// matching lines before it have been printed.
+// (rxg_match_batch_host_ex) instead of one engine call per line, with the
+// device UTF-8 check fused into it. As in the reference, a line that is not
+// valid UTF-8 is an error (exit 2, "rxvm: invalid UTF-8 at byte N" with N
+// inside that line, the runtime_error of decode_utf8) after the matching
+// lines before it have been printed.
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -23,33 +26,6 @@
 namespace {
 
 constexpr int kMatch = 0, kNoMatch = 1, kError = 2;   // rxvm.cpp:30-32
-
-// Offset of the first invalid UTF-8 sequence in [p, p+n), or n.
-size_t utf8_invalid_at(const unsigned char* p, size_t n) {
-    size_t i = 0;
-    while (i < n) {
-        const unsigned b0 = p[i];
-        if (b0 < 0x80) {
-            ++i;
-            continue;
-        }
-        int len;
-        unsigned cp;
-        if ((b0 & 0xE0) == 0xC0) { len = 2; cp = b0 & 0x1F; }
-        else if ((b0 & 0xF0) == 0xE0) { len = 3; cp = b0 & 0x0F; }
-        else if ((b0 & 0xF8) == 0xF0) { len = 4; cp = b0 & 0x07; }
-        else return i;
-        if (i + static_cast<size_t>(len) > n) return i;
-        for (int k = 1; k < len; ++k) {
-            if ((p[i + k] & 0xC0) != 0x80) return i;
-            cp = (cp << 6) | (p[i + k] & 0x3F);
-        }
-        static const unsigned kMin[5] = {0, 0, 0x80, 0x800, 0x10000};
-        if (cp < kMin[len] || cp > 0x10FFFF || (cp >= 0xD800 && cp <= 0xDFFF)) return i;
-        i += static_cast<size_t>(len);
-    }
-    return n;
-}
 
 int usage() {
     std::fprintf(stderr, "usage: rxgmatch [--count] [--device N] PATTERN [INPUT...]\n");
@@ -108,23 +84,18 @@ int main(int argc, char** argv) {
         if (k + 1 < lines) return starts[k + 1] - 1;
         return buf.back() == '\n' ? buf.size() - 1 : buf.size();
     };
-    // first line that is not valid UTF-8 (the reference throws there)
-    size_t bad_line = lines;
-    {
-        const size_t bad = utf8_invalid_at(reinterpret_cast<const unsigned char*>(buf.data()), buf.size());
-        if (bad < buf.size())
-            for (size_t k = 0; k < lines; ++k)
-                if (starts[k] <= bad && (k + 1 == lines || bad < starts[k + 1])) bad_line = k;
-    }
     std::vector<uint8_t> res(lines + 1, 0);
-    uint64_t matches = 0;
-    if (rxg_match_batch_host(h, reinterpret_cast<const uint8_t*>(buf.data()), buf.size(), '\n', 0, &matches,
-                             res.data()) != RXG_OK) {
+    uint64_t matches = 0, bad = UINT64_MAX;
+    if (rxg_match_batch_host_ex(h, reinterpret_cast<const uint8_t*>(buf.data()), buf.size(), '\n', 0, &matches,
+                                res.data(), &bad) != RXG_OK) {
         std::fprintf(stderr, "rxvm: %s\n", rxg_last_error());
         rxg_heap_destroy(h);
         return kError;
     }
     rxg_heap_destroy(h);
+    // first line that is not valid UTF-8 (the reference throws there)
+    size_t bad_line = lines;
+    if (bad != UINT64_MAX) bad_line = static_cast<size_t>(std::upper_bound(starts.begin(), starts.end(), bad) - starts.begin()) - 1;
     bool any = false;
     uint64_t shown = 0;
     for (size_t k = 0; k < lines && k < bad_line; ++k) {
@@ -140,7 +111,8 @@ int main(int argc, char** argv) {
     if (count_only) std::printf("%llu\n", static_cast<unsigned long long>(shown));
     if (bad_line < lines) {
         std::fflush(stdout);
-        std::fprintf(stderr, "rxvm: invalid UTF-8 in line %zu\n", bad_line + 1);
+        std::fprintf(stderr, "rxvm: invalid UTF-8 at byte %llu\n",
+                     static_cast<unsigned long long>(bad - starts[bad_line]));
         return kError;
     }
     return any ? kMatch : kNoMatch;

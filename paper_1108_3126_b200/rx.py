@@ -311,11 +311,48 @@ class Matcher:
                                             res.ctypes.data if res is not None else None))
         return cnt.value, (res[:nstr] if res is not None else None)
 
+    def match_batch_utf8(self, text, delimiter: int = 10, stride: int = 0, results: bool = False):
+        """match_batch plus the fused device UTF-8 check of every string (the
+        `rxvm match` loop: getline, decode_utf8, lockstep_accepts) ->
+        (count, results|None, first_bad) with first_bad the byte offset
+        rx::decode_utf8 would name, or None when every string decodes."""
+        p, n, keep = _ptr(text)
+        res = None
+        if results:
+            nstr = count_strings(text, delimiter, stride)
+            res = np.zeros(max(nstr, 1) + 1, np.uint8)
+        cnt = C.c_uint64(0)
+        bad = C.c_uint64(0)
+        _check(L.lib().rxg_match_batch_host_ex(self._h, p, n, delimiter, stride, C.byref(cnt),
+                                               res.ctypes.data if res is not None else None, C.byref(bad)))
+        return cnt.value, (res[:nstr] if res is not None else None), (None if bad.value == 2**64 - 1 else bad.value)
+
 
 def _stream_ptr(stream):
     if stream is None:
         return None
     return C.c_void_p(stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
+
+
+def utf8_check(text, delimiter: int = -1, stride: int = 0, device: int = 0):
+    """Device check of a host buffer against rx::decode_utf8 (utf8.cpp:16-46),
+    each string decoded separately (delimiter/stride as match_batch; -1/0 =
+    one string) -> None when valid, else the offset of the byte decode_utf8
+    names in its "invalid UTF-8 at byte N" error (plus the string's offset)."""
+    p, n, keep = _ptr(text)
+    bad = C.c_uint64(0)
+    _check(L.lib().rxg_utf8_check_host(device, p, n, delimiter, stride, C.byref(bad)))
+    return None if bad.value == 2**64 - 1 else bad.value
+
+
+def utf8_check_device(d_text, nbytes: int, d_first_bad, delimiter: int = -1, stride: int = 0, device: int = 0,
+                      stream=None):
+    """Asynchronous device variant: d_text / d_first_bad are device pointers
+    (ints) or tensors; *d_first_bad = offset or 2**64-1 (int64 -1)."""
+    tp = d_text.data_ptr() if hasattr(d_text, "data_ptr") else d_text
+    bp = d_first_bad.data_ptr() if hasattr(d_first_bad, "data_ptr") else d_first_bad
+    _check(L.lib().rxg_utf8_check(device, C.c_void_p(tp), nbytes, delimiter, stride, C.c_void_p(bp),
+                                  _stream_ptr(stream)))
 
 
 def count_strings(text, delimiter: int = 10, stride: int = 0) -> int:

@@ -42,6 +42,30 @@ def build_oracle(with_ref: bool | None = None) -> None:
 class Oracle:
     """Plain-C restatement of rx::lockstep_accepts over a heap table."""
 
+    @staticmethod
+    def _raw():
+        if not ORACLE_SO.exists():
+            build_oracle(with_ref=False)
+        l = C.CDLL(str(ORACLE_SO))
+        l.oracle_decode_utf8_error.restype = C.c_int64
+        l.oracle_decode_utf8_error.argtypes = [C.c_void_p, C.c_uint64]
+        l.oracle_utf8_first_bad.restype = C.c_uint64
+        l.oracle_utf8_first_bad.argtypes = [C.c_void_p, C.c_uint64, C.c_int32, C.c_uint32]
+        return l
+
+    @staticmethod
+    def decode_utf8_error(b: bytes):
+        """decode_utf8 restated: None or the byte index it throws at."""
+        a = np.frombuffer(bytes(b), np.uint8)
+        r = Oracle._raw().oracle_decode_utf8_error(a.ctypes.data if len(a) else None, len(a))
+        return None if r < 0 else int(r)
+
+    @staticmethod
+    def utf8_first_bad(text, delimiter=-1, stride=0):
+        a = np.ascontiguousarray(np.frombuffer(bytes(text), np.uint8) if not isinstance(text, np.ndarray) else text)
+        r = Oracle._raw().oracle_utf8_first_bad(a.ctypes.data if len(a) else None, len(a), delimiter, stride)
+        return None if r == 2**64 - 1 else int(r)
+
     def __init__(self, heap):
         if not ORACLE_SO.exists():
             build_oracle(with_ref=False)
@@ -200,12 +224,21 @@ class Ref:
                 "ref_run": (C.c_uint64, [P, P, P, C.c_int]),
                 "ref_enumerate": (C.c_int, [C.c_int, C.c_char_p, C.c_char_p, C.c_size_t]),
                 "ref_random_regexes": (C.c_int, [C.c_int, C.c_int, C.c_char_p, C.c_uint64, C.c_char_p, C.c_size_t]),
+                "ref_decode_utf8_error": (C.c_int64, [P, C.c_size_t]),
             }
             for k, (r, a) in sig.items():
                 f = getattr(l, k)
                 f.restype, f.argtypes = r, a
             cls._lib = l
         return cls._lib
+
+    @classmethod
+    def decode_utf8_error(cls, b: bytes):
+        """rx::decode_utf8 itself: None or N of its "invalid UTF-8 at byte N"."""
+        a = np.frombuffer(bytes(b), np.uint8)
+        r = cls.lib().ref_decode_utf8_error(a.ctypes.data if len(a) else None, len(a))
+        assert r != -2
+        return None if r < 0 else int(r)
 
     # ── front end ──
     @classmethod

@@ -67,7 +67,11 @@ def test_invalid_utf8_line_is_an_error_after_earlier_matches():
     r = run(["(a|b)*b"], data)
     assert r.returncode == 2
     assert r.stdout == b"ab\nb\n"
-    assert b"invalid UTF-8" in r.stderr
+    assert r.stderr == b"rxvm: invalid UTF-8 at byte 0\n"   # decode_utf8's message for that line
+    # the byte offset is within the line, as decode_utf8(line) reports it
+    r = run(["(a|b)*b"], b"ab\na\xc3\xa9\xe4\xb8\nb\n")
+    assert r.returncode == 2 and r.stdout == b"ab\n"
+    assert r.stderr == b"rxvm: invalid UTF-8 at byte 3\n"
 
 
 @pytest.mark.gpu
