@@ -61,7 +61,7 @@ extern "C" {
 #define RXG_NODE_STAR 4
 
 /* single-string engines (rxg_match_one*) */
-#define RXG_ENGINE_AUTO 0     /* fastest available */
+#define RXG_ENGINE_AUTO 0     /* memoized step (chunk-parallel) when its table fits, else PERNODE */
 #define RXG_ENGINE_DFA_SEQ 1  /* one thread walks the memoized step table */
 #define RXG_ENGINE_PERNODE 2  /* K1: paper §8 thread-per-node lockstep, bitset form, one CTA */
 #define RXG_ENGINE_ROUNDS 3   /* literal §8 protocol: one thread per heap node, c/n stamps, rounds */

@@ -749,6 +749,7 @@ int rxg_host_emulate_lines_tma(const rxg_heap* h, const uint8_t* text, uint64_t 
 
 int rxg_match_one_ex(rxg_heap* h, const uint8_t* d_bytes, uint64_t len, int engine, int32_t* d_accept,
                      const rxg_one_opts* opts, void* stream) {
+    if (engine == RXG_ENGINE_AUTO && h && !h->dfa_ok) engine = RXG_ENGINE_PERNODE;   // table over the cap
     const bool dfa_engine = engine == RXG_ENGINE_AUTO || engine == RXG_ENGINE_DFA_SEQ || engine == RXG_ENGINE_CHUNKED;
     if (int rc = need_device(h, dfa_engine)) return rc;
     if (!d_accept || (!d_bytes && len)) return fail(RXG_EINVAL, "bad arguments");
@@ -824,7 +825,7 @@ int rxg_match_one_device(rxg_heap* h, const uint8_t* d_bytes, uint64_t len, int 
 }
 
 int rxg_match_one(rxg_heap* h, const uint8_t* bytes, uint64_t len, int engine, int32_t* accept) {
-    if (int rc = need_device(h, engine != RXG_ENGINE_PERNODE && engine != RXG_ENGINE_ROUNDS)) return rc;
+    if (int rc = need_device(h, engine == RXG_ENGINE_DFA_SEQ || engine == RXG_ENGINE_CHUNKED)) return rc;
     if (!accept || (!bytes && len)) return fail(RXG_EINVAL, "bad arguments");
     std::lock_guard<std::mutex> host_lock(h->host_mu);
     DeviceGuard g(h->device);
