@@ -10,8 +10,8 @@
 // per CTA, one CTA per SM (the table plus ring use ~188 KB of shared memory).
 //
 // Step per input byte (the memoized lockstep macro step, see tables.hpp):
-//     b = PRMT(word, k)            extract byte
-//     s = LDS.U16 [s + 4b]         s and the entries are absolute shared addresses
+//     a = IDP.4A(word, 4<<8k, s)   extract byte k, scale by the 4-byte column stride, add row
+//     s = LDS.U16 [a]              s and the entries are absolute shared addresses
 //     n += hi32(s * 2^17)          START_A (the accepted-line-end row) is the only
 //                                  row at >= 0x8000 the main loop can enter
 // Columns are 4 B apart, so the bytes of one row map to banks (row + b) mod 32
@@ -92,8 +92,14 @@ __device__ __forceinline__ uint32_t step_b(const Args& a, uint32_t s, uint32_t b
     else return tab(s + b * kLtColBytes);
 }
 
-template <bool CLS>
+template <bool CLS, bool IDP = false>
 __device__ __forceinline__ uint32_t step(const Args& a, uint32_t s, uint32_t word, int k) {
+    if constexpr (IDP) {
+        // one IDP.4A.U8 extracts byte k, scales it by the column stride and adds the row
+        // (replaces PRMT + IMAD; measured neutral on (c)/(d): the loop is shared-memory bound)
+        if constexpr (CLS) return tab(s * a.row_bytes + lds32(__dp4a(word, 4u << (8 * k), a.cmap_addr)));
+        else return tab(__dp4a(word, static_cast<unsigned>(kLtColBytes) << (8 * k), s));
+    }
     return step_b<CLS>(a, s, __byte_perm(word, 0, 0x4440 + k));
 }
 
@@ -259,7 +265,7 @@ __global__ void __launch_bounds__(C::warps * 32) k_lines_tma(const __grid_consta
                     for (int k = 0; k < 4; ++k)
 #pragma unroll
                         for (int j = 0; j < C::chains; ++j) {
-                            s[j] = step<CLS>(a, s[j], word_of(v[j], w), k);
+                            s[j] = step<CLS, true>(a, s[j], word_of(v[j], w), k);
                             cnt += counted<CLS>(a, s[j]);
                         }
 #pragma unroll
@@ -326,8 +332,9 @@ CUtensorMapSwizzle swizzle_of(int slice) {
 template <class C, bool CLS>
 int per_sm_of(uint32_t smem) {
     int per_sm = 0;
-    cudaFuncSetAttribute(k_lines_tma<C, CLS>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_lines_tma<C, CLS>, C::warps * 32, smem);
+    auto* k = k_lines_tma<C, CLS>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, C::warps * 32, smem);
     return per_sm < 1 ? 1 : per_sm;
 }
 
