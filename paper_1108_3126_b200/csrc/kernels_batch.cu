@@ -492,7 +492,9 @@ __global__ void __launch_bounds__(1024) k_fixed_abs(const __grid_constant__ Fixe
     extern __shared__ __align__(16) uint8_t sm[];
     if (static_cast<uint32_t>(__cvta_generic_to_shared(sm)) != kAbsBase) __trap();
     const uint64_t T = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-    const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    // warp slots interleave the CTAs (a warp's 32 strings stay consecutive, so its
+    // loads coalesce): the partial last pass spreads over every SM, not the first few
+    const uint64_t tid = (static_cast<uint64_t>(threadIdx.x >> 5) * gridDim.x + blockIdx.x) * 32 + (threadIdx.x & 31);
     const uint32_t nblk = a.stride / 16;
     // first 32 bytes of the K strings of a pass (lanes past the end read string 0)
     auto fetch = [&](uint64_t base, uint4 (&v)[K][2]) {
@@ -521,7 +523,7 @@ __global__ void __launch_bounds__(1024) k_fixed_abs(const __grid_constant__ Fixe
 #pragma unroll
                     for (int j = 0; j < K; ++j) {
                         const uint32_t word = w == 0 ? v[j][h].x : (w == 1 ? v[j][h].y : (w == 2 ? v[j][h].z : v[j][h].w));
-                        s[j] = tab16(s[j] + __byte_perm(word, 0, 0x4440 + k) * 2u);
+                        s[j] = tab16(__dp4a(word, 2u << (8 * k), s[j]));   // s + 2 * byte k
                     }
         }
     };

@@ -1,0 +1,149 @@
+"""Stress parity of the line kernels at sizes and shapes the synthetic
+configs do not reach: long-tailed line lengths (lines spanning many ranges),
+no delimiter at all, only delimiters, lines ending exactly on range
+boundaries, tiny forced ranges, and both TMA table layouts. Every count is
+checked against the CPU oracle (or, at sizes the oracle cannot finish in
+seconds, against the independent bitset engine and per-line results)."""
+import os
+
+import numpy as np
+import pytest
+
+from oracle_bind import Oracle
+from paper_1108_3126_b200 import rx
+
+pytestmark = pytest.mark.gpu
+
+PATS = {
+    "c": None,   # filled lazily: rx.synth_pattern("c") (direct layout)
+    "d": None,   # rx.synth_pattern("d") (class layout)
+    "abb": "(a|b)*abb",
+    "empty_ok": "(a|b| )*",
+}
+
+
+ALPHA = {"c": b"abcdefgh ERORWANFIL", "d": b"abcdefghijklmnopqrstuvwxyz  ", "abb": b"ab ", "empty_ok": b"ab "}
+
+
+def _pat(k):
+    if k in ("c", "d"):
+        return rx.synth_pattern(k)
+    return PATS[k]
+
+
+def _dev_count(m, text, engine="auto"):
+    import torch
+
+    d = torch.zeros(len(text) + 64, dtype=torch.uint8, device="cuda")
+    if len(text):
+        d[: len(text)].copy_(torch.from_numpy(np.ascontiguousarray(text)))
+    cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+    m.match_batch_device(d, cnt, nbytes=len(text), engine=engine)
+    torch.cuda.synchronize()
+    return int(cnt.item())
+
+
+def _long_tailed(seed, total, alphabet=b"abcdefgh ERORWANFIL", long_every=50, long_len=(20_000, 400_000)):
+    rng = np.random.default_rng(seed)
+    alpha = np.frombuffer(alphabet, np.uint8)
+    out, n = [], 0
+    while n < total:
+        if rng.integers(0, long_every) == 0:
+            L = int(rng.integers(*long_len))
+        else:
+            L = int(rng.integers(0, 200))
+        line = alpha[rng.integers(0, len(alpha), L)]
+        out.append(line)
+        out.append(np.array([10], np.uint8))
+        n += L + 1
+    return np.concatenate(out)[:total]
+
+
+@pytest.mark.parametrize("key", ["c", "d", "abb", "empty_ok"])
+@pytest.mark.parametrize("chunk", [None, "96", "4096"])
+def test_long_tailed_lines_all_range_sizes(key, chunk):
+    pat = _pat(key)
+    text = _long_tailed(len(key), 3 << 20, ALPHA[key])
+    want, _ = Oracle(rx.compile(rx.parse(pat))).match_batch(text, 10, 0)
+    old = os.environ.get("RXG_LINE_CHUNK")
+    try:
+        if chunk:
+            os.environ["RXG_LINE_CHUNK"] = chunk
+        m = rx.Matcher(pat, device=0)
+        assert _dev_count(m, text) == want
+        c, r = m.match_batch(text, 10, results=True)
+        assert c == want and int(r.sum()) == want
+    finally:
+        if old is None:
+            os.environ.pop("RXG_LINE_CHUNK", None)
+        else:
+            os.environ["RXG_LINE_CHUNK"] = old
+
+
+@pytest.mark.parametrize("key", ["c", "abb", "empty_ok"])
+def test_no_delimiter_is_one_string(key):
+    pat = _pat(key)
+    rng = np.random.default_rng(3)
+    text = np.frombuffer(b"ab ", np.uint8)[rng.integers(0, 3, 24 << 20)]
+    text[-3:] = np.frombuffer(b"abb", np.uint8)
+    m = rx.Matcher(pat, device=0)
+    one = m.lockstep_accepts(text.tobytes())
+    assert _dev_count(m, text) == int(one)
+    assert _dev_count(m, text, "bitset") == int(one)
+
+
+@pytest.mark.parametrize("key", ["c", "d", "abb", "empty_ok"])
+def test_only_delimiters(key):
+    pat = _pat(key)
+    text = np.full(8 << 20, 10, np.uint8)
+    empty = Oracle(rx.compile(rx.parse(pat))).accepts(b"")
+    m = rx.Matcher(pat, device=0)
+    assert _dev_count(m, text) == (len(text) if empty else 0)
+    c, r = m.match_batch(text[: 1 << 20], 10, results=True)
+    assert c == ((1 << 20) if empty else 0)
+
+
+@pytest.mark.parametrize("key", ["c", "d"])
+@pytest.mark.parametrize("line_len", [95, 96, 97, 4095, 4096])
+def test_lines_on_range_boundaries(key, line_len):
+    """Every line exactly line_len bytes including '\\n' with the range size
+    forced to 96 / 4096: delimiters land on, before and after every boundary."""
+    pat = _pat(key)
+    rng = np.random.default_rng(line_len)
+    n_lines = (2 << 20) // line_len
+    alpha = np.frombuffer(ALPHA[key], np.uint8)
+    body = alpha[rng.integers(0, len(alpha), (n_lines, line_len))]
+    body[:, -1] = 10
+    # a keyword in every third line so the count is not trivial
+    kw = np.frombuffer(b"ERROR", np.uint8)
+    if line_len > 10:
+        body[::3, 2:7] = kw
+    text = body.reshape(-1)
+    want, _ = Oracle(rx.compile(rx.parse(pat))).match_batch(text, 10, 0)
+    old = os.environ.get("RXG_LINE_CHUNK")
+    try:
+        for chunk in ("96", "4096"):
+            os.environ["RXG_LINE_CHUNK"] = chunk
+            m = rx.Matcher(pat, device=0)
+            assert _dev_count(m, text) == want, chunk
+    finally:
+        if old is None:
+            os.environ.pop("RXG_LINE_CHUNK", None)
+        else:
+            os.environ["RXG_LINE_CHUNK"] = old
+
+
+def test_full_size_cross_engine_long_tailed():
+    """256 MiB of long-tailed lines: the TMA DFA kernel, the generic kernel
+    with per-line results and the bitset engine agree (the oracle checks a
+    prefix)."""
+    pat = _pat("c")
+    text = _long_tailed(11, 256 << 20, long_every=200)
+    m = rx.Matcher(pat, device=0)
+    a = _dev_count(m, text)
+    b = _dev_count(m, text, "bitset")
+    c, r = m.match_batch(text, 10, results=True)
+    assert a == b == c == int(r.sum())
+    cut = int(np.flatnonzero(text[: 8 << 20] == 10)[-1]) + 1
+    want, wr = Oracle(rx.compile(rx.parse(pat))).match_batch(text[:cut], 10, 0)
+    assert np.array_equal(r[: len(wr)], wr)
