@@ -391,13 +391,25 @@ int batch_device(rxg_heap* h, const uint8_t* d_text, uint64_t len, int32_t delim
         if (reinterpret_cast<uintptr_t>(d_text) & 15) return fail(RXG_EINVAL, "text must be 16-byte aligned");
         TableSlot* slot = nullptr;
         if (int rc = line_table(h, delimiter, &slot)) return rc;
-        if (!d_results && slot->lt.ok) {
+        if (slot->lt.ok && !std::getenv("RXG_NO_LT")) {   // RXG_NO_LT: generic kernel (tests)
             uint32_t chunk = env_chunk();
             if (chunk % lines_tma_slice()) chunk = 0;
-            const cudaError_t e = launch_lines_tma(slot->lt, d_text, len, static_cast<uint8_t>(delimiter), chunk,
-                                                   d_count, st);
-            if (e != cudaSuccess) return cuda_fail(e, "launch_lines_tma");
-            ls.kernels = 1;
+            if (!d_results) {
+                const cudaError_t e = launch_lines_tma(slot->lt, d_text, len, static_cast<uint8_t>(delimiter), chunk,
+                                                       d_count, st);
+                if (e != cudaSuccess) return cuda_fail(e, "launch_lines_tma");
+                ls.kernels = 1;
+            } else if (len) {   // per-line results: range delimiter counts, scan, the same walk
+                chunk = lines_tma_chunk(slot->lt, len, chunk);
+                const size_t sb = lines_tma_results_scratch(len, chunk);
+                void* scratch = nullptr;
+                RXG_CUDA(cudaMallocAsync(&scratch, sb, st));
+                const cudaError_t e = launch_lines_tma_results(slot->lt, d_text, len, static_cast<uint8_t>(delimiter),
+                                                               chunk, d_count, d_results, scratch, sb, st);
+                cudaFreeAsync(scratch, st);
+                if (e != cudaSuccess) return cuda_fail(e, "launch_lines_tma_results");
+                ls.kernels = 3;
+            }
         } else {
             const DevTable* t = &slot->dev;
             uint32_t chunk = env_chunk();

@@ -23,6 +23,7 @@
 // kernels_batch.cu: a range owns the lines starting in it, enters in SKIP
 // unless the previous byte is the delimiter, and finishes its last line
 // through the tail copy of the table with direct global loads.
+#include <cub/device/device_scan.cuh>
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -56,6 +57,17 @@ struct Args {
     uint32_t delim;
     uint32_t row_bytes, cmap_addr, acc_shift;   // class layout
     unsigned long long* count;
+    uint8_t* results;                           // per-line results (RES): line index -> 0/1
+    const unsigned long long* line_base;        // per range: delimiters before its start
+};
+
+// Per-line results bookkeeping of one range (RES): li = index of the line the
+// walk is in (delimiters before the range start, +1 per delimiter), own =
+// whether that line belongs to this range (it started inside it).
+struct LineCursor {
+    uint64_t li;
+    bool own;
+    bool live;   // false for lanes past the last range (they read zero fill)
 };
 
 // Kernel shape: warps per CTA, ranges per lane, bytes per range per stage, ring depth.
@@ -167,10 +179,26 @@ __device__ uint32_t finish_line(const Args& a, uint32_t s, uint64_t pos) {
     return step_b<CLS>(a, s, a.delim);
 }
 
-// A range processed entirely with direct loads (the remainder pieces).
+// One byte of a RES walk: step, count, and at a delimiter record the line
+// that just ended (if owned) and move to the next one.
 template <bool CLS>
-__device__ void range_direct(const Args& a, uint64_t c0, uint64_t c1, uint32_t& cnt) {
+__device__ __forceinline__ uint32_t step_res(const Args& a, uint32_t s, uint32_t b, uint32_t& cnt, LineCursor& lc) {
+    s = step_b<CLS>(a, s, b);
+    const uint32_t c = counted<CLS>(a, s);
+    cnt += c;
+    if (b == a.delim) {
+        if (lc.own) a.results[lc.li] = static_cast<uint8_t>(c);
+        ++lc.li;
+        lc.own = lc.live;
+    }
+    return s;
+}
+
+// A range processed entirely with direct loads (the remainder pieces).
+template <bool CLS, bool RES>
+__device__ void range_direct(const Args& a, uint64_t c0, uint64_t c1, uint64_t range, uint32_t& cnt) {
     uint32_t s = (c0 == 0 || a.text[c0 - 1] == a.delim) ? a.start : a.skip;
+    LineCursor lc{RES ? a.line_base[range] : 0, s == a.start, true};
     uint32_t last = 0;
     uint64_t pos = c0;
     for (; pos + 16 <= c1; pos += 16) {
@@ -179,20 +207,32 @@ __device__ void range_direct(const Args& a, uint64_t c0, uint64_t c1, uint32_t& 
         for (int w = 0; w < 4; ++w)
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-                s = step<CLS>(a, s, word_of(v, w), k);
-                cnt += counted<CLS>(a, s);
+                if constexpr (RES) {
+                    s = step_res<CLS>(a, s, __byte_perm(word_of(v, w), 0, 0x4440 + k), cnt, lc);
+                } else {
+                    s = step<CLS>(a, s, word_of(v, w), k);
+                    cnt += counted<CLS>(a, s);
+                }
             }
         last = v.w >> 24;
     }
     for (; pos < c1; ++pos) {
         last = a.text[pos];
-        s = step_b<CLS>(a, s, last);
-        cnt += counted<CLS>(a, s);
+        if constexpr (RES) {
+            s = step_res<CLS>(a, s, last, cnt, lc);
+        } else {
+            s = step_b<CLS>(a, s, last);
+            cnt += counted<CLS>(a, s);
+        }
     }
-    if (s != a.skip && last != a.delim) cnt += finish_line<CLS>(a, s + a.tail_delta, c1) == a.term_acc;
+    if (s != a.skip && last != a.delim) {
+        const uint32_t ok = finish_line<CLS>(a, s + a.tail_delta, c1) == a.term_acc;
+        cnt += ok;
+        if constexpr (RES) a.results[lc.li] = static_cast<uint8_t>(ok);
+    }
 }
 
-template <class C, bool CLS>
+template <class C, bool CLS, bool RES>
 __global__ void __launch_bounds__(C::warps * 32) k_lines_tma(const __grid_constant__ Args a,
                                                              const __grid_constant__ CUtensorMap map) {
     extern __shared__ __align__(1024) uint8_t sm[];
@@ -218,7 +258,7 @@ __global__ void __launch_bounds__(C::warps * 32) k_lines_tma(const __grid_consta
         const uint64_t r0 = a.rows * a.chunk;
         for (uint32_t p = lane; p < a.rem_pieces; p += 32) {
             const uint64_t c0 = r0 + static_cast<uint64_t>(p) * a.rem_piece;
-            range_direct<CLS>(a, c0, min(c0 + a.rem_piece, a.len), cnt);
+            range_direct<CLS, RES>(a, c0, min(c0 + a.rem_piece, a.len), a.rows + p, cnt);
         }
     }
 
@@ -236,6 +276,7 @@ __global__ void __launch_bounds__(C::warps * 32) k_lines_tma(const __grid_consta
         }
         uint32_t s[C::chains];
         bool valid[C::chains];
+        LineCursor lc[C::chains];
 #pragma unroll
         for (int j = 0; j < C::chains; ++j) {
             const uint64_t row = row0 + j * 32 + lane;
@@ -245,6 +286,7 @@ __global__ void __launch_bounds__(C::warps * 32) k_lines_tma(const __grid_consta
                 const uint64_t c0 = row * a.chunk;
                 s[j] = (c0 == 0 || a.text[c0 - 1] == a.delim) ? a.start : a.skip;
             }
+            lc[j] = LineCursor{RES && valid[j] ? a.line_base[row] : 0, valid[j] && s[j] == a.start, valid[j]};
         }
         uint32_t last[C::chains] = {};
         for (uint32_t col = 0; col < ncol; ++col) {
@@ -265,8 +307,12 @@ __global__ void __launch_bounds__(C::warps * 32) k_lines_tma(const __grid_consta
                     for (int k = 0; k < 4; ++k)
 #pragma unroll
                         for (int j = 0; j < C::chains; ++j) {
-                            s[j] = step<CLS, true>(a, s[j], word_of(v[j], w), k);
-                            cnt += counted<CLS>(a, s[j]);
+                            if constexpr (RES) {
+                                s[j] = step_res<CLS>(a, s[j], __byte_perm(word_of(v[j], w), 0, 0x4440 + k), cnt, lc[j]);
+                            } else {
+                                s[j] = step<CLS, true>(a, s[j], word_of(v[j], w), k);
+                                cnt += counted<CLS>(a, s[j]);
+                            }
                         }
 #pragma unroll
                 for (int j = 0; j < C::chains; ++j) last[j] = v[j].w >> 24;
@@ -282,7 +328,9 @@ __global__ void __launch_bounds__(C::warps * 32) k_lines_tma(const __grid_consta
         for (int j = 0; j < C::chains; ++j) {
             if (valid[j] && s[j] != a.skip && last[j] != a.delim) {
                 const uint64_t row = row0 + j * 32 + lane;
-                cnt += finish_line<CLS>(a, s[j] + a.tail_delta, (row + 1) * a.chunk) == a.term_acc;
+                const uint32_t ok = finish_line<CLS>(a, s[j] + a.tail_delta, (row + 1) * a.chunk) == a.term_acc;
+                cnt += ok;
+                if constexpr (RES) a.results[lc[j].li] = static_cast<uint8_t>(ok);
             }
         }
     }
@@ -329,10 +377,37 @@ CUtensorMapSwizzle swizzle_of(int slice) {
     }
 }
 
-template <class C, bool CLS>
+// Delimiters per range (RES): TMA rows [i*chunk, +chunk), then the remainder
+// pieces [rows*chunk + p*rem_piece, +rem_piece). One warp per range, 512
+// coalesced bytes per iteration (ranges start 16-byte aligned).
+__global__ void __launch_bounds__(256) k_lt_range_delims(const uint8_t* __restrict__ text, uint64_t len, uint32_t chunk,
+                                                         uint64_t rows, uint32_t rem_piece, uint64_t nranges,
+                                                         uint32_t delim, unsigned long long* __restrict__ out) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t nwarps = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5);
+    const uint32_t d4 = delim * 0x01010101u;
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); i < nranges;
+         i += nwarps) {
+        const uint64_t c0 = i < rows ? i * chunk : rows * chunk + (i - rows) * rem_piece;
+        const uint64_t c1 = min(c0 + (i < rows ? chunk : rem_piece), len);
+        uint32_t n = 0;
+        uint64_t pos = c0 + 16 * lane;
+        for (; pos + 16 <= c1; pos += 512) {
+            const uint4 v = __ldcs(reinterpret_cast<const uint4*>(text + pos));
+            n += __popc(__vcmpeq4(v.x, d4)) + __popc(__vcmpeq4(v.y, d4)) + __popc(__vcmpeq4(v.z, d4)) +
+                 __popc(__vcmpeq4(v.w, d4));
+        }
+        n /= 8;
+        for (; pos < c1; ++pos) n += text[pos] == delim;   // the last partial group (one lane)
+        n = __reduce_add_sync(0xFFFFFFFFu, n);
+        if (lane == 0) out[i] = n;
+    }
+}
+
+template <class C, bool CLS, bool RES>
 int per_sm_of(uint32_t smem) {
     int per_sm = 0;
-    auto* k = k_lines_tma<C, CLS>;
+    auto* k = k_lines_tma<C, CLS, RES>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, C::warps * 32, smem);
     return per_sm < 1 ? 1 : per_sm;
@@ -344,7 +419,7 @@ uint32_t auto_chunk(const LtTable& t, uint64_t len) {
     const uint32_t smem = place_stages<C>(t, a);
     int dev = 0;
     cudaGetDevice(&dev);
-    const uint64_t rows = static_cast<uint64_t>(per_sm_of<C, CLS>(smem)) * device_sm_count(dev) * C::warps * C::rows;
+    const uint64_t rows = static_cast<uint64_t>(per_sm_of<C, CLS, false>(smem)) * device_sm_count(dev) * C::warps * C::rows;
     uint64_t c = (len + rows - 1) / rows;
     c = (c + C::slice - 1) / C::slice * C::slice;
     if (c < 4u * C::slice) c = 4u * C::slice;
@@ -352,9 +427,33 @@ uint32_t auto_chunk(const LtTable& t, uint64_t len) {
     return static_cast<uint32_t>(c);
 }
 
-template <class C, bool CLS>
+// Ranges of a launch: full TMA rows plus the remainder pieces.
+struct RangeSplit {
+    uint64_t rows;
+    uint32_t rem_piece, rem_pieces;
+};
+
+RangeSplit split_ranges(uint64_t len, uint32_t chunk) {
+    RangeSplit r{};
+    r.rows = len / chunk;
+    const uint64_t rem = len - r.rows * chunk;
+    r.rem_piece = static_cast<uint32_t>(((rem + 31) / 32 + 15) & ~uint64_t(15));
+    if (r.rem_piece < 16) r.rem_piece = 16;
+    r.rem_pieces = rem ? static_cast<uint32_t>((rem + r.rem_piece - 1) / r.rem_piece) : 0;
+    return r;
+}
+
+size_t res_scratch_bytes(uint64_t nranges) {
+    size_t temp = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, temp, static_cast<unsigned long long*>(nullptr),
+                                  static_cast<unsigned long long*>(nullptr), static_cast<int64_t>(nranges));
+    return 2 * nranges * sizeof(unsigned long long) + temp + 256;
+}
+
+template <class C, bool CLS, bool RES>
 cudaError_t launch(const LtTable& t, const uint8_t* text, uint64_t len, uint8_t delim, uint32_t chunk,
-                   unsigned long long* count, cudaStream_t st) {
+                   unsigned long long* count, uint8_t* results, void* scratch, size_t scratch_bytes,
+                   cudaStream_t st) {
     if (len == 0) return cudaSuccess;
     if (chunk == 0) chunk = auto_chunk<C, CLS>(t, len);
     if (chunk % C::slice) return cudaErrorInvalidValue;
@@ -362,12 +461,30 @@ cudaError_t launch(const LtTable& t, const uint8_t* text, uint64_t len, uint8_t 
     a.text = text;
     a.len = len;
     a.chunk = chunk;
-    a.rows = len / chunk;
+    const RangeSplit rs = split_ranges(len, chunk);
+    a.rows = rs.rows;
     a.tiles = (a.rows + C::rows - 1) / C::rows;
-    const uint64_t rem = len - a.rows * chunk;
-    a.rem_piece = static_cast<uint32_t>(((rem + 31) / 32 + 15) & ~uint64_t(15));
-    if (a.rem_piece < 16) a.rem_piece = 16;
-    a.rem_pieces = rem ? static_cast<uint32_t>((rem + a.rem_piece - 1) / a.rem_piece) : 0;
+    a.rem_piece = rs.rem_piece;
+    a.rem_pieces = rs.rem_pieces;
+    if constexpr (RES) {
+        const uint64_t nr = rs.rows + rs.rem_pieces;
+        if (!scratch || scratch_bytes < res_scratch_bytes(nr)) return cudaErrorInvalidValue;
+        auto* per = static_cast<unsigned long long*>(scratch);
+        auto* base = per + nr;
+        void* temp = base + nr;
+        size_t temp_bytes = scratch_bytes - 2 * nr * sizeof(unsigned long long);
+        int dev = 0;
+        cudaGetDevice(&dev);
+        const uint64_t want = (nr + 7) / 8, cap = static_cast<uint64_t>(device_sm_count(dev)) * 8;
+        k_lt_range_delims<<<static_cast<unsigned>(want < cap ? want : cap), 256, 0, st>>>(text, len, chunk, rs.rows,
+                                                                                          rs.rem_piece, nr, delim, per);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+        e = cub::DeviceScan::ExclusiveSum(temp, temp_bytes, per, base, static_cast<int64_t>(nr), st);
+        if (e != cudaSuccess) return e;
+        a.results = results;
+        a.line_base = base;
+    }
     a.img_lo = static_cast<const uint4*>(t.d_lo);
     a.lo_addr = t.lo_addr;
     a.lo_words = t.lo_bytes / 16;
@@ -407,70 +524,63 @@ cudaError_t launch(const LtTable& t, const uint8_t* text, uint64_t len, uint8_t 
                                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
     }
-    const int per_sm = per_sm_of<C, CLS>(smem);
+    const int per_sm = per_sm_of<C, CLS, RES>(smem);
     int dev = 0;
     cudaGetDevice(&dev);
     const uint64_t cap = static_cast<uint64_t>(per_sm) * device_sm_count(dev);
     const uint64_t want = (a.tiles + C::warps - 1) / C::warps;
     const int grid = static_cast<int>(want == 0 ? 1 : (want < cap ? want : cap));
-    k_lines_tma<C, CLS><<<grid, C::warps * 32, smem, st>>>(a, map);
+    k_lines_tma<C, CLS, RES><<<grid, C::warps * 32, smem, st>>>(a, map);
     return cudaGetLastError();
 }
 
-// Kernel shapes (RXG_LT_SHAPE selects one for tuning runs; unset = per-layout default).
+// Kernel shapes (RXG_LT_SHAPE=0 forces S0 for tuning runs; unset = per-layout default).
 // Measured on config (c), 1 GB, B200 (tools/ab_lines.py): 16-byte slices are
 // TMA-request bound (~3.3 TB/s); 32-byte slices with 24 warps x 2 ranges x 3
-// stages reach ~5.05 TB/s; 4 stages / 3 ranges per lane give the same.
+// stages reach ~5.05 TB/s, x 3 ranges x 2 stages ~5.1 TB/s (direct layout);
+// the class layout (two LDS per byte, ~225 KB with its ring) fits only S0.
 using S0 = Shape<24, 2, 32, 3>;
-using S1 = Shape<16, 2, 32, 4>;
-using S2 = Shape<24, 2, 32, 2>;
-using S3 = Shape<16, 3, 32, 3>;
-using S4 = Shape<32, 2, 16, 4>;
-using S5 = Shape<16, 4, 32, 2>;
 using S6 = Shape<24, 3, 32, 2>;
-using S7 = Shape<20, 3, 32, 2>;
-using S8 = Shape<12, 4, 32, 3>;
 
 int shape_id() {
     const char* e = std::getenv("RXG_LT_SHAPE");
     return e ? std::atoi(e) : -1;
 }
 
-
-template <class C>
-cudaError_t launch2(const LtTable& t, const uint8_t* text, uint64_t len, uint8_t delim, uint32_t chunk,
-                    unsigned long long* count, cudaStream_t st) {
-    return t.cls ? launch<C, true>(t, text, len, delim, chunk, count, st)
-                 : launch<C, false>(t, text, len, delim, chunk, count, st);
-}
-
-// Default shape per layout (measured, config c / d): the direct layout (one
-// LDS per byte) gains from a third range per lane, the class layout (two LDS
-// per byte, ~225 KB with its ring) does not fit it.
-cudaError_t launch_default(const LtTable& t, const uint8_t* text, uint64_t len, uint8_t delim, uint32_t chunk,
-                           unsigned long long* count, cudaStream_t st) {
-    return t.cls ? launch<S0, true>(t, text, len, delim, chunk, count, st)
-                 : launch<S6, false>(t, text, len, delim, chunk, count, st);
+template <bool RES>
+cudaError_t launch_any(const LtTable& t, const uint8_t* text, uint64_t len, uint8_t delim, uint32_t chunk,
+                       unsigned long long* count, uint8_t* results, void* scratch, size_t scratch_bytes,
+                       cudaStream_t st) {
+    if (t.cls || shape_id() == 0)
+        return t.cls ? launch<S0, true, RES>(t, text, len, delim, chunk, count, results, scratch, scratch_bytes, st)
+                     : launch<S0, false, RES>(t, text, len, delim, chunk, count, results, scratch, scratch_bytes, st);
+    return launch<S6, false, RES>(t, text, len, delim, chunk, count, results, scratch, scratch_bytes, st);
 }
 
 }  // namespace
 
 cudaError_t launch_lines_tma(const LtTable& t, const uint8_t* text, uint64_t len, uint8_t delim, uint32_t chunk,
                              unsigned long long* count, cudaStream_t st) {
-    switch (shape_id()) {
-    case 0: return launch2<S0>(t, text, len, delim, chunk, count, st);
-    case 1: return launch2<S1>(t, text, len, delim, chunk, count, st);
-    case 2: return launch2<S2>(t, text, len, delim, chunk, count, st);
-    case 3: return launch2<S3>(t, text, len, delim, chunk, count, st);
-    case 4: return launch2<S4>(t, text, len, delim, chunk, count, st);
-    case 5: return launch2<S5>(t, text, len, delim, chunk, count, st);
-    case 6: return launch2<S6>(t, text, len, delim, chunk, count, st);
-    case 7: return launch2<S7>(t, text, len, delim, chunk, count, st);
-    case 8: return launch2<S8>(t, text, len, delim, chunk, count, st);
-    default: return launch_default(t, text, len, delim, chunk, count, st);
-    }
+    return launch_any<false>(t, text, len, delim, chunk, count, nullptr, nullptr, 0, st);
 }
 
-uint32_t lines_tma_slice() { return shape_id() == 4 ? 16 : 32; }
+uint32_t lines_tma_chunk(const LtTable& t, uint64_t len, uint32_t chunk) {
+    if (chunk) return chunk;
+    if (t.cls || shape_id() == 0) return t.cls ? auto_chunk<S0, true>(t, len) : auto_chunk<S0, false>(t, len);
+    return auto_chunk<S6, false>(t, len);
+}
+
+size_t lines_tma_results_scratch(uint64_t len, uint32_t chunk) {
+    const RangeSplit rs = split_ranges(len, chunk);
+    return res_scratch_bytes(rs.rows + rs.rem_pieces);
+}
+
+cudaError_t launch_lines_tma_results(const LtTable& t, const uint8_t* text, uint64_t len, uint8_t delim,
+                                     uint32_t chunk, unsigned long long* count, uint8_t* results, void* scratch,
+                                     size_t scratch_bytes, cudaStream_t st) {
+    return launch_any<true>(t, text, len, delim, chunk, count, results, scratch, scratch_bytes, st);
+}
+
+uint32_t lines_tma_slice() { return 32; }
 
 }  // namespace rxg

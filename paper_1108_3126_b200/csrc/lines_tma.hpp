@@ -65,4 +65,14 @@ cudaError_t launch_lines_tma(const LtTable& t, const uint8_t* text, uint64_t len
                              unsigned long long* count, cudaStream_t st);
 uint32_t lines_tma_slice();
 
+// Per-line results on the same kernel: a delimiter count per range, an
+// exclusive scan (the line index of each range's first line), then the walk
+// writes results[line] at every delimiter of an owned line and for its tail.
+// chunk must be the effective one (lines_tma_chunk); scratch on device.
+uint32_t lines_tma_chunk(const LtTable& t, uint64_t len, uint32_t chunk);
+size_t lines_tma_results_scratch(uint64_t len, uint32_t chunk);
+cudaError_t launch_lines_tma_results(const LtTable& t, const uint8_t* text, uint64_t len, uint8_t delim,
+                                     uint32_t chunk, unsigned long long* count, uint8_t* results, void* scratch,
+                                     size_t scratch_bytes, cudaStream_t st);
+
 }  // namespace rxg

@@ -147,3 +147,23 @@ def test_full_size_cross_engine_long_tailed():
     cut = int(np.flatnonzero(text[: 8 << 20] == 10)[-1]) + 1
     want, wr = Oracle(rx.compile(rx.parse(pat))).match_batch(text[:cut], 10, 0)
     assert np.array_equal(r[: len(wr)], wr)
+
+
+@pytest.mark.parametrize("key", ["c", "d", "abb"])
+def test_generic_line_kernel_results(key):
+    """The generic line kernel (k_lines: tables too large for the TMA
+    layouts) forced with RXG_NO_LT, per-line results against the oracle and
+    the TMA kernel."""
+    pat = _pat(key)
+    text = _long_tailed(7, 2 << 20, ALPHA[key], long_every=100, long_len=(2_000, 50_000))
+    want_c, want_r = Oracle(rx.compile(rx.parse(pat))).match_batch(text, 10, 0)
+    m = rx.Matcher(pat, device=0)
+    c1, r1 = m.match_batch(text, 10, results=True)
+    os.environ["RXG_NO_LT"] = "1"
+    try:
+        c2, r2 = m.match_batch(text, 10, results=True)
+        c3 = _dev_count(m, text)
+    finally:
+        os.environ.pop("RXG_NO_LT", None)
+    assert c1 == c2 == c3 == want_c
+    assert np.array_equal(r1, want_r) and np.array_equal(r2, want_r)
