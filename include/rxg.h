@@ -169,7 +169,7 @@ typedef struct rxg_one_opts {
                                          (rx::ParStats, parallel.hpp:52-58) */
     uint32_t* d_trace;                /* ROUNDS: per symbol the next schedule as (N+1)-bit rows, bit N = null;
                                          zeroed by the caller (test_parallel.cpp:114-137) */
-    uint32_t chunk;                   /* CHUNKED: bytes per range (multiple of 256), 0 = auto */
+    uint32_t chunk;                   /* CHUNKED: bytes per range (multiple of 32 on the TMA path, 64 otherwise), 0 = auto */
     uint32_t lookback;                /* CHUNKED: bytes walked before a range to guess its entry state (0 = 64) */
     unsigned long long* d_repairs;    /* CHUNKED: ranges re-walked by the in-order repair pass */
 } rxg_one_opts;

@@ -785,7 +785,7 @@ int rxg_match_one_ex(rxg_heap* h, const uint8_t* d_bytes, uint64_t len, int engi
         static const bool no_tma = std::getenv("RXG_NO_TMA") != nullptr;
         if (h->plain->chunk_lt.ok && !no_tma) {
             uint32_t chunk = o.chunk ? o.chunk : chunked_tma_auto_chunk(len, h->device);
-            if (chunk % 256) return fail(RXG_EINVAL, "chunk must be a multiple of 256 on the TMA path");
+            if (chunk % 32) return fail(RXG_EINVAL, "chunk must be a multiple of 32 on the TMA path");
             void* scratch = nullptr;
             RXG_CUDA(cudaMallocAsync(&scratch, chunked_tma_scratch_bytes(len, chunk), st));
             const cudaError_t e = launch_chunked_tma(h->plain->chunk_lt, h->plain->d_chunk, d_bytes, len, chunk,

@@ -71,7 +71,7 @@ struct Args {
     uint32_t start, row_bytes, cmap_addr, acc_off;
     uint32_t* g;
     uint32_t* e;
-    uint32_t* mid;      // nranges x (chunk / kMidT)
+    uint32_t* mid;      // nranges x ceil(chunk / kMidT)
     unsigned int* ticket;
     unsigned long long* first_bad;
     int32_t* accept;
@@ -122,7 +122,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_chunk_tma(const __grid_constant
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    const uint32_t per = a.chunk / kMidT;
+    const uint32_t per = (a.chunk + kMidT - 1) / kMidT;   // checkpoints per range (the last may be partial)
     // the remainder range (past the last full row) walks with direct loads
     if (blockIdx.x == 0 && threadIdx.x == 0 && a.nranges > a.rows) {
         const uint64_t r = a.rows, c0 = r * a.chunk;
@@ -147,13 +147,14 @@ __global__ void __launch_bounds__(kWarps * 32) k_chunk_tma(const __grid_constant
                 tma::issue<kStageBytes>(&map, stage[st], bar0 + st * 8, static_cast<int32_t>(st * kSlice),
                                         static_cast<int32_t>(row0));
         }
-        uint32_t s[kChains];
+        uint32_t s[kChains], guess[kChains];
         bool valid[kChains];
 #pragma unroll
         for (int j = 0; j < kChains; ++j) {
             const uint64_t r = row0 + j * 32 + lane;
             valid[j] = r < a.rows;
             s[j] = valid[j] ? entry_guess<CLS>(a, r) : a.start;
+            guess[j] = s[j];
             if (valid[j]) a.g[r] = s[j];
         }
         for (uint32_t col = 0; col < ncol; ++col) {
@@ -182,15 +183,27 @@ __global__ void __launch_bounds__(kWarps * 32) k_chunk_tma(const __grid_constant
                 tma::issue<kStageBytes>(&map, stage[st], bar0 + st * 8, static_cast<int32_t>((col + kStages) * kSlice),
                                         static_cast<int32_t>(row0));
             }
-            if (((col + 1) * kSlice) % kMidT == 0) {
+            if (((col + 1) * kSlice) % kMidT == 0 || col + 1 == ncol) {
 #pragma unroll
                 for (int j = 0; j < kChains; ++j)
-                    if (valid[j]) a.mid[(row0 + j * 32 + lane) * per + ((col + 1) * kSlice) / kMidT - 1] = s[j];
+                    if (valid[j]) a.mid[(row0 + j * 32 + lane) * per + ((col + 1) * kSlice - 1) / kMidT] = s[j];
             }
         }
 #pragma unroll
         for (int j = 0; j < kChains; ++j)
             if (valid[j]) a.e[row0 + j * 32 + lane] = s[j];
+        // boundaries inside the tile, from registers: row j*32+lane follows
+        // j*32+lane-1 (lane - 1, or lane 31 of the previous chain)
+        uint32_t bad = ~0u;
+#pragma unroll
+        for (int j = kChains - 1; j >= 0; --j) {
+            const uint32_t up = __shfl_up_sync(0xFFFFFFFFu, s[j], 1);
+            const uint32_t wrap = j > 0 ? __shfl_sync(0xFFFFFFFFu, s[j > 0 ? j - 1 : 0], 31) : 0u;
+            const bool has_pred = lane > 0 || j > 0;
+            if (valid[j] && has_pred && guess[j] != (lane > 0 ? up : wrap)) bad = j * 32 + lane;
+        }
+        bad = __reduce_min_sync(0xFFFFFFFFu, bad);
+        if (lane == 0 && bad != ~0u) atomicMin(a.first_bad, row0 + bad);
     }
     // last CTA: parallel boundary check (flag word after the mbarriers: no
     // static shared memory, which would move the dynamic window off 0x400)
@@ -203,12 +216,17 @@ __global__ void __launch_bounds__(kWarps * 32) k_chunk_tma(const __grid_constant
     __syncthreads();
     if (!*last) return;
     __threadfence();
+    // only the boundaries between tiles (and before the remainder range) are
+    // left: the first row of every tile > 0, and range `rows`
     unsigned long long bad = ~0ull;
-    for (uint64_t j = 1 + threadIdx.x; j < a.nranges; j += blockDim.x)
+    for (uint64_t t = 1 + threadIdx.x; t <= a.tiles; t += blockDim.x) {
+        const uint64_t j = t < a.tiles ? t * kRows : a.rows;
+        if (j >= a.nranges || (t == a.tiles && a.nranges == a.rows)) continue;
         if (a.g[j] != a.e[j - 1]) {
             bad = j;
             break;
         }
+    }
     if (bad != ~0ull) atomicMin(a.first_bad, bad);
 }
 
@@ -230,7 +248,7 @@ __global__ void __launch_bounds__(32) k_chunk_tma_fix(const __grid_constant__ Ar
     load_image(a, sm);
     __syncwarp();
     const uint32_t lane = threadIdx.x;
-    const uint32_t per = a.chunk / kMidT;
+    const uint32_t per = (a.chunk + kMidT - 1) / kMidT;
     unsigned long long repairs = 0;
     const unsigned long long fb = *a.first_bad;
     uint32_t exact = a.nranges == 0 ? a.start : (fb == ~0ull ? a.e[a.nranges - 1] : a.e[fb - 1]);
@@ -313,20 +331,20 @@ uint32_t chunked_tma_auto_chunk(uint64_t len, int device) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     const uint64_t ranges = static_cast<uint64_t>(sms) * kWarps * kRows;
     uint64_t c = (len + ranges - 1) / ranges;
-    c = (c + kMidT - 1) / kMidT * kMidT;
+    c = (c + kSlice - 1) / kSlice * kSlice;   // slice multiple: keeps the grid at one CTA per SM
     if (c < kMidT) c = kMidT;
     return static_cast<uint32_t>(c);
 }
 
 size_t chunked_tma_scratch_bytes(uint64_t len, uint32_t chunk) {
     const uint64_t n = (len + chunk - 1) / chunk;
-    return 16 + (2 * n + n * (chunk / kMidT)) * sizeof(uint32_t) + 64;
+    return 16 + (2 * n + n * ((chunk + kMidT - 1) / kMidT)) * sizeof(uint32_t) + 64;
 }
 
 cudaError_t launch_chunked_tma(const LtTable& t, const void* d_img, const uint8_t* text, uint64_t len, uint32_t chunk,
                                uint32_t lookback, void* scratch, int32_t* accept, unsigned long long* repairs,
                                int device, cudaStream_t st) {
-    if (chunk == 0 || chunk % kMidT) return cudaErrorInvalidValue;
+    if (chunk == 0 || chunk % kSlice) return cudaErrorInvalidValue;
     Args a{};
     a.text = text;
     a.len = len;

@@ -76,20 +76,31 @@ __global__ void __launch_bounds__(256) k_chunk_walk(const __grid_constant__ Chun
     extern __shared__ __align__(16) uint8_t sm[];
     load_table(sm, a.img, a.img_words);
     const uint32_t per = a.chunk / kMid;
-    for (uint64_t j = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < a.nranges;
-         j += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-        const uint64_t c0 = j * a.chunk;
-        const uint64_t c1 = min(c0 + a.chunk, a.len);
-        uint32_t s = a.start;
-        if (j > 0) s = walk<E, CLS>(a, sm, a.start, c0 > a.lookback ? c0 - a.lookback : 0, c0);
-        a.g[j] = s;
-        uint32_t* mid = a.mid + j * per;
-        uint32_t k = 0;
-        for (uint64_t p = c0; p < c1; p += kMid, ++k) {
-            s = walk<E, CLS>(a, sm, s, p, min(p + kMid, c1));
-            mid[k] = s;
+    const uint32_t lane = threadIdx.x & 31;
+    // whole warps iterate together (ranges j = base + tid), so the boundary
+    // j-1 -> j is checked from registers for every lane but lane 0
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t base = static_cast<uint64_t>(blockIdx.x) * blockDim.x; base < a.nranges; base += stride) {
+        const uint64_t j = base + threadIdx.x;
+        const bool live = j < a.nranges;
+        uint32_t s = a.start, guess = a.start;
+        if (live) {
+            const uint64_t c0 = j * a.chunk;
+            const uint64_t c1 = min(c0 + a.chunk, a.len);
+            if (j > 0) s = walk<E, CLS>(a, sm, a.start, c0 > a.lookback ? c0 - a.lookback : 0, c0);
+            guess = s;
+            a.g[j] = s;
+            uint32_t* mid = a.mid + j * per;
+            uint32_t k = 0;
+            for (uint64_t p = c0; p < c1; p += kMid, ++k) {
+                s = walk<E, CLS>(a, sm, s, p, min(p + kMid, c1));
+                mid[k] = s;
+            }
+            a.e[j] = s;
         }
-        a.e[j] = s;
+        const uint32_t prev = __shfl_up_sync(0xFFFFFFFFu, s, 1);
+        const uint32_t bad = __reduce_min_sync(0xFFFFFFFFu, live && lane > 0 && guess != prev ? lane : ~0u);
+        if (lane == 0 && bad != ~0u) atomicMin(a.first_bad, j + bad);
     }
     // The last CTA to finish checks every range boundary in parallel, so the
     // in-order repair pass only starts where a guess was actually wrong.
@@ -102,8 +113,8 @@ __global__ void __launch_bounds__(256) k_chunk_walk(const __grid_constant__ Chun
     __syncthreads();
     if (!last) return;
     __threadfence();
-    unsigned long long bad = ~0ull;
-    for (uint64_t j = 1 + threadIdx.x; j < a.nranges; j += blockDim.x)
+    unsigned long long bad = ~0ull;   // the warp-boundary ranges (j = 32, 64, ...) are left
+    for (uint64_t j = 32 * (1 + static_cast<uint64_t>(threadIdx.x)); j < a.nranges; j += 32ull * blockDim.x)
         if (a.g[j] != a.e[j - 1]) {
             bad = j;
             break;

@@ -48,20 +48,22 @@ def test_random_small_against_oracle(engine):
             assert m.lockstep_accepts(w, engine) == o.accepts(w), (p, w)
 
 
-def test_chunked_long_strings_with_small_ranges():
-    """Many ranges and repairs: parity on non-synchronizing automata too."""
+@pytest.mark.parametrize("chunk", [256, 96, 288])
+def test_chunked_long_strings_with_small_ranges(chunk):
+    """Many ranges and repairs: parity on non-synchronizing automata too; range
+    sizes that are not multiples of the 256-byte checkpoint period."""
     rng = np.random.default_rng(2)
     for p in ["(a|b)*abb", "(aa)*", "((a|b)(a|b))*", "(ab|ba)*a", "a*b*a*b*"]:
         m = rx.Matcher(p)
         o = O(p)
-        for n in (0, 1, 63, 64, 65, 5000, 100_000):
+        for n in (0, 1, 63, 64, 65, 5000, 100_000, 1_000_003):
             w = rng.choice([97, 98], size=n).astype(np.uint8)
             if p == "(aa)*":
                 w[:] = 97
             d = torch.from_numpy(w).cuda() if n else torch.zeros(1, dtype=torch.uint8, device="cuda")
             acc = torch.zeros(1, dtype=torch.int32, device="cuda")
             rep = torch.zeros(1, dtype=torch.int64, device="cuda")
-            m.match_one_ex(d, acc, "chunked", nbytes=n, chunk=256, lookback=16, d_repairs=rep)
+            m.match_one_ex(d, acc, "chunked", nbytes=n, chunk=chunk, lookback=16, d_repairs=rep)
             torch.cuda.synchronize()
             assert bool(acc.item()) == o.accepts(w.tobytes()), (p, n)
 
