@@ -91,7 +91,17 @@ def single_e():
     ok = k1 == final == ch
     log(f"(e) 256 MiB: K1 {tk:.1f}s accept={k1}; {nchunks} chunks of 4 MiB verified by the oracle in {tv:.0f}s; "
         f"chunked engine accept={ch} -> {'PASS' if ok else 'FAIL'}")
-    return ok
+    # negative twin (last byte 'a'): the chunk-parallel engine against the
+    # sequential walk of the same memoized table over the full string
+    d[-1] = ord("a")
+    res = {}
+    for e in ("chunked", "dfa_seq"):
+        m.match_one_ex(d, acc, e)
+        torch.cuda.synchronize()
+        res[e] = bool(acc.item())
+    ok2 = res["chunked"] == res["dfa_seq"] is False
+    log(f"(E) 256 MiB negative twin: {res} -> {'PASS' if ok2 else 'FAIL'}")
+    return ok and ok2
 
 
 def main():
