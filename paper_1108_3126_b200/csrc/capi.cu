@@ -793,7 +793,7 @@ int rxg_match_one_ex(rxg_heap* h, const uint8_t* d_bytes, uint64_t len, int engi
                                                      h->device, st);
             cudaFreeAsync(scratch, st);
             if (e != cudaSuccess) return cuda_fail(e, "launch_chunked_tma");
-            g_launches = 2;
+            g_launches = 1;   // walk, seam check and repair in one kernel
             return RXG_OK;
         }
         uint32_t chunk = o.chunk ? o.chunk : chunked_auto_chunk(*t, len, h->device);

@@ -7,9 +7,11 @@
 // SWIZZLE_32B). Each range first guesses its entry state by walking the
 // `lookback` bytes before it from the start state (direct loads), then walks
 // its own bytes from the ring, recording the state every kMidT bytes and at
-// its end. The last CTA to finish checks every range boundary in parallel;
-// an in-order repair pass (one warp) re-walks only ranges whose guess was
-// wrong, stopping as soon as the re-walk meets the recorded trajectory.
+// its end. Each warp checks the range boundaries inside its tile from
+// registers; the last CTA to finish checks the seams between tiles, then one
+// of its warps runs the in-order repair pass, re-walking only ranges whose
+// guess was wrong and stopping as soon as the re-walk meets the recorded
+// trajectory. One launch.
 // Exact for every pattern.
 #include <cstdlib>
 #include <cstring>
@@ -73,7 +75,7 @@ struct Args {
     uint32_t* e;
     uint32_t* mid;      // nranges x ceil(chunk / kMidT)
     unsigned int* ticket;
-    unsigned long long* first_bad;
+    unsigned long long* bad_inv;   // ~(first range whose entry guess is wrong); 0 = none (zero-initialised)
     int32_t* accept;
     unsigned long long* repairs;
 };
@@ -88,6 +90,17 @@ template <bool CLS>
 __device__ uint32_t walk(const Args& a, uint32_t s, uint64_t lo, uint64_t hi) {
     uint64_t p = lo;
     for (; p < hi && (p & 15); ++p) s = stepb<CLS>(a, s, a.text[p]);
+    for (; p + 64 <= hi; p += 64) {   // four independent loads in flight, then 64 steps
+        uint4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = __ldg(reinterpret_cast<const uint4*>(a.text + p) + u);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int w = 0; w < 4; ++w)
+#pragma unroll
+                for (int k = 0; k < 4; ++k) s = stepb<CLS>(a, s, __byte_perm(tma::word_of(v[u], w), 0, 0x4440 + k));
+    }
     for (; p + 16 <= hi; p += 16) {
         const uint4 v = __ldg(reinterpret_cast<const uint4*>(a.text + p));
 #pragma unroll
@@ -107,6 +120,58 @@ template <bool CLS>
 __device__ uint32_t entry_guess(const Args& a, uint64_t r) {
     const uint64_t c0 = r * a.chunk;
     return r == 0 ? a.start : walk<CLS>(a, a.start, c0 > a.lookback ? c0 - a.lookback : 0, c0);
+}
+
+// In-order repair from the first wrong guess (one warp, the table already in
+// shared memory), then the answer. Run by warp 0 of the last CTA.
+template <bool CLS>
+__device__ void repair_and_answer(const Args& a) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t per = (a.chunk + kMidT - 1) / kMidT;
+    unsigned long long repairs = 0;
+    const unsigned long long fb = ~*reinterpret_cast<volatile unsigned long long*>(a.bad_inv);
+    uint32_t exact = a.nranges == 0 ? a.start : (fb == ~0ull ? a.e[a.nranges - 1] : a.e[fb - 1]);
+    for (uint64_t base = fb == ~0ull ? a.nranges : fb; base < a.nranges; base += 32) {
+        uint64_t j = base;
+        while (j < a.nranges && j < base + 32) {
+            const uint64_t jj = j + lane;
+            const bool ok = jj >= a.nranges || jj >= base + 32 || (jj == j ? a.g[jj] == exact : a.g[jj] == a.e[jj - 1]);
+            const uint32_t bad = __ballot_sync(0xFFFFFFFFu, !ok);
+            if (!bad) {
+                const uint64_t lastr = min(base + 32, a.nranges) - 1;
+                exact = a.e[lastr];
+                j = lastr + 1;
+                break;
+            }
+            const uint64_t r = j + (__ffs(bad) - 1);
+            const uint32_t entry = r == j ? exact : a.e[r - 1];
+            uint32_t s = entry;
+            if (lane == 0) {
+                const uint64_t c0 = r * a.chunk, c1 = min(c0 + a.chunk, a.len);
+                uint32_t* mid = a.mid + r * per;
+                uint32_t k = 0;
+                for (uint64_t p = c0; p < c1; p += kMidT, ++k) {
+                    s = walk<CLS>(a, s, p, min(p + kMidT, c1));
+                    if (s == mid[k]) {   // trajectories coincide from here on
+                        s = a.e[r];
+                        break;
+                    }
+                    mid[k] = s;
+                }
+                a.g[r] = entry;
+                a.e[r] = s;
+                ++repairs;
+            }
+            __syncwarp();
+            exact = __shfl_sync(0xFFFFFFFFu, s, 0);
+            j = r + 1;
+        }
+    }
+    if (lane == 0) {
+        const uint32_t acc_addr = CLS ? kLtSmemBase + 1024 + exact * a.row_bytes + a.acc_off : exact + a.acc_off;
+        *a.accept = static_cast<int32_t>(tma::lds16(acc_addr));
+        if (a.repairs) *a.repairs = repairs;
+    }
 }
 
 template <bool CLS>
@@ -138,7 +203,8 @@ __global__ void __launch_bounds__(kWarps * 32) k_chunk_tma(const __grid_constant
     uint32_t phase = 0;
     const uint32_t ncol = a.chunk / kSlice;
     const uint32_t* stage = a.stage_addr + warp * kStages;
-    for (uint64_t tile = static_cast<uint64_t>(blockIdx.x) * kWarps + warp; tile < a.tiles;
+    // tiles interleave the CTAs (tile = warp * grid + cta): small inputs spread over every SM
+    for (uint64_t tile = static_cast<uint64_t>(warp) * gridDim.x + blockIdx.x; tile < a.tiles;
          tile += static_cast<uint64_t>(gridDim.x) * kWarps) {
         const uint64_t row0 = tile * kRows;
         if (lane == 0) {
@@ -203,7 +269,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_chunk_tma(const __grid_constant
             if (valid[j] && has_pred && guess[j] != (lane > 0 ? up : wrap)) bad = j * 32 + lane;
         }
         bad = __reduce_min_sync(0xFFFFFFFFu, bad);
-        if (lane == 0 && bad != ~0u) atomicMin(a.first_bad, row0 + bad);
+        if (lane == 0 && bad != ~0u) atomicMax(a.bad_inv, ~(row0 + bad));
     }
     // last CTA: parallel boundary check (flag word after the mbarriers: no
     // static shared memory, which would move the dynamic window off 0x400)
@@ -227,71 +293,11 @@ __global__ void __launch_bounds__(kWarps * 32) k_chunk_tma(const __grid_constant
             break;
         }
     }
-    if (bad != ~0ull) atomicMin(a.first_bad, bad);
-}
-
-// In-order repair from the first wrong guess (one warp), then the answer.
-template <bool CLS>
-__global__ void __launch_bounds__(32) k_chunk_tma_fix(const __grid_constant__ Args a) {
-    extern __shared__ __align__(1024) uint8_t sm[];
-    if (static_cast<uint32_t>(__cvta_generic_to_shared(sm)) != kLtSmemBase) __trap();
-    const unsigned long long fb0 = *a.first_bad;
-    if (fb0 == ~0ull) {   // every guess was right: the answer is the last range's exit state
-        if (threadIdx.x == 0) {
-            const uint32_t s = a.nranges ? a.e[a.nranges - 1] : a.start;
-            const uint32_t off = CLS ? 1024 + s * a.row_bytes + a.acc_off : s - kLtSmemBase + a.acc_off;
-            *a.accept = reinterpret_cast<const uint16_t*>(reinterpret_cast<const uint8_t*>(a.img) + off)[0];
-            if (a.repairs) *a.repairs = 0;
-        }
-        return;
-    }
-    load_image(a, sm);
-    __syncwarp();
-    const uint32_t lane = threadIdx.x;
-    const uint32_t per = (a.chunk + kMidT - 1) / kMidT;
-    unsigned long long repairs = 0;
-    const unsigned long long fb = *a.first_bad;
-    uint32_t exact = a.nranges == 0 ? a.start : (fb == ~0ull ? a.e[a.nranges - 1] : a.e[fb - 1]);
-    for (uint64_t base = fb == ~0ull ? a.nranges : fb; base < a.nranges; base += 32) {
-        uint64_t j = base;
-        while (j < a.nranges && j < base + 32) {
-            const uint64_t jj = j + lane;
-            const bool ok = jj >= a.nranges || jj >= base + 32 || (jj == j ? a.g[jj] == exact : a.g[jj] == a.e[jj - 1]);
-            const uint32_t bad = __ballot_sync(0xFFFFFFFFu, !ok);
-            if (!bad) {
-                const uint64_t lastr = min(base + 32, a.nranges) - 1;
-                exact = a.e[lastr];
-                j = lastr + 1;
-                break;
-            }
-            const uint64_t r = j + (__ffs(bad) - 1);
-            const uint32_t entry = r == j ? exact : a.e[r - 1];
-            uint32_t s = entry;
-            if (lane == 0) {
-                const uint64_t c0 = r * a.chunk, c1 = min(c0 + a.chunk, a.len);
-                uint32_t* mid = a.mid + r * per;
-                uint32_t k = 0;
-                for (uint64_t p = c0; p < c1; p += kMidT, ++k) {
-                    s = walk<CLS>(a, s, p, min(p + kMidT, c1));
-                    if (s == mid[k]) {
-                        s = a.e[r];
-                        break;
-                    }
-                    mid[k] = s;
-                }
-                a.g[r] = entry;
-                a.e[r] = s;
-                ++repairs;
-            }
-            __syncwarp();
-            exact = __shfl_sync(0xFFFFFFFFu, s, 0);
-            j = r + 1;
-        }
-    }
-    if (lane == 0) {
-        const uint32_t acc_addr = CLS ? kLtSmemBase + 1024 + exact * a.row_bytes + a.acc_off : exact + a.acc_off;
-        *a.accept = static_cast<int32_t>(tma::lds16(acc_addr));
-        if (a.repairs) *a.repairs = repairs;
+    if (bad != ~0ull) atomicMax(a.bad_inv, ~bad);
+    __syncthreads();
+    if (threadIdx.x < 32) {   // the repair pass and the answer, in this CTA (no second launch)
+        __threadfence();
+        repair_and_answer<CLS>(a);
     }
 }
 
@@ -304,23 +310,17 @@ cudaError_t run(const LtTable& t, Args& a, int device, cudaStream_t st) {
     for (int k = 0; k < kWarps * kStages; ++k, p += kStageBytes) a.stage_addr[k] = p;
     a.bar_addr = align_up(p, 8);
     const uint32_t smem = a.bar_addr + kWarps * kStages * 8 + 16 - kLtSmemBase;
-    const uint32_t fix_smem = t.lo_bytes;
     CUtensorMap map;
     std::memset(&map, 0, sizeof(map));
     if (a.rows > 0 && tma::make_map(&map, a.text, a.rows, a.chunk, kSlice, kRows) != CUDA_SUCCESS)
         return cudaErrorInvalidValue;
     cudaError_t e = cudaFuncSetAttribute(k_chunk_tma<CLS>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(k_chunk_tma_fix<CLS>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(fix_smem));
-    if (e != cudaSuccess) return e;
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-    const uint64_t want = (a.tiles + kWarps - 1) / kWarps;
+    const uint64_t want = a.tiles;   // at most one tile per CTA needed to reach every SM
     const int grid = static_cast<int>(want == 0 ? 1 : (want < static_cast<uint64_t>(sms) ? want : sms));
     k_chunk_tma<CLS><<<grid, kWarps * 32, smem, st>>>(a, map);
-    e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
-    k_chunk_tma_fix<CLS><<<1, 32, fix_smem, st>>>(a);
     return cudaGetLastError();
 }
 
@@ -332,7 +332,7 @@ uint32_t chunked_tma_auto_chunk(uint64_t len, int device) {
     const uint64_t ranges = static_cast<uint64_t>(sms) * kWarps * kRows;
     uint64_t c = (len + ranges - 1) / ranges;
     c = (c + kSlice - 1) / kSlice * kSlice;   // slice multiple: keeps the grid at one CTA per SM
-    if (c < kMidT) c = kMidT;
+    if (c < 2 * kSlice) c = 2 * kSlice;       // small inputs: short ranges (the lookback is 64 B)
     return static_cast<uint32_t>(c);
 }
 
@@ -360,21 +360,17 @@ cudaError_t launch_chunked_tma(const LtTable& t, const void* d_img, const uint8_
     a.cmap_addr = t.cmap_addr;
     a.acc_off = t.acc_off;
     a.ticket = static_cast<unsigned int*>(scratch);
-    a.first_bad = reinterpret_cast<unsigned long long*>(static_cast<uint8_t*>(scratch) + 8);
+    a.bad_inv = reinterpret_cast<unsigned long long*>(static_cast<uint8_t*>(scratch) + 8);
     uint32_t* sc = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(scratch) + 16);
     a.g = sc;
     a.e = sc + a.nranges;
     a.mid = sc + 2 * a.nranges;
     a.accept = accept;
     a.repairs = repairs;
-    // ticket = 0, first_bad = ~0 (device-side memsets: no host staging)
-    cudaError_t e = cudaMemsetAsync(scratch, 0, 8, st);
-    if (e == cudaSuccess) e = cudaMemsetAsync(static_cast<uint8_t*>(scratch) + 8, 0xFF, 8, st);
+    // ticket = 0 and bad_inv = 0 (no wrong guess): one 16-byte memset
+    const cudaError_t e = cudaMemsetAsync(scratch, 0, 16, st);
     if (e != cudaSuccess) return e;
-    if (len == 0) {
-        // empty string: accept iff the start state accepts; reuse the repair kernel with no ranges
-        return t.cls ? run<true>(t, a, device, st) : run<false>(t, a, device, st);
-    }
+    // (len == 0: one CTA, no ranges; the repair pass answers from the start state)
     return t.cls ? run<true>(t, a, device, st) : run<false>(t, a, device, st);
 }
 
