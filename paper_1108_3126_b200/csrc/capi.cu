@@ -385,7 +385,7 @@ int ensure_stage(rxg_heap* h, size_t bytes) {
 int batch_device(rxg_heap* h, const uint8_t* d_text, uint64_t len, int32_t delimiter, uint32_t stride,
                  unsigned long long* d_count, uint8_t* d_results, cudaStream_t st, bool zero_count) {
     LaunchStats ls;
-    if (zero_count) RXG_CUDA(cudaMemsetAsync(d_count, 0, sizeof(unsigned long long), st));
+    if (zero_count) RXG_CUDA(write_u64(d_count, 0, st));
     if (delimiter >= 0) {
         if (delimiter > 255) return fail(RXG_EINVAL, "delimiter must be a byte");
         if (reinterpret_cast<uintptr_t>(d_text) & 15) return fail(RXG_EINVAL, "text must be 16-byte aligned");
@@ -860,7 +860,7 @@ int batch_any(rxg_heap* h, const uint8_t* d_text, uint64_t len, int32_t delimite
     if (delimiter < 0 || delimiter > 255) return fail(RXG_EUNSUPPORTED, "the bitset batch engine takes delimited lines");
     const PernodeTables* t = nullptr;
     if (int rc = pernode_tables(h, &t)) return rc;
-    if (zero_count) RXG_CUDA(cudaMemsetAsync(d_count, 0, sizeof(unsigned long long), st));
+    if (zero_count) RXG_CUDA(write_u64(d_count, 0, st));
     const size_t sb = lines_bitset_scratch_bytes(len);
     void* scratch = nullptr;
     RXG_CUDA(cudaMallocAsync(&scratch, sb, st));
@@ -934,11 +934,11 @@ int rxg_match_batch_host_ex(rxg_heap* h, const uint8_t* text, uint64_t len, int3
         cudaEventCreateWithFlags(&copied[i], cudaEventDisableTiming);
         cudaEventCreateWithFlags(&consumed[i], cudaEventDisableTiming);
     }
-    RXG_CUDA(cudaMemsetAsync(h->d_count, 0, sizeof(unsigned long long), h->stream));
+    RXG_CUDA(write_u64(h->d_count, 0, h->stream));
     unsigned long long* d_bad = nullptr;
     if (utf8_first_bad) {
         RXG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_bad), sizeof(unsigned long long), h->stream));
-        RXG_CUDA(cudaMemsetAsync(d_bad, 0xFF, sizeof(unsigned long long), h->stream));
+        RXG_CUDA(write_u64(d_bad, ~0ull, h->stream));
     }
     int rc = RXG_OK;
     int launches = 1;
@@ -990,7 +990,7 @@ int rxg_utf8_check(int device, const uint8_t* d_text, uint64_t len, int32_t deli
     DeviceGuard g(device);
     const cudaStream_t st = static_cast<cudaStream_t>(stream);
     auto* out = reinterpret_cast<unsigned long long*>(d_first_bad);
-    RXG_CUDA(cudaMemsetAsync(out, 0xFF, sizeof(unsigned long long), st));
+    RXG_CUDA(write_u64(out, ~0ull, st));
     const cudaError_t e = launch_utf8_check(d_text, len, delimiter, delimiter < 0 ? stride : 0, 0, out, device, st);
     if (e != cudaSuccess) return cuda_fail(e, "launch_utf8_check");
     g_launches = len ? 1 : 0;

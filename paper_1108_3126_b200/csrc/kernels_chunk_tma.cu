@@ -367,7 +367,7 @@ cudaError_t launch_chunked_tma(const LtTable& t, const void* d_img, const uint8_
     a.mid = sc + 2 * a.nranges;
     a.accept = accept;
     a.repairs = repairs;
-    // ticket = 0 and bad_inv = 0 (no wrong guess): one 16-byte memset
+    // ticket = 0 and bad_inv = 0 (no wrong guess)
     const cudaError_t e = cudaMemsetAsync(scratch, 0, 16, st);
     if (e != cudaSuccess) return e;
     // (len == 0: one CTA, no ranges; the repair pass answers from the start state)

@@ -241,8 +241,8 @@ cudaError_t launch_chunked(const DevTable& t, const uint8_t* text, uint64_t len,
     a.repairs = repairs;
     if (chunk == 0 || chunk % kMid) return cudaErrorInvalidValue;
     {
-        cudaError_t e = cudaMemsetAsync(scratch, 0, 8, st);   // ticket
-        if (e == cudaSuccess) e = cudaMemsetAsync(static_cast<uint8_t*>(scratch) + 8, 0xFF, 8, st);   // first_bad
+        cudaError_t e = write_u64(scratch, 0, st);   // ticket
+        if (e == cudaSuccess) e = write_u64(static_cast<uint8_t*>(scratch) + 8, ~0ull, st);   // first_bad
         if (e != cudaSuccess) return e;
     }
     if (t.esize == 2) return t.cls ? run<uint16_t, true>(t, a, device, st) : run<uint16_t, false>(t, a, device, st);

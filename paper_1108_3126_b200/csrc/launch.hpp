@@ -47,4 +47,7 @@ cudaError_t launch_fixed_abs(const DevTable& t_abs, const uint8_t* text, uint64_
 
 int device_sm_count(int device);
 
+// Stream-ordered store of 0 or ~0 to one u64 (counters, tickets).
+cudaError_t write_u64(void* dst, uint64_t value, cudaStream_t st);
+
 }  // namespace rxg
