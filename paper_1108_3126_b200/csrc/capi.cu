@@ -432,9 +432,22 @@ int batch_device(rxg_heap* h, const uint8_t* d_text, uint64_t len, int32_t delim
         const DevTable* t = nullptr;
         const DevTable* ta = nullptr;
         if (int rc = plain_table(h, &t, &ta)) return rc;
-        const cudaError_t e = ta && stride % 16 == 0
-                                  ? launch_fixed_abs(*ta, d_text, len / stride, stride, d_count, d_results, st, &ls)
-                                  : launch_fixed(*t, d_text, len / stride, stride, d_count, d_results, st, &ls);
+        cudaError_t e;
+        if (ta && fixed_tma_fits(ta->img_bytes, stride, h->smem_limit) && !std::getenv("RXG_NO_FIXED_TMA")) {
+            uint64_t done = 0;
+            const uint64_t n = len / stride;
+            e = launch_fixed_tma(*ta, d_text, n, stride, d_count, d_results, h->device, st, &done);
+            ls.kernels = done ? 1 : 0;
+            if (e == cudaSuccess && done < n) {   // the few strings past the last full TMA row
+                LaunchStats l2;
+                e = launch_fixed_abs(*ta, d_text + done * stride, n - done, stride, d_count,
+                                     d_results ? d_results + done : nullptr, st, &l2);
+                ls.kernels += l2.kernels;
+            }
+        } else {
+            e = ta && stride % 16 == 0 ? launch_fixed_abs(*ta, d_text, len / stride, stride, d_count, d_results, st, &ls)
+                                       : launch_fixed(*t, d_text, len / stride, stride, d_count, d_results, st, &ls);
+        }
         if (e != cudaSuccess) return cuda_fail(e, "launch_fixed");
     }
     g_launches = static_cast<int>(ls.kernels) + (zero_count ? 0 : 0);

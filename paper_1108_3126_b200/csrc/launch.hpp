@@ -47,6 +47,14 @@ cudaError_t launch_fixed_abs(const DevTable& t_abs, const uint8_t* text, uint64_
 
 int device_sm_count(int device);
 
+// Fixed stride on the TMA data path (stride a multiple of 32; the absolute
+// raw-byte u16 table plus a 144 KB ring must fit shared memory).
+bool fixed_tma_fits(uint32_t img_bytes, uint32_t stride, int smem_limit);
+// *n_done = strings handled (stride 32 leaves the last n % 4 to the caller).
+cudaError_t launch_fixed_tma(const DevTable& t_abs, const uint8_t* text, uint64_t n, uint32_t stride,
+                             unsigned long long* count, uint8_t* results, int device, cudaStream_t st,
+                             uint64_t* n_done);
+
 // Stream-ordered store of 0 or ~0 to one u64 (counters, tickets).
 cudaError_t write_u64(void* dst, uint64_t value, cudaStream_t st);
 

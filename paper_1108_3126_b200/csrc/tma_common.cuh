@@ -59,6 +59,16 @@ __device__ __forceinline__ void issue(const CUtensorMap* map, uint32_t dst, uint
         : "memory");
 }
 
+// One bulk (non-tensor) copy global -> shared of `bytes` (multiple of 16,
+// both addresses 16-byte aligned) completing on mbarrier `bar`; called by one
+// thread after the barrier is initialised.
+__device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(bar)
+                 : "memory");
+}
+
 // Physical 16-byte granule of logical granule g in row r of a stage (TMA
 // swizzle none / 32B / 64B / 128B by slice width).
 template <int SL>

@@ -167,3 +167,25 @@ def test_generic_line_kernel_results(key):
         os.environ.pop("RXG_NO_LT", None)
     assert c1 == c2 == c3 == want_c
     assert np.array_equal(r1, want_r) and np.array_equal(r2, want_r)
+
+
+@pytest.mark.parametrize("stride", [32, 64, 96, 48])
+@pytest.mark.parametrize("n", [1, 95, 96, 97, 20_011])
+def test_fixed_stride_kernels(stride, n):
+    """Fixed-stride batches: the TMA kernel (stride a multiple of 32), the LDG
+    kernel (RXG_NO_FIXED_TMA, and stride 48) and the oracle agree per string."""
+    rng = np.random.default_rng(stride * 1000 + n)
+    for pat in ["(a|b)*abb", rx.synth_pattern("b"), "(a|())(a|())aa(a|b)*"]:
+        text = np.frombuffer(b"ab", np.uint8)[rng.integers(0, 2, n * stride)]
+        if "abb" in pat:
+            text.reshape(n, stride)[::3, -3:] = np.frombuffer(b"abb", np.uint8)
+        want_c, want_r = Oracle(rx.compile(rx.parse(pat))).match_batch(text, -1, stride)
+        m = rx.Matcher(pat, device=0)
+        c1, r1 = m.match_batch(text, -1, stride, results=True)
+        os.environ["RXG_NO_FIXED_TMA"] = "1"
+        try:
+            c2, r2 = m.match_batch(text, -1, stride, results=True)
+        finally:
+            os.environ.pop("RXG_NO_FIXED_TMA", None)
+        assert c1 == c2 == want_c, (pat, c1, c2, want_c)
+        assert np.array_equal(r1, want_r) and np.array_equal(r2, want_r)
