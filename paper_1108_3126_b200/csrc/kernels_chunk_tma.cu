@@ -112,10 +112,6 @@ __device__ uint32_t walk(const Args& a, uint32_t s, uint64_t lo, uint64_t hi) {
     return s;
 }
 
-__device__ __forceinline__ void load_image(const Args& a, uint8_t* sm) {
-    for (uint32_t i = threadIdx.x; i < a.img_words; i += blockDim.x) reinterpret_cast<uint4*>(sm)[i] = a.img[i];
-}
-
 template <bool CLS>
 __device__ uint32_t entry_guess(const Args& a, uint64_t r) {
     const uint64_t c0 = r * a.chunk;
@@ -179,14 +175,20 @@ __global__ void __launch_bounds__(kWarps * 32) k_chunk_tma(const __grid_constant
                                                            const __grid_constant__ CUtensorMap map) {
     extern __shared__ __align__(1024) uint8_t sm[];
     if (static_cast<uint32_t>(__cvta_generic_to_shared(sm)) != kLtSmemBase) __trap();
-    load_image(a, sm);
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t bar0 = a.bar_addr + warp * kStages * 8;
+    const uint32_t tbar = a.bar_addr + kWarps * kStages * 8 + 8;   // after the ring barriers and the `last` flag
+    if (threadIdx.x == 0) {   // the table image by one bulk copy
+        tma::mbar_init(tbar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        tma::bulk_load(kLtSmemBase, a.img, a.img_words * 16u, tbar);
+    }
     if (lane == 0) {
         for (int st = 0; st < kStages; ++st) tma::mbar_init(bar0 + st * 8, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
+    tma::mbar_wait(tbar, 0);
     const uint32_t per = (a.chunk + kMidT - 1) / kMidT;   // checkpoints per range (the last may be partial)
     // the remainder range (past the last full row) walks with direct loads
     if (blockIdx.x == 0 && threadIdx.x == 0 && a.nranges > a.rows) {
@@ -309,7 +311,7 @@ cudaError_t run(const LtTable& t, Args& a, int device, cudaStream_t st) {
     uint32_t p = align_up(t.smem_table_end, 1024);
     for (int k = 0; k < kWarps * kStages; ++k, p += kStageBytes) a.stage_addr[k] = p;
     a.bar_addr = align_up(p, 8);
-    const uint32_t smem = a.bar_addr + kWarps * kStages * 8 + 16 - kLtSmemBase;
+    const uint32_t smem = a.bar_addr + kWarps * kStages * 8 + 16 - kLtSmemBase;   // ring barriers, `last`, table barrier
     CUtensorMap map;
     std::memset(&map, 0, sizeof(map));
     if (a.rows > 0 && tma::make_map(&map, a.text, a.rows, a.chunk, kSlice, kRows) != CUDA_SUCCESS)

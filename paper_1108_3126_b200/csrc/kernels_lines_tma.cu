@@ -238,20 +238,35 @@ __global__ void __launch_bounds__(C::warps * 32) k_lines_tma(const __grid_consta
     extern __shared__ __align__(1024) uint8_t sm[];
     const uint32_t base = static_cast<uint32_t>(__cvta_generic_to_shared(sm));
     if (base != kLtSmemBase) __trap();   // the table's absolute addresses assume this window
-    {
-        uint4* lo = reinterpret_cast<uint4*>(sm + (a.lo_addr - base));
-        for (uint32_t i = threadIdx.x; i < a.lo_words; i += blockDim.x) lo[i] = a.img_lo[i];
-        uint4* hi = reinterpret_cast<uint4*>(sm + (a.hi_addr - base));
-        for (uint32_t i = threadIdx.x; i < a.hi_words; i += blockDim.x) hi[i] = a.img_hi[i];
-    }
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t bar0 = a.bar_addr + warp * C::stages * 8;
+    // the table images arrive by bulk copy (one request each, not a per-thread
+    // load/store loop); the stage ring may live in the image's unused rows, so
+    // no stage is filled before the images have landed
+    const uint32_t tbar = a.bar_addr + C::warps * C::stages * 8;
+    if (threadIdx.x == 0) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map)) : "memory");
+        mbar_init(tbar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(tbar),
+                     "r"((a.lo_words + a.hi_words) * 16u)
+                     : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         a.lo_addr),
+                     "l"(reinterpret_cast<uint64_t>(a.img_lo)), "r"(a.lo_words * 16u), "r"(tbar)
+                     : "memory");
+        if (a.hi_words)
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                             a.hi_addr),
+                         "l"(reinterpret_cast<uint64_t>(a.img_hi)), "r"(a.hi_words * 16u), "r"(tbar)
+                         : "memory");
+    }
     if (lane == 0) {
         for (int st = 0; st < C::stages; ++st) mbar_init(bar0 + st * 8, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (threadIdx.x == 0) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map)) : "memory");
-    __syncthreads();
+    __syncthreads();   // barrier initialisation visible to every thread
+    mbar_wait(tbar, 0);
 
     uint32_t cnt = 0;
     if (blockIdx.x == 0 && warp == 0) {
@@ -365,7 +380,7 @@ uint32_t place_stages(const LtTable& t, Args& a) {
     uint32_t p = align_up(t.cls ? t.smem_table_end : kLtAccAddr + t.hi_bytes, 1024);
     for (; k < C::warps * C::stages; ++k, p += C::stage_bytes) a.stage_addr[k] = p;
     a.bar_addr = align_up(p, 8);
-    return a.bar_addr + C::warps * C::stages * 8 - kLtSmemBase;
+    return a.bar_addr + C::warps * C::stages * 8 + 8 - kLtSmemBase;   // ring barriers + the table barrier
 }
 
 CUtensorMapSwizzle swizzle_of(int slice) {
