@@ -1,0 +1,8 @@
+# All configs through bench.py (defaults: CPU baseline + e2e), then the reference arm for (c).
+mkdir -p gpurun_out/bench
+for c in c d b e a; do
+  python bench.py --config $c > gpurun_out/bench/bench_$c.json 2> gpurun_out/bench/bench_$c.err
+  tail -1 gpurun_out/bench/bench_$c.json | cut -c1-200
+done
+python bench.py --impl reference > gpurun_out/bench/ref_c.json 2> gpurun_out/bench/ref_c.err
+tail -1 gpurun_out/bench/ref_c.json | cut -c1-200
