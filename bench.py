@@ -287,8 +287,9 @@ def main():
     nbytes = len(text_np)
     units = count_units(text_np, delim, stride)
     m = rx.Matcher(pattern, device=dev)
-    if delim >= 0:
-        m.tune(text_np[: 1 << 20], delimiter=delim)   # planner: table bank placement from a 1 MiB sample
+    # planner: table bank placement from a 1 MiB sample (lines, or the single-string table)
+    if delim >= 0 or single:
+        m.tune(text_np[: 1 << 20], delimiter=delim if delim >= 0 else -1)
     info = m.info()
 
     host = torch.from_numpy(text_np).pin_memory()

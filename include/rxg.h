@@ -83,12 +83,13 @@ typedef struct rxg_heap_info {
     int32_t positions;     /* |C| (Chr nodes) */
     int32_t words;         /* W = ceil((|C|+1)/32) */
     int32_t classes;       /* byte classes (class 0 = matches nothing) */
-    int32_t dfa_states;    /* memoized E sets (0 if over the cap) */
+    int32_t dfa_states;    /* states of the minimised memoized step (0 if over the cap) */
     int32_t byte_symbols;  /* 1 if every literal is ASCII */
     int32_t device;        /* CUDA device, or -1 for a host-only handle */
     int32_t nullable;      /* root eps-reaches null: the empty string matches */
     uint32_t line_table_bytes;   /* shared-memory image for '\n' lines (0 if none) */
     uint32_t plain_table_bytes;  /* shared-memory image for single strings / fixed stride */
+    int32_t dfa_sets;      /* distinct memoized E sets before minimisation (0 if over the cap) */
 } rxg_heap_info;
 
 const char* rxg_strerror(int status);

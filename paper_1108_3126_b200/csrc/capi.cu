@@ -77,6 +77,7 @@ struct rxg_heap {
     int device = -1;
     Program prog;
     bool dfa_ok = false;
+    int32_t dfa_sets = 0;   // states before minimisation
     Dfa dfa;
     int smem_limit = 0;
     std::mutex mu;
@@ -347,6 +348,7 @@ int make_heap(Heap&& hp, int device, rxg_heap** out) {
     h->device = device;
     h->prog = build_program(hp);
     h->dfa_ok = build_dfa(h->prog, kMaxDfaStates, h->dfa);
+    if (h->dfa_ok) h->dfa_sets = minimize_dfa(h->dfa);
     if (device >= 0) {
         DeviceGuard g(device);
         int ndev = 0;
@@ -618,6 +620,7 @@ int rxg_heap_info_get(const rxg_heap* h, rxg_heap_info* info) {
     info->words = h->prog.W;
     info->classes = h->prog.n_classes;
     info->dfa_states = h->dfa_ok ? h->dfa.n_states : 0;
+    info->dfa_sets = h->dfa_ok ? h->dfa_sets : 0;
     info->byte_symbols = h->prog.byte_symbols;
     info->device = h->device;
     info->nullable = h->prog.test(h->prog.init, h->prog.n_pos);
@@ -1065,6 +1068,7 @@ int rxg_match_many(int device, const char* patterns, int32_t n_patterns, const u
                 if (bad_pattern) *bad_pattern = k;
                 return fail(RXG_ETOOBIG, "pattern " + std::to_string(k) + ": memoized step table too large");
             }
+            minimize_dfa(d);
             const uint32_t S = static_cast<uint32_t>(d.n_states), C = static_cast<uint32_t>(pg.n_classes);
             const uint32_t acc_off = 256, rows_off = (256 + S + 15) & ~15u;
             const uint32_t bytes = (rows_off + S * C * 2 + 15) & ~15u;

@@ -285,6 +285,57 @@ bool build_dfa(const Program& p, int32_t max_states, Dfa& d) {
     return d.dead >= 0;
 }
 
+int32_t minimize_dfa(Dfa& d, uint64_t max_work) {
+    const int32_t S = d.n_states, C = d.n_classes;
+    if (S <= 1) return S;
+    std::vector<int32_t> blk(static_cast<size_t>(S)), nb(static_cast<size_t>(S));
+    for (int32_t s = 0; s < S; ++s) blk[static_cast<size_t>(s)] = d.accept[static_cast<size_t>(s)];
+    int32_t nblocks = -1;
+    uint64_t work = 0;
+    std::vector<int32_t> sig(static_cast<size_t>(C) + 1);
+    for (;;) {
+        std::unordered_map<std::string, int32_t> ids;
+        ids.reserve(static_cast<size_t>(S) * 2);
+        for (int32_t s = 0; s < S; ++s) {
+            sig[0] = blk[static_cast<size_t>(s)];
+            for (int32_t c = 0; c < C; ++c)
+                sig[static_cast<size_t>(c) + 1] = blk[static_cast<size_t>(d.next[static_cast<size_t>(s) * C + c])];
+            std::string key(reinterpret_cast<const char*>(sig.data()), sig.size() * sizeof(int32_t));
+            auto it = ids.emplace(std::move(key), static_cast<int32_t>(ids.size())).first;
+            nb[static_cast<size_t>(s)] = it->second;
+        }
+        work += static_cast<uint64_t>(S) * static_cast<uint64_t>(C + 1);
+        const int32_t k = static_cast<int32_t>(ids.size());
+        blk.swap(nb);
+        if (k == nblocks) break;   // stable: the partition no longer splits
+        nblocks = k;
+        if (work > max_work) return S;
+    }
+    if (nblocks == S) return S;
+    Dfa m;
+    m.n_states = nblocks;
+    m.n_classes = C;
+    const size_t W = d.sets.size() / static_cast<size_t>(S);
+    std::vector<int32_t> rep(static_cast<size_t>(nblocks), -1);
+    for (int32_t s = 0; s < S; ++s)
+        if (rep[static_cast<size_t>(blk[static_cast<size_t>(s)])] < 0) rep[static_cast<size_t>(blk[static_cast<size_t>(s)])] = s;
+    m.next.resize(static_cast<size_t>(nblocks) * C);
+    m.accept.resize(static_cast<size_t>(nblocks));
+    m.sets.resize(static_cast<size_t>(nblocks) * W);
+    for (int32_t b = 0; b < nblocks; ++b) {
+        const int32_t r = rep[static_cast<size_t>(b)];
+        m.accept[static_cast<size_t>(b)] = d.accept[static_cast<size_t>(r)];
+        for (int32_t c = 0; c < C; ++c)
+            m.next[static_cast<size_t>(b) * C + c] = blk[static_cast<size_t>(d.next[static_cast<size_t>(r) * C + c])];
+        std::copy(d.sets.begin() + static_cast<std::ptrdiff_t>(r * W), d.sets.begin() + static_cast<std::ptrdiff_t>((r + 1) * W),
+                  m.sets.begin() + static_cast<std::ptrdiff_t>(b * W));
+    }
+    m.start = blk[static_cast<size_t>(d.start)];
+    m.dead = d.dead >= 0 ? blk[static_cast<size_t>(d.dead)] : -1;
+    d = std::move(m);
+    return S;
+}
+
 BitsetPlan build_bitset_plan(const Program& p) {
     const size_t W = static_cast<size_t>(p.W);
     BitsetPlan plan;

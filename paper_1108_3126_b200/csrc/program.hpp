@@ -66,6 +66,13 @@ struct Dfa {
 // partially filled) if more than max_states states would be needed.
 bool build_dfa(const Program& p, int32_t max_states, Dfa& out);
 
+// Moore partition refinement: merges states with the same accept bit on
+// every continuation (the kernels only need each string's accept bit, which
+// the minimal automaton gives for every input). `sets` keeps one member's E
+// set per merged state. Returns the state count before minimisation; leaves
+// the automaton unchanged if the refinement would exceed `max_work` steps.
+int32_t minimize_dfa(Dfa& d, uint64_t max_work = 400'000'000ull);
+
 // Decomposition of F' used by the bitset kernels:
 //   F'(q) = ({q+1} if shift[q]) ∪ R(q),   R(q) = rows[group[q]] (group -1 = empty)
 // Identical residual rows share one group (dedup by row equality).

@@ -88,6 +88,14 @@ __device__ __forceinline__ uint32_t step(uint32_t s, uint32_t b, uint32_t row_by
     else return lds16(s + b * kLtColBytes);
 }
 
+// Same step on byte k of a word: one IDP.4A extracts the byte, scales it and
+// adds the base (the row for the direct layout, the class map otherwise).
+template <bool CLS>
+__device__ __forceinline__ uint32_t step_w(uint32_t s, uint32_t word, int k, uint32_t row_bytes, uint32_t cmap_addr) {
+    if constexpr (CLS) return lds16(s * row_bytes + lds32(__dp4a(word, 4u << (8 * k), cmap_addr)));
+    else return lds16(__dp4a(word, kLtColBytes << (8 * k), s));
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn();
 
 // 2-D view [rows][chunk] of `text` with a (slice x box_rows) box.

@@ -171,3 +171,25 @@ def test_dfa_tables_against_reference_random():
         assert c == rc and np.array_equal(res, rr), p
         if m.info()["dfa_states"] <= 25:
             assert m.emulate_lines_tma(text, 10, 32) == rc
+
+
+def test_minimised_memoized_step():
+    """Moore refinement of the memoized step: the kernels only need each
+    string's accept bit, so states with the same accept bit on every
+    continuation merge. (e)'s keyword union is absorbed by the star of single
+    letters ([a-z ]*abb: 1,209 E sets, 5 states); (d) halves. Per-string
+    results of the minimised table equal the oracle's."""
+    want = {"a": (5, 5), "c": (14, 14), "d": (624, 309), "e": (1209, 5)}
+    for cfg, (sets, states) in want.items():
+        i = rx.Matcher(rx.synth_pattern(cfg), device=-1).info()
+        assert (i["dfa_sets"], i["dfa_states"]) == (sets, states), cfg
+    rng = np.random.default_rng(8)
+    for p in ["(a|b|ab|ba|aab)*abb", "((a|b)*a(a|b)|a)*", "(aa|ab|ba|bb)*", "(a|())*(b|())*a*", "((ab)*|(ba)*)*b"]:
+        m = rx.Matcher(p, device=-1)
+        i = m.info()
+        assert 0 < i["dfa_states"] <= i["dfa_sets"]
+        lines = [bytes(rng.choice([97, 98], size=int(rng.integers(0, 14))).astype(np.uint8)) for _ in range(3000)]
+        text = np.frombuffer(b"\n".join(lines) + b"\n", np.uint8)
+        ocount, ores = Oracle(rx.compile(rx.parse(p))).match_batch(text, 10, 0)
+        count, res = m.emulate_batch(text, 10, 0, 64)
+        assert count == ocount and np.array_equal(res, ores), p

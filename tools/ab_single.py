@@ -13,6 +13,9 @@ m = rx.Matcher(pat, device=0)
 acc = torch.zeros(1, dtype=torch.int32, device=0)
 rep = torch.zeros(1, dtype=torch.int64, device=0)
 for v in sys.argv[3:]:
+    if v == "tune":   # bank placement of the single-string table from a 1 MiB sample
+        m.tune(text[: 1 << 20], delimiter=-1)
+        continue
     eng, _, reps = v.partition(":")
     reps = int(reps or 3)
     kw = {"d_repairs": rep} if eng in ("chunked", "auto") else {}
