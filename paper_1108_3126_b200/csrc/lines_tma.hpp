@@ -53,12 +53,23 @@ std::vector<double> lt_sample_freq_plain(const Program& p, const Dfa& d, const u
 // stage ring goes after smem_table_end.
 LtTable make_chunk_tma_table(const Program& p, const Dfa& d, const std::vector<double>* freq = nullptr);
 
+// Row pairing + bank placement of the direct layouts (see lines_tma_table.cpp).
+struct RowPlacement {
+    std::vector<uint32_t> pair, half;   // per row: its pair and half (0 = low u16, 1 = high)
+    std::vector<uint32_t> pair_off;     // per pair: bank offset (words mod 32)
+    uint32_t npairs = 0;
+};
+RowPlacement lt_place_pairs(const std::vector<double>* freq, uint32_t nrows, bool pair_rows);
+
 // Host emulation of the table walk, for CPU tests.
 uint32_t lt_step(const LtTable& t, uint32_t s, uint8_t byte);
 inline uint32_t lt_count(const LtTable& t, uint32_t s) { return s >> t.acc_shift; }
 
-// Largest DFA the direct layout takes; bigger ones use the class layout.
-constexpr int32_t kLtDirectMaxStates = 25;
+// Largest DFA the direct layouts take (rows of 256 columns, absolute u16
+// addresses below 64 KB: two rows per column word for lines, one for the
+// single-string table); bigger ones use the class layout.
+constexpr int32_t kLtDirectMaxStates = 52;
+constexpr int32_t kLtChunkDirectMaxStates = 56;
 
 // chunk = bytes per range (multiple of lines_tma_slice()), 0 = one wave of ranges.
 cudaError_t launch_lines_tma(const LtTable& t, const uint8_t* text, uint64_t len, uint8_t delim, uint32_t chunk,

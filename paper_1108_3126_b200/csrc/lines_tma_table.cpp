@@ -19,6 +19,7 @@
 // never results.
 #include <algorithm>
 #include <array>
+#include <cstdlib>
 #include <cstring>
 
 #include "lines_tma.hpp"
@@ -33,6 +34,8 @@ void put16(std::vector<uint8_t>& img, uint32_t off, uint32_t v) {
 }
 
 uint32_t align_up(uint32_t x, uint32_t a) { return (x + a - 1) / a * a; }
+
+LtTable make_direct_table(const Program& p, const Dfa& d, uint8_t delim, const std::vector<double>* freq);
 
 }  // namespace
 
@@ -59,14 +62,26 @@ std::vector<double> lt_sample_freq_plain(const Program& p, const Dfa& d, const u
     return f;
 }
 
-std::vector<uint32_t> lt_place_rows(const std::vector<double>& f, uint32_t nrows) {
-    // 32-bin bank histograms per row (byte b of a row sits in bank (offset + b) mod 32)
+// Rows of the direct layouts hold u16 entries in 4-byte columns, so two rows
+// share every column word: row A's entry for byte b in the low half, row B's
+// in the high half. Lanes in A and B reading the same byte read the same word
+// (one wavefront); reading different bytes they hit different banks, as in a
+// single row. Pairing the hottest rows therefore removes their mutual bank
+// conflicts outright ((c): 86% + 13% of all steps sit in two states).
+// Rows are paired in order of sampled frequency, then each pair gets the bank
+// offset that collides least with the pairs already placed.
+RowPlacement lt_place_pairs(const std::vector<double>* f, uint32_t nrows, bool pair_rows) {
+    RowPlacement pl;
+    pl.pair.assign(nrows, 0);
+    pl.half.assign(nrows, 0);
     std::vector<std::array<double, 32>> H(nrows);
     std::vector<double> tot(nrows, 0.0);
     for (uint32_t r = 0; r < nrows; ++r) {
         H[r].fill(0.0);
+        if (!f) continue;
         for (int b = 0; b < 256; ++b) {
-            const double x = r * 256u + static_cast<uint32_t>(b) < f.size() ? f[r * 256u + static_cast<uint32_t>(b)] : 0.0;
+            const size_t i = static_cast<size_t>(r) * 256u + static_cast<size_t>(b);
+            const double x = i < f->size() ? (*f)[i] : 0.0;
             H[r][static_cast<size_t>(b & 31)] += x;
             tot[r] += x;
         }
@@ -74,28 +89,40 @@ std::vector<uint32_t> lt_place_rows(const std::vector<double>& f, uint32_t nrows
     std::vector<uint32_t> order(nrows);
     for (uint32_t r = 0; r < nrows; ++r) order[r] = r;
     std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return tot[a] > tot[b]; });
-    std::vector<uint32_t> off(nrows, 0);
+    const uint32_t per = pair_rows && !std::getenv("RXG_NO_ROW_PAIRS") ? 2u : 1u;   // env: A/B switch (tools)
+    pl.npairs = (nrows + per - 1) / per;
+    std::vector<std::array<double, 32>> HP(pl.npairs);
+    std::vector<double> tp(pl.npairs, 0.0);
+    for (uint32_t i = 0; i < nrows; ++i) {
+        const uint32_t r = order[i], q = i / per;
+        pl.pair[r] = q;
+        pl.half[r] = i % per;
+        if (i % per == 0) HP[q].fill(0.0);
+        for (int k = 0; k < 32; ++k) HP[q][static_cast<size_t>(k)] += H[r][static_cast<size_t>(k)];
+        tp[q] += tot[r];
+    }
+    pl.pair_off.assign(pl.npairs, 0);
     std::vector<uint32_t> placed;
-    for (uint32_t r : order) {
-        if (tot[r] == 0.0) {
-            off[r] = (r * 9u) & 31u;
+    for (uint32_t q = 0; q < pl.npairs; ++q) {   // pairs are already in hotness order
+        if (tp[q] == 0.0) {
+            pl.pair_off[q] = (q * 9u) & 31u;
             continue;
         }
         double best = -1.0;
         uint32_t bo = 0;
         for (uint32_t o = 0; o < 32; ++o) {
             double c = 0.0;
-            for (uint32_t r2 : placed)
-                for (uint32_t k = 0; k < 32; ++k) c += H[r][k] * H[r2][(k + o + 32 - off[r2]) & 31u];
+            for (uint32_t q2 : placed)
+                for (uint32_t k = 0; k < 32; ++k) c += HP[q][k] * HP[q2][(k + o + 32 - pl.pair_off[q2]) & 31u];
             if (best < 0.0 || c < best) {
                 best = c;
                 bo = o;
             }
         }
-        off[r] = bo;
-        placed.push_back(r);
+        pl.pair_off[q] = bo;
+        placed.push_back(q);
     }
-    return off;
+    return pl;
 }
 
 namespace {
@@ -239,27 +266,29 @@ LtTable make_class_table(const Program& p, const Dfa& d, uint8_t delim, const st
 LtTable make_lines_tma_table(const Program& p, const Dfa& d, uint8_t delim, const std::vector<double>* freq,
                              bool force_class) {
     if (force_class || d.n_states > kLtDirectMaxStates) return make_class_table(p, d, delim, freq);
+    LtTable t = make_direct_table(p, d, delim, freq);
+    return t.ok ? t : make_class_table(p, d, delim, freq);   // the direct rows did not fit below 64 KB
+}
+
+namespace {
+
+LtTable make_direct_table(const Program& p, const Dfa& d, uint8_t delim, const std::vector<double>* freq) {
     LtTable t;
     const uint32_t S = static_cast<uint32_t>(d.n_states);
     const uint32_t R = kLtRowBytes;
-    const uint32_t slot = R + 128;   // worst case row + alignment pad
-    // main rows: states 0..S-1, SKIP (S), VOID (S+1), each at a chosen bank offset
-    std::vector<uint32_t> off;
-    if (freq) {
-        off = lt_place_rows(*freq, S + 2);
-    } else {
-        off.resize(S + 2);
-        for (uint32_t r = 0; r < S + 2; ++r) off[r] = (r * 9u) & 31u;
-    }
-    if ((S + 2) * slot + kLtSmemBase > kLtAccAddr) return t;
-    t.lo_addr = (kLtAccAddr - (S + 2) * slot) & ~127u;
-    std::vector<uint32_t> addr(S + 2);
+    const uint32_t slot = R + 128;   // worst case pair + alignment pad
+    // main rows: states 0..S-1, SKIP (S), VOID (S+1), two per column word, each
+    // pair at a chosen bank offset
+    const RowPlacement pl = lt_place_pairs(freq, S + 2, true);
+    if (pl.npairs * slot + kLtSmemBase > kLtAccAddr) return t;
+    t.lo_addr = (kLtAccAddr - pl.npairs * slot) & ~127u;
+    std::vector<uint32_t> paddr(pl.npairs), addr(S + 2);
     uint32_t cur = t.lo_addr;
-    for (uint32_t r = 0; r < S + 2; ++r) {
-        const uint32_t want = off[r] * 4u;
-        addr[r] = cur + ((want + 128u - (cur & 127u)) & 127u);
-        cur = addr[r] + R;
+    for (uint32_t q = 0; q < pl.npairs; ++q) {
+        paddr[q] = cur + ((pl.pair_off[q] * 4u + 128u - (cur & 127u)) & 127u);
+        cur = paddr[q] + R;
     }
+    for (uint32_t r = 0; r < S + 2; ++r) addr[r] = paddr[pl.pair[r]] + 2u * pl.half[r];
     if (cur > kLtAccAddr) return t;
     // upper region: START_A at 0x8000, tail copies at main + tail_delta, TERM rows
     t.tail_delta = align_up(kLtAccAddr + R - t.lo_addr, 128);
@@ -300,12 +329,18 @@ LtTable make_lines_tma_table(const Program& p, const Dfa& d, uint8_t delim, cons
         put_hi(t.term_acc, b, t.term_acc);
         put_hi(t.term_rej, b, t.term_rej);
     }
-    std::memcpy(&t.hi[0], &t.lo[t.start - t.lo_addr], R);   // START_A = start row
+    for (int b = 0; b < 256; ++b) {   // START_A = the start row (low halves of its own words)
+        uint16_t v;
+        std::memcpy(&v, &t.lo[t.start - t.lo_addr + kLtColBytes * static_cast<uint32_t>(b)], 2);
+        put_hi(kLtAccAddr, b, v);
+    }
 
     t.smem_table_end = kLtAccAddr + t.hi_bytes;
     t.ok = true;
     return t;
 }
+
+}  // namespace
 
 LtTable make_chunk_tma_table(const Program& p, const Dfa& d, const std::vector<double>* freq) {
     LtTable t;
@@ -314,28 +349,30 @@ LtTable make_chunk_tma_table(const Program& p, const Dfa& d, const std::vector<d
         return static_cast<uint32_t>(d.next[static_cast<size_t>(s) * static_cast<size_t>(d.n_classes) + c]);
     };
     t.lo_addr = kLtSmemBase;
-    if (S <= kLtDirectMaxStates) {
+    if (S <= kLtChunkDirectMaxStates) {
         // direct: rows of 256 four-byte columns at chosen bank offsets
+        // direct: rows of 256 four-byte columns at chosen bank offsets; a row's
+        // accept flag follows its columns. (Row pairs measured slower here:
+        // config (e) 2.96 vs 3.25 TB/s with fewer bank conflicts; unpaired.)
         const uint32_t R = kLtRowBytes;
-        std::vector<uint32_t> off;
-        if (freq) off = lt_place_rows(*freq, S);
-        else for (uint32_t r = 0; r < S; ++r) off.push_back((r * 9u) & 31u);
-        std::vector<uint32_t> addr(S);
+        const RowPlacement pl = lt_place_pairs(freq, S, false);
+        std::vector<uint32_t> paddr(pl.npairs), addr(S);
         uint32_t cur = kLtSmemBase;
-        for (uint32_t r = 0; r < S; ++r) {
-            addr[r] = cur + ((off[r] * 4u + 128u - (cur & 127u)) & 127u);
-            cur = addr[r] + R;
+        for (uint32_t q = 0; q < pl.npairs; ++q) {
+            paddr[q] = cur + ((pl.pair_off[q] * 4u + 128u - (cur & 127u)) & 127u);
+            cur = paddr[q] + R + 4u;
         }
+        for (uint32_t r = 0; r < S; ++r) addr[r] = paddr[pl.pair[r]] + 2u * pl.half[r];
         if (cur > 0x10000u) return t;
         t.lo_bytes = align_up(cur - kLtSmemBase, 16);
         t.lo.assign(t.lo_bytes, 0);
         for (uint32_t s = 0; s < S; ++s) {
             for (int b = 0; b < 256; ++b)
                 put16(t.lo, addr[s] - kLtSmemBase + kLtColBytes * static_cast<uint32_t>(b), addr[next(s, p.byte_class[b])]);
-            put16(t.lo, addr[s] - kLtSmemBase + 2u, d.accept[s]);   // high half of column 0
+            put16(t.lo, addr[s] - kLtSmemBase + R, d.accept[s]);
         }
         t.start = addr[static_cast<uint32_t>(d.start)];
-        t.acc_off = 2;
+        t.acc_off = R;
     } else {
         t.cls = true;
         const uint32_t ncols = static_cast<uint32_t>(p.n_classes) + 1;   // + the accept column

@@ -189,3 +189,24 @@ def test_fixed_stride_kernels(stride, n):
             os.environ.pop("RXG_NO_FIXED_TMA", None)
         assert c1 == c2 == want_c, (pat, c1, c2, want_c)
         assert np.array_equal(r1, want_r) and np.array_equal(r2, want_r)
+
+
+@pytest.mark.parametrize("k", [3, 4, 5])
+def test_mid_size_dfas_both_layouts(k):
+    """(a|b)*a(a|b)^k needs 2^(k+1) live states: 17 and 33 take the direct layouts
+    (33 only with two rows per column word), 65 the class layout."""
+    pat = "(a|b)*a" + "(a|b)" * k
+    m = rx.Matcher(pat, device=0)
+    assert m.info()["dfa_states"] == 2 ** (k + 1) + 1   # + the dead state
+    rng = np.random.default_rng(k)
+    lines = [bytes(rng.choice([97, 98, 99], size=int(rng.integers(0, 40))).astype(np.uint8)) for _ in range(20000)]
+    text = np.frombuffer(b"\n".join(lines) + b"\n", np.uint8)
+    o = Oracle(rx.compile(rx.parse(pat)))
+    want_c, want_r = o.match_batch(text, 10, 0)
+    m.tune(text[: 1 << 18])
+    assert _dev_count(m, text) == want_c
+    c, r = m.match_batch(text, 10, results=True)
+    assert c == want_c and np.array_equal(r, want_r)
+    w = np.frombuffer(b"ab" * 300_000 + b"a" + b"b" * k, np.uint8)
+    for eng in ("chunked", "dfa_seq"):
+        assert m.lockstep_accepts(w.tobytes(), eng) == o.accepts(w.tobytes()), eng
