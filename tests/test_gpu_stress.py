@@ -169,7 +169,7 @@ def test_generic_line_kernel_results(key):
     assert np.array_equal(r1, want_r) and np.array_equal(r2, want_r)
 
 
-@pytest.mark.parametrize("stride", [32, 64, 96, 48])
+@pytest.mark.parametrize("stride", [32, 64, 96, 48, 7, 33])
 @pytest.mark.parametrize("n", [1, 95, 96, 97, 20_011])
 def test_fixed_stride_kernels(stride, n):
     """Fixed-stride batches: the TMA kernel (stride a multiple of 32), the LDG
