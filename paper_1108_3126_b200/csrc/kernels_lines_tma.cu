@@ -552,7 +552,8 @@ cudaError_t launch(const LtTable& t, const uint8_t* text, uint64_t len, uint8_t 
 // Kernel shapes (RXG_LT_SHAPE=0 forces S0 for tuning runs; unset = per-layout default).
 // Measured on config (c), 1 GB, B200 (tools/ab_lines.py): 16-byte slices are
 // TMA-request bound (~3.3 TB/s); 32-byte slices with 24 warps x 2 ranges x 3
-// stages reach ~5.05 TB/s, x 3 ranges x 2 stages ~5.1 TB/s (direct layout);
+// stages reach ~5.05 TB/s, x 3 ranges x 2 stages ~5.1-5.25 TB/s (direct layout);
+// 24x4x2, 32x3x2 and 16x4x3 measured 4.77-5.0 TB/s with the paired rows;
 // the class layout (two LDS per byte, ~225 KB with its ring) fits only S0.
 using S0 = Shape<24, 2, 32, 3>;
 using S6 = Shape<24, 3, 32, 2>;
