@@ -97,10 +97,13 @@ struct rxg_heap {
     RoundsTables rounds;
     void* d_pernode = nullptr;
     PernodeTables pernode;
+    // CountSlot per stream (launch.hpp): zero when idle, re-zeroed by the kernels
+    std::map<cudaStream_t, unsigned long long*> slots;
 
     ~rxg_heap() {
         if (device < 0) return;
         DeviceGuard g(device);
+        for (auto& kv : slots) cudaFree(kv.second);
         if (plain && plain->dptr) cudaFree(plain->dptr);
         if (plain && plain->d_abs) cudaFree(plain->d_abs);
         if (plain && plain->d_chunk) cudaFree(plain->d_chunk);
@@ -173,6 +176,30 @@ int need_device(rxg_heap* h, bool dfa = true) {
         return fail(RXG_EUNSUPPORTED, "pattern has a literal that is not a Unicode scalar value");
     if (dfa && !h->dfa_ok)
         return fail(RXG_ETOOBIG, "memoized step table exceeds " + std::to_string(kMaxDfaStates) + " states");
+    return RXG_OK;
+}
+
+// The completion slot of `st` (allocated and zeroed on its first use, in
+// stream order).
+int stream_slot(rxg_heap* h, cudaStream_t st, CountSlot* out, bool accumulate) {
+    unsigned long long* p = nullptr;
+    {
+        std::lock_guard<std::mutex> lk(h->mu);
+        auto it = h->slots.find(st);
+        if (it != h->slots.end()) p = it->second;
+    }
+    if (!p) {
+        RXG_CUDA(cudaMalloc(&p, 4 * sizeof(unsigned long long)));
+        RXG_CUDA(cudaMemsetAsync(p, 0, 4 * sizeof(unsigned long long), st));
+        std::lock_guard<std::mutex> lk(h->mu);
+        auto ins = h->slots.emplace(st, p);
+        if (!ins.second) {   // another thread won the race for this stream
+            cudaFree(p);
+            p = ins.first->second;
+        }
+    }
+    out->p = p;
+    out->accumulate = accumulate;
     return RXG_OK;
 }
 
@@ -387,7 +414,13 @@ int ensure_stage(rxg_heap* h, size_t bytes) {
 int batch_device(rxg_heap* h, const uint8_t* d_text, uint64_t len, int32_t delimiter, uint32_t stride,
                  unsigned long long* d_count, uint8_t* d_results, cudaStream_t st, bool zero_count) {
     LaunchStats ls;
-    if (zero_count) RXG_CUDA(write_u64(d_count, 0, st));
+    // TMA kernels publish the count through the stream's slot (no memset);
+    // the other kernels add into a zeroed counter
+    CountSlot cs;
+    if (int rc = stream_slot(h, st, &cs, !zero_count)) return rc;
+    auto zero_count_now = [&]() -> cudaError_t {
+        return zero_count ? write_u64(d_count, 0, st) : cudaSuccess;
+    };
     if (delimiter >= 0) {
         if (delimiter > 255) return fail(RXG_EINVAL, "delimiter must be a byte");
         if (reinterpret_cast<uintptr_t>(d_text) & 15) return fail(RXG_EINVAL, "text must be 16-byte aligned");
@@ -398,7 +431,7 @@ int batch_device(rxg_heap* h, const uint8_t* d_text, uint64_t len, int32_t delim
             if (chunk % lines_tma_slice()) chunk = 0;
             if (!d_results) {
                 const cudaError_t e = launch_lines_tma(slot->lt, d_text, len, static_cast<uint8_t>(delimiter), chunk,
-                                                       d_count, st);
+                                                       d_count, cs, st);
                 if (e != cudaSuccess) return cuda_fail(e, "launch_lines_tma");
                 ls.kernels = 1;
             } else if (len) {   // per-line results: range delimiter counts, scan, the same walk
@@ -407,12 +440,15 @@ int batch_device(rxg_heap* h, const uint8_t* d_text, uint64_t len, int32_t delim
                 void* scratch = nullptr;
                 RXG_CUDA(cudaMallocAsync(&scratch, sb, st));
                 const cudaError_t e = launch_lines_tma_results(slot->lt, d_text, len, static_cast<uint8_t>(delimiter),
-                                                               chunk, d_count, d_results, scratch, sb, st);
+                                                               chunk, d_count, d_results, scratch, sb, cs, st);
                 cudaFreeAsync(scratch, st);
                 if (e != cudaSuccess) return cuda_fail(e, "launch_lines_tma_results");
                 ls.kernels = 3;
+            } else {
+                RXG_CUDA(zero_count_now());
             }
         } else {
+            RXG_CUDA(zero_count_now());
             const DevTable* t = &slot->dev;
             uint32_t chunk = env_chunk();
             if (chunk == 0 || chunk % 16) chunk = lines_auto_chunk(*t, len);
@@ -438,21 +474,24 @@ int batch_device(rxg_heap* h, const uint8_t* d_text, uint64_t len, int32_t delim
         if (ta && fixed_tma_fits(ta->img_bytes, stride, h->smem_limit) && !std::getenv("RXG_NO_FIXED_TMA")) {
             uint64_t done = 0;
             const uint64_t n = len / stride;
-            e = launch_fixed_tma(*ta, d_text, n, stride, d_count, d_results, h->device, st, &done);
+            e = launch_fixed_tma(*ta, d_text, n, stride, d_count, d_results, cs, h->device, st, &done);
             ls.kernels = done ? 1 : 0;
-            if (e == cudaSuccess && done < n) {   // the few strings past the last full TMA row
+            if (e == cudaSuccess && done < n) {   // the few strings past the last full TMA row (adds to the count)
                 LaunchStats l2;
                 e = launch_fixed_abs(*ta, d_text + done * stride, n - done, stride, d_count,
                                      d_results ? d_results + done : nullptr, st, &l2);
                 ls.kernels += l2.kernels;
             }
         } else {
-            e = ta && stride % 16 == 0 ? launch_fixed_abs(*ta, d_text, len / stride, stride, d_count, d_results, st, &ls)
-                                       : launch_fixed(*t, d_text, len / stride, stride, d_count, d_results, st, &ls);
+            e = zero_count_now();
+            if (e == cudaSuccess)
+                e = ta && stride % 16 == 0
+                        ? launch_fixed_abs(*ta, d_text, len / stride, stride, d_count, d_results, st, &ls)
+                        : launch_fixed(*t, d_text, len / stride, stride, d_count, d_results, st, &ls);
         }
         if (e != cudaSuccess) return cuda_fail(e, "launch_fixed");
     }
-    g_launches = static_cast<int>(ls.kernels) + (zero_count ? 0 : 0);
+    g_launches = static_cast<int>(ls.kernels);
     return RXG_OK;
 }
 
@@ -804,9 +843,11 @@ int rxg_match_one_ex(rxg_heap* h, const uint8_t* d_bytes, uint64_t len, int engi
             if (chunk % 32) return fail(RXG_EINVAL, "chunk must be a multiple of 32 on the TMA path");
             void* scratch = nullptr;
             RXG_CUDA(cudaMallocAsync(&scratch, chunked_tma_scratch_bytes(len, chunk), st));
+            CountSlot cs;
+            if (int rc = stream_slot(h, st, &cs, false)) return rc;
             const cudaError_t e = launch_chunked_tma(h->plain->chunk_lt, h->plain->d_chunk, d_bytes, len, chunk,
                                                      o.lookback ? o.lookback : 64, scratch, d_accept, o.d_repairs,
-                                                     h->device, st);
+                                                     cs, h->device, st);
             cudaFreeAsync(scratch, st);
             if (e != cudaSuccess) return cuda_fail(e, "launch_chunked_tma");
             g_launches = 1;   // walk, seam check and repair in one kernel

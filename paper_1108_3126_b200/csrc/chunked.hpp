@@ -21,6 +21,6 @@ uint32_t chunked_tma_auto_chunk(uint64_t len, int device);
 size_t chunked_tma_scratch_bytes(uint64_t len, uint32_t chunk);
 cudaError_t launch_chunked_tma(const LtTable& t, const void* d_img, const uint8_t* text, uint64_t len, uint32_t chunk,
                                uint32_t lookback, void* scratch, int32_t* accept, unsigned long long* repairs,
-                               int device, cudaStream_t st);
+                               CountSlot cs, int device, cudaStream_t st);
 
 }  // namespace rxg

@@ -167,6 +167,9 @@ __device__ void repair_and_answer(const Args& a) {
         const uint32_t acc_addr = CLS ? kLtSmemBase + 1024 + exact * a.row_bytes + a.acc_off : exact + a.acc_off;
         *a.accept = static_cast<int32_t>(tma::lds16(acc_addr));
         if (a.repairs) *a.repairs = repairs;
+        // idle slot for the next launch on this stream (CountSlot, launch.hpp)
+        atomicExch(a.bad_inv, 0ull);
+        atomicExch(a.ticket, 0u);
     }
 }
 
@@ -345,7 +348,7 @@ size_t chunked_tma_scratch_bytes(uint64_t len, uint32_t chunk) {
 
 cudaError_t launch_chunked_tma(const LtTable& t, const void* d_img, const uint8_t* text, uint64_t len, uint32_t chunk,
                                uint32_t lookback, void* scratch, int32_t* accept, unsigned long long* repairs,
-                               int device, cudaStream_t st) {
+                               CountSlot cs, int device, cudaStream_t st) {
     if (chunk == 0 || chunk % kSlice) return cudaErrorInvalidValue;
     Args a{};
     a.text = text;
@@ -361,17 +364,14 @@ cudaError_t launch_chunked_tma(const LtTable& t, const void* d_img, const uint8_
     a.row_bytes = t.row_bytes;
     a.cmap_addr = t.cmap_addr;
     a.acc_off = t.acc_off;
-    a.ticket = static_cast<unsigned int*>(scratch);
-    a.bad_inv = reinterpret_cast<unsigned long long*>(static_cast<uint8_t*>(scratch) + 8);
+    a.ticket = reinterpret_cast<unsigned int*>(cs.p + 1);   // zero when idle: no memset per call
+    a.bad_inv = cs.p + 2;
     uint32_t* sc = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(scratch) + 16);
     a.g = sc;
     a.e = sc + a.nranges;
     a.mid = sc + 2 * a.nranges;
     a.accept = accept;
     a.repairs = repairs;
-    // ticket = 0 and bad_inv = 0 (no wrong guess)
-    const cudaError_t e = cudaMemsetAsync(scratch, 0, 16, st);
-    if (e != cudaSuccess) return e;
     // (len == 0: one CTA, no ranges; the repair pass answers from the start state)
     return t.cls ? run<true>(t, a, device, st) : run<false>(t, a, device, st);
 }

@@ -33,6 +33,8 @@ struct FArgs {
     uint32_t bar_addr;
     uint32_t stage_addr[kFW * kFSt];
     unsigned long long* count;
+    unsigned long long* slot;   // CountSlot (launch.hpp)
+    int accumulate;
     uint8_t* results;
 };
 
@@ -124,7 +126,7 @@ __global__ void __launch_bounds__(kFW * 32) k_fixed_tma(const __grid_constant__ 
         }
     }
     cnt = __reduce_add_sync(0xFFFFFFFFu, cnt);
-    if (lane == 0 && cnt) atomicAdd(a.count, static_cast<unsigned long long>(cnt));
+    tma::publish_count(a.slot, a.count, a.accumulate != 0, cnt, a.bar_addr + kFW * kFSt * 8 + 8);
 }
 
 uint32_t align_up(uint32_t x, uint32_t a) { return (x + a - 1) / a * a; }
@@ -134,7 +136,7 @@ cudaError_t run(FArgs& a, const uint8_t* text, uint32_t stride, uint32_t img_byt
     uint32_t p = align_up(kFBase + img_bytes, 1024);
     for (int k = 0; k < kFW * kFSt; ++k, p += kFStageBytes) a.stage_addr[k] = p;
     a.bar_addr = align_up(p, 8);
-    const uint32_t smem = a.bar_addr + kFW * kFSt * 8 + 8 - kFBase;   // ring barriers + the table barrier
+    const uint32_t smem = a.bar_addr + kFW * kFSt * 8 + 8 + 4 * kFW - kFBase;   // ring barriers, table barrier, warp sums
     CUtensorMap map;
     std::memset(&map, 0, sizeof(map));
     if (PACK) {
@@ -163,19 +165,19 @@ cudaError_t run(FArgs& a, const uint8_t* text, uint32_t stride, uint32_t img_byt
 }  // namespace
 
 bool fixed_tma_fits(uint32_t img_bytes, uint32_t stride, int smem_limit) {
-    const uint32_t need = align_up(kFBase + img_bytes, 1024) + kFW * kFSt * kFStageBytes + kFW * kFSt * 8 + 8 - kFBase;
+    const uint32_t need = align_up(kFBase + img_bytes, 1024) + kFW * kFSt * kFStageBytes + kFW * kFSt * 8 + 8 + 4 * kFW - kFBase;
     return stride % kFSlice == 0 && static_cast<int>(need) <= smem_limit;
 }
 
 cudaError_t launch_fixed_tma(const DevTable& t_abs, const uint8_t* text, uint64_t n, uint32_t stride,
-                             unsigned long long* count, uint8_t* results, int device, cudaStream_t st,
+                             unsigned long long* count, uint8_t* results, CountSlot cs, int device, cudaStream_t st,
                              uint64_t* n_done) {
     if (n_done) *n_done = 0;
     if (t_abs.cls || t_abs.esize != 2 || stride % kFSlice) return cudaErrorInvalidValue;
     const bool pack = stride == 32;
     FArgs a{};
     a.n = pack ? n / 4 * 4 : n;   // packed: the last n % 4 strings are left to the caller
-    if (a.n == 0) return cudaSuccess;
+    if (a.n == 0) return cs.accumulate ? cudaSuccess : cudaMemsetAsync(count, 0, sizeof(unsigned long long), st);
     a.tiles = (a.n + kFRows - 1) / kFRows;
     a.ncol = pack ? 1 : stride / kFSlice;
     a.img = static_cast<const uint4*>(t_abs.img);
@@ -183,6 +185,8 @@ cudaError_t launch_fixed_tma(const DevTable& t_abs, const uint8_t* text, uint64_
     a.start = t_abs.start + kFBase;
     a.acc_col = t_abs.ncols * 2u;
     a.count = count;
+    a.slot = cs.p;
+    a.accumulate = cs.accumulate ? 1 : 0;
     a.results = results;
     if (n_done) *n_done = a.n;
     if (pack)

@@ -32,6 +32,7 @@
 
 #include "launch.hpp"
 #include "lines_tma.hpp"
+#include "tma_common.cuh"
 
 namespace rxg {
 
@@ -57,6 +58,8 @@ struct Args {
     uint32_t delim;
     uint32_t row_bytes, cmap_addr, acc_shift;   // class layout
     unsigned long long* count;
+    unsigned long long* slot;                   // CountSlot (launch.hpp)
+    int accumulate;
     uint8_t* results;                           // per-line results (RES): line index -> 0/1
     const unsigned long long* line_base;        // per range: delimiters before its start
 };
@@ -350,7 +353,7 @@ __global__ void __launch_bounds__(C::warps * 32) k_lines_tma(const __grid_consta
         }
     }
     cnt = __reduce_add_sync(0xFFFFFFFFu, cnt);
-    if (lane == 0 && cnt) atomicAdd(a.count, static_cast<unsigned long long>(cnt));
+    tma::publish_count(a.slot, a.count, a.accumulate != 0, cnt, a.bar_addr + C::warps * C::stages * 8 + 8);
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -380,7 +383,7 @@ uint32_t place_stages(const LtTable& t, Args& a) {
     uint32_t p = align_up(t.cls ? t.smem_table_end : kLtAccAddr + t.hi_bytes, 1024);
     for (; k < C::warps * C::stages; ++k, p += C::stage_bytes) a.stage_addr[k] = p;
     a.bar_addr = align_up(p, 8);
-    return a.bar_addr + C::warps * C::stages * 8 + 8 - kLtSmemBase;   // ring barriers + the table barrier
+    return a.bar_addr + C::warps * C::stages * 8 + 8 + 4 * C::warps - kLtSmemBase;   // ring barriers, table barrier, warp sums
 }
 
 CUtensorMapSwizzle swizzle_of(int slice) {
@@ -468,8 +471,10 @@ size_t res_scratch_bytes(uint64_t nranges) {
 template <class C, bool CLS, bool RES>
 cudaError_t launch(const LtTable& t, const uint8_t* text, uint64_t len, uint8_t delim, uint32_t chunk,
                    unsigned long long* count, uint8_t* results, void* scratch, size_t scratch_bytes,
-                   cudaStream_t st) {
-    if (len == 0) return cudaSuccess;
+                   CountSlot cs, cudaStream_t st) {
+    if (len == 0) {   // nothing to launch: the count is 0 (or unchanged when accumulating)
+        return cs.accumulate ? cudaSuccess : cudaMemsetAsync(count, 0, sizeof(unsigned long long), st);
+    }
     if (chunk == 0) chunk = auto_chunk<C, CLS>(t, len);
     if (chunk % C::slice) return cudaErrorInvalidValue;
     Args a{};
@@ -517,6 +522,8 @@ cudaError_t launch(const LtTable& t, const uint8_t* text, uint64_t len, uint8_t 
     a.cmap_addr = t.cmap_addr;
     a.acc_shift = t.acc_shift;
     a.count = count;
+    a.slot = cs.p;
+    a.accumulate = cs.accumulate ? 1 : 0;
 
     CUtensorMap map;
     std::memset(&map, 0, sizeof(map));
@@ -566,18 +573,18 @@ int shape_id() {
 template <bool RES>
 cudaError_t launch_any(const LtTable& t, const uint8_t* text, uint64_t len, uint8_t delim, uint32_t chunk,
                        unsigned long long* count, uint8_t* results, void* scratch, size_t scratch_bytes,
-                       cudaStream_t st) {
+                       CountSlot cs, cudaStream_t st) {
     if (t.cls || shape_id() == 0)
-        return t.cls ? launch<S0, true, RES>(t, text, len, delim, chunk, count, results, scratch, scratch_bytes, st)
-                     : launch<S0, false, RES>(t, text, len, delim, chunk, count, results, scratch, scratch_bytes, st);
-    return launch<S6, false, RES>(t, text, len, delim, chunk, count, results, scratch, scratch_bytes, st);
+        return t.cls ? launch<S0, true, RES>(t, text, len, delim, chunk, count, results, scratch, scratch_bytes, cs, st)
+                     : launch<S0, false, RES>(t, text, len, delim, chunk, count, results, scratch, scratch_bytes, cs, st);
+    return launch<S6, false, RES>(t, text, len, delim, chunk, count, results, scratch, scratch_bytes, cs, st);
 }
 
 }  // namespace
 
 cudaError_t launch_lines_tma(const LtTable& t, const uint8_t* text, uint64_t len, uint8_t delim, uint32_t chunk,
-                             unsigned long long* count, cudaStream_t st) {
-    return launch_any<false>(t, text, len, delim, chunk, count, nullptr, nullptr, 0, st);
+                             unsigned long long* count, CountSlot cs, cudaStream_t st) {
+    return launch_any<false>(t, text, len, delim, chunk, count, nullptr, nullptr, 0, cs, st);
 }
 
 uint32_t lines_tma_chunk(const LtTable& t, uint64_t len, uint32_t chunk) {
@@ -593,8 +600,8 @@ size_t lines_tma_results_scratch(uint64_t len, uint32_t chunk) {
 
 cudaError_t launch_lines_tma_results(const LtTable& t, const uint8_t* text, uint64_t len, uint8_t delim,
                                      uint32_t chunk, unsigned long long* count, uint8_t* results, void* scratch,
-                                     size_t scratch_bytes, cudaStream_t st) {
-    return launch_any<true>(t, text, len, delim, chunk, count, results, scratch, scratch_bytes, st);
+                                     size_t scratch_bytes, CountSlot cs, cudaStream_t st) {
+    return launch_any<true>(t, text, len, delim, chunk, count, results, scratch, scratch_bytes, cs, st);
 }
 
 uint32_t lines_tma_slice() { return 32; }

@@ -47,12 +47,23 @@ cudaError_t launch_fixed_abs(const DevTable& t_abs, const uint8_t* text, uint64_
 
 int device_sm_count(int device);
 
+// Per-(heap, stream) completion slot in device memory, all zero when idle:
+// [0] count accumulator, [1] CTA ticket, [2] aux (chunk engine: ~first wrong
+// range). Kernels add their counts to [0]; the last CTA to finish publishes
+// the total to the caller's counter (overwrite, or add when accumulating)
+// and zeroes the slot again, so no memset launch precedes a call. Launches
+// that share a slot are ordered by their stream.
+struct CountSlot {
+    unsigned long long* p = nullptr;
+    bool accumulate = false;
+};
+
 // Fixed stride on the TMA data path (stride a multiple of 32; the absolute
 // raw-byte u16 table plus a 144 KB ring must fit shared memory).
 bool fixed_tma_fits(uint32_t img_bytes, uint32_t stride, int smem_limit);
 // *n_done = strings handled (stride 32 leaves the last n % 4 to the caller).
 cudaError_t launch_fixed_tma(const DevTable& t_abs, const uint8_t* text, uint64_t n, uint32_t stride,
-                             unsigned long long* count, uint8_t* results, int device, cudaStream_t st,
+                             unsigned long long* count, uint8_t* results, CountSlot cs, int device, cudaStream_t st,
                              uint64_t* n_done);
 
 // Stream-ordered store of 0 or ~0 to one u64 (counters, tickets).

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <vector>
 
+#include "launch.hpp"
 #include "program.hpp"
 
 namespace rxg {
@@ -73,7 +74,7 @@ constexpr int32_t kLtChunkDirectMaxStates = 56;
 
 // chunk = bytes per range (multiple of lines_tma_slice()), 0 = one wave of ranges.
 cudaError_t launch_lines_tma(const LtTable& t, const uint8_t* text, uint64_t len, uint8_t delim, uint32_t chunk,
-                             unsigned long long* count, cudaStream_t st);
+                             unsigned long long* count, CountSlot cs, cudaStream_t st);
 uint32_t lines_tma_slice();
 
 // Per-line results on the same kernel: a delimiter count per range, an
@@ -84,6 +85,6 @@ uint32_t lines_tma_chunk(const LtTable& t, uint64_t len, uint32_t chunk);
 size_t lines_tma_results_scratch(uint64_t len, uint32_t chunk);
 cudaError_t launch_lines_tma_results(const LtTable& t, const uint8_t* text, uint64_t len, uint8_t delim,
                                      uint32_t chunk, unsigned long long* count, uint8_t* results, void* scratch,
-                                     size_t scratch_bytes, cudaStream_t st);
+                                     size_t scratch_bytes, CountSlot cs, cudaStream_t st);
 
 }  // namespace rxg

@@ -69,6 +69,31 @@ __device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_
                  : "memory");
 }
 
+// End of a counting kernel, called by every thread with its warp's count in
+// `warp_cnt` (valid in lane 0). The CTA's warps sum through `sums` (one u32
+// per warp, shared window address); thread 0 adds (1 << 40) | sum to slot[0]
+// in one atomic, so the CTA ticket and the count travel together; the CTA that
+// sees gridDim.x - 1 earlier tickets publishes the total and re-zeroes the
+// slot (CountSlot, launch.hpp). One L2 round trip per CTA, no fences.
+__device__ __forceinline__ void publish_count(unsigned long long* slot, unsigned long long* count, bool accumulate,
+                                              uint32_t warp_cnt, uint32_t sums) {
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) asm volatile("st.shared.u32 [%0], %1;" ::"r"(sums + 4 * warp), "r"(warp_cnt) : "memory");
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long c = 0;
+        for (uint32_t w = 0; w < (blockDim.x >> 5); ++w) c += lds32(sums + 4 * w);
+        constexpr unsigned long long kTicket = 1ull << 40;
+        const unsigned long long old = atomicAdd(slot, kTicket | c);
+        if ((old >> 40) == gridDim.x - 1) {
+            const unsigned long long total = (old & (kTicket - 1)) + c;
+            if (accumulate) atomicAdd(count, total);
+            else *count = total;
+            atomicExch(slot, 0ull);
+        }
+    }
+}
+
 // Physical 16-byte granule of logical granule g in row r of a stage (TMA
 // swizzle none / 32B / 64B / 128B by slice width).
 template <int SL>

@@ -210,3 +210,33 @@ def test_mid_size_dfas_both_layouts(k):
     w = np.frombuffer(b"ab" * 300_000 + b"a" + b"b" * k, np.uint8)
     for eng in ("chunked", "dfa_seq"):
         assert m.lockstep_accepts(w.tobytes(), eng) == o.accepts(w.tobytes()), eng
+
+
+def test_back_to_back_launches_on_streams():
+    """The TMA kernels publish counts through a per-stream slot that the last
+    CTA re-zeroes (no memset launch): many launches back to back, on two
+    streams at once and mixed with the other kernels, all exact."""
+    import torch
+
+    pat = _pat("c")
+    text = _long_tailed(5, 4 << 20, ALPHA["c"], long_every=500, long_len=(1000, 5000))
+    want, _ = Oracle(rx.compile(rx.parse(pat))).match_batch(text, 10, 0)
+    m = rx.Matcher(pat, device=0)
+    d = torch.zeros(len(text) + 64, dtype=torch.uint8, device="cuda")
+    d[: len(text)].copy_(torch.from_numpy(text))
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    c1 = torch.full((50,), -1, dtype=torch.int64, device="cuda")
+    c2 = torch.full((50,), -1, dtype=torch.int64, device="cuda")
+    for i in range(50):
+        m.match_batch_device(d, c1[i:i + 1], nbytes=len(text), stream=s1)
+        m.match_batch_device(d, c2[i:i + 1], nbytes=len(text), stream=s2, engine="dfa" if i % 3 else "bitset")
+    torch.cuda.synchronize()
+    assert (c1 == want).all() and (c2 == want).all()
+    # single-string engine on the same streams (its slot holds the ticket and the repair flag)
+    w = torch.from_numpy(rx.synth_input("a")).cuda()
+    acc = torch.zeros(20, dtype=torch.int32, device="cuda")
+    for i in range(20):
+        m2 = rx.Matcher(rx.synth_pattern("a"), device=0) if i == 0 else m2
+        m2.match_one_device(w, acc[i:i + 1], stream=s1 if i % 2 else s2)
+    torch.cuda.synchronize()
+    assert acc.all()
