@@ -186,7 +186,9 @@ int rxg_match_one_ex(rxg_heap* h, const uint8_t* d_bytes, uint64_t len, int engi
  * d_count (device u64) receives the number of matching strings (it is
  * overwritten). d_results (device, nullable) receives one 0/1 byte per
  * string; it needs room for (#delimiters + 1) bytes in line mode. d_text
- * must be 16-byte aligned. */
+ * must be 16-byte aligned. The first call on a stream allocates a 32-byte
+ * per-(heap, stream) completion slot (the kernels publish the count through
+ * it, no memset per call); make that first call outside CUDA-graph capture. */
 int rxg_match_batch(rxg_heap* h, const uint8_t* d_text, uint64_t len, int32_t delimiter,
                     uint32_t stride, unsigned long long* d_count, uint8_t* d_results,
                     void* stream);
