@@ -90,6 +90,8 @@ typedef struct rxg_heap_info {
     uint32_t line_table_bytes;   /* shared-memory image for '\n' lines (0 if none) */
     uint32_t plain_table_bytes;  /* shared-memory image for single strings / fixed stride */
     int32_t dfa_sets;      /* distinct memoized E sets before minimisation (0 if over the cap) */
+    int32_t line_tma_layout;   /* TMA table built for '\n' lines so far: 0 none, 1 direct, 2 class */
+    int32_t line_col_bytes;    /* its column stride (direct layout; chosen by rxg_heap_tune) */
 } rxg_heap_info;
 
 const char* rxg_strerror(int status);

@@ -666,6 +666,12 @@ int rxg_heap_info_get(const rxg_heap* h, rxg_heap_info* info) {
     if (h->dfa_ok) {
         info->line_table_bytes = static_cast<uint32_t>(make_line_table(h->prog, h->dfa, '\n').img.size());
         info->plain_table_bytes = static_cast<uint32_t>(make_plain_table(h->prog, h->dfa).img.size());
+        std::lock_guard<std::mutex> lk(const_cast<rxg_heap*>(h)->mu);
+        auto it = h->lines.find('\n');
+        if (it != h->lines.end() && it->second->lt.ok) {
+            info->line_tma_layout = it->second->lt.cls ? 2 : 1;
+            info->line_col_bytes = it->second->lt.cls ? 0 : it->second->lt.col_bytes;
+        }
     }
     return RXG_OK;
 }

@@ -57,6 +57,7 @@ struct Args {
     uint32_t start, skip, void_row, tail_delta, term_acc;
     uint32_t delim;
     uint32_t row_bytes, cmap_addr, acc_shift;   // class layout
+    uint32_t col_bytes;                         // direct layout: column stride
     unsigned long long* count;
     unsigned long long* slot;                   // CountSlot (launch.hpp)
     int accumulate;
@@ -104,7 +105,7 @@ __device__ __forceinline__ uint32_t lds32(uint32_t addr) {
 template <bool CLS>
 __device__ __forceinline__ uint32_t step_b(const Args& a, uint32_t s, uint32_t b) {
     if constexpr (CLS) return tab(s * a.row_bytes + lds32(a.cmap_addr + b * 4u));
-    else return tab(s + b * kLtColBytes);
+    else return tab(s + b * a.col_bytes);
 }
 
 template <bool CLS, bool IDP = false>
@@ -113,7 +114,7 @@ __device__ __forceinline__ uint32_t step(const Args& a, uint32_t s, uint32_t wor
         // one IDP.4A.U8 extracts byte k, scales it by the column stride and adds the row
         // (replaces PRMT + IMAD; measured neutral on (c)/(d): the loop is shared-memory bound)
         if constexpr (CLS) return tab(s * a.row_bytes + lds32(__dp4a(word, 4u << (8 * k), a.cmap_addr)));
-        else return tab(__dp4a(word, static_cast<unsigned>(kLtColBytes) << (8 * k), s));
+        else return tab(__dp4a(word, a.col_bytes << (8 * k), s));
     }
     return step_b<CLS>(a, s, __byte_perm(word, 0, 0x4440 + k));
 }
@@ -521,6 +522,7 @@ cudaError_t launch(const LtTable& t, const uint8_t* text, uint64_t len, uint8_t 
     a.row_bytes = t.row_bytes;
     a.cmap_addr = t.cmap_addr;
     a.acc_shift = t.acc_shift;
+    a.col_bytes = t.col_bytes;
     a.count = count;
     a.slot = cs.p;
     a.accumulate = cs.accumulate ? 1 : 0;

@@ -29,6 +29,7 @@ struct LtTable {
     uint32_t row_bytes = 0, cmap_addr = 0, acc_shift = 15;
     uint32_t hole_lo = 0, hole_hi = 0;   // unused rows inside the table (class layout): stage slots go here
     uint32_t acc_off = 0;                // plain (chunk) tables: byte offset of a row's accept flag
+    uint32_t col_bytes = kLtColBytes;    // direct layouts: column stride (entry for byte b at row + col_bytes*b)
     std::vector<uint8_t> lo, hi;     // images of [lo_addr, +lo) main rows and [hi_addr, +hi) upper rows
     uint32_t lo_addr = 0, hi_addr = 0;
     uint32_t lo_bytes = 0, hi_bytes = 0;
@@ -56,11 +57,13 @@ LtTable make_chunk_tma_table(const Program& p, const Dfa& d, const std::vector<d
 
 // Row pairing + bank placement of the direct layouts (see lines_tma_table.cpp).
 struct RowPlacement {
-    std::vector<uint32_t> pair, half;   // per row: its pair and half (0 = low u16, 1 = high)
-    std::vector<uint32_t> pair_off;     // per pair: bank offset (words mod 32)
-    uint32_t npairs = 0;
+    std::vector<uint32_t> pair, half;   // per row: its group and 2-byte slot in the group
+    std::vector<uint32_t> pair_off;     // per group: bank offset (words mod 32)
+    uint32_t npairs = 0;                // groups
+    uint32_t col_bytes = kLtColBytes;
 };
-RowPlacement lt_place_pairs(const std::vector<double>* freq, uint32_t nrows, bool pair_rows);
+uint32_t lt_choose_col_bytes(const std::vector<double>* freq, uint32_t nrows);
+RowPlacement lt_place_groups(const std::vector<double>* freq, uint32_t nrows, uint32_t col_bytes, bool group_rows);
 
 // Host emulation of the table walk, for CPU tests.
 uint32_t lt_step(const LtTable& t, uint32_t s, uint8_t byte);

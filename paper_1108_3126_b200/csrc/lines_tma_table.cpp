@@ -35,7 +35,8 @@ void put16(std::vector<uint8_t>& img, uint32_t off, uint32_t v) {
 
 uint32_t align_up(uint32_t x, uint32_t a) { return (x + a - 1) / a * a; }
 
-LtTable make_direct_table(const Program& p, const Dfa& d, uint8_t delim, const std::vector<double>* freq);
+LtTable make_direct_table(const Program& p, const Dfa& d, uint8_t delim, const std::vector<double>* freq,
+                          uint32_t c);
 
 }  // namespace
 
@@ -62,48 +63,108 @@ std::vector<double> lt_sample_freq_plain(const Program& p, const Dfa& d, const u
     return f;
 }
 
-// Rows of the direct layouts hold u16 entries in 4-byte columns, so two rows
-// share every column word: row A's entry for byte b in the low half, row B's
-// in the high half. Lanes in A and B reading the same byte read the same word
-// (one wavefront); reading different bytes they hit different banks, as in a
-// single row. Pairing the hottest rows therefore removes their mutual bank
-// conflicts outright ((c): 86% + 13% of all steps sit in two states).
-// Rows are paired in order of sampled frequency, then each pair gets the bank
-// offset that collides least with the pairs already placed.
-RowPlacement lt_place_pairs(const std::vector<double>* f, uint32_t nrows, bool pair_rows) {
-    RowPlacement pl;
-    pl.pair.assign(nrows, 0);
-    pl.half.assign(nrows, 0);
+// Direct layouts: row r holds the u16 entry for byte b at base_r + c*b, c the
+// column stride in bytes (even). The entries of one row occupy every other
+// half-word of a c*256-byte span, so g = c/2 rows interleave in one span at
+// 2-byte offsets (a "group"). Lanes of one group reading the same byte read
+// the same or the next word: never a bank conflict. With c = 4 the entry
+// for byte b is word b, so bytes 32 apart ('a'/'A', 'e'/'E', ' '/'@') share a
+// bank; c = 6 or 10 spread bytes over banks floor(c*b/4) mod 32 instead.
+// The stride is chosen from sampled state x byte frequencies (the expected
+// colliding mass of the two hottest rows); groups are filled hottest rows
+// first, then each group gets the bank offset that collides least with the
+// groups already placed. Placement changes speed only, never results.
+namespace {
+
+uint32_t col_word(uint32_t c, uint32_t h, uint32_t b) { return (2u * h + c * b) / 4u; }
+
+std::vector<std::array<double, 32>> bank_hist(const std::vector<double>* f, uint32_t nrows, uint32_t c,
+                                              std::vector<double>& tot) {
     std::vector<std::array<double, 32>> H(nrows);
-    std::vector<double> tot(nrows, 0.0);
+    tot.assign(nrows, 0.0);
     for (uint32_t r = 0; r < nrows; ++r) {
         H[r].fill(0.0);
         if (!f) continue;
-        for (int b = 0; b < 256; ++b) {
-            const size_t i = static_cast<size_t>(r) * 256u + static_cast<size_t>(b);
+        for (uint32_t b = 0; b < 256; ++b) {
+            const size_t i = static_cast<size_t>(r) * 256u + b;
             const double x = i < f->size() ? (*f)[i] : 0.0;
-            H[r][static_cast<size_t>(b & 31)] += x;
+            H[r][col_word(c, 0, b) & 31u] += x;
             tot[r] += x;
         }
     }
+    return H;
+}
+
+}  // namespace
+
+uint32_t lt_choose_col_bytes(const std::vector<double>* f, uint32_t nrows) {
+    if (const char* e = std::getenv("RXG_COL_BYTES")) {   // A/B override (tools)
+        const uint32_t v = static_cast<uint32_t>(std::atoi(e));
+        if (v >= 4 && v % 2 == 0 && v <= 14) return v;
+    }
+    if (!f) return kLtColBytes;
+    std::vector<double> tot(nrows, 0.0);
+    for (uint32_t r = 0; r < nrows; ++r)
+        for (uint32_t b = 0; b < 256; ++b) {
+            const size_t i = static_cast<size_t>(r) * 256u + b;
+            tot[r] += i < f->size() ? (*f)[i] : 0.0;
+        }
     std::vector<uint32_t> order(nrows);
     for (uint32_t r = 0; r < nrows; ++r) order[r] = r;
     std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return tot[a] > tot[b]; });
-    const uint32_t per = pair_rows && !std::getenv("RXG_NO_ROW_PAIRS") ? 2u : 1u;   // env: A/B switch (tools)
+    const uint32_t top = std::min<uint32_t>(2, nrows);
+    uint32_t best_c = kLtColBytes;
+    double best = -1.0;
+    for (uint32_t c : {4u, 6u, 10u}) {
+        // colliding mass: (row h, byte b) vs (row h', byte b') in one group,
+        // different words in the same bank
+        double cost = 0.0;
+        for (uint32_t i = 0; i < top; ++i)
+            for (uint32_t j = 0; j < top; ++j)
+                for (uint32_t b = 0; b < 256; ++b) {
+                    const double x = (*f)[static_cast<size_t>(order[i]) * 256u + b];
+                    if (x == 0.0) continue;
+                    const uint32_t wa = col_word(c, i, b);
+                    for (uint32_t b2 = 0; b2 < 256; ++b2) {
+                        const double y = (*f)[static_cast<size_t>(order[j]) * 256u + b2];
+                        if (y == 0.0) continue;
+                        const uint32_t wb = col_word(c, j, b2);
+                        if (wa != wb && ((wa ^ wb) & 31u) == 0) cost += x * y;
+                    }
+                }
+        if (best < 0.0 || cost < best * 0.98) {   // a larger stride must win clearly
+            best = cost;
+            best_c = c;
+        }
+    }
+    return best_c;
+}
+
+RowPlacement lt_place_groups(const std::vector<double>* f, uint32_t nrows, uint32_t c, bool group_rows) {
+    RowPlacement pl;
+    pl.col_bytes = c;
+    pl.pair.assign(nrows, 0);
+    pl.half.assign(nrows, 0);
+    std::vector<double> tot;
+    const std::vector<std::array<double, 32>> H = bank_hist(f, nrows, c, tot);
+    std::vector<uint32_t> order(nrows);
+    for (uint32_t r = 0; r < nrows; ++r) order[r] = r;
+    std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return tot[a] > tot[b]; });
+    const uint32_t per = group_rows && !std::getenv("RXG_NO_ROW_PAIRS") ? c / 2u : 1u;   // env: A/B switch (tools)
     pl.npairs = (nrows + per - 1) / per;
     std::vector<std::array<double, 32>> HP(pl.npairs);
     std::vector<double> tp(pl.npairs, 0.0);
+    for (uint32_t q = 0; q < pl.npairs; ++q) HP[q].fill(0.0);
     for (uint32_t i = 0; i < nrows; ++i) {
         const uint32_t r = order[i], q = i / per;
         pl.pair[r] = q;
         pl.half[r] = i % per;
-        if (i % per == 0) HP[q].fill(0.0);
         for (int k = 0; k < 32; ++k) HP[q][static_cast<size_t>(k)] += H[r][static_cast<size_t>(k)];
         tp[q] += tot[r];
     }
     pl.pair_off.assign(pl.npairs, 0);
     std::vector<uint32_t> placed;
-    for (uint32_t q = 0; q < pl.npairs; ++q) {   // pairs are already in hotness order
+    for (uint32_t q = 0; q < pl.npairs; ++q) {   // groups are already in hotness order
         if (tp[q] == 0.0) {
             pl.pair_off[q] = (q * 9u) & 31u;
             continue;
@@ -111,11 +172,11 @@ RowPlacement lt_place_pairs(const std::vector<double>* f, uint32_t nrows, bool p
         double best = -1.0;
         uint32_t bo = 0;
         for (uint32_t o = 0; o < 32; ++o) {
-            double c = 0.0;
+            double cc = 0.0;
             for (uint32_t q2 : placed)
-                for (uint32_t k = 0; k < 32; ++k) c += HP[q][k] * HP[q2][(k + o + 32 - pl.pair_off[q2]) & 31u];
-            if (best < 0.0 || c < best) {
-                best = c;
+                for (uint32_t k = 0; k < 32; ++k) cc += HP[q][k] * HP[q2][(k + o + 32 - pl.pair_off[q2]) & 31u];
+            if (best < 0.0 || cc < best) {
+                best = cc;
                 bo = o;
             }
         }
@@ -266,22 +327,25 @@ LtTable make_class_table(const Program& p, const Dfa& d, uint8_t delim, const st
 LtTable make_lines_tma_table(const Program& p, const Dfa& d, uint8_t delim, const std::vector<double>* freq,
                              bool force_class) {
     if (force_class || d.n_states > kLtDirectMaxStates) return make_class_table(p, d, delim, freq);
-    LtTable t = make_direct_table(p, d, delim, freq);
+    const uint32_t c = lt_choose_col_bytes(freq, static_cast<uint32_t>(d.n_states) + 2);
+    LtTable t = make_direct_table(p, d, delim, freq, c);
+    if (!t.ok && c != kLtColBytes) t = make_direct_table(p, d, delim, freq, kLtColBytes);
     return t.ok ? t : make_class_table(p, d, delim, freq);   // the direct rows did not fit below 64 KB
 }
 
 namespace {
 
-LtTable make_direct_table(const Program& p, const Dfa& d, uint8_t delim, const std::vector<double>* freq) {
+// Main rows (states 0..S-1, SKIP (S), VOID (S+1)) in groups sharing column
+// words, each group at a chosen bank offset; column stride c.
+LtTable make_direct_table(const Program& p, const Dfa& d, uint8_t delim, const std::vector<double>* freq,
+                          uint32_t c) {
     LtTable t;
     const uint32_t S = static_cast<uint32_t>(d.n_states);
-    const uint32_t R = kLtRowBytes;
-    const uint32_t slot = R + 128;   // worst case pair + alignment pad
-    // main rows: states 0..S-1, SKIP (S), VOID (S+1), two per column word, each
-    // pair at a chosen bank offset
-    const RowPlacement pl = lt_place_pairs(freq, S + 2, true);
-    if (pl.npairs * slot + kLtSmemBase > kLtAccAddr) return t;
-    t.lo_addr = (kLtAccAddr - pl.npairs * slot) & ~127u;
+    const RowPlacement pl = lt_place_groups(freq, S + 2, c, true);
+    if (pl.npairs * (256u * c + 128u) + kLtSmemBase > kLtAccAddr) return t;
+    const uint32_t R = 256u * c;
+    t.col_bytes = c;
+    t.lo_addr = (kLtAccAddr - pl.npairs * (R + 128u)) & ~127u;
     std::vector<uint32_t> paddr(pl.npairs), addr(S + 2);
     uint32_t cur = t.lo_addr;
     for (uint32_t q = 0; q < pl.npairs; ++q) {
@@ -309,8 +373,8 @@ LtTable make_direct_table(const Program& p, const Dfa& d, uint8_t delim, const s
     auto next = [&](uint32_t s, int b) {
         return static_cast<uint32_t>(d.next[static_cast<size_t>(s) * static_cast<size_t>(d.n_classes) + p.byte_class[b]]);
     };
-    auto put_lo = [&](uint32_t row, int b, uint32_t v) { put16(t.lo, row - t.lo_addr + kLtColBytes * static_cast<uint32_t>(b), v); };
-    auto put_hi = [&](uint32_t row, int b, uint32_t v) { put16(t.hi, row - kLtAccAddr + kLtColBytes * static_cast<uint32_t>(b), v); };
+    auto put_lo = [&](uint32_t row, int b, uint32_t v) { put16(t.lo, row - t.lo_addr + c * static_cast<uint32_t>(b), v); };
+    auto put_hi = [&](uint32_t row, int b, uint32_t v) { put16(t.hi, row - kLtAccAddr + c * static_cast<uint32_t>(b), v); };
     for (uint32_t s = 0; s < S; ++s) {
         const bool acc = d.accept[s] != 0;
         for (int b = 0; b < 256; ++b) {
@@ -331,7 +395,7 @@ LtTable make_direct_table(const Program& p, const Dfa& d, uint8_t delim, const s
     }
     for (int b = 0; b < 256; ++b) {   // START_A = the start row (low halves of its own words)
         uint16_t v;
-        std::memcpy(&v, &t.lo[t.start - t.lo_addr + kLtColBytes * static_cast<uint32_t>(b)], 2);
+        std::memcpy(&v, &t.lo[t.start - t.lo_addr + c * static_cast<uint32_t>(b)], 2);
         put_hi(kLtAccAddr, b, v);
     }
 
@@ -355,7 +419,7 @@ LtTable make_chunk_tma_table(const Program& p, const Dfa& d, const std::vector<d
         // accept flag follows its columns. (Row pairs measured slower here:
         // config (e) 2.96 vs 3.25 TB/s with fewer bank conflicts; unpaired.)
         const uint32_t R = kLtRowBytes;
-        const RowPlacement pl = lt_place_pairs(freq, S, false);
+        const RowPlacement pl = lt_place_groups(freq, S, kLtColBytes, false);
         std::vector<uint32_t> paddr(pl.npairs), addr(S);
         uint32_t cur = kLtSmemBase;
         for (uint32_t q = 0; q < pl.npairs; ++q) {
@@ -418,8 +482,8 @@ uint32_t lt_step(const LtTable& t, uint32_t s, uint8_t byte) {
         std::memcpy(&v, &t.lo[s * t.row_bytes + colabs - t.lo_addr], 2);
         return v;
     }
-    if (s < kLtAccAddr) std::memcpy(&v, &t.lo[s - t.lo_addr + kLtColBytes * byte], 2);
-    else std::memcpy(&v, &t.hi[s - kLtAccAddr + kLtColBytes * byte], 2);
+    if (s < kLtAccAddr) std::memcpy(&v, &t.lo[s - t.lo_addr + t.col_bytes * byte], 2);
+    else std::memcpy(&v, &t.hi[s - kLtAccAddr + t.col_bytes * byte], 2);
     return v;
 }
 
