@@ -42,12 +42,19 @@ LtTable make_direct_table(const Program& p, const Dfa& d, uint8_t delim, const s
 
 std::vector<double> lt_sample_freq(const Program& p, const Dfa& d, uint8_t delim, const uint8_t* sample,
                                    uint64_t len) {
+    // rows: states 0..S-1, SKIP (S), VOID (S+1), START_A (S+2). SKIP is
+    // estimated (a range walks about half a line in SKIP; ~1/64 of its bytes
+    // for ranges of a few dozen lines); START_A takes the byte after every
+    // accepted line end.
     const size_t S = static_cast<size_t>(d.n_states);
-    std::vector<double> f((S + 2) * 256, 0.0);
+    std::vector<double> f((S + 3) * 256, 0.0);
     int32_t s = d.start;
+    bool after_acc = false;
     for (uint64_t i = 0; i < len; ++i) {
         const uint8_t b = sample[i];
-        f[static_cast<size_t>(s) * 256 + b] += 1.0;
+        f[(after_acc ? S + 2 : static_cast<size_t>(s)) * 256 + b] += 1.0;
+        f[S * 256 + b] += 1.0 / 64.0;
+        after_acc = b == delim && d.accept[static_cast<size_t>(s)] != 0;
         s = b == delim ? d.start : d.next[static_cast<size_t>(s) * static_cast<size_t>(d.n_classes) + p.byte_class[b]];
     }
     return f;
@@ -345,6 +352,29 @@ LtTable make_direct_table(const Program& p, const Dfa& d, uint8_t delim, const s
     if (pl.npairs * (256u * c + 128u) + kLtSmemBase > kLtAccAddr) return t;
     const uint32_t R = 256u * c;
     t.col_bytes = c;
+    // START_A (counted: the only main-loop row at >= 0x8000) at the bank offset
+    // that collides least with the groups under the sampled bytes after
+    // accepted line ends
+    uint32_t acc_off = 0;
+    if (freq && freq->size() >= static_cast<size_t>(S + 3) * 256) {
+        std::vector<double> tot;
+        const auto H = bank_hist(freq, S + 3, c, tot);
+        std::vector<std::array<double, 32>> HG(pl.npairs);
+        for (auto& h : HG) h.fill(0.0);
+        for (uint32_t r = 0; r < S + 2; ++r)
+            for (int k = 0; k < 32; ++k) HG[pl.pair[r]][static_cast<size_t>(k)] += H[r][static_cast<size_t>(k)];
+        double best = -1.0;
+        for (uint32_t o = 0; o < 32; ++o) {
+            double cc = 0.0;
+            for (uint32_t q = 0; q < pl.npairs; ++q)
+                for (uint32_t k = 0; k < 32; ++k) cc += H[S + 2][k] * HG[q][(k + o + 32 - pl.pair_off[q]) & 31u];
+            if (best < 0.0 || cc < best) {
+                best = cc;
+                acc_off = o;
+            }
+        }
+    }
+    const uint32_t acc_row = kLtAccAddr + 4u * acc_off;
     t.lo_addr = (kLtAccAddr - pl.npairs * (R + 128u)) & ~127u;
     std::vector<uint32_t> paddr(pl.npairs), addr(S + 2);
     uint32_t cur = t.lo_addr;
@@ -355,7 +385,7 @@ LtTable make_direct_table(const Program& p, const Dfa& d, uint8_t delim, const s
     for (uint32_t r = 0; r < S + 2; ++r) addr[r] = paddr[pl.pair[r]] + 2u * pl.half[r];
     if (cur > kLtAccAddr) return t;
     // upper region: START_A at 0x8000, tail copies at main + tail_delta, TERM rows
-    t.tail_delta = align_up(kLtAccAddr + R - t.lo_addr, 128);
+    t.tail_delta = align_up(acc_row + R - t.lo_addr, 128);
     t.term_acc = align_up(cur + t.tail_delta, 4);
     t.term_rej = t.term_acc + R;
     const uint32_t hi_end = t.term_rej + R;
@@ -379,7 +409,7 @@ LtTable make_direct_table(const Program& p, const Dfa& d, uint8_t delim, const s
         const bool acc = d.accept[s] != 0;
         for (int b = 0; b < 256; ++b) {
             if (b == delim) {
-                put_lo(main_row(s), b, acc ? kLtAccAddr : t.start);
+                put_lo(main_row(s), b, acc ? acc_row : t.start);
                 put_hi(tail_row(s), b, acc ? t.term_acc : t.term_rej);
             } else {
                 put_lo(main_row(s), b, main_row(next(s, b)));
@@ -396,7 +426,7 @@ LtTable make_direct_table(const Program& p, const Dfa& d, uint8_t delim, const s
     for (int b = 0; b < 256; ++b) {   // START_A = the start row (low halves of its own words)
         uint16_t v;
         std::memcpy(&v, &t.lo[t.start - t.lo_addr + c * static_cast<uint32_t>(b)], 2);
-        put_hi(kLtAccAddr, b, v);
+        put_hi(acc_row, b, v);
     }
 
     t.smem_table_end = kLtAccAddr + t.hi_bytes;
