@@ -42,21 +42,27 @@ LtTable make_direct_table(const Program& p, const Dfa& d, uint8_t delim, const s
 
 std::vector<double> lt_sample_freq(const Program& p, const Dfa& d, uint8_t delim, const uint8_t* sample,
                                    uint64_t len) {
-    // rows: states 0..S-1, SKIP (S), VOID (S+1), START_A (S+2). SKIP is
-    // estimated (a range walks about half a line in SKIP; ~1/64 of its bytes
-    // for ranges of a few dozen lines); START_A takes the byte after every
-    // accepted line end.
+    // rows: states 0..S-1, SKIP (S), VOID (S+1), START_A (S+2). START_A takes
+    // the byte after every accepted line end. SKIP is estimated: a range
+    // walks about half a line before its first delimiter, and ranges of a
+    // large input are a few KB (one wave of ~340k ranges per GB), so SKIP's
+    // share of the steps is about (mean line length / 2) / 4 KB.
     const size_t S = static_cast<size_t>(d.n_states);
     std::vector<double> f((S + 3) * 256, 0.0);
     int32_t s = d.start;
     bool after_acc = false;
+    uint64_t lines = 0;
     for (uint64_t i = 0; i < len; ++i) {
         const uint8_t b = sample[i];
         f[(after_acc ? S + 2 : static_cast<size_t>(s)) * 256 + b] += 1.0;
-        f[S * 256 + b] += 1.0 / 64.0;
         after_acc = b == delim && d.accept[static_cast<size_t>(s)] != 0;
+        lines += b == delim;
         s = b == delim ? d.start : d.next[static_cast<size_t>(s) * static_cast<size_t>(d.n_classes) + p.byte_class[b]];
     }
+    const double mean_line = static_cast<double>(len) / static_cast<double>(lines ? lines : 1);
+    double skip_share = std::min(0.5, mean_line / 2.0 / 4096.0);
+    if (const char* e = std::getenv("RXG_SKIP_SHARE")) skip_share = std::atof(e);   // A/B override (tools)
+    for (uint64_t i = 0; i < len; ++i) f[S * 256 + sample[i]] += skip_share;
     return f;
 }
 
@@ -208,9 +214,11 @@ std::vector<uint32_t> number_states(const Program& p, const Dfa& d, uint8_t deli
     if (!freq || freq->size() < static_cast<size_t>(S) * 256) return row;
     auto off_of = [&](uint32_t r) { return (base_word + r * rb_words) & 31u; };
     // bank histogram of each state in a row at offset 0: column c sits in word c/2
-    std::vector<std::array<double, 32>> H(S);
-    std::vector<double> tot(S, 0.0);
-    for (uint32_t s = 0; s < S; ++s) {
+    // (SKIP, row S, too when the sample covers it: lt_sample_freq estimates it)
+    const uint32_t NS = freq->size() >= static_cast<size_t>(S + 1) * 256 && nmain > S ? S + 1 : S;
+    std::vector<std::array<double, 32>> H(NS);
+    std::vector<double> tot(NS, 0.0);
+    for (uint32_t s = 0; s < NS; ++s) {
         H[s].fill(0.0);
         for (int b = 0; b < 256; ++b) {
             const double x = (*freq)[static_cast<size_t>(s) * 256 + static_cast<size_t>(b)];
@@ -220,8 +228,8 @@ std::vector<uint32_t> number_states(const Program& p, const Dfa& d, uint8_t deli
             tot[s] += x;
         }
     }
-    std::vector<uint32_t> order(S);
-    for (uint32_t s = 0; s < S; ++s) order[s] = s;
+    std::vector<uint32_t> order(NS);
+    for (uint32_t s = 0; s < NS; ++s) order[s] = s;
     std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return tot[a] > tot[b]; });
     // free rows per bank offset
     std::array<std::vector<uint32_t>, 32> free_rows;
