@@ -7,9 +7,11 @@ without the built library raises immediately.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "librxg.so"
+# RXG_LIB: load another build (A/B timing of two builds in one process tree; tools only)
+LIB_PATH = Path(os.environ["RXG_LIB"]) if os.environ.get("RXG_LIB") else Path(__file__).resolve().parent / "librxg.so"
 
 RXG_OK = 0
 RXG_EINVAL = 1

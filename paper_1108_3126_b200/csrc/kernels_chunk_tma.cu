@@ -118,6 +118,42 @@ __device__ uint32_t entry_guess(const Args& a, uint64_t r) {
     return r == 0 ? a.start : walk<CLS>(a, a.start, c0 > a.lookback ? c0 - a.lookback : 0, c0);
 }
 
+// Entry guesses of a lane's ranges (rows row0 + 32 j + lane): with the
+// default 64-byte lookback every chain's four 16-byte loads are issued
+// together and the chains walk interleaved, instead of one dependent walk
+// after the other.
+template <bool CLS, int CH>
+__device__ void entry_guesses(const Args& a, uint64_t row0, uint32_t lane, uint32_t (&s)[CH], const bool (&valid)[CH]) {
+    bool fast = a.lookback == 64;
+#pragma unroll
+    for (int j = 0; j < CH; ++j) fast &= !valid[j] || (row0 + j * 32 + lane) * a.chunk >= 64;
+    if (!fast) {
+#pragma unroll
+        for (int j = 0; j < CH; ++j) s[j] = valid[j] ? entry_guess<CLS>(a, row0 + j * 32 + lane) : a.start;
+        return;
+    }
+    uint4 v[CH][4];
+#pragma unroll
+    for (int j = 0; j < CH; ++j) {
+        const uint64_t c0 = valid[j] ? (row0 + j * 32 + lane) * a.chunk : 64;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[j][u] = __ldg(reinterpret_cast<const uint4*>(a.text + c0 - 64) + u);
+        s[j] = a.start;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int w = 0; w < 4; ++w)
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+#pragma unroll
+                for (int j = 0; j < CH; ++j)
+                    s[j] = stepb<CLS>(a, s[j], __byte_perm(tma::word_of(v[j][u], w), 0, 0x4440 + k));
+#pragma unroll
+    for (int j = 0; j < CH; ++j)
+        if (!valid[j]) s[j] = a.start;
+}
+
 // In-order repair from the first wrong guess (one warp, the table already in
 // shared memory), then the answer. Run by warp 0 of the last CTA.
 template <bool CLS>
@@ -174,7 +210,7 @@ __device__ void repair_and_answer(const Args& a) {
 }
 
 template <bool CLS>
-__global__ void __launch_bounds__(kWarps * 32) k_chunk_tma(const __grid_constant__ Args a,
+__global__ void __launch_bounds__(kWarps * 32, 1) k_chunk_tma(const __grid_constant__ Args a,
                                                            const __grid_constant__ CUtensorMap map) {
     extern __shared__ __align__(1024) uint8_t sm[];
     if (static_cast<uint32_t>(__cvta_generic_to_shared(sm)) != kLtSmemBase) __trap();
@@ -222,11 +258,13 @@ __global__ void __launch_bounds__(kWarps * 32) k_chunk_tma(const __grid_constant
         bool valid[kChains];
 #pragma unroll
         for (int j = 0; j < kChains; ++j) {
-            const uint64_t r = row0 + j * 32 + lane;
-            valid[j] = r < a.rows;
-            s[j] = valid[j] ? entry_guess<CLS>(a, r) : a.start;
+            valid[j] = row0 + j * 32 + lane < a.rows;
+        }
+        entry_guesses<CLS, kChains>(a, row0, lane, s, valid);
+#pragma unroll
+        for (int j = 0; j < kChains; ++j) {
             guess[j] = s[j];
-            if (valid[j]) a.g[r] = s[j];
+            if (valid[j]) a.g[row0 + j * 32 + lane] = s[j];
         }
         for (uint32_t col = 0; col < ncol; ++col) {
             const uint32_t st = col % kStages;

@@ -39,7 +39,7 @@ struct FArgs {
 };
 
 template <bool RES, bool PACK>
-__global__ void __launch_bounds__(kFW * 32) k_fixed_tma(const __grid_constant__ FArgs a,
+__global__ void __launch_bounds__(kFW * 32, 1) k_fixed_tma(const __grid_constant__ FArgs a,
                                                          const __grid_constant__ CUtensorMap map) {
     extern __shared__ __align__(1024) uint8_t sm[];
     if (static_cast<uint32_t>(__cvta_generic_to_shared(sm)) != kFBase) __trap();

@@ -237,7 +237,7 @@ __device__ void range_direct(const Args& a, uint64_t c0, uint64_t c1, uint64_t r
 }
 
 template <class C, bool CLS, bool RES>
-__global__ void __launch_bounds__(C::warps * 32) k_lines_tma(const __grid_constant__ Args a,
+__global__ void __launch_bounds__(C::warps * 32, 1) k_lines_tma(const __grid_constant__ Args a,
                                                              const __grid_constant__ CUtensorMap map) {
     extern __shared__ __align__(1024) uint8_t sm[];
     const uint32_t base = static_cast<uint32_t>(__cvta_generic_to_shared(sm));
