@@ -198,6 +198,45 @@ __device__ __forceinline__ uint32_t step_res(const Args& a, uint32_t s, uint32_t
     return s;
 }
 
+// The straddling lines of all of a lane's ranges, walked interleaved (their
+// loads in flight together) instead of one after the other. s[j] enters as
+// the tail-copy row; TERM rows absorb, so a finished chain keeps stepping
+// harmlessly until the others are done. Returns per chain whether its line
+// was accepted (live[j] false: no straddling line).
+template <bool CLS, int K>
+__device__ void finish_lines(const Args& a, uint32_t (&s)[K], uint64_t (&pos)[K], const bool (&live)[K],
+                             uint32_t (&ok)[K]) {
+    bool more = false;
+#pragma unroll
+    for (int j = 0; j < K; ++j) more |= live[j];
+    while (more) {
+        uint4 v[K];
+#pragma unroll
+        for (int j = 0; j < K; ++j)
+            v[j] = live[j] && s[j] < a.term_acc && pos[j] + 16 <= a.len
+                       ? __ldg(reinterpret_cast<const uint4*>(a.text + pos[j]))
+                       : make_uint4(0, 0, 0, 0);
+        more = false;
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+            if (!live[j] || s[j] >= a.term_acc) continue;
+            if (pos[j] + 16 <= a.len) {
+#pragma unroll
+                for (int w = 0; w < 4; ++w)
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) s[j] = step<CLS>(a, s[j], word_of(v[j], w), k);
+                pos[j] += 16;
+            } else {   // the last bytes of the buffer, then the virtual delimiter
+                for (; pos[j] < a.len; ++pos[j]) s[j] = step_b<CLS>(a, s[j], a.text[pos[j]]);
+                if (s[j] < a.term_acc) s[j] = step_b<CLS>(a, s[j], a.delim);
+            }
+            more |= s[j] < a.term_acc;
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < K; ++j) ok[j] = live[j] && s[j] == a.term_acc;
+}
+
 // A range processed entirely with direct loads (the remainder pieces).
 template <bool CLS, bool RES>
 __device__ void range_direct(const Args& a, uint64_t c0, uint64_t c1, uint64_t range, uint32_t& cnt) {
@@ -343,13 +382,22 @@ __global__ void __launch_bounds__(C::warps * 32, 1) k_lines_tma(const __grid_con
                                           static_cast<int32_t>(row0));
             }
         }
+        {
+            bool live[C::chains];
+            uint64_t pos[C::chains];
+            uint32_t ok[C::chains];
 #pragma unroll
-        for (int j = 0; j < C::chains; ++j) {
-            if (valid[j] && s[j] != a.skip && last[j] != a.delim) {
-                const uint64_t row = row0 + j * 32 + lane;
-                const uint32_t ok = finish_line<CLS>(a, s[j] + a.tail_delta, (row + 1) * a.chunk) == a.term_acc;
-                cnt += ok;
-                if constexpr (RES) a.results[lc[j].li] = static_cast<uint8_t>(ok);
+            for (int j = 0; j < C::chains; ++j) {
+                live[j] = valid[j] && s[j] != a.skip && last[j] != a.delim;
+                pos[j] = (row0 + j * 32 + lane + 1) * a.chunk;
+                s[j] += a.tail_delta;
+            }
+            finish_lines<CLS, C::chains>(a, s, pos, live, ok);
+#pragma unroll
+            for (int j = 0; j < C::chains; ++j) {
+                cnt += ok[j];
+                if constexpr (RES)
+                    if (live[j]) a.results[lc[j].li] = static_cast<uint8_t>(ok[j]);
             }
         }
     }
