@@ -175,7 +175,13 @@ typedef struct rxg_one_opts {
     uint32_t chunk;                   /* CHUNKED: bytes per range (multiple of 32 on the TMA path, 64 otherwise), 0 = auto */
     uint32_t lookback;                /* CHUNKED: bytes walked before a range to guess its entry state (0 = 64) */
     unsigned long long* d_repairs;    /* CHUNKED: ranges re-walked by the in-order repair pass */
+    uint32_t flags;                   /* RXG_ONE_ENTRY: start in entry_state instead of the start state */
+    uint32_t entry_state;             /* CHUNKED: opaque table state (from a d_exit_state of the same pattern) */
+    uint32_t* d_exit_state;           /* CHUNKED: the table state after the string (device, nullable). States
+                                         are interchangeable between heaps of the same pattern built alike
+                                         (same tuning); this is how segments of one string chain. */
 } rxg_one_opts;
+#define RXG_ONE_ENTRY 1u
 
 int rxg_match_one_ex(rxg_heap* h, const uint8_t* d_bytes, uint64_t len, int engine, int32_t* d_accept,
                      const rxg_one_opts* opts, void* stream);
@@ -229,6 +235,17 @@ int rxg_utf8_check(int device, const uint8_t* d_text, uint64_t len, int32_t deli
 /* Same on a host buffer (synchronous). */
 int rxg_utf8_check_host(int device, const uint8_t* text, uint64_t len, int32_t delimiter,
                         uint32_t stride, uint64_t* first_bad);
+
+/* One long string split over `ndev` GPUs (chunk-speculative
+ * matching across devices): segment k starts in the state its 64-byte prefix
+ * leads to from the start state (one small walk), every device runs the
+ * chunk-parallel engine on its segment at once, then the host chains the
+ * segments' entry and exit states in order and re-runs a segment only where
+ * its guessed entry differs from the exact exit of the previous one. Exact
+ * for every pattern; *accept = rx::lockstep_accepts over the whole string.
+ * The same device may appear more than once. */
+int rxg_match_one_multi(const int* devices, int ndev, const char* pattern, size_t plen, const uint8_t* text,
+                        uint64_t len, int32_t* accept, int32_t* resegments);
 
 /* Byte-balanced sharding of a host buffer over `ndev` GPUs (split at string
  * boundaries), one stream per device, and one NCCL all-reduce of the int64

@@ -44,7 +44,8 @@ class rxg_heap_info(C.Structure):
 
 class rxg_one_opts(C.Structure):
     _fields_ = [("checkpoint_every", C.c_uint32), ("d_checkpoints", C.c_void_p), ("d_stats", C.c_void_p),
-                ("d_trace", C.c_void_p), ("chunk", C.c_uint32), ("lookback", C.c_uint32), ("d_repairs", C.c_void_p)]
+                ("d_trace", C.c_void_p), ("chunk", C.c_uint32), ("lookback", C.c_uint32), ("d_repairs", C.c_void_p),
+                ("flags", C.c_uint32), ("entry_state", C.c_uint32), ("d_exit_state", C.c_void_p)]
 
 
 # name -> (restype, argtypes). Every symbol declared in include/rxg.h.
@@ -85,6 +86,8 @@ _SIG = {
                                         C.c_int32, C.c_uint32, C.POINTER(C.c_uint64), _P]),
     "rxg_match_many": (C.c_int, [C.c_int, C.c_char_p, C.c_int32, _P, C.c_uint64, C.c_int32, C.c_uint32, _P,
                                  C.POINTER(C.c_uint64), C.POINTER(C.c_int32)]),
+    "rxg_match_one_multi": (C.c_int, [C.POINTER(C.c_int), C.c_int, C.c_char_p, C.c_size_t, _P, C.c_uint64,
+                                      C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
     "rxg_shard_bounds": (C.c_int, [_P, C.c_uint64, C.c_int32, C.c_uint32, C.c_int, C.POINTER(C.c_uint64)]),
     "rxg_last_launch_count": (C.c_int, []),
     "rxg_synth_pattern": (C.c_int, [C.c_char, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]),

@@ -822,6 +822,9 @@ int rxg_host_emulate_lines_tma(const rxg_heap* h, const uint8_t* text, uint64_t 
 
 int rxg_match_one_ex(rxg_heap* h, const uint8_t* d_bytes, uint64_t len, int engine, int32_t* d_accept,
                      const rxg_one_opts* opts, void* stream) {
+    if (opts && ((opts->flags & RXG_ONE_ENTRY) || opts->d_exit_state) && engine != RXG_ENGINE_CHUNKED &&
+        engine != RXG_ENGINE_AUTO)
+        return fail(RXG_EUNSUPPORTED, "entry / exit states need the chunked engine");
     if (engine == RXG_ENGINE_AUTO && h && !h->dfa_ok) engine = RXG_ENGINE_PERNODE;   // table over the cap
     const bool dfa_engine = engine == RXG_ENGINE_AUTO || engine == RXG_ENGINE_DFA_SEQ || engine == RXG_ENGINE_CHUNKED;
     if (int rc = need_device(h, dfa_engine)) return rc;
@@ -853,7 +856,9 @@ int rxg_match_one_ex(rxg_heap* h, const uint8_t* d_bytes, uint64_t len, int engi
             if (int rc = stream_slot(h, st, &cs, false)) return rc;
             const cudaError_t e = launch_chunked_tma(h->plain->chunk_lt, h->plain->d_chunk, d_bytes, len, chunk,
                                                      o.lookback ? o.lookback : 64, scratch, d_accept, o.d_repairs,
-                                                     cs, h->device, st);
+                                                     cs, h->device, st,
+                                                     (o.flags & RXG_ONE_ENTRY) ? o.entry_state : kStartState,
+                                                     o.d_exit_state);
             cudaFreeAsync(scratch, st);
             if (e != cudaSuccess) return cuda_fail(e, "launch_chunked_tma");
             g_launches = 1;   // walk, seam check and repair in one kernel
@@ -865,7 +870,8 @@ int rxg_match_one_ex(rxg_heap* h, const uint8_t* d_bytes, uint64_t len, int engi
         void* scratch = nullptr;
         RXG_CUDA(cudaMallocAsync(&scratch, chunked_scratch_bytes(len, chunk), st));
         const cudaError_t e = launch_chunked(*t, d_bytes, len, chunk, lookback, scratch, d_accept, o.d_repairs,
-                                             h->device, st);
+                                             h->device, st, (o.flags & RXG_ONE_ENTRY) ? o.entry_state : kStartState,
+                                             o.d_exit_state);
         cudaFreeAsync(scratch, st);
         if (e != cudaSuccess) return cuda_fail(e, "launch_chunked");
         g_launches = 2;
@@ -1169,6 +1175,113 @@ int rxg_match_many(int device, const char* patterns, int32_t n_patterns, const u
     if (e != cudaSuccess) rc = cuda_fail(e, "rxg_match_many");
     cudaFree(d);
     g_launches = 1;
+    return rc;
+}
+
+int rxg_match_one_multi(const int* devices, int ndev, const char* pattern, size_t plen, const uint8_t* text,
+                        uint64_t len, int32_t* accept, int32_t* resegments) {
+    if (!devices || ndev <= 0 || !accept || (!text && len)) return fail(RXG_EINVAL, "bad arguments");
+    constexpr uint64_t kPre = 64;   // the chunk engine's lookback
+    struct Seg {
+        rxg_heap* h = nullptr;
+        uint8_t* d = nullptr;        // [prefix | segment], 16-byte aligned parts
+        uint32_t* d_st = nullptr;    // [guess, exit]
+        int32_t* d_acc = nullptr;
+        uint64_t lo = 0, hi = 0, pre = 0;
+        uint32_t st[2] = {0, 0};
+        int32_t acc = 0;
+    };
+    std::vector<Seg> seg(static_cast<size_t>(ndev));
+    int rc = RXG_OK;
+    auto run = [&](Seg& g, bool guess, uint32_t entry) -> int {
+        DeviceGuard dg(g.h->device);
+        rxg_one_opts o{};
+        o.flags = RXG_ONE_ENTRY;
+        if (guess) {   // the state the 64-byte prefix leads to from the start state
+            o.flags = 0;
+            o.d_exit_state = g.d_st;
+            if (int r = rxg_match_one_ex(g.h, g.d, g.pre, RXG_ENGINE_CHUNKED, g.d_acc, &o, g.h->stream)) return r;
+            return RXG_OK;
+        }
+        o.entry_state = entry;
+        o.d_exit_state = g.d_st + 1;
+        return rxg_match_one_ex(g.h, g.d + g.pre, g.hi - g.lo, RXG_ENGINE_CHUNKED, g.d_acc, &o, g.h->stream);
+    };
+    for (int k = 0; k < ndev && rc == RXG_OK; ++k) {
+        Seg& g = seg[static_cast<size_t>(k)];
+        g.lo = len * static_cast<uint64_t>(k) / static_cast<uint64_t>(ndev) / 16 * 16;
+        g.hi = k + 1 == ndev ? len : len * static_cast<uint64_t>(k + 1) / static_cast<uint64_t>(ndev) / 16 * 16;
+        g.pre = std::min<uint64_t>(kPre, g.lo);
+        if ((rc = rxg_heap_create_pattern(pattern, plen, devices[k], &g.h))) break;
+        if ((rc = need_device(g.h))) break;
+        DeviceGuard dg(g.h->device);
+        if (cudaMalloc(&g.d, g.pre + (g.hi - g.lo) + 32) != cudaSuccess || cudaMalloc(&g.d_st, 16) != cudaSuccess ||
+            cudaMalloc(&g.d_acc, 16) != cudaSuccess) {
+            rc = fail(RXG_ENOMEM, "device allocation failed");
+            break;
+        }
+        const cudaError_t e = cudaMemcpyAsync(g.d, text + g.lo - g.pre, g.pre + (g.hi - g.lo), cudaMemcpyHostToDevice,
+                                              g.h->stream);
+        if (e != cudaSuccess) {
+            rc = cuda_fail(e, "segment upload");
+            break;
+        }
+        // segment k > 0 guesses its entry from its prefix; every device runs at once
+        if (k > 0) {
+            if ((rc = run(g, true, 0))) break;
+            if (cudaMemcpyAsync(&g.st[0], g.d_st, 4, cudaMemcpyDeviceToHost, g.h->stream) != cudaSuccess) {
+                rc = cuda_fail(cudaGetLastError(), "guess readback");
+                break;
+            }
+        }
+    }
+    // phase 1: the guesses land, then each segment runs from its guess
+    for (int k = 0; k < ndev && rc == RXG_OK; ++k) {
+        Seg& g = seg[static_cast<size_t>(k)];
+        DeviceGuard dg(g.h->device);
+        if (cudaStreamSynchronize(g.h->stream) != cudaSuccess) {
+            rc = cuda_fail(cudaGetLastError(), "guess");
+            break;
+        }
+        rc = run(g, false, k == 0 ? kStartState : g.st[0]);
+        if (rc == RXG_OK && (cudaMemcpyAsync(&g.st[1], g.d_st + 1, 4, cudaMemcpyDeviceToHost, g.h->stream) != cudaSuccess ||
+                             cudaMemcpyAsync(&g.acc, g.d_acc, 4, cudaMemcpyDeviceToHost, g.h->stream) != cudaSuccess))
+            rc = cuda_fail(cudaGetLastError(), "segment readback");
+    }
+    // phase 2: chain the exact states in order; re-run a segment whose guess was wrong
+    int32_t reruns = 0;
+    uint32_t exact = 0;
+    for (int k = 0; k < ndev && rc == RXG_OK; ++k) {
+        Seg& g = seg[static_cast<size_t>(k)];
+        DeviceGuard dg(g.h->device);
+        if (cudaStreamSynchronize(g.h->stream) != cudaSuccess) {
+            rc = cuda_fail(cudaGetLastError(), "segment");
+            break;
+        }
+        if (k > 0 && g.st[0] != exact) {
+            ++reruns;
+            if ((rc = run(g, false, exact))) break;
+            if (cudaMemcpyAsync(&g.st[1], g.d_st + 1, 4, cudaMemcpyDeviceToHost, g.h->stream) != cudaSuccess ||
+                cudaMemcpyAsync(&g.acc, g.d_acc, 4, cudaMemcpyDeviceToHost, g.h->stream) != cudaSuccess ||
+                cudaStreamSynchronize(g.h->stream) != cudaSuccess) {
+                rc = cuda_fail(cudaGetLastError(), "segment re-run");
+                break;
+            }
+        }
+        exact = g.st[1];
+        *accept = g.acc;
+    }
+    for (auto& g : seg) {
+        if (!g.h) continue;
+        DeviceGuard dg(g.h->device);
+        cudaStreamSynchronize(g.h->stream);
+        if (g.d) cudaFree(g.d);
+        if (g.d_st) cudaFree(g.d_st);
+        if (g.d_acc) cudaFree(g.d_acc);
+        rxg_heap_destroy(g.h);
+    }
+    if (resegments) *resegments = reruns;
+    g_launches = ndev + reruns;
     return rc;
 }
 

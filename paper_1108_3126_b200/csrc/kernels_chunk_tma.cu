@@ -78,6 +78,8 @@ struct Args {
     unsigned long long* bad_inv;   // ~(first range whose entry guess is wrong); 0 = none (zero-initialised)
     int32_t* accept;
     unsigned long long* repairs;
+    uint32_t entry;        // table state the string starts in (the start state unless chained)
+    uint32_t* exit_state;  // nullable: table state after the string
 };
 
 template <bool CLS>
@@ -115,7 +117,7 @@ __device__ uint32_t walk(const Args& a, uint32_t s, uint64_t lo, uint64_t hi) {
 template <bool CLS>
 __device__ uint32_t entry_guess(const Args& a, uint64_t r) {
     const uint64_t c0 = r * a.chunk;
-    return r == 0 ? a.start : walk<CLS>(a, a.start, c0 > a.lookback ? c0 - a.lookback : 0, c0);
+    return r == 0 ? a.entry : walk<CLS>(a, a.start, c0 > a.lookback ? c0 - a.lookback : 0, c0);
 }
 
 // Entry guesses of a lane's ranges (rows row0 + 32 j + lane): with the
@@ -162,7 +164,7 @@ __device__ void repair_and_answer(const Args& a) {
     const uint32_t per = (a.chunk + kMidT - 1) / kMidT;
     unsigned long long repairs = 0;
     const unsigned long long fb = ~*reinterpret_cast<volatile unsigned long long*>(a.bad_inv);
-    uint32_t exact = a.nranges == 0 ? a.start : (fb == ~0ull ? a.e[a.nranges - 1] : a.e[fb - 1]);
+    uint32_t exact = a.nranges == 0 ? a.entry : (fb == ~0ull ? a.e[a.nranges - 1] : a.e[fb - 1]);
     for (uint64_t base = fb == ~0ull ? a.nranges : fb; base < a.nranges; base += 32) {
         uint64_t j = base;
         while (j < a.nranges && j < base + 32) {
@@ -203,6 +205,7 @@ __device__ void repair_and_answer(const Args& a) {
         const uint32_t acc_addr = CLS ? kLtSmemBase + 1024 + exact * a.row_bytes + a.acc_off : exact + a.acc_off;
         *a.accept = static_cast<int32_t>(tma::lds16(acc_addr));
         if (a.repairs) *a.repairs = repairs;
+        if (a.exit_state) *a.exit_state = exact;
         // idle slot for the next launch on this stream (CountSlot, launch.hpp)
         atomicExch(a.bad_inv, 0ull);
         atomicExch(a.ticket, 0u);
@@ -386,7 +389,7 @@ size_t chunked_tma_scratch_bytes(uint64_t len, uint32_t chunk) {
 
 cudaError_t launch_chunked_tma(const LtTable& t, const void* d_img, const uint8_t* text, uint64_t len, uint32_t chunk,
                                uint32_t lookback, void* scratch, int32_t* accept, unsigned long long* repairs,
-                               CountSlot cs, int device, cudaStream_t st) {
+                               CountSlot cs, int device, cudaStream_t st, uint32_t entry, uint32_t* exit_state) {
     if (chunk == 0 || chunk % kSlice) return cudaErrorInvalidValue;
     Args a{};
     a.text = text;
@@ -399,6 +402,8 @@ cudaError_t launch_chunked_tma(const LtTable& t, const void* d_img, const uint8_
     a.img = static_cast<const uint4*>(d_img);
     a.img_words = t.lo_bytes / 16;
     a.start = t.start;
+    a.entry = entry == kStartState ? t.start : entry;
+    a.exit_state = exit_state;
     a.row_bytes = t.row_bytes;
     a.cmap_addr = t.cmap_addr;
     a.acc_off = t.acc_off;

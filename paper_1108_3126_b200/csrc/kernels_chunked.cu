@@ -36,6 +36,8 @@ struct ChunkArgs {
     uint32_t* e;         // nranges
     uint32_t* mid;       // nranges x (chunk / kMid)
     int32_t* accept;
+    uint32_t entry;                // table state the string starts in
+    uint32_t* exit_state;          // nullable: table state after the string
     unsigned long long* repairs;   // ranges re-walked (instrumentation, nullable)
     unsigned int* ticket;          // zeroed before the walk: CTAs finished
     unsigned long long* first_bad; // set to ~0 before the walk: first range whose entry guess is wrong
@@ -83,7 +85,7 @@ __global__ void __launch_bounds__(256) k_chunk_walk(const __grid_constant__ Chun
     for (uint64_t base = static_cast<uint64_t>(blockIdx.x) * blockDim.x; base < a.nranges; base += stride) {
         const uint64_t j = base + threadIdx.x;
         const bool live = j < a.nranges;
-        uint32_t s = a.start, guess = a.start;
+        uint32_t s = a.entry, guess = a.entry;
         if (live) {
             const uint64_t c0 = j * a.chunk;
             const uint64_t c1 = min(c0 + a.chunk, a.len);
@@ -133,7 +135,7 @@ __global__ void __launch_bounds__(32) k_chunk_fix(const __grid_constant__ ChunkA
     unsigned long long repairs = 0;
     const unsigned long long fb = *a.first_bad;
     // ranges before the first wrong guess chain exactly (range 0 starts at the true start)
-    uint32_t exact = a.nranges == 0 ? a.start : (fb == ~0ull ? a.e[a.nranges - 1] : a.e[fb - 1]);
+    uint32_t exact = a.nranges == 0 ? a.entry : (fb == ~0ull ? a.e[a.nranges - 1] : a.e[fb - 1]);
     for (uint64_t base = fb == ~0ull ? a.nranges : fb; base < a.nranges; base += 32) {
         // ranges base..base+31: find mismatches in order; after a repair the
         // exact exit may change, so re-scan from the repaired range.
@@ -176,6 +178,7 @@ __global__ void __launch_bounds__(32) k_chunk_fix(const __grid_constant__ ChunkA
     }
     if (lane == 0) {
         *a.accept = static_cast<int32_t>(*reinterpret_cast<const E*>(sm + exact + a.acc_col));
+        if (a.exit_state) *a.exit_state = exact;
         if (a.repairs) *a.repairs = repairs;
     }
 }
@@ -218,7 +221,8 @@ uint32_t chunked_auto_chunk(const DevTable& t, uint64_t len, int device) {
 }
 
 cudaError_t launch_chunked(const DevTable& t, const uint8_t* text, uint64_t len, uint32_t chunk, uint32_t lookback,
-                           void* scratch, int32_t* accept, unsigned long long* repairs, int device, cudaStream_t st) {
+                           void* scratch, int32_t* accept, unsigned long long* repairs, int device, cudaStream_t st,
+                           uint32_t entry, uint32_t* exit_state) {
     ChunkArgs a{};
     a.text = text;
     a.len = len;
@@ -229,6 +233,8 @@ cudaError_t launch_chunked(const DevTable& t, const uint8_t* text, uint64_t len,
     a.img_words = t.img_bytes / 16;
     a.cls_off = t.cls_off;
     a.start = t.start;
+    a.entry = entry == kStartState ? t.start : entry;
+    a.exit_state = exit_state;
     a.dead = t.dead;
     a.acc_col = t.ncols * static_cast<uint32_t>(t.esize);
     a.ticket = static_cast<unsigned int*>(scratch);

@@ -393,6 +393,18 @@ def match_many(patterns, text, delimiter: int = 10, stride: int = 0, device: int
     return res[: len(patterns) * ns.value].reshape(len(patterns), ns.value)
 
 
+def match_one_multi(devices, pattern, text):
+    """One long string split over several GPUs (chunk-speculative across
+    devices, exact) -> (accept, segments re-run)."""
+    devs = (C.c_int * len(devices))(*devices)
+    pat = _b(pattern)
+    p, n, keep = _ptr(text)
+    acc = C.c_int32(0)
+    rer = C.c_int32(0)
+    _check(L.lib().rxg_match_one_multi(devs, len(devices), pat, len(pat), p, n, C.byref(acc), C.byref(rer)))
+    return bool(acc.value), rer.value
+
+
 def shard_bounds(text, ndev: int, delimiter: int = 10, stride: int = 0) -> list[int]:
     p, n, keep = _ptr(text)
     off = (C.c_uint64 * (ndev + 1))()

@@ -158,3 +158,54 @@ def test_config_e_k1_checkpoints_verified_chunk_parallel():
     pos_addr, _, _ = rx.Matcher(p, device=-1).tables()
     assert verify_checkpoints(rx.compile(rx.parse(p)), pos_addr, len(pos_addr), rows, w, every) == n // every
     assert bool(acc.item()) == bool((rows[-1][len(pos_addr) >> 5] >> (len(pos_addr) & 31)) & 1)
+
+
+def test_chunked_entry_exit_states_chain_segments():
+    """A string cut anywhere: the exit state of the first part, used as the
+    entry of the second, gives the whole string's answer (including
+    non-synchronizing automata), and chaining from the start state equals
+    the default run."""
+    rng = np.random.default_rng(21)
+    for p in ["(a|b)*abb", "(aa)*", "((a|b)(a|b))*", rx.synth_pattern("c")]:
+        m = rx.Matcher(p)
+        o = O(p)
+        alpha = [97, 98] if "ERROR" not in p else list(b"abcdefgh ERORWANFIL")
+        w = rng.choice(alpha, size=200_003).astype(np.uint8)
+        if p == "(aa)*":
+            w[:] = 97
+        for cut in (0, 1, 4096, 100_000, 200_003):
+            d1 = torch.from_numpy(w[:cut].copy()).cuda() if cut else torch.zeros(16, dtype=torch.uint8, device="cuda")
+            d2 = torch.from_numpy(w[cut:].copy()).cuda() if cut < len(w) else torch.zeros(16, dtype=torch.uint8, device="cuda")
+            ex = torch.zeros(2, dtype=torch.int32, device="cuda")
+            acc = torch.zeros(1, dtype=torch.int32, device="cuda")
+            m.match_one_ex(d1, acc, "chunked", nbytes=cut, d_exit_state=ex[0:1])
+            torch.cuda.synchronize()
+            e1 = int(ex[0].item()) & 0xFFFFFFFF
+            m.match_one_ex(d2, acc, "chunked", nbytes=len(w) - cut, flags=1, entry_state=e1, d_exit_state=ex[1:2])
+            torch.cuda.synchronize()
+            assert bool(acc.item()) == o.accepts(w.tobytes()), (p, cut)
+
+
+@pytest.mark.parametrize("ndev", [1, 2, 3, 5])
+def test_match_one_multi_segments(ndev):
+    """rxg_match_one_multi with the one GPU listed several times: segments
+    run from guessed entries, wrong guesses are re-run in order; exact."""
+    rng = np.random.default_rng(ndev)
+    for p, n in [("(a|b)*abb", 3_000_000), ("(aa)*", 1_000_002), (rx.synth_pattern("e"), 2_000_000)]:
+        if p == "(aa)*":
+            w = np.full(n, 97, np.uint8)
+        elif "abb" in p and len(p) < 20:
+            w = rng.choice([97, 98], size=n).astype(np.uint8)
+            w[-3:] = np.frombuffer(b"abb", np.uint8)
+        else:
+            w = rx.synth_input("e", n)
+        acc, reruns = rx.match_one_multi([0] * ndev, p, w)
+        want = rx.Matcher(p).lockstep_accepts(w.tobytes(), "dfa_seq")
+        assert acc == want, (p, ndev)
+    # (aaa)*: a 64-byte prefix leaves the counter at 64 mod 3, the true state
+    # at a 16-aligned cut is (offset mod 3): wrong guesses must be re-run
+    w = np.full(3_000_000, 97, np.uint8)
+    acc, reruns = rx.match_one_multi([0] * ndev, "(aaa)*", w)
+    assert acc is True
+    if ndev > 2:
+        assert reruns > 0
