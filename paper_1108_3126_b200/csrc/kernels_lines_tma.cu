@@ -611,9 +611,13 @@ cudaError_t launch(const LtTable& t, const uint8_t* text, uint64_t len, uint8_t 
 // TMA-request bound (~3.3 TB/s); 32-byte slices with 24 warps x 2 ranges x 3
 // stages reach ~5.05 TB/s, x 3 ranges x 2 stages ~5.1-5.25 TB/s (direct layout);
 // 24x4x2, 32x3x2 and 16x4x3 measured 4.77-5.0 TB/s with the paired rows;
-// the class layout (two LDS per byte, ~225 KB with its ring) fits only S0.
+// the class layout uses SC (below).
 using S0 = Shape<24, 2, 32, 3>;
 using S6 = Shape<24, 3, 32, 2>;
+// class layout (two LDS per byte, random rows): fewer warps and a deeper ring,
+// (d) 1,761 GB/s vs 1,681 for S0 (16x2x5 1,737, 12x2x6 1,724, 20x2x4 1,697,
+// 16x3x2 1,676, 24x2x2 1,683, 32x2x2 1,603)
+using SC = Shape<16, 2, 32, 4>;
 
 int shape_id() {
     const char* e = std::getenv("RXG_LT_SHAPE");
@@ -624,9 +628,9 @@ template <bool RES>
 cudaError_t launch_any(const LtTable& t, const uint8_t* text, uint64_t len, uint8_t delim, uint32_t chunk,
                        unsigned long long* count, uint8_t* results, void* scratch, size_t scratch_bytes,
                        CountSlot cs, cudaStream_t st) {
-    if (t.cls || shape_id() == 0)
-        return t.cls ? launch<S0, true, RES>(t, text, len, delim, chunk, count, results, scratch, scratch_bytes, cs, st)
-                     : launch<S0, false, RES>(t, text, len, delim, chunk, count, results, scratch, scratch_bytes, cs, st);
+    if (t.cls) return launch<SC, true, RES>(t, text, len, delim, chunk, count, results, scratch, scratch_bytes, cs, st);
+    if (shape_id() == 0)
+        return launch<S0, false, RES>(t, text, len, delim, chunk, count, results, scratch, scratch_bytes, cs, st);
     return launch<S6, false, RES>(t, text, len, delim, chunk, count, results, scratch, scratch_bytes, cs, st);
 }
 
@@ -639,7 +643,8 @@ cudaError_t launch_lines_tma(const LtTable& t, const uint8_t* text, uint64_t len
 
 uint32_t lines_tma_chunk(const LtTable& t, uint64_t len, uint32_t chunk) {
     if (chunk) return chunk;
-    if (t.cls || shape_id() == 0) return t.cls ? auto_chunk<S0, true>(t, len) : auto_chunk<S0, false>(t, len);
+    if (t.cls) return auto_chunk<SC, true>(t, len);
+    if (shape_id() == 0) return auto_chunk<S0, false>(t, len);
     return auto_chunk<S6, false>(t, len);
 }
 
