@@ -34,6 +34,63 @@ struct ParseError : std::runtime_error {
     ParseError(size_t p, const std::string& what) : std::runtime_error(what), pos(p) {}
 };
 
+// rx::decode_utf8 / encode_utf8 (utf8.hpp): the host-side conversions the
+// reference's callers apply around the matcher (rxvm.cpp:85-87). Same
+// acceptance rules and error text ("invalid UTF-8 at byte N").
+inline std::u32string decode_utf8(std::string_view bytes) {
+    std::u32string out;
+    out.reserve(bytes.size());
+    auto fail = [](size_t at) -> void { throw std::runtime_error("invalid UTF-8 at byte " + std::to_string(at)); };
+    for (size_t i = 0; i < bytes.size();) {
+        const auto lead = static_cast<unsigned char>(bytes[i]);
+        if (lead < 0x80) {
+            out.push_back(lead);
+            ++i;
+            continue;
+        }
+        const size_t n = (lead & 0xE0) == 0xC0 ? 2 : (lead & 0xF0) == 0xE0 ? 3 : (lead & 0xF8) == 0xF0 ? 4 : 0;
+        if (n == 0 || i + n > bytes.size()) fail(i);
+        char32_t cp = lead & (n == 2 ? 0x1F : n == 3 ? 0x0F : 0x07);
+        for (size_t k = 1; k < n; ++k) {
+            const auto b = static_cast<unsigned char>(bytes[i + k]);
+            if ((b & 0xC0) != 0x80) fail(i + k);
+            cp = (cp << 6) | (b & 0x3F);
+        }
+        const char32_t least = n == 2 ? 0x80 : n == 3 ? 0x800 : 0x10000;
+        if (cp < least || cp > 0x10FFFF || (cp >= 0xD800 && cp <= 0xDFFF)) fail(i);
+        out.push_back(cp);
+        i += n;
+    }
+    return out;
+}
+
+inline std::string encode_utf8(char32_t cp) {
+    std::string s;
+    if (cp < 0x80) {
+        s += static_cast<char>(cp);
+    } else if (cp < 0x800) {
+        s += static_cast<char>(0xC0 | (cp >> 6));
+        s += static_cast<char>(0x80 | (cp & 0x3F));
+    } else if (cp < 0x10000) {
+        s += static_cast<char>(0xE0 | (cp >> 12));
+        s += static_cast<char>(0x80 | ((cp >> 6) & 0x3F));
+        s += static_cast<char>(0x80 | (cp & 0x3F));
+    } else {
+        s += static_cast<char>(0xF0 | (cp >> 18));
+        s += static_cast<char>(0x80 | ((cp >> 12) & 0x3F));
+        s += static_cast<char>(0x80 | ((cp >> 6) & 0x3F));
+        s += static_cast<char>(0x80 | (cp & 0x3F));
+    }
+    return s;
+}
+
+inline std::string encode_utf8(std::u32string_view text) {
+    std::string s;
+    s.reserve(text.size());
+    for (char32_t cp : text) s += encode_utf8(cp);
+    return s;
+}
+
 // The facade keeps the validated pattern; compile() lays it out.
 struct Regex {
     std::string text;
@@ -69,28 +126,7 @@ inline void check(int rc) {
 }
 // Symbols to the UTF-8 bytes the device matches (literals are expanded to
 // UTF-8 byte chains, so this is exact for every scalar).
-inline std::string narrow(InputView w) {
-    std::string s;
-    s.reserve(w.size());
-    for (char32_t cp : w) {
-        if (cp < 0x80) {
-            s += static_cast<char>(cp);
-        } else if (cp < 0x800) {
-            s += static_cast<char>(0xC0 | (cp >> 6));
-            s += static_cast<char>(0x80 | (cp & 0x3F));
-        } else if (cp < 0x10000) {
-            s += static_cast<char>(0xE0 | (cp >> 12));
-            s += static_cast<char>(0x80 | ((cp >> 6) & 0x3F));
-            s += static_cast<char>(0x80 | (cp & 0x3F));
-        } else {
-            s += static_cast<char>(0xF0 | (cp >> 18));
-            s += static_cast<char>(0x80 | ((cp >> 12) & 0x3F));
-            s += static_cast<char>(0x80 | ((cp >> 6) & 0x3F));
-            s += static_cast<char>(0x80 | (cp & 0x3F));
-        }
-    }
-    return s;
-}
+inline std::string narrow(InputView w) { return encode_utf8(w); }
 }  // namespace detail
 
 // The compiled heap (heap.hpp:28-37) plus its device-resident tables. The
@@ -198,7 +234,8 @@ inline bool par_accepts(const Heap& h, InputView w, unsigned workers, uint64_t s
 
 // The `rxvm match` loop as one call: per-line results for a '\n'-separated
 // UTF-8 buffer (std::getline semantics). Returns the number of matching lines.
-inline uint64_t match_lines(const Heap& h, std::string_view text, std::vector<uint8_t>* per_line = nullptr) {
+inline uint64_t match_lines(const Heap& h, std::string_view text, std::vector<uint8_t>* per_line = nullptr,
+                            uint64_t* utf8_first_bad = nullptr) {
     uint64_t count = 0;
     if (per_line) {
         uint64_t lines = 0;
@@ -206,8 +243,11 @@ inline uint64_t match_lines(const Heap& h, std::string_view text, std::vector<ui
         if (!text.empty() && text.back() != '\n') ++lines;
         per_line->assign(lines + 1, 0);
     }
-    detail::check(rxg_match_batch_host(h.device_handle(), reinterpret_cast<const uint8_t*>(text.data()), text.size(),
-                                       '\n', 0, &count, per_line ? per_line->data() : nullptr));
+    // utf8_first_bad: the device UTF-8 check of every line, fused into the same pass
+    // (UINT64_MAX when every line decodes; else the buffer offset decode_utf8 names)
+    detail::check(rxg_match_batch_host_ex(h.device_handle(), reinterpret_cast<const uint8_t*>(text.data()),
+                                          text.size(), '\n', 0, &count, per_line ? per_line->data() : nullptr,
+                                          utf8_first_bad));
     if (per_line && !per_line->empty()) per_line->pop_back();
     return count;
 }

@@ -29,6 +29,21 @@ int main(int argc, char** argv) {
     } catch (const rx::ParseError& e) {
         CHECK(e.pos == 3);
     }
+    // decode_utf8 / encode_utf8 (utf8.hpp) with the reference's error text
+    CHECK(rx::decode_utf8("a\xc3\xa9\xe4\xb8\xad") == U"a\u00e9\u4e2d");
+    CHECK(rx::encode_utf8(U"a\u00e9\U0001F600") == "a\xc3\xa9\xf0\x9f\x98\x80");
+    try {
+        rx::decode_utf8("ab\xe4\xb8");
+        CHECK(false);
+    } catch (const std::runtime_error& e) {
+        CHECK(std::string(e.what()) == "invalid UTF-8 at byte 2");
+    }
+    try {
+        rx::decode_utf8("\xed\xa0\x80");
+        CHECK(false);
+    } catch (const std::runtime_error& e) {
+        CHECK(std::string(e.what()) == "invalid UTF-8 at byte 0");
+    }
     if (gpu) {
         CHECK(rx::lockstep_accepts(h, U"aab"));
         CHECK(!rx::lockstep_accepts(h, U"aa"));
@@ -39,6 +54,9 @@ int main(int argc, char** argv) {
         std::vector<uint8_t> per;
         const uint64_t n = rx::match_lines(rx::compile(*rx::parse("(a|b)*abb")), "abb\nab\n\nbabb\nx", &per);
         CHECK(n == 2 && per.size() == 5 && per[0] == 1 && per[1] == 0 && per[2] == 0 && per[3] == 1 && per[4] == 0);
+        uint64_t bad = 0;
+        rx::match_lines(rx::compile(*rx::parse("(a|b)*abb")), "abb\na\xffb\n", nullptr, &bad);
+        CHECK(bad == 5);   // the 0xFF byte: decode_utf8 of line 2 fails at its byte 1
     }
     std::printf("%s %d failures\n", gpu ? "gpu" : "cpu", failures);
     return failures ? 1 : 0;
