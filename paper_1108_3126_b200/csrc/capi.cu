@@ -800,13 +800,14 @@ int rxg_host_emulate_lines_tma(const rxg_heap* h, const uint8_t* text, uint64_t 
     }
     uint64_t cnt = 0;
     for (const auto& [c0, c1] : ranges) {
-        uint32_t s = (c0 == 0 || text[c0 - 1] == d) ? t.start : t.skip;
+        uint32_t s = c0 == 0 ? t.start : t.skip;   // the line at a range's first byte is the previous range's
         for (uint64_t i = c0; i < c1; ++i) {
             s = lt_step(t, s, text[i]);
             cnt += lt_count(t, s);
         }
-        if (s != t.skip && text[c1 - 1] != d) {
-            s += t.tail_delta;
+        const bool next_line = text[c1 - 1] == d && c1 < len;
+        if (next_line || (s != t.skip && text[c1 - 1] != d)) {
+            s = (next_line ? t.start : s) + t.tail_delta;
             uint64_t pos = c1;
             while (pos < len && s < t.term_acc) {
                 const uint64_t end = std::min<uint64_t>((pos / 16 + 1) * 16, len);

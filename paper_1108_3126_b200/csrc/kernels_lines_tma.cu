@@ -19,10 +19,11 @@
 // 32), so lanes in different states reading the same byte land in
 // different banks.
 //
-// Line ownership (every line matched exactly once) is the rule of
-// kernels_batch.cu: a range owns the lines starting in it, enters in SKIP
-// unless the previous byte is the delimiter, and finishes its last line
-// through the tail copy of the table with direct global loads.
+// Line ownership (every line matched exactly once): a range owns the lines
+// starting in it after its first byte, plus the line starting right after
+// it when its last byte is the delimiter; it enters in SKIP (range 0 in the
+// start state) and finishes its last line through the tail copy of the
+// table with direct global loads (see range_direct).
 #include <cub/device/device_scan.cuh>
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -237,10 +238,16 @@ __device__ void finish_lines(const Args& a, uint32_t (&s)[K], uint64_t (&pos)[K]
     for (int j = 0; j < K; ++j) ok[j] = live[j] && s[j] == a.term_acc;
 }
 
+// Line ownership. Every range but the first starts in SKIP (no read of the
+// byte before it), so the line starting exactly at a range's first byte is
+// skipped there; the previous range takes it instead: a range whose last
+// byte is the delimiter walks the next line from the start state, exactly
+// like a line straddling its end. Each line is matched by one range.
+//
 // A range processed entirely with direct loads (the remainder pieces).
 template <bool CLS, bool RES>
 __device__ void range_direct(const Args& a, uint64_t c0, uint64_t c1, uint64_t range, uint32_t& cnt) {
-    uint32_t s = (c0 == 0 || a.text[c0 - 1] == a.delim) ? a.start : a.skip;
+    uint32_t s = c0 == 0 ? a.start : a.skip;
     LineCursor lc{RES ? a.line_base[range] : 0, s == a.start, true};
     uint32_t last = 0;
     uint64_t pos = c0;
@@ -268,8 +275,9 @@ __device__ void range_direct(const Args& a, uint64_t c0, uint64_t c1, uint64_t r
             cnt += counted<CLS>(a, s);
         }
     }
-    if (s != a.skip && last != a.delim) {
-        const uint32_t ok = finish_line<CLS>(a, s + a.tail_delta, c1) == a.term_acc;
+    const bool next_line = last == a.delim && c1 < a.len;
+    if (next_line || (s != a.skip && last != a.delim)) {
+        const uint32_t ok = finish_line<CLS>(a, (next_line ? a.start : s) + a.tail_delta, c1) == a.term_acc;
         cnt += ok;
         if constexpr (RES) a.results[lc.li] = static_cast<uint8_t>(ok);
     }
@@ -340,10 +348,7 @@ __global__ void __launch_bounds__(C::warps * 32, 1) k_lines_tma(const __grid_con
             const uint64_t row = row0 + j * 32 + lane;
             valid[j] = row < a.rows;
             s[j] = a.void_row;
-            if (valid[j]) {
-                const uint64_t c0 = row * a.chunk;
-                s[j] = (c0 == 0 || a.text[c0 - 1] == a.delim) ? a.start : a.skip;
-            }
+            if (valid[j]) s[j] = row == 0 ? a.start : a.skip;   // see the ownership note above range_direct
             lc[j] = LineCursor{RES && valid[j] ? a.line_base[row] : 0, valid[j] && s[j] == a.start, valid[j]};
         }
         uint32_t last[C::chains] = {};
@@ -388,9 +393,10 @@ __global__ void __launch_bounds__(C::warps * 32, 1) k_lines_tma(const __grid_con
             uint32_t ok[C::chains];
 #pragma unroll
             for (int j = 0; j < C::chains; ++j) {
-                live[j] = valid[j] && s[j] != a.skip && last[j] != a.delim;
                 pos[j] = (row0 + j * 32 + lane + 1) * a.chunk;
-                s[j] += a.tail_delta;
+                const bool next_line = last[j] == a.delim && pos[j] < a.len;   // the line starting right after
+                live[j] = valid[j] && (next_line || (s[j] != a.skip && last[j] != a.delim));
+                s[j] = (next_line ? a.start : s[j]) + a.tail_delta;
             }
             finish_lines<CLS, C::chains>(a, s, pos, live, ok);
 #pragma unroll
