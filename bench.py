@@ -56,7 +56,8 @@ def peaks():
 
 
 class ClockSampler:
-    """SM clocks and throttle reasons sampled (NVML, ~1 ms) during the timed region."""
+    """SM clocks and throttle reasons sampled (NVML, every ~0.25 ms, plus one sample at
+    the start and one at the end) during the timed region."""
 
     REASONS = {  # nvmlClocksEventReasons bits
         "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40, "sw_power_cap": 0x4,
@@ -91,20 +92,20 @@ class ClockSampler:
     def _loop(self):
         while not self.stop.is_set():
             self._sample()
-            time.sleep(0.001)
+            time.sleep(0.00025)
 
     def __enter__(self):
         if self.h is not None:
+            self._sample()
             self.t = threading.Thread(target=self._loop, daemon=True)
             self.t.start()
         return self
 
     def __exit__(self, *exc):
         if self.h is not None:
+            self._sample()   # the end of the region (the GPU is still busy: the caller syncs after)
             self.stop.set()
             self.t.join()
-            if not self.rows:   # region shorter than one poll: sample right at its end
-                self._sample()
 
     def summary(self):
         if not self.rows:
