@@ -57,7 +57,8 @@ struct Args {
     uint32_t stage_addr[kMaxSlots];
     uint32_t start, skip, void_row, tail_delta, term_acc;
     uint32_t delim;
-    uint32_t row_bytes, cmap_addr, acc_shift;   // class layout
+    uint32_t row_bytes, cmap_addr, acc_shift;   // class layouts
+    uint32_t rows_addr, range_x, range_k;       // range-clamped columns
     uint32_t col_bytes;                         // direct layout: column stride
     unsigned long long* count;
     unsigned long long* slot;                   // CountSlot (launch.hpp)
@@ -103,27 +104,30 @@ __device__ __forceinline__ uint32_t lds32(uint32_t addr) {
 
 // One memoized step on byte b. Direct layout: s is an absolute row address.
 // Class layout: s is a row index, the class map gives the column address.
-template <bool CLS>
+// Table layouts (template parameter L): 0 direct, 1 class (class-map LDS),
+// 2 class rows with range-clamped columns (column = min(b ^ x, k), no LDS).
+template <int L>
 __device__ __forceinline__ uint32_t step_b(const Args& a, uint32_t s, uint32_t b) {
-    if constexpr (CLS) return tab(s * a.row_bytes + lds32(a.cmap_addr + b * 4u));
+    if constexpr (L == 2) return tab(s * a.row_bytes + a.rows_addr + 2u * min(b ^ a.range_x, a.range_k));
+    else if constexpr (L == 1) return tab(s * a.row_bytes + lds32(a.cmap_addr + b * 4u));
     else return tab(s + b * a.col_bytes);
 }
 
-template <bool CLS, bool IDP = false>
+template <int L, bool IDP = false>
 __device__ __forceinline__ uint32_t step(const Args& a, uint32_t s, uint32_t word, int k) {
-    if constexpr (IDP) {
+    if constexpr (IDP && L != 2) {
         // one IDP.4A.U8 extracts byte k, scales it by the column stride and adds the row
         // (replaces PRMT + IMAD; measured neutral on (c)/(d): the loop is shared-memory bound)
-        if constexpr (CLS) return tab(s * a.row_bytes + lds32(__dp4a(word, 4u << (8 * k), a.cmap_addr)));
+        if constexpr (L == 1) return tab(s * a.row_bytes + lds32(__dp4a(word, 4u << (8 * k), a.cmap_addr)));
         else return tab(__dp4a(word, a.col_bytes << (8 * k), s));
     }
-    return step_b<CLS>(a, s, __byte_perm(word, 0, 0x4440 + k));
+    return step_b<L>(a, s, __byte_perm(word, 0, 0x4440 + k));
 }
 
 // 1 iff s is START_A (the accepted-line-end row).
-template <bool CLS>
+template <int L>
 __device__ __forceinline__ uint32_t counted(const Args& a, uint32_t s) {
-    if constexpr (CLS) return s >> a.acc_shift;
+    if constexpr (L != 0) return s >> a.acc_shift;
     else return __umulhi(s, 1u << 17);
 }
 
@@ -166,7 +170,7 @@ __device__ __forceinline__ uint32_t granule(uint32_t r, uint32_t g) {
 }
 
 // Finish the line straddling a range end with direct loads (tail copy rows).
-template <bool CLS>
+template <int L>
 __device__ uint32_t finish_line(const Args& a, uint32_t s, uint64_t pos) {
     while (pos < a.len) {
         if (pos + 16 <= a.len) {
@@ -174,22 +178,22 @@ __device__ uint32_t finish_line(const Args& a, uint32_t s, uint64_t pos) {
 #pragma unroll
             for (int w = 0; w < 4; ++w)
 #pragma unroll
-                for (int k = 0; k < 4; ++k) s = step<CLS>(a, s, word_of(v, w), k);
+                for (int k = 0; k < 4; ++k) s = step<L>(a, s, word_of(v, w), k);
             pos += 16;
         } else {
-            for (; pos < a.len; ++pos) s = step_b<CLS>(a, s, a.text[pos]);
+            for (; pos < a.len; ++pos) s = step_b<L>(a, s, a.text[pos]);
         }
         if (s >= a.term_acc) return s;
     }
-    return step_b<CLS>(a, s, a.delim);
+    return step_b<L>(a, s, a.delim);
 }
 
 // One byte of a RES walk: step, count, and at a delimiter record the line
 // that just ended (if owned) and move to the next one.
-template <bool CLS>
+template <int L>
 __device__ __forceinline__ uint32_t step_res(const Args& a, uint32_t s, uint32_t b, uint32_t& cnt, LineCursor& lc) {
-    s = step_b<CLS>(a, s, b);
-    const uint32_t c = counted<CLS>(a, s);
+    s = step_b<L>(a, s, b);
+    const uint32_t c = counted<L>(a, s);
     cnt += c;
     if (b == a.delim) {
         if (lc.own) a.results[lc.li] = static_cast<uint8_t>(c);
@@ -204,7 +208,7 @@ __device__ __forceinline__ uint32_t step_res(const Args& a, uint32_t s, uint32_t
 // the tail-copy row; TERM rows absorb, so a finished chain keeps stepping
 // harmlessly until the others are done. Returns per chain whether its line
 // was accepted (live[j] false: no straddling line).
-template <bool CLS, int K>
+template <int L, int K>
 __device__ void finish_lines(const Args& a, uint32_t (&s)[K], uint64_t (&pos)[K], const bool (&live)[K],
                              uint32_t (&ok)[K]) {
     bool more = false;
@@ -225,11 +229,11 @@ __device__ void finish_lines(const Args& a, uint32_t (&s)[K], uint64_t (&pos)[K]
 #pragma unroll
                 for (int w = 0; w < 4; ++w)
 #pragma unroll
-                    for (int k = 0; k < 4; ++k) s[j] = step<CLS>(a, s[j], word_of(v[j], w), k);
+                    for (int k = 0; k < 4; ++k) s[j] = step<L>(a, s[j], word_of(v[j], w), k);
                 pos[j] += 16;
             } else {   // the last bytes of the buffer, then the virtual delimiter
-                for (; pos[j] < a.len; ++pos[j]) s[j] = step_b<CLS>(a, s[j], a.text[pos[j]]);
-                if (s[j] < a.term_acc) s[j] = step_b<CLS>(a, s[j], a.delim);
+                for (; pos[j] < a.len; ++pos[j]) s[j] = step_b<L>(a, s[j], a.text[pos[j]]);
+                if (s[j] < a.term_acc) s[j] = step_b<L>(a, s[j], a.delim);
             }
             more |= s[j] < a.term_acc;
         }
@@ -245,7 +249,7 @@ __device__ void finish_lines(const Args& a, uint32_t (&s)[K], uint64_t (&pos)[K]
 // like a line straddling its end. Each line is matched by one range.
 //
 // A range processed entirely with direct loads (the remainder pieces).
-template <bool CLS, bool RES>
+template <int L, bool RES>
 __device__ void range_direct(const Args& a, uint64_t c0, uint64_t c1, uint64_t range, uint32_t& cnt) {
     uint32_t s = c0 == 0 ? a.start : a.skip;
     LineCursor lc{RES ? a.line_base[range] : 0, s == a.start, true};
@@ -258,10 +262,10 @@ __device__ void range_direct(const Args& a, uint64_t c0, uint64_t c1, uint64_t r
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 if constexpr (RES) {
-                    s = step_res<CLS>(a, s, __byte_perm(word_of(v, w), 0, 0x4440 + k), cnt, lc);
+                    s = step_res<L>(a, s, __byte_perm(word_of(v, w), 0, 0x4440 + k), cnt, lc);
                 } else {
-                    s = step<CLS>(a, s, word_of(v, w), k);
-                    cnt += counted<CLS>(a, s);
+                    s = step<L>(a, s, word_of(v, w), k);
+                    cnt += counted<L>(a, s);
                 }
             }
         last = v.w >> 24;
@@ -269,21 +273,21 @@ __device__ void range_direct(const Args& a, uint64_t c0, uint64_t c1, uint64_t r
     for (; pos < c1; ++pos) {
         last = a.text[pos];
         if constexpr (RES) {
-            s = step_res<CLS>(a, s, last, cnt, lc);
+            s = step_res<L>(a, s, last, cnt, lc);
         } else {
-            s = step_b<CLS>(a, s, last);
-            cnt += counted<CLS>(a, s);
+            s = step_b<L>(a, s, last);
+            cnt += counted<L>(a, s);
         }
     }
     const bool next_line = last == a.delim && c1 < a.len;
     if (next_line || (s != a.skip && last != a.delim)) {
-        const uint32_t ok = finish_line<CLS>(a, (next_line ? a.start : s) + a.tail_delta, c1) == a.term_acc;
+        const uint32_t ok = finish_line<L>(a, (next_line ? a.start : s) + a.tail_delta, c1) == a.term_acc;
         cnt += ok;
         if constexpr (RES) a.results[lc.li] = static_cast<uint8_t>(ok);
     }
 }
 
-template <class C, bool CLS, bool RES>
+template <class C, int L, bool RES>
 __global__ void __launch_bounds__(C::warps * 32, 1) k_lines_tma(const __grid_constant__ Args a,
                                                              const __grid_constant__ CUtensorMap map) {
     extern __shared__ __align__(1024) uint8_t sm[];
@@ -324,7 +328,7 @@ __global__ void __launch_bounds__(C::warps * 32, 1) k_lines_tma(const __grid_con
         const uint64_t r0 = a.rows * a.chunk;
         for (uint32_t p = lane; p < a.rem_pieces; p += 32) {
             const uint64_t c0 = r0 + static_cast<uint64_t>(p) * a.rem_piece;
-            range_direct<CLS, RES>(a, c0, min(c0 + a.rem_piece, a.len), a.rows + p, cnt);
+            range_direct<L, RES>(a, c0, min(c0 + a.rem_piece, a.len), a.rows + p, cnt);
         }
     }
 
@@ -371,10 +375,10 @@ __global__ void __launch_bounds__(C::warps * 32, 1) k_lines_tma(const __grid_con
 #pragma unroll
                         for (int j = 0; j < C::chains; ++j) {
                             if constexpr (RES) {
-                                s[j] = step_res<CLS>(a, s[j], __byte_perm(word_of(v[j], w), 0, 0x4440 + k), cnt, lc[j]);
+                                s[j] = step_res<L>(a, s[j], __byte_perm(word_of(v[j], w), 0, 0x4440 + k), cnt, lc[j]);
                             } else {
-                                s[j] = step<CLS, true>(a, s[j], word_of(v[j], w), k);
-                                cnt += counted<CLS>(a, s[j]);
+                                s[j] = step<L, true>(a, s[j], word_of(v[j], w), k);
+                                cnt += counted<L>(a, s[j]);
                             }
                         }
 #pragma unroll
@@ -398,7 +402,7 @@ __global__ void __launch_bounds__(C::warps * 32, 1) k_lines_tma(const __grid_con
                 live[j] = valid[j] && (next_line || (s[j] != a.skip && last[j] != a.delim));
                 s[j] = (next_line ? a.start : s[j]) + a.tail_delta;
             }
-            finish_lines<CLS, C::chains>(a, s, pos, live, ok);
+            finish_lines<L, C::chains>(a, s, pos, live, ok);
 #pragma unroll
             for (int j = 0; j < C::chains; ++j) {
                 cnt += ok[j];
@@ -477,22 +481,22 @@ __global__ void __launch_bounds__(256) k_lt_range_delims(const uint8_t* __restri
     }
 }
 
-template <class C, bool CLS, bool RES>
+template <class C, int L, bool RES>
 int per_sm_of(uint32_t smem) {
     int per_sm = 0;
-    auto* k = k_lines_tma<C, CLS, RES>;
+    auto* k = k_lines_tma<C, L, RES>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, C::warps * 32, smem);
     return per_sm < 1 ? 1 : per_sm;
 }
 
-template <class C, bool CLS>
+template <class C, int L>
 uint32_t auto_chunk(const LtTable& t, uint64_t len) {
     Args a{};
     const uint32_t smem = place_stages<C>(t, a);
     int dev = 0;
     cudaGetDevice(&dev);
-    const uint64_t rows = static_cast<uint64_t>(per_sm_of<C, CLS, false>(smem)) * device_sm_count(dev) * C::warps * C::rows;
+    const uint64_t rows = static_cast<uint64_t>(per_sm_of<C, L, false>(smem)) * device_sm_count(dev) * C::warps * C::rows;
     uint64_t c = (len + rows - 1) / rows;
     c = (c + C::slice - 1) / C::slice * C::slice;
     if (c < 4u * C::slice) c = 4u * C::slice;
@@ -523,14 +527,14 @@ size_t res_scratch_bytes(uint64_t nranges) {
     return 2 * nranges * sizeof(unsigned long long) + temp + 256;
 }
 
-template <class C, bool CLS, bool RES>
+template <class C, int L, bool RES>
 cudaError_t launch(const LtTable& t, const uint8_t* text, uint64_t len, uint8_t delim, uint32_t chunk,
                    unsigned long long* count, uint8_t* results, void* scratch, size_t scratch_bytes,
                    CountSlot cs, cudaStream_t st) {
     if (len == 0) {   // nothing to launch: the count is 0 (or unchanged when accumulating)
         return cs.accumulate ? cudaSuccess : cudaMemsetAsync(count, 0, sizeof(unsigned long long), st);
     }
-    if (chunk == 0) chunk = auto_chunk<C, CLS>(t, len);
+    if (chunk == 0) chunk = auto_chunk<C, L>(t, len);
     if (chunk % C::slice) return cudaErrorInvalidValue;
     Args a{};
     a.text = text;
@@ -577,6 +581,9 @@ cudaError_t launch(const LtTable& t, const uint8_t* text, uint64_t len, uint8_t 
     a.cmap_addr = t.cmap_addr;
     a.acc_shift = t.acc_shift;
     a.col_bytes = t.col_bytes;
+    a.rows_addr = kLtSmemBase + 1024;
+    a.range_x = t.range_x;
+    a.range_k = t.range_k;
     a.count = count;
     a.slot = cs.p;
     a.accumulate = cs.accumulate ? 1 : 0;
@@ -602,13 +609,13 @@ cudaError_t launch(const LtTable& t, const uint8_t* text, uint64_t len, uint8_t 
                                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
     }
-    const int per_sm = per_sm_of<C, CLS, RES>(smem);
+    const int per_sm = per_sm_of<C, L, RES>(smem);
     int dev = 0;
     cudaGetDevice(&dev);
     const uint64_t cap = static_cast<uint64_t>(per_sm) * device_sm_count(dev);
     const uint64_t want = (a.tiles + C::warps - 1) / C::warps;
     const int grid = static_cast<int>(want == 0 ? 1 : (want < cap ? want : cap));
-    k_lines_tma<C, CLS, RES><<<grid, C::warps * 32, smem, st>>>(a, map);
+    k_lines_tma<C, L, RES><<<grid, C::warps * 32, smem, st>>>(a, map);
     return cudaGetLastError();
 }
 
@@ -624,6 +631,8 @@ using S6 = Shape<24, 3, 32, 2>;
 // (d) 1,761 GB/s vs 1,681 for S0 (16x2x5 1,737, 12x2x6 1,724, 20x2x4 1,697,
 // 16x3x2 1,676, 24x2x2 1,683, 32x2x2 1,603)
 using SC = Shape<16, 2, 32, 4>;
+// range-clamped class rows: larger rows, a shallower ring so table + ring fit
+using SR = Shape<16, 2, 32, 3>;
 
 int shape_id() {
     const char* e = std::getenv("RXG_LT_SHAPE");
@@ -634,10 +643,12 @@ template <bool RES>
 cudaError_t launch_any(const LtTable& t, const uint8_t* text, uint64_t len, uint8_t delim, uint32_t chunk,
                        unsigned long long* count, uint8_t* results, void* scratch, size_t scratch_bytes,
                        CountSlot cs, cudaStream_t st) {
-    if (t.cls) return launch<SC, true, RES>(t, text, len, delim, chunk, count, results, scratch, scratch_bytes, cs, st);
+    if (t.cls && t.range_k)
+        return launch<SR, 2, RES>(t, text, len, delim, chunk, count, results, scratch, scratch_bytes, cs, st);
+    if (t.cls) return launch<SC, 1, RES>(t, text, len, delim, chunk, count, results, scratch, scratch_bytes, cs, st);
     if (shape_id() == 0)
-        return launch<S0, false, RES>(t, text, len, delim, chunk, count, results, scratch, scratch_bytes, cs, st);
-    return launch<S6, false, RES>(t, text, len, delim, chunk, count, results, scratch, scratch_bytes, cs, st);
+        return launch<S0, 0, RES>(t, text, len, delim, chunk, count, results, scratch, scratch_bytes, cs, st);
+    return launch<S6, 0, RES>(t, text, len, delim, chunk, count, results, scratch, scratch_bytes, cs, st);
 }
 
 }  // namespace
@@ -649,9 +660,10 @@ cudaError_t launch_lines_tma(const LtTable& t, const uint8_t* text, uint64_t len
 
 uint32_t lines_tma_chunk(const LtTable& t, uint64_t len, uint32_t chunk) {
     if (chunk) return chunk;
-    if (t.cls) return auto_chunk<SC, true>(t, len);
-    if (shape_id() == 0) return auto_chunk<S0, false>(t, len);
-    return auto_chunk<S6, false>(t, len);
+    if (t.cls && t.range_k) return auto_chunk<SR, 2>(t, len);
+    if (t.cls) return auto_chunk<SC, 1>(t, len);
+    if (shape_id() == 0) return auto_chunk<S0, 0>(t, len);
+    return auto_chunk<S6, 0>(t, len);
 }
 
 size_t lines_tma_results_scratch(uint64_t len, uint32_t chunk) {

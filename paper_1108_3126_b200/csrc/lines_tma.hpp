@@ -30,6 +30,7 @@ struct LtTable {
     uint32_t hole_lo = 0, hole_hi = 0;   // unused rows inside the table (class layout): stage slots go here
     uint32_t acc_off = 0;                // plain (chunk) tables: byte offset of a row's accept flag
     uint32_t col_bytes = kLtColBytes;    // direct layouts: column stride (entry for byte b at row + col_bytes*b)
+    uint32_t range_x = 0, range_k = 0;   // class layout with range-clamped columns: column = min(b ^ x, k) (k = 0: class map)
     std::vector<uint8_t> lo, hi;     // images of [lo_addr, +lo) main rows and [hi_addr, +hi) upper rows
     uint32_t lo_addr = 0, hi_addr = 0;
     uint32_t lo_bytes = 0, hi_bytes = 0;

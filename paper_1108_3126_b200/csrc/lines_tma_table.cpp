@@ -207,7 +207,8 @@ namespace {
 // numbered greedily (hottest first) into the offset class that collides least
 // with the already numbered hot states under the sampled class frequencies.
 std::vector<uint32_t> number_states(const Program& p, const Dfa& d, uint8_t delim, const std::vector<double>* freq,
-                                    uint32_t nmain, uint32_t base_word, uint32_t rb_words, uint32_t delim_col) {
+                                    uint32_t nmain, uint32_t base_word, uint32_t rb_words, uint32_t delim_col,
+                                    uint32_t range_x = 0, uint32_t range_k = 0) {
     const uint32_t S = static_cast<uint32_t>(d.n_states);
     std::vector<uint32_t> row(nmain);
     for (uint32_t s = 0; s < nmain; ++s) row[s] = s;
@@ -223,7 +224,8 @@ std::vector<uint32_t> number_states(const Program& p, const Dfa& d, uint8_t deli
         for (int b = 0; b < 256; ++b) {
             const double x = (*freq)[static_cast<size_t>(s) * 256 + static_cast<size_t>(b)];
             if (x == 0.0) continue;
-            const uint32_t c = b == delim ? delim_col : p.byte_class[b];
+            const uint32_t c = range_k ? std::min<uint32_t>(static_cast<uint32_t>(b) ^ range_x, range_k)
+                                       : (b == delim ? delim_col : p.byte_class[b]);
             H[s][(c / 2) & 31u] += x;
             tot[s] += x;
         }
@@ -270,12 +272,43 @@ std::vector<uint32_t> number_states(const Program& p, const Dfa& d, uint8_t deli
 }
 
 // Class layout (large DFAs): rows indexed by byte class, u16 row-index entries.
-LtTable make_class_table(const Program& p, const Dfa& d, uint8_t delim, const std::vector<double>* freq) {
+// Range-clamped columns for the class layout: column = min(byte ^ x, k), so
+// no class map is read per byte (one IMNMX instead of an LDS). Every byte
+// that matters (a class other than 0, or the delimiter) must land below k;
+// column k collects the class-0 bytes. Returns k = 0 when no x gives at most
+// `max_cols` columns.
+uint32_t range_cols(const Program& p, uint8_t delim, uint32_t max_cols, uint32_t* x_out) {
+    uint32_t best_k = 0, best_x = 0;
+    for (uint32_t x = 0; x < 256; ++x) {
+        uint32_t hi = 0;
+        for (uint32_t b = 0; b < 256; ++b)
+            if (b == delim || p.byte_class[b] != 0) hi = std::max(hi, b ^ x);
+        const uint32_t k = hi + 1;
+        if (k + 1 <= max_cols && (best_k == 0 || k < best_k)) {
+            best_k = k;
+            best_x = x;
+        }
+    }
+    *x_out = best_x;
+    return best_k;
+}
+
+LtTable make_class_table(const Program& p, const Dfa& d, uint8_t delim, const std::vector<double>* freq,
+                         uint32_t range_x = 0, uint32_t range_k = 0) {
     LtTable t;
     t.cls = true;
+    t.range_x = range_x;
+    t.range_k = range_k;
     const uint32_t S = static_cast<uint32_t>(d.n_states);
-    const uint32_t ncols = static_cast<uint32_t>(p.n_classes) + 1;   // + the delimiter column
-    const uint32_t delim_col = ncols - 1;
+    // class layout: the byte classes + the delimiter column; range layout: k + 1 columns
+    const uint32_t ncols = range_k ? range_k + 1 : static_cast<uint32_t>(p.n_classes) + 1;
+    const uint32_t delim_col = range_k ? (static_cast<uint32_t>(delim) ^ range_x) : ncols - 1;
+    auto class_of_col = [&](uint32_t c) -> int32_t {   // -1: the delimiter column
+        if (!range_k) return c == delim_col ? -1 : static_cast<int32_t>(c);
+        if (c == range_k) return 0;
+        const uint32_t b = c ^ range_x;
+        return b == delim ? -1 : static_cast<int32_t>(p.byte_class[b]);
+    };
     uint32_t rb = align_up(ncols * 2u, 4u);
     if (((rb / 4u) & 1u) == 0) rb += 4;   // odd word stride: consecutive rows rotate banks
     t.row_bytes = rb;
@@ -302,7 +335,8 @@ LtTable make_class_table(const Program& p, const Dfa& d, uint8_t delim, const st
         std::memcpy(&t.lo[static_cast<size_t>(b) * 4], &v, 4);
     }
     auto put = [&](uint32_t row, uint32_t col, uint32_t v) { put16(t.lo, 1024 + row * rb + col * 2u, v); };
-    const std::vector<uint32_t> R = number_states(p, d, delim, freq, S + 2, rows_addr / 4u, rb / 4u, delim_col);
+    const std::vector<uint32_t> R = number_states(p, d, delim, freq, S + 2, rows_addr / 4u, rb / 4u, delim_col,
+                                                  range_x, range_k);
     const uint32_t skip = R[S], vd = R[S + 1], tail0 = acc + 1, term_a = acc + 1 + S + 2, term_r = term_a + 1;
     t.start = R[static_cast<uint32_t>(d.start)];
     t.skip = skip;
@@ -314,18 +348,19 @@ LtTable make_class_table(const Program& p, const Dfa& d, uint8_t delim, const st
         const bool ac = d.accept[s] != 0;
         const uint32_t r = R[s];
         for (uint32_t c = 0; c < ncols; ++c) {
-            if (c == delim_col) {
+            const int32_t cl = class_of_col(c);
+            if (cl < 0) {
                 put(r, c, ac ? acc : t.start);
                 put(tail0 + r, c, ac ? term_a : term_r);
             } else {
-                const uint32_t nx = R[static_cast<uint32_t>(d.next[static_cast<size_t>(s) * static_cast<size_t>(d.n_classes) + c])];
+                const uint32_t nx = R[static_cast<uint32_t>(d.next[static_cast<size_t>(s) * static_cast<size_t>(d.n_classes) + static_cast<uint32_t>(cl)])];
                 put(r, c, nx);
                 put(tail0 + r, c, tail0 + nx);
             }
         }
     }
     for (uint32_t c = 0; c < ncols; ++c) {
-        put(skip, c, c == delim_col ? t.start : skip);
+        put(skip, c, class_of_col(c) < 0 ? t.start : skip);
         put(vd, c, vd);
         put(term_a, c, term_a);
         put(term_r, c, term_r);
@@ -341,7 +376,19 @@ LtTable make_class_table(const Program& p, const Dfa& d, uint8_t delim, const st
 
 LtTable make_lines_tma_table(const Program& p, const Dfa& d, uint8_t delim, const std::vector<double>* freq,
                              bool force_class) {
-    if (force_class || d.n_states > kLtDirectMaxStates) return make_class_table(p, d, delim, freq);
+    if (force_class || d.n_states > kLtDirectMaxStates) {
+        // range-clamped columns when they fit (no class-map lookup per byte)
+        uint32_t x = 0;
+        const uint32_t k = std::getenv("RXG_NO_RANGE_LAYOUT") ? 0 : range_cols(p, delim, 128, &x);
+        if (k && !force_class) {
+            LtTable t = make_class_table(p, d, delim, freq, x, k);
+            // the range kernel's 96 KB stage ring goes into the unused rows first
+            const uint32_t hole = t.hole_hi > t.hole_lo ? (t.hole_hi - t.hole_lo) / 2048u * 2048u : 0u;
+            const uint32_t ring = 96u * 1024u;
+            if (t.ok && t.lo_bytes + (ring > hole ? ring - hole : 0u) + 4096u <= 224u * 1024u) return t;
+        }
+        return make_class_table(p, d, delim, freq);
+    }
     const uint32_t c = lt_choose_col_bytes(freq, static_cast<uint32_t>(d.n_states) + 2);
     LtTable t = make_direct_table(p, d, delim, freq, c);
     if (!t.ok && c != kLtColBytes) t = make_direct_table(p, d, delim, freq, kLtColBytes);
@@ -516,7 +563,8 @@ uint32_t lt_step(const LtTable& t, uint32_t s, uint8_t byte) {
     uint16_t v;
     if (t.cls) {
         uint32_t colabs;
-        std::memcpy(&colabs, &t.lo[static_cast<size_t>(byte) * 4], 4);
+        if (t.range_k) colabs = kLtSmemBase + 1024 + 2u * std::min<uint32_t>(static_cast<uint32_t>(byte) ^ t.range_x, t.range_k);
+        else std::memcpy(&colabs, &t.lo[static_cast<size_t>(byte) * 4], 4);
         std::memcpy(&v, &t.lo[s * t.row_bytes + colabs - t.lo_addr], 2);
         return v;
     }
