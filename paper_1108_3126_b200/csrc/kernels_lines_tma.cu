@@ -59,6 +59,8 @@ struct Args {
     uint32_t delim;
     uint32_t row_bytes, cmap_addr, acc_shift;   // class layouts
     uint32_t rows_addr, range_x, range_k;       // range-clamped columns
+    uint32_t range_x4;                          // range_x in every byte (XOR a whole word)
+    uint32_t acc_mul;                           // class layouts: 2^(32 - acc_shift) (count = hi32(s * acc_mul))
     uint32_t col_bytes;                         // direct layout: column stride
     unsigned long long* count;
     unsigned long long* slot;                   // CountSlot (launch.hpp)
@@ -124,10 +126,16 @@ __device__ __forceinline__ uint32_t step(const Args& a, uint32_t s, uint32_t wor
     return step_b<L>(a, s, __byte_perm(word, 0, 0x4440 + k));
 }
 
+// Range layout step on byte k of a word already XORed with range_x in every
+// byte: PRMT, IMNMX, IMAD, LDS.
+__device__ __forceinline__ uint32_t step_rx(const Args& a, uint32_t s, uint32_t wx, int k) {
+    return tab(s * a.row_bytes + a.rows_addr + 2u * min(__byte_perm(wx, 0, 0x4440 + k), a.range_k));
+}
+
 // 1 iff s is START_A (the accepted-line-end row).
 template <int L>
 __device__ __forceinline__ uint32_t counted(const Args& a, uint32_t s) {
-    if constexpr (L != 0) return s >> a.acc_shift;
+    if constexpr (L != 0) return __umulhi(s, a.acc_mul);   // s >> acc_shift as one IMAD.HI with the add
     else return __umulhi(s, 1u << 17);
 }
 
@@ -369,7 +377,10 @@ __global__ void __launch_bounds__(C::warps * 32, 1) k_lines_tma(const __grid_con
                     v[j] = lds128(stage[st] + r * C::slice + (granule<C::slice>(r, g) << 4));
                 }
 #pragma unroll
-                for (int w = 0; w < 4; ++w)
+                for (int w = 0; w < 4; ++w) {
+                    uint32_t wx[C::chains];   // range layout: the word XORed once, not each byte
+#pragma unroll
+                    for (int j = 0; j < C::chains; ++j) wx[j] = L == 2 ? word_of(v[j], w) ^ a.range_x4 : 0u;
 #pragma unroll
                     for (int k = 0; k < 4; ++k)
 #pragma unroll
@@ -377,10 +388,11 @@ __global__ void __launch_bounds__(C::warps * 32, 1) k_lines_tma(const __grid_con
                             if constexpr (RES) {
                                 s[j] = step_res<L>(a, s[j], __byte_perm(word_of(v[j], w), 0, 0x4440 + k), cnt, lc[j]);
                             } else {
-                                s[j] = step<L, true>(a, s[j], word_of(v[j], w), k);
+                                s[j] = L == 2 ? step_rx(a, s[j], wx[j], k) : step<L, true>(a, s[j], word_of(v[j], w), k);
                                 cnt += counted<L>(a, s[j]);
                             }
                         }
+                }
 #pragma unroll
                 for (int j = 0; j < C::chains; ++j) last[j] = v[j].w >> 24;
             }
@@ -584,6 +596,8 @@ cudaError_t launch(const LtTable& t, const uint8_t* text, uint64_t len, uint8_t 
     a.rows_addr = kLtSmemBase + 1024;
     a.range_x = t.range_x;
     a.range_k = t.range_k;
+    a.range_x4 = t.range_x * 0x01010101u;
+    a.acc_mul = t.cls ? 1u << (32 - t.acc_shift) : 0u;
     a.count = count;
     a.slot = cs.p;
     a.accumulate = cs.accumulate ? 1 : 0;
