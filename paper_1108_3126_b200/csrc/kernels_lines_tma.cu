@@ -343,7 +343,8 @@ __global__ void __launch_bounds__(C::warps * 32, 1) k_lines_tma(const __grid_con
     uint32_t phase = 0;   // bit st = parity of stage st's next completion
     const uint32_t ncol = a.chunk / C::slice;
     const uint32_t* stage = a.stage_addr + warp * C::stages;
-    for (uint64_t tile = static_cast<uint64_t>(blockIdx.x) * C::warps + warp; tile < a.tiles;
+    // tiles interleave the CTAs (tile = warp * grid + cta): small inputs spread over every SM
+    for (uint64_t tile = static_cast<uint64_t>(warp) * gridDim.x + blockIdx.x; tile < a.tiles;
          tile += static_cast<uint64_t>(gridDim.x) * C::warps) {
         const uint64_t row0 = tile * C::rows;
         if (lane == 0) {
@@ -627,7 +628,7 @@ cudaError_t launch(const LtTable& t, const uint8_t* text, uint64_t len, uint8_t 
     int dev = 0;
     cudaGetDevice(&dev);
     const uint64_t cap = static_cast<uint64_t>(per_sm) * device_sm_count(dev);
-    const uint64_t want = (a.tiles + C::warps - 1) / C::warps;
+    const uint64_t want = a.tiles;   // at most one tile per CTA needed to reach every SM
     const int grid = static_cast<int>(want == 0 ? 1 : (want < cap ? want : cap));
     k_lines_tma<C, L, RES><<<grid, C::warps * 32, smem, st>>>(a, map);
     return cudaGetLastError();
