@@ -223,21 +223,34 @@ __device__ void finish_lines(const Args& a, uint32_t (&s)[K], uint64_t (&pos)[K]
 #pragma unroll
     for (int j = 0; j < K; ++j) more |= live[j];
     while (more) {
-        uint4 v[K];
+        // 16 * U bytes per chain per round trip (lines end within a few dozen
+        // bytes; measured better than 32 bytes on (c) despite a 16-byte spill)
+        constexpr int U = 4;
+        uint4 v[K][U];
 #pragma unroll
         for (int j = 0; j < K; ++j)
-            v[j] = live[j] && s[j] < a.term_acc && pos[j] + 16 <= a.len
-                       ? __ldg(reinterpret_cast<const uint4*>(a.text + pos[j]))
-                       : make_uint4(0, 0, 0, 0);
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                v[j][u] = live[j] && s[j] < a.term_acc && pos[j] + 16 * (u + 1) <= a.len
+                              ? __ldg(reinterpret_cast<const uint4*>(a.text + pos[j]) + u)
+                              : make_uint4(0, 0, 0, 0);
         more = false;
 #pragma unroll
         for (int j = 0; j < K; ++j) {
             if (!live[j] || s[j] >= a.term_acc) continue;
-            if (pos[j] + 16 <= a.len) {
+            if (pos[j] + 16 * U <= a.len) {
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+#pragma unroll
+                    for (int w = 0; w < 4; ++w)
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) s[j] = step<L>(a, s[j], word_of(v[j][u], w), k);
+                pos[j] += 16 * U;
+            } else if (pos[j] + 16 <= a.len) {
 #pragma unroll
                 for (int w = 0; w < 4; ++w)
 #pragma unroll
-                    for (int k = 0; k < 4; ++k) s[j] = step<L>(a, s[j], word_of(v[j], w), k);
+                    for (int k = 0; k < 4; ++k) s[j] = step<L>(a, s[j], word_of(v[j][0], w), k);
                 pos[j] += 16;
             } else {   // the last bytes of the buffer, then the virtual delimiter
                 for (; pos[j] < a.len; ++pos[j]) s[j] = step_b<L>(a, s[j], a.text[pos[j]]);
