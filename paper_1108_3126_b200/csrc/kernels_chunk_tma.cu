@@ -71,6 +71,7 @@ struct Args {
     uint32_t bar_addr;
     uint32_t stage_addr[kWarps * kStages];
     uint32_t start, row_bytes, cmap_addr, acc_off;
+    uint32_t range_x, range_k;   // range-clamped class columns (L == 2)
     uint32_t* g;
     uint32_t* e;
     uint32_t* mid;      // nranges x ceil(chunk / kMidT)
@@ -82,16 +83,17 @@ struct Args {
     uint32_t* exit_state;  // nullable: table state after the string
 };
 
-template <bool CLS>
+template <int L>
 __device__ __forceinline__ uint32_t stepb(const Args& a, uint32_t s, uint32_t b) {
-    return tma::step<CLS>(s, b, a.row_bytes, a.cmap_addr);
+    if constexpr (L == 2) return tma::lds16(s * a.row_bytes + kLtSmemBase + 1024 + 2u * min(b ^ a.range_x, a.range_k));
+    else return tma::step<L != 0>(s, b, a.row_bytes, a.cmap_addr);
 }
 
 // Walk [lo, hi) with direct loads.
-template <bool CLS>
+template <int L>
 __device__ uint32_t walk(const Args& a, uint32_t s, uint64_t lo, uint64_t hi) {
     uint64_t p = lo;
-    for (; p < hi && (p & 15); ++p) s = stepb<CLS>(a, s, a.text[p]);
+    for (; p < hi && (p & 15); ++p) s = stepb<L>(a, s, a.text[p]);
     for (; p + 64 <= hi; p += 64) {   // four independent loads in flight, then 64 steps
         uint4 v[4];
 #pragma unroll
@@ -101,37 +103,37 @@ __device__ uint32_t walk(const Args& a, uint32_t s, uint64_t lo, uint64_t hi) {
 #pragma unroll
             for (int w = 0; w < 4; ++w)
 #pragma unroll
-                for (int k = 0; k < 4; ++k) s = stepb<CLS>(a, s, __byte_perm(tma::word_of(v[u], w), 0, 0x4440 + k));
+                for (int k = 0; k < 4; ++k) s = stepb<L>(a, s, __byte_perm(tma::word_of(v[u], w), 0, 0x4440 + k));
     }
     for (; p + 16 <= hi; p += 16) {
         const uint4 v = __ldg(reinterpret_cast<const uint4*>(a.text + p));
 #pragma unroll
         for (int w = 0; w < 4; ++w)
 #pragma unroll
-            for (int k = 0; k < 4; ++k) s = stepb<CLS>(a, s, __byte_perm(tma::word_of(v, w), 0, 0x4440 + k));
+            for (int k = 0; k < 4; ++k) s = stepb<L>(a, s, __byte_perm(tma::word_of(v, w), 0, 0x4440 + k));
     }
-    for (; p < hi; ++p) s = stepb<CLS>(a, s, a.text[p]);
+    for (; p < hi; ++p) s = stepb<L>(a, s, a.text[p]);
     return s;
 }
 
-template <bool CLS>
+template <int L>
 __device__ uint32_t entry_guess(const Args& a, uint64_t r) {
     const uint64_t c0 = r * a.chunk;
-    return r == 0 ? a.entry : walk<CLS>(a, a.start, c0 > a.lookback ? c0 - a.lookback : 0, c0);
+    return r == 0 ? a.entry : walk<L>(a, a.start, c0 > a.lookback ? c0 - a.lookback : 0, c0);
 }
 
 // Entry guesses of a lane's ranges (rows row0 + 32 j + lane): with the
 // default 64-byte lookback every chain's four 16-byte loads are issued
 // together and the chains walk interleaved, instead of one dependent walk
 // after the other.
-template <bool CLS, int CH>
+template <int L, int CH>
 __device__ void entry_guesses(const Args& a, uint64_t row0, uint32_t lane, uint32_t (&s)[CH], const bool (&valid)[CH]) {
     bool fast = a.lookback == 64;
 #pragma unroll
     for (int j = 0; j < CH; ++j) fast &= !valid[j] || (row0 + j * 32 + lane) * a.chunk >= 64;
     if (!fast) {
 #pragma unroll
-        for (int j = 0; j < CH; ++j) s[j] = valid[j] ? entry_guess<CLS>(a, row0 + j * 32 + lane) : a.start;
+        for (int j = 0; j < CH; ++j) s[j] = valid[j] ? entry_guess<L>(a, row0 + j * 32 + lane) : a.start;
         return;
     }
     uint4 v[CH][4];
@@ -150,7 +152,7 @@ __device__ void entry_guesses(const Args& a, uint64_t row0, uint32_t lane, uint3
             for (int k = 0; k < 4; ++k)
 #pragma unroll
                 for (int j = 0; j < CH; ++j)
-                    s[j] = stepb<CLS>(a, s[j], __byte_perm(tma::word_of(v[j][u], w), 0, 0x4440 + k));
+                    s[j] = stepb<L>(a, s[j], __byte_perm(tma::word_of(v[j][u], w), 0, 0x4440 + k));
 #pragma unroll
     for (int j = 0; j < CH; ++j)
         if (!valid[j]) s[j] = a.start;
@@ -158,7 +160,7 @@ __device__ void entry_guesses(const Args& a, uint64_t row0, uint32_t lane, uint3
 
 // In-order repair from the first wrong guess (one warp, the table already in
 // shared memory), then the answer. Run by warp 0 of the last CTA.
-template <bool CLS>
+template <int L>
 __device__ void repair_and_answer(const Args& a) {
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t per = (a.chunk + kMidT - 1) / kMidT;
@@ -185,7 +187,7 @@ __device__ void repair_and_answer(const Args& a) {
                 uint32_t* mid = a.mid + r * per;
                 uint32_t k = 0;
                 for (uint64_t p = c0; p < c1; p += kMidT, ++k) {
-                    s = walk<CLS>(a, s, p, min(p + kMidT, c1));
+                    s = walk<L>(a, s, p, min(p + kMidT, c1));
                     if (s == mid[k]) {   // trajectories coincide from here on
                         s = a.e[r];
                         break;
@@ -202,7 +204,7 @@ __device__ void repair_and_answer(const Args& a) {
         }
     }
     if (lane == 0) {
-        const uint32_t acc_addr = CLS ? kLtSmemBase + 1024 + exact * a.row_bytes + a.acc_off : exact + a.acc_off;
+        const uint32_t acc_addr = L != 0 ? kLtSmemBase + 1024 + exact * a.row_bytes + a.acc_off : exact + a.acc_off;
         *a.accept = static_cast<int32_t>(tma::lds16(acc_addr));
         if (a.repairs) *a.repairs = repairs;
         if (a.exit_state) *a.exit_state = exact;
@@ -212,7 +214,7 @@ __device__ void repair_and_answer(const Args& a) {
     }
 }
 
-template <bool CLS>
+template <int L>
 __global__ void __launch_bounds__(kWarps * 32, 1) k_chunk_tma(const __grid_constant__ Args a,
                                                            const __grid_constant__ CUtensorMap map) {
     extern __shared__ __align__(1024) uint8_t sm[];
@@ -235,11 +237,11 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_chunk_tma(const __grid_const
     // the remainder range (past the last full row) walks with direct loads
     if (blockIdx.x == 0 && threadIdx.x == 0 && a.nranges > a.rows) {
         const uint64_t r = a.rows, c0 = r * a.chunk;
-        uint32_t s = entry_guess<CLS>(a, r);
+        uint32_t s = entry_guess<L>(a, r);
         a.g[r] = s;
         uint32_t k = 0;
         for (uint64_t p = c0; p < a.len; p += kMidT, ++k) {
-            s = walk<CLS>(a, s, p, min(p + kMidT, a.len));
+            s = walk<L>(a, s, p, min(p + kMidT, a.len));
             a.mid[r * per + k] = s;
         }
         a.e[r] = s;
@@ -263,7 +265,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_chunk_tma(const __grid_const
         for (int j = 0; j < kChains; ++j) {
             valid[j] = row0 + j * 32 + lane < a.rows;
         }
-        entry_guesses<CLS, kChains>(a, row0, lane, s, valid);
+        entry_guesses<L, kChains>(a, row0, lane, s, valid);
 #pragma unroll
         for (int j = 0; j < kChains; ++j) {
             guess[j] = s[j];
@@ -287,7 +289,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_chunk_tma(const __grid_const
                     for (int k = 0; k < 4; ++k)
 #pragma unroll
                         for (int j = 0; j < kChains; ++j)
-                            s[j] = stepb<CLS>(a, s[j], __byte_perm(tma::word_of(v[j], w), 0, 0x4440 + k));
+                            s[j] = stepb<L>(a, s[j], __byte_perm(tma::word_of(v[j], w), 0, 0x4440 + k));
             }
             __syncwarp();
             if (lane == 0 && col + kStages < ncol) {
@@ -343,13 +345,13 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_chunk_tma(const __grid_const
     __syncthreads();
     if (threadIdx.x < 32) {   // the repair pass and the answer, in this CTA (no second launch)
         __threadfence();
-        repair_and_answer<CLS>(a);
+        repair_and_answer<L>(a);
     }
 }
 
 uint32_t align_up(uint32_t x, uint32_t a) { return (x + a - 1) / a * a; }
 
-template <bool CLS>
+template <int L>
 cudaError_t run(const LtTable& t, Args& a, int device, cudaStream_t st) {
     // stage ring after the table image, mbarriers after the ring
     uint32_t p = align_up(t.smem_table_end, 1024);
@@ -360,13 +362,13 @@ cudaError_t run(const LtTable& t, Args& a, int device, cudaStream_t st) {
     std::memset(&map, 0, sizeof(map));
     if (a.rows > 0 && tma::make_map(&map, a.text, a.rows, a.chunk, kSlice, kRows) != CUDA_SUCCESS)
         return cudaErrorInvalidValue;
-    cudaError_t e = cudaFuncSetAttribute(k_chunk_tma<CLS>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaError_t e = cudaFuncSetAttribute(k_chunk_tma<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     const uint64_t want = a.tiles;   // at most one tile per CTA needed to reach every SM
     const int grid = static_cast<int>(want == 0 ? 1 : (want < static_cast<uint64_t>(sms) ? want : sms));
-    k_chunk_tma<CLS><<<grid, kWarps * 32, smem, st>>>(a, map);
+    k_chunk_tma<L><<<grid, kWarps * 32, smem, st>>>(a, map);
     return cudaGetLastError();
 }
 
@@ -416,7 +418,9 @@ cudaError_t launch_chunked_tma(const LtTable& t, const void* d_img, const uint8_
     a.accept = accept;
     a.repairs = repairs;
     // (len == 0: one CTA, no ranges; the repair pass answers from the start state)
-    return t.cls ? run<true>(t, a, device, st) : run<false>(t, a, device, st);
+    a.range_x = t.range_x;
+    a.range_k = t.range_k;
+    return t.cls ? (t.range_k ? run<2>(t, a, device, st) : run<1>(t, a, device, st)) : run<0>(t, a, device, st);
 }
 
 }  // namespace rxg

@@ -277,12 +277,12 @@ std::vector<uint32_t> number_states(const Program& p, const Dfa& d, uint8_t deli
 // that matters (a class other than 0, or the delimiter) must land below k;
 // column k collects the class-0 bytes. Returns k = 0 when no x gives at most
 // `max_cols` columns.
-uint32_t range_cols(const Program& p, uint8_t delim, uint32_t max_cols, uint32_t* x_out) {
+uint32_t range_cols(const Program& p, uint8_t delim, uint32_t max_cols, uint32_t* x_out, bool with_delim = true) {
     uint32_t best_k = 0, best_x = 0;
     for (uint32_t x = 0; x < 256; ++x) {
         uint32_t hi = 0;
         for (uint32_t b = 0; b < 256; ++b)
-            if (b == delim || p.byte_class[b] != 0) hi = std::max(hi, b ^ x);
+            if ((with_delim && b == delim) || p.byte_class[b] != 0) hi = std::max(hi, b ^ x);
         const uint32_t k = hi + 1;
         if (k + 1 <= max_cols && (best_k == 0 || k < best_k)) {
             best_k = k;
@@ -524,7 +524,16 @@ LtTable make_chunk_tma_table(const Program& p, const Dfa& d, const std::vector<d
         t.acc_off = R;
     } else {
         t.cls = true;
-        const uint32_t ncols = static_cast<uint32_t>(p.n_classes) + 1;   // + the accept column
+        // range-clamped columns (no class map lookup) when the bytes that matter fit
+        uint32_t rx = 0;
+        const uint32_t rk = std::getenv("RXG_NO_RANGE_LAYOUT") ? 0 : range_cols(p, 0xFF, 128, &rx, false);
+        t.range_x = rx;
+        t.range_k = rk;
+        auto class_of_col = [&](uint32_t c) -> uint32_t {
+            if (!rk) return c;
+            return c >= rk ? 0u : p.byte_class[c ^ rx];
+        };
+        const uint32_t ncols = (rk ? rk + 1 : static_cast<uint32_t>(p.n_classes)) + 1;   // + the accept column
         uint32_t rb = align_up(ncols * 2u, 4u);
         if (((rb / 4u) & 1u) == 0) rb += 4;
         t.row_bytes = rb;
@@ -541,12 +550,12 @@ LtTable make_chunk_tma_table(const Program& p, const Dfa& d, const std::vector<d
         if (freq) {
             std::vector<double> f2(static_cast<size_t>(S) * 256);
             std::copy(freq->begin(), freq->begin() + static_cast<std::ptrdiff_t>(f2.size()), f2.begin());
-            R = number_states(p, d, 0xFF, &f2, S, rows_addr / 4u, rb / 4u, ncols);   // no delimiter column used
+            R = number_states(p, d, 0xFF, &f2, S, rows_addr / 4u, rb / 4u, ncols, rx, rk);   // no delimiter column
         } else {
             for (uint32_t s = 0; s < S; ++s) R[s] = s;
         }
         for (uint32_t s = 0; s < S; ++s) {
-            for (uint32_t c = 0; c + 1 < ncols; ++c) put16(t.lo, 1024 + R[s] * rb + c * 2u, R[next(s, c)]);
+            for (uint32_t c = 0; c + 1 < ncols; ++c) put16(t.lo, 1024 + R[s] * rb + c * 2u, R[next(s, class_of_col(c))]);
             put16(t.lo, 1024 + R[s] * rb + (ncols - 1) * 2u, d.accept[s]);
         }
         t.start = R[static_cast<uint32_t>(d.start)];

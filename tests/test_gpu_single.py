@@ -209,3 +209,28 @@ def test_match_one_multi_segments(ndev):
     assert acc is True
     if ndev > 2:
         assert reruns > 0
+
+
+@pytest.mark.parametrize("layout", ["range", "class"])
+def test_chunked_class_tables(layout):
+    """Single strings whose minimal DFA exceeds the direct layout: the chunk
+    kernel's class rows, with range-clamped columns or the class map, against
+    the sequential walk and the oracle."""
+    import os
+
+    if layout == "class":
+        os.environ["RXG_NO_RANGE_LAYOUT"] = "1"
+    try:
+        rng = np.random.default_rng(5)
+        for p, alpha in [("(a|b)*a" + "(a|b)" * 6, b"ab"), (rx.synth_pattern("d"), b"abcdefghijklmnopqrstuvwxyz ")]:
+            m = rx.Matcher(p)
+            assert m.info()["dfa_states"] > 56
+            a = np.frombuffer(alpha, np.uint8)
+            for n in (1000, 300_001):
+                w = a[rng.integers(0, len(a), n)].tobytes()
+                want = m.lockstep_accepts(w, "dfa_seq")
+                assert m.lockstep_accepts(w, "chunked") == want, (p[:20], n)
+                if n == 1000:
+                    assert want == O(p).accepts(w)
+    finally:
+        os.environ.pop("RXG_NO_RANGE_LAYOUT", None)
