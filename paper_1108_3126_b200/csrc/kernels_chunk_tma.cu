@@ -16,8 +16,12 @@
 #include <cstdlib>
 #include <cstring>
 
+#include <cooperative_groups.h>
+
 #include "chunked.hpp"
 #include "tma_common.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace rxg {
 
@@ -57,6 +61,7 @@ namespace {
 constexpr int kWarps = 24, kChains = 2, kRows = 32 * kChains, kStages = 3;
 constexpr uint32_t kSlice = 32, kStageBytes = kRows * kSlice;
 constexpr uint32_t kMidT = 256;   // trajectory checkpoint period (bytes)
+constexpr int kRepairRounds = 64; // parallel repair rounds before the in-order pass
 
 struct Args {
     const uint8_t* text;
@@ -75,8 +80,9 @@ struct Args {
     uint32_t* g;
     uint32_t* e;
     uint32_t* mid;      // nranges x ceil(chunk / kMidT)
-    unsigned int* ticket;
+    unsigned int* ticket;          // CTAs finished (non-cooperative launch; zero when idle)
     unsigned long long* bad_inv;   // ~(first range whose entry guess is wrong); 0 = none (zero-initialised)
+    unsigned long long* round_inv; // the same per repair round, two slots alternating (zero when idle)
     int32_t* accept;
     unsigned long long* repairs;
     uint32_t entry;        // table state the string starts in (the start state unless chained)
@@ -210,11 +216,10 @@ __device__ void repair_and_answer(const Args& a) {
         if (a.exit_state) *a.exit_state = exact;
         // idle slot for the next launch on this stream (CountSlot, launch.hpp)
         atomicExch(a.bad_inv, 0ull);
-        atomicExch(a.ticket, 0u);
     }
 }
 
-template <int L>
+template <int L, bool COOP>
 __global__ void __launch_bounds__(kWarps * 32, 1) k_chunk_tma(const __grid_constant__ Args a,
                                                            const __grid_constant__ CUtensorMap map) {
     extern __shared__ __align__(1024) uint8_t sm[];
@@ -319,33 +324,107 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_chunk_tma(const __grid_const
         bad = __reduce_min_sync(0xFFFFFFFFu, bad);
         if (lane == 0 && bad != ~0u) atomicMax(a.bad_inv, ~(row0 + bad));
     }
-    // last CTA: parallel boundary check (flag word after the mbarriers: no
-    // static shared memory, which would move the dynamic window off 0x400)
-    uint32_t* last = reinterpret_cast<uint32_t*>(sm + (a.bar_addr + kWarps * kStages * 8 - kLtSmemBase));
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();
-        *last = atomicAdd(a.ticket, 1u) == gridDim.x - 1;
-    }
-    __syncthreads();
-    if (!*last) return;
-    __threadfence();
-    // only the boundaries between tiles (and before the remainder range) are
-    // left: the first row of every tile > 0, and range `rows`
-    unsigned long long bad = ~0ull;
-    for (uint64_t t = 1 + threadIdx.x; t <= a.tiles; t += blockDim.x) {
-        const uint64_t j = t < a.tiles ? t * kRows : a.rows;
-        if (j >= a.nranges || (t == a.tiles && a.nranges == a.rows)) continue;
-        if (a.g[j] != a.e[j - 1]) {
-            bad = j;
-            break;
+    if constexpr (!COOP) {
+        // small inputs: the last CTA to finish checks the seams between tiles
+        // and one of its warps repairs in order (no grid-wide sync)
+        uint32_t* last = reinterpret_cast<uint32_t*>(sm + (a.bar_addr + kWarps * kStages * 8 - kLtSmemBase));
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            *last = atomicAdd(a.ticket, 1u) == gridDim.x - 1;
         }
-    }
-    if (bad != ~0ull) atomicMax(a.bad_inv, ~bad);
-    __syncthreads();
-    if (threadIdx.x < 32) {   // the repair pass and the answer, in this CTA (no second launch)
+        __syncthreads();
+        if (!*last) return;
         __threadfence();
+        unsigned long long bad = ~0ull;
+        for (uint64_t t = 1 + threadIdx.x; t <= a.tiles; t += blockDim.x) {
+            const uint64_t j = t < a.tiles ? t * kRows : a.rows;
+            if (j >= a.nranges || (t == a.tiles && a.nranges == a.rows)) continue;
+            if (a.g[j] != a.e[j - 1]) {
+                bad = j;
+                break;
+            }
+        }
+        if (bad != ~0ull) atomicMax(a.bad_inv, ~bad);
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            __threadfence();
+            repair_and_answer<L>(a);
+            if (threadIdx.x == 0) *a.ticket = 0;
+        }
+        return;
+    }
+    // Large inputs, whole grid (cooperative launch): the seams between tiles,
+    // then parallel repair rounds, then, if a chain of wrong guesses is still
+    // unresolved, the in-order repair by one warp.
+    cg::grid_group grid = cg::this_grid();
+    grid.sync();
+    const uint64_t nthreads = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    const uint64_t gtid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    {   // the first row of every tile > 0, and range `rows`
+        unsigned long long bad = ~0ull;
+        for (uint64_t t = 1 + gtid; t <= a.tiles; t += nthreads) {
+            const uint64_t j = t < a.tiles ? t * kRows : a.rows;
+            if (j >= a.nranges || (t == a.tiles && a.nranges == a.rows)) continue;
+            if (a.g[j] != a.e[j - 1]) {
+                bad = j;
+                break;
+            }
+        }
+        if (bad != ~0ull) atomicMax(a.bad_inv, ~bad);
+    }
+    grid.sync();
+    unsigned long long fb = ~*reinterpret_cast<volatile unsigned long long*>(a.bad_inv);
+    // Round: every range j >= fb whose guess differs from its predecessor's
+    // exit re-walks from that exit (stopping where it meets its recorded
+    // trajectory). Ranges below the first mismatch are exact and final, so
+    // each round moves the frontier at least one range; chains of sticky
+    // states (a keyword seen once keeps the automaton accepting) resolve in
+    // as many rounds as the longest run of ranges without the keyword.
+    for (int round = 0; round < kRepairRounds && fb != ~0ull; ++round) {
+        const uint32_t per = (a.chunk + kMidT - 1) / kMidT;
+        for (uint64_t j = fb + gtid; j < a.nranges; j += nthreads) {
+            if (j == 0) continue;
+            const uint32_t entry = *reinterpret_cast<volatile uint32_t*>(a.e + j - 1);
+            if (a.g[j] == entry) continue;
+            const uint64_t c0 = j * a.chunk, c1 = min(c0 + a.chunk, a.len);
+            uint32_t st = entry;
+            uint32_t* mid = a.mid + j * per;
+            uint32_t k = 0;
+            for (uint64_t p = c0; p < c1; p += kMidT, ++k) {
+                st = walk<L>(a, st, p, min(p + kMidT, c1));
+                if (st == mid[k]) {   // trajectories coincide from here on
+                    st = a.e[j];
+                    break;
+                }
+                mid[k] = st;
+            }
+            a.g[j] = entry;
+            *reinterpret_cast<volatile uint32_t*>(a.e + j) = st;
+        }
+        unsigned long long* slot = a.round_inv + (round & 1);
+        if (gtid == 0) *slot = 0;
+        grid.sync();
+        {
+            unsigned long long bad = ~0ull;
+            for (uint64_t j = fb + gtid; j < a.nranges; j += nthreads)
+                if (j > 0 && a.g[j] != a.e[j - 1]) {
+                    bad = j;
+                    break;
+                }
+            if (bad != ~0ull) atomicMax(slot, ~bad);
+        }
+        grid.sync();
+        fb = ~*reinterpret_cast<volatile unsigned long long*>(slot);
+    }
+    if (blockIdx.x == 0 && threadIdx.x < 32) {   // what is left in order, and the answer
+        if (threadIdx.x == 0) *a.bad_inv = ~fb;
+        __syncwarp();
         repair_and_answer<L>(a);
+        if (threadIdx.x == 0) {
+            a.round_inv[0] = 0;
+            a.round_inv[1] = 0;
+        }
     }
 }
 
@@ -362,14 +441,24 @@ cudaError_t run(const LtTable& t, Args& a, int device, cudaStream_t st) {
     std::memset(&map, 0, sizeof(map));
     if (a.rows > 0 && tma::make_map(&map, a.text, a.rows, a.chunk, kSlice, kRows) != CUDA_SUCCESS)
         return cudaErrorInvalidValue;
-    cudaError_t e = cudaFuncSetAttribute(k_chunk_tma<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    // grid-wide repair rounds pay off above a few MB; below, the launch and two
+    // grid syncs cost more than the in-order repair can
+    const bool coop = a.len >= (4ull << 20);
+    auto* kern = coop ? k_chunk_tma<L, true> : k_chunk_tma<L, false>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     const uint64_t want = a.tiles;   // at most one tile per CTA needed to reach every SM
     const int grid = static_cast<int>(want == 0 ? 1 : (want < static_cast<uint64_t>(sms) ? want : sms));
-    k_chunk_tma<L><<<grid, kWarps * 32, smem, st>>>(a, map);
-    return cudaGetLastError();
+    if (!coop) {
+        kern<<<grid, kWarps * 32, smem, st>>>(a, map);
+        return cudaGetLastError();
+    }
+    // cooperative: every CTA is resident (one per SM), the repair rounds sync the grid
+    void* args[] = {&a, &map};
+    return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(kern), dim3(grid), dim3(kWarps * 32), args, smem,
+                                       st);
 }
 
 }  // namespace
@@ -409,8 +498,10 @@ cudaError_t launch_chunked_tma(const LtTable& t, const void* d_img, const uint8_
     a.row_bytes = t.row_bytes;
     a.cmap_addr = t.cmap_addr;
     a.acc_off = t.acc_off;
-    a.ticket = reinterpret_cast<unsigned int*>(cs.p + 1);   // zero when idle: no memset per call
-    a.bad_inv = cs.p + 2;
+    a.bad_inv = cs.p + 1;
+    a.round_inv = cs.p + 2;
+    a.ticket = reinterpret_cast<unsigned int*>(cs.p + 3) + 1;   // the high half of the second round slot
+                                                               // (rounds run only cooperatively)
     uint32_t* sc = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(scratch) + 16);
     a.g = sc;
     a.e = sc + a.nranges;

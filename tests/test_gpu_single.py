@@ -234,3 +234,30 @@ def test_chunked_class_tables(layout):
                     assert want == O(p).accepts(w)
     finally:
         os.environ.pop("RXG_NO_RANGE_LAYOUT", None)
+
+
+def test_chunked_sticky_states_parallel_rounds():
+    """A keyword seen once keeps (d)'s automaton accepting: on one long string
+    of words nearly every range's guessed entry is wrong. Large inputs repair
+    in parallel rounds (cooperative launch), small ones in order; both exact,
+    including strings where the keyword appears only near the start or end."""
+    rng = np.random.default_rng(13)
+    p = rx.synth_pattern("d")
+    m = rx.Matcher(p)
+    words = rx.synth_input("d", 24 << 20).copy()
+    words[words == 10] = 32
+    for n in (1 << 20, 24 << 20):
+        w = words[:n]
+        want = m.lockstep_accepts(w.tobytes(), "dfa_seq")
+        assert m.lockstep_accepts(w.tobytes(), "chunked") == want, n
+    # a string whose only keyword match region is near the end, and one with a
+    # byte outside [a-z ] at the end (the sink leaves): the answers flip
+    w = words.copy()
+    w[-1] = ord("#")
+    assert m.lockstep_accepts(w.tobytes(), "chunked") == m.lockstep_accepts(w.tobytes(), "dfa_seq")
+    acc_rounds = rx.Matcher("(a|b)*a(a|b)*")   # sticky after the first 'a'
+    w = np.full(24 << 20, ord("b"), np.uint8)
+    w[int(rng.integers(0, 100))] = ord("a")
+    assert acc_rounds.lockstep_accepts(w.tobytes(), "chunked") is True
+    w[:] = ord("b")
+    assert acc_rounds.lockstep_accepts(w.tobytes(), "chunked") is False
