@@ -425,7 +425,7 @@ def main():
             "config": {
                 "workload": f"config ({cfg}): {desc}",
                 "pattern_nodes": info["nodes"], "positions": info["positions"], "words": info["words"],
-                "dfa_states": info["dfa_states"], "line_col_bytes": m.info()["line_col_bytes"], "input_bytes_per_gpu": nbytes, "strings_per_gpu": units,
+                "dfa_states": info["dfa_states"], "line_col_bytes": m.info()["line_col_bytes"], "chunk_lookback": m.info()["chunk_lookback"], "input_bytes_per_gpu": nbytes, "strings_per_gpu": units,
                 "matches_rank0": result,
                 "l2": "inputs larger than L2 (126 MB)" if l2_flush is None else "L2 flushed between timed steps (512 MiB write, then 256 MiB read)",
                 "parallelism": f"dp{world} (string shards, count all-reduce)" if world > 1 else "dp1",

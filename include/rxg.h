@@ -92,6 +92,7 @@ typedef struct rxg_heap_info {
     int32_t dfa_sets;      /* distinct memoized E sets before minimisation (0 if over the cap) */
     int32_t line_tma_layout;   /* TMA table built for '\n' lines so far: 0 none, 1 direct, 2 class */
     int32_t line_col_bytes;    /* its column stride (direct layout; chosen by rxg_heap_tune) */
+    int32_t chunk_lookback;    /* single-string engine: bytes walked to guess a range's entry (tuned) */
 } rxg_heap_info;
 
 const char* rxg_strerror(int status);

@@ -39,7 +39,7 @@ class rxg_heap_info(C.Structure):
                 ("classes", C.c_int32), ("dfa_states", C.c_int32), ("byte_symbols", C.c_int32),
                 ("device", C.c_int32), ("nullable", C.c_int32),
                 ("line_table_bytes", C.c_uint32), ("plain_table_bytes", C.c_uint32), ("dfa_sets", C.c_int32),
-                ("line_tma_layout", C.c_int32), ("line_col_bytes", C.c_int32)]
+                ("line_tma_layout", C.c_int32), ("line_col_bytes", C.c_int32), ("chunk_lookback", C.c_int32)]
 
 
 class rxg_one_opts(C.Structure):

@@ -78,6 +78,7 @@ struct rxg_heap {
     Program prog;
     bool dfa_ok = false;
     int32_t dfa_sets = 0;   // states before minimisation
+    uint32_t lookback = 64; // chunk engine lookback (rxg_heap_tune with delimiter -1 shortens it)
     Dfa dfa;
     int smem_limit = 0;
     std::mutex mu;
@@ -660,6 +661,7 @@ int rxg_heap_info_get(const rxg_heap* h, rxg_heap_info* info) {
     info->classes = h->prog.n_classes;
     info->dfa_states = h->dfa_ok ? h->dfa.n_states : 0;
     info->dfa_sets = h->dfa_ok ? h->dfa_sets : 0;
+    info->chunk_lookback = static_cast<int32_t>(h->lookback);
     info->byte_symbols = h->prog.byte_symbols;
     info->device = h->device;
     info->nullable = h->prog.test(h->prog.init, h->prog.n_pos);
@@ -762,8 +764,9 @@ int rxg_heap_tune(rxg_heap* h, const uint8_t* sample, uint64_t len, int32_t deli
     if (!h || (!sample && len) || delimiter < -1 || delimiter > 255) return fail(RXG_EINVAL, "bad arguments");
     if (!h->dfa_ok) return RXG_OK;
     std::lock_guard<std::mutex> lk(h->mu);
-    if (delimiter < 0) {   // one long string: placement of the chunk-parallel table
+    if (delimiter < 0) {   // one long string: placement of the chunk-parallel table, and its lookback
         h->line_freq[-1] = lt_sample_freq_plain(h->prog, h->dfa, sample, len);
+        h->lookback = lt_sync_lookback(h->prog, h->dfa, sample, len);
         if (h->plain && h->device >= 0) {
             DeviceGuard g(h->device);
             return build_chunk_lt(h);
@@ -856,7 +859,7 @@ int rxg_match_one_ex(rxg_heap* h, const uint8_t* d_bytes, uint64_t len, int engi
             CountSlot cs;
             if (int rc = stream_slot(h, st, &cs, false)) return rc;
             const cudaError_t e = launch_chunked_tma(h->plain->chunk_lt, h->plain->d_chunk, d_bytes, len, chunk,
-                                                     o.lookback ? o.lookback : 64, scratch, d_accept, o.d_repairs,
+                                                     o.lookback ? o.lookback : h->lookback, scratch, d_accept, o.d_repairs,
                                                      cs, h->device, st,
                                                      (o.flags & RXG_ONE_ENTRY) ? o.entry_state : kStartState,
                                                      o.d_exit_state);
@@ -867,7 +870,7 @@ int rxg_match_one_ex(rxg_heap* h, const uint8_t* d_bytes, uint64_t len, int engi
         }
         uint32_t chunk = o.chunk ? o.chunk : chunked_auto_chunk(*t, len, h->device);
         if (chunk % 64) return fail(RXG_EINVAL, "chunk must be a multiple of 64");
-        const uint32_t lookback = o.lookback ? o.lookback : 64;
+        const uint32_t lookback = o.lookback ? o.lookback : h->lookback;
         void* scratch = nullptr;
         RXG_CUDA(cudaMallocAsync(&scratch, chunked_scratch_bytes(len, chunk), st));
         const cudaError_t e = launch_chunked(*t, d_bytes, len, chunk, lookback, scratch, d_accept, o.d_repairs,

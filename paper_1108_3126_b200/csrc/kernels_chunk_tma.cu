@@ -132,26 +132,20 @@ __device__ uint32_t entry_guess(const Args& a, uint64_t r) {
 // default 64-byte lookback every chain's four 16-byte loads are issued
 // together and the chains walk interleaved, instead of one dependent walk
 // after the other.
-template <int L, int CH>
-__device__ void entry_guesses(const Args& a, uint64_t row0, uint32_t lane, uint32_t (&s)[CH], const bool (&valid)[CH]) {
-    bool fast = a.lookback == 64;
-#pragma unroll
-    for (int j = 0; j < CH; ++j) fast &= !valid[j] || (row0 + j * 32 + lane) * a.chunk >= 64;
-    if (!fast) {
-#pragma unroll
-        for (int j = 0; j < CH; ++j) s[j] = valid[j] ? entry_guess<L>(a, row0 + j * 32 + lane) : a.start;
-        return;
-    }
-    uint4 v[CH][4];
+template <int L, int CH, int U>
+__device__ void entry_guesses_u(const Args& a, uint64_t row0, uint32_t lane, uint32_t (&s)[CH],
+                                const bool (&valid)[CH]) {
+    constexpr uint64_t LB = 16 * U;
+    uint4 v[CH][U];
 #pragma unroll
     for (int j = 0; j < CH; ++j) {
-        const uint64_t c0 = valid[j] ? (row0 + j * 32 + lane) * a.chunk : 64;
+        const uint64_t c0 = valid[j] ? (row0 + j * 32 + lane) * a.chunk : LB;
 #pragma unroll
-        for (int u = 0; u < 4; ++u) v[j][u] = __ldg(reinterpret_cast<const uint4*>(a.text + c0 - 64) + u);
+        for (int u = 0; u < U; ++u) v[j][u] = __ldg(reinterpret_cast<const uint4*>(a.text + c0 - LB) + u);
         s[j] = a.start;
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
+    for (int u = 0; u < U; ++u)
 #pragma unroll
         for (int w = 0; w < 4; ++w)
 #pragma unroll
@@ -162,6 +156,22 @@ __device__ void entry_guesses(const Args& a, uint64_t row0, uint32_t lane, uint3
 #pragma unroll
     for (int j = 0; j < CH; ++j)
         if (!valid[j]) s[j] = a.start;
+}
+
+template <int L, int CH>
+__device__ void entry_guesses(const Args& a, uint64_t row0, uint32_t lane, uint32_t (&s)[CH], const bool (&valid)[CH]) {
+    const uint32_t lb = a.lookback;
+    bool fast = lb == 16 || lb == 32 || lb == 64;
+#pragma unroll
+    for (int j = 0; j < CH; ++j) fast &= !valid[j] || (row0 + j * 32 + lane) * a.chunk >= lb;
+    if (!fast) {
+#pragma unroll
+        for (int j = 0; j < CH; ++j) s[j] = valid[j] ? entry_guess<L>(a, row0 + j * 32 + lane) : a.start;
+        return;
+    }
+    if (lb == 16) entry_guesses_u<L, CH, 1>(a, row0, lane, s, valid);
+    else if (lb == 32) entry_guesses_u<L, CH, 2>(a, row0, lane, s, valid);
+    else entry_guesses_u<L, CH, 4>(a, row0, lane, s, valid);
 }
 
 // In-order repair from the first wrong guess (one warp, the table already in

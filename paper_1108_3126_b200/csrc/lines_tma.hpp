@@ -46,6 +46,10 @@ struct LtTable {
 LtTable make_lines_tma_table(const Program& p, const Dfa& d, uint8_t delim, const std::vector<double>* freq = nullptr,
                              bool force_class = false);
 std::vector<double> lt_sample_freq(const Program& p, const Dfa& d, uint8_t delim, const uint8_t* sample, uint64_t len);
+// Shortest lookback in {16, 32, 64} whose guess (walk the k bytes before a
+// position from the start state) is the true state at >= 99.9% of the
+// sample's positions: the chunk engine's default for this pattern.
+uint32_t lt_sync_lookback(const Program& p, const Dfa& d, const uint8_t* sample, uint64_t len);
 // Same for one long string (no delimiter): S x 256 counts.
 std::vector<double> lt_sample_freq_plain(const Program& p, const Dfa& d, const uint8_t* sample, uint64_t len);
 

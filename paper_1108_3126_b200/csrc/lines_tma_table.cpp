@@ -66,6 +66,26 @@ std::vector<double> lt_sample_freq(const Program& p, const Dfa& d, uint8_t delim
     return f;
 }
 
+uint32_t lt_sync_lookback(const Program& p, const Dfa& d, const uint8_t* sample, uint64_t len) {
+    // the true state before every byte of the sample
+    std::vector<int32_t> st(len + 1);
+    st[0] = d.start;
+    for (uint64_t i = 0; i < len; ++i)
+        st[i + 1] = d.next[static_cast<size_t>(st[i]) * static_cast<size_t>(d.n_classes) + p.byte_class[sample[i]]];
+    for (uint32_t k : {16u, 32u}) {
+        uint64_t tried = 0, wrong = 0;
+        for (uint64_t pos = 64; pos <= len; pos += 61) {
+            int32_t g = d.start;
+            for (uint64_t i = pos - k; i < pos; ++i)
+                g = d.next[static_cast<size_t>(g) * static_cast<size_t>(d.n_classes) + p.byte_class[sample[i]]];
+            ++tried;
+            wrong += g != st[pos];
+        }
+        if (tried >= 64 && wrong * 1000 <= tried) return k;   // at most 0.1% of ranges repaired
+    }
+    return 64;
+}
+
 std::vector<double> lt_sample_freq_plain(const Program& p, const Dfa& d, const uint8_t* sample, uint64_t len) {
     std::vector<double> f(static_cast<size_t>(d.n_states) * 256, 0.0);
     int32_t s = d.start;
