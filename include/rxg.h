@@ -90,7 +90,7 @@ typedef struct rxg_heap_info {
     uint32_t line_table_bytes;   /* shared-memory image for '\n' lines (0 if none) */
     uint32_t plain_table_bytes;  /* shared-memory image for single strings / fixed stride */
     int32_t dfa_sets;      /* distinct memoized E sets before minimisation (0 if over the cap) */
-    int32_t line_tma_layout;   /* TMA table built for '\n' lines so far: 0 none, 1 direct, 2 class */
+    int32_t line_tma_layout;   /* TMA table built for '\n' lines so far: 0 none, 1 direct, 2 class map, 3 class rows with range-clamped columns */
     int32_t line_col_bytes;    /* its column stride (direct layout; chosen by rxg_heap_tune) */
     int32_t chunk_lookback;    /* single-string engine: bytes walked to guess a range's entry (tuned) */
 } rxg_heap_info;

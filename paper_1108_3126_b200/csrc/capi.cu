@@ -671,7 +671,7 @@ int rxg_heap_info_get(const rxg_heap* h, rxg_heap_info* info) {
         std::lock_guard<std::mutex> lk(const_cast<rxg_heap*>(h)->mu);
         auto it = h->lines.find('\n');
         if (it != h->lines.end() && it->second->lt.ok) {
-            info->line_tma_layout = it->second->lt.cls ? 2 : 1;
+            info->line_tma_layout = !it->second->lt.cls ? 1 : it->second->lt.range_k ? 3 : 2;
             info->line_col_bytes = it->second->lt.cls ? 0 : it->second->lt.col_bytes;
         }
     }

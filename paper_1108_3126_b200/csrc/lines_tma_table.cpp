@@ -396,11 +396,12 @@ LtTable make_class_table(const Program& p, const Dfa& d, uint8_t delim, const st
 
 LtTable make_lines_tma_table(const Program& p, const Dfa& d, uint8_t delim, const std::vector<double>* freq,
                              bool force_class) {
+    force_class = force_class || std::getenv("RXG_FORCE_CLASS") != nullptr;   // tests: class layouts on small DFAs
     if (force_class || d.n_states > kLtDirectMaxStates) {
         // range-clamped columns when they fit (no class-map lookup per byte)
         uint32_t x = 0;
         const uint32_t k = std::getenv("RXG_NO_RANGE_LAYOUT") ? 0 : range_cols(p, delim, 128, &x);
-        if (k && !force_class) {
+        if (k) {
             LtTable t = make_class_table(p, d, delim, freq, x, k);
             // the range kernel's 96 KB stage ring goes into the unused rows first
             const uint32_t hole = t.hole_hi > t.hole_lo ? (t.hole_hi - t.hole_lo) / 2048u * 2048u : 0u;

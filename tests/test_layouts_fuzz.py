@@ -1,0 +1,77 @@
+"""Random regexes through every line-table layout (direct, class rows with
+range-clamped columns, class rows with a class map; RXG_FORCE_CLASS and
+RXG_NO_RANGE_LAYOUT force the latter two on small DFAs): the host model of
+the TMA line kernel (CPU) and the kernel itself (GPU) against the oracle."""
+import os
+
+import numpy as np
+import pytest
+
+from oracle_bind import Oracle, Ref
+from paper_1108_3126_b200 import rx
+from test_gpu_stress import _dev_count
+
+LAYOUT_ID = {"direct": 1, "classmap": 2, "range": 3}
+LAYOUTS = {"direct": {}, "range": {"RXG_FORCE_CLASS": "1"},
+           "classmap": {"RXG_FORCE_CLASS": "1", "RXG_NO_RANGE_LAYOUT": "1"}}
+
+
+def _regexes(n, seed):
+    if Ref.available():
+        return Ref.random_regexes(n, 14, seed, "abc ")
+    rng = np.random.default_rng(seed)   # fallback: small hand-made mixes
+    atoms = ["a", "b", "c", " ", "()", "(a|b)", "(b|c)*", "a*", "(ab|c)"]
+    return ["".join(rng.choice(atoms, size=int(rng.integers(1, 6)))) + "*" * int(rng.integers(0, 2)) for _ in range(n)]
+
+
+def _lines(seed, n=3000):
+    rng = np.random.default_rng(seed)
+    alpha = np.frombuffer(b"abc ", np.uint8)
+    out = [alpha[rng.integers(0, 4, int(rng.integers(0, 30)))].tobytes() for _ in range(n)]
+    return np.frombuffer(b"\n".join(out) + b"\n", np.uint8)
+
+
+class _env:
+    def __init__(self, kv):
+        self.kv = kv
+
+    def __enter__(self):
+        self.old = {k: os.environ.get(k) for k in self.kv}
+        os.environ.update(self.kv)
+
+    def __exit__(self, *a):
+        for k, v in self.old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+@pytest.mark.parametrize("layout", list(LAYOUTS))
+def test_host_model_all_layouts(layout):
+    text = _lines(1)
+    for p in _regexes(40, 3):
+        want, _ = Oracle(rx.compile(rx.parse(p))).match_batch(text, 10, 0)
+        with _env(LAYOUTS[layout]):
+            m = rx.Matcher(p, device=-1)
+            for chunk in (64, 512):
+                assert m.emulate_lines_tma(text, 10, chunk) == want, (layout, p, chunk)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("layout", list(LAYOUTS))
+def test_kernel_all_layouts(layout):
+    text = _lines(2, 20000)
+    seen = set()
+    for p in _regexes(60, 5):
+        want_c, want_r = Oracle(rx.compile(rx.parse(p))).match_batch(text, 10, 0)
+        with _env(LAYOUTS[layout]):
+            m = rx.Matcher(p, device=0)
+            c, r = m.match_batch(text, 10, results=True)
+            c2, _ = m.match_batch(text, 10)
+            c3 = _dev_count(m, text)
+            lay = m.info()["line_tma_layout"]
+        assert c == c2 == c3 == want_c and np.array_equal(r, want_r), (layout, p)
+        assert lay in (0, LAYOUT_ID[layout]), (layout, p, lay)   # 0: DFA too large for any line table
+        seen.add(lay)
+    assert LAYOUT_ID[layout] in seen
