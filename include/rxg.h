@@ -153,6 +153,12 @@ int rxg_host_emulate_batch(const rxg_heap* h, const uint8_t* text, uint64_t len,
  * (chunk: multiple of 32). RXG_ETOOBIG if the DFA does not fit that layout. */
 int rxg_host_emulate_lines_tma(const rxg_heap* h, const uint8_t* text, uint64_t len, int32_t delimiter,
                                uint32_t chunk, uint64_t* count);
+/* Host emulation of the single-string TMA table (the chunked engine's
+ * layout for this heap): walks the whole string from the start state.
+ * layout (nullable): 1 direct, 2 class map, 3 range-clamped class rows,
+ * 4 packed per-byte transition words (DFA <= 6 states). Tests only. */
+int rxg_host_emulate_chunk_tma(const rxg_heap* h, const uint8_t* text, uint64_t len, int32_t* accept,
+                               int32_t* layout);
 
 /* ── matching ─────────────────────────────────────────────────────────── */
 

@@ -72,6 +72,7 @@ _SIG = {
     "rxg_host_emulate_batch": (C.c_int, [_P, _P, C.c_uint64, C.c_int32, C.c_uint32, C.c_uint32,
                                          C.POINTER(C.c_uint64), _P]),
     "rxg_host_emulate_lines_tma": (C.c_int, [_P, _P, C.c_uint64, C.c_int32, C.c_uint32, C.POINTER(C.c_uint64)]),
+    "rxg_host_emulate_chunk_tma": (C.c_int, [_P, _P, C.c_uint64, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
     "rxg_match_one": (C.c_int, [_P, _P, C.c_uint64, C.c_int, C.POINTER(C.c_int32)]),
     "rxg_match_one_ex": (C.c_int, [_P, _P, C.c_uint64, C.c_int, _P, C.POINTER(rxg_one_opts), _P]),
     "rxg_match_one_device": (C.c_int, [_P, _P, C.c_uint64, C.c_int, _P, _P]),

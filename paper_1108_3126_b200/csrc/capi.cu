@@ -282,7 +282,8 @@ int build_chunk_lt(rxg_heap* h) {
     auto f = h->line_freq.find(-1);
     LtTable lt = make_chunk_tma_table(h->prog, h->dfa, f == h->line_freq.end() ? nullptr : &f->second);
     void* d = nullptr;
-    if (lt.ok && static_cast<int>(lt.smem_table_end - kLtSmemBase) + 150 * 1024 <= h->smem_limit) {
+    const int ring = (lt.packed ? 193 : 145) * 1024;   // stage ring + barriers of the kernel's shape
+    if (lt.ok && static_cast<int>(lt.smem_table_end - kLtSmemBase) + ring <= h->smem_limit) {
         RXG_CUDA(cudaMalloc(&d, lt.lo.size()));
         RXG_CUDA(h2d(d, lt.lo.data(), lt.lo.size()));
     } else {
@@ -782,6 +783,20 @@ int rxg_heap_tune(rxg_heap* h, const uint8_t* sample, uint64_t len, int32_t deli
     return RXG_OK;
 }
 
+int rxg_host_emulate_chunk_tma(const rxg_heap* h, const uint8_t* text, uint64_t len, int32_t* accept,
+                               int32_t* layout) {
+    if (!h || !accept || (!text && len)) return fail(RXG_EINVAL, "bad arguments");
+    if (!h->dfa_ok) return fail(RXG_ETOOBIG, "no memoized step table");
+    auto f = h->line_freq.find(-1);
+    const LtTable t = make_chunk_tma_table(h->prog, h->dfa, f == h->line_freq.end() ? nullptr : &f->second);
+    if (!t.ok) return fail(RXG_ETOOBIG, "DFA too large for the TMA chunk layout");
+    uint32_t s = t.start;
+    for (uint64_t i = 0; i < len; ++i) s = lt_chunk_step(t, s, text[i]);
+    *accept = lt_chunk_accept(t, s) ? 1 : 0;
+    if (layout) *layout = t.packed ? 4 : !t.cls ? 1 : t.range_k ? 3 : 2;
+    return RXG_OK;
+}
+
 int rxg_host_emulate_lines_tma(const rxg_heap* h, const uint8_t* text, uint64_t len, int32_t delimiter,
                                uint32_t chunk, uint64_t* count) {
     if (!h || !count || (!text && len) || delimiter < 0 || delimiter > 255) return fail(RXG_EINVAL, "bad arguments");
@@ -852,7 +867,7 @@ int rxg_match_one_ex(rxg_heap* h, const uint8_t* d_bytes, uint64_t len, int engi
         if (int rc = plain_table(h, &t)) return rc;
         static const bool no_tma = std::getenv("RXG_NO_TMA") != nullptr;
         if (h->plain->chunk_lt.ok && !no_tma) {
-            uint32_t chunk = o.chunk ? o.chunk : chunked_tma_auto_chunk(len, h->device);
+            uint32_t chunk = o.chunk ? o.chunk : chunked_tma_auto_chunk(h->plain->chunk_lt, len, h->device);
             if (chunk % 32) return fail(RXG_EINVAL, "chunk must be a multiple of 32 on the TMA path");
             void* scratch = nullptr;
             RXG_CUDA(cudaMallocAsync(&scratch, chunked_tma_scratch_bytes(len, chunk), st));

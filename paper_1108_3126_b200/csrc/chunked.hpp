@@ -21,7 +21,7 @@ cudaError_t launch_chunked(const DevTable& t, const uint8_t* text, uint64_t len,
                            uint32_t entry = kStartState, uint32_t* exit_state = nullptr);
 
 // TMA-staged variant (tables from make_chunk_tma_table; d_img = device copy of t.lo).
-uint32_t chunked_tma_auto_chunk(uint64_t len, int device);
+uint32_t chunked_tma_auto_chunk(const LtTable& t, uint64_t len, int device);
 size_t chunked_tma_scratch_bytes(uint64_t len, uint32_t chunk);
 cudaError_t launch_chunked_tma(const LtTable& t, const void* d_img, const uint8_t* text, uint64_t len, uint32_t chunk,
                                uint32_t lookback, void* scratch, int32_t* accept, unsigned long long* repairs,

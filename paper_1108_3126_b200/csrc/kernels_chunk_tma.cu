@@ -58,8 +58,29 @@ CUresult make_map(CUtensorMap* map, const uint8_t* text, uint64_t rows, uint32_t
 
 namespace {
 
-constexpr int kWarps = 24, kChains = 2, kRows = 32 * kChains, kStages = 3;
-constexpr uint32_t kSlice = 32, kStageBytes = kRows * kSlice;
+// Ring shape: warps per CTA, ranges per lane, bytes per range per stage, ring depth.
+template <int W, int K, int SL, int ST>
+struct Shape {
+    static constexpr int warps = W, chains = K, rows = 32 * K, stages = ST;
+    static constexpr uint32_t slice = SL, stage_bytes = static_cast<uint32_t>(rows * SL);
+};
+using ShapeA = Shape<24, 2, 32, 3>;   // table layouts with a dependent load per byte (latency bound)
+using ShapeP = Shape<12, 2, 128, 2>;  // packed layout: 128-byte row slices (measured 70 vs 86 us on (e) with ShapeA)
+
+// Calls f(shape tag) with the ring shape of table t (RXG_CHUNK_SHAPE: A/B override).
+template <class F>
+auto with_shape(const LtTable& t, F f) {
+    static const int force = [] {
+        const char* e = std::getenv("RXG_CHUNK_SHAPE");
+        return e ? std::atoi(e) : 0;
+    }();
+    if (force == 5) return f(Shape<12, 2, 128, 2>{});
+    if (force == 8) return f(Shape<16, 1, 128, 3>{});
+    if (force == 1) return f(Shape<24, 2, 32, 3>{});
+    return t.packed ? f(ShapeP{}) : f(ShapeA{});
+}
+
+constexpr int kMaxSlots = 128;
 constexpr uint32_t kMidT = 256;   // trajectory checkpoint period (bytes)
 constexpr int kRepairRounds = 64; // parallel repair rounds before the in-order pass
 
@@ -74,7 +95,7 @@ struct Args {
     const uint4* img;
     uint32_t img_words;
     uint32_t bar_addr;
-    uint32_t stage_addr[kWarps * kStages];
+    uint32_t stage_addr[kMaxSlots];
     uint32_t start, row_bytes, cmap_addr, acc_off;
     uint32_t range_x, range_k;   // range-clamped class columns (L == 2)
     uint32_t* g;
@@ -85,19 +106,47 @@ struct Args {
     unsigned long long* round_inv; // the same per repair round, two slots alternating (zero when idle)
     int32_t* accept;
     unsigned long long* repairs;
+    uint32_t acc_mask;     // packed layout: accept bit of each state
     uint32_t entry;        // table state the string starts in (the start state unless chained)
     uint32_t* exit_state;  // nullable: table state after the string
 };
 
+// Packed layout (L == 3): the table word of byte b holds next*5 at bit
+// 5*state for every state, one copy per lane (lane l reads bank l only);
+// the state chain is one funnel shift per byte: s' = w >> (s & 31). Bits of
+// s above the low five are don't-care (shf.wrap masks the amount), canon()
+// clears them where states are stored or compared.
+__device__ __forceinline__ uint32_t shr_wrap(uint32_t w, uint32_t s) {
+    uint32_t r;
+    asm("shf.r.wrap.b32 %0, %1, %1, %2;" : "=r"(r) : "r"(w), "r"(s));
+    return r;
+}
+
+__device__ __forceinline__ uint32_t lane_base() { return kLtSmemBase + ((threadIdx.x & 31u) << 2); }
+
+template <int L>
+__device__ __forceinline__ uint32_t canon(uint32_t s) {
+    return L == 3 ? (s & 31u) : s;
+}
+
 template <int L>
 __device__ __forceinline__ uint32_t stepb(const Args& a, uint32_t s, uint32_t b) {
-    if constexpr (L == 2) return tma::lds16(s * a.row_bytes + kLtSmemBase + 1024 + 2u * min(b ^ a.range_x, a.range_k));
+    if constexpr (L == 3) return shr_wrap(tma::lds32(lane_base() + (b << 7)), s);
+    else if constexpr (L == 2) return tma::lds16(s * a.row_bytes + kLtSmemBase + 1024 + 2u * min(b ^ a.range_x, a.range_k));
     else return tma::step<L != 0>(s, b, a.row_bytes, a.cmap_addr);
+}
+
+// Step on byte k of a 4-byte word (lb = lane_base(), hoisted by the caller).
+template <int L>
+__device__ __forceinline__ uint32_t stepw(const Args& a, uint32_t s, uint32_t word, int k, uint32_t lb) {
+    if constexpr (L == 3) return shr_wrap(tma::lds32(__dp4a(word, 128u << (8 * k), lb)), s);
+    else return stepb<L>(a, s, __byte_perm(word, 0, 0x4440 + k));
 }
 
 // Walk [lo, hi) with direct loads.
 template <int L>
 __device__ uint32_t walk(const Args& a, uint32_t s, uint64_t lo, uint64_t hi) {
+    const uint32_t lb = lane_base();
     uint64_t p = lo;
     for (; p < hi && (p & 15); ++p) s = stepb<L>(a, s, a.text[p]);
     for (; p + 64 <= hi; p += 64) {   // four independent loads in flight, then 64 steps
@@ -109,17 +158,17 @@ __device__ uint32_t walk(const Args& a, uint32_t s, uint64_t lo, uint64_t hi) {
 #pragma unroll
             for (int w = 0; w < 4; ++w)
 #pragma unroll
-                for (int k = 0; k < 4; ++k) s = stepb<L>(a, s, __byte_perm(tma::word_of(v[u], w), 0, 0x4440 + k));
+                for (int k = 0; k < 4; ++k) s = stepw<L>(a, s, tma::word_of(v[u], w), k, lb);
     }
     for (; p + 16 <= hi; p += 16) {
         const uint4 v = __ldg(reinterpret_cast<const uint4*>(a.text + p));
 #pragma unroll
         for (int w = 0; w < 4; ++w)
 #pragma unroll
-            for (int k = 0; k < 4; ++k) s = stepb<L>(a, s, __byte_perm(tma::word_of(v, w), 0, 0x4440 + k));
+            for (int k = 0; k < 4; ++k) s = stepw<L>(a, s, tma::word_of(v, w), k, lb);
     }
     for (; p < hi; ++p) s = stepb<L>(a, s, a.text[p]);
-    return s;
+    return canon<L>(s);
 }
 
 template <int L>
@@ -136,6 +185,7 @@ template <int L, int CH, int U>
 __device__ void entry_guesses_u(const Args& a, uint64_t row0, uint32_t lane, uint32_t (&s)[CH],
                                 const bool (&valid)[CH]) {
     constexpr uint64_t LB = 16 * U;
+    const uint32_t lb = lane_base();
     uint4 v[CH][U];
 #pragma unroll
     for (int j = 0; j < CH; ++j) {
@@ -152,10 +202,9 @@ __device__ void entry_guesses_u(const Args& a, uint64_t row0, uint32_t lane, uin
             for (int k = 0; k < 4; ++k)
 #pragma unroll
                 for (int j = 0; j < CH; ++j)
-                    s[j] = stepb<L>(a, s[j], __byte_perm(tma::word_of(v[j][u], w), 0, 0x4440 + k));
+                    s[j] = stepw<L>(a, s[j], tma::word_of(v[j][u], w), k, lb);
 #pragma unroll
-    for (int j = 0; j < CH; ++j)
-        if (!valid[j]) s[j] = a.start;
+    for (int j = 0; j < CH; ++j) s[j] = valid[j] ? canon<L>(s[j]) : a.start;
 }
 
 template <int L, int CH>
@@ -220,8 +269,12 @@ __device__ void repair_and_answer(const Args& a) {
         }
     }
     if (lane == 0) {
-        const uint32_t acc_addr = L != 0 ? kLtSmemBase + 1024 + exact * a.row_bytes + a.acc_off : exact + a.acc_off;
-        *a.accept = static_cast<int32_t>(tma::lds16(acc_addr));
+        if constexpr (L == 3) {
+            *a.accept = static_cast<int32_t>((a.acc_mask >> (exact / 5u)) & 1u);
+        } else {
+            const uint32_t acc_addr = L != 0 ? kLtSmemBase + 1024 + exact * a.row_bytes + a.acc_off : exact + a.acc_off;
+            *a.accept = static_cast<int32_t>(tma::lds16(acc_addr));
+        }
         if (a.repairs) *a.repairs = repairs;
         if (a.exit_state) *a.exit_state = exact;
         // idle slot for the next launch on this stream (CountSlot, launch.hpp)
@@ -229,21 +282,21 @@ __device__ void repair_and_answer(const Args& a) {
     }
 }
 
-template <int L, bool COOP>
-__global__ void __launch_bounds__(kWarps * 32, 1) k_chunk_tma(const __grid_constant__ Args a,
+template <class C, int L, bool COOP>
+__global__ void __launch_bounds__(C::warps * 32, 1) k_chunk_tma(const __grid_constant__ Args a,
                                                            const __grid_constant__ CUtensorMap map) {
     extern __shared__ __align__(1024) uint8_t sm[];
     if (static_cast<uint32_t>(__cvta_generic_to_shared(sm)) != kLtSmemBase) __trap();
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t bar0 = a.bar_addr + warp * kStages * 8;
-    const uint32_t tbar = a.bar_addr + kWarps * kStages * 8 + 8;   // after the ring barriers and the `last` flag
+    const uint32_t bar0 = a.bar_addr + warp * C::stages * 8;
+    const uint32_t tbar = a.bar_addr + C::warps * C::stages * 8 + 8;   // after the ring barriers and the `last` flag
     if (threadIdx.x == 0) {   // the table image by one bulk copy
         tma::mbar_init(tbar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         tma::bulk_load(kLtSmemBase, a.img, a.img_words * 16u, tbar);
     }
     if (lane == 0) {
-        for (int st = 0; st < kStages; ++st) tma::mbar_init(bar0 + st * 8, 1);
+        for (int st = 0; st < C::stages; ++st) tma::mbar_init(bar0 + st * 8, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -262,70 +315,72 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_chunk_tma(const __grid_const
         a.e[r] = s;
     }
     uint32_t phase = 0;
-    const uint32_t ncol = a.chunk / kSlice;
-    const uint32_t* stage = a.stage_addr + warp * kStages;
+    const uint32_t ncol = a.chunk / C::slice;
+    const uint32_t* stage = a.stage_addr + warp * C::stages;
+    const uint32_t lb = lane_base();
     // tiles interleave the CTAs (tile = warp * grid + cta): small inputs spread over every SM
     for (uint64_t tile = static_cast<uint64_t>(warp) * gridDim.x + blockIdx.x; tile < a.tiles;
-         tile += static_cast<uint64_t>(gridDim.x) * kWarps) {
-        const uint64_t row0 = tile * kRows;
+         tile += static_cast<uint64_t>(gridDim.x) * C::warps) {
+        const uint64_t row0 = tile * C::rows;
         if (lane == 0) {
-            const uint32_t pro = ncol < kStages ? ncol : kStages;
+            const uint32_t pro = ncol < C::stages ? ncol : C::stages;
             for (uint32_t st = 0; st < pro; ++st)
-                tma::issue<kStageBytes>(&map, stage[st], bar0 + st * 8, static_cast<int32_t>(st * kSlice),
+                tma::issue<C::stage_bytes>(&map, stage[st], bar0 + st * 8, static_cast<int32_t>(st * C::slice),
                                         static_cast<int32_t>(row0));
         }
-        uint32_t s[kChains], guess[kChains];
-        bool valid[kChains];
+        uint32_t s[C::chains], guess[C::chains];
+        bool valid[C::chains];
 #pragma unroll
-        for (int j = 0; j < kChains; ++j) {
+        for (int j = 0; j < C::chains; ++j) {
             valid[j] = row0 + j * 32 + lane < a.rows;
         }
-        entry_guesses<L, kChains>(a, row0, lane, s, valid);
+        entry_guesses<L, C::chains>(a, row0, lane, s, valid);
 #pragma unroll
-        for (int j = 0; j < kChains; ++j) {
+        for (int j = 0; j < C::chains; ++j) {
             guess[j] = s[j];
             if (valid[j]) a.g[row0 + j * 32 + lane] = s[j];
         }
         for (uint32_t col = 0; col < ncol; ++col) {
-            const uint32_t st = col % kStages;
+            const uint32_t st = col % C::stages;
             tma::mbar_wait(bar0 + st * 8, (phase >> st) & 1u);
             phase ^= 1u << st;
 #pragma unroll
-            for (int g = 0; g < 2; ++g) {
-                uint4 v[kChains];
+            for (int g = 0; g < static_cast<int>(C::slice / 16); ++g) {
+                uint4 v[C::chains];
 #pragma unroll
-                for (int j = 0; j < kChains; ++j) {
+                for (int j = 0; j < C::chains; ++j) {
                     const uint32_t r = j * 32 + lane;
-                    v[j] = tma::lds128(stage[st] + r * kSlice + (tma::granule<kSlice>(r, g) << 4));
+                    v[j] = tma::lds128(stage[st] + r * C::slice + (tma::granule<C::slice>(r, g) << 4));
                 }
 #pragma unroll
                 for (int w = 0; w < 4; ++w)
 #pragma unroll
                     for (int k = 0; k < 4; ++k)
 #pragma unroll
-                        for (int j = 0; j < kChains; ++j)
-                            s[j] = stepb<L>(a, s[j], __byte_perm(tma::word_of(v[j], w), 0, 0x4440 + k));
+                        for (int j = 0; j < C::chains; ++j) s[j] = stepw<L>(a, s[j], tma::word_of(v[j], w), k, lb);
             }
             __syncwarp();
-            if (lane == 0 && col + kStages < ncol) {
+            if (lane == 0 && col + C::stages < ncol) {
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                tma::issue<kStageBytes>(&map, stage[st], bar0 + st * 8, static_cast<int32_t>((col + kStages) * kSlice),
+                tma::issue<C::stage_bytes>(&map, stage[st], bar0 + st * 8, static_cast<int32_t>((col + C::stages) * C::slice),
                                         static_cast<int32_t>(row0));
             }
-            if (((col + 1) * kSlice) % kMidT == 0 || col + 1 == ncol) {
+            if (((col + 1) * C::slice) % kMidT == 0 || col + 1 == ncol) {
 #pragma unroll
-                for (int j = 0; j < kChains; ++j)
-                    if (valid[j]) a.mid[(row0 + j * 32 + lane) * per + ((col + 1) * kSlice - 1) / kMidT] = s[j];
+                for (int j = 0; j < C::chains; ++j)
+                    if (valid[j]) a.mid[(row0 + j * 32 + lane) * per + ((col + 1) * C::slice - 1) / kMidT] = canon<L>(s[j]);
             }
         }
 #pragma unroll
-        for (int j = 0; j < kChains; ++j)
+        for (int j = 0; j < C::chains; ++j) {
+            s[j] = canon<L>(s[j]);
             if (valid[j]) a.e[row0 + j * 32 + lane] = s[j];
+        }
         // boundaries inside the tile, from registers: row j*32+lane follows
         // j*32+lane-1 (lane - 1, or lane 31 of the previous chain)
         uint32_t bad = ~0u;
 #pragma unroll
-        for (int j = kChains - 1; j >= 0; --j) {
+        for (int j = C::chains - 1; j >= 0; --j) {
             const uint32_t up = __shfl_up_sync(0xFFFFFFFFu, s[j], 1);
             const uint32_t wrap = j > 0 ? __shfl_sync(0xFFFFFFFFu, s[j > 0 ? j - 1 : 0], 31) : 0u;
             const bool has_pred = lane > 0 || j > 0;
@@ -337,7 +392,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_chunk_tma(const __grid_const
     if constexpr (!COOP) {
         // small inputs: the last CTA to finish checks the seams between tiles
         // and one of its warps repairs in order (no grid-wide sync)
-        uint32_t* last = reinterpret_cast<uint32_t*>(sm + (a.bar_addr + kWarps * kStages * 8 - kLtSmemBase));
+        uint32_t* last = reinterpret_cast<uint32_t*>(sm + (a.bar_addr + C::warps * C::stages * 8 - kLtSmemBase));
         __syncthreads();
         if (threadIdx.x == 0) {
             __threadfence();
@@ -348,7 +403,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_chunk_tma(const __grid_const
         __threadfence();
         unsigned long long bad = ~0ull;
         for (uint64_t t = 1 + threadIdx.x; t <= a.tiles; t += blockDim.x) {
-            const uint64_t j = t < a.tiles ? t * kRows : a.rows;
+            const uint64_t j = t < a.tiles ? t * C::rows : a.rows;
             if (j >= a.nranges || (t == a.tiles && a.nranges == a.rows)) continue;
             if (a.g[j] != a.e[j - 1]) {
                 bad = j;
@@ -374,7 +429,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_chunk_tma(const __grid_const
     {   // the first row of every tile > 0, and range `rows`
         unsigned long long bad = ~0ull;
         for (uint64_t t = 1 + gtid; t <= a.tiles; t += nthreads) {
-            const uint64_t j = t < a.tiles ? t * kRows : a.rows;
+            const uint64_t j = t < a.tiles ? t * C::rows : a.rows;
             if (j >= a.nranges || (t == a.tiles && a.nranges == a.rows)) continue;
             if (a.g[j] != a.e[j - 1]) {
                 bad = j;
@@ -440,21 +495,21 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_chunk_tma(const __grid_const
 
 uint32_t align_up(uint32_t x, uint32_t a) { return (x + a - 1) / a * a; }
 
-template <int L>
+template <class C, int L>
 cudaError_t run(const LtTable& t, Args& a, int device, cudaStream_t st) {
     // stage ring after the table image, mbarriers after the ring
     uint32_t p = align_up(t.smem_table_end, 1024);
-    for (int k = 0; k < kWarps * kStages; ++k, p += kStageBytes) a.stage_addr[k] = p;
+    for (int k = 0; k < C::warps * C::stages; ++k, p += C::stage_bytes) a.stage_addr[k] = p;
     a.bar_addr = align_up(p, 8);
-    const uint32_t smem = a.bar_addr + kWarps * kStages * 8 + 16 - kLtSmemBase;   // ring barriers, `last`, table barrier
+    const uint32_t smem = a.bar_addr + C::warps * C::stages * 8 + 16 - kLtSmemBase;   // ring barriers, `last`, table barrier
     CUtensorMap map;
     std::memset(&map, 0, sizeof(map));
-    if (a.rows > 0 && tma::make_map(&map, a.text, a.rows, a.chunk, kSlice, kRows) != CUDA_SUCCESS)
+    if (a.rows > 0 && tma::make_map(&map, a.text, a.rows, a.chunk, C::slice, C::rows) != CUDA_SUCCESS)
         return cudaErrorInvalidValue;
     // grid-wide repair rounds pay off above a few MB; below, the launch and two
     // grid syncs cost more than the in-order repair can
     const bool coop = a.len >= (4ull << 20);
-    auto* kern = coop ? k_chunk_tma<L, true> : k_chunk_tma<L, false>;
+    auto* kern = coop ? k_chunk_tma<C, L, true> : k_chunk_tma<C, L, false>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     int sms = 148;
@@ -462,25 +517,30 @@ cudaError_t run(const LtTable& t, Args& a, int device, cudaStream_t st) {
     const uint64_t want = a.tiles;   // at most one tile per CTA needed to reach every SM
     const int grid = static_cast<int>(want == 0 ? 1 : (want < static_cast<uint64_t>(sms) ? want : sms));
     if (!coop) {
-        kern<<<grid, kWarps * 32, smem, st>>>(a, map);
+        kern<<<grid, C::warps * 32, smem, st>>>(a, map);
         return cudaGetLastError();
     }
     // cooperative: every CTA is resident (one per SM), the repair rounds sync the grid
     void* args[] = {&a, &map};
-    return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(kern), dim3(grid), dim3(kWarps * 32), args, smem,
+    return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(kern), dim3(grid), dim3(C::warps * 32), args, smem,
                                        st);
 }
 
 }  // namespace
 
-uint32_t chunked_tma_auto_chunk(uint64_t len, int device) {
+template <class C>
+uint32_t auto_chunk(uint64_t len, int device) {
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-    const uint64_t ranges = static_cast<uint64_t>(sms) * kWarps * kRows;
+    const uint64_t ranges = static_cast<uint64_t>(sms) * C::warps * C::rows;
     uint64_t c = (len + ranges - 1) / ranges;
-    c = (c + kSlice - 1) / kSlice * kSlice;   // slice multiple: keeps the grid at one CTA per SM
-    if (c < 2 * kSlice) c = 2 * kSlice;       // small inputs: short ranges (the lookback is 64 B)
+    c = (c + C::slice - 1) / C::slice * C::slice;   // slice multiple: keeps the grid at one CTA per SM
+    if (c < 2 * C::slice) c = 2 * C::slice;         // small inputs: short ranges (the lookback is 64 B)
     return static_cast<uint32_t>(c);
+}
+
+uint32_t chunked_tma_auto_chunk(const LtTable& t, uint64_t len, int device) {
+    return with_shape(t, [&](auto c) { return auto_chunk<decltype(c)>(len, device); });
 }
 
 size_t chunked_tma_scratch_bytes(uint64_t len, uint32_t chunk) {
@@ -491,7 +551,8 @@ size_t chunked_tma_scratch_bytes(uint64_t len, uint32_t chunk) {
 cudaError_t launch_chunked_tma(const LtTable& t, const void* d_img, const uint8_t* text, uint64_t len, uint32_t chunk,
                                uint32_t lookback, void* scratch, int32_t* accept, unsigned long long* repairs,
                                CountSlot cs, int device, cudaStream_t st, uint32_t entry, uint32_t* exit_state) {
-    if (chunk == 0 || chunk % kSlice) return cudaErrorInvalidValue;
+    const uint32_t slice = with_shape(t, [](auto c) { return decltype(c)::slice; });
+    if (chunk == 0 || chunk % slice) return cudaErrorInvalidValue;
     Args a{};
     a.text = text;
     a.len = len;
@@ -499,7 +560,6 @@ cudaError_t launch_chunked_tma(const LtTable& t, const void* d_img, const uint8_
     a.lookback = lookback;
     a.rows = len / chunk;
     a.nranges = (len + chunk - 1) / chunk;
-    a.tiles = (a.rows + kRows - 1) / kRows;
     a.img = static_cast<const uint4*>(d_img);
     a.img_words = t.lo_bytes / 16;
     a.start = t.start;
@@ -521,7 +581,18 @@ cudaError_t launch_chunked_tma(const LtTable& t, const void* d_img, const uint8_
     // (len == 0: one CTA, no ranges; the repair pass answers from the start state)
     a.range_x = t.range_x;
     a.range_k = t.range_k;
-    return t.cls ? (t.range_k ? run<2>(t, a, device, st) : run<1>(t, a, device, st)) : run<0>(t, a, device, st);
+    a.acc_mask = t.acc_mask;
+    if (t.packed)
+        return with_shape(t, [&](auto c) {
+            using C = decltype(c);
+            a.tiles = (a.rows + C::rows - 1) / C::rows;
+            return run<C, 3>(t, a, device, st);
+        });
+    return with_shape(t, [&](auto c) {
+        using C = decltype(c);
+        a.tiles = (a.rows + C::rows - 1) / C::rows;
+        return t.cls ? (t.range_k ? run<C, 2>(t, a, device, st) : run<C, 1>(t, a, device, st)) : run<C, 0>(t, a, device, st);
+    });
 }
 
 }  // namespace rxg

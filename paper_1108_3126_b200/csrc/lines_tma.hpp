@@ -31,6 +31,11 @@ struct LtTable {
     uint32_t acc_off = 0;                // plain (chunk) tables: byte offset of a row's accept flag
     uint32_t col_bytes = kLtColBytes;    // direct layouts: column stride (entry for byte b at row + col_bytes*b)
     uint32_t range_x = 0, range_k = 0;   // class layout with range-clamped columns: column = min(b ^ x, k) (k = 0: class map)
+    // packed layout (chunk tables, DFA <= kLtPackedMaxStates): one u32 per byte holding the
+    // whole transition function, 5-bit fields next*5 at bit 5*state, replicated per lane
+    // (word for byte b, lane l at 0x400 + 128 b + 4 l); states are 5*state, acc_mask bit i = accept(i)
+    bool packed = false;
+    uint32_t acc_mask = 0;
     std::vector<uint8_t> lo, hi;     // images of [lo_addr, +lo) main rows and [hi_addr, +hi) upper rows
     uint32_t lo_addr = 0, hi_addr = 0;
     uint32_t lo_bytes = 0, hi_bytes = 0;
@@ -72,6 +77,9 @@ RowPlacement lt_place_groups(const std::vector<double>* freq, uint32_t nrows, ui
 
 // Host emulation of the table walk, for CPU tests.
 uint32_t lt_step(const LtTable& t, uint32_t s, uint8_t byte);
+// Same for the plain (chunk) tables; lt_chunk_accept: accept bit of a table state.
+uint32_t lt_chunk_step(const LtTable& t, uint32_t s, uint8_t byte);
+bool lt_chunk_accept(const LtTable& t, uint32_t s);
 inline uint32_t lt_count(const LtTable& t, uint32_t s) { return s >> t.acc_shift; }
 
 // Largest DFA the direct layouts take (rows of 256 columns, absolute u16
@@ -79,6 +87,7 @@ inline uint32_t lt_count(const LtTable& t, uint32_t s) { return s >> t.acc_shift
 // single-string table); bigger ones use the class layout.
 constexpr int32_t kLtDirectMaxStates = 52;
 constexpr int32_t kLtChunkDirectMaxStates = 56;
+constexpr int32_t kLtPackedMaxStates = 6;
 
 // chunk = bytes per range (multiple of lines_tma_slice()), 0 = one wave of ranges.
 cudaError_t launch_lines_tma(const LtTable& t, const uint8_t* text, uint64_t len, uint8_t delim, uint32_t chunk,

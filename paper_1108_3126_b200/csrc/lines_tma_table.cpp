@@ -519,7 +519,20 @@ LtTable make_chunk_tma_table(const Program& p, const Dfa& d, const std::vector<d
         return static_cast<uint32_t>(d.next[static_cast<size_t>(s) * static_cast<size_t>(d.n_classes) + c]);
     };
     t.lo_addr = kLtSmemBase;
-    if (S <= kLtChunkDirectMaxStates) {
+    if (static_cast<int32_t>(S) <= kLtPackedMaxStates && !std::getenv("RXG_NO_PACKED")) {
+        // packed: the step is a variable shift of one per-byte word (no dependent
+        // table load on the state chain), the word read from the lane's own bank
+        t.packed = true;
+        t.lo_bytes = 256u * 128u;
+        t.lo.assign(t.lo_bytes, 0);
+        for (uint32_t b = 0; b < 256; ++b) {
+            uint32_t w = 0;
+            for (uint32_t s = 0; s < S; ++s) w |= (5u * next(s, p.byte_class[b])) << (5u * s);
+            for (uint32_t l = 0; l < 32; ++l) std::memcpy(&t.lo[b * 128u + l * 4u], &w, 4);
+        }
+        for (uint32_t s = 0; s < S; ++s) t.acc_mask |= static_cast<uint32_t>(d.accept[s] != 0) << s;
+        t.start = 5u * static_cast<uint32_t>(d.start);
+    } else if (S <= kLtChunkDirectMaxStates) {
         // direct: rows of 256 four-byte columns at chosen bank offsets
         // direct: rows of 256 four-byte columns at chosen bank offsets; a row's
         // accept flag follows its columns. (Row pairs measured slower here:
@@ -601,6 +614,32 @@ uint32_t lt_step(const LtTable& t, uint32_t s, uint8_t byte) {
     if (s < kLtAccAddr) std::memcpy(&v, &t.lo[s - t.lo_addr + t.col_bytes * byte], 2);
     else std::memcpy(&v, &t.hi[s - kLtAccAddr + t.col_bytes * byte], 2);
     return v;
+}
+
+uint32_t lt_chunk_step(const LtTable& t, uint32_t s, uint8_t byte) {
+    if (t.packed) {
+        uint32_t w;
+        std::memcpy(&w, &t.lo[static_cast<size_t>(byte) * 128u], 4);
+        return (w >> (s & 31u)) & 31u;
+    }
+    uint16_t v;
+    if (t.cls) {
+        uint32_t colabs;
+        if (t.range_k) colabs = kLtSmemBase + 1024 + 2u * std::min<uint32_t>(static_cast<uint32_t>(byte) ^ t.range_x, t.range_k);
+        else std::memcpy(&colabs, &t.lo[static_cast<size_t>(byte) * 4], 4);
+        std::memcpy(&v, &t.lo[s * t.row_bytes + colabs - t.lo_addr], 2);
+        return v;
+    }
+    std::memcpy(&v, &t.lo[s - t.lo_addr + kLtColBytes * byte], 2);
+    return v;
+}
+
+bool lt_chunk_accept(const LtTable& t, uint32_t s) {
+    if (t.packed) return (t.acc_mask >> ((s & 31u) / 5u)) & 1u;
+    uint16_t v;
+    const uint32_t addr = t.cls ? kLtSmemBase + 1024 + s * t.row_bytes + t.acc_off : s + t.acc_off;
+    std::memcpy(&v, &t.lo[addr - t.lo_addr], 2);
+    return v != 0;
 }
 
 }  // namespace rxg

@@ -263,6 +263,13 @@ class Matcher:
                                               res.ctypes.data))
         return cnt.value, res[:nstr]
 
+    def emulate_chunk_tma(self, text) -> tuple[bool, int]:
+        """Host walk of the single-string TMA table -> (accepted, layout id) (tests)."""
+        p, n, keep = _ptr(text)
+        acc, lay = C.c_int32(0), C.c_int32(0)
+        _check(L.lib().rxg_host_emulate_chunk_tma(self._h, p, n, C.byref(acc), C.byref(lay)))
+        return bool(acc.value), lay.value
+
     def emulate_lines_tma(self, text, delimiter: int = 10, chunk: int = 256) -> int:
         """Host emulation of the TMA line kernel's table layout and partition -> count."""
         p, n, keep = _ptr(text)

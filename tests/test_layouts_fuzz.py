@@ -75,3 +75,58 @@ def test_kernel_all_layouts(layout):
         assert lay in (0, LAYOUT_ID[layout]), (layout, p, lay)   # 0: DFA too large for any line table
         seen.add(lay)
     assert LAYOUT_ID[layout] in seen
+
+
+# ── single-string (chunk) tables: packed per-byte words (<= 6 states), direct, class ──
+
+CHUNK_LAYOUTS = {"default": {}, "nopacked": {"RXG_NO_PACKED": "1"}}
+
+
+def _strings(seed, n=60):
+    rng = np.random.default_rng(seed)
+    alpha = np.frombuffer(b"abc ", np.uint8)
+    return [alpha[rng.integers(0, 4, int(rng.integers(0, 40)))].tobytes() for _ in range(n)]
+
+
+@pytest.mark.parametrize("layout", list(CHUNK_LAYOUTS))
+def test_chunk_table_host_model(layout):
+    seen = set()
+    for p in _regexes(60, 11) + ["(a|b)*abb", "a*", "()", "(a|b|c| )*"]:
+        o = Oracle(rx.compile(rx.parse(p)))
+        with _env(CHUNK_LAYOUTS[layout]):
+            m = rx.Matcher(p, device=-1)
+            states = m.info()["dfa_states"]
+            for w in _strings(hash(p) & 0xFFFF):
+                acc, lay = m.emulate_chunk_tma(w)
+                assert acc == o.accepts(w), (layout, p, w)
+                assert (lay == 4) == (layout == "default" and 0 < states <= 6), (p, states, lay)
+                seen.add(lay)
+    assert (4 in seen) == (layout == "default")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("layout", list(CHUNK_LAYOUTS))
+def test_chunk_kernel_layouts(layout):
+    import torch
+
+    rng = np.random.default_rng(7)
+    alpha = np.frombuffer(b"abc ", np.uint8)
+    for p in _regexes(25, 13) + ["(a|b)*abb", "(a|b|c| )*"]:
+        o = Oracle(rx.compile(rx.parse(p)))
+        with _env(CHUNK_LAYOUTS[layout]):
+            m = rx.Matcher(p, device=0)
+            for n in (0, 1, 100, 5000, 300_000, 5 << 20):   # up to the cooperative-launch path
+                w = alpha[rng.integers(0, 4, n)]
+                if n > 3 and rng.integers(0, 2):
+                    w[-3:] = np.frombuffer(b"abb", np.uint8)
+                want = o.accepts(w.tobytes()) if n <= 300_000 else None
+                d = torch.zeros(n + 64, dtype=torch.uint8, device="cuda")
+                d[:n].copy_(torch.from_numpy(w))
+                acc = torch.zeros(1, dtype=torch.int32, device="cuda")
+                m.match_one_ex(d, acc, engine="chunked", nbytes=n)
+                got = bool(acc.item())
+                if want is None:   # long: the sequential DFA engine is the check
+                    acc2 = torch.zeros(1, dtype=torch.int32, device="cuda")
+                    m.match_one_ex(d, acc2, engine="dfa_seq", nbytes=n)
+                    want = bool(acc2.item())
+                assert got == want, (layout, p, n)
