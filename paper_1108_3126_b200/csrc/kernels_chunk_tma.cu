@@ -50,8 +50,16 @@ CUresult make_map(CUtensorMap* map, const uint8_t* text, uint64_t rows, uint32_t
     const CUtensorMapSwizzle sw = slice == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
                                   : slice == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
                                   : slice == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE;
+    // 128-byte slices: promote to 256 B so a row's next slice is already in L2
+    CUtensorMapL2promotion promo = slice >= 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B : CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
+    if (const char* e = std::getenv("RXG_TMA_PROMO")) {   // tuning override
+        const int v = std::atoi(e);
+        promo = v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+                : v == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                : v == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+    }
     return enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(text), dims, strides, box, estr,
-               CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+               CU_TENSOR_MAP_INTERLEAVE_NONE, sw, promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
 }
 
 }  // namespace tma
@@ -65,18 +73,20 @@ struct Shape {
     static constexpr uint32_t slice = SL, stage_bytes = static_cast<uint32_t>(rows * SL);
 };
 using ShapeA = Shape<24, 2, 32, 3>;   // table layouts with a dependent load per byte (latency bound)
-using ShapeP = Shape<12, 2, 128, 2>;  // packed layout: 128-byte row slices (measured 70 vs 86 us on (e) with ShapeA)
+using ShapeP = Shape<16, 1, 128, 3>;  // packed layout: 128-byte row slices, 256 B L2 promotion
+                                      // ((e) 1 GiB: 194 us vs 253 us for the row layout on ShapeA)
 
 // Calls f(shape tag) with the ring shape of table t (RXG_CHUNK_SHAPE: A/B override).
+// chunk: the caller's range width (0 = auto); a packed table with a chunk that is
+// not a multiple of 128 runs on the 32-byte ring.
 template <class F>
-auto with_shape(const LtTable& t, F f) {
+auto with_shape(const LtTable& t, uint32_t chunk, F f) {
     static const int force = [] {
         const char* e = std::getenv("RXG_CHUNK_SHAPE");
         return e ? std::atoi(e) : 0;
     }();
-    if (force == 5) return f(Shape<12, 2, 128, 2>{});
-    if (force == 8) return f(Shape<16, 1, 128, 3>{});
-    if (force == 1) return f(Shape<24, 2, 32, 3>{});
+    if (force == 5 && chunk % 128 == 0) return f(Shape<12, 2, 128, 2>{});
+    if (force == 1 || (t.packed && chunk % ShapeP::slice)) return f(ShapeA{});
     return t.packed ? f(ShapeP{}) : f(ShapeA{});
 }
 
@@ -300,10 +310,12 @@ __global__ void __launch_bounds__(C::warps * 32, 1) k_chunk_tma(const __grid_con
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    tma::mbar_wait(tbar, 0);
+    // the table copy is waited for where it is first used: after each warp has
+    // issued its first ring stages, so the two transfers overlap
     const uint32_t per = (a.chunk + kMidT - 1) / kMidT;   // checkpoints per range (the last may be partial)
     // the remainder range (past the last full row) walks with direct loads
     if (blockIdx.x == 0 && threadIdx.x == 0 && a.nranges > a.rows) {
+        tma::mbar_wait(tbar, 0);
         const uint64_t r = a.rows, c0 = r * a.chunk;
         uint32_t s = entry_guess<L>(a, r);
         a.g[r] = s;
@@ -328,6 +340,7 @@ __global__ void __launch_bounds__(C::warps * 32, 1) k_chunk_tma(const __grid_con
                 tma::issue<C::stage_bytes>(&map, stage[st], bar0 + st * 8, static_cast<int32_t>(st * C::slice),
                                         static_cast<int32_t>(row0));
         }
+        tma::mbar_wait(tbar, 0);
         uint32_t s[C::chains], guess[C::chains];
         bool valid[C::chains];
 #pragma unroll
@@ -389,6 +402,7 @@ __global__ void __launch_bounds__(C::warps * 32, 1) k_chunk_tma(const __grid_con
         bad = __reduce_min_sync(0xFFFFFFFFu, bad);
         if (lane == 0 && bad != ~0u) atomicMax(a.bad_inv, ~(row0 + bad));
     }
+    tma::mbar_wait(tbar, 0);   // warps without a tile (the repair below reads the table)
     if constexpr (!COOP) {
         // small inputs: the last CTA to finish checks the seams between tiles
         // and one of its warps repairs in order (no grid-wide sync)
@@ -540,7 +554,7 @@ uint32_t auto_chunk(uint64_t len, int device) {
 }
 
 uint32_t chunked_tma_auto_chunk(const LtTable& t, uint64_t len, int device) {
-    return with_shape(t, [&](auto c) { return auto_chunk<decltype(c)>(len, device); });
+    return with_shape(t, 0, [&](auto c) { return auto_chunk<decltype(c)>(len, device); });
 }
 
 size_t chunked_tma_scratch_bytes(uint64_t len, uint32_t chunk) {
@@ -551,7 +565,7 @@ size_t chunked_tma_scratch_bytes(uint64_t len, uint32_t chunk) {
 cudaError_t launch_chunked_tma(const LtTable& t, const void* d_img, const uint8_t* text, uint64_t len, uint32_t chunk,
                                uint32_t lookback, void* scratch, int32_t* accept, unsigned long long* repairs,
                                CountSlot cs, int device, cudaStream_t st, uint32_t entry, uint32_t* exit_state) {
-    const uint32_t slice = with_shape(t, [](auto c) { return decltype(c)::slice; });
+    const uint32_t slice = with_shape(t, chunk, [](auto c) { return decltype(c)::slice; });
     if (chunk == 0 || chunk % slice) return cudaErrorInvalidValue;
     Args a{};
     a.text = text;
@@ -583,12 +597,12 @@ cudaError_t launch_chunked_tma(const LtTable& t, const void* d_img, const uint8_
     a.range_k = t.range_k;
     a.acc_mask = t.acc_mask;
     if (t.packed)
-        return with_shape(t, [&](auto c) {
+        return with_shape(t, chunk, [&](auto c) {
             using C = decltype(c);
             a.tiles = (a.rows + C::rows - 1) / C::rows;
             return run<C, 3>(t, a, device, st);
         });
-    return with_shape(t, [&](auto c) {
+    return with_shape(t, chunk, [&](auto c) {
         using C = decltype(c);
         a.tiles = (a.rows + C::rows - 1) / C::rows;
         return t.cls ? (t.range_k ? run<C, 2>(t, a, device, st) : run<C, 1>(t, a, device, st)) : run<C, 0>(t, a, device, st);
