@@ -100,11 +100,14 @@ struct rxg_heap {
     PernodeTables pernode;
     // CountSlot per stream (launch.hpp): zero when idle, re-zeroed by the kernels
     std::map<cudaStream_t, unsigned long long*> slots;
+    // per stream: the chunked engine's seam arrival counters (zero when idle), grow-only
+    std::map<cudaStream_t, std::pair<unsigned int*, size_t>> seams;
 
     ~rxg_heap() {
         if (device < 0) return;
         DeviceGuard g(device);
         for (auto& kv : slots) cudaFree(kv.second);
+        for (auto& kv : seams) cudaFree(kv.second.first);
         if (plain && plain->dptr) cudaFree(plain->dptr);
         if (plain && plain->d_abs) cudaFree(plain->d_abs);
         if (plain && plain->d_chunk) cudaFree(plain->d_chunk);
@@ -201,6 +204,23 @@ int stream_slot(rxg_heap* h, cudaStream_t st, CountSlot* out, bool accumulate) {
     }
     out->p = p;
     out->accumulate = accumulate;
+    return RXG_OK;
+}
+
+// Zeroed counters for `n` seams on stream st (kept per stream; the kernel re-zeroes them).
+int seam_counters(rxg_heap* h, cudaStream_t st, size_t n, unsigned int** out) {
+    std::lock_guard<std::mutex> lk(h->mu);
+    auto& e = h->seams[st];
+    if (e.second < n) {
+        if (e.first) RXG_CUDA(cudaFreeAsync(e.first, st));
+        e.first = nullptr;
+        e.second = 0;
+        const size_t cap = std::max<size_t>(n, 4096);
+        RXG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&e.first), cap * sizeof(unsigned int), st));
+        RXG_CUDA(cudaMemsetAsync(e.first, 0, cap * sizeof(unsigned int), st));
+        e.second = cap;
+    }
+    *out = e.first;
     return RXG_OK;
 }
 
@@ -873,6 +893,8 @@ int rxg_match_one_ex(rxg_heap* h, const uint8_t* d_bytes, uint64_t len, int engi
             RXG_CUDA(cudaMallocAsync(&scratch, chunked_tma_scratch_bytes(len, chunk), st));
             CountSlot cs;
             if (int rc = stream_slot(h, st, &cs, false)) return rc;
+            // one counter per tile seam (tiles hold >= 32 ranges) and the remainder's
+            if (int rc = seam_counters(h, st, (len / chunk + 1) / 32 + 2, &cs.seam)) return rc;
             const cudaError_t e = launch_chunked_tma(h->plain->chunk_lt, h->plain->d_chunk, d_bytes, len, chunk,
                                                      o.lookback ? o.lookback : h->lookback, scratch, d_accept, o.d_repairs,
                                                      cs, h->device, st,

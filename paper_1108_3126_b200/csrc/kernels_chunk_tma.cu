@@ -117,6 +117,7 @@ struct Args {
     int32_t* accept;
     unsigned long long* repairs;
     uint32_t acc_mask;     // packed layout: accept bit of each state
+    unsigned int* seam;    // cooperative launch: tiles + 1 arrival counters (zero when idle; see seam_arrive)
     uint32_t entry;        // table state the string starts in (the start state unless chained)
     uint32_t* exit_state;  // nullable: table state after the string
 };
@@ -292,6 +293,19 @@ __device__ void repair_and_answer(const Args& a) {
     }
 }
 
+// Seam j (first row of a tile, or the remainder range) is checked by the
+// second of its two neighbours to finish: each arrives on the seam's counter
+// after publishing its g / e values, and the one that reads 1 compares
+// g[j] with e[j - 1]. (Cooperative launch; the grid sync that follows makes
+// the verdict visible, and the counters are zeroed again after it.)
+__device__ __forceinline__ void seam_arrive(const Args& a, uint64_t t, uint64_t j) {
+    __threadfence();
+    if (atomicAdd(a.seam + t, 1u) != 1u) return;
+    __threadfence();
+    if (*reinterpret_cast<volatile const uint32_t*>(a.g + j) != *reinterpret_cast<volatile const uint32_t*>(a.e + j - 1))
+        atomicMax(a.bad_inv, ~static_cast<unsigned long long>(j));
+}
+
 template <class C, int L, bool COOP>
 __global__ void __launch_bounds__(C::warps * 32, 1) k_chunk_tma(const __grid_constant__ Args a,
                                                            const __grid_constant__ CUtensorMap map) {
@@ -325,6 +339,7 @@ __global__ void __launch_bounds__(C::warps * 32, 1) k_chunk_tma(const __grid_con
             a.mid[r * per + k] = s;
         }
         a.e[r] = s;
+        if (COOP && a.rows > 0) seam_arrive(a, a.tiles, a.rows);
     }
     uint32_t phase = 0;
     const uint32_t ncol = a.chunk / C::slice;
@@ -401,6 +416,14 @@ __global__ void __launch_bounds__(C::warps * 32, 1) k_chunk_tma(const __grid_con
         }
         bad = __reduce_min_sync(0xFFFFFFFFu, bad);
         if (lane == 0 && bad != ~0u) atomicMax(a.bad_inv, ~(row0 + bad));
+        if constexpr (COOP) {   // the seams with the neighbouring tiles (this warp's g / e are written)
+            __syncwarp();
+            if (lane == 0) {
+                if (tile > 0) seam_arrive(a, tile, row0);
+                if (tile + 1 < a.tiles) seam_arrive(a, tile + 1, row0 + C::rows);
+                else if (a.nranges > a.rows) seam_arrive(a, a.tiles, a.rows);
+            }
+        }
     }
     tma::mbar_wait(tbar, 0);   // warps without a tile (the repair below reads the table)
     if constexpr (!COOP) {
@@ -440,19 +463,7 @@ __global__ void __launch_bounds__(C::warps * 32, 1) k_chunk_tma(const __grid_con
     grid.sync();
     const uint64_t nthreads = static_cast<uint64_t>(gridDim.x) * blockDim.x;
     const uint64_t gtid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    {   // the first row of every tile > 0, and range `rows`
-        unsigned long long bad = ~0ull;
-        for (uint64_t t = 1 + gtid; t <= a.tiles; t += nthreads) {
-            const uint64_t j = t < a.tiles ? t * C::rows : a.rows;
-            if (j >= a.nranges || (t == a.tiles && a.nranges == a.rows)) continue;
-            if (a.g[j] != a.e[j - 1]) {
-                bad = j;
-                break;
-            }
-        }
-        if (bad != ~0ull) atomicMax(a.bad_inv, ~bad);
-    }
-    grid.sync();
+    for (uint64_t t = gtid; t <= a.tiles; t += nthreads) a.seam[t] = 0;   // idle again (seams checked in-stream)
     unsigned long long fb = ~*reinterpret_cast<volatile unsigned long long*>(a.bad_inv);
     // Round: every range j >= fb whose guess differs from its predecessor's
     // exit re-walks from that exit (stopping where it meets its recorded
@@ -522,7 +533,7 @@ cudaError_t run(const LtTable& t, Args& a, int device, cudaStream_t st) {
         return cudaErrorInvalidValue;
     // grid-wide repair rounds pay off above a few MB; below, the launch and two
     // grid syncs cost more than the in-order repair can
-    const bool coop = a.len >= (4ull << 20);
+    const bool coop = a.len >= (4ull << 20) && a.seam;
     auto* kern = coop ? k_chunk_tma<C, L, true> : k_chunk_tma<C, L, false>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
@@ -583,6 +594,7 @@ cudaError_t launch_chunked_tma(const LtTable& t, const void* d_img, const uint8_
     a.cmap_addr = t.cmap_addr;
     a.acc_off = t.acc_off;
     a.bad_inv = cs.p + 1;
+    a.seam = cs.seam;
     a.round_inv = cs.p + 2;
     a.ticket = reinterpret_cast<unsigned int*>(cs.p + 3) + 1;   // the high half of the second round slot
                                                                // (rounds run only cooperatively)

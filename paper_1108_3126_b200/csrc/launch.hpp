@@ -56,6 +56,7 @@ int device_sm_count(int device);
 struct CountSlot {
     unsigned long long* p = nullptr;
     bool accumulate = false;
+    unsigned int* seam = nullptr;   // chunked engine: zeroed seam counters of this stream
 };
 
 // Fixed stride on the TMA data path (stride a multiple of 32; the absolute
