@@ -541,14 +541,20 @@ cudaError_t run(const LtTable& t, Args& a, int device, cudaStream_t st) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     const uint64_t want = a.tiles;   // at most one tile per CTA needed to reach every SM
     const int grid = static_cast<int>(want == 0 ? 1 : (want < static_cast<uint64_t>(sms) ? want : sms));
-    if (!coop) {
-        kern<<<grid, C::warps * 32, smem, st>>>(a, map);
-        return cudaGetLastError();
-    }
-    // cooperative: every CTA is resident (one per SM), the repair rounds sync the grid
-    void* args[] = {&a, &map};
-    return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(kern), dim3(grid), dim3(C::warps * 32), args, smem,
-                                       st);
+    // cooperative (>= 4 MiB): every CTA is resident (one per SM), the repair rounds sync the grid
+    // (programmatic dependent launch measured no gain here: a cooperative grid
+    // holding every SM's shared memory cannot overlap the previous one)
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(C::warps * 32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr;
+    attr.id = cudaLaunchAttributeCooperative;
+    attr.val.cooperative = 1;
+    cfg.attrs = &attr;
+    cfg.numAttrs = coop ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, a, map);
 }
 
 }  // namespace
