@@ -166,7 +166,11 @@ int rxg_host_emulate_chunk_tma(const rxg_heap* h, const uint8_t* text, uint64_t 
 int rxg_match_one(rxg_heap* h, const uint8_t* bytes, uint64_t len, int engine, int32_t* accept);
 
 /* One string, device buffer, asynchronous on `stream` (cudaStream_t or NULL).
- * d_accept is a device int32. */
+ * d_accept is a device int32. The chunk-parallel engine keeps its scratch
+ * (guesses, exits, checkpoints: ~16 B per 256 input bytes) and seam counters
+ * per (heap, stream), grown to the largest string seen on that stream and
+ * freed with the heap; make the first call of a given size outside
+ * CUDA-graph capture. */
 int rxg_match_one_device(rxg_heap* h, const uint8_t* d_bytes, uint64_t len, int engine,
                          int32_t* d_accept, void* stream);
 
@@ -180,7 +184,8 @@ typedef struct rxg_one_opts {
     uint32_t* d_trace;                /* ROUNDS: per symbol the next schedule as (N+1)-bit rows, bit N = null;
                                          zeroed by the caller (test_parallel.cpp:114-137) */
     uint32_t chunk;                   /* CHUNKED: bytes per range (multiple of 32 on the TMA path, 64 otherwise), 0 = auto */
-    uint32_t lookback;                /* CHUNKED: bytes walked before a range to guess its entry state (0 = 64) */
+    uint32_t lookback;                /* CHUNKED: bytes walked before a range to guess its entry state
+                                         (0 = the heap's default: 64, or 16/32/64 after rxg_heap_tune) */
     unsigned long long* d_repairs;    /* CHUNKED: ranges re-walked by the in-order repair pass */
     uint32_t flags;                   /* RXG_ONE_ENTRY: start in entry_state instead of the start state */
     uint32_t entry_state;             /* CHUNKED: opaque table state (from a d_exit_state of the same pattern) */
