@@ -166,7 +166,8 @@ int rxg_host_emulate_chunk_tma(const rxg_heap* h, const uint8_t* text, uint64_t 
 int rxg_match_one(rxg_heap* h, const uint8_t* bytes, uint64_t len, int engine, int32_t* accept);
 
 /* One string, device buffer, asynchronous on `stream` (cudaStream_t or NULL).
- * d_accept is a device int32. The chunk-parallel engine keeps its scratch
+ * d_accept is a device int32; d_bytes must be 16-byte aligned (RXG_EINVAL
+ * otherwise: every engine reads 16-byte vectors). The chunk-parallel engine keeps its scratch
  * (guesses, exits, checkpoints: ~16 B per 256 input bytes) and seam counters
  * per (heap, stream), grown to the largest string seen on that stream and
  * freed with the heap; make the first call of a given size outside

@@ -887,6 +887,8 @@ int rxg_match_one_ex(rxg_heap* h, const uint8_t* d_bytes, uint64_t len, int engi
     const bool dfa_engine = engine == RXG_ENGINE_AUTO || engine == RXG_ENGINE_DFA_SEQ || engine == RXG_ENGINE_CHUNKED;
     if (int rc = need_device(h, dfa_engine)) return rc;
     if (!d_accept || (!d_bytes && len)) return fail(RXG_EINVAL, "bad arguments");
+    // every single-string engine reads 16-byte vectors at 16-byte offsets of the string
+    if (reinterpret_cast<uintptr_t>(d_bytes) & 15) return fail(RXG_EINVAL, "string must be 16-byte aligned");
     rxg_one_opts o{};
     if (opts) o = *opts;
     DeviceGuard g(h->device);

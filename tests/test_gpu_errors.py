@@ -33,6 +33,18 @@ def test_batch_argument_errors():
     assert int(cnt.item()) == 0   # 4096 zero bytes: one line, no match
 
 
+def test_single_string_alignment():
+    m = rx.Matcher("(a|b)*abb", device=0)
+    d = torch.zeros(4096 + 64, dtype=torch.uint8, device="cuda")
+    d[4000:4003] = torch.tensor(list(b"abb"), dtype=torch.uint8)
+    acc = torch.zeros(1, dtype=torch.int32, device="cuda")
+    for eng in ("auto", "chunked", "dfa_seq", "pernode"):
+        assert _status(m.match_one_ex, d[1:], acc, engine=eng, nbytes=4002) == L.RXG_EINVAL
+    m.match_one_ex(d[16:], acc, nbytes=4003 - 16)   # aligned: fine, and the context is healthy
+    torch.cuda.synchronize()
+    assert int(acc.item()) == 0   # zeros before "abb" are outside (a|b)*
+
+
 def test_utf8_check_argument_errors():
     d = torch.zeros(64, dtype=torch.uint8, device="cuda")
     out = torch.zeros(1, dtype=torch.int64, device="cuda")
