@@ -240,3 +240,32 @@ def test_back_to_back_launches_on_streams():
         m2.match_one_device(w, acc[i:i + 1], stream=s1 if i % 2 else s2)
     torch.cuda.synchronize()
     assert acc.all()
+
+
+@pytest.mark.parametrize("chunk", [0, 128, 256, 96])
+def test_chunked_cooperative_path_wrong_guesses(chunk):
+    """Strings >= 4 MiB take the cooperative launch (seams checked in-stream by
+    the later neighbour, parallel repair rounds). Non-synchronizing automata
+    with a 16-byte lookback guess wrong at many seams; the answer must still
+    equal the sequential walk's."""
+    import torch
+
+    rng = np.random.default_rng(17)
+    for p in ["(aa)*", "(aaa)*", "((a|b)(a|b))*", "(ab|ba)*a", "(a|b)*abb"]:
+        m = rx.Matcher(p, device=0)
+        for n in (4 << 20, (6 << 20) + 5, (12 << 20) + 1):
+            if p in ("(aa)*", "(aaa)*"):
+                w = np.full(n, 97, np.uint8)
+                if rng.integers(0, 2):
+                    w[int(rng.integers(0, n))] = 98   # one wrong byte somewhere
+            else:
+                w = rng.choice([97, 98], size=n).astype(np.uint8)
+            d = torch.zeros(n + 64, dtype=torch.uint8, device="cuda")
+            d[:n].copy_(torch.from_numpy(w))
+            acc = torch.zeros(1, dtype=torch.int32, device="cuda")
+            ref = torch.zeros(1, dtype=torch.int32, device="cuda")
+            rep = torch.zeros(1, dtype=torch.int64, device="cuda")
+            m.match_one_ex(d, acc, "chunked", nbytes=n, chunk=chunk, lookback=16, d_repairs=rep)
+            m.match_one_ex(d, ref, "dfa_seq", nbytes=n)
+            torch.cuda.synchronize()
+            assert bool(acc.item()) == bool(ref.item()), (p, n, chunk)
