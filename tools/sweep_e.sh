@@ -1,1 +1,2 @@
-for t in "RXG_TILES_PER_WARP=3" "RXG_TILES_PER_WARP=2" "RXG_TILES_PER_WARP=4" "RXG_TILES_PER_WARP=6" "RXG_STATIC_TILES=1 RXG_TILES_PER_WARP=1" "RXG_TILES_PER_WARP=1"; do env $t TAG="$t" python tools/sweep_e.py; done
+# (e) device time vs size: packed layout (default) against the row layout, same box
+for t in "TAG=packed" "RXG_NO_PACKED=1"; do env $t TAG="$t" python tools/sweep_e.py; done
