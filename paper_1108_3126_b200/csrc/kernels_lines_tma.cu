@@ -139,6 +139,8 @@ __device__ __forceinline__ uint32_t counted(const Args& a, uint32_t s) {
     else return __umulhi(s, 1u << 17);
 }
 
+__device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
+
 __device__ __forceinline__ uint32_t word_of(const uint4& v, int w) {
     return w == 0 ? v.x : (w == 1 ? v.y : (w == 2 ? v.z : v.w));
 }
@@ -211,6 +213,70 @@ __device__ __forceinline__ uint32_t step_res(const Args& a, uint32_t s, uint32_t
     return s;
 }
 
+// Walk [b0, b1) from s through the tail rows, stopping once a TERM row is
+// reached; at the end of the buffer the virtual final delimiter is applied.
+template <int L>
+__device__ uint32_t walk_block(const Args& a, uint32_t s, uint64_t b0, uint64_t b1) {
+    uint64_t p = b0;
+    for (; p < b1 && s < a.term_acc; p += 16) {
+        if (p + 16 <= b1 && !(p & 15)) {
+            const uint4 v = __ldg(reinterpret_cast<const uint4*>(a.text + p));
+#pragma unroll
+            for (int w = 0; w < 4; ++w)
+#pragma unroll
+                for (int k = 0; k < 4; ++k) s = step<L>(a, s, word_of(v, w), k);
+        } else {
+            for (uint64_t q = p; q < min(p + 16, b1); ++q) s = step_b<L>(a, s, a.text[q]);
+        }
+    }
+    if (b1 == a.len && s < a.term_acc) s = step_b<L>(a, s, a.delim);
+    return s;
+}
+
+// A long straddling line (one chain, warp-uniform s0 / p0), walked by the
+// whole warp: each lane takes the next kCoopBlock bytes, guesses its entry state by
+// walking the 64 bytes before its block from the start row, walks the block,
+// and the guesses are checked in lane order against the exact exit of the
+// lane before (a wrong one is re-walked from it). A delimiter inside a lookback
+// means the line ended there, so the TERM row the guess reaches is then right.
+constexpr uint32_t kCoopBlock = 1024;
+constexpr uint64_t kCoopTail = 16384;   // bytes a chain walks alone before the warp takes over
+
+template <int L>
+__device__ uint32_t coop_walk(const Args& a, uint32_t s_true, uint64_t p0) {
+    const uint32_t lane = threadIdx.x & 31;
+    while (s_true < a.term_acc && p0 < a.len) {
+        const uint64_t b0 = p0 + static_cast<uint64_t>(lane) * kCoopBlock;
+        const uint64_t b1 = min(b0 + kCoopBlock, a.len);
+        uint32_t g, e;
+        if (b0 >= a.len) {
+            g = e = a.term_acc;   // past the buffer: passes its entry through (fixed below)
+        } else {
+            g = lane == 0 ? s_true : walk_block<L>(a, a.start + a.tail_delta, b0 - 64, b0);
+            e = walk_block<L>(a, g, b0, b1);
+        }
+        for (;;) {
+            const uint32_t up = __shfl_up_sync(0xFFFFFFFFu, e, 1);
+            const bool ok = lane == 0 || g == up;
+            const uint32_t bad = __ballot_sync(0xFFFFFFFFu, !ok);
+            if (!bad) break;
+            const int m = __ffs(bad) - 1;
+            const uint32_t ent = __shfl_sync(0xFFFFFFFFu, e, m - 1);   // exact: lanes < m agree
+            if (ent >= a.term_acc) {   // the line ended before block m
+                if (lane >= static_cast<uint32_t>(m)) g = e = ent;
+                break;
+            }
+            if (lane == static_cast<uint32_t>(m)) {
+                g = ent;
+                e = b0 >= a.len ? ent : walk_block<L>(a, ent, b0, b1);
+            }
+        }
+        s_true = __shfl_sync(0xFFFFFFFFu, e, 31);
+        p0 += 32ull * kCoopBlock;
+    }
+    return s_true;
+}
+
 // The straddling lines of all of a lane's ranges, walked interleaved (their
 // loads in flight together) instead of one after the other. s[j] enters as
 // the tail-copy row; TERM rows absorb, so a finished chain keeps stepping
@@ -220,9 +286,13 @@ template <int L, int K>
 __device__ void finish_lines(const Args& a, uint32_t (&s)[K], uint64_t (&pos)[K], const bool (&live)[K],
                              uint32_t (&ok)[K]) {
     bool more = false;
+    uint64_t begin[K];
 #pragma unroll
-    for (int j = 0; j < K; ++j) more |= live[j];
-    while (more) {
+    for (int j = 0; j < K; ++j) {
+        more |= live[j];
+        begin[j] = pos[j];
+    }
+    while (__any_sync(0xFFFFFFFFu, more)) {
         // 16 * U bytes per chain per round trip (lines end within a few dozen
         // bytes; measured better than 32 bytes on (c) despite a 16-byte spill)
         constexpr int U = 4;
@@ -257,6 +327,21 @@ __device__ void finish_lines(const Args& a, uint32_t (&s)[K], uint64_t (&pos)[K]
                 if (s[j] < a.term_acc) s[j] = step_b<L>(a, s[j], a.delim);
             }
             more |= s[j] < a.term_acc;
+        }
+        bool long_tail = false;
+#pragma unroll
+        for (int j = 0; j < K; ++j) long_tail |= live[j] && s[j] < a.term_acc && pos[j] - begin[j] >= kCoopTail;
+        if (__any_sync(0xFFFFFFFFu, long_tail)) break;
+    }
+    // lines still open after kCoopTail bytes: the whole warp walks them, one at a time
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+        uint32_t need = __ballot_sync(0xFFFFFFFFu, live[j] && s[j] < a.term_acc);
+        while (need) {
+            const int src = __ffs(need) - 1;
+            need &= need - 1;
+            const uint32_t st = coop_walk<L>(a, __shfl_sync(0xFFFFFFFFu, s[j], src), __shfl_sync(0xFFFFFFFFu, pos[j], src));
+            if (lane_id() == static_cast<uint32_t>(src)) s[j] = st;
         }
     }
 #pragma unroll

@@ -269,3 +269,30 @@ def test_chunked_cooperative_path_wrong_guesses(chunk):
             m.match_one_ex(d, ref, "dfa_seq", nbytes=n)
             torch.cuda.synchronize()
             assert bool(acc.item()) == bool(ref.item()), (p, n, chunk)
+
+
+@pytest.mark.parametrize("key", ["c", "abb", "empty_ok"])
+def test_very_long_lines_warp_cooperative(key):
+    """Lines of several MB: the range that owns one hands it to its whole warp
+    after 16 KB (kCoopTail), which walks it in 1 KB blocks with checked guesses.
+    Counts and per-line results against the oracle; the 24 MB buffer must not
+    take seconds (the serial finish ran at ~25 ns/byte)."""
+    import time
+
+    pat = _pat(key)
+    rng = np.random.default_rng(11)
+    alpha = np.frombuffer(ALPHA[key], np.uint8)
+    parts = []
+    for n in (100, 9_000_000, 30, 0, 5_000_001, 77, 8_000_000, 12):
+        parts.append(alpha[rng.integers(0, len(alpha), n)])
+        parts.append(np.array([10], np.uint8))
+    text = np.concatenate(parts)[:-1]   # unterminated last line
+    want_c, want_r = Oracle(rx.compile(rx.parse(pat))).match_batch(text, 10, 0)
+    m = rx.Matcher(pat, device=0)
+    assert _dev_count(m, text) == want_c
+    t0 = time.perf_counter()
+    assert _dev_count(m, text) == want_c
+    dt = time.perf_counter() - t0
+    c, r = m.match_batch(text, 10, results=True)
+    assert c == want_c and np.array_equal(r, want_r)
+    assert dt < 0.25, dt
