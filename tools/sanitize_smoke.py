@@ -18,6 +18,13 @@ for cfg, text in (("c", text_c), ("d", text_d)):
     m.match_batch_device(d, cnt, engine="bitset")        # k_lines_bitset
     torch.cuda.synchronize()
     assert c1 == c2 == int(r.sum()) == int(cnt.item()), cfg
+# one 300 KB line: the range that owns it hands it to its whole warp (kCoopTail)
+mc = rx.Matcher(rx.synth_pattern("c"), device=0)
+long_text = np.concatenate([text_c[:4096], np.full(300_000, ord("a"), np.uint8), text_c[4096:8192]])
+long_text[4096 + 150_000] = 10
+cl1, _ = mc.match_batch(long_text, 10)
+cl2, rl = mc.match_batch(long_text, 10, results=True)
+assert cl1 == cl2 == int(rl.sum())
 os.environ["RXG_NO_LT"] = "1"
 m = rx.Matcher(rx.synth_pattern("c"), device=0)
 c3, _ = m.match_batch(text_c, 10, results=True)          # k_lines (generic) + k_count_delims
