@@ -467,6 +467,11 @@ __global__ void __launch_bounds__(C::warps * 32, 1) k_lines_tma(const __grid_con
             const uint32_t st = col % C::stages;
             mbar_wait(bar0 + st * 8, (phase >> st) & 1u);
             phase ^= 1u << st;
+            // RES: per chain, bit i of dl / cl = byte i of the current 32 bytes is a
+            // delimiter / ends an accepted line; lines are recorded once per 32 bytes.
+            uint32_t dl[C::chains], cl[C::chains];
+#pragma unroll
+            for (int j = 0; j < C::chains; ++j) dl[j] = cl[j] = 0;
 #pragma unroll
             for (int g = 0; g < C::slice / 16; ++g) {
                 uint4 v[C::chains];
@@ -480,17 +485,40 @@ __global__ void __launch_bounds__(C::warps * 32, 1) k_lines_tma(const __grid_con
                     uint32_t wx[C::chains];   // range layout: the word XORed once, not each byte
 #pragma unroll
                     for (int j = 0; j < C::chains; ++j) wx[j] = L == 2 ? word_of(v[j], w) ^ a.range_x4 : 0u;
+                    const int sh = 16 * (g & 1) + 4 * w;   // bit of byte 0 of this word
 #pragma unroll
                     for (int k = 0; k < 4; ++k)
 #pragma unroll
                         for (int j = 0; j < C::chains; ++j) {
-                            if constexpr (RES) {
-                                s[j] = step_res<L>(a, s[j], __byte_perm(word_of(v[j], w), 0, 0x4440 + k), cnt, lc[j]);
-                            } else {
-                                s[j] = L == 2 ? step_rx(a, s[j], wx[j], k) : step<L, true>(a, s[j], word_of(v[j], w), k);
-                                cnt += counted<L>(a, s[j]);
-                            }
+                            s[j] = L == 2 ? step_rx(a, s[j], wx[j], k) : step<L, true>(a, s[j], word_of(v[j], w), k);
+                            const uint32_t c = counted<L>(a, s[j]);
+                            cnt += c;
+                            if constexpr (RES) cl[j] |= c << (sh + k);
                         }
+                    if constexpr (RES) {
+#pragma unroll
+                        for (int j = 0; j < C::chains; ++j) {
+                            // 0xFF per delimiter byte -> one bit per byte (the 4 bits sum without carries)
+                            const uint32_t m = __vcmpeq4(word_of(v[j], w), a.delim * 0x01010101u) & 0x08040201u;
+                            dl[j] |= ((m * 0x01010101u) >> 24) << sh;
+                        }
+                    }
+                }
+                if constexpr (RES) {
+                    if ((g & 1) || g + 1 == C::slice / 16) {
+#pragma unroll
+                        for (int j = 0; j < C::chains; ++j) {
+                            uint32_t dm = dl[j];
+                            while (dm) {   // the lines that ended in these 32 bytes, in byte order
+                                const uint32_t i = __ffs(dm) - 1;
+                                if (lc[j].own) a.results[lc[j].li] = static_cast<uint8_t>((cl[j] >> i) & 1u);
+                                ++lc[j].li;
+                                lc[j].own = lc[j].live;
+                                dm &= dm - 1;
+                            }
+                            dl[j] = cl[j] = 0;
+                        }
+                    }
                 }
 #pragma unroll
                 for (int j = 0; j < C::chains; ++j) last[j] = v[j].w >> 24;
