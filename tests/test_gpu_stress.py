@@ -296,3 +296,37 @@ def test_very_long_lines_warp_cooperative(key):
     c, r = m.match_batch(text, 10, results=True)
     assert c == want_c and np.array_equal(r, want_r)
     assert dt < 0.25, dt
+
+
+@pytest.mark.parametrize("key", ["c", "d", "abb", "empty_ok"])
+@pytest.mark.parametrize("chunk", [None, "96", "4096"])
+def test_short_lines_results_every_offset(key, chunk):
+    """Lines of 0-40 bytes: delimiters at every offset of the 32-byte groups the
+    per-line walk records from its bit masks, runs of empty lines, and lines
+    crossing group and range boundaries. Per-line results against the oracle."""
+    pat = _pat(key)
+    rng = np.random.default_rng(17)
+    alpha = np.frombuffer(ALPHA[key], np.uint8)
+    lens = rng.integers(0, 41, 60_000)
+    lens[rng.random(len(lens)) < 0.2] = 0
+    parts = []
+    for n in lens:
+        parts.append(alpha[rng.integers(0, len(alpha), n)])
+        parts.append(np.array([10], np.uint8))
+    text = np.concatenate(parts)
+    if key == "c":   # keywords so that lines match
+        for p in rng.integers(0, len(text) - 5, 4000):
+            text[p:p + 5] = np.frombuffer(b"ERROR", np.uint8)
+    want_c, want_r = Oracle(rx.compile(rx.parse(pat))).match_batch(text, 10, 0)
+    old = os.environ.get("RXG_LINE_CHUNK")
+    try:
+        if chunk:
+            os.environ["RXG_LINE_CHUNK"] = chunk
+        m = rx.Matcher(pat, device=0)
+        c, r = m.match_batch(text, 10, results=True)
+        assert c == want_c and np.array_equal(r, want_r)
+    finally:
+        if old is None:
+            os.environ.pop("RXG_LINE_CHUNK", None)
+        else:
+            os.environ["RXG_LINE_CHUNK"] = old
