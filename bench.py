@@ -4,24 +4,30 @@
 Metric (BASELINE.json): input GB/s matched at 1/2/4/8 B200 and % of the
 binding roofline, beside the reference's CPU lockstep matcher.
 
-Default workload: config (c) of SURVEY.md §8(d) — the 64-node
+Headline workload: config (c) of SURVEY.md §8(d) — the 64-node
 alternation/star log regex over 10M synthetic '\\n'-terminated lines
-(~1.03 GB) — the configuration BASELINE.json names "sharded at 1/2/4/8
-GPUs". A "step" is one pass of the batch matcher (K2) over the whole
-resident buffer. Other configs: --config a|b|c|d|e.
+(~1.02 GB), the configuration BASELINE.json names "sharded at 1/2/4/8 GPUs".
+A "step" is one pass of the batch matcher (K2) over the whole job.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config c] [--impl b200|reference]
 
-Under torchrun (N > 1) every rank matches its own shard of the same shape
-(weak scaling; rank r uses generator seed canonical+r) and the only
-collective is one all-reduce of the 8-byte match count per step.
+Multi-GPU (torchrun, one process per GPU) is STRONG scaling for the batch
+configs (b, c, d): every rank builds the same job, cuts it with the product's
+rxg_shard_bounds (byte-balanced at string boundaries), matches only its shard,
+and the product's rxg_match_batch_allreduce sums the 8-byte count over NCCL —
+the only inter-GPU traffic. `value` = whole-job bytes / (max over ranks of the
+step time including that all-reduce); the kernel-only span is reported next
+to it. Single-string configs (a, e) run as replicas (one string has a
+sequential dependency chain).
+
+At N=1 the line also carries sub-records for the other four configs, each
+with its own roofline and CPU reference sample.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
-import subprocess
 import sys
 import threading
 import time
@@ -40,19 +46,53 @@ CONFIGS = {
     "d": (10, 0, "1024-node keyword union over 1 GiB of ~1 KiB lines"),
     "e": (-2, 0, "4096-node keyword-star regex over one 256 MiB string"),
 }
-W_WORDS = {"a": 1, "b": 3, "c": 1, "d": 16, "e": 65}
+NOMINAL_INT32_TOPS = 148 * 128 * 1.965e9 / 1e12   # all lanes issuing one 32-bit op per clock
 
 
 def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
 
-def peaks():
+def cpu_model() -> str:
+    try:
+        for ln in Path("/proc/cpuinfo").read_text().splitlines():
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def hbm_peak():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
         d = json.loads(p.read_text())
-        return float(d["hbm_gbs"]), "measured"
-    return 6650.0, "fallback"
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json, copy bandwidth)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+_INT32 = None
+
+
+def int32_peak(dev: int):
+    """Measured INT32 lane-instruction peak (tools/peaks/int32_peak.cu): best of
+    LOP3, IADD3 and LOP3+IMAD, in Tops/s; falls back to the nominal figure."""
+    global _INT32
+    if _INT32 is None:
+        import ctypes as C
+
+        so = ROOT / "tools" / "peaks" / "libint32peak.so"
+        try:
+            lib = C.CDLL(str(so))
+            out = (C.c_double * 3)()
+            rc = lib.int32_peak(dev, 3, out)
+            if rc != 0:
+                raise RuntimeError(f"int32_peak rc={rc}")
+            mix = {"lop3": out[0], "iadd3": out[1], "lop3_imad": out[2]}
+            _INT32 = (max(mix.values()), "measured live (tools/peaks/int32_peak.cu)", mix)
+        except Exception as e:  # noqa: BLE001 - report, do not fail the bench
+            _INT32 = (NOMINAL_INT32_TOPS, f"nominal (measurement unavailable: {e})", {})
+    return _INT32
 
 
 class ClockSampler:
@@ -66,7 +106,6 @@ class ClockSampler:
     def __init__(self, device: int):
         self.device = device
         self.period = float(os.environ.get("RXG_CLOCK_PERIOD_S", "0.00025"))
-        self.off = os.environ.get("RXG_NO_CLOCKS") is not None   # A/B of the sampler's own cost
         self.rows = []
         self.stop = threading.Event()
         self.h = None
@@ -97,14 +136,15 @@ class ClockSampler:
             time.sleep(self.period)
 
     def __enter__(self):
-        if self.h is not None and not self.off:
+        if self.h is not None:
+            self.stop.clear()
             self._sample()
             self.t = threading.Thread(target=self._loop, daemon=True)
             self.t.start()
         return self
 
     def __exit__(self, *exc):
-        if self.h is not None and not self.off:
+        if self.h is not None:
             self.stop.set()
             self.t.join()
 
@@ -116,12 +156,6 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def make_input(cfg: str, seed: int, nbytes: int | None = None):
-    from paper_1108_3126_b200 import rx
-
-    return rx.synth_pattern(cfg), rx.synth_input(cfg, nbytes, seed=seed)
-
-
 def count_units(text: np.ndarray, delim: int, stride: int) -> int:
     if delim == -2:
         return 1
@@ -131,14 +165,41 @@ def count_units(text: np.ndarray, delim: int, stride: int) -> int:
     return n + (1 if len(text) and text[-1] != delim else 0)
 
 
+def roofline(nbytes: int, words: int, kern_ms: float, traffic, cfg: str, dev: int) -> dict:
+    """t_roof = max(B / BW_HBM, B·W / INT32_peak); frac = t_roof / t."""
+    bw, bw_src = hbm_peak()
+    i32, i32_src, mix = int32_peak(dev)
+    t_hbm = nbytes / (bw * 1e9)
+    t_int = nbytes * words / (i32 * 1e12)
+    bound = "hbm" if t_hbm >= t_int else "int32"
+    t = kern_ms / 1e3
+    achieved_gbs = nbytes / t / 1e9
+    r = {
+        "bound": bound,
+        "achieved": achieved_gbs if bound == "hbm" else nbytes * words / t / 1e12,
+        "peak": bw if bound == "hbm" else i32,
+        "unit": "GB/s" if bound == "hbm" else "Tops/s (32-bit state-word updates, B*W)",
+        "frac": max(t_hbm, t_int) / t,
+        "traffic": traffic,
+        "traffic_source": (f"dram__bytes_read.sum+dram__bytes_write.sum per launch from an earlier ncu --set full "
+                           f"capture of config ({cfg}) (profiles/traffic.json), not measured in this run")
+        if traffic else None,
+        "algorithmic_bytes_per_launch": nbytes,
+        "state_words": words,
+        "hbm": {"achieved": achieved_gbs, "peak": bw, "frac": achieved_gbs / bw, "peak_source": bw_src},
+        "int32": {"t_roof_ms": t_int * 1e3, "peak_tops": i32, "peak_source": i32_src, "mix_tops": mix},
+        "model": "SURVEY.md 8(d): max(B/BW_HBM, B*W/INT32_peak); the memoized-step kernels do O(1) work per byte",
+    }
+    return r
+
+
 # ── CPU legs (reference library compiled from /root/reference sources) ─────
 
 def cpu_reference(cfg: str, pattern: str, text: np.ndarray, target_s: float = 12.0, threads: int | None = None):
     """Time rx::lockstep_accepts (oracle/_ref) on a bounded sample of the
-    workload with all host threads. Returns (GB/s, sample description, cores, kind)."""
+    workload with all host threads. Returns (GB/s, sample description, cores, kind, seconds)."""
     sys.path.insert(0, str(ROOT / "tests"))
     from oracle_bind import REF_SO, Oracle, RefHeap
-    from paper_1108_3126_b200 import rx
 
     threads = threads or os.cpu_count() or 1
     delim, stride, _ = CONFIGS[cfg]
@@ -146,6 +207,8 @@ def cpu_reference(cfg: str, pattern: str, text: np.ndarray, target_s: float = 12
     if kind == "reference":
         h = RefHeap(pattern.encode())
     else:
+        from paper_1108_3126_b200 import rx   # front end only: the port needs the heap table
+
         h = Oracle(rx.compile(rx.parse(pattern)))
 
     def run(sample: np.ndarray, nthreads: int):
@@ -155,7 +218,6 @@ def cpu_reference(cfg: str, pattern: str, text: np.ndarray, target_s: float = 12
             return time.perf_counter() - t0, int(ok)
         if kind == "reference":
             # decode_utf8 happens in ref_prepare; time only lockstep_accepts
-            import ctypes as C
             a = np.ascontiguousarray(sample)
             prep = h.l.ref_prepare(a.ctypes.data, a.nbytes, delim, stride)
             t0 = time.perf_counter()
@@ -190,30 +252,40 @@ def cpu_reference(cfg: str, pattern: str, text: np.ndarray, target_s: float = 12
     return len(sample) / dt / 1e9, desc, cores, kind, dt
 
 
+def cpu_record(cfg, pattern, text, target_s):
+    try:
+        gbs, sdesc, cores, kind, _ = cpu_reference(cfg, pattern, text, target_s=target_s)
+        return {"value": gbs, "unit": "GB/s", "cores": cores, "kind": kind, "sample": sdesc, "cpu_model": cpu_model()}
+    except Exception as e:  # noqa: BLE001 - the baseline is reported, never the product path
+        return {"value": None, "unit": "GB/s", "cores": None, "kind": None, "sample": f"unavailable: {e}",
+                "cpu_model": cpu_model()}
+
+
 # ── reference arm ──────────────────────────────────────────────────────────
 
 def run_reference_arm(args):
     """The reference's own CPU lockstep matcher (oracle/_ref = proj/src compiled
     from source) on a bounded sample of the same workload, all host threads.
-    The sample is sized once (~args.ref_step_s per step) and decoded once;
-    each step times rx::lockstep_accepts over all of its strings."""
+    The inputs come from the C restatement of the generators (oracle/), so
+    this arm never loads the product library. The sample is sized once
+    (~args.ref_step_s per step, so --steps 20 --warmup 5 ends in a few
+    minutes; the full (c) job takes ~60 s per pass on 16 cores) and decoded
+    once; each step times rx::lockstep_accepts over all of its strings."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     sys.path.insert(0, str(ROOT / "tests"))
-    from oracle_bind import REF_SO, Oracle, RefHeap
-    from paper_1108_3126_b200 import rx
+    import oracle_bind as ob
 
     cfg = args.config
     delim, stride, _ = CONFIGS[cfg]
-    pattern, text = make_input(cfg, 0)
+    pattern, text = ob.synth_pattern(cfg), ob.synth_input(cfg)
     threads = os.cpu_count() or 1
-    # size the sample with one calibration run of the shared helper
     _, desc, cores, kind, _ = cpu_reference(cfg, pattern, text, target_s=args.ref_step_s, threads=threads)
     nbytes = int(desc.split()[1])
     sample = text[:nbytes]
     if kind == "reference":
-        h = RefHeap(pattern.encode())
+        h = ob.RefHeap(pattern.encode())
         if delim == -2:
             w = sample.tobytes()
             run = lambda: h.accepts(w)  # noqa: E731
@@ -222,7 +294,9 @@ def run_reference_arm(args):
             prep = h.l.ref_prepare(a.ctypes.data, a.nbytes, delim, stride)
             run = lambda: h.l.ref_run(h.p, prep, None, cores)  # noqa: E731
     else:
-        o = Oracle(rx.compile(rx.parse(pattern)))
+        from paper_1108_3126_b200 import rx
+
+        o = ob.Oracle(rx.compile(rx.parse(pattern)))
         run = (lambda: o.accepts(sample.tobytes())) if delim == -2 else \
             (lambda: o.match_batch(sample, delim, stride, results=False, threads=cores))
     times = []
@@ -236,10 +310,12 @@ def run_reference_arm(args):
     line = {
         "metric": "input GB/s matched", "value": v, "unit": "GB/s", "impl": "reference", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": float(np.median(times)) * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "higher_is_better": True, "scaling": "strong" if delim != -2 else "weak", "vs_baseline": None,
+        "dtype": "u8", "data": "synthetic",
         "config": {"workload": f"config ({cfg}): {CONFIGS[cfg][2]}", "input_bytes": int(len(text)),
                    "sample_bytes": int(len(sample))},
-        "cpu_baseline": {"value": v, "unit": "GB/s", "cores": cores, "kind": kind, "sample": desc},
+        "cpu_baseline": {"value": v, "unit": "GB/s", "cores": cores, "kind": kind, "sample": desc,
+                         "cpu_model": cpu_model()},
         "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -247,6 +323,275 @@ def run_reference_arm(args):
 
 
 # ── B200 arm ───────────────────────────────────────────────────────────────
+
+class Ctx:
+    def __init__(self, args):
+        import torch
+        import torch.distributed as dist
+
+        self.torch, self.dist = torch, dist
+        self.args = args
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        if self.world > 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            torch.cuda.set_device(self.local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+        self.dev = self.local
+        torch.cuda.set_device(self.dev)
+        self.comm = None
+        if self.world > 1:
+            from paper_1108_3126_b200 import rx
+
+            uid = [rx.Comm.unique_id() if self.rank == 0 else None]
+            dist.broadcast_object_list(uid, src=0)
+            self.comm = rx.Comm(uid[0], self.world, self.rank, self.dev)
+        self.clk = ClockSampler(self.dev)
+
+    def barrier(self):
+        if self.world > 1:
+            self.dist.barrier()
+        self.torch.cuda.synchronize(self.dev)
+
+    def max_over_ranks(self, x: float) -> float:
+        if self.world == 1:
+            return x
+        t = self.torch.tensor([x], dtype=self.torch.float64, device=self.dev)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+
+def timed(ctx, step, steps: int, flush, clocks: bool):
+    """K steps on the device, events on the launching stream. Inputs larger
+    than L2: one interval around all K steps; otherwise L2 is flushed before
+    every step (outside the interval) and the intervals are summed.
+    Returns (ms per step on this rank, max over ranks)."""
+    torch = ctx.torch
+    stream = torch.cuda.current_stream(ctx.dev)
+    ctx.barrier()
+    # A device-side spin (outside the timed interval) holds the stream while the
+    # host enqueues the K steps, so first-call host latency never shows up as an
+    # idle gap inside an interval. Host costs per call are what e2e measures.
+    torch.cuda._sleep(int(2.0e6 * (0.3 + 0.02 * steps)))
+    if flush is None:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            step()
+        e1.record(stream)
+        ev = [(e0, e1)]
+    else:
+        ev = []
+        for _ in range(steps):
+            flush()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            step()
+            e1.record(stream)
+            ev.append((e0, e1))
+    if clocks:
+        with ctx.clk:
+            torch.cuda.synchronize(ctx.dev)
+    else:
+        torch.cuda.synchronize(ctx.dev)
+    total = float(sum(a.elapsed_time(b) for a, b in ev))
+    ctx.barrier()
+    return total / steps, ctx.max_over_ranks(total) / steps
+
+
+def make_flush(ctx, nbytes: int):
+    torch = ctx.torch
+    if nbytes >= 256 << 20:
+        return None, "inputs larger than L2 (126 MB)"
+    dirty = torch.empty(512 << 20, dtype=torch.uint8, device=ctx.dev)
+    clean = torch.ones(256 << 20, dtype=torch.uint8, device=ctx.dev)
+
+    def flush():
+        # write a buffer larger than L2, then read another one so the lines the
+        # timed kernel finds in L2 are clean (no write-back during the step)
+        dirty.zero_()
+        clean.sum(dtype=torch.int64)
+
+    return flush, "L2 flushed between timed steps (512 MiB write, then 256 MiB read)"
+
+
+def bench_batch(ctx, cfg: str, steps: int, warmup: int, headline: bool) -> dict:
+    """Strong scaling: the job is the config's whole buffer; rank r matches its shard."""
+    from paper_1108_3126_b200 import _lib, rx
+
+    torch = ctx.torch
+    delim, stride, desc = CONFIGS[cfg]
+    pattern, text = rx.synth_pattern(cfg), rx.synth_input(cfg, seed=0)
+    job_bytes = len(text)
+    bounds = rx.shard_bounds(text, ctx.world, delimiter=delim if delim >= 0 else -1, stride=stride)
+    lo, hi = rx.shard(text, ctx.world, ctx.rank, delimiter=delim if delim >= 0 else -1, stride=stride)
+    shard = text[lo:hi]
+    nb = len(shard)
+    m = rx.Matcher(pattern, device=ctx.dev)
+    if delim >= 0:   # planner: bank placement from the head of the JOB (identical tables on every rank)
+        m.tune(text[: 1 << 20], delimiter=delim)
+    info = m.info()
+    host = torch.from_numpy(shard).pin_memory()
+    d_text = torch.empty(nb + 64, dtype=torch.uint8, device=ctx.dev)
+    d_text[:nb].copy_(host)
+    d_count = torch.zeros(1, dtype=torch.int64, device=ctx.dev)
+    stream = torch.cuda.current_stream(ctx.dev)
+    flush, l2 = make_flush(ctx, nb)
+
+    def kernel_step():
+        m.match_batch_device(d_text, d_count, delimiter=delim, stride=stride, stream=stream, nbytes=nb)
+
+    def job_step():
+        if ctx.comm is None:
+            kernel_step()
+        else:
+            rx.match_batch_allreduce(m, ctx.comm, d_text, d_count, delimiter=delim, stride=stride, stream=stream,
+                                     nbytes=nb)
+
+    for _ in range(warmup):
+        job_step()
+    torch.cuda.synchronize(ctx.dev)
+    launches = _lib.lib().rxg_last_launch_count()
+    matches = int(d_count.item())   # the job's total (all-reduced when N > 1)
+    _, ms_step = timed(ctx, job_step, steps, flush, clocks=headline)
+    if ctx.world > 1:
+        for _ in range(2):
+            kernel_step()
+        kern_local, kern_max = timed(ctx, kernel_step, steps, flush, clocks=False)
+    else:
+        kern_local, kern_max = ms_step, ms_step
+    traffic = None
+    tf = ROOT / "profiles" / "traffic.json"
+    if tf.exists() and ctx.world == 1:
+        traffic = json.loads(tf.read_text()).get(cfg)
+    rec = {
+        "metric": "input GB/s matched",
+        "value": job_bytes / (ms_step / 1e3) / 1e9,
+        "unit": "GB/s",
+        "ms_per_step": ms_step,
+        "scaling": "strong",
+        "config": {
+            "workload": f"config ({cfg}): {desc}",
+            "pattern_nodes": info["nodes"], "positions": info["positions"], "words": info["words"],
+            "dfa_states": info["dfa_states"], "line_col_bytes": m.info()["line_col_bytes"],
+            "job_bytes": job_bytes, "job_strings": count_units(text, delim, stride),
+            "shard_bytes_rank0": int(bounds[1] - bounds[0]), "shards": [int(x) for x in bounds],
+            "matches": matches, "l2": l2,
+            "parallelism": f"dp{ctx.world} (string shards, count all-reduce over NCCL)" if ctx.world > 1 else "dp1",
+            "engine": "k2_lines" if delim >= 0 else "k2_fixed",
+        },
+        "roofline": roofline(nb, info["words"], kern_local, traffic, cfg, ctx.dev),
+        "gpu_launches": launches * steps,
+    }
+    if ctx.world > 1:
+        rec["spans"] = {"kernel_ms_per_step": kern_max, "kernel_plus_allreduce_ms_per_step": ms_step,
+                        "kernel_value": job_bytes / (kern_max / 1e3) / 1e9,
+                        "note": "max over ranks; kernel = this rank's shard only, no collective"}
+    # end to end through the C ABI with host buffers: this rank's shard, H2D
+    # inside the call (pipelined 64 MiB pieces), the count read back, then the
+    # 8-byte count all-reduce across ranks
+    if not ctx.args.no_e2e:
+        def e2e_time(buf):
+            m.match_batch(buf, delimiter=delim, stride=stride)   # warm
+            ctx.barrier()
+            k = max(1, steps // 2)
+            t0 = time.perf_counter()
+            for _ in range(k):
+                cnt, _ = m.match_batch(buf, delimiter=delim, stride=stride)
+                if ctx.world > 1:
+                    c = torch.tensor([cnt], dtype=torch.int64, device=ctx.dev)
+                    ctx.dist.all_reduce(c)
+                    c.item()
+            return ctx.max_over_ranks((time.perf_counter() - t0) / k)
+
+        t_pin = e2e_time(host.numpy())
+        t_page = e2e_time(shard)
+        rec["e2e"] = {"value": job_bytes / t_pin / 1e9, "unit": "GB/s", "h2d_bytes_per_step": nb,
+                      "d2h_bytes_per_step": 8, "host_buffer": "pinned",
+                      "pageable": {"value": job_bytes / t_page / 1e9, "unit": "GB/s"}}
+    if ctx.world > 1:   # secondary: weak scaling (every rank the whole job)
+        d_full = torch.empty(job_bytes + 64, dtype=torch.uint8, device=ctx.dev)
+        d_full[:job_bytes].copy_(torch.from_numpy(text))
+
+        def weak_step():
+            rx.match_batch_allreduce(m, ctx.comm, d_full, d_count, delimiter=delim, stride=stride, stream=stream,
+                                     nbytes=job_bytes)
+
+        for _ in range(2):
+            weak_step()
+        _, wms = timed(ctx, weak_step, steps, make_flush(ctx, job_bytes)[0], clocks=False)
+        rec["weak"] = {"value": ctx.world * job_bytes / (wms / 1e3) / 1e9, "unit": "GB/s", "ms_per_step": wms,
+                       "note": "every rank matches the whole job, count all-reduce"}
+        del d_full
+    if ctx.rank == 0 and ctx.world == 1 and not ctx.args.no_cpu:
+        rec["cpu_baseline"] = cpu_record(cfg, pattern, text, ctx.args.cpu_target_s if headline else ctx.args.sub_cpu_s)
+    return rec
+
+
+def bench_single(ctx, cfg: str, steps: int, warmup: int, headline: bool) -> dict:
+    """One long string (replicas only when N > 1)."""
+    from paper_1108_3126_b200 import _lib, rx
+
+    torch = ctx.torch
+    pattern, text = rx.synth_pattern(cfg), rx.synth_input(cfg, seed=0)
+    nb = len(text)
+    m = rx.Matcher(pattern, device=ctx.dev)
+    m.tune(text[: 1 << 20], delimiter=-1)
+    info = m.info()
+    host = torch.from_numpy(text).pin_memory()
+    d_text = torch.empty(nb + 64, dtype=torch.uint8, device=ctx.dev)
+    d_text[:nb].copy_(host)
+    d_acc = torch.zeros(1, dtype=torch.int32, device=ctx.dev)
+    stream = torch.cuda.current_stream(ctx.dev)
+    flush, l2 = make_flush(ctx, nb)
+    engine = ctx.args.engine
+
+    def step():
+        m.match_one_device(d_text[:nb], d_acc, engine=engine, stream=stream)
+
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize(ctx.dev)
+    launches = _lib.lib().rxg_last_launch_count()
+    accept = int(d_acc.item())
+    local, ms_step = timed(ctx, step, steps, flush, clocks=headline)
+    traffic = None
+    tf = ROOT / "profiles" / "traffic.json"
+    if tf.exists():
+        traffic = json.loads(tf.read_text()).get(cfg)
+    rec = {
+        "metric": "input GB/s matched",
+        "value": ctx.world * nb / (ms_step / 1e3) / 1e9,
+        "unit": "GB/s",
+        "ms_per_step": ms_step,
+        "scaling": "weak",
+        "config": {
+            "workload": f"config ({cfg}): {CONFIGS[cfg][2]}",
+            "pattern_nodes": info["nodes"], "positions": info["positions"], "words": info["words"],
+            "dfa_states": info["dfa_states"], "chunk_lookback": m.info()["chunk_lookback"], "input_bytes": nb,
+            "accept": accept, "l2": l2,
+            "parallelism": f"{ctx.world} replicas (one string is a sequential chain)" if ctx.world > 1 else "dp1",
+            "engine": engine,
+            "ns_per_symbol": ms_step * 1e6 / nb,
+        },
+        "roofline": roofline(nb, info["words"], local, traffic, cfg, ctx.dev),
+        "gpu_launches": launches * steps,
+    }
+    if not ctx.args.no_e2e:
+        w = host.numpy()
+        m.lockstep_accepts(w)   # warm
+        k = max(1, steps // 2)
+        t0 = time.perf_counter()
+        for _ in range(k):
+            m.lockstep_accepts(w)
+        t = ctx.max_over_ranks((time.perf_counter() - t0) / k)
+        rec["e2e"] = {"value": ctx.world * nb / t / 1e9, "unit": "GB/s", "h2d_bytes_per_step": nb,
+                      "d2h_bytes_per_step": 4, "host_buffer": "pinned"}
+    if ctx.rank == 0 and ctx.world == 1 and not ctx.args.no_cpu:
+        rec["cpu_baseline"] = cpu_record(cfg, pattern, text, ctx.args.cpu_target_s if headline else ctx.args.sub_cpu_s)
+    return rec
+
 
 def main():
     ap = argparse.ArgumentParser()
@@ -256,208 +601,65 @@ def main():
     ap.add_argument("--config", default="c", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--engine", default="auto")
-    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline legs")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-sub", action="store_true", help="headline config only (no sub-records)")
     ap.add_argument("--ref-step-s", type=float, default=8.0)
     ap.add_argument("--cpu-target-s", type=float, default=12.0)
+    ap.add_argument("--sub-cpu-s", type=float, default=6.0)
     args = ap.parse_args()
-    args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup
-
     if args.impl == "reference":
         return run_reference_arm(args)
+    args.warmup = max(args.warmup, 3)
 
-    import torch
-    import torch.distributed as dist
-
-    from paper_1108_3126_b200 import rx
-    from paper_1108_3126_b200 import _lib
-
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
-        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    dev = local
-    torch.cuda.set_device(dev)
+    ctx = Ctx(args)
     cfg = args.config
-    delim, stride, desc = CONFIGS[cfg]
-    single = delim == -2
 
-    pattern, text_np = make_input(cfg, seed=0 if rank == 0 else 1000 + rank)
-    nbytes = len(text_np)
-    units = count_units(text_np, delim, stride)
-    m = rx.Matcher(pattern, device=dev)
-    # planner: table bank placement from a 1 MiB sample (lines, or the single-string table)
-    if delim >= 0 or single:
-        m.tune(text_np[: 1 << 20], delimiter=delim if delim >= 0 else -1)
-    info = m.info()
+    def run(c, headline):
+        fn = bench_single if CONFIGS[c][0] == -2 else bench_batch
+        return fn(ctx, c, args.steps, args.warmup, headline)
 
-    host = torch.from_numpy(text_np).pin_memory()
-    d_text = torch.empty(nbytes + 64, dtype=torch.uint8, device=dev)
-    d_text[:nbytes].copy_(host, non_blocking=False)
-    d_count = torch.zeros(1, dtype=torch.int64, device=dev)
-    d_acc = torch.zeros(1, dtype=torch.int32, device=dev)
-    stream = torch.cuda.current_stream(dev)
-    l2_flush = None
-    if nbytes < 256 << 20:
-        l2_flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
-        l2_clean = torch.ones(256 << 20, dtype=torch.uint8, device=dev)
-
-    def flush_l2():
-        # write a buffer larger than L2, then read another one so the lines the
-        # timed kernel finds in L2 are clean (no write-back during the step)
-        l2_flush.zero_()
-        l2_clean.sum(dtype=torch.int64)
-
-    def step():
-        if single:
-            m.match_one_device(d_text[:nbytes], d_acc, engine=args.engine, stream=stream)
-        else:
-            m.match_batch_device(d_text, d_count, delimiter=delim, stride=stride, stream=stream, nbytes=nbytes)
-
-    clk = ClockSampler(dev)   # NVML initialised before the warm-up, not inside the timed region
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize(dev)
-    launches_per_step = _lib.lib().rxg_last_launch_count()
-
-    # parity of the timed configuration against the resident result
-    result = int(d_acc.item()) if single else int(d_count.item())
-
-    # Every timed step is enqueued first (L2 flush + events + step, no host
-    # sync in between), so no host-side stall (NVML sampling, launch latency)
-    # can open a gap inside a timed interval; the clock sampler runs while the
-    # queue drains. (Sampling during the enqueue measured +7 us/step on (e).)
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize(dev)
-    # A device-side spin (outside the timed interval) holds the stream while the
-    # host enqueues the K steps: the first call's host latency (measured 10-65 us
-    # in a fresh process) then never shows up as an idle gap between ev0 and the
-    # first kernel. Host costs per call are what e2e measures.
-    torch.cuda._sleep(int(2.0e6 * (0.3 + 0.02 * args.steps)))   # ~2 GHz: 0.3 ms + 20 us per step
-    if l2_flush is None:
-        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))]
-        dbg = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)] if os.environ.get("RXG_BENCH_STEPS") else None
-        ev[0][0].record(stream)
-        for i in range(args.steps):
-            step()
-            if world > 1:
-                dist.all_reduce(d_count)   # the match-count gather (8 bytes)
-            if dbg:
-                dbg[i].record(stream)
-        ev[0][1].record(stream)
-    else:
-        ev = []
-        for _ in range(args.steps):
-            flush_l2()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            step()
-            if world > 1:
-                dist.all_reduce(d_count)
-            e1.record(stream)
-            ev.append((e0, e1))
-    with clk:
-        torch.cuda.synchronize(dev)
-    if l2_flush is None:
-        total_ms = ev[0][0].elapsed_time(ev[0][1])
-        if dbg:
-            log("per-step us:", [round(a.elapsed_time(b) * 1e3, 1) for a, b in zip([ev[0][0]] + dbg[:-1], dbg)])
-        times = [total_ms / args.steps] * args.steps
-    else:
-        times = [e0.elapsed_time(e1) for e0, e1 in ev]
-        total_ms = float(sum(times))
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize(dev)
-
-    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms = float(t.item())
-    ms_per_step = total_ms / args.steps
-    total_bytes = nbytes * world
-    value = total_bytes / (ms_per_step / 1e3) / 1e9
-
-    # kernel-only roofline figure (1 rank's dominant kernel, events around the launch)
-    hbm, peak_src = peaks()
-    kern_ms = float(np.median(times)) if l2_flush is not None else ms_per_step
-    achieved = nbytes / (kern_ms / 1e3) / 1e9
-
-    # end-to-end through the C ABI with host buffers (H2D inside the timed region)
-    e2e = None
-    if not args.no_e2e:
-        host_np = host.numpy()
-        if single:
-            m.lockstep_accepts(host_np)   # warm
-            t0 = time.perf_counter()
-            for _ in range(max(1, args.steps // 2)):
-                m.lockstep_accepts(host_np)
-            e2e_s = (time.perf_counter() - t0) / max(1, args.steps // 2)
-            d2h = 4
-        else:
-            m.match_batch(host_np, delimiter=delim, stride=stride)
-            t0 = time.perf_counter()
-            for _ in range(max(1, args.steps // 2)):
-                cnt, _ = m.match_batch(host_np, delimiter=delim, stride=stride)
-            e2e_s = (time.perf_counter() - t0) / max(1, args.steps // 2)
-            d2h = 8
-        e2e_t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
-        e2e = {"value": total_bytes / float(e2e_t.item()) / 1e9, "unit": "GB/s", "h2d_bytes_per_step": nbytes,
-               "d2h_bytes_per_step": d2h}
-
-    traffic = None
-    tf = ROOT / "profiles" / "traffic.json"
-    if tf.exists():
-        traffic = json.loads(tf.read_text()).get(cfg)
-
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
-        try:
-            gbs, sdesc, cores, kind, _ = cpu_reference(cfg, pattern, text_np, target_s=args.cpu_target_s)
-            cpu = {"value": gbs, "unit": "GB/s", "cores": cores, "kind": kind, "sample": sdesc}
-        except Exception as e:  # the baseline is reported, never the product path
-            cpu = {"value": None, "unit": "GB/s", "cores": None, "kind": None, "sample": f"unavailable: {e}"}
-
-    if rank == 0:
+    rec = run(cfg, True)
+    subs = {}
+    if ctx.world == 1 and not args.no_sub:
+        for c in sorted(CONFIGS):
+            if c != cfg:
+                try:
+                    subs[c] = run(c, False)
+                except Exception as e:  # noqa: BLE001 - a failing sub-record must not hide the headline
+                    subs[c] = {"error": repr(e)}
+                ctx.torch.cuda.empty_cache()
+    if ctx.rank == 0:
         line = {
             "metric": "input GB/s matched",
-            "value": value,
+            "value": rec["value"],
             "unit": "GB/s",
-            "n_gpus": world,
+            "n_gpus": ctx.world,
             "steps": args.steps,
             "warmup": args.warmup,
-            "ms_per_step": ms_per_step,
+            "ms_per_step": rec["ms_per_step"],
             "higher_is_better": True,
-            "scaling": "weak",
+            "scaling": rec["scaling"],
             "vs_baseline": None,
             "dtype": "u8",
             "data": "synthetic",
-            "config": {
-                "workload": f"config ({cfg}): {desc}",
-                "pattern_nodes": info["nodes"], "positions": info["positions"], "words": info["words"],
-                "dfa_states": info["dfa_states"], "line_col_bytes": m.info()["line_col_bytes"], "chunk_lookback": m.info()["chunk_lookback"], "input_bytes_per_gpu": nbytes, "strings_per_gpu": units,
-                "matches_rank0": result,
-                "l2": "inputs larger than L2 (126 MB)" if l2_flush is None else "L2 flushed between timed steps (512 MiB write, then 256 MiB read)",
-                "parallelism": f"dp{world} (string shards, count all-reduce)" if world > 1 else "dp1",
-                "engine": args.engine if single else "k2_lines" if delim >= 0 else "k2_fixed",
-            },
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                         "frac": achieved / hbm, "traffic": traffic, "peak_source": peak_src,
-                         "algorithmic_bytes_per_launch": nbytes},
-            "cpu_baseline": cpu,
-            "e2e": e2e,
-            "gpu_launches": launches_per_step * args.steps,
-            "clocks": clk.summary(),
+            "config": rec["config"],
+            "roofline": rec["roofline"],
+            "cpu_baseline": rec.get("cpu_baseline"),
+            "e2e": rec.get("e2e"),
+            "gpu_launches": rec["gpu_launches"],
+            "clocks": ctx.clk.summary(),
         }
+        for k in ("spans", "weak"):
+            if k in rec:
+                line[k] = rec[k]
+        if subs:
+            line["configs"] = subs
         print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.destroy_process_group()
+    if ctx.comm is not None:
+        ctx.comm.close()
+    if ctx.world > 1:
+        ctx.dist.destroy_process_group()
     return 0
 
 

@@ -260,9 +260,47 @@ int rxg_utf8_check_host(int device, const uint8_t* text, uint64_t len, int32_t d
 int rxg_match_one_multi(const int* devices, int ndev, const char* pattern, size_t plen, const uint8_t* text,
                         uint64_t len, int32_t* accept, int32_t* resegments);
 
-/* Byte-balanced sharding of a host buffer over `ndev` GPUs (split at string
- * boundaries), one stream per device, and one NCCL all-reduce of the int64
- * match count across the devices (the only inter-GPU traffic). */
+/* ── several GPUs ────────────────────────────────────
+ * Strings are independent: a batch is cut into contiguous byte-balanced
+ * shards at string boundaries (rxg_shard_bounds), each GPU matches its shard,
+ * and one all-reduce of the 8-byte match count is the only inter-GPU
+ * traffic. The reference has no multi-device code (its data-parallel axis is
+ * crosscheck's job pool over independent cases, crosscheck.cpp:119-149). */
+
+/* One process per GPU (torchrun / MPI): a NCCL communicator over the ranks.
+ * Rank 0 makes the 128-byte id, the host plumbing broadcasts it, every rank
+ * calls rxg_comm_init_rank (collective: blocks until all ranks joined). */
+typedef struct rxg_comm rxg_comm;
+int rxg_comm_unique_id(uint8_t* id, size_t cap);
+int rxg_comm_init_rank(const uint8_t* id, size_t id_len, int nranks, int rank, int device, rxg_comm** out);
+void rxg_comm_destroy(rxg_comm* c);
+
+/* rxg_match_batch on this rank's shard, then ncclAllReduce(sum) of *d_count
+ * across the communicator, both enqueued on `stream`: when the stream reaches
+ * the end, d_count holds the whole job's match count on every rank. */
+int rxg_match_batch_allreduce(rxg_heap* h, rxg_comm* c, const uint8_t* d_text, uint64_t len,
+                              int32_t delimiter, uint32_t stride, unsigned long long* d_count,
+                              uint8_t* d_results, void* stream);
+
+/* One process, several GPUs: a persistent handle. The pattern is compiled and
+ * its memoized step built once, then uploaded to every device; one worker
+ * thread per device drives that device's pipelined host path (copy of piece
+ * k+1 overlapping the match of piece k); NCCL communicators (ncclCommInitAll)
+ * are created once. A device may be listed more than once (shards then share
+ * that GPU; NCCL needs distinct GPUs, so the counts are summed on the host). */
+typedef struct rxg_multi rxg_multi;
+int rxg_multi_create(const int* devices, int ndev, const char* pattern, size_t plen, rxg_multi** out);
+void rxg_multi_destroy(rxg_multi* m);
+int rxg_multi_info(const rxg_multi* m, int32_t* ndev, int32_t* uses_nccl);
+/* rxg_heap_tune for every device (sampled once). */
+int rxg_multi_tune(rxg_multi* m, const uint8_t* sample, uint64_t len, int32_t delimiter);
+/* Shard a host buffer over the handle's devices; *count = total matches
+ * (all-reduced over NCCL when the devices are distinct); results (nullable):
+ * one 0/1 byte per string, in order. Synchronous; one call at a time per handle. */
+int rxg_multi_match_batch(rxg_multi* m, const uint8_t* text, uint64_t len, int32_t delimiter,
+                          uint32_t stride, uint64_t* count, uint8_t* results);
+
+/* One-shot form of the above (handle created and destroyed inside the call). */
 int rxg_match_batch_multi(const int* devices, int ndev, const char* pattern, size_t plen,
                           const uint8_t* text, uint64_t len, int32_t delimiter, uint32_t stride,
                           uint64_t* count, uint8_t* results);

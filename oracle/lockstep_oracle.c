@@ -165,7 +165,7 @@ int oracle_lockstep_accepts(const oracle_heap* h, oracle_ws* ws, const uint32_t*
 }
 
 /* lockstep.cpp:77-80 from an arbitrary start set: S <- step_char(evolve(S), a)
- * for each byte, stopping early on the empty set. s_io holds the start set on
+ * for each byte (bytes are the symbols here: ASCII inputs only), stopping early on the empty set. s_io holds the start set on
  * entry (n_io entries, null allowed) and the final set on exit; capacity n+1.
  * Used to verify a long single-string run chunk by chunk from checkpoints
  * (SURVEY.md §8(c) parity plan item 2). */
@@ -188,14 +188,54 @@ int32_t oracle_walk_from(const oracle_heap* h, int32_t* s_io, int32_t n_io, cons
     return ns;
 }
 
+/* rx::decode_utf8 (proj/src/utf8.cpp:16-46): bytes -> Unicode scalars.
+ * Returns the number of scalars, or -1 where the reference throws
+ * std::runtime_error (malformed, truncated, overlong, surrogate, > U+10FFFF). */
+static int64_t decode_utf8(const uint8_t* s, uint64_t n, uint32_t* out) {
+    static const uint32_t min_for_len[5] = {0, 0, 0x80, 0x800, 0x10000};
+    uint64_t i = 0, k = 0;
+    while (i < n) {
+        const uint32_t b0 = s[i];
+        if (b0 < 0x80) {
+            out[k++] = b0;
+            ++i;
+            continue;
+        }
+        uint32_t len, cp;
+        if ((b0 & 0xE0) == 0xC0) { len = 2; cp = b0 & 0x1F; }
+        else if ((b0 & 0xF0) == 0xE0) { len = 3; cp = b0 & 0x0F; }
+        else if ((b0 & 0xF8) == 0xF0) { len = 4; cp = b0 & 0x07; }
+        else return -1;
+        if (i + len > n) return -1;
+        for (uint32_t j = 1; j < len; ++j) {
+            const uint32_t b = s[i + j];
+            if ((b & 0xC0) != 0x80) return -1;
+            cp = (cp << 6) | (b & 0x3F);
+        }
+        if (cp < min_for_len[len] || cp > 0x10FFFF || (cp >= 0xD800 && cp <= 0xDFFF)) return -1;
+        out[k++] = cp;
+        i += len;
+    }
+    return (int64_t)k;
+}
+
+/* One string as the `rxvm match` loop sees it (rxvm.cpp:85-87): decode_utf8,
+ * then lockstep_accepts. A string decode_utf8 rejects (the reference throws)
+ * counts as no match, the product's documented behaviour (include/rxg.h). */
+static int accepts_utf8(const oracle_heap* h, oracle_ws* ws, const uint8_t* bytes, uint64_t len, uint32_t* w,
+                        int32_t* a, int32_t* b) {
+    const int64_t ns = decode_utf8(bytes, len, w);
+    if (ns < 0) return 0;
+    return oracle_lockstep_accepts(h, ws, w, (uint64_t)ns, a, b, NULL);
+}
+
 int oracle_accepts_bytes(const oracle_heap* h, const uint8_t* bytes, uint64_t len) {
     oracle_ws ws;
     oracle_ws_init(&ws, h->n);
     int32_t* a = (int32_t*)malloc((size_t)(h->n + 1) * sizeof(int32_t));
     int32_t* b = (int32_t*)malloc((size_t)(h->n + 1) * sizeof(int32_t));
     uint32_t* w = (uint32_t*)malloc((len ? len : 1) * sizeof(uint32_t));
-    for (uint64_t i = 0; i < len; ++i) w[i] = bytes[i];
-    const int r = oracle_lockstep_accepts(h, &ws, w, len, a, b, NULL);
+    const int r = accepts_utf8(h, &ws, bytes, len, w, a, b);
     free(w);
     free(a);
     free(b);
@@ -231,9 +271,7 @@ static void* run_job(void* arg) {
             cap = len * 2;
             w = (uint32_t*)realloc(w, cap * sizeof(uint32_t));
         }
-        const uint8_t* src = j->text + j->starts[k];
-        for (uint64_t i = 0; i < len; ++i) w[i] = src[i];
-        const int r = oracle_lockstep_accepts(j->h, &ws, w, len, a, b, NULL);
+        const int r = accepts_utf8(j->h, &ws, j->text + j->starts[k], len, w, a, b);
         if (j->results) j->results[k] = (uint8_t)r;
         j->count += (uint64_t)r;
     }

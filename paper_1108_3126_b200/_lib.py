@@ -85,6 +85,15 @@ _SIG = {
     "rxg_utf8_check_host": (C.c_int, [C.c_int, _P, C.c_uint64, C.c_int32, C.c_uint32, C.POINTER(C.c_uint64)]),
     "rxg_match_batch_multi": (C.c_int, [C.POINTER(C.c_int), C.c_int, C.c_char_p, C.c_size_t, _P, C.c_uint64,
                                         C.c_int32, C.c_uint32, C.POINTER(C.c_uint64), _P]),
+    "rxg_comm_unique_id": (C.c_int, [_P, C.c_size_t]),
+    "rxg_comm_init_rank": (C.c_int, [_P, C.c_size_t, C.c_int, C.c_int, C.c_int, C.POINTER(_P)]),
+    "rxg_comm_destroy": (None, [_P]),
+    "rxg_match_batch_allreduce": (C.c_int, [_P, _P, _P, C.c_uint64, C.c_int32, C.c_uint32, _P, _P, _P]),
+    "rxg_multi_create": (C.c_int, [C.POINTER(C.c_int), C.c_int, C.c_char_p, C.c_size_t, C.POINTER(_P)]),
+    "rxg_multi_destroy": (None, [_P]),
+    "rxg_multi_info": (C.c_int, [_P, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
+    "rxg_multi_tune": (C.c_int, [_P, _P, C.c_uint64, C.c_int32]),
+    "rxg_multi_match_batch": (C.c_int, [_P, _P, C.c_uint64, C.c_int32, C.c_uint32, C.POINTER(C.c_uint64), _P]),
     "rxg_match_many": (C.c_int, [C.c_int, C.c_char_p, C.c_int32, _P, C.c_uint64, C.c_int32, C.c_uint32, _P,
                                  C.POINTER(C.c_uint64), C.POINTER(C.c_int32)]),
     "rxg_match_one_multi": (C.c_int, [C.POINTER(C.c_int), C.c_int, C.c_char_p, C.c_size_t, _P, C.c_uint64,

@@ -19,7 +19,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-Wall", f"-I{ROOT / 'include'}", f"-I{CSRC}"]
 SOURCES = ["frontend.cpp", "program.cpp", "tables.cpp", "lines_tma_table.cpp", "synth.cpp",
            "kernels_batch.cu", "kernels_lines_tma.cu", "kernels_single.cu", "kernels_pernode.cu", "kernels_chunked.cu", "kernels_chunk_tma.cu", "kernels_many.cu", "kernels_utf8.cu", "kernels_fixed_tma.cu",
-           "capi.cu"]
+           "capi.cu", "multi.cu"]
 
 
 def nvcc():
@@ -66,6 +66,12 @@ def build(verbose: bool = False, force: bool = False) -> Path:
     if force or not CLI.exists() or cli_src.stat().st_mtime > CLI.stat().st_mtime or OUT.stat().st_mtime > CLI.stat().st_mtime:
         subprocess.run(["g++", "-std=c++17", "-O2", f"-I{ROOT / 'include'}", str(cli_src), f"-L{PKG}", "-lrxg",
                         "-Wl,-rpath,$ORIGIN", "-o", str(CLI)], check=True)
+    # measurement tool (not product): the INT32 peak of SURVEY.md §8(d)'s roofline
+    peak_src = ROOT / "tools" / "peaks" / "int32_peak.cu"
+    peak_so = ROOT / "tools" / "peaks" / "libint32peak.so"
+    if force or not peak_so.exists() or peak_src.stat().st_mtime > peak_so.stat().st_mtime:
+        subprocess.run([nvcc(), "-O3", "-lineinfo"] + ARCH + ["-Xcompiler", "-fPIC", "-shared", "-o", str(peak_so),
+                        str(peak_src)], check=True)
     return OUT
 
 

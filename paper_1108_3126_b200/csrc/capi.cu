@@ -1,9 +1,7 @@
 // extern "C" boundary (include/rxg.h). Host C++ around the kernels: handle
 // lifetime, lazy per-delimiter table images, stream-ordered scratch, the
-// pipelined host-buffer path and the multi-GPU sharder.
-#include <dlfcn.h>
-#include <nccl.h>
-
+// pipelined host-buffer path and the single string split over devices
+// (the batch sharder and communicators are in multi.cu).
 #include <algorithm>
 #include <cstring>
 #include <map>
@@ -24,13 +22,22 @@
 #include "many.hpp"
 #include "synth.hpp"
 #include "tables.hpp"
+#include "heap_internal.hpp"
 
 using namespace rxg;
+using rxg::detail::DeviceGuard;
+using rxg::detail::cuda_fail;
+using rxg::detail::fail;
 
 namespace {
 
 thread_local std::string g_err;
 thread_local int g_launches = 0;
+
+}  // namespace
+
+namespace rxg {
+namespace detail {
 
 int fail(int code, const std::string& msg) {
     g_err = msg;
@@ -41,95 +48,37 @@ int cuda_fail(cudaError_t e, const char* where) {
     return fail(RXG_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
 }
 
+void set_launches(int n) { g_launches = n; }
+int launches() { return g_launches; }
+
+}  // namespace detail
+}  // namespace rxg
+
 #define RXG_CUDA(call)                                  \
     do {                                                \
         cudaError_t e_ = (call);                        \
         if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
     } while (0)
 
-struct DeviceGuard {
-    int prev = -1;
-    explicit DeviceGuard(int dev) {
-        if (dev >= 0 && cudaGetDevice(&prev) == cudaSuccess && prev != dev) cudaSetDevice(dev);
-        else prev = -1;
-    }
-    ~DeviceGuard() {
-        if (prev >= 0) cudaSetDevice(prev);
-    }
-};
-
-struct TableSlot {
-    KTable host;
-    DevTable dev;
-    void* dptr = nullptr;
-    LtTable lt;   // TMA line layout (delimited slots only; lt.ok false if it does not fit)
-    DevTable abs;  // plain slot: entries rebased to absolute shared addresses (fixed-stride kernel)
-    void* d_abs = nullptr;
-    LtTable chunk_lt;   // plain slot: TMA chunk-parallel layout (chunk_lt.ok false if it does not fit)
-    void* d_chunk = nullptr;
-};
-
-constexpr int32_t kMaxDfaStates = 16384;
-
-}  // namespace
-
-struct rxg_heap {
-    int device = -1;
-    Program prog;
-    bool dfa_ok = false;
-    int32_t dfa_sets = 0;   // states before minimisation
-    uint32_t lookback = 64; // chunk engine lookback (rxg_heap_tune with delimiter -1 shortens it)
-    Dfa dfa;
-    int smem_limit = 0;
-    std::mutex mu;
-    std::mutex host_mu;   // host-buffer calls share the staging buffers and streams
-    std::unique_ptr<TableSlot> plain;
-    std::map<int, std::unique_ptr<TableSlot>> lines;
-    std::map<int, std::vector<double>> line_freq;   // sampled state x byte counts per delimiter (rxg_heap_tune)
-    // staging for host-buffer calls
-    uint8_t* d_stage[2] = {nullptr, nullptr};
-    size_t stage_bytes = 0;
-    unsigned long long* d_count = nullptr;
-    int32_t* d_accept = nullptr;
-    cudaStream_t stream = nullptr;
-    cudaStream_t copy_stream = nullptr;
-    // lazily built tables of the thread-per-node engines
-    void* d_rounds = nullptr;
-    RoundsTables rounds;
-    void* d_pernode = nullptr;
-    PernodeTables pernode;
-    // CountSlot per stream (launch.hpp): zero when idle, re-zeroed by the kernels
-    std::map<cudaStream_t, unsigned long long*> slots;
-    // per stream: the chunked engine's seam arrival counters (zero when idle), grow-only
-    std::map<cudaStream_t, std::pair<unsigned int*, size_t>> seams;
-    // per stream: the chunked engine's scratch (guesses, exits, checkpoints), grow-only
-    // (a stream-ordered malloc/free pair per call measured +2-3 us per launch on (e))
-    std::map<cudaStream_t, std::pair<void*, size_t>> scratch;
-
-    ~rxg_heap() {
-        if (device < 0) return;
-        DeviceGuard g(device);
-        for (auto& kv : slots) cudaFree(kv.second);
-        for (auto& kv : seams) cudaFree(kv.second.first);
-        for (auto& kv : scratch) cudaFree(kv.second.first);
-        if (plain && plain->dptr) cudaFree(plain->dptr);
-        if (plain && plain->d_abs) cudaFree(plain->d_abs);
-        if (plain && plain->d_chunk) cudaFree(plain->d_chunk);
-        for (auto& kv : lines) {
-            if (kv.second->dptr) cudaFree(kv.second->dptr);
-            if (kv.second->lt.d_lo) cudaFree(kv.second->lt.d_lo);
-            if (kv.second->lt.d_hi) cudaFree(kv.second->lt.d_hi);
-        }
-        for (auto* p : d_stage)
-            if (p) cudaFree(p);
-        if (d_count) cudaFree(d_count);
-        if (d_accept) cudaFree(d_accept);
-        if (stream) cudaStreamDestroy(stream);
-        if (copy_stream) cudaStreamDestroy(copy_stream);
-        if (d_rounds) cudaFree(d_rounds);
-        if (d_pernode) cudaFree(d_pernode);
-    }
-};
+rxg_heap::~rxg_heap() {
+    if (device < 0) return;
+    DeviceGuard g(device);
+    for (auto& kv : slots) cudaFree(kv.second);
+    for (auto& kv : seams) cudaFree(kv.second.first);
+    for (auto& kv : scratch) cudaFree(kv.second.first);
+    if (plain && plain->dev.img) cudaFree(const_cast<void*>(plain->dev.img));
+    for (auto& kv : lines)
+        if (kv.second->dev.img) cudaFree(const_cast<void*>(kv.second->dev.img));
+    for (void* p : allocs) cudaFree(p);
+    for (auto* p : d_stage)
+        if (p) cudaFree(p);
+    if (d_count) cudaFree(d_count);
+    if (d_accept) cudaFree(d_accept);
+    if (stream) cudaStreamDestroy(stream);
+    if (copy_stream) cudaStreamDestroy(copy_stream);
+    if (d_rounds) cudaFree(d_rounds);
+    if (d_pernode) cudaFree(d_pernode);
+}
 
 namespace {
 
@@ -147,11 +96,12 @@ int upload(rxg_heap* h, std::unique_ptr<TableSlot>& slot, KTable&& kt) {
                                      " B of shared memory, limit " + std::to_string(h->smem_limit));
     auto s = std::make_unique<TableSlot>();
     s->host = std::move(kt);
-    RXG_CUDA(cudaMalloc(&s->dptr, s->host.img.size()));
-    RXG_CUDA(h2d(s->dptr, s->host.img.data(), s->host.img.size()));
+    void* dptr = nullptr;
+    RXG_CUDA(cudaMalloc(&dptr, s->host.img.size()));
     DevTable& d = s->dev;
+    d.img = dptr;   // freed by ~rxg_heap
+    RXG_CUDA(h2d(dptr, s->host.img.data(), s->host.img.size()));
     const KTable& k = s->host;
-    d.img = s->dptr;
     d.img_bytes = static_cast<uint32_t>(k.img.size());
     d.cls = k.cls;
     d.esize = k.esize;
@@ -177,50 +127,60 @@ int ensure_cuda(int device) {
     return RXG_OK;
 }
 
-int need_device(rxg_heap* h, bool dfa = true) {
-    if (!h) return fail(RXG_EINVAL, "null heap");
-    if (h->device < 0) return fail(RXG_ENODEV, "host-only heap handle");
-    if (!h->prog.byte_symbols)
-        return fail(RXG_EUNSUPPORTED, "pattern has a literal that is not a Unicode scalar value");
-    if (dfa && !h->dfa_ok)
-        return fail(RXG_ETOOBIG, "memoized step table exceeds " + std::to_string(kMaxDfaStates) + " states");
+// Per-stream state is keyed by the stream's unique id, not the handle value:
+// cudaStreamPerThread (and the legacy NULL stream under per-thread default
+// streams) name a different stream in every thread.
+unsigned long long stream_key(cudaStream_t st) {
+    unsigned long long id = 0;
+    if (cudaStreamGetId(st, &id) != cudaSuccess) {
+        cudaGetLastError();
+        id = static_cast<unsigned long long>(reinterpret_cast<uintptr_t>(st)) | (1ull << 63);
+    }
+    return id;
+}
+
+// Allocating per-stream state inside a CUDA-graph capture would tie it to the
+// graph; the first call (or a growing one) must happen outside capture.
+int refuse_if_capturing(cudaStream_t st, const char* what) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone)
+        return fail(RXG_EINVAL, std::string(what) + " must be allocated outside CUDA-graph capture: make the first "
+                                                    "call of this size on this stream before capturing");
     return RXG_OK;
 }
 
 // The completion slot of `st` (allocated and zeroed on its first use, in
 // stream order).
 int stream_slot(rxg_heap* h, cudaStream_t st, CountSlot* out, bool accumulate) {
-    unsigned long long* p = nullptr;
-    {
-        std::lock_guard<std::mutex> lk(h->mu);
-        auto it = h->slots.find(st);
-        if (it != h->slots.end()) p = it->second;
-    }
+    const unsigned long long key = stream_key(st);
+    std::lock_guard<std::mutex> lk(h->mu);
+    auto it = h->slots.find(key);
+    unsigned long long* p = it != h->slots.end() ? it->second : nullptr;
     if (!p) {
+        if (int rc = refuse_if_capturing(st, "the per-stream completion slot")) return rc;
         RXG_CUDA(cudaMalloc(&p, 4 * sizeof(unsigned long long)));
         RXG_CUDA(cudaMemsetAsync(p, 0, 4 * sizeof(unsigned long long), st));
-        std::lock_guard<std::mutex> lk(h->mu);
-        auto ins = h->slots.emplace(st, p);
-        if (!ins.second) {   // another thread won the race for this stream
-            cudaFree(p);
-            p = ins.first->second;
-        }
+        h->slots.emplace(key, p);
     }
     out->p = p;
     out->accumulate = accumulate;
     return RXG_OK;
 }
 
-// Zeroed counters for `n` seams on stream st (kept per stream; the kernel re-zeroes them).
+// Zeroed counters for `n` seams on stream st (kept per stream; the kernel
+// re-zeroes them). A smaller buffer that is outgrown is retired, not freed:
+// a graph captured earlier may still point at it.
 int seam_counters(rxg_heap* h, cudaStream_t st, size_t n, unsigned int** out) {
+    const unsigned long long key = stream_key(st);
     std::lock_guard<std::mutex> lk(h->mu);
-    auto& e = h->seams[st];
+    auto& e = h->seams[key];
     if (e.second < n) {
-        if (e.first) RXG_CUDA(cudaFreeAsync(e.first, st));
+        if (int rc = refuse_if_capturing(st, "the chunked engine's seam counters")) return rc;
+        if (e.first) h->allocs.push_back(e.first);
         e.first = nullptr;
         e.second = 0;
         const size_t cap = std::max<size_t>(n, 4096);
-        RXG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&e.first), cap * sizeof(unsigned int), st));
+        RXG_CUDA(cudaMalloc(reinterpret_cast<void**>(&e.first), cap * sizeof(unsigned int)));
         RXG_CUDA(cudaMemsetAsync(e.first, 0, cap * sizeof(unsigned int), st));
         e.second = cap;
     }
@@ -228,15 +188,18 @@ int seam_counters(rxg_heap* h, cudaStream_t st, size_t n, unsigned int** out) {
     return RXG_OK;
 }
 
-// Scratch of at least `bytes` for launches on stream st (stream-ordered reuse).
+// Scratch of at least `bytes` for launches on stream st (stream-ordered reuse;
+// outgrown buffers are retired until the heap is destroyed).
 int stream_scratch(rxg_heap* h, cudaStream_t st, size_t bytes, void** out) {
+    const unsigned long long key = stream_key(st);
     std::lock_guard<std::mutex> lk(h->mu);
-    auto& e = h->scratch[st];
+    auto& e = h->scratch[key];
     if (e.second < bytes) {
-        if (e.first) RXG_CUDA(cudaFreeAsync(e.first, st));
+        if (int rc = refuse_if_capturing(st, "the chunked engine's scratch")) return rc;
+        if (e.first) h->allocs.push_back(e.first);
         e.first = nullptr;
         e.second = 0;
-        RXG_CUDA(cudaMallocAsync(&e.first, bytes, st));
+        RXG_CUDA(cudaMalloc(&e.first, bytes));
         e.second = bytes;
     }
     *out = e.first;
@@ -316,25 +279,29 @@ int pernode_tables(rxg_heap* h, const PernodeTables** out) {
     return RXG_OK;
 }
 
-// (Re)build the TMA chunk-parallel table of the plain slot (caller holds h->mu).
+// (Re)build and publish the TMA chunk-parallel table of the plain slot
+// (caller holds h->mu; the previous image stays allocated, see ChunkImage).
 int build_chunk_lt(rxg_heap* h) {
     auto f = h->line_freq.find(-1);
-    LtTable lt = make_chunk_tma_table(h->prog, h->dfa, f == h->line_freq.end() ? nullptr : &f->second);
-    void* d = nullptr;
+    auto img = std::make_shared<ChunkImage>();
+    img->lt = make_chunk_tma_table(h->prog, h->dfa, f == h->line_freq.end() ? nullptr : &f->second);
+    LtTable& lt = img->lt;
     const int ring = (lt.packed ? 193 : 145) * 1024;   // stage ring + barriers of the kernel's shape
-    if (lt.ok && static_cast<int>(lt.smem_table_end - kLtSmemBase) + ring <= h->smem_limit) {
+    if (h->tma_ok && lt.ok && static_cast<int>(lt.smem_table_end - kLtSmemBase) + ring <= h->smem_limit) {
+        void* d = nullptr;
         RXG_CUDA(cudaMalloc(&d, lt.lo.size()));
+        h->allocs.push_back(d);
         RXG_CUDA(h2d(d, lt.lo.data(), lt.lo.size()));
+        img->d = d;
     } else {
         lt.ok = false;
     }
-    if (h->plain->d_chunk) cudaFree(h->plain->d_chunk);
-    h->plain->d_chunk = d;
-    h->plain->chunk_lt = std::move(lt);
+    h->plain->chunk = std::move(img);
     return RXG_OK;
 }
 
-int plain_table(rxg_heap* h, const DevTable** out, const DevTable** abs_out = nullptr) {
+int plain_table(rxg_heap* h, const DevTable** out, const DevTable** abs_out = nullptr,
+                std::shared_ptr<const ChunkImage>* chunk_out = nullptr) {
     std::lock_guard<std::mutex> lk(h->mu);
     if (!h->plain) {
         const int rc = upload(h, h->plain, make_plain_table(h->prog, h->dfa));
@@ -342,7 +309,7 @@ int plain_table(rxg_heap* h, const DevTable** out, const DevTable** abs_out = nu
         const KTable& k = h->plain->host;
         // rebased copy for k_fixed_abs: raw-byte u16 rows whose entries are
         // absolute shared addresses (the dynamic window starts at 0x400)
-        if (!k.cls && k.esize == 2 && k.img.size() + 0x400 < 0x10000) {
+        if (h->tma_ok && !k.cls && k.esize == 2 && k.img.size() + 0x400 < 0x10000) {
             std::vector<uint8_t> img = k.img;
             for (uint32_t r = 0; r < static_cast<uint32_t>(k.n_states); ++r)
                 for (uint32_t c = 0; c < static_cast<uint32_t>(k.ncols); ++c) {
@@ -351,38 +318,44 @@ int plain_table(rxg_heap* h, const DevTable** out, const DevTable** abs_out = nu
                     v = static_cast<uint16_t>(v + 0x400);
                     std::memcpy(&img[r * k.row_bytes + c * 2u], &v, 2);
                 }
-            RXG_CUDA(cudaMalloc(&h->plain->d_abs, img.size()));
-            RXG_CUDA(h2d(h->plain->d_abs, img.data(), img.size()));
+            void* d_abs = nullptr;
+            RXG_CUDA(cudaMalloc(&d_abs, img.size()));
+            h->allocs.push_back(d_abs);
+            RXG_CUDA(h2d(d_abs, img.data(), img.size()));
             h->plain->abs = h->plain->dev;
-            h->plain->abs.img = h->plain->d_abs;
+            h->plain->abs.img = d_abs;
+            h->plain->has_abs = true;
         }
         if (int rc = build_chunk_lt(h)) return rc;
     }
     *out = &h->plain->dev;
-    if (abs_out) *abs_out = h->plain->d_abs ? &h->plain->abs : nullptr;
+    if (abs_out) *abs_out = h->plain->has_abs ? &h->plain->abs : nullptr;
+    if (chunk_out) *chunk_out = h->plain->chunk;
     return RXG_OK;
 }
 
-// (Re)build and upload the TMA line layout for `delim` (caller holds h->mu).
-int build_lt(rxg_heap* h, int delim, LtTable& out) {
+// (Re)build, upload and publish the TMA line layout for `delim` (caller
+// holds h->mu; the previous image stays allocated until the heap dies).
+int build_lt(rxg_heap* h, int delim, std::shared_ptr<const LtTable>& out) {
     auto f = h->line_freq.find(delim);
-    LtTable lt = make_lines_tma_table(h->prog, h->dfa, static_cast<uint8_t>(delim),
-                                      f == h->line_freq.end() ? nullptr : &f->second);
-    if (lt.ok && static_cast<int>(lt.smem_table_end - kLtSmemBase) + 64 * 1024 <= h->smem_limit) {
-        RXG_CUDA(cudaMalloc(&lt.d_lo, lt.lo.size()));
-        RXG_CUDA(cudaMalloc(&lt.d_hi, lt.hi.size()));
-        RXG_CUDA(h2d(lt.d_lo, lt.lo.data(), lt.lo.size()));
-        RXG_CUDA(h2d(lt.d_hi, lt.hi.data(), lt.hi.size()));
+    auto lt = std::make_shared<LtTable>(make_lines_tma_table(h->prog, h->dfa, static_cast<uint8_t>(delim),
+                                                             f == h->line_freq.end() ? nullptr : &f->second));
+    if (h->tma_ok && lt->ok && static_cast<int>(lt->smem_table_end - kLtSmemBase) + 64 * 1024 <= h->smem_limit) {
+        RXG_CUDA(cudaMalloc(&lt->d_lo, lt->lo.size()));
+        h->allocs.push_back(lt->d_lo);
+        RXG_CUDA(cudaMalloc(&lt->d_hi, lt->hi.size()));
+        h->allocs.push_back(lt->d_hi);
+        RXG_CUDA(h2d(lt->d_lo, lt->lo.data(), lt->lo.size()));
+        RXG_CUDA(h2d(lt->d_hi, lt->hi.data(), lt->hi.size()));
     } else {
-        lt.ok = false;
+        lt->ok = false;
     }
-    if (out.d_lo) cudaFree(out.d_lo);
-    if (out.d_hi) cudaFree(out.d_hi);
     out = std::move(lt);
     return RXG_OK;
 }
 
-int line_table(rxg_heap* h, int delim, TableSlot** out) {
+// The slot for `delim` and a snapshot of its TMA line image (nullable).
+int line_table(rxg_heap* h, int delim, TableSlot** out, std::shared_ptr<const LtTable>* lt_out = nullptr) {
     std::lock_guard<std::mutex> lk(h->mu);
     auto it = h->lines.find(delim);
     if (it == h->lines.end()) {
@@ -395,6 +368,7 @@ int line_table(rxg_heap* h, int delim, TableSlot** out) {
         it = h->lines.emplace(delim, std::move(slot)).first;
     }
     *out = it->second.get();
+    if (lt_out) *lt_out = it->second->lt;
     return RXG_OK;
 }
 
@@ -411,12 +385,9 @@ Heap heap_from_c(const rxg_node* nodes, const int32_t* knodes, int32_t n) {
     return h;
 }
 
-int make_heap(Heap&& hp, int device, rxg_heap** out) {
-    auto h = std::make_unique<rxg_heap>();
+// Device side of a new handle: streams, counters, shared-memory limits.
+int init_device(rxg_heap* h, int device) {
     h->device = device;
-    h->prog = build_program(hp);
-    h->dfa_ok = build_dfa(h->prog, kMaxDfaStates, h->dfa);
-    if (h->dfa_ok) h->dfa_sets = minimize_dfa(h->dfa);
     if (device >= 0) {
         DeviceGuard g(device);
         int ndev = 0;
@@ -424,6 +395,12 @@ int make_heap(Heap&& hp, int device, rxg_heap** out) {
             return fail(RXG_ECUDA, "no CUDA device " + std::to_string(device));
         RXG_CUDA(cudaSetDevice(device));
         RXG_CUDA(cudaDeviceGetAttribute(&h->smem_limit, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+        // The TMA layouts hold absolute shared addresses and assume the dynamic
+        // window starts at 0x400 (1 KB reserved per block); elsewhere use the
+        // generic kernels instead of trapping at launch.
+        int reserved = 0;
+        RXG_CUDA(cudaDeviceGetAttribute(&reserved, cudaDevAttrReservedSharedMemoryPerBlock, device));
+        h->tma_ok = reserved == static_cast<int>(kLtSmemBase);
         RXG_CUDA(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
         RXG_CUDA(cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking));
         RXG_CUDA(cudaMalloc(&h->d_count, sizeof(unsigned long long)));
@@ -436,7 +413,36 @@ int make_heap(Heap&& hp, int device, rxg_heap** out) {
             cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
         }
     }
+    return RXG_OK;
+}
+
+int make_heap(Heap&& hp, int device, rxg_heap** out) {
+    auto h = std::make_unique<rxg_heap>();
+    h->prog = build_program(hp);
+    h->dfa_ok = build_dfa(h->prog, kMaxDfaStates, h->dfa);
+    if (h->dfa_ok) h->dfa_sets = minimize_dfa(h->dfa);
+    if (int rc = init_device(h.get(), device)) return rc;
     *out = h.release();
+    return RXG_OK;
+}
+
+// Install sampled placement for `delimiter` (-1: the single-string table and
+// its lookback) and rebuild the affected device tables (caller holds h->mu).
+int apply_tuning(rxg_heap* h, int32_t delimiter, std::vector<double> freq, uint32_t lookback) {
+    h->line_freq[delimiter] = std::move(freq);
+    if (delimiter < 0) {
+        h->lookback = lookback;
+        if (h->plain && h->device >= 0) {
+            DeviceGuard g(h->device);
+            return build_chunk_lt(h);
+        }
+        return RXG_OK;
+    }
+    auto it = h->lines.find(delimiter);
+    if (it != h->lines.end() && it->second->lt && it->second->lt->ok && h->device >= 0) {
+        DeviceGuard g(h->device);
+        return build_lt(h, delimiter, it->second->lt);
+    }
     return RXG_OK;
 }
 
@@ -466,21 +472,23 @@ int batch_device(rxg_heap* h, const uint8_t* d_text, uint64_t len, int32_t delim
         if (delimiter > 255) return fail(RXG_EINVAL, "delimiter must be a byte");
         if (reinterpret_cast<uintptr_t>(d_text) & 15) return fail(RXG_EINVAL, "text must be 16-byte aligned");
         TableSlot* slot = nullptr;
-        if (int rc = line_table(h, delimiter, &slot)) return rc;
-        if (slot->lt.ok && !std::getenv("RXG_NO_LT")) {   // RXG_NO_LT: generic kernel (tests)
+        std::shared_ptr<const LtTable> lt;
+        if (int rc = line_table(h, delimiter, &slot, &lt)) return rc;
+        static const bool no_lt = std::getenv("RXG_NO_LT") != nullptr;   // generic kernel (tests)
+        if (lt && lt->ok && !no_lt) {
             uint32_t chunk = env_chunk();
             if (chunk % lines_tma_slice()) chunk = 0;
             if (!d_results) {
-                const cudaError_t e = launch_lines_tma(slot->lt, d_text, len, static_cast<uint8_t>(delimiter), chunk,
+                const cudaError_t e = launch_lines_tma(*lt, d_text, len, static_cast<uint8_t>(delimiter), chunk,
                                                        d_count, cs, st);
                 if (e != cudaSuccess) return cuda_fail(e, "launch_lines_tma");
                 ls.kernels = 1;
             } else if (len) {   // per-line results: range delimiter counts, scan, the same walk
-                chunk = lines_tma_chunk(slot->lt, len, chunk);
+                chunk = lines_tma_chunk(*lt, len, chunk);
                 const size_t sb = lines_tma_results_scratch(len, chunk);
                 void* scratch = nullptr;
                 RXG_CUDA(cudaMallocAsync(&scratch, sb, st));
-                const cudaError_t e = launch_lines_tma_results(slot->lt, d_text, len, static_cast<uint8_t>(delimiter),
+                const cudaError_t e = launch_lines_tma_results(*lt, d_text, len, static_cast<uint8_t>(delimiter),
                                                                chunk, d_count, d_results, scratch, sb, cs, st);
                 cudaFreeAsync(scratch, st);
                 if (e != cudaSuccess) return cuda_fail(e, "launch_lines_tma_results");
@@ -512,7 +520,8 @@ int batch_device(rxg_heap* h, const uint8_t* d_text, uint64_t len, int32_t delim
         const DevTable* ta = nullptr;
         if (int rc = plain_table(h, &t, &ta)) return rc;
         cudaError_t e;
-        if (ta && fixed_tma_fits(ta->img_bytes, stride, h->smem_limit) && !std::getenv("RXG_NO_FIXED_TMA")) {
+        static const bool no_fixed_tma = std::getenv("RXG_NO_FIXED_TMA") != nullptr;   // tests
+        if (ta && fixed_tma_fits(ta->img_bytes, stride, h->smem_limit) && !no_fixed_tma) {
             uint64_t done = 0;
             const uint64_t n = len / stride;
             e = launch_fixed_tma(*ta, d_text, n, stride, d_count, d_results, cs, h->device, st, &done);
@@ -559,15 +568,69 @@ std::vector<uint64_t> pieces(const uint8_t* text, uint64_t len, int32_t delimite
     return b;
 }
 
+}  // namespace
+
+namespace rxg {
+namespace detail {
+
 uint64_t count_strings(const uint8_t* text, uint64_t lo, uint64_t hi, int32_t delimiter, uint32_t stride) {
     if (delimiter < 0) return (hi - lo) / stride;
     uint64_t n = 0;
-    for (uint64_t i = lo; i < hi; ++i) n += text[i] == static_cast<uint8_t>(delimiter);
+    for (const uint8_t* p = text + lo; p < text + hi;) {
+        const void* q = std::memchr(p, delimiter, static_cast<size_t>(text + hi - p));
+        if (!q) break;
+        ++n;
+        p = static_cast<const uint8_t*>(q) + 1;
+    }
     if (hi > lo && text[hi - 1] != static_cast<uint8_t>(delimiter)) ++n;
     return n;
 }
 
-}  // namespace
+int need_device(rxg_heap* h, bool dfa) {
+    if (!h) return fail(RXG_EINVAL, "null heap");
+    if (h->device < 0) return fail(RXG_ENODEV, "host-only heap handle");
+    if (!h->prog.byte_symbols)
+        return fail(RXG_EUNSUPPORTED, "pattern has a literal that is not a Unicode scalar value");
+    if (dfa && !h->dfa_ok)
+        return fail(RXG_ETOOBIG, "memoized step table exceeds " + std::to_string(kMaxDfaStates) + " states");
+    return RXG_OK;
+}
+
+int clone_heap(const rxg_heap* proto, int device, rxg_heap** out) {
+    auto h = std::make_unique<rxg_heap>();
+    h->prog = proto->prog;
+    h->dfa_ok = proto->dfa_ok;
+    h->dfa_sets = proto->dfa_sets;
+    h->dfa = proto->dfa;
+    {
+        std::lock_guard<std::mutex> lk(const_cast<rxg_heap*>(proto)->mu);
+        h->lookback = proto->lookback;
+        h->line_freq = proto->line_freq;
+    }
+    if (int rc = init_device(h.get(), device)) return rc;
+    *out = h.release();
+    return RXG_OK;
+}
+
+int adopt_tuning(rxg_heap* h, const rxg_heap* proto, int32_t delimiter) {
+    std::vector<double> f;
+    uint32_t lb;
+    {
+        std::lock_guard<std::mutex> lk(const_cast<rxg_heap*>(proto)->mu);
+        auto it = proto->line_freq.find(delimiter);
+        if (it == proto->line_freq.end()) return RXG_OK;
+        f = it->second;
+        lb = proto->lookback;
+    }
+    std::lock_guard<std::mutex> lk(h->mu);
+    return apply_tuning(h, delimiter, std::move(f), lb);
+}
+
+}  // namespace detail
+}  // namespace rxg
+
+using rxg::detail::count_strings;
+using rxg::detail::need_device;
 
 extern "C" {
 
@@ -710,9 +773,10 @@ int rxg_heap_info_get(const rxg_heap* h, rxg_heap_info* info) {
         info->plain_table_bytes = static_cast<uint32_t>(make_plain_table(h->prog, h->dfa).img.size());
         std::lock_guard<std::mutex> lk(const_cast<rxg_heap*>(h)->mu);
         auto it = h->lines.find('\n');
-        if (it != h->lines.end() && it->second->lt.ok) {
-            info->line_tma_layout = !it->second->lt.cls ? 1 : it->second->lt.range_k ? 3 : 2;
-            info->line_col_bytes = it->second->lt.cls ? 0 : it->second->lt.col_bytes;
+        const LtTable* lt = it != h->lines.end() ? it->second->lt.get() : nullptr;
+        if (lt && lt->ok) {
+            info->line_tma_layout = !lt->cls ? 1 : lt->range_k ? 3 : 2;
+            info->line_col_bytes = lt->cls ? 0 : lt->col_bytes;
         }
     }
     return RXG_OK;
@@ -803,23 +867,12 @@ int rxg_host_emulate_batch(const rxg_heap* h, const uint8_t* text, uint64_t len,
 int rxg_heap_tune(rxg_heap* h, const uint8_t* sample, uint64_t len, int32_t delimiter) {
     if (!h || (!sample && len) || delimiter < -1 || delimiter > 255) return fail(RXG_EINVAL, "bad arguments");
     if (!h->dfa_ok) return RXG_OK;
+    // sampling reads only the immutable program and DFA: no lock needed
+    std::vector<double> f = delimiter < 0 ? lt_sample_freq_plain(h->prog, h->dfa, sample, len)
+                                          : lt_sample_freq(h->prog, h->dfa, static_cast<uint8_t>(delimiter), sample, len);
+    const uint32_t lb = delimiter < 0 ? lt_sync_lookback(h->prog, h->dfa, sample, len) : 0;
     std::lock_guard<std::mutex> lk(h->mu);
-    if (delimiter < 0) {   // one long string: placement of the chunk-parallel table, and its lookback
-        h->line_freq[-1] = lt_sample_freq_plain(h->prog, h->dfa, sample, len);
-        h->lookback = lt_sync_lookback(h->prog, h->dfa, sample, len);
-        if (h->plain && h->device >= 0) {
-            DeviceGuard g(h->device);
-            return build_chunk_lt(h);
-        }
-        return RXG_OK;
-    }
-    h->line_freq[delimiter] = lt_sample_freq(h->prog, h->dfa, static_cast<uint8_t>(delimiter), sample, len);
-    auto it = h->lines.find(delimiter);
-    if (it != h->lines.end() && it->second->lt.ok && h->device >= 0) {
-        DeviceGuard g(h->device);
-        return build_lt(h, delimiter, it->second->lt);
-    }
-    return RXG_OK;
+    return apply_tuning(h, delimiter, std::move(f), lb);
 }
 
 int rxg_host_emulate_chunk_tma(const rxg_heap* h, const uint8_t* text, uint64_t len, int32_t* accept,
@@ -905,10 +958,11 @@ int rxg_match_one_ex(rxg_heap* h, const uint8_t* d_bytes, uint64_t len, int engi
     case RXG_ENGINE_AUTO:
     case RXG_ENGINE_CHUNKED: {
         const DevTable* t = nullptr;
-        if (int rc = plain_table(h, &t)) return rc;
+        std::shared_ptr<const ChunkImage> ci;
+        if (int rc = plain_table(h, &t, nullptr, &ci)) return rc;
         static const bool no_tma = std::getenv("RXG_NO_TMA") != nullptr;
-        if (h->plain->chunk_lt.ok && !no_tma) {
-            uint32_t chunk = o.chunk ? o.chunk : chunked_tma_auto_chunk(h->plain->chunk_lt, len, h->device);
+        if (ci && ci->lt.ok && !no_tma) {
+            uint32_t chunk = o.chunk ? o.chunk : chunked_tma_auto_chunk(ci->lt, len, h->device);
             if (chunk % 32) return fail(RXG_EINVAL, "chunk must be a multiple of 32 on the TMA path");
             void* scratch = nullptr;
             if (int rc = stream_scratch(h, st, chunked_tma_scratch_bytes(len, chunk), &scratch)) return rc;
@@ -916,7 +970,7 @@ int rxg_match_one_ex(rxg_heap* h, const uint8_t* d_bytes, uint64_t len, int engi
             if (int rc = stream_slot(h, st, &cs, false)) return rc;
             // one counter per tile seam (tiles hold >= 32 ranges) and the remainder's
             if (int rc = seam_counters(h, st, (len / chunk + 1) / 32 + 2, &cs.seam)) return rc;
-            const cudaError_t e = launch_chunked_tma(h->plain->chunk_lt, h->plain->d_chunk, d_bytes, len, chunk,
+            const cudaError_t e = launch_chunked_tma(ci->lt, ci->d, d_bytes, len, chunk,
                                                      o.lookback ? o.lookback : h->lookback, scratch, d_accept, o.d_repairs,
                                                      cs, h->device, st,
                                                      (o.flags & RXG_ONE_ENTRY) ? o.entry_state : kStartState,
@@ -980,7 +1034,10 @@ int rxg_match_one(rxg_heap* h, const uint8_t* bytes, uint64_t len, int engine, i
     return RXG_OK;
 }
 
-namespace {
+}  // extern "C"
+
+namespace rxg {
+namespace detail {
 
 // Batch on device buffers with engine selection; zero_count = overwrite the
 // count (false: accumulate, for the pieces of the pipelined host path).
@@ -1003,7 +1060,12 @@ int batch_any(rxg_heap* h, const uint8_t* d_text, uint64_t len, int32_t delimite
     return RXG_OK;
 }
 
-}  // namespace
+}  // namespace detail
+}  // namespace rxg
+
+using rxg::detail::batch_any;
+
+extern "C" {
 
 int rxg_match_batch_ex(rxg_heap* h, const uint8_t* d_text, uint64_t len, int32_t delimiter, uint32_t stride,
                        int engine, unsigned long long* d_count, uint8_t* d_results, void* stream) {
@@ -1025,13 +1087,18 @@ int rxg_match_batch_host(rxg_heap* h, const uint8_t* text, uint64_t len, int32_t
     return rxg_match_batch_host_ex(h, text, len, delimiter, stride, count, results, nullptr);
 }
 
-int rxg_match_batch_host_ex(rxg_heap* h, const uint8_t* text, uint64_t len, int32_t delimiter, uint32_t stride,
-                            uint64_t* count, uint8_t* results, uint64_t* utf8_first_bad) {
+}  // extern "C"
+
+namespace rxg {
+namespace detail {
+
+int host_batch(rxg_heap* h, const uint8_t* text, uint64_t len, int32_t delimiter, uint32_t stride, uint64_t* count,
+               uint8_t* results, uint64_t* utf8_first_bad) {
     if (int rc = need_device(h, false)) return rc;
     if (utf8_first_bad && delimiter > 127) return fail(RXG_EINVAL, "UTF-8 check needs an ASCII delimiter");
     if (!h->dfa_ok && delimiter < 0) return fail(RXG_ETOOBIG, "memoized step table over the cap (fixed stride needs it)");
     std::lock_guard<std::mutex> host_lock(h->host_mu);
-    if (!count || (!text && len)) return fail(RXG_EINVAL, "bad arguments");
+    if (!text && len) return fail(RXG_EINVAL, "bad arguments");
     if (delimiter < 0 && (stride == 0 || len % stride)) return fail(RXG_EINVAL, "fixed stride must divide the buffer length");
     DeviceGuard g(h->device);
     if (delimiter >= 0 && delimiter <= 255 && h->dfa_ok) {
@@ -1099,7 +1166,7 @@ int rxg_match_batch_host_ex(rxg_heap* h, const uint8_t* text, uint64_t len, int3
         if (d_bad) cudaMemcpyAsync(&bad, d_bad, sizeof(bad), cudaMemcpyDeviceToHost, h->stream);
         const cudaError_t e = cudaStreamSynchronize(h->stream);
         if (e != cudaSuccess) rc = cuda_fail(e, "match_batch_host");
-        *count = c;
+        if (count) *count = c;
         if (utf8_first_bad) *utf8_first_bad = bad;
     }
     if (d_res) cudaFreeAsync(d_res, h->stream);
@@ -1111,6 +1178,17 @@ int rxg_match_batch_host_ex(rxg_heap* h, const uint8_t* text, uint64_t len, int3
     }
     g_launches = launches;
     return rc;
+}
+
+}  // namespace detail
+}  // namespace rxg
+
+extern "C" {
+
+int rxg_match_batch_host_ex(rxg_heap* h, const uint8_t* text, uint64_t len, int32_t delimiter, uint32_t stride,
+                            uint64_t* count, uint8_t* results, uint64_t* utf8_first_bad) {
+    if (!count) return fail(RXG_EINVAL, "bad arguments");
+    return rxg::detail::host_batch(h, text, len, delimiter, stride, count, results, utf8_first_bad);
 }
 
 int rxg_utf8_check(int device, const uint8_t* d_text, uint64_t len, int32_t delimiter, uint32_t stride,
@@ -1368,114 +1446,6 @@ int rxg_shard_bounds(const uint8_t* text, uint64_t len, int32_t delimiter, uint3
     }
     offsets[ndev] = len;
     return RXG_OK;
-}
-
-int rxg_match_batch_multi(const int* devices, int ndev, const char* pattern, size_t plen, const uint8_t* text,
-                          uint64_t len, int32_t delimiter, uint32_t stride, uint64_t* count, uint8_t* results) {
-    if (!devices || ndev <= 0 || !count) return fail(RXG_EINVAL, "bad arguments");
-    std::vector<uint64_t> off(static_cast<size_t>(ndev) + 1);
-    if (int rc = rxg_shard_bounds(text, len, delimiter, stride, ndev, off.data())) return rc;
-    std::vector<rxg_heap*> hs(static_cast<size_t>(ndev), nullptr);
-    auto cleanup = [&] {
-        for (auto* x : hs) rxg_heap_destroy(x);
-    };
-    std::vector<uint8_t*> d_text(static_cast<size_t>(ndev), nullptr);
-    std::vector<uint8_t*> d_res(static_cast<size_t>(ndev), nullptr);
-    std::vector<uint64_t> res_base(static_cast<size_t>(ndev), 0);
-    uint64_t nstr = 0;
-    int rc = RXG_OK;
-    for (int k = 0; k < ndev && rc == RXG_OK; ++k) {
-        rc = rxg_heap_create_pattern(pattern, plen, devices[k], &hs[static_cast<size_t>(k)]);
-        if (rc) break;
-        rxg_heap* h = hs[static_cast<size_t>(k)];
-        if ((rc = need_device(h, false))) break;
-        if (!h->dfa_ok && delimiter < 0) {
-            rc = fail(RXG_ETOOBIG, "memoized step table over the cap (fixed stride needs it)");
-            break;
-        }
-        DeviceGuard g(h->device);
-        const uint64_t n = off[static_cast<size_t>(k) + 1] - off[static_cast<size_t>(k)];
-        if (cudaMalloc(&d_text[static_cast<size_t>(k)], std::max<uint64_t>(n, 16)) != cudaSuccess) {
-            rc = fail(RXG_ENOMEM, "device allocation failed");
-            break;
-        }
-        if (results) {
-            res_base[static_cast<size_t>(k)] = nstr;
-            const uint64_t m = count_strings(text, off[static_cast<size_t>(k)], off[static_cast<size_t>(k) + 1], delimiter, stride);
-            nstr += m;
-            cudaMalloc(&d_res[static_cast<size_t>(k)], std::max<uint64_t>(m, 1) + 1);
-        }
-        if (results && !d_res[static_cast<size_t>(k)]) {
-            rc = fail(RXG_ENOMEM, "device allocation failed");
-            break;
-        }
-        if (n) {
-            const cudaError_t e = cudaMemcpyAsync(d_text[static_cast<size_t>(k)], text + off[static_cast<size_t>(k)], n,
-                                                  cudaMemcpyHostToDevice, h->stream);
-            if (e != cudaSuccess) {
-                rc = cuda_fail(e, "shard upload");
-                break;
-            }
-        }
-        rc = batch_any(h, d_text[static_cast<size_t>(k)], n, delimiter, stride, RXG_BATCH_AUTO, h->d_count,
-                       d_res[static_cast<size_t>(k)], h->stream, true);
-    }
-    if (rc == RXG_OK && ndev > 1) {
-        // One all-reduce of the 8-byte count: the only inter-GPU traffic.
-        void* lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
-        auto init_all = lib ? reinterpret_cast<ncclResult_t (*)(ncclComm_t*, int, const int*)>(dlsym(lib, "ncclCommInitAll")) : nullptr;
-        auto allreduce = lib ? reinterpret_cast<ncclResult_t (*)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t)>(dlsym(lib, "ncclAllReduce")) : nullptr;
-        auto gstart = lib ? reinterpret_cast<ncclResult_t (*)()>(dlsym(lib, "ncclGroupStart")) : nullptr;
-        auto gend = lib ? reinterpret_cast<ncclResult_t (*)()>(dlsym(lib, "ncclGroupEnd")) : nullptr;
-        auto destroy = lib ? reinterpret_cast<ncclResult_t (*)(ncclComm_t)>(dlsym(lib, "ncclCommDestroy")) : nullptr;
-        if (!init_all || !allreduce || !gstart || !gend || !destroy) {
-            rc = fail(RXG_ENCCL, "libnccl.so.2 not loadable");
-        } else {
-            std::vector<ncclComm_t> comms(static_cast<size_t>(ndev));
-            if (init_all(comms.data(), ndev, devices) != ncclSuccess) {
-                rc = fail(RXG_ENCCL, "ncclCommInitAll failed");
-            } else {
-                gstart();
-                for (int k = 0; k < ndev; ++k) {
-                    rxg_heap* h = hs[static_cast<size_t>(k)];
-                    allreduce(h->d_count, h->d_count, 1, ncclUint64, ncclSum, comms[static_cast<size_t>(k)], h->stream);
-                }
-                if (gend() != ncclSuccess) rc = fail(RXG_ENCCL, "ncclAllReduce failed");
-                for (int k = 0; k < ndev; ++k) {
-                    DeviceGuard g(devices[k]);
-                    cudaStreamSynchronize(hs[static_cast<size_t>(k)]->stream);
-                }
-                for (auto c : comms) destroy(c);
-            }
-        }
-    }
-    if (rc == RXG_OK) {
-        // the heaps' streams are non-blocking: read back on them, then wait
-        unsigned long long c = 0;
-        cudaError_t e = cudaSuccess;
-        for (int k = 0; k < ndev && e == cudaSuccess; ++k) {
-            rxg_heap* h = hs[static_cast<size_t>(k)];
-            DeviceGuard gk(h->device);
-            if (k == 0) e = cudaMemcpyAsync(&c, h->d_count, sizeof(c), cudaMemcpyDeviceToHost, h->stream);
-            const uint64_t m = results ? (k + 1 < ndev ? res_base[static_cast<size_t>(k) + 1] : nstr) - res_base[static_cast<size_t>(k)] : 0;
-            if (e == cudaSuccess && m)
-                e = cudaMemcpyAsync(results + res_base[static_cast<size_t>(k)], d_res[static_cast<size_t>(k)], m,
-                                    cudaMemcpyDeviceToHost, h->stream);
-            if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
-        }
-        if (e != cudaSuccess) rc = cuda_fail(e, "rxg_match_batch_multi readback");
-        *count = c;
-    }
-    for (int k = 0; k < ndev; ++k) {
-        if (!hs[static_cast<size_t>(k)]) continue;
-        DeviceGuard g(devices[k]);
-        cudaDeviceSynchronize();
-        if (d_text[static_cast<size_t>(k)]) cudaFree(d_text[static_cast<size_t>(k)]);
-        if (d_res[static_cast<size_t>(k)]) cudaFree(d_res[static_cast<size_t>(k)]);
-    }
-    cleanup();
-    g_launches = ndev;
-    return rc;
 }
 
 int rxg_synth_pattern(char config, char* out, size_t cap, size_t* out_len) {

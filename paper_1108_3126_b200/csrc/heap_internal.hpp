@@ -1,0 +1,129 @@
+// Internal definition of the rxg_heap handle (include/rxg.h) and the host
+// helpers shared by capi.cu (single device) and multi.cu (communicators and
+// the persistent multi-device handle). Not part of the C ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "rxg.h"
+#include "launch.hpp"
+#include "lines_tma.hpp"
+#include "pernode.hpp"
+#include "program.hpp"
+#include "tables.hpp"
+
+namespace rxg {
+
+// A TMA table image published to launches. Never mutated after publication:
+// a retune (rxg_heap_tune) builds a new one and swaps the shared_ptr under
+// rxg_heap::mu; launches copy the shared_ptr under the same lock, so a
+// launch never reads a half-replaced table. The device copies are owned by
+// the heap (rxg_heap::allocs) and freed only when the heap is destroyed, so
+// a kernel still running on a replaced image (or a CUDA graph captured
+// earlier) keeps valid memory.
+struct ChunkImage {
+    LtTable lt;
+    const void* d = nullptr;   // device copy of lt.lo
+};
+
+struct TableSlot {
+    KTable host;
+    DevTable dev;
+    std::shared_ptr<const LtTable> lt;        // TMA line layout (delimited slots; null or !ok if it does not fit)
+    DevTable abs;                             // plain slot: entries rebased to absolute shared addresses
+    bool has_abs = false;
+    std::shared_ptr<const ChunkImage> chunk;  // plain slot: TMA chunk-parallel layout (null or !lt.ok if it does not fit)
+};
+
+constexpr int32_t kMaxDfaStates = 16384;
+
+}  // namespace rxg
+
+struct rxg_heap {
+    int device = -1;
+    rxg::Program prog;
+    bool dfa_ok = false;
+    bool tma_ok = true;     // the dynamic shared window starts at 0x400 (the TMA layouts' absolute addresses)
+    int32_t dfa_sets = 0;   // states before minimisation
+    uint32_t lookback = 64; // chunk engine lookback (rxg_heap_tune with delimiter -1 shortens it)
+    rxg::Dfa dfa;
+    int smem_limit = 0;
+    std::mutex mu;          // guards everything below that is created lazily or replaced
+    std::mutex host_mu;     // host-buffer calls share the staging buffers and streams
+    std::unique_ptr<rxg::TableSlot> plain;
+    std::map<int, std::unique_ptr<rxg::TableSlot>> lines;
+    std::map<int, std::vector<double>> line_freq;   // sampled state x byte counts per delimiter (rxg_heap_tune)
+    // device allocations of table images and retired stream scratch: freed with the heap
+    std::vector<void*> allocs;
+    // staging for host-buffer calls
+    uint8_t* d_stage[2] = {nullptr, nullptr};
+    size_t stage_bytes = 0;
+    unsigned long long* d_count = nullptr;
+    int32_t* d_accept = nullptr;
+    cudaStream_t stream = nullptr;
+    cudaStream_t copy_stream = nullptr;
+    // lazily built tables of the thread-per-node engines
+    void* d_rounds = nullptr;
+    rxg::RoundsTables rounds;
+    void* d_pernode = nullptr;
+    rxg::PernodeTables pernode;
+    // Per stream, keyed by cudaStreamGetId (so cudaStreamPerThread from two
+    // threads gives two keys): the CountSlot (launch.hpp, zero when idle), the
+    // chunked engine's seam arrival counters (zero when idle, grow-only) and
+    // its scratch (guesses, exits, checkpoints; grow-only).
+    std::map<unsigned long long, unsigned long long*> slots;
+    std::map<unsigned long long, std::pair<unsigned int*, size_t>> seams;
+    std::map<unsigned long long, std::pair<void*, size_t>> scratch;
+
+    ~rxg_heap();
+};
+
+namespace rxg {
+namespace detail {
+
+int fail(int code, const std::string& msg);
+int cuda_fail(cudaError_t e, const char* where);
+void set_launches(int n);
+int launches();
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        if (dev >= 0 && cudaGetDevice(&prev) == cudaSuccess && prev != dev) cudaSetDevice(dev);
+        else prev = -1;
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+int need_device(rxg_heap* h, bool dfa = true);
+
+// A heap for `device` with the program, memoized step and tuning of `proto`
+// (built once on the host, uploaded per device).
+int clone_heap(const rxg_heap* proto, int device, rxg_heap** out);
+// Copy proto's sampled placement for `delimiter` into h and rebuild h's tables.
+int adopt_tuning(rxg_heap* h, const rxg_heap* proto, int32_t delimiter);
+
+// Batch on device buffers with engine selection; zero_count = overwrite the
+// count (false: accumulate).
+int batch_any(rxg_heap* h, const uint8_t* d_text, uint64_t len, int32_t delimiter, uint32_t stride, int engine,
+              unsigned long long* d_count, uint8_t* d_results, cudaStream_t st, bool zero_count);
+
+// The pipelined host-buffer path (pieces of 64 MiB: copy k+1 while matching k).
+// On return (RXG_OK) the stream is idle, h->d_count holds the count, and the
+// results / utf8 check are in host memory; *count (nullable) is read back.
+int host_batch(rxg_heap* h, const uint8_t* text, uint64_t len, int32_t delimiter, uint32_t stride, uint64_t* count,
+               uint8_t* results, uint64_t* utf8_first_bad);
+
+uint64_t count_strings(const uint8_t* text, uint64_t lo, uint64_t hi, int32_t delimiter, uint32_t stride);
+
+}  // namespace detail
+}  // namespace rxg

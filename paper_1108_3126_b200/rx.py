@@ -372,8 +372,95 @@ def count_strings(text, delimiter: int = 10, stride: int = 0) -> int:
     return n
 
 
+class Comm:
+    """A NCCL communicator over one-process-per-GPU ranks (rxg_comm).
+
+    Rank 0 calls ``Comm.unique_id()``; the host plumbing (torch.distributed,
+    MPI, a file) broadcasts the 128 bytes; every rank then constructs
+    ``Comm(uid, nranks, rank, device)`` (collective)."""
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = (C.c_uint8 * 128)()
+        _check(L.lib().rxg_comm_unique_id(buf, 128))
+        return bytes(buf)
+
+    def __init__(self, uid: bytes, nranks: int, rank: int, device: int):
+        assert len(uid) == 128
+        self._c = C.c_void_p()
+        ub = (C.c_uint8 * 128).from_buffer_copy(uid)
+        _check(L.lib().rxg_comm_init_rank(ub, 128, nranks, rank, device, C.byref(self._c)))
+        self.nranks, self.rank, self.device = nranks, rank, device
+
+    def close(self):
+        if self._c:
+            L.lib().rxg_comm_destroy(self._c)
+            self._c = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def match_batch_allreduce(m: "Matcher", comm: Comm, d_text, d_count, d_results=None, delimiter: int = 10,
+                          stride: int = 0, stream=None, nbytes: int | None = None):
+    """This rank's shard through K2, then the NCCL sum of d_count over the ranks, on `stream`."""
+    n = d_text.numel() if nbytes is None else nbytes
+    _check(L.lib().rxg_match_batch_allreduce(m.handle, comm._c, d_text.data_ptr(), n, delimiter, stride,
+                                             d_count.data_ptr(),
+                                             d_results.data_ptr() if d_results is not None else None,
+                                             _stream_ptr(stream)))
+
+
+class MultiMatcher:
+    """One pattern resident on several GPUs (rxg_multi): tables built once and
+    uploaded per device, one worker thread per device, communicators created
+    once. A device may be listed twice (the counts are then summed on the host)."""
+
+    def __init__(self, devices, pattern):
+        devs = (C.c_int * len(devices))(*devices)
+        pat = _b(pattern)
+        self._m = C.c_void_p()
+        _check(L.lib().rxg_multi_create(devs, len(devices), pat, len(pat), C.byref(self._m)))
+        self.devices = list(devices)
+
+    def close(self):
+        if self._m:
+            L.lib().rxg_multi_destroy(self._m)
+            self._m = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def info(self) -> dict:
+        n, u = C.c_int32(0), C.c_int32(0)
+        _check(L.lib().rxg_multi_info(self._m, C.byref(n), C.byref(u)))
+        return {"devices": n.value, "nccl": bool(u.value)}
+
+    def tune(self, sample, delimiter: int = 10):
+        p, n, keep = _ptr(sample)
+        _check(L.lib().rxg_multi_tune(self._m, p, n, delimiter))
+
+    def match_batch(self, text, delimiter: int = 10, stride: int = 0, results: bool = False):
+        """Shard a host buffer over the devices -> (count, results|None)."""
+        p, n, keep = _ptr(text)
+        res = None
+        if results:
+            nstr = count_strings(text, delimiter, stride)
+            res = np.zeros(max(nstr, 1) + 1, np.uint8)
+        cnt = C.c_uint64(0)
+        _check(L.lib().rxg_multi_match_batch(self._m, p, n, delimiter, stride, C.byref(cnt),
+                                             res.ctypes.data if res is not None else None))
+        return cnt.value, (res[:nstr] if res is not None else None)
+
+
 def match_batch_multi(devices, pattern, text, delimiter: int = 10, stride: int = 0, results: bool = False):
-    """Shard a host buffer over several GPUs; one NCCL all-reduce of the count."""
+    """One-shot: shard a host buffer over several GPUs; one NCCL all-reduce of the count."""
     devs = (C.c_int * len(devices))(*devices)
     pat = _b(pattern)
     p, n, keep = _ptr(text)
@@ -410,6 +497,13 @@ def match_one_multi(devices, pattern, text):
     rer = C.c_int32(0)
     _check(L.lib().rxg_match_one_multi(devs, len(devices), pat, len(pat), p, n, C.byref(acc), C.byref(rer)))
     return bool(acc.value), rer.value
+
+
+def shard(text, nshards: int, index: int, delimiter: int = 10, stride: int = 0) -> tuple[int, int]:
+    """[lo, hi) of shard `index` of a job cut into `nshards` byte-balanced shards at
+    string boundaries (rxg_shard_bounds): what rank `index` of a strong-scaled run matches."""
+    b = shard_bounds(text, nshards, delimiter, stride)
+    return b[index], b[index + 1]
 
 
 def shard_bounds(text, ndev: int, delimiter: int = 10, stride: int = 0) -> list[int]:

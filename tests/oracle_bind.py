@@ -152,6 +152,41 @@ class Oracle:
         return int(cnt), (res[:nstr] if res is not None else None)
 
 
+def _raw_synth():
+    l = Oracle._raw()
+    l.oracle_synth_pattern.restype = C.c_size_t
+    l.oracle_synth_pattern.argtypes = [C.c_char, C.c_char_p, C.c_size_t]
+    l.oracle_synth_input.restype = C.c_uint64
+    l.oracle_synth_input.argtypes = [C.c_char, C.c_uint64, C.c_void_p, C.c_uint64]
+    l.oracle_synth_input_size.restype = C.c_uint64
+    l.oracle_synth_input_size.argtypes = [C.c_char]
+    l.oracle_mt64_nth.restype = C.c_uint64
+    l.oracle_mt64_nth.argtypes = [C.c_uint64, C.c_uint64]
+    return l
+
+
+def synth_pattern(cfg: str) -> str:
+    """SURVEY.md §8(d) pattern of a config, from the C restatement (no librxg)."""
+    l = _raw_synth()
+    n = l.oracle_synth_pattern(cfg.encode(), None, 0)
+    buf = C.create_string_buffer(n + 1)
+    l.oracle_synth_pattern(cfg.encode(), buf, n + 1)
+    return buf.value.decode()
+
+
+def synth_input(cfg: str, nbytes: int | None = None, seed: int = 0) -> np.ndarray:
+    """SURVEY.md §8(d) input of a config (first nbytes; c: whole lines), from the C restatement."""
+    l = _raw_synth()
+    cap = nbytes if nbytes is not None else int(l.oracle_synth_input_size(cfg.encode()))
+    buf = np.empty(max(cap, 1), np.uint8)
+    n = l.oracle_synth_input(cfg.encode(), seed, buf.ctypes.data, cap)
+    return buf[:n]
+
+
+def mt64_nth(seed: int, n: int) -> int:
+    return int(_raw_synth().oracle_mt64_nth(seed, n))
+
+
 def verify_checkpoints(heap, pos_addr, n_pos, checkpoints, text, every, threads=None):
     """Chunk-parallel check of a long single-string run.
     checkpoints[k] is the position-form set E after (k+1)*every symbols: the

@@ -1,13 +1,14 @@
-"""The N>1 path on CPU (world_size 2, gloo): shard a batch at string
-boundaries, match each shard with the host emulation of the line kernel
-(same table image and ownership rules as the GPU), all-reduce the 8-byte
-count — the only collective — and compare with the oracle on the whole
-buffer. Also checks the weak-scaling layout bench.py uses (per-rank seeds)."""
+"""The N>1 path on CPU (world_size 2, gloo), driving the same sharding code as
+bench.py's strong-scaled run: every rank builds the whole job, takes its shard
+with rx.shard (rxg_shard_bounds: byte-balanced, cut at string boundaries),
+matches it with the host emulation of the line kernel (same table image,
+tuned from the head of the job, same ownership rules as the GPU), and the
+8-byte count is all-reduced — the only collective. The total must equal the
+oracle on the whole job; fixed-stride jobs shard at stride multiples."""
 import os
 import socket
 
 import numpy as np
-import pytest
 import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
@@ -34,26 +35,33 @@ def _worker(rank, world, port, q):
     from paper_1108_3126_b200 import rx
 
     try:
-        # strong split of one buffer
-        pat = rx.synth_pattern("c")
-        text = rx.synth_input("c", 1 << 20)
-        b = rx.shard_bounds(text, world, delimiter=10)
-        shard = text[b[rank]:b[rank + 1]]
+        out = {}
+        for cfg, nbytes in (("c", 1 << 20), ("d", 1 << 20)):
+            pat = rx.synth_pattern(cfg)
+            text = rx.synth_input(cfg, nbytes)
+            lo, hi = rx.shard(text, world, rank, delimiter=10)
+            m = rx.Matcher(pat, device=-1)
+            m.tune(text[: 1 << 16])   # the job's head, as bench.py: identical tables on every rank
+            local = m.emulate_lines_tma(text[lo:hi], 10, 64)
+            cnt = torch.tensor([local], dtype=torch.int64)
+            dist.all_reduce(cnt)
+            out[cfg] = (int(cnt.item()), lo, hi)
+        # fixed stride: shards at stride multiples
+        pat = rx.synth_pattern("b")
+        text = rx.synth_input("b", 32 * 1000)
+        lo, hi = rx.shard(text, world, rank, delimiter=-1, stride=32)
+        assert lo % 32 == 0 and hi % 32 == 0
         m = rx.Matcher(pat, device=-1)
-        m.tune(shard[: 1 << 16])
-        local = m.emulate_lines_tma(shard, 10, 64)
+        local, _ = m.emulate_batch(text[lo:hi], delimiter=-1, stride=32)
         cnt = torch.tensor([local], dtype=torch.int64)
         dist.all_reduce(cnt)
-        # weak scaling: every rank its own shard of the config's shape
-        own = rx.synth_input("c", 1 << 18, seed=0 if rank == 0 else 1000 + rank)
-        wcnt = torch.tensor([m.emulate_lines_tma(own, 10, 64)], dtype=torch.int64)
-        dist.all_reduce(wcnt)
-        q.put((rank, int(cnt.item()), int(wcnt.item())))
+        out["b"] = (int(cnt.item()), lo, hi)
+        q.put((rank, out))
     finally:
         dist.destroy_process_group()
 
 
-def test_two_rank_count_allreduce():
+def test_two_rank_strong_shards_count_allreduce():
     from oracle_bind import Oracle
     from paper_1108_3126_b200 import rx
 
@@ -64,15 +72,32 @@ def test_two_rank_count_allreduce():
     procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
-    out = [q.get(timeout=120) for _ in range(world)]
+    out = dict(q.get(timeout=180) for _ in range(world))
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    pat = rx.synth_pattern("c")
-    o = Oracle(rx.compile(rx.parse(pat)))
-    want, _ = o.match_batch(rx.synth_input("c", 1 << 20), 10, 0, results=False)
-    wweak = sum(o.match_batch(rx.synth_input("c", 1 << 18, seed=0 if r == 0 else 1000 + r), 10, 0, results=False)[0]
-                for r in range(world))
-    for rank, c, wc in out:
-        assert c == want
-        assert wc == wweak
+    for cfg, nbytes, delim, stride in (("c", 1 << 20, 10, 0), ("d", 1 << 20, 10, 0), ("b", 32 * 1000, -1, 32)):
+        text = rx.synth_input(cfg, nbytes)
+        o = Oracle(rx.compile(rx.parse(rx.synth_pattern(cfg))))
+        want, _ = o.match_batch(text, delim, stride, results=False)
+        # shards tile the job, in rank order, and split no string
+        assert out[0][cfg][1] == 0 and out[0][cfg][2] == out[1][cfg][1] and out[1][cfg][2] == len(text)
+        if delim >= 0:
+            assert text[out[0][cfg][2] - 1] == delim
+        for r in range(world):
+            assert out[r][cfg][0] == want, (cfg, r)
+
+
+def test_shard_bounds_edge_cases():
+    from paper_1108_3126_b200 import rx
+
+    # more shards than strings, empty job, no delimiter at all, long lines
+    assert rx.shard_bounds(b"ab\ncd\n", 4, 10) [-1] == 6
+    b = rx.shard_bounds(b"ab\ncd\n", 4, 10)
+    assert b == sorted(b) and all(x in (0, 3, 6) for x in b)
+    assert rx.shard_bounds(b"", 3, 10) == [0, 0, 0, 0]
+    assert rx.shard_bounds(b"abcdef", 3, 10) == [0, 6, 6, 6]
+    t = np.frombuffer(b"x" * 1000 + b"\n" + b"y\n", np.uint8)
+    b = rx.shard_bounds(t, 2, 10)
+    assert b == [0, 1001, 1003]
+    assert rx.shard_bounds(b"a" * 96, 2, -1, 32) == [0, 32, 96]

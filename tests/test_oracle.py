@@ -127,3 +127,37 @@ def test_oracle_against_reference_random():
         for _ in range(8):
             w = bytes(rng.choice([97, 98, 99], size=int(rng.integers(0, 30))).astype(np.uint8))
             assert o.accepts(w) == r.accepts(w), (p, w)
+
+
+def test_synth_restatement_equals_product_generator():
+    """oracle/synth_oracle.c (the reference arm's inputs, no librxg) emits the
+    same bytes as the product's generator for every config (prefixes for the
+    big ones), and its mt19937_64 passes the standard's known answer."""
+    import oracle_bind as ob
+    from paper_1108_3126_b200 import rx
+
+    assert ob.mt64_nth(5489, 10000) == 9981545732273789042   # [rand.predef]
+    for c in "aAbcde":
+        assert ob.synth_pattern(c) == rx.synth_pattern(c), c
+    for c, n in [("a", None), ("A", None), ("b", None), ("c", 4 << 20), ("d", 4 << 20), ("e", 1 << 20)]:
+        assert np.array_equal(ob.synth_input(c, n), rx.synth_input(c, n)), c
+    assert np.array_equal(ob.synth_input("c", 1 << 20, seed=1003), rx.synth_input("c", 1 << 20, seed=1003))
+
+
+def test_oracle_decodes_utf8_like_the_reference():
+    """The C oracle matches decoded scalars (utf8.cpp:16-46), not bytes: a
+    one-scalar literal pattern accepts its 2/3/4-byte encoding, a byte-wise
+    reading would not; malformed strings never match (the reference throws)."""
+    from oracle_bind import Oracle, Ref, RefHeap
+    from paper_1108_3126_b200 import rx
+
+    for pat, good, bad in [("é", "é", "e"), ("(λ|b)*", "λbλ", "λc"), ("😀a", "😀a", "😀")]:
+        o = Oracle(rx.compile(rx.parse(pat)))
+        assert o.accepts(good.encode()) and not o.accepts(bad.encode())
+        if Ref.available():   # the reference on the decoded scalars agrees
+            r = RefHeap(pat.encode())
+            assert r.accepts(good) and not r.accepts(bad)
+    o = Oracle(rx.compile(rx.parse("(a|())*")))
+    assert not o.accepts(b"a\xffa") and not o.accepts(b"\xc3")
+    cnt, res = o.match_batch(np.frombuffer("é\na\n\xff\n".encode("latin-1"), np.uint8), 10, 0)
+    assert list(res) == [0, 1, 0]
