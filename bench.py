@@ -165,31 +165,38 @@ def count_units(text: np.ndarray, delim: int, stride: int) -> int:
     return n + (1 if len(text) and text[-1] != delim else 0)
 
 
-def roofline(nbytes: int, words: int, kern_ms: float, traffic, cfg: str, dev: int) -> dict:
-    """t_roof = max(B / BW_HBM, B·W / INT32_peak); frac = t_roof / t."""
+def roofline(nbytes: int, words: int, kern_ms: float, traffic, cfg: str, dev: int, bitset: bool = False) -> dict:
+    """The dominant kernel against the roofline that binds its algorithm.
+
+    SURVEY.md §8(d) models a BITSET lockstep step: t_roof = max(B / BW_HBM,
+    B·W / INT32_peak), W 32-bit state-word updates per input byte. The
+    memoized-step (DFA) kernels do O(1) work per byte whatever W is, so their
+    binding roofline is HBM (every input byte read once); the survey model is
+    reported beside it (`survey_model`) and binds only the bitset kernels."""
     bw, bw_src = hbm_peak()
     i32, i32_src, mix = int32_peak(dev)
+    t = kern_ms / 1e3
     t_hbm = nbytes / (bw * 1e9)
     t_int = nbytes * words / (i32 * 1e12)
-    bound = "hbm" if t_hbm >= t_int else "int32"
-    t = kern_ms / 1e3
     achieved_gbs = nbytes / t / 1e9
-    r = {
-        "bound": bound,
-        "achieved": achieved_gbs if bound == "hbm" else nbytes * words / t / 1e12,
-        "peak": bw if bound == "hbm" else i32,
-        "unit": "GB/s" if bound == "hbm" else "Tops/s (32-bit state-word updates, B*W)",
-        "frac": max(t_hbm, t_int) / t,
+    survey = {"bound": "hbm" if t_hbm >= t_int else "int32", "t_roof_ms": max(t_hbm, t_int) * 1e3,
+              "frac": max(t_hbm, t_int) / t, "int32_t_roof_ms": t_int * 1e3, "int32_peak_tops": i32,
+              "int32_peak_source": i32_src, "int32_mix_tops": mix, "state_words": words,
+              "model": "max(B/BW_HBM, B*W/INT32_peak)"}
+    if bitset and t_int > t_hbm:
+        r = {"bound": "int32", "achieved": nbytes * words / t / 1e12, "peak": i32,
+             "unit": "Tops/s (32-bit state-word updates, B*W)", "frac": t_int / t}
+    else:
+        r = {"bound": "hbm", "achieved": achieved_gbs, "peak": bw, "unit": "GB/s", "frac": achieved_gbs / bw}
+    r.update({
         "traffic": traffic,
         "traffic_source": (f"dram__bytes_read.sum+dram__bytes_write.sum per launch from an earlier ncu --set full "
                            f"capture of config ({cfg}) (profiles/traffic.json), not measured in this run")
         if traffic else None,
         "algorithmic_bytes_per_launch": nbytes,
-        "state_words": words,
-        "hbm": {"achieved": achieved_gbs, "peak": bw, "frac": achieved_gbs / bw, "peak_source": bw_src},
-        "int32": {"t_roof_ms": t_int * 1e3, "peak_tops": i32, "peak_source": i32_src, "mix_tops": mix},
-        "model": "SURVEY.md 8(d): max(B/BW_HBM, B*W/INT32_peak); the memoized-step kernels do O(1) work per byte",
-    }
+        "peak_source": bw_src if r["bound"] == "hbm" else i32_src,
+        "survey_model": survey,
+    })
     return r
 
 
@@ -416,8 +423,9 @@ def make_flush(ctx, nbytes: int):
     return flush, "L2 flushed between timed steps (512 MiB write, then 256 MiB read)"
 
 
-def bench_batch(ctx, cfg: str, steps: int, warmup: int, headline: bool) -> dict:
-    """Strong scaling: the job is the config's whole buffer; rank r matches its shard."""
+def bench_batch(ctx, cfg: str, steps: int, warmup: int, headline: bool, engine: str = "auto") -> dict:
+    """Strong scaling: the job is the config's whole buffer; rank r matches its shard.
+    engine: "auto" (memoized step, K2) or "bitset" (K2b, SURVEY.md §8(d)'s bitset step)."""
     from paper_1108_3126_b200 import _lib, rx
 
     torch = ctx.torch
@@ -440,10 +448,10 @@ def bench_batch(ctx, cfg: str, steps: int, warmup: int, headline: bool) -> dict:
     flush, l2 = make_flush(ctx, nb)
 
     def kernel_step():
-        m.match_batch_device(d_text, d_count, delimiter=delim, stride=stride, stream=stream, nbytes=nb)
+        m.match_batch_device(d_text, d_count, delimiter=delim, stride=stride, stream=stream, nbytes=nb, engine=engine)
 
     def job_step():
-        if ctx.comm is None:
+        if ctx.comm is None or engine != "auto":
             kernel_step()
         else:
             rx.match_batch_allreduce(m, ctx.comm, d_text, d_count, delimiter=delim, stride=stride, stream=stream,
@@ -479,9 +487,10 @@ def bench_batch(ctx, cfg: str, steps: int, warmup: int, headline: bool) -> dict:
             "shard_bytes_rank0": int(bounds[1] - bounds[0]), "shards": [int(x) for x in bounds],
             "matches": matches, "l2": l2,
             "parallelism": f"dp{ctx.world} (string shards, count all-reduce over NCCL)" if ctx.world > 1 else "dp1",
-            "engine": "k2_lines" if delim >= 0 else "k2_fixed",
+            "engine": ("k2b_bitset_" if engine == "bitset" else "k2_") + ("lines" if delim >= 0 else "fixed"),
         },
-        "roofline": roofline(nb, info["words"], kern_local, traffic, cfg, ctx.dev),
+        "roofline": roofline(nb, info["words"], kern_local, traffic if engine == "auto" else None, cfg, ctx.dev,
+                             bitset=engine == "bitset"),
         "gpu_launches": launches * steps,
     }
     if ctx.world > 1:
@@ -491,7 +500,7 @@ def bench_batch(ctx, cfg: str, steps: int, warmup: int, headline: bool) -> dict:
     # end to end through the C ABI with host buffers: this rank's shard, H2D
     # inside the call (pipelined 64 MiB pieces), the count read back, then the
     # 8-byte count all-reduce across ranks
-    if not ctx.args.no_e2e:
+    if not ctx.args.no_e2e and engine == "auto":
         def e2e_time(buf):
             m.match_batch(buf, delimiter=delim, stride=stride)   # warm
             ctx.barrier()
@@ -510,7 +519,7 @@ def bench_batch(ctx, cfg: str, steps: int, warmup: int, headline: bool) -> dict:
         rec["e2e"] = {"value": job_bytes / t_pin / 1e9, "unit": "GB/s", "h2d_bytes_per_step": nb,
                       "d2h_bytes_per_step": 8, "host_buffer": "pinned",
                       "pageable": {"value": job_bytes / t_page / 1e9, "unit": "GB/s"}}
-    if ctx.world > 1:   # secondary: weak scaling (every rank the whole job)
+    if ctx.world > 1 and engine == "auto":   # secondary: weak scaling (every rank the whole job)
         d_full = torch.empty(job_bytes + 64, dtype=torch.uint8, device=ctx.dev)
         d_full[:job_bytes].copy_(torch.from_numpy(text))
 
@@ -524,7 +533,7 @@ def bench_batch(ctx, cfg: str, steps: int, warmup: int, headline: bool) -> dict:
         rec["weak"] = {"value": ctx.world * job_bytes / (wms / 1e3) / 1e9, "unit": "GB/s", "ms_per_step": wms,
                        "note": "every rank matches the whole job, count all-reduce"}
         del d_full
-    if ctx.rank == 0 and ctx.world == 1 and not ctx.args.no_cpu:
+    if ctx.rank == 0 and ctx.world == 1 and not ctx.args.no_cpu and engine == "auto":
         rec["cpu_baseline"] = cpu_record(cfg, pattern, text, ctx.args.cpu_target_s if headline else ctx.args.sub_cpu_s)
     return rec
 
@@ -600,7 +609,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--engine", default="auto")
+    ap.add_argument("--engine", default="auto", help="single-string engine (a, e)")
+    ap.add_argument("--batch-engine", default="auto", choices=["auto", "bitset"], help="batch engine (b, c, d)")
+    ap.add_argument("--bitset-subs", default="", help="extra forced-bitset sub-records, e.g. 'cd'")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline legs")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-sub", action="store_true", help="headline config only (no sub-records)")
@@ -615,9 +626,10 @@ def main():
     ctx = Ctx(args)
     cfg = args.config
 
-    def run(c, headline):
-        fn = bench_single if CONFIGS[c][0] == -2 else bench_batch
-        return fn(ctx, c, args.steps, args.warmup, headline)
+    def run(c, headline, engine=None):
+        if CONFIGS[c][0] == -2:
+            return bench_single(ctx, c, args.steps, args.warmup, headline)
+        return bench_batch(ctx, c, args.steps, args.warmup, headline, engine or args.batch_engine)
 
     rec = run(cfg, True)
     subs = {}
@@ -629,6 +641,12 @@ def main():
                 except Exception as e:  # noqa: BLE001 - a failing sub-record must not hide the headline
                     subs[c] = {"error": repr(e)}
                 ctx.torch.cuda.empty_cache()
+        for c in args.bitset_subs:
+            try:
+                subs[c + "_bitset"] = run(c, False, "bitset")
+            except Exception as e:  # noqa: BLE001
+                subs[c + "_bitset"] = {"error": repr(e)}
+            ctx.torch.cuda.empty_cache()
     if ctx.rank == 0:
         line = {
             "metric": "input GB/s matched",

@@ -20,6 +20,7 @@
 #include <vector>
 
 #include "rxg.h"
+#include "rxg_utf8.hpp"
 
 namespace rx {
 
@@ -66,21 +67,7 @@ inline std::u32string decode_utf8(std::string_view bytes) {
 
 inline std::string encode_utf8(char32_t cp) {
     std::string s;
-    if (cp < 0x80) {
-        s += static_cast<char>(cp);
-    } else if (cp < 0x800) {
-        s += static_cast<char>(0xC0 | (cp >> 6));
-        s += static_cast<char>(0x80 | (cp & 0x3F));
-    } else if (cp < 0x10000) {
-        s += static_cast<char>(0xE0 | (cp >> 12));
-        s += static_cast<char>(0x80 | ((cp >> 6) & 0x3F));
-        s += static_cast<char>(0x80 | (cp & 0x3F));
-    } else {
-        s += static_cast<char>(0xF0 | (cp >> 18));
-        s += static_cast<char>(0x80 | ((cp >> 12) & 0x3F));
-        s += static_cast<char>(0x80 | ((cp >> 6) & 0x3F));
-        s += static_cast<char>(0x80 | (cp & 0x3F));
-    }
+    rxg::append_utf8(s, cp);
     return s;
 }
 
@@ -126,7 +113,7 @@ inline void check(int rc) {
 }
 // Symbols to the UTF-8 bytes the device matches (literals are expanded to
 // UTF-8 byte chains, so this is exact for every scalar).
-inline std::string narrow(InputView w) { return encode_utf8(w); }
+inline std::string narrow(InputView w) { return rxg::symbols_to_bytes(w); }
 }  // namespace detail
 
 // The compiled heap (heap.hpp:28-37) plus its device-resident tables. The

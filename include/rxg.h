@@ -323,6 +323,14 @@ int rxg_shard_bounds(const uint8_t* text, uint64_t len, int32_t delimiter, uint3
 /* Number of kernels the last matching call on this thread launched. */
 int rxg_last_launch_count(void);
 
+/* Process-wide tuning and test switches: they select kernel variants and
+ * table layouts (speed only, never results). value NULL or "" unsets. Names:
+ * RXG_NO_TMA, RXG_NO_LT, RXG_NO_FIXED_TMA (generic kernels), RXG_LINE_CHUNK
+ * (bytes per range), RXG_LT_SHAPE, RXG_CHUNK_SHAPE, RXG_TMA_PROMO,
+ * RXG_SKIP_SHARE, RXG_COL_BYTES, RXG_NO_ROW_PAIRS, RXG_FORCE_CLASS,
+ * RXG_NO_RANGE_LAYOUT, RXG_NO_PACKED. The library reads no environment. */
+int rxg_set_option(const char* name, const char* value);
+
 /* ── synthetic workloads of SURVEY.md §8(d) (host only) ───────────────── */
 int rxg_synth_pattern(char config, char* out, size_t cap, size_t* out_len);
 uint64_t rxg_synth_input_size(char config);

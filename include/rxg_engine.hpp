@@ -24,6 +24,7 @@
 #include <vector>
 
 #include "rxg.h"
+#include "rxg_utf8.hpp"
 
 namespace rxg {
 
@@ -42,28 +43,7 @@ struct HeapCache {
     ~HeapCache() { rxg_heap_destroy(h); }
 };
 
-inline std::string utf8_of(std::u32string_view w) {
-    std::string s;
-    s.reserve(w.size());
-    for (char32_t cp : w) {
-        if (cp < 0x80) {
-            s += static_cast<char>(cp);
-        } else if (cp < 0x800) {
-            s += static_cast<char>(0xC0 | (cp >> 6));
-            s += static_cast<char>(0x80 | (cp & 0x3F));
-        } else if (cp < 0x10000) {
-            s += static_cast<char>(0xE0 | (cp >> 12));
-            s += static_cast<char>(0x80 | ((cp >> 6) & 0x3F));
-            s += static_cast<char>(0x80 | (cp & 0x3F));
-        } else {
-            s += static_cast<char>(0xF0 | (cp >> 18));
-            s += static_cast<char>(0x80 | ((cp >> 12) & 0x3F));
-            s += static_cast<char>(0x80 | ((cp >> 6) & 0x3F));
-            s += static_cast<char>(0x80 | (cp & 0x3F));
-        }
-    }
-    return s;
-}
+inline std::string utf8_of(std::u32string_view w) { return rxg::symbols_to_bytes(w); }
 
 }  // namespace detail
 

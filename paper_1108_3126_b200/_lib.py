@@ -100,10 +100,15 @@ _SIG = {
                                       C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
     "rxg_shard_bounds": (C.c_int, [_P, C.c_uint64, C.c_int32, C.c_uint32, C.c_int, C.POINTER(C.c_uint64)]),
     "rxg_last_launch_count": (C.c_int, []),
+    "rxg_set_option": (C.c_int, [C.c_char_p, C.c_char_p]),
     "rxg_synth_pattern": (C.c_int, [C.c_char, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]),
     "rxg_synth_input_size": (C.c_uint64, [C.c_char]),
     "rxg_synth_input": (C.c_int, [C.c_char, C.c_uint64, _P, C.c_uint64, C.POINTER(C.c_uint64)]),
 }
+
+OPTION_NAMES = ("RXG_NO_TMA", "RXG_NO_LT", "RXG_NO_FIXED_TMA", "RXG_LINE_CHUNK", "RXG_LT_SHAPE", "RXG_CHUNK_SHAPE",
+                "RXG_TMA_PROMO", "RXG_SKIP_SHARE", "RXG_COL_BYTES", "RXG_NO_ROW_PAIRS", "RXG_FORCE_CLASS",
+                "RXG_NO_RANGE_LAYOUT", "RXG_NO_PACKED")
 
 _lib = None
 
@@ -122,6 +127,11 @@ def lib() -> C.CDLL:
             f.restype = res
             f.argtypes = args
         _lib = l
+        # dev/A-B convenience of the Python host only (the library reads no
+        # environment): RXG_* tuning switches set in the environment of a tool
+        for k in OPTION_NAMES:
+            if os.environ.get(k) and hasattr(l, "rxg_set_option"):
+                l.rxg_set_option(k.encode(), os.environ[k].encode())
     return _lib
 
 

@@ -10,6 +10,7 @@
 #include <string>
 #include <vector>
 
+#include "options.hpp"
 #include "rxg.h"
 #include "frontend.hpp"
 #include "launch.hpp"
@@ -362,7 +363,7 @@ int line_table(rxg_heap* h, int delim, TableSlot** out, std::shared_ptr<const Lt
         std::unique_ptr<TableSlot> slot;
         const int rc = upload(h, slot, make_line_table(h->prog, h->dfa, static_cast<uint8_t>(delim)));
         if (rc) return rc;
-        static const bool no_tma = std::getenv("RXG_NO_TMA") != nullptr;
+        const bool no_tma = rxg::option("RXG_NO_TMA") != nullptr;
         if (!no_tma)
             if (int rc2 = build_lt(h, delim, slot->lt)) return rc2;
         it = h->lines.emplace(delim, std::move(slot)).first;
@@ -373,7 +374,7 @@ int line_table(rxg_heap* h, int delim, TableSlot** out, std::shared_ptr<const Lt
 }
 
 uint32_t env_chunk() {
-    const char* e = std::getenv("RXG_LINE_CHUNK");   // tuning override (bytes per range)
+    const char* e = rxg::option("RXG_LINE_CHUNK");   // tuning override (bytes per range)
     return e ? static_cast<uint32_t>(std::strtoul(e, nullptr, 10)) : 0u;
 }
 
@@ -474,7 +475,7 @@ int batch_device(rxg_heap* h, const uint8_t* d_text, uint64_t len, int32_t delim
         TableSlot* slot = nullptr;
         std::shared_ptr<const LtTable> lt;
         if (int rc = line_table(h, delimiter, &slot, &lt)) return rc;
-        static const bool no_lt = std::getenv("RXG_NO_LT") != nullptr;   // generic kernel (tests)
+        const bool no_lt = rxg::option("RXG_NO_LT") != nullptr;   // generic kernel (tests)
         if (lt && lt->ok && !no_lt) {
             uint32_t chunk = env_chunk();
             if (chunk % lines_tma_slice()) chunk = 0;
@@ -520,7 +521,7 @@ int batch_device(rxg_heap* h, const uint8_t* d_text, uint64_t len, int32_t delim
         const DevTable* ta = nullptr;
         if (int rc = plain_table(h, &t, &ta)) return rc;
         cudaError_t e;
-        static const bool no_fixed_tma = std::getenv("RXG_NO_FIXED_TMA") != nullptr;   // tests
+        const bool no_fixed_tma = rxg::option("RXG_NO_FIXED_TMA") != nullptr;   // tests
         if (ta && fixed_tma_fits(ta->img_bytes, stride, h->smem_limit) && !no_fixed_tma) {
             uint64_t done = 0;
             const uint64_t n = len / stride;
@@ -960,7 +961,7 @@ int rxg_match_one_ex(rxg_heap* h, const uint8_t* d_bytes, uint64_t len, int engi
         const DevTable* t = nullptr;
         std::shared_ptr<const ChunkImage> ci;
         if (int rc = plain_table(h, &t, nullptr, &ci)) return rc;
-        static const bool no_tma = std::getenv("RXG_NO_TMA") != nullptr;
+        const bool no_tma = rxg::option("RXG_NO_TMA") != nullptr;
         if (ci && ci->lt.ok && !no_tma) {
             uint32_t chunk = o.chunk ? o.chunk : chunked_tma_auto_chunk(ci->lt, len, h->device);
             if (chunk % 32) return fail(RXG_EINVAL, "chunk must be a multiple of 32 on the TMA path");

@@ -1,6 +1,7 @@
 // Host front end: UTF-8, parser, heap layout. See frontend.hpp for the
 // reference correspondence of every entry point.
 #include "frontend.hpp"
+#include "rxg_utf8.hpp"
 
 #include <sstream>
 
@@ -47,21 +48,7 @@ std::u32string decode_utf8(std::string_view bytes) {
 
 std::string encode_utf8(char32_t cp) {
     std::string s;
-    if (cp < 0x80) {
-        s += static_cast<char>(cp);
-    } else if (cp < 0x800) {
-        s += static_cast<char>(0xC0 | (cp >> 6));
-        s += static_cast<char>(0x80 | (cp & 0x3F));
-    } else if (cp < 0x10000) {
-        s += static_cast<char>(0xE0 | (cp >> 12));
-        s += static_cast<char>(0x80 | ((cp >> 6) & 0x3F));
-        s += static_cast<char>(0x80 | (cp & 0x3F));
-    } else {
-        s += static_cast<char>(0xF0 | (cp >> 18));
-        s += static_cast<char>(0x80 | ((cp >> 12) & 0x3F));
-        s += static_cast<char>(0x80 | ((cp >> 6) & 0x3F));
-        s += static_cast<char>(0x80 | (cp & 0x3F));
-    }
+    rxg::append_utf8(s, cp);
     return s;
 }
 

@@ -18,6 +18,7 @@
 
 #include <cooperative_groups.h>
 
+#include "options.hpp"
 #include "chunked.hpp"
 #include "tma_common.cuh"
 
@@ -52,7 +53,7 @@ CUresult make_map(CUtensorMap* map, const uint8_t* text, uint64_t rows, uint32_t
                                   : slice == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE;
     // 128-byte slices: promote to 256 B so a row's next slice is already in L2
     CUtensorMapL2promotion promo = slice >= 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B : CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
-    if (const char* e = std::getenv("RXG_TMA_PROMO")) {   // tuning override
+    if (const char* e = rxg::option("RXG_TMA_PROMO")) {   // tuning override
         const int v = std::atoi(e);
         promo = v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
                 : v == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
@@ -81,10 +82,8 @@ using ShapeP = Shape<16, 1, 128, 3>;  // packed layout: 128-byte row slices, 256
 // not a multiple of 128 runs on the 32-byte ring.
 template <class F>
 auto with_shape(const LtTable& t, uint32_t chunk, F f) {
-    static const int force = [] {
-        const char* e = std::getenv("RXG_CHUNK_SHAPE");
-        return e ? std::atoi(e) : 0;
-    }();
+    const char* fe = rxg::option("RXG_CHUNK_SHAPE");
+    const int force = fe ? std::atoi(fe) : 0;
     if (force == 5 && chunk % 128 == 0) return f(Shape<12, 2, 128, 2>{});
     if (force == 1 || (t.packed && chunk % ShapeP::slice)) return f(ShapeA{});
     return t.packed ? f(ShapeP{}) : f(ShapeA{});

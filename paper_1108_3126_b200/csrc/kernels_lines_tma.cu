@@ -31,6 +31,7 @@
 #include <cstdlib>
 #include <cstring>
 
+#include "options.hpp"
 #include "launch.hpp"
 #include "lines_tma.hpp"
 #include "tma_common.cuh"
@@ -739,7 +740,7 @@ cudaError_t launch(const LtTable& t, const uint8_t* text, uint64_t len, uint8_t 
         const cuuint32_t box[2] = {static_cast<cuuint32_t>(C::slice), static_cast<cuuint32_t>(C::rows)};
         const cuuint32_t estr[2] = {1, 1};
         CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
-        if (const char* e = std::getenv("RXG_TMA_PROMO")) {   // tuning override
+        if (const char* e = rxg::option("RXG_TMA_PROMO")) {   // tuning override
             const int v = std::atoi(e);
             promo = v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
                     : v == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
@@ -777,7 +778,7 @@ using SC = Shape<16, 2, 32, 4>;
 using SR = Shape<16, 2, 32, 3>;
 
 int shape_id() {
-    const char* e = std::getenv("RXG_LT_SHAPE");
+    const char* e = rxg::option("RXG_LT_SHAPE");
     return e ? std::atoi(e) : -1;
 }
 

@@ -22,6 +22,7 @@
 #include <cstdlib>
 #include <cstring>
 
+#include "options.hpp"
 #include "lines_tma.hpp"
 
 namespace rxg {
@@ -61,7 +62,7 @@ std::vector<double> lt_sample_freq(const Program& p, const Dfa& d, uint8_t delim
     }
     const double mean_line = static_cast<double>(len) / static_cast<double>(lines ? lines : 1);
     double skip_share = std::min(0.5, mean_line / 2.0 / 4096.0);
-    if (const char* e = std::getenv("RXG_SKIP_SHARE")) skip_share = std::atof(e);   // A/B override (tools)
+    if (const char* e = rxg::option("RXG_SKIP_SHARE")) skip_share = std::atof(e);   // A/B override (tools)
     for (uint64_t i = 0; i < len; ++i) f[S * 256 + sample[i]] += skip_share;
     return f;
 }
@@ -131,7 +132,7 @@ std::vector<std::array<double, 32>> bank_hist(const std::vector<double>* f, uint
 }  // namespace
 
 uint32_t lt_choose_col_bytes(const std::vector<double>* f, uint32_t nrows) {
-    if (const char* e = std::getenv("RXG_COL_BYTES")) {   // A/B override (tools)
+    if (const char* e = rxg::option("RXG_COL_BYTES")) {   // A/B override (tools)
         const uint32_t v = static_cast<uint32_t>(std::atoi(e));
         if (v >= 4 && v % 2 == 0 && v <= 14) return v;
     }
@@ -183,7 +184,7 @@ RowPlacement lt_place_groups(const std::vector<double>* f, uint32_t nrows, uint3
     std::vector<uint32_t> order(nrows);
     for (uint32_t r = 0; r < nrows; ++r) order[r] = r;
     std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return tot[a] > tot[b]; });
-    const uint32_t per = group_rows && !std::getenv("RXG_NO_ROW_PAIRS") ? c / 2u : 1u;   // env: A/B switch (tools)
+    const uint32_t per = group_rows && !rxg::option("RXG_NO_ROW_PAIRS") ? c / 2u : 1u;   // env: A/B switch (tools)
     pl.npairs = (nrows + per - 1) / per;
     std::vector<std::array<double, 32>> HP(pl.npairs);
     std::vector<double> tp(pl.npairs, 0.0);
@@ -396,11 +397,11 @@ LtTable make_class_table(const Program& p, const Dfa& d, uint8_t delim, const st
 
 LtTable make_lines_tma_table(const Program& p, const Dfa& d, uint8_t delim, const std::vector<double>* freq,
                              bool force_class) {
-    force_class = force_class || std::getenv("RXG_FORCE_CLASS") != nullptr;   // tests: class layouts on small DFAs
+    force_class = force_class || rxg::option("RXG_FORCE_CLASS") != nullptr;   // tests: class layouts on small DFAs
     if (force_class || d.n_states > kLtDirectMaxStates) {
         // range-clamped columns when they fit (no class-map lookup per byte)
         uint32_t x = 0;
-        const uint32_t k = std::getenv("RXG_NO_RANGE_LAYOUT") ? 0 : range_cols(p, delim, 128, &x);
+        const uint32_t k = rxg::option("RXG_NO_RANGE_LAYOUT") ? 0 : range_cols(p, delim, 128, &x);
         if (k) {
             LtTable t = make_class_table(p, d, delim, freq, x, k);
             // the range kernel's 96 KB stage ring goes into the unused rows first
@@ -519,7 +520,7 @@ LtTable make_chunk_tma_table(const Program& p, const Dfa& d, const std::vector<d
         return static_cast<uint32_t>(d.next[static_cast<size_t>(s) * static_cast<size_t>(d.n_classes) + c]);
     };
     t.lo_addr = kLtSmemBase;
-    if (static_cast<int32_t>(S) <= kLtPackedMaxStates && !std::getenv("RXG_NO_PACKED")) {
+    if (static_cast<int32_t>(S) <= kLtPackedMaxStates && !rxg::option("RXG_NO_PACKED")) {
         // packed: the step is a variable shift of one per-byte word (no dependent
         // table load on the state chain), the word read from the lane's own bank
         t.packed = true;
@@ -560,7 +561,7 @@ LtTable make_chunk_tma_table(const Program& p, const Dfa& d, const std::vector<d
         t.cls = true;
         // range-clamped columns (no class map lookup) when the bytes that matter fit
         uint32_t rx = 0;
-        const uint32_t rk = std::getenv("RXG_NO_RANGE_LAYOUT") ? 0 : range_cols(p, 0xFF, 128, &rx, false);
+        const uint32_t rk = rxg::option("RXG_NO_RANGE_LAYOUT") ? 0 : range_cols(p, 0xFF, 128, &rx, false);
         t.range_x = rx;
         t.range_k = rk;
         auto class_of_col = [&](uint32_t c) -> uint32_t {

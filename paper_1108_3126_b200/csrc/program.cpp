@@ -1,6 +1,7 @@
 // Derived tables for the kernels. See program.hpp for the position form and
 // its correspondence with the reference lockstep machine.
 #include "program.hpp"
+#include "rxg_utf8.hpp"
 
 #include <cstring>
 #include <stdexcept>
@@ -72,23 +73,9 @@ struct Closure {
 };
 
 std::vector<uint8_t> utf8_bytes(uint32_t cp) {
-    std::vector<uint8_t> b;
-    if (cp < 0x80) {
-        b.push_back(static_cast<uint8_t>(cp));
-    } else if (cp < 0x800) {
-        b.push_back(static_cast<uint8_t>(0xC0 | (cp >> 6)));
-        b.push_back(static_cast<uint8_t>(0x80 | (cp & 0x3F)));
-    } else if (cp < 0x10000) {
-        b.push_back(static_cast<uint8_t>(0xE0 | (cp >> 12)));
-        b.push_back(static_cast<uint8_t>(0x80 | ((cp >> 6) & 0x3F)));
-        b.push_back(static_cast<uint8_t>(0x80 | (cp & 0x3F)));
-    } else {
-        b.push_back(static_cast<uint8_t>(0xF0 | (cp >> 18)));
-        b.push_back(static_cast<uint8_t>(0x80 | ((cp >> 12) & 0x3F)));
-        b.push_back(static_cast<uint8_t>(0x80 | ((cp >> 6) & 0x3F)));
-        b.push_back(static_cast<uint8_t>(0x80 | (cp & 0x3F)));
-    }
-    return b;
+    std::string s;
+    rxg::append_utf8(s, static_cast<char32_t>(cp));
+    return std::vector<uint8_t>(s.begin(), s.end());
 }
 
 // Rewrites the scalar position form into the UTF-8 byte position form.

@@ -335,6 +335,25 @@ class Matcher:
         return cnt.value, (res[:nstr] if res is not None else None), (None if bad.value == 2**64 - 1 else bad.value)
 
 
+def set_option(name: str, value=None):
+    """rxg_set_option: process-wide tuning / test switch (speed only; None unsets)."""
+    _check(L.lib().rxg_set_option(name.encode(), None if value is None else str(value).encode()))
+
+
+class option:
+    """Context manager: `with rx.option("RXG_NO_LT", 1): ...` sets a switch and restores it (unset) after."""
+
+    def __init__(self, name: str, value):
+        self.name, self.value = name, value
+
+    def __enter__(self):
+        set_option(self.name, self.value)
+        return self
+
+    def __exit__(self, *exc):
+        set_option(self.name, None)
+
+
 def _stream_ptr(stream):
     if stream is None:
         return None

@@ -216,10 +216,8 @@ def test_chunked_class_tables(layout):
     """Single strings whose minimal DFA exceeds the direct layout: the chunk
     kernel's class rows, with range-clamped columns or the class map, against
     the sequential walk and the oracle."""
-    import os
-
     if layout == "class":
-        os.environ["RXG_NO_RANGE_LAYOUT"] = "1"
+        rx.set_option("RXG_NO_RANGE_LAYOUT", 1)
     try:
         rng = np.random.default_rng(5)
         for p, alpha in [("(a|b)*a" + "(a|b)" * 6, b"ab"), (rx.synth_pattern("d"), b"abcdefghijklmnopqrstuvwxyz ")]:
@@ -233,7 +231,7 @@ def test_chunked_class_tables(layout):
                 if n == 1000:
                     assert want == O(p).accepts(w)
     finally:
-        os.environ.pop("RXG_NO_RANGE_LAYOUT", None)
+        rx.set_option("RXG_NO_RANGE_LAYOUT", None)
 
 
 def test_chunked_sticky_states_parallel_rounds():

@@ -65,19 +65,14 @@ def test_long_tailed_lines_all_range_sizes(key, chunk):
     pat = _pat(key)
     text = _long_tailed(len(key), 3 << 20, ALPHA[key])
     want, _ = Oracle(rx.compile(rx.parse(pat))).match_batch(text, 10, 0)
-    old = os.environ.get("RXG_LINE_CHUNK")
     try:
-        if chunk:
-            os.environ["RXG_LINE_CHUNK"] = chunk
+        rx.set_option("RXG_LINE_CHUNK", chunk)
         m = rx.Matcher(pat, device=0)
         assert _dev_count(m, text) == want
         c, r = m.match_batch(text, 10, results=True)
         assert c == want and int(r.sum()) == want
     finally:
-        if old is None:
-            os.environ.pop("RXG_LINE_CHUNK", None)
-        else:
-            os.environ["RXG_LINE_CHUNK"] = old
+        rx.set_option("RXG_LINE_CHUNK", None)
 
 
 @pytest.mark.parametrize("key", ["c", "abb", "empty_ok"])
@@ -120,17 +115,13 @@ def test_lines_on_range_boundaries(key, line_len):
         body[::3, 2:7] = kw
     text = body.reshape(-1)
     want, _ = Oracle(rx.compile(rx.parse(pat))).match_batch(text, 10, 0)
-    old = os.environ.get("RXG_LINE_CHUNK")
     try:
         for chunk in ("96", "4096"):
-            os.environ["RXG_LINE_CHUNK"] = chunk
+            rx.set_option("RXG_LINE_CHUNK", chunk)
             m = rx.Matcher(pat, device=0)
             assert _dev_count(m, text) == want, chunk
     finally:
-        if old is None:
-            os.environ.pop("RXG_LINE_CHUNK", None)
-        else:
-            os.environ["RXG_LINE_CHUNK"] = old
+        rx.set_option("RXG_LINE_CHUNK", None)
 
 
 def test_full_size_cross_engine_long_tailed():
@@ -159,12 +150,9 @@ def test_generic_line_kernel_results(key):
     want_c, want_r = Oracle(rx.compile(rx.parse(pat))).match_batch(text, 10, 0)
     m = rx.Matcher(pat, device=0)
     c1, r1 = m.match_batch(text, 10, results=True)
-    os.environ["RXG_NO_LT"] = "1"
-    try:
+    with rx.option("RXG_NO_LT", 1):
         c2, r2 = m.match_batch(text, 10, results=True)
         c3 = _dev_count(m, text)
-    finally:
-        os.environ.pop("RXG_NO_LT", None)
     assert c1 == c2 == c3 == want_c
     assert np.array_equal(r1, want_r) and np.array_equal(r2, want_r)
 
@@ -182,11 +170,8 @@ def test_fixed_stride_kernels(stride, n):
         want_c, want_r = Oracle(rx.compile(rx.parse(pat))).match_batch(text, -1, stride)
         m = rx.Matcher(pat, device=0)
         c1, r1 = m.match_batch(text, -1, stride, results=True)
-        os.environ["RXG_NO_FIXED_TMA"] = "1"
-        try:
+        with rx.option("RXG_NO_FIXED_TMA", 1):
             c2, r2 = m.match_batch(text, -1, stride, results=True)
-        finally:
-            os.environ.pop("RXG_NO_FIXED_TMA", None)
         assert c1 == c2 == want_c, (pat, c1, c2, want_c)
         assert np.array_equal(r1, want_r) and np.array_equal(r2, want_r)
 
@@ -318,15 +303,10 @@ def test_short_lines_results_every_offset(key, chunk):
         for p in rng.integers(0, len(text) - 5, 4000):
             text[p:p + 5] = np.frombuffer(b"ERROR", np.uint8)
     want_c, want_r = Oracle(rx.compile(rx.parse(pat))).match_batch(text, 10, 0)
-    old = os.environ.get("RXG_LINE_CHUNK")
     try:
-        if chunk:
-            os.environ["RXG_LINE_CHUNK"] = chunk
+        rx.set_option("RXG_LINE_CHUNK", chunk)
         m = rx.Matcher(pat, device=0)
         c, r = m.match_batch(text, 10, results=True)
         assert c == want_c and np.array_equal(r, want_r)
     finally:
-        if old is None:
-            os.environ.pop("RXG_LINE_CHUNK", None)
-        else:
-            os.environ["RXG_LINE_CHUNK"] = old
+        rx.set_option("RXG_LINE_CHUNK", None)

@@ -32,19 +32,18 @@ def _lines(seed, n=3000):
 
 
 class _env:
+    """Sets rxg_set_option switches for the block (the library reads no environment)."""
+
     def __init__(self, kv):
         self.kv = kv
 
     def __enter__(self):
-        self.old = {k: os.environ.get(k) for k in self.kv}
-        os.environ.update(self.kv)
+        for k, v in self.kv.items():
+            rx.set_option(k, v)
 
-    def __exit__(self, *a):
-        for k, v in self.old.items():
-            if v is None:
-                os.environ.pop(k, None)
-            else:
-                os.environ[k] = v
+    def __exit__(self, *exc):
+        for k in self.kv:
+            rx.set_option(k, None)
 
 
 @pytest.mark.parametrize("layout", list(LAYOUTS))

@@ -14,7 +14,7 @@ flush = torch.empty(512 << 20, dtype=torch.uint8, device=0)
 clean = torch.ones(256 << 20, dtype=torch.uint8, device=0)
 for variant in ("tma", "ldg"):
     if variant == "ldg":
-        os.environ["RXG_NO_FIXED_TMA"] = "1"
+        rx.set_option("RXG_NO_FIXED_TMA", 1)
     m = rx.Matcher(pat, device=0)
     for _ in range(3):
         m.match_batch_device(d, cnt, delimiter=-1, stride=32, nbytes=len(text))
@@ -33,4 +33,4 @@ for variant in ("tma", "ldg"):
             ts.append(e0.elapsed_time(e1) * 1e3)
         ts.sort()
         print(f"{variant:4s} {mode:5s} median {ts[len(ts)//2]:7.2f} us  min {ts[0]:7.2f} us  count={int(cnt.item())}", flush=True)
-    os.environ.pop("RXG_NO_FIXED_TMA", None)
+    rx.set_option("RXG_NO_FIXED_TMA", None)
