@@ -193,6 +193,11 @@ typedef struct rxg_one_opts {
     uint32_t* d_exit_state;           /* CHUNKED: the table state after the string (device, nullable). States
                                          are interchangeable between heaps of the same pattern built alike
                                          (same tuning); this is how segments of one string chain. */
+    unsigned long long* d_enqueued;   /* ROUNDS: rx::LockstepStats.enqueued of the same string (lockstep.hpp:16-18):
+                                         the addresses evolve enqueues = every macro step's claims but the
+                                         end-of-input step's */
+    uint32_t* d_schedule;             /* ROUNDS: nodes scheduled at the start of each macro step, len + 1 entries max
+                                         (rx::ParStats.schedule_sizes, parallel.hpp:57) */
 } rxg_one_opts;
 #define RXG_ONE_ENTRY 1u
 
@@ -259,6 +264,75 @@ int rxg_utf8_check_host(int device, const uint8_t* text, uint64_t len, int32_t d
  * The same device may appear more than once. */
 int rxg_match_one_multi(const int* devices, int ndev, const char* pattern, size_t plen, const uint8_t* text,
                         uint64_t len, int32_t* accept, int32_t* resegments);
+
+/* One string through the literal §8 protocol (RXG_ENGINE_ROUNDS, host buffer,
+ * synchronous) with the reference's instrumentation: rx::LockstepStats
+ * (lockstep.hpp:16-18) and rx::ParStats (parallel.hpp:52-58). schedule
+ * (host, nullable) receives one entry per macro step (len + 1 max);
+ * *schedule_len = entries. RXG_EUNSUPPORTED for non-ASCII literals. */
+typedef struct rxg_match_stats {
+    uint64_t enqueued;
+    uint64_t claims, launches, macro_steps;
+    uint32_t max_claims_per_node_step;
+    uint32_t* schedule;
+    uint64_t schedule_len;
+} rxg_match_stats;
+int rxg_match_one_stats(rxg_heap* h, const uint8_t* bytes, uint64_t len, int32_t* accept, rxg_match_stats* stats);
+
+/* ── the paper's protocol on caller-held state (parallel.hpp:24-103) ────
+ * rx::ParState in plain arrays: c / n stamps (N x int64: c[i] == t scheduled,
+ * -t claimed; n[j] == t + 1 scheduled next), claim counters (N x u32), the
+ * macro-step counter t and the four flags. rxg_par_task runs one par_task
+ * (parallel.cpp:50-78) on the device; rxg_par_run_rounds runs the rounds of
+ * one macro step (parallel.cpp:120-154: dispatch {i : c[i] == t} fixed per
+ * round, until no task schedules more work), *launches = rounds. Both copy
+ * the state in and out (host arrays); symbol 0xFFFFFFFF = end of input. */
+typedef struct rxg_par_state {
+    int64_t* c;
+    int64_t* n;
+    uint32_t* claim_count;
+    int64_t t;
+    int32_t more_c, any_n, accept_pending, accept_next;
+} rxg_par_state;
+int rxg_par_task(rxg_heap* h, rxg_par_state* st, int32_t node, uint32_t symbol);
+int rxg_par_run_rounds(rxg_heap* h, rxg_par_state* st, uint32_t symbol, uint64_t* launches);
+
+/* ── syntax trees (regex.hpp:26-66) and set-level functions (lockstep.hpp:24-49), host ──
+ * A tree is an array of nodes whose children precede them (kinds in
+ * rx::Regex::Kind order), one root, no sharing. */
+#define RXG_AST_EPS 0
+#define RXG_AST_CHR 1
+#define RXG_AST_STAR 2
+#define RXG_AST_SEQ 3
+#define RXG_AST_ALT 4
+typedef struct rxg_ast_node {
+    uint8_t kind;
+    uint8_t pad[3];
+    uint32_t sym;
+    int32_t left;
+    int32_t right;
+} rxg_ast_node;
+/* rx::parse (regex.cpp:186-194): *n_out nodes (min(n, cap) written), *root. */
+int rxg_parse_ast(const char* pattern, size_t len, rxg_ast_node* nodes, int32_t cap, int32_t* n_out, int32_t* root,
+                  size_t* err_pos);
+/* rx::print (regex.cpp:196-200) of a tree. */
+int rxg_print_ast(const rxg_ast_node* nodes, int32_t n, int32_t root, char* out, size_t cap, size_t* out_len);
+/* rx::compile (heap.cpp:13-72) of a tree: the heap has exactly n nodes. */
+int rxg_compile_ast(const rxg_ast_node* nodes, int32_t n, int32_t root, rxg_node* heap, int32_t* knodes,
+                    int32_t cap, int32_t* n_out);
+/* rx::evolve_ordered (lockstep.cpp:10-35): s = the set in std::set order
+ * (ascending, -1 = null first); out (capacity n) = Chr addresses in worklist
+ * discovery order; *enqueued += pushes (LockstepStats, nullable). */
+int rxg_evolve(const rxg_node* nodes, const int32_t* knodes, int32_t n, const int32_t* s, int32_t ns,
+               int32_t* out, int32_t* n_out, uint64_t* enqueued);
+/* rx::eps_reaches_null (lockstep.cpp:42-62). */
+int rxg_eps_reaches_null(const rxg_node* nodes, const int32_t* knodes, int32_t n, const int32_t* s, int32_t ns,
+                         int32_t* result);
+/* rx::step_char (lockstep.cpp:64-73): out (capacity ns) ascending; RXG_EINVAL
+ * when a member is neither a Chr node nor null (the reference throws
+ * std::invalid_argument). */
+int rxg_step_char(const rxg_node* nodes, const int32_t* knodes, int32_t n, const int32_t* s, int32_t ns, uint32_t a,
+                  int32_t* out, int32_t* n_out);
 
 /* ── several GPUs ────────────────────────────────────
  * Strings are independent: a batch is cut into contiguous byte-balanced

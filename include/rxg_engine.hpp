@@ -16,6 +16,7 @@
 // string of one compiled pattern back to back.
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
 #include <cstring>
 #include <stdexcept>
@@ -30,7 +31,7 @@ namespace rxg {
 
 struct EngineResult {
     bool accepted;
-    uint64_t steps;   // symbols consumed on the device (the engine's counter)
+    uint64_t steps;   // the lockstep engine's counter: rx::LockstepStats.enqueued (engines.cpp:60-64)
 };
 
 namespace detail {
@@ -44,6 +45,26 @@ struct HeapCache {
 };
 
 inline std::string utf8_of(std::u32string_view w) { return rxg::symbols_to_bytes(w); }
+
+// rx::LockstepStats.enqueued of lockstep_accepts(heap, w) from the C ABI's
+// set functions (lockstep.cpp:75-82 driving rxg_evolve / rxg_step_char).
+template <class HeapT>
+uint64_t enqueued_of(const HeapT& heap, std::u32string_view w) {
+    const auto* nodes = reinterpret_cast<const rxg_node*>(heap.nodes.data());
+    const int32_t n = static_cast<int32_t>(heap.nodes.size());
+    std::vector<int32_t> s{0}, e(static_cast<size_t>(n) + 1), t(static_cast<size_t>(n) + 1);
+    uint64_t enq = 0;
+    for (char32_t a : w) {
+        int32_t ne = 0, nt = 0;
+        if (rxg_evolve(nodes, heap.knodes.data(), n, s.data(), static_cast<int32_t>(s.size()), e.data(), &ne, &enq))
+            break;
+        std::sort(e.begin(), e.begin() + ne);
+        if (rxg_step_char(nodes, heap.knodes.data(), n, e.data(), ne, static_cast<uint32_t>(a), t.data(), &nt) || !nt)
+            break;
+        s.assign(t.begin(), t.begin() + nt);
+    }
+    return enq;
+}
 
 }  // namespace detail
 
@@ -78,10 +99,19 @@ EngineResult engine_run(const HeapT& heap, std::u32string_view w, int device = 0
     }
     const std::string b = detail::utf8_of(w);
     int32_t acc = 0;
-    // RXG_ENGINE_AUTO: memoized step when its table fits, else the thread-per-node bitset engine
+    if (engine == RXG_ENGINE_AUTO) {
+        // the literal §8 protocol kernel answers and counts in one launch: its
+        // claims per macro step are the addresses rx::evolve enqueues
+        rxg_match_stats ms{};
+        const int rc = rxg_match_one_stats(cache.h, reinterpret_cast<const uint8_t*>(b.data()), b.size(), &acc, &ms);
+        if (rc == RXG_OK) return {acc != 0, ms.enqueued};
+        if (rc != RXG_EUNSUPPORTED) raise(rc);
+    }
+    // memoized step when its table fits, else the thread-per-node bitset engine;
+    // the counter from the host set functions (non-ASCII literals only)
     const int rc = rxg_match_one(cache.h, reinterpret_cast<const uint8_t*>(b.data()), b.size(), engine, &acc);
     if (rc != RXG_OK) raise(rc);
-    return {acc != 0, static_cast<uint64_t>(w.size())};
+    return {acc != 0, detail::enqueued_of(heap, w)};
 }
 
 }  // namespace rxg

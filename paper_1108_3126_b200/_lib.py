@@ -45,7 +45,8 @@ class rxg_heap_info(C.Structure):
 class rxg_one_opts(C.Structure):
     _fields_ = [("checkpoint_every", C.c_uint32), ("d_checkpoints", C.c_void_p), ("d_stats", C.c_void_p),
                 ("d_trace", C.c_void_p), ("chunk", C.c_uint32), ("lookback", C.c_uint32), ("d_repairs", C.c_void_p),
-                ("flags", C.c_uint32), ("entry_state", C.c_uint32), ("d_exit_state", C.c_void_p)]
+                ("flags", C.c_uint32), ("entry_state", C.c_uint32), ("d_exit_state", C.c_void_p),
+                ("d_enqueued", C.c_void_p), ("d_schedule", C.c_void_p)]
 
 
 # name -> (restype, argtypes). Every symbol declared in include/rxg.h.
@@ -101,6 +102,16 @@ _SIG = {
     "rxg_shard_bounds": (C.c_int, [_P, C.c_uint64, C.c_int32, C.c_uint32, C.c_int, C.POINTER(C.c_uint64)]),
     "rxg_last_launch_count": (C.c_int, []),
     "rxg_set_option": (C.c_int, [C.c_char_p, C.c_char_p]),
+    "rxg_match_one_stats": (C.c_int, [_P, _P, C.c_uint64, C.POINTER(C.c_int32), _P]),
+    "rxg_par_task": (C.c_int, [_P, _P, C.c_int32, C.c_uint32]),
+    "rxg_par_run_rounds": (C.c_int, [_P, _P, C.c_uint32, C.POINTER(C.c_uint64)]),
+    "rxg_parse_ast": (C.c_int, [C.c_char_p, C.c_size_t, _P, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                                C.POINTER(C.c_size_t)]),
+    "rxg_print_ast": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]),
+    "rxg_compile_ast": (C.c_int, [_P, C.c_int32, C.c_int32, _P, _P, C.c_int32, C.POINTER(C.c_int32)]),
+    "rxg_evolve": (C.c_int, [_P, _P, C.c_int32, _P, C.c_int32, _P, C.POINTER(C.c_int32), C.POINTER(C.c_uint64)]),
+    "rxg_eps_reaches_null": (C.c_int, [_P, _P, C.c_int32, _P, C.c_int32, C.POINTER(C.c_int32)]),
+    "rxg_step_char": (C.c_int, [_P, _P, C.c_int32, _P, C.c_int32, C.c_uint32, _P, C.POINTER(C.c_int32)]),
     "rxg_synth_pattern": (C.c_int, [C.c_char, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]),
     "rxg_synth_input_size": (C.c_uint64, [C.c_char]),
     "rxg_synth_input": (C.c_int, [C.c_char, C.c_uint64, _P, C.c_uint64, C.POINTER(C.c_uint64)]),

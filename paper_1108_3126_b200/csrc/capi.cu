@@ -1007,7 +1007,8 @@ int rxg_match_one_ex(rxg_heap* h, const uint8_t* d_bytes, uint64_t len, int engi
         if (h->prog.scalar_pos) return fail(RXG_EUNSUPPORTED, "the literal rounds engine compares bytes: ASCII literals only");
         const RoundsTables* t = nullptr;
         if (int rc = rounds_tables(h, &t)) return rc;
-        const cudaError_t e = launch_rounds(*t, d_bytes, len, d_accept, o.d_stats, o.d_trace, st);
+        const cudaError_t e = launch_rounds(*t, d_bytes, len, d_accept, o.d_stats, o.d_trace, st, o.d_enqueued,
+                                            o.d_schedule);
         if (e != cudaSuccess) return cuda_fail(e, "launch_rounds");
         g_launches = 1;
         return RXG_OK;
@@ -1015,6 +1016,102 @@ int rxg_match_one_ex(rxg_heap* h, const uint8_t* d_bytes, uint64_t len, int engi
     default:
         return fail(RXG_EINVAL, "unknown engine");
     }
+}
+
+int rxg_par_task(rxg_heap* h, rxg_par_state* st, int32_t node, uint32_t symbol);
+int rxg_par_run_rounds(rxg_heap* h, rxg_par_state* st, uint32_t symbol, uint64_t* launches);
+
+namespace {
+
+// One k_par launch on a copy of the caller's ParState (single >= 0: par_task).
+int par_call(rxg_heap* h, rxg_par_state* st, uint32_t symbol, int32_t single, uint64_t* launches) {
+    if (int rc = need_device(h, false)) return rc;
+    if (!st || !st->c || !st->n || !st->claim_count) return fail(RXG_EINVAL, "bad state");
+    const RoundsTables* t = nullptr;
+    if (int rc = rounds_tables(h, &t)) return rc;
+    if (single >= t->n) return fail(RXG_EINVAL, "node out of range");
+    std::lock_guard<std::mutex> host_lock(h->host_mu);
+    DeviceGuard g(h->device);
+    const size_t N = static_cast<size_t>(t->n);
+    const size_t bytes = 2 * N * 8 + N * 4 + 4 * 4 + 8;
+    uint8_t* d = nullptr;
+    RXG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d), bytes, h->stream));
+    auto* dc = reinterpret_cast<long long*>(d);
+    auto* dn = dc + N;
+    auto* dl = reinterpret_cast<unsigned long long*>(dn + N);
+    auto* dflags = reinterpret_cast<int*>(dl + 1);
+    auto* dclaims = reinterpret_cast<uint32_t*>(dflags + 4);
+    int flags[4] = {st->more_c, st->any_n, st->accept_pending, st->accept_next};
+    unsigned long long nl = 0;
+    cudaError_t e = cudaMemcpyAsync(dc, st->c, N * 8, cudaMemcpyHostToDevice, h->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(dn, st->n, N * 8, cudaMemcpyHostToDevice, h->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(dclaims, st->claim_count, N * 4, cudaMemcpyHostToDevice, h->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(dflags, flags, sizeof(flags), cudaMemcpyHostToDevice, h->stream);
+    if (e == cudaSuccess) e = launch_par(*t, dc, dn, dclaims, dflags, st->t, symbol, single, dl, h->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(st->c, dc, N * 8, cudaMemcpyDeviceToHost, h->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(st->n, dn, N * 8, cudaMemcpyDeviceToHost, h->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(st->claim_count, dclaims, N * 4, cudaMemcpyDeviceToHost, h->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(flags, dflags, sizeof(flags), cudaMemcpyDeviceToHost, h->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&nl, dl, 8, cudaMemcpyDeviceToHost, h->stream);
+    cudaFreeAsync(d, h->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "k_par");
+    st->more_c = flags[0];
+    st->any_n = flags[1];
+    st->accept_pending = flags[2];
+    st->accept_next = flags[3];
+    if (launches) *launches = single >= 0 ? 0 : nl;
+    g_launches = 1;
+    return RXG_OK;
+}
+
+}  // namespace
+
+int rxg_match_one_stats(rxg_heap* h, const uint8_t* bytes, uint64_t len, int32_t* accept, rxg_match_stats* stats) {
+    if (int rc = need_device(h, false)) return rc;
+    if (!accept || !stats || (!bytes && len)) return fail(RXG_EINVAL, "bad arguments");
+    if (h->prog.scalar_pos) return fail(RXG_EUNSUPPORTED, "the literal rounds engine compares bytes: ASCII literals only");
+    const RoundsTables* t = nullptr;
+    if (int rc = rounds_tables(h, &t)) return rc;
+    std::lock_guard<std::mutex> host_lock(h->host_mu);
+    DeviceGuard g(h->device);
+    // [accept | 5 counters | text | schedule]
+    const size_t sched = stats->schedule ? (len + 1) * 4 : 0;
+    const size_t off_text = 64, bytes_all = off_text + ((len + 16 + 15) & ~size_t(15)) + sched;
+    uint8_t* d = nullptr;
+    RXG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d), bytes_all, h->stream));
+    auto* d_acc = reinterpret_cast<int32_t*>(d);
+    auto* d_cnt = reinterpret_cast<unsigned long long*>(d + 8);   // claims, rounds, steps, maxc, enqueued
+    uint8_t* d_text = d + off_text;
+    auto* d_sched = stats->schedule ? reinterpret_cast<uint32_t*>(d + off_text + ((len + 16 + 15) & ~size_t(15))) : nullptr;
+    unsigned long long host[5] = {0, 0, 0, 0, 0};
+    cudaError_t e = len ? cudaMemcpyAsync(d_text, bytes, len, cudaMemcpyHostToDevice, h->stream) : cudaSuccess;
+    if (e == cudaSuccess) e = launch_rounds(*t, d_text, len, d_acc, d_cnt, nullptr, h->stream, d_cnt + 4, d_sched);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(accept, d_acc, 4, cudaMemcpyDeviceToHost, h->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(host, d_cnt, sizeof(host), cudaMemcpyDeviceToHost, h->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+    if (e == cudaSuccess && d_sched && host[2])
+        e = cudaMemcpy(stats->schedule, d_sched, host[2] * 4, cudaMemcpyDeviceToHost);
+    cudaFreeAsync(d, h->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "rxg_match_one_stats");
+    stats->claims = host[0];
+    stats->launches = host[1];
+    stats->macro_steps = host[2];
+    stats->max_claims_per_node_step = static_cast<uint32_t>(host[3]);
+    stats->enqueued = host[4];
+    stats->schedule_len = d_sched ? host[2] : 0;
+    g_launches = 1;
+    return RXG_OK;
+}
+
+int rxg_par_task(rxg_heap* h, rxg_par_state* st, int32_t node, uint32_t symbol) {
+    if (node < 0) return fail(RXG_EINVAL, "node out of range");
+    return par_call(h, st, symbol, node, nullptr);
+}
+
+int rxg_par_run_rounds(rxg_heap* h, rxg_par_state* st, uint32_t symbol, uint64_t* launches) {
+    return par_call(h, st, symbol, -1, launches);
 }
 
 int rxg_match_one_device(rxg_heap* h, const uint8_t* d_bytes, uint64_t len, int engine, int32_t* d_accept,

@@ -45,6 +45,8 @@ struct RoundsArgs {
     unsigned long long* stats;   // [claims, rounds, macro_steps, max_claims_per_node_step] or null
     uint32_t* trace;             // per symbol: next-schedule bitset ((N+1+31)/32 words, bit N = null), or null
     uint32_t trace_words;
+    unsigned long long* enqueued;   // rx::LockstepStats.enqueued of the same run, or null (see below)
+    uint32_t* schedule;             // per macro step: nodes scheduled at its start (ParStats.schedule_sizes), or null
 };
 
 enum : uint8_t { kEps = 0, kChr = 1, kAlt = 2, kSeq = 3, kStar = 4 };
@@ -57,8 +59,8 @@ __global__ void __launch_bounds__(1024) k_rounds(const __grid_constant__ RoundsA
     int32_t* n = c + N;
     uint32_t* claims = reinterpret_cast<uint32_t*>(n + N);
     __shared__ int more, accept_pending, accept_next, any_n;
-    __shared__ unsigned long long s_claims, s_rounds, s_steps;
-    __shared__ uint32_t s_maxc;
+    __shared__ unsigned long long s_claims, s_rounds, s_steps, s_step_claims, s_eoi_claims;
+    __shared__ uint32_t s_maxc, s_sched;
     for (int32_t i = threadIdx.x; i < N; i += blockDim.x) {
         c[i] = 0;
         n[i] = 0;
@@ -66,16 +68,27 @@ __global__ void __launch_bounds__(1024) k_rounds(const __grid_constant__ RoundsA
     }
     if (threadIdx.x == 0) {
         accept_pending = accept_next = any_n = 0;
-        s_claims = s_rounds = s_steps = 0;
-        s_maxc = 0;
+        s_claims = s_rounds = s_steps = s_step_claims = s_eoi_claims = 0;
+        s_maxc = s_sched = 0;
     }
     __syncthreads();
     int32_t t = 1;
     if (threadIdx.x == 0) c[0] = t;   // schedule_root (parallel.cpp:14-17)
     int32_t* cur = c;
     int32_t* nxt = n;
+    const bool instrument = a.stats || a.enqueued || a.schedule;
     for (uint64_t pos = 0; pos <= a.len; ++pos) {
         const uint32_t sym = pos < a.len ? static_cast<uint32_t>(a.text[pos]) : kEndOfInput;
+        if (a.schedule) {   // |current_schedule()| at the macro step's start (parallel.cpp:160-161)
+            uint32_t k = 0;
+            for (int32_t i = threadIdx.x; i < N; i += blockDim.x) k += cur[i] == t;
+            atomicAdd(&s_sched, k);
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                a.schedule[pos] = s_sched;
+                s_sched = 0;
+            }
+        }
         // run_rounds (parallel.cpp:120-154)
         for (;;) {
             __syncthreads();
@@ -129,7 +142,7 @@ __global__ void __launch_bounds__(1024) k_rounds(const __grid_constant__ RoundsA
             if (!more) break;
         }
         // macro boundary: instrumentation + optional trace of the next schedule
-        if (a.stats) {
+        if (instrument) {
             uint32_t local = 0, mx = 0;
             for (int32_t i = threadIdx.x; i < N; i += blockDim.x) {
                 local += claims[i];
@@ -137,8 +150,19 @@ __global__ void __launch_bounds__(1024) k_rounds(const __grid_constant__ RoundsA
                 claims[i] = 0;
             }
             atomicAdd(&s_claims, static_cast<unsigned long long>(local));
+            atomicAdd(&s_step_claims, static_cast<unsigned long long>(local));
             atomicMax(&s_maxc, mx);
-            if (threadIdx.x == 0) ++s_steps;
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                ++s_steps;
+                // the claims of one macro step are exactly the addresses
+                // rx::evolve enqueues for the same set (both walk the eps
+                // graph from S once, stopping at Chr nodes), so
+                // LockstepStats.enqueued = every step's claims but the
+                // end-of-input step's, which lockstep_accepts never runs
+                if (pos == a.len) s_eoi_claims = s_step_claims;
+                s_step_claims = 0;
+            }
         }
         if (a.trace && pos < a.len) {
             uint32_t* row = a.trace + pos * a.trace_words;
@@ -176,7 +200,94 @@ __global__ void __launch_bounds__(1024) k_rounds(const __grid_constant__ RoundsA
             a.stats[2] = s_steps;
             a.stats[3] = s_maxc;
         }
+        if (a.enqueued) *a.enqueued = s_claims - s_eoi_claims;
     }
+}
+
+// ── k_par: one par_task or one run_rounds on caller-held state ──────────
+//
+// The reference's ParState (parallel.hpp:24-41) lives with the caller
+// (int64 c/n stamps, claim counters, flags); this kernel applies either one
+// par_task (parallel.cpp:50-78) to node `single`, or run_rounds
+// (parallel.cpp:120-154): rounds over the dispatch list {i : c[i] == t},
+// fixed at each round's start, until no task schedules more work. One CTA,
+// one thread per node (strided), CAS claims on the global int64 stamps.
+struct ParArgs {
+    const uint8_t* kind;
+    const uint32_t* sym;
+    const int32_t* left;
+    const int32_t* right;
+    const int32_t* knode;
+    int32_t n;
+    long long* c;
+    long long* nx;
+    uint32_t* claims;
+    int* flags;                  // more_c, any_n, accept_pending, accept_next
+    long long t;
+    uint32_t symbol;             // kEndOfInput: every Chr test fails
+    int32_t single;              // >= 0: one par_task on this node; < 0: run_rounds
+    unsigned long long* launches;
+};
+
+__device__ void par_task_dev(const ParArgs& a, int32_t i) {
+    const long long t = a.t;
+    if (atomicCAS(reinterpret_cast<unsigned long long*>(&a.c[i]), static_cast<unsigned long long>(t),
+                  static_cast<unsigned long long>(-t)) != static_cast<unsigned long long>(t))
+        return;
+    atomicAdd(&a.claims[i], 1u);
+    const uint8_t k = a.kind[i];
+    if (k == kChr) {
+        if (a.symbol != kEndOfInput && a.sym[i] == a.symbol) {
+            const int32_t j = a.knode[i];
+            if (j < 0) atomicExch(&a.flags[3], 1);
+            else atomicExch(reinterpret_cast<unsigned long long*>(&a.nx[j]), static_cast<unsigned long long>(t + 1));
+            atomicExch(&a.flags[1], 1);
+        }
+        return;
+    }
+    int32_t succ[2];
+    int ns = 0;
+    if (k == kAlt) { succ[0] = a.left[i]; succ[1] = a.right[i]; ns = 2; }
+    else if (k == kSeq) { succ[0] = a.left[i]; ns = 1; }
+    else if (k == kStar) { succ[0] = a.left[i]; succ[1] = a.knode[i]; ns = 2; }
+    else { succ[0] = a.knode[i]; ns = 1; }
+    for (int e = 0; e < ns; ++e) {
+        const int32_t q = succ[e];
+        if (q < 0) {
+            atomicExch(&a.flags[2], 1);
+            continue;
+        }
+        const long long v = *reinterpret_cast<volatile long long*>(&a.c[q]);
+        if (v == t || v == -t) continue;   // already scheduled or simulated
+        *reinterpret_cast<volatile long long*>(&a.c[q]) = t;   // racing stores write the same value
+        atomicExch(&a.flags[0], 1);
+    }
+}
+
+__global__ void __launch_bounds__(1024) k_par(const __grid_constant__ ParArgs a) {
+    if (a.single >= 0) {
+        if (threadIdx.x == 0) par_task_dev(a, a.single);
+        return;
+    }
+    __shared__ unsigned long long launch;
+    if (threadIdx.x == 0) launch = 0;
+    for (;;) {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            a.flags[0] = 0;   // more_c
+            ++launch;
+        }
+        uint32_t mine = 0;   // the dispatch list, fixed at the round start
+        for (int32_t i = threadIdx.x, b = 0; i < a.n; i += blockDim.x, ++b)
+            if (*reinterpret_cast<volatile long long*>(&a.c[i]) == a.t) mine |= 1u << b;
+        __syncthreads();
+        for (int32_t i = threadIdx.x, b = 0; i < a.n; i += blockDim.x, ++b)
+            if ((mine >> b) & 1u) par_task_dev(a, i);
+        __threadfence_block();
+        __syncthreads();
+        if (!*reinterpret_cast<volatile int*>(&a.flags[0])) break;
+    }
+    if (threadIdx.x == 0) *a.launches = launch;
 }
 
 // ── k_pernode (K1) ───────────────────────────────────────────────────────
@@ -562,8 +673,30 @@ __global__ void __launch_bounds__(256) k_delim_count(const uint8_t* __restrict__
 
 }  // namespace
 
+cudaError_t launch_par(const RoundsTables& t, long long* c, long long* n, uint32_t* claims, int* flags, long long tt,
+                       uint32_t symbol, int32_t single, unsigned long long* launches, cudaStream_t st) {
+    ParArgs a{};
+    a.kind = t.kind;
+    a.sym = t.sym;
+    a.left = t.left;
+    a.right = t.right;
+    a.knode = t.knode;
+    a.n = t.n;
+    a.c = c;
+    a.nx = n;
+    a.claims = claims;
+    a.flags = flags;
+    a.t = tt;
+    a.symbol = symbol;
+    a.single = single;
+    a.launches = launches;
+    k_par<<<1, 1024, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_rounds(const RoundsTables& t, const uint8_t* text, uint64_t len, int32_t* accept,
-                          unsigned long long* stats, uint32_t* trace, cudaStream_t st) {
+                          unsigned long long* stats, uint32_t* trace, cudaStream_t st,
+                          unsigned long long* enqueued, uint32_t* schedule) {
     RoundsArgs a{};
     a.text = text;
     a.len = len;
@@ -577,6 +710,8 @@ cudaError_t launch_rounds(const RoundsTables& t, const uint8_t* text, uint64_t l
     a.stats = stats;
     a.trace = trace;
     a.trace_words = static_cast<uint32_t>((t.n + 1 + 31) / 32);
+    a.enqueued = enqueued;
+    a.schedule = schedule;
     const uint32_t smem = static_cast<uint32_t>(t.n) * 12u;
     cudaError_t e = cudaFuncSetAttribute(k_rounds, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;

@@ -33,8 +33,18 @@ constexpr int32_t kRoundsMaxNodes = 32 * 1024;   // one CTA of 1024 threads, <= 
 
 // stats (device, 4 x u64, nullable): claims, rounds, macro steps, max claims per node per step.
 // trace (device, zeroed, nullable): per symbol the next schedule as (N+1)-bit rows, bit N = null.
+// enqueued (device u64, nullable): rx::LockstepStats.enqueued of the same
+// string (every macro step's claims but the end-of-input step's);
+// schedule (device, len + 1 x u32, nullable): ParStats.schedule_sizes.
 cudaError_t launch_rounds(const RoundsTables& t, const uint8_t* text, uint64_t len, int32_t* accept,
-                          unsigned long long* stats, uint32_t* trace, cudaStream_t st);
+                          unsigned long long* stats, uint32_t* trace, cudaStream_t st,
+                          unsigned long long* enqueued = nullptr, uint32_t* schedule = nullptr);
+
+// One par_task (single >= 0) or one run_rounds (single < 0) on caller-held
+// ParState arrays in device memory: c, n (int64 x N), claims (u32 x N),
+// flags {more_c, any_n, accept_pending, accept_next}; *launches = rounds.
+cudaError_t launch_par(const RoundsTables& t, long long* c, long long* n, uint32_t* claims, int* flags, long long tt,
+                       uint32_t symbol, int32_t single, unsigned long long* launches, cudaStream_t st);
 
 // every > 0: E after every `every` symbols into checkpoints ((len/every) x W words).
 cudaError_t launch_pernode(const PernodeTables& t, const uint8_t* text, uint64_t len, uint32_t every,

@@ -28,3 +28,21 @@ def test_facade_front_end(binary):
 def test_facade_matching_on_gpu(binary):
     r = subprocess.run([str(binary), "gpu"], capture_output=True, text=True)
     assert r.returncode == 0, r.stderr + r.stdout
+
+
+REF_TESTS = ROOT / "oracle" / "_ref" / "ref_api_tests"
+
+
+@pytest.mark.gpu
+def test_reference_unit_suites_against_facade():
+    """The reference's own tests/test_lockstep.cpp and tests/test_parallel.cpp
+    (compiled unmodified from the reference sources by oracle/Makefile, with
+    <rx/*.hpp> resolving to include/rx_b200.hpp) pass on the GPU: evolve /
+    step_char / eps_reaches_null goldens, acceptance, LockstepStats.enqueued
+    work bound, par_task claim-once, macro steps, ParStats counters and
+    par_report."""
+    if not REF_TESTS.exists():
+        pytest.skip("oracle/_ref/ref_api_tests not built (needs /root/reference at build time)")
+    r = subprocess.run([str(REF_TESTS)], capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-4000:] + r.stdout[-4000:]
+    assert " 0 failures" in r.stdout
