@@ -42,6 +42,12 @@ class rxg_heap_info(C.Structure):
                 ("line_tma_layout", C.c_int32), ("line_col_bytes", C.c_int32), ("chunk_lookback", C.c_int32)]
 
 
+class rxg_match_stats(C.Structure):
+    _fields_ = [("enqueued", C.c_uint64), ("claims", C.c_uint64), ("launches", C.c_uint64),
+                ("macro_steps", C.c_uint64), ("max_claims_per_node_step", C.c_uint32),
+                ("schedule", C.POINTER(C.c_uint32)), ("schedule_len", C.c_uint64)]
+
+
 class rxg_one_opts(C.Structure):
     _fields_ = [("checkpoint_every", C.c_uint32), ("d_checkpoints", C.c_void_p), ("d_stats", C.c_void_p),
                 ("d_trace", C.c_void_p), ("chunk", C.c_uint32), ("lookback", C.c_uint32), ("d_repairs", C.c_void_p),
@@ -102,7 +108,7 @@ _SIG = {
     "rxg_shard_bounds": (C.c_int, [_P, C.c_uint64, C.c_int32, C.c_uint32, C.c_int, C.POINTER(C.c_uint64)]),
     "rxg_last_launch_count": (C.c_int, []),
     "rxg_set_option": (C.c_int, [C.c_char_p, C.c_char_p]),
-    "rxg_match_one_stats": (C.c_int, [_P, _P, C.c_uint64, C.POINTER(C.c_int32), _P]),
+    "rxg_match_one_stats": (C.c_int, [_P, _P, C.c_uint64, C.POINTER(C.c_int32), C.POINTER(rxg_match_stats)]),
     "rxg_par_task": (C.c_int, [_P, _P, C.c_int32, C.c_uint32]),
     "rxg_par_run_rounds": (C.c_int, [_P, _P, C.c_uint32, C.POINTER(C.c_uint64)]),
     "rxg_parse_ast": (C.c_int, [C.c_char_p, C.c_size_t, _P, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32),

@@ -18,7 +18,7 @@ BUILD = ROOT / "build" / "rxg"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-Wall", f"-I{ROOT / 'include'}", f"-I{CSRC}"]
 SOURCES = ["frontend.cpp", "program.cpp", "tables.cpp", "lines_tma_table.cpp", "synth.cpp",
-           "kernels_batch.cu", "kernels_lines_tma.cu", "kernels_single.cu", "kernels_pernode.cu", "kernels_chunked.cu", "kernels_chunk_tma.cu", "kernels_many.cu", "kernels_utf8.cu", "kernels_fixed_tma.cu",
+           "kernels_batch.cu", "kernels_lines_tma.cu", "kernels_single.cu", "kernels_pernode.cu", "kernels_chunked.cu", "kernels_chunk_tma.cu", "kernels_many.cu", "kernels_utf8.cu", "kernels_fixed_tma.cu", "kernels_bits_tma.cu",
            "capi.cu", "multi.cu", "options.cpp", "setops.cpp"]
 
 

@@ -280,6 +280,30 @@ int pernode_tables(rxg_heap* h, const PernodeTables** out) {
     return RXG_OK;
 }
 
+// K2b tables on the TMA data path (null image if the position set is too
+// wide for a lane or the shared window does not start at 0x400).
+int bits_image(rxg_heap* h, std::shared_ptr<const BitsImage>* out) {
+    std::lock_guard<std::mutex> lk(h->mu);
+    if (!h->bits_built) {
+        h->bits_built = true;
+        auto b = std::make_shared<BitsImage>();
+        b->t = make_bits_tables(h->prog);
+        if (b->t.ok && h->tma_ok) {
+            void* d = nullptr;
+            const size_t ib = b->t.img.size() * 4, rb = b->t.regs.size() * 4;
+            RXG_CUDA(cudaMalloc(&d, ib + rb));
+            h->allocs.push_back(d);
+            RXG_CUDA(h2d(d, b->t.img.data(), ib));
+            RXG_CUDA(h2d(static_cast<uint8_t*>(d) + ib, b->t.regs.data(), rb));
+            b->d_img = d;
+            b->d_regs = reinterpret_cast<const uint32_t*>(static_cast<uint8_t*>(d) + ib);
+            h->bits = std::move(b);
+        }
+    }
+    *out = h->bits;
+    return RXG_OK;
+}
+
 // (Re)build and publish the TMA chunk-parallel table of the plain slot
 // (caller holds h->mu; the previous image stays allocated, see ChunkImage).
 int build_chunk_lt(rxg_heap* h) {
@@ -1143,7 +1167,28 @@ int batch_any(rxg_heap* h, const uint8_t* d_text, uint64_t len, int32_t delimite
               unsigned long long* d_count, uint8_t* d_results, cudaStream_t st, bool zero_count) {
     const bool bitset = engine == RXG_BATCH_BITSET || (engine == RXG_BATCH_AUTO && !h->dfa_ok);
     if (!bitset) return batch_device(h, d_text, len, delimiter, stride, d_count, d_results, st, zero_count);
-    if (delimiter < 0 || delimiter > 255) return fail(RXG_EUNSUPPORTED, "the bitset batch engine takes delimited lines");
+    if (delimiter > 255) return fail(RXG_EINVAL, "delimiter must be a byte");
+    std::shared_ptr<const BitsImage> bi;
+    if (int rc = bits_image(h, &bi)) return rc;
+    const bool no_bits_tma = rxg::option("RXG_NO_BITS_TMA") != nullptr;   // tests: the warp-per-line kernel
+    if (bi && !no_bits_tma) {
+        if (delimiter < 0 && (stride == 0 || len % stride)) return fail(RXG_EINVAL, "fixed stride must divide the buffer length");
+        if (reinterpret_cast<uintptr_t>(d_text) & 15) return fail(RXG_EINVAL, "text must be 16-byte aligned");
+        CountSlot cs;
+        if (int rc = stream_slot(h, st, &cs, !zero_count)) return rc;
+        const uint32_t chunk = bits_chunk(*bi, len, delimiter, stride, 0);
+        if (chunk == 0) return fail(RXG_EUNSUPPORTED, "stride too large for the bitset engine's ranges");
+        const size_t sb = d_results ? bits_scratch_bytes(len, chunk, delimiter >= 0, true) : 0;
+        void* scratch = nullptr;
+        if (sb) RXG_CUDA(cudaMallocAsync(&scratch, sb, st));
+        const cudaError_t e = launch_bits(*bi, d_text, len, delimiter, stride, chunk, d_count, d_results, scratch, sb,
+                                          cs, st);
+        if (scratch) cudaFreeAsync(scratch, st);
+        if (e != cudaSuccess) return cuda_fail(e, "launch_bits");
+        g_launches = len ? (d_results && delimiter >= 0 ? 3 : 1) : 0;
+        return RXG_OK;
+    }
+    if (delimiter < 0) return fail(RXG_EUNSUPPORTED, "fixed stride needs the memoized step or the TMA bitset engine");
     const PernodeTables* t = nullptr;
     if (int rc = pernode_tables(h, &t)) return rc;
     if (zero_count) RXG_CUDA(write_u64(d_count, 0, st));

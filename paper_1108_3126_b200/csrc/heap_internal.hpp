@@ -14,6 +14,7 @@
 
 #include "rxg.h"
 #include "launch.hpp"
+#include "bits.hpp"
 #include "lines_tma.hpp"
 #include "pernode.hpp"
 #include "program.hpp"
@@ -74,6 +75,8 @@ struct rxg_heap {
     rxg::RoundsTables rounds;
     void* d_pernode = nullptr;
     rxg::PernodeTables pernode;
+    std::shared_ptr<const rxg::BitsImage> bits;   // K2b on the TMA path (null until first use)
+    bool bits_built = false;
     // Per stream, keyed by cudaStreamGetId (so cudaStreamPerThread from two
     // threads gives two keys): the CountSlot (launch.hpp, zero when idle), the
     // chunked engine's seam arrival counters (zero when idle, grow-only) and

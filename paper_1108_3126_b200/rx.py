@@ -283,6 +283,20 @@ class Matcher:
         _check(L.lib().rxg_match_one(self._h, p, n, L.ENGINES[engine], C.byref(acc)))
         return bool(acc.value)
 
+    def lockstep_stats(self, w):
+        """One string through the literal §8 protocol kernel with the reference's
+        instrumentation -> (accepted, {enqueued, claims, launches, macro_steps,
+        max_claims_per_node_step, schedule_sizes})."""
+        p, n, keep = _ptr(w)
+        sched = (C.c_uint32 * (n + 1))()
+        st = L.rxg_match_stats()
+        st.schedule = C.cast(sched, C.POINTER(C.c_uint32))
+        acc = C.c_int32(0)
+        _check(L.lib().rxg_match_one_stats(self._h, p, n, C.byref(acc), C.byref(st)))
+        return bool(acc.value), {"enqueued": st.enqueued, "claims": st.claims, "launches": st.launches,
+                                 "macro_steps": st.macro_steps, "max_claims_per_node_step": st.max_claims_per_node_step,
+                                 "schedule_sizes": list(sched[: st.schedule_len])}
+
     def match_one_ex(self, d_text, d_accept, engine: str = "auto", stream=None, nbytes: int | None = None, **opts):
         """Async single-string match with engine options / instrumentation (device tensors):
         checkpoint_every + d_checkpoints (pernode), d_stats / d_trace (rounds), chunk / lookback / d_repairs (chunked)."""
