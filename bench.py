@@ -538,8 +538,10 @@ def bench_batch(ctx, cfg: str, steps: int, warmup: int, headline: bool, engine: 
     return rec
 
 
-def bench_single(ctx, cfg: str, steps: int, warmup: int, headline: bool) -> dict:
-    """One long string (replicas only when N > 1)."""
+def bench_single(ctx, cfg: str, steps: int, warmup: int, headline: bool, engine: str | None = None) -> dict:
+    """One long string (replicas only when N > 1). engine: single-string engine
+    ("auto" = the chunk-parallel memoized step; "pernode" = K1, the paper's
+    thread-per-node scheme, segmented across SMs)."""
     from paper_1108_3126_b200 import _lib, rx
 
     torch = ctx.torch
@@ -554,7 +556,7 @@ def bench_single(ctx, cfg: str, steps: int, warmup: int, headline: bool) -> dict
     d_acc = torch.zeros(1, dtype=torch.int32, device=ctx.dev)
     stream = torch.cuda.current_stream(ctx.dev)
     flush, l2 = make_flush(ctx, nb)
-    engine = ctx.args.engine
+    engine = engine or ctx.args.engine
 
     def step():
         m.match_one_device(d_text[:nb], d_acc, engine=engine, stream=stream)
@@ -587,7 +589,7 @@ def bench_single(ctx, cfg: str, steps: int, warmup: int, headline: bool) -> dict
         "roofline": roofline(nb, info["words"], local, traffic, cfg, ctx.dev),
         "gpu_launches": launches * steps,
     }
-    if not ctx.args.no_e2e:
+    if not ctx.args.no_e2e and engine == "auto":
         w = host.numpy()
         m.lockstep_accepts(w)   # warm
         k = max(1, steps // 2)
@@ -597,7 +599,7 @@ def bench_single(ctx, cfg: str, steps: int, warmup: int, headline: bool) -> dict
         t = ctx.max_over_ranks((time.perf_counter() - t0) / k)
         rec["e2e"] = {"value": ctx.world * nb / t / 1e9, "unit": "GB/s", "h2d_bytes_per_step": nb,
                       "d2h_bytes_per_step": 4, "host_buffer": "pinned"}
-    if ctx.rank == 0 and ctx.world == 1 and not ctx.args.no_cpu:
+    if ctx.rank == 0 and ctx.world == 1 and not ctx.args.no_cpu and engine == "auto":
         rec["cpu_baseline"] = cpu_record(cfg, pattern, text, ctx.args.cpu_target_s if headline else ctx.args.sub_cpu_s)
     return rec
 
@@ -611,7 +613,8 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--engine", default="auto", help="single-string engine (a, e)")
     ap.add_argument("--batch-engine", default="auto", choices=["auto", "bitset"], help="batch engine (b, c, d)")
-    ap.add_argument("--bitset-subs", default="", help="extra forced-bitset sub-records, e.g. 'cd'")
+    ap.add_argument("--bitset-subs", default="cd", help="forced-bitset (K2b) sub-records at N=1 ('' = none)")
+    ap.add_argument("--k1-subs", default="e", help="K1 (engine=pernode) sub-records at N=1 ('' = none)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline legs")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-sub", action="store_true", help="headline config only (no sub-records)")
@@ -646,6 +649,12 @@ def main():
                 subs[c + "_bitset"] = run(c, False, "bitset")
             except Exception as e:  # noqa: BLE001
                 subs[c + "_bitset"] = {"error": repr(e)}
+            ctx.torch.cuda.empty_cache()
+        for c in args.k1_subs:   # the paper's thread-per-node scheme on the single-string configs
+            try:
+                subs[c + "_k1"] = bench_single(ctx, c, max(2, args.steps // 4), 2, False, engine="pernode")
+            except Exception as e:  # noqa: BLE001
+                subs[c + "_k1"] = {"error": repr(e)}
             ctx.torch.cuda.empty_cache()
     if ctx.rank == 0:
         line = {

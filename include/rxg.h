@@ -63,7 +63,9 @@ extern "C" {
 /* single-string engines (rxg_match_one*) */
 #define RXG_ENGINE_AUTO 0     /* memoized step (chunk-parallel) when its table fits, else PERNODE */
 #define RXG_ENGINE_DFA_SEQ 1  /* one thread walks the memoized step table */
-#define RXG_ENGINE_PERNODE 2  /* K1: paper §8 thread-per-node lockstep, bitset form, one CTA */
+#define RXG_ENGINE_PERNODE 2  /* K1: paper §8 thread-per-node lockstep, bitset form, one warp per
+                                 string; strings of 1 MiB and more as segments across SMs (warp per
+                                 segment, guessed entry sets, exact repair rounds; cooperative launch) */
 #define RXG_ENGINE_ROUNDS 3   /* literal §8 protocol: one thread per heap node, c/n stamps, rounds */
 #define RXG_ENGINE_CHUNKED 4  /* chunk-parallel walk of the step table (all SMs) */
 
@@ -200,6 +202,7 @@ typedef struct rxg_one_opts {
                                          (rx::ParStats.schedule_sizes, parallel.hpp:57) */
 } rxg_one_opts;
 #define RXG_ONE_ENTRY 1u
+#define RXG_ONE_SINGLE_WARP 2u   /* PERNODE: walk a long string with one warp (no segments) */
 
 int rxg_match_one_ex(rxg_heap* h, const uint8_t* d_bytes, uint64_t len, int engine, int32_t* d_accept,
                      const rxg_one_opts* opts, void* stream);

@@ -14,17 +14,24 @@ constexpr int32_t kBitsMaxWords = 16;                 // position set per lane: 
 constexpr uint32_t kBitsMaxTableBytes = 96 * 1024;    // shared-memory image budget
 
 // Bitset step tables in the kernel's bit order (positions 0..n_pos-1, the
-// accept bit A at bit 32*WT - 1). img: M[256][WT] (the positions each byte
-// matches), then for WT > 4 the loop-invariant rows (regs), then the (T, R)
-// rows of groups >= GR. regs: SH[WT], E0[WT], GR x (T[WT], R[WT]).
+// accept bit A at bit 32*WT - 1), for one delimiter (-1: fixed stride).
+// WT <= 4: one row per byte [M&SH, M&T_0, M&T_1, D] (M = the positions the
+//   byte matches, SH = positions whose follow is the next position, T_g =
+//   positions whose residual follow row is R_g, D = all ones on the
+//   delimiter), then the byte class map and per class M&T_g for groups
+//   g >= 2, then R_g (g >= 2);
+//   regs = E0, R_0, R_1 (kept in registers).
+// WT 8, 16: one row per byte [M, D, pad]; then SH, E0 and (T_g, R_g) for
+//   every group, read as shared-memory broadcasts.
 struct BitsTables {
     bool ok = false;
     int32_t WT = 0, G = 0, GR = 2;
+    uint32_t row_words = 0, xt_row_words = 0;
     std::vector<uint32_t> img, regs;
-    uint32_t regs_off = 0, xg_off = 0;   // byte offsets in img
+    uint32_t cmap_off = 0, xt_off = 0, xg_off = 0;   // byte offsets in img
 };
 
-BitsTables make_bits_tables(const Program& p);
+BitsTables make_bits_tables(const Program& p, int32_t delim);
 
 // Device copies (owned by the heap).
 struct BitsImage {

@@ -282,12 +282,14 @@ int pernode_tables(rxg_heap* h, const PernodeTables** out) {
 
 // K2b tables on the TMA data path (null image if the position set is too
 // wide for a lane or the shared window does not start at 0x400).
-int bits_image(rxg_heap* h, std::shared_ptr<const BitsImage>* out) {
+int bits_image(rxg_heap* h, int32_t delimiter, std::shared_ptr<const BitsImage>* out) {
+    const int key = delimiter < 0 ? -1 : delimiter;
     std::lock_guard<std::mutex> lk(h->mu);
-    if (!h->bits_built) {
-        h->bits_built = true;
+    auto it = h->bits.find(key);
+    if (it == h->bits.end()) {
+        it = h->bits.emplace(key, nullptr).first;
         auto b = std::make_shared<BitsImage>();
-        b->t = make_bits_tables(h->prog);
+        b->t = make_bits_tables(h->prog, key);
         if (b->t.ok && h->tma_ok) {
             void* d = nullptr;
             const size_t ib = b->t.img.size() * 4, rb = b->t.regs.size() * 4;
@@ -297,10 +299,10 @@ int bits_image(rxg_heap* h, std::shared_ptr<const BitsImage>* out) {
             RXG_CUDA(h2d(static_cast<uint8_t*>(d) + ib, b->t.regs.data(), rb));
             b->d_img = d;
             b->d_regs = reinterpret_cast<const uint32_t*>(static_cast<uint8_t*>(d) + ib);
-            h->bits = std::move(b);
+            it->second = std::move(b);
         }
     }
-    *out = h->bits;
+    *out = it->second;
     return RXG_OK;
 }
 
@@ -1022,7 +1024,21 @@ int rxg_match_one_ex(rxg_heap* h, const uint8_t* d_bytes, uint64_t len, int engi
         const PernodeTables* t = nullptr;
         if (int rc = pernode_tables(h, &t)) return rc;
         if (o.checkpoint_every && !o.d_checkpoints) return fail(RXG_EINVAL, "checkpoint buffer missing");
-        const cudaError_t e = launch_pernode(*t, d_bytes, len, o.checkpoint_every, o.d_checkpoints, d_accept, st);
+        // long strings without checkpoints: segments across SMs (stream-ordered scratch)
+        PernodeSegScratch ss;
+        void* sbuf = nullptr;
+        const bool seg = !o.checkpoint_every && len >= kPernodeSegMin && !(o.flags & RXG_ONE_SINGLE_WARP);
+        if (seg) {
+            RXG_CUDA(cudaMallocAsync(&sbuf, pernode_seg_scratch_bytes(t->W), st));
+            ss.entry = static_cast<uint32_t*>(sbuf);
+            ss.exits = ss.entry + kPernodeMaxSegs * static_cast<size_t>(t->W);
+            ss.changed = reinterpret_cast<unsigned int*>(ss.exits + 2 * kPernodeMaxSegs * static_cast<size_t>(t->W));
+            ss.max_segs = kPernodeMaxSegs;
+            RXG_CUDA(cudaMemsetAsync(ss.changed, 0, 16, st));
+        }
+        const cudaError_t e = launch_pernode(*t, d_bytes, len, o.checkpoint_every, o.d_checkpoints, d_accept, st,
+                                             seg ? &ss : nullptr);
+        if (sbuf) cudaFreeAsync(sbuf, st);
         if (e != cudaSuccess) return cuda_fail(e, "launch_pernode");
         g_launches = 1;
         return RXG_OK;
@@ -1169,7 +1185,7 @@ int batch_any(rxg_heap* h, const uint8_t* d_text, uint64_t len, int32_t delimite
     if (!bitset) return batch_device(h, d_text, len, delimiter, stride, d_count, d_results, st, zero_count);
     if (delimiter > 255) return fail(RXG_EINVAL, "delimiter must be a byte");
     std::shared_ptr<const BitsImage> bi;
-    if (int rc = bits_image(h, &bi)) return rc;
+    if (int rc = bits_image(h, delimiter, &bi)) return rc;
     const bool no_bits_tma = rxg::option("RXG_NO_BITS_TMA") != nullptr;   // tests: the warp-per-line kernel
     if (bi && !no_bits_tma) {
         if (delimiter < 0 && (stride == 0 || len % stride)) return fail(RXG_EINVAL, "fixed stride must divide the buffer length");
@@ -1239,7 +1255,6 @@ int host_batch(rxg_heap* h, const uint8_t* text, uint64_t len, int32_t delimiter
                uint8_t* results, uint64_t* utf8_first_bad) {
     if (int rc = need_device(h, false)) return rc;
     if (utf8_first_bad && delimiter > 127) return fail(RXG_EINVAL, "UTF-8 check needs an ASCII delimiter");
-    if (!h->dfa_ok && delimiter < 0) return fail(RXG_ETOOBIG, "memoized step table over the cap (fixed stride needs it)");
     std::lock_guard<std::mutex> host_lock(h->host_mu);
     if (!text && len) return fail(RXG_EINVAL, "bad arguments");
     if (delimiter < 0 && (stride == 0 || len % stride)) return fail(RXG_EINVAL, "fixed stride must divide the buffer length");

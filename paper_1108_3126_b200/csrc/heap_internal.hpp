@@ -75,8 +75,8 @@ struct rxg_heap {
     rxg::RoundsTables rounds;
     void* d_pernode = nullptr;
     rxg::PernodeTables pernode;
-    std::shared_ptr<const rxg::BitsImage> bits;   // K2b on the TMA path (null until first use)
-    bool bits_built = false;
+    // K2b tables on the TMA path per delimiter (-1: fixed stride); a null entry: not supported
+    std::map<int, std::shared_ptr<const rxg::BitsImage>> bits;
     // Per stream, keyed by cudaStreamGetId (so cudaStreamPerThread from two
     // threads gives two keys): the CountSlot (launch.hpp, zero when idle), the
     // chunked engine's seam arrival counters (zero when idle, grow-only) and

@@ -38,7 +38,7 @@ namespace rxg {
 
 // ── host tables ───────────────────────────────────────────────────────────
 
-BitsTables make_bits_tables(const Program& p) {
+BitsTables make_bits_tables(const Program& p, int32_t delim) {
     BitsTables t;
     const int32_t Wsrc = p.W;
     int32_t wt = (p.n_pos + 1 + 31) / 32;   // A gets bit 32*wt - 1 (>= n_pos)
@@ -52,7 +52,6 @@ BitsTables make_bits_tables(const Program& p) {
             if ((src[q >> 5] >> (q & 31)) & 1u) dst[q >> 5] |= 1u << (q & 31);
         if ((src[p.n_pos >> 5] >> (p.n_pos & 31)) & 1u) dst[A >> 5] |= 1u << (A & 31);
     };
-    auto set = [&](std::vector<uint32_t>& v, size_t row, int32_t bit) { v[row * WT + (bit >> 5)] |= 1u << (bit & 31); };
     // follow rows F'(q) in the kernel bit order
     std::vector<uint32_t> fol(static_cast<size_t>(p.n_pos) * WT, 0u);
     for (int32_t q = 0; q < p.n_pos; ++q) remap(&p.follow[static_cast<size_t>(q) * Wsrc], &fol[static_cast<size_t>(q) * WT]);
@@ -80,32 +79,81 @@ BitsTables make_bits_tables(const Program& p) {
             rows.insert(rows.end(), resid.begin(), resid.end());
             trig.insert(trig.end(), WT, 0u);
         }
-        set(trig, static_cast<size_t>(it->second), q);
+        trig[static_cast<size_t>(it->second) * WT + (q >> 5)] |= 1u << (q & 31);
     }
-    t.GR = t.G <= 2 ? 2 : 4;
-    // shared-memory image: M[256][WT]; for WT > 4 also SH, E0 and the first GR
-    // groups (broadcast reads); then groups >= GR as (T, R) pairs
+    t.GR = 2;
     std::vector<uint32_t> E0(WT, 0u);
     remap(p.init.data(), E0.data());
-    std::vector<uint32_t>& img = t.img;
-    img.assign(static_cast<size_t>(256) * WT, 0u);
+    std::vector<uint32_t> M(static_cast<size_t>(256) * WT, 0u);
     for (int b = 0; b < 256; ++b) {
         const int32_t c = p.byte_class[b];
-        if (c) remap(&p.class_mask[static_cast<size_t>(c) * Wsrc], &img[static_cast<size_t>(b) * WT]);
-        for (int32_t w = 0; w < WT; ++w) img[static_cast<size_t>(b) * WT + w] &= ~(w == A >> 5 ? 1u << (A & 31) : 0u);
+        if (c && b != delim) remap(&p.class_mask[static_cast<size_t>(c) * Wsrc], &M[static_cast<size_t>(b) * WT]);
+        M[static_cast<size_t>(b) * WT + (A >> 5)] &= ~(1u << (A & 31));   // A matches no byte
     }
-    auto group_rows = [&](int32_t g, std::vector<uint32_t>& out) {   // T then R of group g (zero past G)
-        for (int32_t w = 0; w < WT; ++w) out.push_back(g < t.G ? trig[static_cast<size_t>(g) * WT + w] : 0u);
-        for (int32_t w = 0; w < WT; ++w) out.push_back(g < t.G ? rows[static_cast<size_t>(g) * WT + w] : 0u);
-    };
-    std::vector<uint32_t>& regs = t.regs;   // SH, E0, then GR x (T, R)
-    regs.insert(regs.end(), SH.begin(), SH.end());
-    regs.insert(regs.end(), E0.begin(), E0.end());
-    for (int32_t g = 0; g < t.GR; ++g) group_rows(g, regs);
-    t.regs_off = static_cast<uint32_t>(img.size()) * 4;
-    if (WT > 4) img.insert(img.end(), regs.begin(), regs.end());
-    t.xg_off = static_cast<uint32_t>(img.size()) * 4;
-    for (int32_t g = t.GR; g < t.G; ++g) group_rows(g, img);
+    auto tg = [&](int32_t g, int32_t w) { return g < t.G ? trig[static_cast<size_t>(g) * WT + w] : 0u; };
+    auto rg = [&](int32_t g, int32_t w) { return g < t.G ? rows[static_cast<size_t>(g) * WT + w] : 0u; };
+    std::vector<uint32_t>& img = t.img;
+    if (WT <= 4) {
+        // per byte: [M & SH, M & T_0, M & T_1, D (all ones on the delimiter), pad], then
+        // the extra groups' rows M & T_g (g >= 2) per byte; R_g (g >= 2) after them
+        t.row_words = (3 * WT + 1 + 3) / 4 * 4;
+        img.assign(static_cast<size_t>(256) * t.row_words, 0u);
+        for (int b = 0; b < 256; ++b) {
+            uint32_t* r = &img[static_cast<size_t>(b) * t.row_words];
+            for (int32_t w = 0; w < WT; ++w) {
+                const uint32_t m = M[static_cast<size_t>(b) * WT + w];
+                r[w] = m & SH[w];
+                r[WT + w] = m & tg(0, w);
+                r[2 * WT + w] = m & tg(1, w);
+            }
+            r[3 * WT] = b == delim ? ~0u : 0u;
+        }
+        // extra groups: the byte -> class map (one byte each), then per class M & T_g
+        t.cmap_off = static_cast<uint32_t>(img.size()) * 4;
+        for (int b = 0; b < 256; b += 4) {
+            uint32_t wd = 0;
+            for (int k = 0; k < 4; ++k) wd |= static_cast<uint32_t>(b + k == delim ? 0 : p.byte_class[b + k]) << (8 * k);
+            img.push_back(wd);
+        }
+        t.xt_off = static_cast<uint32_t>(img.size()) * 4;
+        const int32_t xg = t.G > 2 ? t.G - 2 : 0;
+        t.xt_row_words = (xg * WT + 3) / 4 * 4;
+        if (xg) {
+            for (int32_t c = 0; c < p.n_classes; ++c) {
+                std::vector<uint32_t> m(WT, 0u), r(t.xt_row_words, 0u);
+                if (c) remap(&p.class_mask[static_cast<size_t>(c) * Wsrc], m.data());
+                m[A >> 5] &= ~(1u << (A & 31));
+                for (int32_t g = 2; g < t.G; ++g)
+                    for (int32_t w = 0; w < WT; ++w) r[(g - 2) * WT + w] = m[w] & tg(g, w);
+                img.insert(img.end(), r.begin(), r.end());
+            }
+        }
+        t.xg_off = static_cast<uint32_t>(img.size()) * 4;
+        for (int32_t g = 2; g < t.G; ++g)
+            for (int32_t w = 0; w < WT; ++w) img.push_back(rg(g, w));
+        // registers: E0, R_0, R_1
+        t.regs.insert(t.regs.end(), E0.begin(), E0.end());
+        for (int32_t g = 0; g < 2; ++g)
+            for (int32_t w = 0; w < WT; ++w) t.regs.push_back(rg(g, w));
+    } else {
+        // per byte: [M, D, pad 3] (the 4-word pad skews rows across banks);
+        // broadcast rows SH, E0, then (T_g, R_g) for every group
+        t.row_words = WT + 4;
+        img.assign(static_cast<size_t>(256) * t.row_words, 0u);
+        for (int b = 0; b < 256; ++b) {
+            uint32_t* r = &img[static_cast<size_t>(b) * t.row_words];
+            for (int32_t w = 0; w < WT; ++w) r[w] = M[static_cast<size_t>(b) * WT + w];
+            r[WT] = b == delim ? ~0u : 0u;
+        }
+        t.xg_off = static_cast<uint32_t>(img.size()) * 4;
+        img.insert(img.end(), SH.begin(), SH.end());
+        img.insert(img.end(), E0.begin(), E0.end());
+        for (int32_t g = 0; g < std::max(t.G, 2); ++g) {
+            for (int32_t w = 0; w < WT; ++w) img.push_back(tg(g, w));
+            for (int32_t w = 0; w < WT; ++w) img.push_back(rg(g, w));
+        }
+    }
+    if (t.regs.empty()) t.regs.push_back(0u);
     while (img.size() % 4) img.push_back(0u);
     t.ok = img.size() * 4 <= kBitsMaxTableBytes;
     return t;
@@ -125,11 +173,14 @@ struct BArgs {
     uint32_t stride;                  // fixed-stride strings (0: lines)
     uint32_t delim4;                  // delimiter in every byte
     int32_t n_groups;
+    uint32_t two;         // the constant 2 (a register operand keeps IMAD on the FMA pipe)
     const uint4* img;
     uint32_t img_words;   // 16-byte units
     uint32_t tab;         // shared address of M
-    uint32_t regs;        // shared address of SH, E0, groups < GR (WT > 4)
-    uint32_t xg;          // shared address of groups >= GR
+    uint32_t cmap;        // shared address of the byte -> class map (extra groups, WT <= 4)
+    uint32_t xt;          // shared address of the extra groups' per-class M & T_g rows (WT <= 4)
+    uint32_t xt_row_bytes;
+    uint32_t xg;          // shared address of the extra R_g rows (WT <= 4) / the broadcast rows (WT > 4)
     const uint32_t* regs_g;   // the same rows in global memory (WT <= 4: loaded into registers)
     uint32_t bar_addr;
     uint32_t stage_addr[kMaxSlots];
@@ -146,32 +197,27 @@ struct Shape {
     static constexpr uint32_t stage_bytes = static_cast<uint32_t>(rows * SL);
 };
 
-// Loop-invariant rows: registers (REG) or shared-memory broadcasts.
+// Loop-invariant rows: E0 and R_0, R_1 in registers (REG, WT <= 4), or the
+// broadcast area of shared memory (SH, E0, then T_g, R_g per group).
 template <int WT, int GR, bool REG>
 struct Rows {
-    uint32_t sh[REG ? WT : 1], e0[REG ? WT : 1], tr[REG ? GR : 1][REG ? WT : 1], rr[REG ? GR : 1][REG ? WT : 1];
-    uint32_t base;   // !REG: shared address of SH, E0, groups
+    uint32_t e0[REG ? WT : 1], rr[REG ? 2 : 1][REG ? WT : 1];
+    uint32_t base;   // !REG: shared address of the broadcast rows
 
     __device__ void load(const BArgs& a) {
         if constexpr (REG) {
             const uint32_t* g = a.regs_g;
 #pragma unroll
             for (int w = 0; w < WT; ++w) {
-                sh[w] = __ldg(g + w);
-                e0[w] = __ldg(g + WT + w);
+                e0[w] = __ldg(g + w);
+                rr[0][w] = __ldg(g + WT + w);
+                rr[1][w] = __ldg(g + 2 * WT + w);
             }
-#pragma unroll
-            for (int k = 0; k < GR; ++k)
-#pragma unroll
-                for (int w = 0; w < WT; ++w) {
-                    tr[k][w] = __ldg(g + 2 * WT + k * 2 * WT + w);
-                    rr[k][w] = __ldg(g + 2 * WT + k * 2 * WT + WT + w);
-                }
         } else {
-            base = a.regs;
+            base = a.xg;
         }
     }
-    // word w of row r (0 SH, 1 E0, 2+2k T_k, 3+2k R_k); shared rows are read 4 words at a time
+    // words 4*w4 .. 4*w4+3 of broadcast row r (0 SH, 1 E0, 2+2g T_g, 3+2g R_g)
     __device__ __forceinline__ void get4(int r, int w4, uint32_t (&out)[4]) const {
         const uint4 v = tma::lds128(base + (r * WT + w4 * 4) * 4);
         out[0] = v.x;
@@ -181,18 +227,19 @@ struct Rows {
     }
 };
 
-template <int WT>
-__device__ __forceinline__ void load_row(uint32_t addr, uint32_t (&m)[WT]) {
-    if constexpr (WT == 1) {
+template <int N>
+__device__ __forceinline__ void load_words(uint32_t addr, uint32_t (&m)[N]) {
+    if constexpr (N == 1) {
         m[0] = tma::lds32(addr);
-    } else if constexpr (WT == 2) {
+    } else if constexpr (N == 2) {
         uint32_t x, y;
         asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(x), "=r"(y) : "r"(addr));
         m[0] = x;
         m[1] = y;
     } else {
+        static_assert(N % 4 == 0, "rows are loaded 16 bytes at a time");
 #pragma unroll
-        for (int w = 0; w < WT; w += 4) {
+        for (int w = 0; w < N; w += 4) {
             const uint4 v = tma::lds128(addr + 4 * w);
             m[w] = v.x;
             m[w + 1] = v.y;
@@ -202,26 +249,85 @@ __device__ __forceinline__ void load_row(uint32_t addr, uint32_t (&m)[WT]) {
     }
 }
 
-// One bitset step on byte b (m = all ones when b ends the string: count the
-// accept bit of E, then restart from E0).
-template <int WT, int GR, bool REG>
-__device__ __forceinline__ void bstep(const BArgs& a, const Rows<WT, GR, REG>& R, uint32_t (&E)[WT], uint32_t row_addr,
-                                      uint32_t m, uint32_t& cnt) {
-    uint32_t M[WT];
-    load_row<WT>(row_addr, M);
-    uint32_t f[WT], nx[WT];
-#pragma unroll
-    for (int w = 0; w < WT; ++w) f[w] = E[w] & M[w];
-    // shift part
-    if constexpr (REG) {
+// Row width in words (BitsTables::row_words).
+template <int WT>
+__host__ __device__ constexpr int row_words() {
+    return WT <= 4 ? (3 * WT + 1 + 3) / 4 * 4 : WT + 4;
+}
+
+// The REG step on a row already loaded (rows of several bytes are loaded
+// ahead: they depend on the input only, not on E).
+template <int WT, int GR, bool REG, bool XG>
+__device__ __forceinline__ void bstep_row(const BArgs& a, const Rows<WT, GR, REG>& R, uint32_t (&E)[WT],
+                                          const uint32_t (&row)[row_words<WT>()], uint32_t row_addr, uint32_t cm,
+                                          uint32_t& m, uint32_t& cnt) {
+    constexpr int RW = row_words<WT>();
+    uint32_t nx[WT];
+    {
+        // shift part: E & M & SH moved up one position
         uint32_t prev = 0;
 #pragma unroll
         for (int w = 0; w < WT; ++w) {
-            const uint32_t s = f[w] & R.sh[w];
-            nx[w] = __funnelshift_l(prev, s, 1);
-            prev = s;
+            const uint32_t sh = E[w] & row[w];
+            // (a register 2, not a literal: keeps the shift an IMAD on the FMA pipe)
+            nx[w] = WT == 1 ? sh * a.two : __funnelshift_l(prev, sh, 1);
+            prev = sh;
         }
+        // the two register groups: any E & M & T_g fires R_g
+        uint32_t acc0 = 0, acc1 = 0;
+#pragma unroll
+        for (int w = 0; w < WT; ++w) {
+            acc0 |= E[w] & row[WT + w];
+            acc1 |= E[w] & row[2 * WT + w];
+        }
+#pragma unroll
+        for (int w = 0; w < WT; ++w) {
+            if (acc0) nx[w] |= R.rr[0][w];
+            if (acc1) nx[w] |= R.rr[1][w];
+        }
+        if constexpr (XG) {   // groups >= 2: per-class M & T_g rows, R_g broadcast
+            const uint32_t b = (row_addr - a.tab) / (RW * 4u);
+            (void)RW;
+            uint32_t cls;
+            asm("ld.shared.u8 %0, [%1];" : "=r"(cls) : "r"(a.cmap + b));
+            const uint32_t xt = a.xt + cls * a.xt_row_bytes;
+            for (int g = 2; g < a.n_groups; ++g) {
+                uint32_t acc = 0;
+#pragma unroll
+                for (int w = 0; w < WT; ++w) acc |= E[w] & tma::lds32(xt + ((g - 2) * WT + w) * 4u);
+                if (acc) {
+#pragma unroll
+                    for (int w = 0; w < WT; ++w) nx[w] |= tma::lds32(a.xg + ((g - 2) * WT + w) * 4u);
+                }
+            }
+        }
+    }
+    const uint32_t D = row[3 * WT];
+    // string end: count A (bit 31 of the last word) on the FMA pipe, restart from E0
+    cnt += __umulhi(E[WT - 1] & D & cm, a.two);
+#pragma unroll
+    for (int w = 0; w < WT; ++w) E[w] = (nx[w] & ~D) | (R.e0[w] & D);
+    m = D;
+}
+
+// One bitset step on the byte whose table row is at row_addr. On the
+// delimiter (the row's D word, returned in m) the accept bit of E is counted
+// (masked by cm) and E restarts from E0.
+template <int WT, int GR, bool REG, bool XG>
+__device__ __forceinline__ void bstep(const BArgs& a, const Rows<WT, GR, REG>& R, uint32_t (&E)[WT], uint32_t row_addr,
+                                      uint32_t cm, uint32_t& m, uint32_t& cnt) {
+    if constexpr (REG) {
+        uint32_t row[row_words<WT>()];
+        load_words<row_words<WT>()>(row_addr, row);
+        bstep_row<WT, GR, REG, XG>(a, R, E, row, row_addr, cm, m, cnt);
     } else {
+        uint32_t nx[WT];
+        uint32_t D;
+        uint32_t M[WT], f[WT];
+        load_words<WT>(row_addr, M);
+        D = tma::lds32(row_addr + WT * 4u);
+#pragma unroll
+        for (int w = 0; w < WT; ++w) f[w] = E[w] & M[w];
         uint32_t prev = 0;
 #pragma unroll
         for (int w4 = 0; w4 < WT / 4; ++w4) {
@@ -229,27 +335,18 @@ __device__ __forceinline__ void bstep(const BArgs& a, const Rows<WT, GR, REG>& R
             R.get4(0, w4, sh);
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
-                const uint32_t s = f[w4 * 4 + j] & sh[j];
-                nx[w4 * 4 + j] = __funnelshift_l(prev, s, 1);
-                prev = s;
+                const uint32_t x = f[w4 * 4 + j] & sh[j];
+                nx[w4 * 4 + j] = __funnelshift_l(prev, x, 1);
+                prev = x;
             }
         }
-    }
-    // residual rows of the first GR groups
-#pragma unroll
-    for (int k = 0; k < GR; ++k) {
-        uint32_t acc = 0;
-        if constexpr (REG) {
-#pragma unroll
-            for (int w = 0; w < WT; ++w) acc |= f[w] & R.tr[k][w];
-            const uint32_t gm = acc ? ~0u : 0u;
-#pragma unroll
-            for (int w = 0; w < WT; ++w) nx[w] |= R.rr[k][w] & gm;
-        } else {
+        const int ng = a.n_groups;
+        for (int g = 0; g < ng; ++g) {
+            uint32_t acc = 0;
 #pragma unroll
             for (int w4 = 0; w4 < WT / 4; ++w4) {
                 uint32_t tr[4];
-                R.get4(2 + 2 * k, w4, tr);
+                R.get4(2 + 2 * g, w4, tr);
 #pragma unroll
                 for (int j = 0; j < 4; ++j) acc |= f[w4 * 4 + j] & tr[j];
             }
@@ -257,40 +354,21 @@ __device__ __forceinline__ void bstep(const BArgs& a, const Rows<WT, GR, REG>& R
 #pragma unroll
                 for (int w4 = 0; w4 < WT / 4; ++w4) {
                     uint32_t rr[4];
-                    R.get4(3 + 2 * k, w4, rr);
+                    R.get4(3 + 2 * g, w4, rr);
 #pragma unroll
                     for (int j = 0; j < 4; ++j) nx[w4 * 4 + j] |= rr[j];
                 }
             }
         }
-    }
-    // further groups from shared memory
-    for (int g = GR; g < a.n_groups; ++g) {
-        const uint32_t tb = a.xg + static_cast<uint32_t>(g - GR) * 2u * WT * 4u;
-        uint32_t T[WT];
-        load_row<WT>(tb, T);
-        uint32_t acc = 0;
-#pragma unroll
-        for (int w = 0; w < WT; ++w) acc |= f[w] & T[w];
-        if (acc) {
-            load_row<WT>(tb + WT * 4, T);
-#pragma unroll
-            for (int w = 0; w < WT; ++w) nx[w] |= T[w];
-        }
-    }
-    // string end: count A (bit 31 of the last word), restart from E0
-    cnt += (E[WT - 1] & m) >> 31;
-    if constexpr (REG) {
-#pragma unroll
-        for (int w = 0; w < WT; ++w) E[w] = (nx[w] & ~m) | (R.e0[w] & m);
-    } else {
+        cnt += __umulhi(E[WT - 1] & D & cm, a.two);
 #pragma unroll
         for (int w4 = 0; w4 < WT / 4; ++w4) {
             uint32_t e0[4];
             R.get4(1, w4, e0);
 #pragma unroll
-            for (int j = 0; j < 4; ++j) E[w4 * 4 + j] = (nx[w4 * 4 + j] & ~m) | (e0[j] & m);
+            for (int j = 0; j < 4; ++j) E[w4 * 4 + j] = (nx[w4 * 4 + j] & ~D) | (e0[j] & D);
         }
+        m = D;
     }
 }
 
@@ -308,17 +386,22 @@ __device__ __forceinline__ void set_empty(uint32_t (&E)[WT]) {
     for (int w = 0; w < WT; ++w) E[w] = 0u;
 }
 
-// Byte k of a 32-bit word as a shared-memory row address of M.
+// Byte k of a 32-bit word as the shared-memory address of its table row.
 template <int WT>
 __device__ __forceinline__ uint32_t row_of(const BArgs& a, uint32_t word, int k) {
-    if constexpr (WT * 4 <= 255) return __dp4a(word, (WT * 4u) << (8 * k), a.tab);
-    else return a.tab + __byte_perm(word, 0, 0x4440 + k) * (WT * 4u);
+    constexpr uint32_t rb = row_words<WT>() * 4u;
+    static_assert(rb <= 255, "IDP.4A scales bytes by an 8-bit factor");
+    return __dp4a(word, rb << (8 * k), a.tab);
+}
+template <int WT>
+__device__ __forceinline__ uint32_t row_b(const BArgs& a, uint32_t b) {
+    return a.tab + b * (row_words<WT>() * 4u);
 }
 
 // The line the walk is in from `pos` on, with direct loads, until its
 // delimiter (or the end of the buffer, a virtual delimiter): its result.
 // E entered holds the state before pos; an empty set ends the walk early.
-template <int WT, int GR, bool REG>
+template <int WT, int GR, bool REG, bool XG>
 __device__ __forceinline__ void set_e0(const Rows<WT, GR, REG>& R, uint32_t (&E)[WT]) {
     if constexpr (REG) {
 #pragma unroll
@@ -337,8 +420,8 @@ __device__ __forceinline__ void set_e0(const Rows<WT, GR, REG>& R, uint32_t (&E)
 // The line the walk is in from `pos` on, with direct loads, until its
 // delimiter (or the end of the buffer, a virtual delimiter): its result.
 // E holds the state before pos; an empty set ends the walk early.
-template <int WT, int GR, bool REG>
-__device__ uint32_t finish_line(const BArgs& a, const Rows<WT, GR, REG>& R, uint32_t (&E)[WT], uint64_t pos) {
+template <int WT, int GR, bool REG, bool XG>
+__device__ __noinline__ uint32_t finish_line(const BArgs& a, const Rows<WT, GR, REG>& R, uint32_t (&E)[WT], uint64_t pos) {
     const uint32_t d = a.delim4 & 0xFFu;
     uint32_t c = 0;
     while (pos < a.len && any_bit(E)) {
@@ -351,14 +434,16 @@ __device__ uint32_t finish_line(const BArgs& a, const Rows<WT, GR, REG>& R, uint
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
                     if ((dm >> (8 * k)) & 1u) return E[WT - 1] >> 31;
-                    bstep<WT, GR, REG>(a, R, E, row_of<WT>(a, x, k), 0u, c);
+                    uint32_t mm;
+                    bstep<WT, GR, REG, XG>(a, R, E, row_of<WT>(a, x, k), ~0u, mm, c);
                 }
             }
             pos += 16;
         } else {
             const uint32_t b = a.text[pos];
             if (b == d) return E[WT - 1] >> 31;
-            bstep<WT, GR, REG>(a, R, E, a.tab + b * (WT * 4u), 0u, c);
+            uint32_t mm;
+            bstep<WT, GR, REG, XG>(a, R, E, row_b<WT>(a, b), ~0u, mm, c);
             ++pos;
         }
     }
@@ -367,46 +452,47 @@ __device__ uint32_t finish_line(const BArgs& a, const Rows<WT, GR, REG>& R, uint
 
 // A remainder piece [c0, c1) of a line batch with direct loads, under K2's
 // ownership rules (range_direct in kernels_lines_tma.cu).
-template <int WT, int GR, bool REG>
-__device__ void piece_direct(const BArgs& a, const Rows<WT, GR, REG>& R, uint64_t c0, uint64_t c1, uint64_t range,
+template <int WT, int GR, bool REG, bool XG>
+__device__ __noinline__ void piece_direct(const BArgs& a, const Rows<WT, GR, REG>& R, uint64_t c0, uint64_t c1, uint64_t range,
                              uint32_t& cnt) {
     uint32_t E[WT];
     const uint32_t d = a.delim4 & 0xFFu;
     bool own = c0 == 0;
-    if (own) set_e0(R, E);
+    if (own) set_e0<WT, GR, REG, XG>(R, E);
     else set_empty(E);
     uint64_t li = a.results ? a.line_base[range] : 0;
     uint32_t last = 0;
     for (uint64_t pos = c0; pos < c1; ++pos) {
         const uint32_t b = a.text[pos];
-        const uint32_t m = b == d ? ~0u : 0u;
-        if (m) {
+        if (b == d) {
             if (own && a.results) a.results[li] = static_cast<uint8_t>(E[WT - 1] >> 31);
             ++li;
             own = true;
         }
-        bstep<WT, GR, REG>(a, R, E, a.tab + b * (WT * 4u), m, cnt);
+        uint32_t mm;   // the delimiter row counts A and restarts from E0
+        bstep<WT, GR, REG, XG>(a, R, E, row_b<WT>(a, b), ~0u, mm, cnt);
         last = b;
     }
     const bool next_line = last == d && c1 < a.len;
     if (next_line || (own && last != d && c1 > c0)) {
-        if (next_line) set_e0(R, E);
-        const uint32_t ok = finish_line<WT, GR, REG>(a, R, E, c1);
+        if (next_line) set_e0<WT, GR, REG, XG>(R, E);
+        const uint32_t ok = finish_line<WT, GR, REG, XG>(a, R, E, c1);
         cnt += ok;
         if (a.results) a.results[li] = static_cast<uint8_t>(ok);
     }
 }
 
 // Fixed-stride strings [s0, s1) with direct loads (the strings past the last full TMA row).
-template <int WT, int GR, bool REG>
-__device__ void strings_direct(const BArgs& a, const Rows<WT, GR, REG>& R, uint64_t s0, uint64_t s1, uint32_t& cnt) {
+template <int WT, int GR, bool REG, bool XG>
+__device__ __noinline__ void strings_direct(const BArgs& a, const Rows<WT, GR, REG>& R, uint64_t s0, uint64_t s1, uint32_t& cnt) {
     for (uint64_t i = s0; i < s1; ++i) {
         uint32_t E[WT];
-        set_e0(R, E);
+        set_e0<WT, GR, REG, XG>(R, E);
         uint32_t c = 0;
         for (uint32_t k = 0; k < a.stride; ++k) {
             const uint32_t b = a.text[i * a.stride + k];
-            bstep<WT, GR, REG>(a, R, E, a.tab + b * (WT * 4u), 0u, c);
+            uint32_t mm;
+            bstep<WT, GR, REG, XG>(a, R, E, row_b<WT>(a, b), ~0u, mm, c);
         }
         const uint32_t ok = E[WT - 1] >> 31;
         cnt += ok;
@@ -414,7 +500,7 @@ __device__ void strings_direct(const BArgs& a, const Rows<WT, GR, REG>& R, uint6
     }
 }
 
-template <class C, int WT, int GR, bool REG, bool FIXED>
+template <class C, int WT, int GR, bool REG, bool XG, bool FIXED, bool RES>
 __global__ void __launch_bounds__(C::warps * 32, 1) k_bits_tma(const __grid_constant__ BArgs a,
                                                              const __grid_constant__ CUtensorMap map) {
     extern __shared__ __align__(1024) uint8_t sm[];
@@ -436,6 +522,8 @@ __global__ void __launch_bounds__(C::warps * 32, 1) k_bits_tma(const __grid_cons
     }
     Rows<WT, GR, REG> R;
     R.load(a);
+    constexpr int GR_ = GR;
+    (void)GR_;
     __syncthreads();
     tma::mbar_wait(tbar, 0);
 
@@ -444,11 +532,11 @@ __global__ void __launch_bounds__(C::warps * 32, 1) k_bits_tma(const __grid_cons
         const uint64_t r0 = a.rows * a.chunk;
         if constexpr (FIXED) {
             const uint64_t n0 = r0 / a.stride, n1 = a.len / a.stride;
-            for (uint64_t i = n0 + lane; i < n1; i += 32) strings_direct<WT, GR, REG>(a, R, i, i + 1, cnt);
+            for (uint64_t i = n0 + lane; i < n1; i += 32) strings_direct<WT, GR, REG, XG>(a, R, i, i + 1, cnt);
         } else {
             for (uint32_t p = lane; p < a.rem_pieces; p += 32) {
                 const uint64_t c0 = r0 + static_cast<uint64_t>(p) * a.rem_piece;
-                piece_direct<WT, GR, REG>(a, R, c0, min(c0 + a.rem_piece, a.len), a.rows + p, cnt);
+                piece_direct<WT, GR, REG, XG>(a, R, c0, min(c0 + a.rem_piece, a.len), a.rows + p, cnt);
             }
         }
     }
@@ -474,12 +562,13 @@ __global__ void __launch_bounds__(C::warps * 32, 1) k_bits_tma(const __grid_cons
             const uint64_t row = row0 + j * 32 + lane;
             valid[j] = row < a.rows;
             cm[j] = valid[j] ? ~0u : 0u;
+            asm volatile("" : "+r"(cm[j]));   // keep the mask in a register (no per-byte recompute)
             // K2's ownership: the first range starts in the start state, every
             // other one in SKIP (the empty set) until its first line boundary
             own[j] = FIXED ? valid[j] : row == 0;
-            if (own[j]) set_e0(R, E[j]);
+            if (own[j]) set_e0<WT, GR, REG, XG>(R, E[j]);
             else set_empty(E[j]);
-            li[j] = !a.results ? 0 : FIXED ? row * (a.chunk / a.stride) : (valid[j] ? a.line_base[row] : 0);
+            li[j] = !RES ? 0 : FIXED ? row * (a.chunk / a.stride) : (valid[j] ? a.line_base[row] : 0);
         }
         uint32_t last[C::chains] = {};
         uint32_t sp = 0;   // fixed stride: byte offset in the current string (the same in every range)
@@ -487,7 +576,8 @@ __global__ void __launch_bounds__(C::warps * 32, 1) k_bits_tma(const __grid_cons
             const uint32_t st = col % C::stages;
             tma::mbar_wait(bar0 + st * 8, (phase >> st) & 1u);
             phase ^= 1u << st;
-#pragma unroll
+            // (code size and compile time: only the one-word kernel unrolls the granules and words)
+#pragma unroll(WT == 1 ? C::slice / 16 : 1)
             for (int g = 0; g < C::slice / 16; ++g) {
                 uint4 v[C::chains];
 #pragma unroll
@@ -495,11 +585,8 @@ __global__ void __launch_bounds__(C::warps * 32, 1) k_bits_tma(const __grid_cons
                     const uint32_t r = j * 32 + lane;
                     v[j] = tma::lds128(stage[st] + r * C::slice + (tma::granule<C::slice>(r, g) << 4));
                 }
-#pragma unroll
+#pragma unroll(REG ? 4 : 1)
                 for (int w = 0; w < 4; ++w) {
-                    uint32_t dm[C::chains];
-#pragma unroll
-                    for (int j = 0; j < C::chains; ++j) dm[j] = FIXED ? 0u : __vcmpeq4(tma::word_of(v[j], w), a.delim4);
 #pragma unroll
                     for (int k = 0; k < 4; ++k) {
                         // fixed stride: the string end is at the same offset in every range (warp-uniform)
@@ -512,33 +599,30 @@ __global__ void __launch_bounds__(C::warps * 32, 1) k_bits_tma(const __grid_cons
                         for (int j = 0; j < C::chains; ++j) {
                             const uint32_t x = tma::word_of(v[j], w);
                             if constexpr (FIXED) {
-                                uint32_t c = 0;
-                                bstep<WT, GR, REG>(a, R, E[j], row_of<WT>(a, x, k), 0u, c);
+                                uint32_t c = 0, mm;
+                                bstep<WT, GR, REG, XG>(a, R, E[j], row_of<WT>(a, x, k), 0u, mm, c);
                                 if (end_fixed) {   // count A after the last byte, restart
                                     const uint32_t ok = (E[j][WT - 1] & cm[j]) >> 31;
                                     cnt += ok;
-                                    if (a.results && valid[j]) a.results[li[j]++] = static_cast<uint8_t>(ok);
-                                    set_e0(R, E[j]);
+                                    if (RES && valid[j]) a.results[li[j]++] = static_cast<uint8_t>(ok);
+                                    set_e0<WT, GR, REG, XG>(R, E[j]);
                                 }
                             } else {
-                                const uint32_t m = __byte_perm(dm[j], 0, (8 + k) * 0x1111);   // sign of byte k
-                                if (a.results && m) {   // a line ends here: record it if owned
-                                    if (own[j] && valid[j]) a.results[li[j]] = static_cast<uint8_t>(E[j][WT - 1] >> 31);
+                                // the delimiter's table row (D = all ones) counts A and restarts E
+                                const uint32_t abit = RES ? E[j][WT - 1] >> 31 : 0u;
+                                uint32_t m;
+                                bstep<WT, GR, REG, XG>(a, R, E[j], row_of<WT>(a, x, k), cm[j], m, cnt);
+                                if (RES && m) {   // a line ended here: record it if owned
+                                    if (own[j] && valid[j]) a.results[li[j]] = static_cast<uint8_t>(abit);
                                     ++li[j];
                                     own[j] = true;
                                 }
-                                bstep<WT, GR, REG>(a, R, E[j], row_of<WT>(a, x, k), m & cm[j], cnt);
                             }
                         }
                     }
                 }
 #pragma unroll
-                for (int j = 0; j < C::chains; ++j) {
-                    last[j] = v[j].w >> 24;
-                    if (!FIXED && !a.results)   // a line starts inside the range: it owns its straddling line
-                        own[j] |= (__vcmpeq4(v[j].x, a.delim4) | __vcmpeq4(v[j].y, a.delim4) |
-                                   __vcmpeq4(v[j].z, a.delim4) | __vcmpeq4(v[j].w, a.delim4)) != 0;
-                }
+                for (int j = 0; j < C::chains; ++j) last[j] = v[j].w >> 24;
             }
             __syncwarp();
             if (lane == 0 && col + C::stages < ncol) {
@@ -555,11 +639,13 @@ __global__ void __launch_bounds__(C::warps * 32, 1) k_bits_tma(const __grid_cons
                 if (!valid[j]) continue;
                 const uint64_t pos = (row0 + j * 32 + lane + 1) * a.chunk;
                 const bool next_line = last[j] == d && pos < a.len;
-                if (next_line) set_e0(R, E[j]);
-                if (next_line || (own[j] && last[j] != d)) {
-                    const uint32_t ok = finish_line<WT, GR, REG>(a, R, E[j], pos);
+                if (next_line) set_e0<WT, GR, REG, XG>(R, E[j]);
+                // (counting only: a range that saw no line start holds the empty set, which
+                // finish_line ends at once, so ownership needs no tracking)
+                if (next_line || ((RES ? own[j] : true) && last[j] != d)) {
+                    const uint32_t ok = finish_line<WT, GR, REG, XG>(a, R, E[j], pos);
                     cnt += ok;
-                    if (a.results) a.results[li[j]] = static_cast<uint8_t>(ok);
+                    if (RES) a.results[li[j]] = static_cast<uint8_t>(ok);
                 }
             }
         }
@@ -618,7 +704,7 @@ Split split_of(uint64_t len, uint32_t chunk, bool lines) {
     return s;
 }
 
-using ShapeR = Shape<16, 2, 32, 3>;   // registers (WT <= 4)
+using ShapeR = Shape<24, 2, 32, 3>;   // registers (WT <= 4)
 using ShapeS = Shape<16, 1, 32, 4>;   // shared-memory rows (WT 8, 16)
 
 template <class C>
@@ -631,10 +717,10 @@ uint32_t stage_space(uint32_t table_bytes, BArgs& a) {
     return a.bar_addr + C::warps * C::stages * 8 + 8 + 4 * C::warps - base;
 }
 
-template <class C, int WT, int GR, bool REG, bool FIXED>
+template <class C, int WT, int GR, bool REG, bool XG, bool FIXED>
 int per_sm(uint32_t smem) {
     int n = 0;
-    auto* k = k_bits_tma<C, WT, GR, REG, FIXED>;
+    auto* k = k_bits_tma<C, WT, GR, REG, XG, FIXED, false>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, C::warps * 32, smem);
     return n < 1 ? 1 : n;
@@ -652,14 +738,14 @@ uint32_t unit_of(uint32_t slice, uint32_t stride) {   // chunk granularity: slic
     return l > (1u << 20) ? 0u : static_cast<uint32_t>(l);
 }
 
-template <class C, int WT, int GR, bool REG, bool FIXED>
+template <class C, int WT, int GR, bool REG, bool XG, bool FIXED>
 uint32_t auto_chunk(const BitsImage& b, uint64_t len, uint32_t stride) {
     BArgs a{};
     const uint32_t smem = stage_space<C>(static_cast<uint32_t>(b.t.img.size() * 4), a);
     int dev = 0;
     cudaGetDevice(&dev);
     const uint64_t ranges =
-        static_cast<uint64_t>(per_sm<C, WT, GR, REG, FIXED>(smem)) * device_sm_count(dev) * C::warps * C::rows;
+        static_cast<uint64_t>(per_sm<C, WT, GR, REG, XG, FIXED>(smem)) * device_sm_count(dev) * C::warps * C::rows;
     const uint32_t unit = unit_of(C::slice, FIXED ? stride : 0);
     if (!unit) return 0;
     uint64_t c = (len + ranges - 1) / ranges;
@@ -670,12 +756,12 @@ uint32_t auto_chunk(const BitsImage& b, uint64_t len, uint32_t stride) {
     return static_cast<uint32_t>(c);
 }
 
-template <class C, int WT, int GR, bool REG, bool FIXED>
+template <class C, int WT, int GR, bool REG, bool XG, bool FIXED>
 cudaError_t run(const BitsImage& b, const uint8_t* text, uint64_t len, int32_t delim, uint32_t stride, uint32_t chunk,
                 unsigned long long* count, uint8_t* results, void* scratch, size_t scratch_bytes, CountSlot cs,
                 cudaStream_t st) {
     if (len == 0) return cs.accumulate ? cudaSuccess : cudaMemsetAsync(count, 0, sizeof(unsigned long long), st);
-    if (chunk == 0) chunk = auto_chunk<C, WT, GR, REG, FIXED>(b, len, stride);
+    if (chunk == 0) chunk = auto_chunk<C, WT, GR, REG, XG, FIXED>(b, len, stride);
     if (chunk == 0 || chunk % C::slice || (FIXED && chunk % stride)) return cudaErrorInvalidValue;
     BArgs a{};
     a.text = text;
@@ -689,11 +775,14 @@ cudaError_t run(const BitsImage& b, const uint8_t* text, uint64_t len, int32_t d
     a.stride = FIXED ? stride : 0;
     a.delim4 = FIXED ? 0u : static_cast<uint32_t>(delim) * 0x01010101u;
     a.n_groups = b.t.G;
+    a.two = 2;
     a.img = static_cast<const uint4*>(b.d_img);
     a.img_words = static_cast<uint32_t>(b.t.img.size() / 4);
     a.regs_g = b.d_regs;
     const uint32_t smem = stage_space<C>(static_cast<uint32_t>(b.t.img.size() * 4), a);
-    a.regs = a.tab + b.t.regs_off;
+    a.xt = a.tab + b.t.xt_off;
+    a.cmap = a.tab + b.t.cmap_off;
+    a.xt_row_bytes = b.t.xt_row_words * 4u;
     a.xg = a.tab + b.t.xg_off;
     a.count = count;
     a.slot = cs.p;
@@ -721,12 +810,18 @@ cudaError_t run(const BitsImage& b, const uint8_t* text, uint64_t len, int32_t d
     std::memset(&map, 0, sizeof(map));
     if (a.rows > 0 && tma::make_map(&map, text, a.rows, chunk, C::slice, C::rows) != CUDA_SUCCESS)
         return cudaErrorInvalidValue;
-    const int ps = per_sm<C, WT, GR, REG, FIXED>(smem);
+    const int ps = per_sm<C, WT, GR, REG, XG, FIXED>(smem);
     int dev = 0;
     cudaGetDevice(&dev);
     const uint64_t cap = static_cast<uint64_t>(ps) * device_sm_count(dev);
     const int grid = static_cast<int>(a.tiles == 0 ? 1 : (a.tiles < cap ? a.tiles : cap));
-    k_bits_tma<C, WT, GR, REG, FIXED><<<grid, C::warps * 32, smem, st>>>(a, map);
+    if (results) {
+        cudaFuncSetAttribute(k_bits_tma<C, WT, GR, REG, XG, FIXED, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(smem));
+        k_bits_tma<C, WT, GR, REG, XG, FIXED, true><<<grid, C::warps * 32, smem, st>>>(a, map);
+    } else {
+        k_bits_tma<C, WT, GR, REG, XG, FIXED, false><<<grid, C::warps * 32, smem, st>>>(a, map);
+    }
     return cudaGetLastError();
 }
 
@@ -734,8 +829,8 @@ struct ChunkF {
     const BitsImage& b;
     uint64_t len;
     uint32_t stride;
-    template <class C, int WT, int GR, bool REG, bool FIXED>
-    uint32_t go() const { return auto_chunk<C, WT, GR, REG, FIXED>(b, len, stride); }
+    template <class C, int WT, int GR, bool REG, bool XG, bool FIXED>
+    uint32_t go() const { return auto_chunk<C, WT, GR, REG, XG, FIXED>(b, len, stride); }
 };
 
 struct LaunchF {
@@ -750,9 +845,9 @@ struct LaunchF {
     size_t scratch_bytes;
     CountSlot cs;
     cudaStream_t st;
-    template <class C, int WT, int GR, bool REG, bool FIXED>
+    template <class C, int WT, int GR, bool REG, bool XG, bool FIXED>
     cudaError_t go() const {
-        return run<C, WT, GR, REG, FIXED>(b, text, len, delim, stride, chunk, count, results, scratch, scratch_bytes,
+        return run<C, WT, GR, REG, XG, FIXED>(b, text, len, delim, stride, chunk, count, results, scratch, scratch_bytes,
                                           cs, st);
     }
 };
@@ -760,11 +855,11 @@ struct LaunchF {
 template <class F>
 auto dispatch(const BitsImage& b, bool fixed, F f) {
     const int WT = b.t.WT;
-    const bool g4 = b.t.GR == 4;
-#define RXG_BITS_CASE(W, S, REG)                                                                             \
-    if (WT == W) {                                                                                           \
-        if (fixed) return g4 ? f.template go<S, W, 4, REG, true>() : f.template go<S, W, 2, REG, true>();    \
-        return g4 ? f.template go<S, W, 4, REG, false>() : f.template go<S, W, 2, REG, false>();             \
+    const bool xg = b.t.G > b.t.GR && b.t.WT <= 4;   // (the broadcast kernels loop over every group)
+#define RXG_BITS_CASE(W, S, REG)                                                                          \
+    if (WT == W) {                                                                                        \
+        if (fixed) return xg ? f.template go<S, W, 2, REG, true, true>() : f.template go<S, W, 2, REG, false, true>(); \
+        return xg ? f.template go<S, W, 2, REG, true, false>() : f.template go<S, W, 2, REG, false, false>();         \
     }
     RXG_BITS_CASE(1, ShapeR, true)
     RXG_BITS_CASE(2, ShapeR, true)
@@ -772,7 +867,7 @@ auto dispatch(const BitsImage& b, bool fixed, F f) {
     RXG_BITS_CASE(8, ShapeS, false)
     RXG_BITS_CASE(16, ShapeS, false)
 #undef RXG_BITS_CASE
-    return f.template go<ShapeR, 1, 2, true, false>();   // unreachable for ok tables
+    return f.template go<ShapeR, 1, 2, true, false, false>();   // unreachable for ok tables
 }
 
 }  // namespace

@@ -22,11 +22,15 @@
 //             per step — the dedup-by-pointer-equality of the paper.
 #include <cstdint>
 
+#include <cooperative_groups.h>
 #include <cub/device/device_scan.cuh>
 
+#include "launch.hpp"
 #include "pernode.hpp"
 
 namespace rxg {
+
+namespace cg = cooperative_groups;
 
 namespace {
 
@@ -312,6 +316,13 @@ struct PernodeArgs {
     uint32_t every;            // checkpoint period (0 = none)
     uint32_t* checkpoints;     // (len / every) x W words: E after every `every` symbols
     int32_t* accept;
+    // segments (cooperative launch, one warp per segment; n_segs == 1: the one-warp walk)
+    uint64_t seg;              // bytes per segment (multiple of 16)
+    int32_t n_segs;
+    uint32_t lookback;         // bytes walked from E0 before a segment to guess its entry set
+    uint32_t* entry;           // n_segs x W: the entry set each segment last walked from
+    uint32_t* exits;           // 2 x n_segs x W: exit sets (double-buffered across repair rounds)
+    unsigned int* changed;     // 2 counters (zero when idle)
 };
 
 // One lockstep step of the warp-wide bitset. DENSE: <= 32 residual rows,
@@ -404,6 +415,13 @@ __device__ __forceinline__ void pernode_step(const PernodeArgs& a, const uint32_
 
 template <int SLOTS, bool DENSE, int GREG>
 __global__ void __launch_bounds__(32) k_pernode(const __grid_constant__ PernodeArgs a) {
+    // K1 over one long string, the paper's scheme per warp. With several
+    // segments (north_star (2) first bullet, scaled across SMs): warp s walks
+    // [s*seg, (s+1)*seg) from a guessed entry set (E0 walked over the
+    // `lookback` bytes before the segment), the exit sets are published, and
+    // repair rounds re-walk every segment whose entry differs from its
+    // predecessor's current exit until no entry changes. Sets are compared
+    // word for word, so the result is exactly the one-warp walk's.
     extern __shared__ __align__(16) uint32_t smp[];
     const int W = a.W;
     const int lane = threadIdx.x;
@@ -443,8 +461,6 @@ __global__ void __launch_bounds__(32) k_pernode(const __grid_constant__ PernodeA
     __syncwarp();
     uint64_t pos = 0;
     bool live = true;
-    // 16 input bytes per uniform load (every lane reads the same vector)
-    const uint64_t head = (16 - (reinterpret_cast<uintptr_t>(a.text) & 15)) & 15;
     auto rowp = [&](uint32_t b) { return a.byte_masks ? masks + b * W : masks + cls[b] * W; };
     auto one = [&](const uint32_t (&Mw)[SLOTS]) {
         pernode_step<SLOTS, DENSE, GREG>(a, Mw, TR, RR, hit, hw, lane, E, SH, HG, TRr, RRr);
@@ -463,8 +479,13 @@ __global__ void __launch_bounds__(32) k_pernode(const __grid_constant__ PernodeA
         for (int k = 0; k < SLOTS; ++k) Mw[k] = lane + 32 * k < W ? M[lane + 32 * k] : 0u;
         one(Mw);
     };
-    for (uint64_t i = 0; i < head && pos < a.len; ++i) single(a.text[pos]);
-    while (live && pos + 16 <= a.len) {
+    auto walk = [&](uint64_t lo, uint64_t hi) {
+    pos = lo;
+    live = true;
+    // 16 input bytes per uniform load (every lane reads the same vector)
+    const uint64_t head = (16 - (reinterpret_cast<uintptr_t>(a.text + lo) & 15)) & 15;
+    for (uint64_t i = 0; i < head && pos < hi; ++i) single(a.text[pos]);
+    while (live && pos + 16 <= hi) {
         const uint4 v = __ldg(reinterpret_cast<const uint4*>(a.text + pos));
         const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
         // the 16 mask rows depend only on the input: load them all before the
@@ -485,8 +506,65 @@ __global__ void __launch_bounds__(32) k_pernode(const __grid_constant__ PernodeA
             live = __any_sync(0xFFFFFFFFu, any);
         }
     }
-    while (live && pos < a.len) single(a.text[pos]);
+    while (live && pos < hi) single(a.text[pos]);
+    };
     const int A = a.n_bits - 1;   // accept bit
+    if (a.n_segs > 1) {
+        const int s = static_cast<int>(blockIdx.x);
+        const uint64_t lo = static_cast<uint64_t>(s) * a.seg, hi = min(lo + a.seg, a.len);
+        auto put = [&](uint32_t* dst) {
+#pragma unroll
+            for (int k = 0; k < SLOTS; ++k)
+                if (lane + 32 * k < W) dst[lane + 32 * k] = E[k];
+        };
+        auto get = [&](const uint32_t* src) {
+#pragma unroll
+            for (int k = 0; k < SLOTS; ++k) E[k] = lane + 32 * k < W ? __ldcg(src + lane + 32 * k) : 0u;
+        };
+        if (s > 0) walk(lo >= a.lookback ? lo - a.lookback : 0, lo);   // the guess (from E0)
+        const size_t sw = static_cast<size_t>(W);
+        put(a.entry + s * sw);
+        walk(lo, hi);
+        put(a.exits + s * sw);
+        cg::grid_group grid = cg::this_grid();
+        __threadfence();
+        grid.sync();
+        for (int r = 0;; ++r) {
+            const uint32_t* prev = a.exits + static_cast<size_t>(r & 1) * a.n_segs * sw;
+            uint32_t* next = a.exits + static_cast<size_t>((r + 1) & 1) * a.n_segs * sw;
+            if (s == 0 && lane == 0) a.changed[(r + 1) & 1] = 0;
+            bool diff = false;
+            if (s > 0)
+                for (int w = lane; w < W; w += 32) diff |= __ldcg(prev + (s - 1) * sw + w) != __ldcg(a.entry + s * sw + w);
+            if (__any_sync(0xFFFFFFFFu, diff)) {   // re-walk from the predecessor's current exit
+                get(prev + (s - 1) * sw);
+                put(a.entry + s * sw);
+                walk(lo, hi);
+                put(next + s * sw);
+                if (lane == 0) atomicAdd(&a.changed[r & 1], 1u);
+            } else {
+                for (int w = lane; w < W; w += 32) next[s * sw + w] = __ldcg(prev + s * sw + w);
+            }
+            __threadfence();
+            grid.sync();
+            if (*reinterpret_cast<volatile unsigned int*>(&a.changed[r & 1]) == 0) {
+                if (s == a.n_segs - 1) {
+                    get(next + s * sw);
+                    uint32_t acc = 0;
+#pragma unroll
+                    for (int k = 0; k < SLOTS; ++k)
+                        if (lane + 32 * k == (A >> 5)) acc = (E[k] >> (A & 31)) & 1u;
+                    acc = __reduce_or_sync(0xFFFFFFFFu, acc);
+                    if (lane == 0) {
+                        *a.accept = static_cast<int32_t>(acc);
+                        a.changed[r & 1] = 0;
+                    }
+                }
+                return;
+            }
+        }
+    }
+    walk(0, a.len);
     uint32_t acc = 0;
 #pragma unroll
     for (int k = 0; k < SLOTS; ++k)
@@ -497,18 +575,60 @@ __global__ void __launch_bounds__(32) k_pernode(const __grid_constant__ PernodeA
 
 template <int SLOTS, bool DENSE, int GREG>
 cudaError_t run_pernode(const PernodeArgs& a, uint32_t smem, cudaStream_t st) {
-    cudaError_t e = cudaFuncSetAttribute(k_pernode<SLOTS, DENSE, GREG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
+    auto* k = k_pernode<SLOTS, DENSE, GREG>;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
-    k_pernode<SLOTS, DENSE, GREG><<<1, 32, smem, st>>>(a);
-    return cudaGetLastError();
+    if (a.n_segs <= 1) {
+        k<<<1, 32, smem, st>>>(a);
+        return cudaGetLastError();
+    }
+    PernodeArgs b = a;
+    void* args[] = {&b};
+    return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k), dim3(a.n_segs), dim3(32), args, smem, st);
 }
 
+// Resident one-warp blocks per SM of the segmented K1 kernel (segments are capped by it).
+template <int SLOTS, bool DENSE, int GREG>
+int pernode_per_sm(uint32_t smem) {
+    auto* k = k_pernode<SLOTS, DENSE, GREG>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    int n = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, 32, smem);
+    return n;
+}
+
+template <bool D, int G>
+struct Tag {
+    static constexpr bool dense = D;
+    static constexpr int greg = G;
+};
+
 template <int SLOTS>
-cudaError_t run_pernode2(const PernodeArgs& a, uint32_t smem, bool dense, cudaStream_t st) {
-    if (a.n_groups <= 1) return run_pernode<SLOTS, true, 1>(a, smem, st);
-    if (a.n_groups <= 2) return run_pernode<SLOTS, true, 2>(a, smem, st);
-    return dense ? run_pernode<SLOTS, true, 0>(a, smem, st) : run_pernode<SLOTS, false, 0>(a, smem, st);
+cudaError_t run_pernode2(PernodeArgs a, uint32_t smem, bool dense, cudaStream_t st, uint64_t seg_want,
+                         const PernodeSegScratch* ss) {
+    auto launch = [&](auto tag) {
+        using T = decltype(tag);
+        if (ss && seg_want) {   // segments across SMs: as many as are co-resident (cooperative launch)
+            const int per = pernode_per_sm<SLOTS, T::dense, T::greg>(smem);
+            int dev = 0;
+            cudaGetDevice(&dev);
+            const uint64_t cap = static_cast<uint64_t>(per > 0 ? per : 1) * device_sm_count(dev);
+            uint64_t n = (a.len + seg_want - 1) / seg_want;
+            if (n > cap) n = cap;
+            if (n > ss->max_segs) n = ss->max_segs;
+            if (n > 1) {
+                a.seg = ((a.len + n - 1) / n + 15) / 16 * 16;
+                a.n_segs = static_cast<int32_t>((a.len + a.seg - 1) / a.seg);
+                a.entry = ss->entry;
+                a.exits = ss->exits;
+                a.changed = ss->changed;
+            }
+        }
+        return run_pernode<SLOTS, T::dense, T::greg>(a, smem, st);
+    };
+    if (a.n_groups <= 1) return launch(Tag<true, 1>{});
+    if (a.n_groups <= 2) return launch(Tag<true, 2>{});
+    return dense ? launch(Tag<true, 0>{}) : launch(Tag<false, 0>{});
 }
 
 // ── K2b: warp-per-line bitset lockstep for batches ───────────────────────
@@ -720,7 +840,7 @@ cudaError_t launch_rounds(const RoundsTables& t, const uint8_t* text, uint64_t l
 }
 
 cudaError_t launch_pernode(const PernodeTables& t, const uint8_t* text, uint64_t len, uint32_t every,
-                           uint32_t* checkpoints, int32_t* accept, cudaStream_t st) {
+                           uint32_t* checkpoints, int32_t* accept, cudaStream_t st, const PernodeSegScratch* ss) {
     PernodeArgs a{};
     a.text = text;
     a.len = len;
@@ -739,18 +859,23 @@ cudaError_t launch_pernode(const PernodeTables& t, const uint8_t* text, uint64_t
     a.every = every;
     a.checkpoints = checkpoints;
     a.accept = accept;
+    a.n_segs = 1;
+    a.lookback = kPernodeLookback;
+    // segments only without checkpoints and for long strings
+    const uint64_t seg_want = (ss && !every && len >= kPernodeSegMin) ? kPernodeSegMin / 4 : 0;
     const bool dense = t.n_groups <= kDenseGroups;
-    a.byte_masks = 256u * static_cast<uint32_t>(t.W) * 4u <= 128u * 1024u;
+    // segments: class-indexed masks keep a warp's shared memory small (more warps per SM)
+    a.byte_masks = !seg_want && 256u * static_cast<uint32_t>(t.W) * 4u <= 128u * 1024u;
     const uint32_t mrows = a.byte_masks ? 256u : static_cast<uint32_t>(t.n_classes);
     const uint32_t group_words = dense ? 2u * static_cast<uint32_t>(t.n_groups * t.W)
                                        : static_cast<uint32_t>((t.n_groups + 31) / 32);
     const uint32_t smem = (mrows * static_cast<uint32_t>(t.W) + group_words) * 4u + 256u;
     const int slots = (t.W + 31) / 32;
-    if (slots <= 1) return run_pernode2<1>(a, smem, dense, st);
-    if (slots <= 2) return run_pernode2<2>(a, smem, dense, st);
-    if (slots <= 3) return run_pernode2<3>(a, smem, dense, st);
-    if (slots <= 4) return run_pernode2<4>(a, smem, dense, st);
-    if (slots <= kMaxSlots) return run_pernode2<kMaxSlots>(a, smem, dense, st);
+    if (slots <= 1) return run_pernode2<1>(a, smem, dense, st, seg_want, ss);
+    if (slots <= 2) return run_pernode2<2>(a, smem, dense, st, seg_want, ss);
+    if (slots <= 3) return run_pernode2<3>(a, smem, dense, st, seg_want, ss);
+    if (slots <= 4) return run_pernode2<4>(a, smem, dense, st, seg_want, ss);
+    if (slots <= kMaxSlots) return run_pernode2<kMaxSlots>(a, smem, dense, st, seg_want, ss);
     return cudaErrorInvalidValue;
 }
 

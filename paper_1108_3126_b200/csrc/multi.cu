@@ -268,7 +268,6 @@ int rxg_multi_match_batch(rxg_multi* m, const uint8_t* text, uint64_t len, int32
     std::lock_guard<std::mutex> call(m->call_mu);
     const int ndev = static_cast<int>(m->devices.size());
     rxg_heap* h0 = m->heaps[0];
-    if (!h0->dfa_ok && delimiter < 0) return fail(RXG_ETOOBIG, "memoized step table over the cap (fixed stride needs it)");
     std::vector<uint64_t> off(static_cast<size_t>(ndev) + 1);
     if (int rc = rxg_shard_bounds(text, len, delimiter, stride, ndev, off.data())) return rc;
     // bank placement from the head of the buffer, sampled once for every device (speed only)

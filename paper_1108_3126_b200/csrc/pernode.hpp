@@ -46,9 +46,25 @@ cudaError_t launch_rounds(const RoundsTables& t, const uint8_t* text, uint64_t l
 cudaError_t launch_par(const RoundsTables& t, long long* c, long long* n, uint32_t* claims, int* flags, long long tt,
                        uint32_t symbol, int32_t single, unsigned long long* launches, cudaStream_t st);
 
-// every > 0: E after every `every` symbols into checkpoints ((len/every) x W words).
+// Segmented K1 (long strings across SMs): device scratch for up to
+// max_segs segments of W words (pernode_seg_scratch_bytes), changed = 2
+// zeroed counters (zero again when the launch completes).
+struct PernodeSegScratch {
+    uint32_t* entry = nullptr;     // max_segs x W
+    uint32_t* exits = nullptr;     // 2 x max_segs x W
+    unsigned int* changed = nullptr;
+    uint64_t max_segs = 0;
+};
+constexpr uint64_t kPernodeSegMin = 1ull << 20;   // strings at least this long are segmented
+constexpr uint32_t kPernodeLookback = 1024;       // bytes walked from E0 to guess a segment's entry
+constexpr uint64_t kPernodeMaxSegs = 8192;
+inline size_t pernode_seg_scratch_bytes(int32_t W) { return 3 * kPernodeMaxSegs * static_cast<size_t>(W) * 4 + 64; }
+
+// every > 0: E after every `every` symbols into checkpoints ((len/every) x W words; one warp).
+// ss (nullable): strings >= kPernodeSegMin without checkpoints run as segments (cooperative launch).
 cudaError_t launch_pernode(const PernodeTables& t, const uint8_t* text, uint64_t len, uint32_t every,
-                           uint32_t* checkpoints, int32_t* accept, cudaStream_t st);
+                           uint32_t* checkpoints, int32_t* accept, cudaStream_t st,
+                           const PernodeSegScratch* ss = nullptr);
 
 // K2b: warp-per-line bitset batch (line mode). scratch: lines_bitset_scratch_bytes(len).
 size_t lines_bitset_scratch_bytes(uint64_t len);

@@ -259,3 +259,32 @@ def test_chunked_sticky_states_parallel_rounds():
     assert acc_rounds.lockstep_accepts(w.tobytes(), "chunked") is True
     w[:] = ord("b")
     assert acc_rounds.lockstep_accepts(w.tobytes(), "chunked") is False
+
+
+@pytest.mark.parametrize("pat,alpha,n", [("(a|b)*abb", b"ab", 3 << 20), ("(aa)*", b"a", 2 << 20), ("(aaa)*", b"a", (3 << 20) + 7),
+                                         ("(a|b)*a(a|b)(a|b)(a|b)", b"ab", 5 << 20), ("(ab|a)*(b|())", b"ab", 2 << 20)])
+def test_pernode_segments_across_sms_equal_one_warp(pat, alpha, n):
+    """K1 over a long string as segments across SMs (guessed entry sets,
+    exact repair rounds) gives the one-warp walk's answer, including
+    non-synchronizing automata ((aa)*, (aaa)*) whose guesses are wrong."""
+    import torch
+
+    rng = np.random.default_rng(n)
+    a = np.frombuffer(alpha, np.uint8)
+    w = a[rng.integers(0, len(a), n)].copy()
+    m = rx.Matcher(pat)
+    d = torch.zeros(n + 64, dtype=torch.uint8, device="cuda")
+    d[:n].copy_(torch.from_numpy(w))
+    acc = torch.zeros(1, dtype=torch.int32, device="cuda")
+    for tail in (b"", b"abb", b"a", b"aa"):
+        if tail:
+            d[n - len(tail):n].copy_(torch.frombuffer(bytearray(tail), dtype=torch.uint8))
+        m.match_one_ex(d, acc, "pernode", nbytes=n)
+        torch.cuda.synchronize()
+        seg = bool(acc.item())
+        m.match_one_ex(d, acc, "pernode", nbytes=n, flags=2)   # RXG_ONE_SINGLE_WARP
+        torch.cuda.synchronize()
+        one = bool(acc.item())
+        m.match_one_ex(d, acc, "dfa_seq", nbytes=n)
+        torch.cuda.synchronize()
+        assert seg == one == bool(acc.item()), (pat, tail)
