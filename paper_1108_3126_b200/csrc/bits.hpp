@@ -15,12 +15,11 @@ constexpr uint32_t kBitsMaxTableBytes = 96 * 1024;    // shared-memory image bud
 
 // Bitset step tables in the kernel's bit order (positions 0..n_pos-1, the
 // accept bit A at bit 32*WT - 1), for one delimiter (-1: fixed stride).
-// WT <= 4: one row per byte [M&SH, M&T_0, M&T_1, D] (M = the positions the
-//   byte matches, SH = positions whose follow is the next position, T_g =
-//   positions whose residual follow row is R_g, D = all ones on the
-//   delimiter), then the byte class map and per class M&T_g for groups
-//   g >= 2, then R_g (g >= 2);
-//   regs = E0, R_0, R_1 (kept in registers).
+// WT <= 4: one row per byte [M, D] (M = the positions the byte matches,
+//   D = all ones on the delimiter), then (T_g, R_g) of groups g >= 2 as
+//   broadcast rows; regs = SH, E0, T_0, R_0, T_1, R_1 (kept in registers;
+//   SH = positions whose follow is the next position, T_g = positions whose
+//   residual follow row is R_g).
 // WT 8, 16: one row per byte [M, D, pad]; then SH, E0 and (T_g, R_g) for
 //   every group, read as shared-memory broadcasts.
 struct BitsTables {

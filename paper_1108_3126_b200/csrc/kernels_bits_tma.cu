@@ -94,47 +94,26 @@ BitsTables make_bits_tables(const Program& p, int32_t delim) {
     auto rg = [&](int32_t g, int32_t w) { return g < t.G ? rows[static_cast<size_t>(g) * WT + w] : 0u; };
     std::vector<uint32_t>& img = t.img;
     if (WT <= 4) {
-        // per byte: [M & SH, M & T_0, M & T_1, D (all ones on the delimiter), pad], then
-        // the extra groups' rows M & T_g (g >= 2) per byte; R_g (g >= 2) after them
-        t.row_words = (3 * WT + 1 + 3) / 4 * 4;
+        // per byte: [M, D (all ones on the delimiter), pad]; then T_g, R_g of the
+        // groups >= 2 (broadcast rows); registers: SH, E0, T_0, R_0, T_1, R_1
+        t.row_words = WT == 1 ? 2 : (WT + 1 + 3) / 4 * 4;
         img.assign(static_cast<size_t>(256) * t.row_words, 0u);
         for (int b = 0; b < 256; ++b) {
             uint32_t* r = &img[static_cast<size_t>(b) * t.row_words];
-            for (int32_t w = 0; w < WT; ++w) {
-                const uint32_t m = M[static_cast<size_t>(b) * WT + w];
-                r[w] = m & SH[w];
-                r[WT + w] = m & tg(0, w);
-                r[2 * WT + w] = m & tg(1, w);
-            }
-            r[3 * WT] = b == delim ? ~0u : 0u;
-        }
-        // extra groups: the byte -> class map (one byte each), then per class M & T_g
-        t.cmap_off = static_cast<uint32_t>(img.size()) * 4;
-        for (int b = 0; b < 256; b += 4) {
-            uint32_t wd = 0;
-            for (int k = 0; k < 4; ++k) wd |= static_cast<uint32_t>(b + k == delim ? 0 : p.byte_class[b + k]) << (8 * k);
-            img.push_back(wd);
-        }
-        t.xt_off = static_cast<uint32_t>(img.size()) * 4;
-        const int32_t xg = t.G > 2 ? t.G - 2 : 0;
-        t.xt_row_words = (xg * WT + 3) / 4 * 4;
-        if (xg) {
-            for (int32_t c = 0; c < p.n_classes; ++c) {
-                std::vector<uint32_t> m(WT, 0u), r(t.xt_row_words, 0u);
-                if (c) remap(&p.class_mask[static_cast<size_t>(c) * Wsrc], m.data());
-                m[A >> 5] &= ~(1u << (A & 31));
-                for (int32_t g = 2; g < t.G; ++g)
-                    for (int32_t w = 0; w < WT; ++w) r[(g - 2) * WT + w] = m[w] & tg(g, w);
-                img.insert(img.end(), r.begin(), r.end());
-            }
+            for (int32_t w = 0; w < WT; ++w) r[w] = M[static_cast<size_t>(b) * WT + w];
+            r[WT] = b == delim ? ~0u : 0u;
         }
         t.xg_off = static_cast<uint32_t>(img.size()) * 4;
-        for (int32_t g = 2; g < t.G; ++g)
+        for (int32_t g = 2; g < t.G; ++g) {
+            for (int32_t w = 0; w < WT; ++w) img.push_back(tg(g, w));
             for (int32_t w = 0; w < WT; ++w) img.push_back(rg(g, w));
-        // registers: E0, R_0, R_1
+        }
+        t.regs.insert(t.regs.end(), SH.begin(), SH.end());
         t.regs.insert(t.regs.end(), E0.begin(), E0.end());
-        for (int32_t g = 0; g < 2; ++g)
+        for (int32_t g = 0; g < 2; ++g) {
+            for (int32_t w = 0; w < WT; ++w) t.regs.push_back(tg(g, w));
             for (int32_t w = 0; w < WT; ++w) t.regs.push_back(rg(g, w));
+        }
     } else {
         // per byte: [M, D, pad 3] (the 4-word pad skews rows across banks);
         // broadcast rows SH, E0, then (T_g, R_g) for every group
@@ -201,7 +180,7 @@ struct Shape {
 // broadcast area of shared memory (SH, E0, then T_g, R_g per group).
 template <int WT, int GR, bool REG>
 struct Rows {
-    uint32_t e0[REG ? WT : 1], rr[REG ? 2 : 1][REG ? WT : 1];
+    uint32_t sh[REG ? WT : 1], e0[REG ? WT : 1], tr[REG ? 2 : 1][REG ? WT : 1], rr[REG ? 2 : 1][REG ? WT : 1];
     uint32_t base;   // !REG: shared address of the broadcast rows
 
     __device__ void load(const BArgs& a) {
@@ -209,9 +188,13 @@ struct Rows {
             const uint32_t* g = a.regs_g;
 #pragma unroll
             for (int w = 0; w < WT; ++w) {
-                e0[w] = __ldg(g + w);
-                rr[0][w] = __ldg(g + WT + w);
-                rr[1][w] = __ldg(g + 2 * WT + w);
+                sh[w] = __ldg(g + w);
+                e0[w] = __ldg(g + WT + w);
+#pragma unroll
+                for (int k = 0; k < 2; ++k) {
+                    tr[k][w] = __ldg(g + 2 * WT + 2 * k * WT + w);
+                    rr[k][w] = __ldg(g + 3 * WT + 2 * k * WT + w);
+                }
             }
         } else {
             base = a.xg;
@@ -252,7 +235,7 @@ __device__ __forceinline__ void load_words(uint32_t addr, uint32_t (&m)[N]) {
 // Row width in words (BitsTables::row_words).
 template <int WT>
 __host__ __device__ constexpr int row_words() {
-    return WT <= 4 ? (3 * WT + 1 + 3) / 4 * 4 : WT + 4;
+    return WT == 1 ? 2 : WT <= 4 ? (WT + 1 + 3) / 4 * 4 : WT + 4;
 }
 
 // The REG step on a row already loaded (rows of several bytes are loaded
@@ -261,14 +244,14 @@ template <int WT, int GR, bool REG, bool XG>
 __device__ __forceinline__ void bstep_row(const BArgs& a, const Rows<WT, GR, REG>& R, uint32_t (&E)[WT],
                                           const uint32_t (&row)[row_words<WT>()], uint32_t row_addr, uint32_t cm,
                                           uint32_t& m, uint32_t& cnt) {
-    constexpr int RW = row_words<WT>();
+
     uint32_t nx[WT];
     {
-        // shift part: E & M & SH moved up one position
+        // shift part: E & M & SH moved up one position (one 3-input LOP3 per word)
         uint32_t prev = 0;
 #pragma unroll
         for (int w = 0; w < WT; ++w) {
-            const uint32_t sh = E[w] & row[w];
+            const uint32_t sh = E[w] & row[w] & R.sh[w];
             // (a register 2, not a literal: keeps the shift an IMAD on the FMA pipe)
             nx[w] = WT == 1 ? sh * a.two : __funnelshift_l(prev, sh, 1);
             prev = sh;
@@ -277,32 +260,29 @@ __device__ __forceinline__ void bstep_row(const BArgs& a, const Rows<WT, GR, REG
         uint32_t acc0 = 0, acc1 = 0;
 #pragma unroll
         for (int w = 0; w < WT; ++w) {
-            acc0 |= E[w] & row[WT + w];
-            acc1 |= E[w] & row[2 * WT + w];
+            acc0 |= E[w] & row[w] & R.tr[0][w];
+            acc1 |= E[w] & row[w] & R.tr[1][w];
         }
 #pragma unroll
         for (int w = 0; w < WT; ++w) {
             if (acc0) nx[w] |= R.rr[0][w];
             if (acc1) nx[w] |= R.rr[1][w];
         }
-        if constexpr (XG) {   // groups >= 2: per-class M & T_g rows, R_g broadcast
-            const uint32_t b = (row_addr - a.tab) / (RW * 4u);
-            (void)RW;
-            uint32_t cls;
-            asm("ld.shared.u8 %0, [%1];" : "=r"(cls) : "r"(a.cmap + b));
-            const uint32_t xt = a.xt + cls * a.xt_row_bytes;
+        if constexpr (XG) {   // groups >= 2: T_g, R_g broadcast rows
+            (void)row_addr;
             for (int g = 2; g < a.n_groups; ++g) {
+                const uint32_t tb = a.xg + static_cast<uint32_t>(g - 2) * 2u * WT * 4u;
                 uint32_t acc = 0;
 #pragma unroll
-                for (int w = 0; w < WT; ++w) acc |= E[w] & tma::lds32(xt + ((g - 2) * WT + w) * 4u);
+                for (int w = 0; w < WT; ++w) acc |= E[w] & row[w] & tma::lds32(tb + w * 4u);
                 if (acc) {
 #pragma unroll
-                    for (int w = 0; w < WT; ++w) nx[w] |= tma::lds32(a.xg + ((g - 2) * WT + w) * 4u);
+                    for (int w = 0; w < WT; ++w) nx[w] |= tma::lds32(tb + (WT + w) * 4u);
                 }
             }
         }
     }
-    const uint32_t D = row[3 * WT];
+    const uint32_t D = row[WT];
     // string end: count A (bit 31 of the last word) on the FMA pipe, restart from E0
     cnt += __umulhi(E[WT - 1] & D & cm, a.two);
 #pragma unroll
@@ -704,7 +684,8 @@ Split split_of(uint64_t len, uint32_t chunk, bool lines) {
     return s;
 }
 
-using ShapeR = Shape<24, 2, 32, 3>;   // registers (WT <= 4)
+using ShapeR = Shape<24, 2, 32, 3>;   // registers (WT 2, 4)
+using ShapeR1 = Shape<24, 4, 32, 2>;  // one word: four independent chains per lane hide the table loads
 using ShapeS = Shape<16, 1, 32, 4>;   // shared-memory rows (WT 8, 16)
 
 template <class C>
@@ -780,9 +761,6 @@ cudaError_t run(const BitsImage& b, const uint8_t* text, uint64_t len, int32_t d
     a.img_words = static_cast<uint32_t>(b.t.img.size() / 4);
     a.regs_g = b.d_regs;
     const uint32_t smem = stage_space<C>(static_cast<uint32_t>(b.t.img.size() * 4), a);
-    a.xt = a.tab + b.t.xt_off;
-    a.cmap = a.tab + b.t.cmap_off;
-    a.xt_row_bytes = b.t.xt_row_words * 4u;
     a.xg = a.tab + b.t.xg_off;
     a.count = count;
     a.slot = cs.p;
