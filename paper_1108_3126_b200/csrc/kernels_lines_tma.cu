@@ -66,18 +66,40 @@ struct Args {
     unsigned long long* count;
     unsigned long long* slot;                   // CountSlot (launch.hpp)
     int accumulate;
-    uint8_t* results;                           // per-line results (RES): line index -> 0/1
-    const unsigned long long* line_base;        // per range: delimiters before its start
+    // per-line results (RES), in one pass: every range records the results of
+    // the lines it owns as range-local bits plus its line count; a scan of
+    // the counts and a scatter kernel place them (no delimiter pre-pass)
+    uint32_t* rbits;                            // rwords words per range
+    uint32_t rwords;
+    unsigned long long* rcount;                 // owned lines per range
 };
 
-// Per-line results bookkeeping of one range (RES): li = index of the line the
-// walk is in (delimiters before the range start, +1 per delimiter), own =
-// whether that line belongs to this range (it started inside it).
+// Per-line results bookkeeping of one range (RES): the results of the lines
+// it owns, in order, packed 32 to a word; own = whether the line the walk is
+// in belongs to this range (it started inside it).
 struct LineCursor {
-    uint64_t li;
+    uint32_t lj;     // owned lines recorded so far
+    uint32_t bits;   // the current word of results
+    uint32_t* out;   // the range's next result word
     bool own;
-    bool live;   // false for lanes past the last range (they read zero fill)
+    bool live;       // false for lanes past the last range (they read zero fill)
+
+    __device__ __forceinline__ void push(uint32_t v) {
+        bits |= v << (lj & 31);
+        if ((++lj & 31) == 0) {
+            *out++ = bits;
+            bits = 0;
+        }
+    }
+    __device__ __forceinline__ void close(unsigned long long* count) {
+        if (lj & 31) *out = bits;
+        *count = lj;
+    }
 };
+
+__device__ __forceinline__ LineCursor cursor_of(const Args& a, uint64_t range, bool own, bool live) {
+    return LineCursor{0u, 0u, a.rbits ? a.rbits + range * a.rwords : nullptr, own, live};
+}
 
 // Kernel shape: warps per CTA, ranges per lane, bytes per range per stage, ring depth.
 template <int W, int K, int SL, int ST>
@@ -207,8 +229,7 @@ __device__ __forceinline__ uint32_t step_res(const Args& a, uint32_t s, uint32_t
     const uint32_t c = counted<L>(a, s);
     cnt += c;
     if (b == a.delim) {
-        if (lc.own) a.results[lc.li] = static_cast<uint8_t>(c);
-        ++lc.li;
+        if (lc.own) lc.push(c);
         lc.own = lc.live;
     }
     return s;
@@ -359,7 +380,7 @@ __device__ void finish_lines(const Args& a, uint32_t (&s)[K], uint64_t (&pos)[K]
 template <int L, bool RES>
 __device__ void range_direct(const Args& a, uint64_t c0, uint64_t c1, uint64_t range, uint32_t& cnt) {
     uint32_t s = c0 == 0 ? a.start : a.skip;
-    LineCursor lc{RES ? a.line_base[range] : 0, s == a.start, true};
+    LineCursor lc = cursor_of(a, range, s == a.start, true);
     uint32_t last = 0;
     uint64_t pos = c0;
     for (; pos + 16 <= c1; pos += 16) {
@@ -390,8 +411,9 @@ __device__ void range_direct(const Args& a, uint64_t c0, uint64_t c1, uint64_t r
     if (next_line || (s != a.skip && last != a.delim)) {
         const uint32_t ok = finish_line<L>(a, (next_line ? a.start : s) + a.tail_delta, c1) == a.term_acc;
         cnt += ok;
-        if constexpr (RES) a.results[lc.li] = static_cast<uint8_t>(ok);
+        if constexpr (RES) lc.push(ok);
     }
+    if constexpr (RES) lc.close(a.rcount + range);
 }
 
 template <class C, int L, bool RES>
@@ -461,7 +483,7 @@ __global__ void __launch_bounds__(C::warps * 32, 1) k_lines_tma(const __grid_con
             valid[j] = row < a.rows;
             s[j] = a.void_row;
             if (valid[j]) s[j] = row == 0 ? a.start : a.skip;   // see the ownership note above range_direct
-            lc[j] = LineCursor{RES && valid[j] ? a.line_base[row] : 0, valid[j] && s[j] == a.start, valid[j]};
+            lc[j] = cursor_of(a, RES && valid[j] ? row : 0, valid[j] && s[j] == a.start, valid[j]);
         }
         uint32_t last[C::chains] = {};
         for (uint32_t col = 0; col < ncol; ++col) {
@@ -512,8 +534,7 @@ __global__ void __launch_bounds__(C::warps * 32, 1) k_lines_tma(const __grid_con
                             uint32_t dm = dl[j];
                             while (dm) {   // the lines that ended in these 32 bytes, in byte order
                                 const uint32_t i = __ffs(dm) - 1;
-                                if (lc[j].own) a.results[lc[j].li] = static_cast<uint8_t>((cl[j] >> i) & 1u);
-                                ++lc[j].li;
+                                if (lc[j].own) lc[j].push((cl[j] >> i) & 1u);
                                 lc[j].own = lc[j].live;
                                 dm &= dm - 1;
                             }
@@ -546,8 +567,10 @@ __global__ void __launch_bounds__(C::warps * 32, 1) k_lines_tma(const __grid_con
 #pragma unroll
             for (int j = 0; j < C::chains; ++j) {
                 cnt += ok[j];
-                if constexpr (RES)
-                    if (live[j]) a.results[lc[j].li] = static_cast<uint8_t>(ok[j]);
+                if constexpr (RES) {
+                    if (live[j]) lc[j].push(ok[j]);
+                    if (valid[j]) lc[j].close(a.rcount + row0 + j * 32 + lane);
+                }
             }
         }
     }
@@ -594,30 +617,21 @@ CUtensorMapSwizzle swizzle_of(int slice) {
     }
 }
 
-// Delimiters per range (RES): TMA rows [i*chunk, +chunk), then the remainder
-// pieces [rows*chunk + p*rem_piece, +rem_piece). One warp per range, 512
-// coalesced bytes per iteration (ranges start 16-byte aligned).
-__global__ void __launch_bounds__(256) k_lt_range_delims(const uint8_t* __restrict__ text, uint64_t len, uint32_t chunk,
-                                                         uint64_t rows, uint32_t rem_piece, uint64_t nranges,
-                                                         uint32_t delim, unsigned long long* __restrict__ out) {
+// Per-line results (RES), second pass: range r's owned lines start at
+// line base[r] (exclusive scan of the counts); one warp per range writes
+// them from its result bits, coalesced.
+__global__ void __launch_bounds__(256) k_lt_scatter(const uint32_t* __restrict__ rbits, uint32_t rwords,
+                                                    const unsigned long long* __restrict__ count,
+                                                    const unsigned long long* __restrict__ base, uint64_t nranges,
+                                                    uint8_t* __restrict__ results) {
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t nwarps = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5);
-    const uint32_t d4 = delim * 0x01010101u;
-    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); i < nranges;
-         i += nwarps) {
-        const uint64_t c0 = i < rows ? i * chunk : rows * chunk + (i - rows) * rem_piece;
-        const uint64_t c1 = min(c0 + (i < rows ? chunk : rem_piece), len);
-        uint32_t n = 0;
-        uint64_t pos = c0 + 16 * lane;
-        for (; pos + 16 <= c1; pos += 512) {
-            const uint4 v = __ldcs(reinterpret_cast<const uint4*>(text + pos));
-            n += __popc(__vcmpeq4(v.x, d4)) + __popc(__vcmpeq4(v.y, d4)) + __popc(__vcmpeq4(v.z, d4)) +
-                 __popc(__vcmpeq4(v.w, d4));
-        }
-        n /= 8;
-        for (; pos < c1; ++pos) n += text[pos] == delim;   // the last partial group (one lane)
-        n = __reduce_add_sync(0xFFFFFFFFu, n);
-        if (lane == 0) out[i] = n;
+    for (uint64_t r = static_cast<uint64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); r < nranges;
+         r += nwarps) {
+        const uint32_t n = static_cast<uint32_t>(count[r]);
+        const uint64_t b = base[r];
+        const uint32_t* bits = rbits + r * rwords;
+        for (uint32_t i = lane; i < n; i += 32) results[b + i] = static_cast<uint8_t>((__ldg(bits + (i >> 5)) >> (i & 31)) & 1u);
     }
 }
 
@@ -660,11 +674,20 @@ RangeSplit split_ranges(uint64_t len, uint32_t chunk) {
     return r;
 }
 
-size_t res_scratch_bytes(uint64_t nranges) {
+// RES scratch: [counts | bases | scan temp | result bits (rwords per range)].
+uint32_t res_words(uint32_t chunk, uint32_t rem_piece) {
+    return ((chunk > rem_piece ? chunk : rem_piece) + 1 + 31) / 32;
+}
+
+size_t res_temp_bytes(uint64_t nranges) {
     size_t temp = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, temp, static_cast<unsigned long long*>(nullptr),
                                   static_cast<unsigned long long*>(nullptr), static_cast<int64_t>(nranges));
-    return 2 * nranges * sizeof(unsigned long long) + temp + 256;
+    return (temp + 255) & ~size_t(255);
+}
+
+size_t res_scratch_bytes(uint64_t nranges, uint32_t rwords) {
+    return 2 * nranges * sizeof(unsigned long long) + res_temp_bytes(nranges) + nranges * rwords * 4ull + 256;
 }
 
 template <class C, int L, bool RES>
@@ -685,24 +708,16 @@ cudaError_t launch(const LtTable& t, const uint8_t* text, uint64_t len, uint8_t 
     a.tiles = (a.rows + C::rows - 1) / C::rows;
     a.rem_piece = rs.rem_piece;
     a.rem_pieces = rs.rem_pieces;
+    const uint64_t nr = rs.rows + rs.rem_pieces;
+    unsigned long long* base = nullptr;
+    void* temp = nullptr;
     if constexpr (RES) {
-        const uint64_t nr = rs.rows + rs.rem_pieces;
-        if (!scratch || scratch_bytes < res_scratch_bytes(nr)) return cudaErrorInvalidValue;
-        auto* per = static_cast<unsigned long long*>(scratch);
-        auto* base = per + nr;
-        void* temp = base + nr;
-        size_t temp_bytes = scratch_bytes - 2 * nr * sizeof(unsigned long long);
-        int dev = 0;
-        cudaGetDevice(&dev);
-        const uint64_t want = (nr + 7) / 8, cap = static_cast<uint64_t>(device_sm_count(dev)) * 8;
-        k_lt_range_delims<<<static_cast<unsigned>(want < cap ? want : cap), 256, 0, st>>>(text, len, chunk, rs.rows,
-                                                                                          rs.rem_piece, nr, delim, per);
-        cudaError_t e = cudaGetLastError();
-        if (e != cudaSuccess) return e;
-        e = cub::DeviceScan::ExclusiveSum(temp, temp_bytes, per, base, static_cast<int64_t>(nr), st);
-        if (e != cudaSuccess) return e;
-        a.results = results;
-        a.line_base = base;
+        a.rwords = res_words(chunk, rs.rem_piece);
+        if (!scratch || scratch_bytes < res_scratch_bytes(nr, a.rwords)) return cudaErrorInvalidValue;
+        a.rcount = static_cast<unsigned long long*>(scratch);
+        base = a.rcount + nr;
+        temp = base + nr;
+        a.rbits = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(temp) + res_temp_bytes(nr));
     }
     a.img_lo = static_cast<const uint4*>(t.d_lo);
     a.lo_addr = t.lo_addr;
@@ -758,6 +773,15 @@ cudaError_t launch(const LtTable& t, const uint8_t* text, uint64_t len, uint8_t 
     const uint64_t want = a.tiles;   // at most one tile per CTA needed to reach every SM
     const int grid = static_cast<int>(want == 0 ? 1 : (want < cap ? want : cap));
     k_lines_tma<C, L, RES><<<grid, C::warps * 32, smem, st>>>(a, map);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess || !RES) return e;
+    // per-line results: place each range's owned lines (scan of the counts, then scatter)
+    size_t temp_bytes = res_temp_bytes(nr);
+    e = cub::DeviceScan::ExclusiveSum(temp, temp_bytes, a.rcount, base, static_cast<int64_t>(nr), st);
+    if (e != cudaSuccess) return e;
+    const uint64_t want2 = (nr + 7) / 8, cap2 = static_cast<uint64_t>(device_sm_count(dev)) * 16;
+    k_lt_scatter<<<static_cast<unsigned>(want2 < cap2 ? want2 : cap2), 256, 0, st>>>(a.rbits, a.rwords, a.rcount, base, nr,
+                                                                                   results);
     return cudaGetLastError();
 }
 
@@ -811,7 +835,7 @@ uint32_t lines_tma_chunk(const LtTable& t, uint64_t len, uint32_t chunk) {
 
 size_t lines_tma_results_scratch(uint64_t len, uint32_t chunk) {
     const RangeSplit rs = split_ranges(len, chunk);
-    return res_scratch_bytes(rs.rows + rs.rem_pieces);
+    return res_scratch_bytes(rs.rows + rs.rem_pieces, res_words(chunk, rs.rem_piece));
 }
 
 cudaError_t launch_lines_tma_results(const LtTable& t, const uint8_t* text, uint64_t len, uint8_t delim,
