@@ -181,6 +181,41 @@ __device__ uint32_t walk(const Args& a, uint32_t s, uint64_t lo, uint64_t hi) {
     return canon<L>(s);
 }
 
+// Packed layout: the transfer function of [lo, hi) — the exit state from
+// every state at once (six chains on one table word per byte), as six 5-bit
+// fields (field i = the encoded exit state from state 5i).
+__device__ uint32_t walk_fn(const Args& a, uint64_t lo, uint64_t hi) {
+    const uint32_t lb = lane_base();
+    uint32_t s[6] = {0u, 5u, 10u, 15u, 20u, 25u};
+    auto one = [&](uint32_t w) {
+#pragma unroll
+        for (int i = 0; i < 6; ++i) s[i] = shr_wrap(w, s[i]);
+    };
+    uint64_t p = lo;
+    for (; p < hi && (p & 15); ++p) one(tma::lds32(lb + (static_cast<uint32_t>(a.text[p]) << 7)));
+    for (; p + 16 <= hi; p += 16) {
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(a.text + p));
+#pragma unroll
+        for (int w = 0; w < 4; ++w)
+#pragma unroll
+            for (int k = 0; k < 4; ++k) one(tma::lds32(__dp4a(tma::word_of(v, w), 128u << (8 * k), lb)));
+    }
+    for (; p < hi; ++p) one(tma::lds32(lb + (static_cast<uint32_t>(a.text[p]) << 7)));
+    uint32_t f = 0;
+#pragma unroll
+    for (int i = 0; i < 6; ++i) f |= (s[i] & 31u) << (5 * i);
+    return f;
+}
+
+// g after f (f's ranges come first): field i = g's field at f's field i.
+__device__ __forceinline__ uint32_t fn_then(uint32_t f, uint32_t g) {
+    uint32_t r = 0;
+#pragma unroll
+    for (int i = 0; i < 6; ++i) r |= (shr_wrap(g, (f >> (5 * i)) & 31u) & 31u) << (5 * i);
+    return r;
+}
+constexpr uint32_t kFnIdentity = 0u | (5u << 5) | (10u << 10) | (15u << 15) | (20u << 20) | (25u << 25);
+
 template <int L>
 __device__ uint32_t entry_guess(const Args& a, uint64_t r) {
     const uint64_t c0 = r * a.chunk;
@@ -464,6 +499,46 @@ __global__ void __launch_bounds__(C::warps * 32, 1) k_chunk_tma(const __grid_con
     const uint64_t gtid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     for (uint64_t t = gtid; t <= a.tiles; t += nthreads) a.seam[t] = 0;   // idle again (seams checked in-stream)
     unsigned long long fb = ~*reinterpret_cast<volatile unsigned long long*>(a.bad_inv);
+    if constexpr (L == 3) {
+        // Packed tables (<= 6 states): no repair rounds. Every range from the
+        // first wrong guess on computes its transfer function (its exit from
+        // every state), the functions are composed in range order (threads own
+        // contiguous runs; warp, block and grid reductions keep the order), and
+        // the composite applied to the exact exit before fb is the answer:
+        // exact for non-synchronising automata ((aaa)*) in one extra pass.
+        if (fb != ~0ull) {
+            const uint64_t nfn = a.nranges - fb;
+            const uint64_t per_t = (nfn + nthreads - 1) / nthreads;
+            uint32_t f = kFnIdentity;
+            for (uint64_t j = fb + gtid * per_t; j < fb + min((gtid + 1) * per_t, nfn); ++j)
+                f = fn_then(f, walk_fn(a, j * a.chunk, min((j + 1) * a.chunk, a.len)));
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {   // lanes in order: lane i then lanes above it
+                const uint32_t g = __shfl_down_sync(0xFFFFFFFFu, f, off);
+                if (lane + off < 32) f = fn_then(f, g);
+            }
+            uint32_t* wf = reinterpret_cast<uint32_t*>(sm + (a.bar_addr + C::warps * C::stages * 8 + 16 - kLtSmemBase));
+            if (lane == 0) wf[warp] = f;
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                uint32_t b = kFnIdentity;
+                for (uint32_t w = 0; w < C::warps; ++w) b = fn_then(b, wf[w]);
+                a.g[blockIdx.x] = b;   // (the guesses are not needed any more)
+            }
+            grid.sync();
+            if (blockIdx.x == 0 && threadIdx.x == 0) {
+                uint32_t x = fb == 0 ? a.entry : a.e[fb - 1];
+                for (uint32_t b = 0; b < gridDim.x; ++b) x = shr_wrap(a.g[b], x) & 31u;
+                *a.accept = static_cast<int32_t>((a.acc_mask >> (x / 5u)) & 1u);
+                if (a.repairs) *a.repairs = nfn;
+                if (a.exit_state) *a.exit_state = x;
+                atomicExch(a.bad_inv, 0ull);
+            }
+            return;
+        }
+        if (blockIdx.x == 0 && threadIdx.x < 32) repair_and_answer<L>(a);   // every guess right: the answer
+        return;
+    }
     // Round: every range j >= fb whose guess differs from its predecessor's
     // exit re-walks from that exit (stopping where it meets its recorded
     // trajectory). Ranges below the first mismatch are exact and final, so
@@ -525,7 +600,7 @@ cudaError_t run(const LtTable& t, Args& a, int device, cudaStream_t st) {
     uint32_t p = align_up(t.smem_table_end, 1024);
     for (int k = 0; k < C::warps * C::stages; ++k, p += C::stage_bytes) a.stage_addr[k] = p;
     a.bar_addr = align_up(p, 8);
-    const uint32_t smem = a.bar_addr + C::warps * C::stages * 8 + 16 - kLtSmemBase;   // ring barriers, `last`, table barrier
+    const uint32_t smem = a.bar_addr + C::warps * C::stages * 8 + 16 + 4 * C::warps - kLtSmemBase;   // ring barriers, `last`, table barrier, per-warp functions
     CUtensorMap map;
     std::memset(&map, 0, sizeof(map));
     if (a.rows > 0 && tma::make_map(&map, a.text, a.rows, a.chunk, C::slice, C::rows) != CUDA_SUCCESS)

@@ -288,3 +288,25 @@ def test_pernode_segments_across_sms_equal_one_warp(pat, alpha, n):
         m.match_one_ex(d, acc, "dfa_seq", nbytes=n)
         torch.cuda.synchronize()
         assert seg == one == bool(acc.item()), (pat, tail)
+
+
+@pytest.mark.parametrize("n", [(64 << 20) + 1, (64 << 20) + 2, 64 << 20, (16 << 20) + 5])
+def test_chunked_nonsynchronizing_by_transfer_functions(n):
+    """(aaa)* / (aa)* over long strings of a's: every entry guess of the
+    chunk-parallel engine is wrong; the packed layout composes the ranges'
+    transfer functions in order instead of repairing range by range. Known
+    answers (n mod 3, n mod 2) and a broken string."""
+    import torch
+
+    d = torch.full((n + 64,), ord("a"), dtype=torch.uint8, device="cuda")
+    acc = torch.zeros(1, dtype=torch.int32, device="cuda")
+    for pat, want in (("(aaa)*", n % 3 == 0), ("(aa)*", n % 2 == 0), ("(aaaa|aaaaaa)*", n % 2 == 0 and n != 2)):
+        m = rx.Matcher(pat)
+        m.match_one_ex(d, acc, "chunked", nbytes=n)
+        torch.cuda.synchronize()
+        assert bool(acc.item()) == want, (pat, n)
+    d[n // 3] = ord("b")
+    m = rx.Matcher("(aaa)*")
+    m.match_one_ex(d, acc, "chunked", nbytes=n)
+    torch.cuda.synchronize()
+    assert not bool(acc.item())
