@@ -193,6 +193,32 @@ __device__ uint32_t walk_fn(const Args& a, uint64_t lo, uint64_t hi) {
     };
     uint64_t p = lo;
     for (; p < hi && (p & 15); ++p) one(tma::lds32(lb + (static_cast<uint32_t>(a.text[p]) << 7)));
+    // 128 bytes per round trip, software pipelined (the next 128 bytes are
+    // requested before these are walked: a lone thread's dependent 16-byte
+    // loads would expose the DRAM latency every 16 bytes)
+    constexpr int U = 8;
+    uint4 nv[U];
+    if (p + 16 * U <= hi) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) nv[u] = __ldcs(reinterpret_cast<const uint4*>(a.text + p) + u);
+    }
+    for (; p + 16 * U <= hi; p += 16 * U) {
+        uint4 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) v[u] = nv[u];
+        if (p + 32 * U <= hi) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) nv[u] = __ldcs(reinterpret_cast<const uint4*>(a.text + p + 16 * U) + u);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            uint32_t t[16];   // the table words depend on the input only: load all 16 first
+#pragma unroll
+            for (int i = 0; i < 16; ++i) t[i] = tma::lds32(__dp4a(tma::word_of(v[u], i >> 2), 128u << (8 * (i & 3)), lb));
+#pragma unroll
+            for (int i = 0; i < 16; ++i) one(t[i]);
+        }
+    }
     for (; p + 16 <= hi; p += 16) {
         const uint4 v = __ldg(reinterpret_cast<const uint4*>(a.text + p));
 #pragma unroll
