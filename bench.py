@@ -590,15 +590,19 @@ def bench_single(ctx, cfg: str, steps: int, warmup: int, headline: bool, engine:
         "gpu_launches": launches * steps,
     }
     if not ctx.args.no_e2e and engine == "auto":
-        w = host.numpy()
-        m.lockstep_accepts(w)   # warm
-        k = max(1, steps // 2)
-        t0 = time.perf_counter()
-        for _ in range(k):
-            m.lockstep_accepts(w)
-        t = ctx.max_over_ranks((time.perf_counter() - t0) / k)
+        def e2e_time(w):
+            m.lockstep_accepts(w)   # warm
+            k = max(1, steps // 2)
+            t0 = time.perf_counter()
+            for _ in range(k):
+                m.lockstep_accepts(w)
+            return ctx.max_over_ranks((time.perf_counter() - t0) / k)
+
+        t = e2e_time(host.numpy())
+        tp = e2e_time(text)
         rec["e2e"] = {"value": ctx.world * nb / t / 1e9, "unit": "GB/s", "h2d_bytes_per_step": nb,
-                      "d2h_bytes_per_step": 4, "host_buffer": "pinned"}
+                      "d2h_bytes_per_step": 4, "host_buffer": "pinned",
+                      "pageable": {"value": ctx.world * nb / tp / 1e9, "unit": "GB/s"}}
     if ctx.rank == 0 and ctx.world == 1 and not ctx.args.no_cpu and engine == "auto":
         rec["cpu_baseline"] = cpu_record(cfg, pattern, text, ctx.args.cpu_target_s if headline else ctx.args.sub_cpu_s)
     return rec

@@ -73,6 +73,8 @@ rxg_heap::~rxg_heap() {
     for (void* p : allocs) cudaFree(p);
     for (auto* p : d_stage)
         if (p) cudaFree(p);
+    for (auto* p : h_pin)
+        if (p) cudaFreeHost(p);
     if (d_count) cudaFree(d_count);
     if (d_accept) cudaFree(d_accept);
     if (stream) cudaStreamDestroy(stream);
@@ -1159,13 +1161,68 @@ int rxg_match_one_device(rxg_heap* h, const uint8_t* d_bytes, uint64_t len, int 
     return rxg_match_one_ex(h, d_bytes, len, engine, d_accept, nullptr, stream);
 }
 
+}  // extern "C"
+
+namespace {
+
+// H2D of one host buffer on h->stream. Pageable input of 4 MiB and more goes
+// through the heap's pinned pieces, filled by a few host threads while the
+// previous piece crosses PCIe (a driver copy from pageable memory runs at the
+// speed of one CPU thread).
+int stage_pageable_aware(rxg_heap* h, uint8_t* dst, const uint8_t* src, uint64_t len) {
+    if (!len) return RXG_OK;
+    cudaPointerAttributes pa{};
+    const bool pageable = len >= (4u << 20) &&
+                          (cudaPointerGetAttributes(&pa, src) != cudaSuccess || pa.type == cudaMemoryTypeUnregistered);
+    cudaGetLastError();
+    if (!pageable) {
+        RXG_CUDA(cudaMemcpyAsync(dst, src, len, cudaMemcpyHostToDevice, h->stream));
+        return RXG_OK;
+    }
+    constexpr uint64_t kPiece = 64ull << 20;
+    const uint64_t piece = std::min<uint64_t>(kPiece, len);
+    if (h->pin_bytes < piece) {
+        for (auto*& p : h->h_pin) {
+            if (p) cudaFreeHost(p);
+            p = nullptr;
+        }
+        h->pin_bytes = 0;
+        for (auto*& p : h->h_pin) RXG_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&p), piece, cudaHostAllocDefault));
+        h->pin_bytes = piece;
+    }
+    if (!h->copier) {
+        const unsigned hc = std::thread::hardware_concurrency();
+        h->copier = std::make_unique<HostCopyPool>(std::min(8u, std::max(2u, hc / 2)));
+    }
+    cudaEvent_t done[2];
+    for (auto& e : done) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    cudaError_t e = cudaSuccess;
+    uint64_t i = 0;
+    for (uint64_t off = 0; off < len && e == cudaSuccess; off += piece, ++i) {
+        const int k = static_cast<int>(i & 1);
+        const uint64_t n = std::min(piece, len - off);
+        if (i >= 2) cudaEventSynchronize(done[k]);
+        h->copier->copy(h->h_pin[k], src + off, n);
+        e = cudaMemcpyAsync(dst + off, h->h_pin[k], n, cudaMemcpyHostToDevice, h->stream);
+        if (e == cudaSuccess) e = cudaEventRecord(done[k], h->stream);
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);   // the pinned pieces are reused by the next call
+    for (auto& d : done) cudaEventDestroy(d);
+    if (e != cudaSuccess) return cuda_fail(e, "staged upload");
+    return RXG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
 int rxg_match_one(rxg_heap* h, const uint8_t* bytes, uint64_t len, int engine, int32_t* accept) {
     if (int rc = need_device(h, engine == RXG_ENGINE_DFA_SEQ || engine == RXG_ENGINE_CHUNKED)) return rc;
     if (!accept || (!bytes && len)) return fail(RXG_EINVAL, "bad arguments");
     std::lock_guard<std::mutex> host_lock(h->host_mu);
     DeviceGuard g(h->device);
     if (int rc = ensure_stage(h, std::max<size_t>(len, 16))) return rc;
-    if (len) RXG_CUDA(cudaMemcpyAsync(h->d_stage[0], bytes, len, cudaMemcpyHostToDevice, h->stream));
+    if (int rc = stage_pageable_aware(h, h->d_stage[0], bytes, len)) return rc;
     if (int rc = rxg_match_one_device(h, h->d_stage[0], len, engine, h->d_accept, h->stream)) return rc;
     RXG_CUDA(cudaMemcpyAsync(accept, h->d_accept, sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream));
     RXG_CUDA(cudaStreamSynchronize(h->stream));
@@ -1285,6 +1342,27 @@ int host_batch(rxg_heap* h, const uint8_t* text, uint64_t len, int32_t delimiter
         }
         RXG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_res), std::max<uint64_t>(nstr, 1) + 1, h->stream));
     }
+    // Pageable input (the C++ facade's std::string, a numpy array): a driver
+    // copy from pageable memory stages through one CPU thread (~11 GB/s
+    // measured); instead a few host threads fill pinned pieces while the
+    // previous piece crosses PCIe and is matched.
+    cudaPointerAttributes pa{};
+    const bool pageable = len >= (4u << 20) &&
+                          (cudaPointerGetAttributes(&pa, text) != cudaSuccess || pa.type == cudaMemoryTypeUnregistered);
+    cudaGetLastError();
+    if (pageable && h->pin_bytes < maxp) {
+        for (auto*& p : h->h_pin) {
+            if (p) cudaFreeHost(p);
+            p = nullptr;
+        }
+        h->pin_bytes = 0;
+        for (auto*& p : h->h_pin) RXG_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&p), maxp, cudaHostAllocDefault));
+        h->pin_bytes = maxp;
+    }
+    if (pageable && !h->copier) {
+        const unsigned hc = std::thread::hardware_concurrency();
+        h->copier = std::make_unique<HostCopyPool>(std::min(8u, std::max(2u, hc / 2)));
+    }
     cudaEvent_t copied[2], consumed[2];
     for (int i = 0; i < 2; ++i) {
         cudaEventCreateWithFlags(&copied[i], cudaEventDisableTiming);
@@ -1302,7 +1380,13 @@ int host_batch(rxg_heap* h, const uint8_t* text, uint64_t len, int32_t delimiter
         const int k = static_cast<int>(i & 1);
         const uint64_t n = b[i + 1] - b[i];
         if (i >= 2) cudaStreamWaitEvent(h->copy_stream, consumed[k], 0);
-        cudaMemcpyAsync(h->d_stage[k], text + b[i], n, cudaMemcpyHostToDevice, h->copy_stream);
+        if (pageable) {   // pinned piece k is free once its previous H2D copy (piece i - 2) has landed
+            if (i >= 2) cudaEventSynchronize(copied[k]);
+            h->copier->copy(h->h_pin[k], text + b[i], n);
+            cudaMemcpyAsync(h->d_stage[k], h->h_pin[k], n, cudaMemcpyHostToDevice, h->copy_stream);
+        } else {
+            cudaMemcpyAsync(h->d_stage[k], text + b[i], n, cudaMemcpyHostToDevice, h->copy_stream);
+        }
         cudaEventRecord(copied[k], h->copy_stream);
         cudaStreamWaitEvent(h->stream, copied[k], 0);
         rc = batch_any(h, h->d_stage[k], n, delimiter, stride, RXG_BATCH_AUTO, h->d_count,

@@ -5,11 +5,14 @@
 
 #include <cuda_runtime.h>
 
+#include <condition_variable>
 #include <cstdint>
+#include <cstring>
 #include <map>
 #include <memory>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "rxg.h"
@@ -45,6 +48,67 @@ struct TableSlot {
 
 constexpr int32_t kMaxDfaStates = 16384;
 
+// A few host threads that copy one buffer in parallel (pageable input into
+// pinned staging: one thread's memcpy runs far below the PCIe link).
+class HostCopyPool {
+public:
+    explicit HostCopyPool(unsigned n) : n_(n ? n : 1) {
+        for (unsigned k = 0; k < n_; ++k) threads_.emplace_back([this, k] { loop(k); });
+    }
+    ~HostCopyPool() {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            quit_ = true;
+        }
+        go_.notify_all();
+        for (auto& t : threads_) t.join();
+    }
+    void copy(void* dst, const void* src, size_t n) {
+        std::unique_lock<std::mutex> lk(mu_);
+        dst_ = static_cast<uint8_t*>(dst);
+        src_ = static_cast<const uint8_t*>(src);
+        len_ = n;
+        pending_ = n_;
+        ++gen_;
+        go_.notify_all();
+        done_.wait(lk, [&] { return pending_ == 0; });
+    }
+
+private:
+    void loop(unsigned k) {
+        uint64_t seen = 0;
+        for (;;) {
+            uint8_t* d;
+            const uint8_t* s;
+            size_t n;
+            {
+                std::unique_lock<std::mutex> lk(mu_);
+                go_.wait(lk, [&] { return quit_ || gen_ != seen; });
+                if (quit_) return;
+                seen = gen_;
+                d = dst_;
+                s = src_;
+                n = len_;
+            }
+            const size_t part = (n / n_ + 4095) & ~size_t(4095);
+            const size_t lo = std::min(n, part * k), hi = std::min(n, lo + part);
+            if (hi > lo) std::memcpy(d + lo, s + lo, hi - lo);
+            std::lock_guard<std::mutex> lk(mu_);
+            if (--pending_ == 0) done_.notify_all();
+        }
+    }
+    unsigned n_;
+    std::vector<std::thread> threads_;
+    std::mutex mu_;
+    std::condition_variable go_, done_;
+    uint64_t gen_ = 0;
+    unsigned pending_ = 0;
+    bool quit_ = false;
+    uint8_t* dst_ = nullptr;
+    const uint8_t* src_ = nullptr;
+    size_t len_ = 0;
+};
+
 }  // namespace rxg
 
 struct rxg_heap {
@@ -66,6 +130,10 @@ struct rxg_heap {
     // staging for host-buffer calls
     uint8_t* d_stage[2] = {nullptr, nullptr};
     size_t stage_bytes = 0;
+    // pageable host input: pinned staging pieces, filled by a few host threads
+    uint8_t* h_pin[2] = {nullptr, nullptr};
+    size_t pin_bytes = 0;
+    std::unique_ptr<rxg::HostCopyPool> copier;
     unsigned long long* d_count = nullptr;
     int32_t* d_accept = nullptr;
     cudaStream_t stream = nullptr;
