@@ -28,6 +28,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 
@@ -450,10 +451,15 @@ __global__ void __launch_bounds__(C::warps * 32, 1) k_lines_tma(const __grid_con
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();   // barrier initialisation visible to every thread
-    mbar_wait(tbar, 0);
+    // class layouts may put ring stages in the image's unused rows: no stage
+    // is filled before the image has landed. The direct layout's ring lies
+    // outside the image, so its first stages are requested before the wait
+    // (the table copy and the first data round trip overlap).
+    if constexpr (L != 0) mbar_wait(tbar, 0);
 
     uint32_t cnt = 0;
-    if (blockIdx.x == 0 && warp == 0) {
+    if (blockIdx.x == 0 && warp == 0 && a.rem_pieces) {
+        mbar_wait(tbar, 0);
         const uint64_t r0 = a.rows * a.chunk;
         for (uint32_t p = lane; p < a.rem_pieces; p += 32) {
             const uint64_t c0 = r0 + static_cast<uint64_t>(p) * a.rem_piece;
@@ -474,6 +480,7 @@ __global__ void __launch_bounds__(C::warps * 32, 1) k_lines_tma(const __grid_con
                 tma_issue<C::stage_bytes>(&map, stage[st], bar0 + st * 8, static_cast<int32_t>(st * C::slice),
                                           static_cast<int32_t>(row0));
         }
+        if constexpr (L == 0) mbar_wait(tbar, 0);
         uint32_t s[C::chains];
         bool valid[C::chains];
         LineCursor lc[C::chains];
@@ -653,6 +660,13 @@ uint32_t auto_chunk(const LtTable& t, uint64_t len) {
     const uint64_t rows = static_cast<uint64_t>(per_sm_of<C, L, false>(smem)) * device_sm_count(dev) * C::warps * C::rows;
     uint64_t c = (len + rows - 1) / rows;
     c = (c + C::slice - 1) / C::slice * C::slice;
+    // Small inputs (a strong-scaled shard): one wave of ranges makes them so
+    // short that each range's fixed costs (entry, straddling-line tail) rule;
+    // up to 2 KB, half a wave of twice-as-long ranges is faster. Measured on
+    // config (c) shards, direct layout (tools/chunk_sweep.py): 1/8 of the job
+    // 384 -> 768 B per range 54.3 -> 48.1 us, 1/4 768 -> 1536 B 76.8 -> 70.7
+    // us, 1/2 and the whole job unchanged.
+    if (L == 0) c = std::max<uint64_t>(c, std::min<uint64_t>(2048, 2 * c));
     if (c < 4u * C::slice) c = 4u * C::slice;
     if (c > (1u << 20)) c = 1u << 20;
     return static_cast<uint32_t>(c);
