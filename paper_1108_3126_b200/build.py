@@ -65,7 +65,7 @@ def build(verbose: bool = False, force: bool = False) -> Path:
     cli_src = CSRC / "tools" / "rxgmatch.cpp"
     if force or not CLI.exists() or cli_src.stat().st_mtime > CLI.stat().st_mtime or OUT.stat().st_mtime > CLI.stat().st_mtime:
         subprocess.run(["g++", "-std=c++17", "-O2", f"-I{ROOT / 'include'}", str(cli_src), f"-L{PKG}", "-lrxg",
-                        "-Wl,-rpath,$ORIGIN", "-o", str(CLI)], check=True)
+                        "-Wl,-rpath,$ORIGIN", "-pthread", "-o", str(CLI)], check=True)
     # measurement tool (not product): the INT32 peak of SURVEY.md §8(d)'s roofline
     peak_src = ROOT / "tools" / "peaks" / "int32_peak.cu"
     peak_so = ROOT / "tools" / "peaks" / "libint32peak.so"

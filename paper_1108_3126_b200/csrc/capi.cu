@@ -75,6 +75,10 @@ rxg_heap::~rxg_heap() {
         if (p) cudaFree(p);
     for (auto* p : h_pin)
         if (p) cudaFreeHost(p);
+    for (auto* p : d_rres)
+        if (p) cudaFree(p);
+    for (auto* p : h_rres)
+        if (p) cudaFreeHost(p);
     if (d_count) cudaFree(d_count);
     if (d_accept) cudaFree(d_accept);
     if (stream) cudaStreamDestroy(stream);
@@ -604,13 +608,7 @@ namespace detail {
 
 uint64_t count_strings(const uint8_t* text, uint64_t lo, uint64_t hi, int32_t delimiter, uint32_t stride) {
     if (delimiter < 0) return (hi - lo) / stride;
-    uint64_t n = 0;
-    for (const uint8_t* p = text + lo; p < text + hi;) {
-        const void* q = std::memchr(p, delimiter, static_cast<size_t>(text + hi - p));
-        if (!q) break;
-        ++n;
-        p = static_cast<const uint8_t*>(q) + 1;
-    }
+    uint64_t n = count_byte(text + lo, hi - lo, static_cast<uint8_t>(delimiter));
     if (hi > lo && text[hi - 1] != static_cast<uint8_t>(delimiter)) ++n;
     return n;
 }
@@ -1331,21 +1329,10 @@ int host_batch(rxg_heap* h, const uint8_t* text, uint64_t len, int32_t delimiter
     uint64_t maxp = 16;
     for (size_t i = 0; i + 1 < b.size(); ++i) maxp = std::max(maxp, b[i + 1] - b[i]);
     if (int rc = ensure_stage(h, (maxp + 15) & ~uint64_t(15))) return rc;
-    uint8_t* d_res = nullptr;
-    std::vector<uint64_t> res_base;
-    uint64_t nstr = 0;
-    if (results) {
-        res_base.resize(b.size());
-        for (size_t i = 0; i + 1 < b.size(); ++i) {
-            res_base[i] = nstr;
-            nstr += count_strings(text, b[i], b[i + 1], delimiter, stride);
-        }
-        RXG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_res), std::max<uint64_t>(nstr, 1) + 1, h->stream));
-    }
-    // Pageable input (the C++ facade's std::string, a numpy array): a driver
-    // copy from pageable memory stages through one CPU thread (~11 GB/s
-    // measured); instead a few host threads fill pinned pieces while the
-    // previous piece crosses PCIe and is matched.
+    // Pageable input (the C++ facade's std::string, a numpy array, a mapped
+    // file): a driver copy from pageable memory stages through one CPU thread
+    // (~11 GB/s measured); instead a few host threads fill pinned pieces while
+    // the previous piece crosses PCIe and is matched.
     cudaPointerAttributes pa{};
     const bool pageable = len >= (4u << 20) &&
                           (cudaPointerGetAttributes(&pa, text) != cudaSuccess || pa.type == cudaMemoryTypeUnregistered);
@@ -1359,14 +1346,21 @@ int host_batch(rxg_heap* h, const uint8_t* text, uint64_t len, int32_t delimiter
         for (auto*& p : h->h_pin) RXG_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&p), maxp, cudaHostAllocDefault));
         h->pin_bytes = maxp;
     }
-    if (pageable && !h->copier) {
+    // Per-string results: piece k's strings are counted on the host threads
+    // (fused into the pageable copy, else a count-only pass) to place them,
+    // matched into a device slot, and brought back through a pinned slot; the
+    // host copies them out two pieces later, so the pipeline never waits on a
+    // download into pageable memory.
+    const bool pool_count = results && delimiter >= 0 && len >= (1u << 20);
+    if ((pageable || pool_count) && !h->copier) {
         const unsigned hc = std::thread::hardware_concurrency();
         h->copier = std::make_unique<HostCopyPool>(std::min(8u, std::max(2u, hc / 2)));
     }
-    cudaEvent_t copied[2], consumed[2];
+    cudaEvent_t copied[2], consumed[2], landed[2];
     for (int i = 0; i < 2; ++i) {
         cudaEventCreateWithFlags(&copied[i], cudaEventDisableTiming);
         cudaEventCreateWithFlags(&consumed[i], cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&landed[i], cudaEventDisableTiming);
     }
     RXG_CUDA(write_u64(h->d_count, 0, h->stream));
     unsigned long long* d_bad = nullptr;
@@ -1376,21 +1370,54 @@ int host_batch(rxg_heap* h, const uint8_t* text, uint64_t len, int32_t delimiter
     }
     int rc = RXG_OK;
     int launches = 1;
+    uint64_t res_at = 0;                 // strings before the current piece
+    uint64_t slot_at[2] = {0, 0}, slot_n[2] = {0, 0};
+    bool slot_busy[2] = {false, false};
+    auto deliver = [&](int k) {          // piece results in pinned slot k -> caller's buffer
+        if (!slot_busy[k]) return;
+        cudaEventSynchronize(landed[k]);
+        std::memcpy(results + slot_at[k], h->h_rres[k], slot_n[k]);
+        slot_busy[k] = false;
+    };
     for (size_t i = 0; i + 1 < b.size() && rc == RXG_OK; ++i) {
         const int k = static_cast<int>(i & 1);
         const uint64_t n = b[i + 1] - b[i];
         if (i >= 2) cudaStreamWaitEvent(h->copy_stream, consumed[k], 0);
+        uint64_t delims = 0;
+        const int cdel = results && delimiter >= 0 ? delimiter : -1;
         if (pageable) {   // pinned piece k is free once its previous H2D copy (piece i - 2) has landed
             if (i >= 2) cudaEventSynchronize(copied[k]);
-            h->copier->copy(h->h_pin[k], text + b[i], n);
+            delims = h->copier->copy(h->h_pin[k], text + b[i], n, cdel);
             cudaMemcpyAsync(h->d_stage[k], h->h_pin[k], n, cudaMemcpyHostToDevice, h->copy_stream);
         } else {
             cudaMemcpyAsync(h->d_stage[k], text + b[i], n, cudaMemcpyHostToDevice, h->copy_stream);
+            if (cdel >= 0)
+                delims = pool_count ? h->copier->copy(nullptr, text + b[i], n, cdel)
+                                    : count_byte(text + b[i], n, static_cast<uint8_t>(cdel));
         }
         cudaEventRecord(copied[k], h->copy_stream);
         cudaStreamWaitEvent(h->stream, copied[k], 0);
+        uint64_t nres = 0;
+        if (results) {
+            nres = delimiter < 0 ? n / stride : delims + (n && text[b[i + 1] - 1] != static_cast<uint8_t>(delimiter));
+            deliver(k);                  // slot k's previous piece (i - 2) is out before it is reused
+            if (nres > h->rres_bytes[k]) {
+                const size_t want = std::max<size_t>(nres + nres / 4, 1u << 16);
+                if (h->d_rres[k]) cudaFree(h->d_rres[k]);
+                if (h->h_rres[k]) cudaFreeHost(h->h_rres[k]);
+                h->d_rres[k] = h->h_rres[k] = nullptr;
+                h->rres_bytes[k] = 0;
+                cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&h->d_rres[k]), want);
+                if (e == cudaSuccess) e = cudaHostAlloc(reinterpret_cast<void**>(&h->h_rres[k]), want, cudaHostAllocDefault);
+                if (e != cudaSuccess) {
+                    rc = cuda_fail(e, "results slots");
+                    break;
+                }
+                h->rres_bytes[k] = want;
+            }
+        }
         rc = batch_any(h, h->d_stage[k], n, delimiter, stride, RXG_BATCH_AUTO, h->d_count,
-                       results ? d_res + res_base[i] : nullptr, h->stream, false);
+                       results ? h->d_rres[k] : nullptr, h->stream, false);
         launches += g_launches;
         if (rc == RXG_OK && d_bad) {   // strings never straddle pieces, so per-piece checks are exact
             const cudaError_t e = launch_utf8_check(h->d_stage[k], n, delimiter, delimiter < 0 ? stride : 0, b[i], d_bad,
@@ -1399,24 +1426,35 @@ int host_batch(rxg_heap* h, const uint8_t* text, uint64_t len, int32_t delimiter
             launches += n ? 1 : 0;
         }
         cudaEventRecord(consumed[k], h->stream);
+        if (rc == RXG_OK && results && nres) {
+            cudaMemcpyAsync(h->h_rres[k], h->d_rres[k], nres, cudaMemcpyDeviceToHost, h->stream);
+            cudaEventRecord(landed[k], h->stream);
+            slot_at[k] = res_at;
+            slot_n[k] = nres;
+            slot_busy[k] = true;
+        }
+        res_at += nres;
     }
     if (rc == RXG_OK) {
         unsigned long long c = 0;
         cudaMemcpyAsync(&c, h->d_count, sizeof(c), cudaMemcpyDeviceToHost, h->stream);
-        if (results && nstr) cudaMemcpyAsync(results, d_res, nstr, cudaMemcpyDeviceToHost, h->stream);
         unsigned long long bad = ~0ull;
         if (d_bad) cudaMemcpyAsync(&bad, d_bad, sizeof(bad), cudaMemcpyDeviceToHost, h->stream);
         const cudaError_t e = cudaStreamSynchronize(h->stream);
         if (e != cudaSuccess) rc = cuda_fail(e, "match_batch_host");
+        if (rc == RXG_OK) {
+            deliver(0);
+            deliver(1);
+        }
         if (count) *count = c;
         if (utf8_first_bad) *utf8_first_bad = bad;
     }
-    if (d_res) cudaFreeAsync(d_res, h->stream);
     if (d_bad) cudaFreeAsync(d_bad, h->stream);
     cudaStreamSynchronize(h->stream);
     for (int i = 0; i < 2; ++i) {
         cudaEventDestroy(copied[i]);
         cudaEventDestroy(consumed[i]);
+        cudaEventDestroy(landed[i]);
     }
     g_launches = launches;
     return rc;

@@ -5,6 +5,7 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <condition_variable>
 #include <cstdint>
 #include <cstring>
@@ -48,8 +49,33 @@ struct TableSlot {
 
 constexpr int32_t kMaxDfaStates = 16384;
 
+// Occurrences of byte d in p[0, n): eight bytes per step, exact (a byte of
+// x ^ d is zero iff bit 7 of ((y & 0x7f) + 0x7f) | y is clear).
+inline uint64_t count_byte(const uint8_t* p, size_t n, uint8_t d) {
+    constexpr uint64_t lo7 = 0x7f7f7f7f7f7f7f7full, ones = 0x0101010101010101ull;
+    const uint64_t pat = ones * d;
+    uint64_t total = 0;
+    size_t i = 0;
+    while (i + 8 <= n) {
+        uint64_t acc = 0;   // per-byte hit counts, at most 255 steps before they are summed
+        const size_t stop = std::min(n & ~size_t(7), i + 8 * 255);
+        for (; i < stop; i += 8) {
+            uint64_t x;
+            std::memcpy(&x, p + i, 8);
+            x ^= pat;
+            acc += (~(((x & lo7) + lo7) | x) >> 7) & ones;
+        }
+        acc = (acc & 0x00ff00ff00ff00ffull) + ((acc >> 8) & 0x00ff00ff00ff00ffull);
+        total += (acc * 0x0001000100010001ull) >> 48;
+    }
+    for (; i < n; ++i) total += p[i] == d;
+    return total;
+}
+
 // A few host threads that copy one buffer in parallel (pageable input into
-// pinned staging: one thread's memcpy runs far below the PCIe link).
+// pinned staging: one thread's memcpy runs far below the PCIe link), counting
+// a delimiter byte on the way (the per-string results' offsets) while the
+// bytes are in cache; with dst null they only count.
 class HostCopyPool {
 public:
     explicit HostCopyPool(unsigned n) : n_(n ? n : 1) {
@@ -63,15 +89,19 @@ public:
         go_.notify_all();
         for (auto& t : threads_) t.join();
     }
-    void copy(void* dst, const void* src, size_t n) {
+    // Returns the number of `delim` bytes in src[0, n) (0 when delim < 0).
+    uint64_t copy(void* dst, const void* src, size_t n, int delim = -1) {
         std::unique_lock<std::mutex> lk(mu_);
         dst_ = static_cast<uint8_t*>(dst);
         src_ = static_cast<const uint8_t*>(src);
         len_ = n;
+        delim_ = delim;
+        hits_ = 0;
         pending_ = n_;
         ++gen_;
         go_.notify_all();
         done_.wait(lk, [&] { return pending_ == 0; });
+        return hits_;
     }
 
 private:
@@ -81,6 +111,7 @@ private:
             uint8_t* d;
             const uint8_t* s;
             size_t n;
+            int delim;
             {
                 std::unique_lock<std::mutex> lk(mu_);
                 go_.wait(lk, [&] { return quit_ || gen_ != seen; });
@@ -89,11 +120,19 @@ private:
                 d = dst_;
                 s = src_;
                 n = len_;
+                delim = delim_;
             }
             const size_t part = (n / n_ + 4095) & ~size_t(4095);
             const size_t lo = std::min(n, part * k), hi = std::min(n, lo + part);
-            if (hi > lo) std::memcpy(d + lo, s + lo, hi - lo);
+            uint64_t hits = 0;
+            constexpr size_t kSub = 256u << 10;   // copy, then count from cache
+            for (size_t at = lo; at < hi; at += kSub) {
+                const size_t m = std::min(kSub, hi - at);
+                if (d) std::memcpy(d + at, s + at, m);
+                if (delim >= 0) hits += count_byte((d ? d : s) + at, m, static_cast<uint8_t>(delim));
+            }
             std::lock_guard<std::mutex> lk(mu_);
+            hits_ += hits;
             if (--pending_ == 0) done_.notify_all();
         }
     }
@@ -107,6 +146,8 @@ private:
     uint8_t* dst_ = nullptr;
     const uint8_t* src_ = nullptr;
     size_t len_ = 0;
+    int delim_ = -1;
+    uint64_t hits_ = 0;
 };
 
 }  // namespace rxg
@@ -134,6 +175,11 @@ struct rxg_heap {
     uint8_t* h_pin[2] = {nullptr, nullptr};
     size_t pin_bytes = 0;
     std::unique_ptr<rxg::HostCopyPool> copier;
+    // per-string results of host-buffer calls: a device and a pinned slot per
+    // pipeline stage (piece k's results cross while piece k+1 is matched)
+    uint8_t* d_rres[2] = {nullptr, nullptr};
+    uint8_t* h_rres[2] = {nullptr, nullptr};
+    size_t rres_bytes[2] = {0, 0};   // grow-only, sized by the strings a piece holds
     unsigned long long* d_count = nullptr;
     int32_t* d_accept = nullptr;
     cudaStream_t stream = nullptr;

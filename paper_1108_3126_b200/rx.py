@@ -399,7 +399,9 @@ def count_strings(text, delimiter: int = 10, stride: int = 0) -> int:
     a = np.frombuffer(_b(text), np.uint8) if not isinstance(text, np.ndarray) else text
     if delimiter < 0:
         return len(a) // stride
-    n = int(np.count_nonzero(a == delimiter))
+    n = 0
+    for at in range(0, len(a), 1 << 18):   # in cache-sized pieces: no buffer-sized temporary
+        n += int(np.count_nonzero(a[at:at + (1 << 18)] == delimiter))
     if len(a) and a[-1] != delimiter:
         n += 1
     return n

@@ -79,3 +79,49 @@ def test_unicode_pattern():
     data = "é中\naé中\nb\n😀é\n".encode()
     r = run(["(a|é)*中"], data)
     assert r.returncode == 0 and r.stdout == "é中\naé中\n".encode()
+
+
+def run_file(args, data: bytes, tmp_path):
+    """stdin redirected from a regular file: the mapped-input path."""
+    f = tmp_path / "in.txt"
+    f.write_bytes(data)
+    with open(f, "rb") as fh:
+        return subprocess.run([str(CLI)] + args, stdin=fh, capture_output=True)
+
+
+@pytest.mark.gpu
+def test_file_stdin_matches_pipe_small(tmp_path):
+    data = b"aab\naa\nb\nab\r\n\nabbb\nab"
+    for pattern in ["a**b", "(a|b)*b", "()"]:
+        assert run_file([pattern], data, tmp_path).stdout == expected_lines(pattern, data)
+    r = run_file(["a*"], b"", tmp_path)   # empty file: no lines
+    assert r.returncode == 1 and r.stdout == b""
+
+
+@pytest.mark.gpu
+def test_large_input_split_across_host_threads(tmp_path):
+    # > 8 MiB: the line table and the output are built in pieces on several
+    # host threads; the output must be the in-order filter of every line
+    text = rx.synth_input("c", 24 << 20).tobytes()
+    pat = rx.synth_pattern("c")
+    lines = text.split(b"\n")
+    if text.endswith(b"\n"):
+        lines = lines[:-1]
+    _, res = rx.Matcher(pat).match_batch(text, results=True)   # per-line results (parity-tested elsewhere)
+    res = res[:len(lines)]
+    want = b"".join(l + b"\n" for l, a in zip(lines, res) if a)
+    piped = run([pat], text)
+    assert piped.returncode == 0 and piped.stdout == want
+    mapped = run_file([pat], text, tmp_path)
+    assert mapped.returncode == 0 and mapped.stdout == want
+    c = run_file(["--count", pat], text, tmp_path)
+    assert int(c.stdout) == want.count(b"\n")
+    # an invalid line deep in the input: everything before it, then the error
+    cut = text.index(b"\n", 20 << 20) + 1
+    bad = text[:cut] + b"xy\xc0z\n" + text[cut:]
+    r = run_file([pat], bad, tmp_path)
+    n_before = text[:cut].count(b"\n")
+    assert r.returncode == 2
+    assert r.stdout == b"".join(l + b"\n" for l, a in zip(lines[:n_before], res[:n_before]) if a)
+    _, _, first_bad = rx.Matcher(pat).match_batch_utf8(bad)
+    assert r.stderr == b"rxvm: invalid UTF-8 at byte %d\n" % (first_bad - cut)   # decode_utf8's offset in that line
