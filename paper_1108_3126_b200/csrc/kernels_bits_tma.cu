@@ -94,14 +94,14 @@ BitsTables make_bits_tables(const Program& p, int32_t delim) {
     auto rg = [&](int32_t g, int32_t w) { return g < t.G ? rows[static_cast<size_t>(g) * WT + w] : 0u; };
     std::vector<uint32_t>& img = t.img;
     if (WT <= 4) {
-        // per byte: [M, D (all ones on the delimiter), pad]; then T_g, R_g of the
+        // per byte: [M, D (2 on the delimiter, else 0), pad]; then T_g, R_g of the
         // groups >= 2 (broadcast rows); registers: SH, E0, T_0, R_0, T_1, R_1
         t.row_words = WT == 1 ? 2 : (WT + 1 + 3) / 4 * 4;
         img.assign(static_cast<size_t>(256) * t.row_words, 0u);
         for (int b = 0; b < 256; ++b) {
             uint32_t* r = &img[static_cast<size_t>(b) * t.row_words];
             for (int32_t w = 0; w < WT; ++w) r[w] = M[static_cast<size_t>(b) * WT + w];
-            r[WT] = b == delim ? ~0u : 0u;
+            r[WT] = b == delim ? 2u : 0u;
         }
         t.xg_off = static_cast<uint32_t>(img.size()) * 4;
         for (int32_t g = 2; g < t.G; ++g) {
@@ -122,7 +122,7 @@ BitsTables make_bits_tables(const Program& p, int32_t delim) {
         for (int b = 0; b < 256; ++b) {
             uint32_t* r = &img[static_cast<size_t>(b) * t.row_words];
             for (int32_t w = 0; w < WT; ++w) r[w] = M[static_cast<size_t>(b) * WT + w];
-            r[WT] = b == delim ? ~0u : 0u;
+            r[WT] = b == delim ? 2u : 0u;
         }
         t.xg_off = static_cast<uint32_t>(img.size()) * 4;
         img.insert(img.end(), SH.begin(), SH.end());
@@ -153,6 +153,7 @@ struct BArgs {
     uint32_t delim4;                  // delimiter in every byte
     int32_t n_groups;
     uint32_t two;         // the constant 2 (a register operand keeps IMAD on the FMA pipe)
+    uint32_t half;        // the constant 2^31 (D >> 1 as an IMAD.HI, not a shift on the ALU pipe)
     const uint4* img;
     uint32_t img_words;   // 16-byte units
     uint32_t tab;         // shared address of M
@@ -263,10 +264,21 @@ __device__ __forceinline__ void bstep_row(const BArgs& a, const Rows<WT, GR, REG
             acc0 |= E[w] & row[w] & R.tr[0][w];
             acc1 |= E[w] & row[w] & R.tr[1][w];
         }
+        if constexpr (WT == 1) {
+            // predicated ORs (2 ALU ops) instead of SEL, SEL, OR3 (3)
+            asm("{\n\t.reg .pred p0, p1;\n\t"
+                "setp.ne.u32 p0, %1, 0;\n\t"
+                "setp.ne.u32 p1, %2, 0;\n\t"
+                "@p0 or.b32 %0, %0, %3;\n\t"
+                "@p1 or.b32 %0, %0, %4;\n\t}"
+                : "+r"(nx[0])
+                : "r"(acc0), "r"(acc1), "r"(R.rr[0][0]), "r"(R.rr[1][0]));
+        } else {
 #pragma unroll
-        for (int w = 0; w < WT; ++w) {
-            if (acc0) nx[w] |= R.rr[0][w];
-            if (acc1) nx[w] |= R.rr[1][w];
+            for (int w = 0; w < WT; ++w) {
+                if (acc0) nx[w] |= R.rr[0][w];
+                if (acc1) nx[w] |= R.rr[1][w];
+            }
         }
         if constexpr (XG) {   // groups >= 2: T_g, R_g broadcast rows
             (void)row_addr;
@@ -282,11 +294,16 @@ __device__ __forceinline__ void bstep_row(const BArgs& a, const Rows<WT, GR, REG
             }
         }
     }
+    // String end, all on the FMA pipe: D is 2 on the delimiter (else 0) and
+    // the delimiter's M row is empty, so nx is empty there. Count A (bit 31 of
+    // the last word) as hi32(E * D), restart as E0 * (D / 2) + nx. Lanes
+    // past the last range hold E0 = 0 in R (they never count).
+    (void)cm;
     const uint32_t D = row[WT];
-    // string end: count A (bit 31 of the last word) on the FMA pipe, restart from E0
-    cnt += __umulhi(E[WT - 1] & D & cm, a.two);
+    asm("mad.hi.u32 %0, %1, %2, %0;" : "+r"(cnt) : "r"(E[WT - 1]), "r"(D));   // one IMAD.HI, no IADD3
+    const uint32_t d1 = __umulhi(D, a.half);
 #pragma unroll
-    for (int w = 0; w < WT; ++w) E[w] = (nx[w] & ~D) | (R.e0[w] & D);
+    for (int w = 0; w < WT; ++w) E[w] = R.e0[w] * d1 + nx[w];
     m = D;
 }
 
@@ -340,13 +357,14 @@ __device__ __forceinline__ void bstep(const BArgs& a, const Rows<WT, GR, REG>& R
                 }
             }
         }
-        cnt += __umulhi(E[WT - 1] & D & cm, a.two);
+        cnt += __umulhi(E[WT - 1] & cm, D);   // D: 2 on the delimiter, else 0
+        const uint32_t d1 = __umulhi(D, a.half);
 #pragma unroll
         for (int w4 = 0; w4 < WT / 4; ++w4) {
             uint32_t e0[4];
             R.get4(1, w4, e0);
 #pragma unroll
-            for (int j = 0; j < 4; ++j) E[w4 * 4 + j] = (nx[w4 * 4 + j] & ~D) | (e0[j] & D);
+            for (int j = 0; j < 4; ++j) E[w4 * 4 + j] = e0[j] * d1 + nx[w4 * 4 + j];   // nx is empty on the delimiter
         }
         m = D;
     }
@@ -537,12 +555,20 @@ __global__ void __launch_bounds__(C::warps * 32, 1) k_bits_tma(const __grid_cons
         bool valid[C::chains], own[C::chains];
         uint64_t li[C::chains];
         uint32_t cm[C::chains];   // all ones for valid ranges: only they count
+        // per chain: REG steps restart from Rc[j].e0, which is empty for lanes
+        // past the last range (they read zero fill and must never count)
+        Rows<WT, GR, REG> Rc[C::chains];
 #pragma unroll
         for (int j = 0; j < C::chains; ++j) {
             const uint64_t row = row0 + j * 32 + lane;
             valid[j] = row < a.rows;
             cm[j] = valid[j] ? ~0u : 0u;
             asm volatile("" : "+r"(cm[j]));   // keep the mask in a register (no per-byte recompute)
+            Rc[j] = R;
+            if constexpr (REG) {
+#pragma unroll
+                for (int w = 0; w < WT; ++w) Rc[j].e0[w] &= cm[j];
+            }
             // K2's ownership: the first range starts in the start state, every
             // other one in SKIP (the empty set) until its first line boundary
             own[j] = FIXED ? valid[j] : row == 0;
@@ -591,7 +617,7 @@ __global__ void __launch_bounds__(C::warps * 32, 1) k_bits_tma(const __grid_cons
                                 // the delimiter's table row (D = all ones) counts A and restarts E
                                 const uint32_t abit = RES ? E[j][WT - 1] >> 31 : 0u;
                                 uint32_t m;
-                                bstep<WT, GR, REG, XG>(a, R, E[j], row_of<WT>(a, x, k), cm[j], m, cnt);
+                                bstep<WT, GR, REG, XG>(a, Rc[j], E[j], row_of<WT>(a, x, k), cm[j], m, cnt);
                                 if (RES && m) {   // a line ended here: record it if owned
                                     if (own[j] && valid[j]) a.results[li[j]] = static_cast<uint8_t>(abit);
                                     ++li[j];
@@ -757,6 +783,7 @@ cudaError_t run(const BitsImage& b, const uint8_t* text, uint64_t len, int32_t d
     a.delim4 = FIXED ? 0u : static_cast<uint32_t>(delim) * 0x01010101u;
     a.n_groups = b.t.G;
     a.two = 2;
+    a.half = 0x80000000u;
     a.img = static_cast<const uint4*>(b.d_img);
     a.img_words = static_cast<uint32_t>(b.t.img.size() / 4);
     a.regs_g = b.d_regs;

@@ -1,0 +1,104 @@
+// Shared-memory bank model of the line kernel's table step (k_lines_tma,
+// class layouts) on a config's text: per warp-wide LDS, wavefronts = the most
+// distinct 4-byte words any one bank is asked for. Scores table layouts on the
+// host before they are built. Tool, not product.
+//
+//   bank_sim CONFIG [HOT...]   (CONFIG a-e; HOT: hot-row counts to model)
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <map>
+#include <numeric>
+#include <random>
+#include <set>
+#include <string>
+#include <vector>
+
+#include "frontend.hpp"
+#include "lines_tma.hpp"
+#include "program.hpp"
+#include "synth.hpp"
+
+using namespace rxg;
+
+int main(int argc, char** argv) {
+    const char cfg = argc > 1 ? argv[1][0] : 'd';
+    const std::string pat = synth_pattern(cfg);
+    Program p = build_program(compile(parse(pat)));
+    Dfa d;
+    if (!build_dfa(p, 16384, d)) return 1;
+    minimize_dfa(d);
+    const uint64_t n = 64ull << 20;
+    std::vector<uint8_t> text(n);
+    const uint64_t got = synth_input(cfg, 0, text.data(), n);
+    text.resize(got);
+    const std::vector<double> freq = lt_sample_freq(p, d, '\n', text.data(), std::min<uint64_t>(got, 1u << 20));
+    LtTable t = make_lines_tma_table(p, d, '\n', &freq);
+    std::printf("config %c: %d states, %d classes, cls %d range_k %u range_x %u row_bytes %u acc_shift %u\n", cfg,
+                d.n_states, d.n_classes, t.cls, t.range_k, t.range_x, t.row_bytes, t.acc_shift);
+    const uint32_t rows_addr = kLtSmemBase + 1024;
+    auto col_of = [&](uint8_t b) { return std::min<uint32_t>(b ^ t.range_x, t.range_k); };
+    // walk: warps of 32 lanes, lane l at range (w*32 + l) * chunk, SKIP entry
+    const uint32_t chunk = 7168, steps = 2048;
+    const uint32_t warps = static_cast<uint32_t>(std::min<uint64_t>(400, got / (32ull * chunk)));
+    std::vector<std::vector<uint32_t>> S(warps * 32), B(warps * 32);
+    std::map<uint32_t, uint64_t> visits;
+    for (uint32_t w = 0; w < warps; ++w)
+        for (uint32_t l = 0; l < 32; ++l) {
+            const uint64_t at = (static_cast<uint64_t>(w) * 32 + l) * chunk;
+            uint32_t s = at == 0 ? t.start : t.skip;
+            auto& sv = S[w * 32 + l];
+            auto& bv = B[w * 32 + l];
+            for (uint32_t k = 0; k < steps; ++k) {
+                const uint8_t b = text[at + k];
+                sv.push_back(s);
+                bv.push_back(b);
+                ++visits[s];
+                s = lt_step(t, s, b);
+            }
+        }
+    std::vector<std::pair<uint64_t, uint32_t>> hot;
+    for (auto& kv : visits) hot.push_back({kv.second, kv.first});
+    std::sort(hot.rbegin(), hot.rend());
+    const double total = static_cast<double>(warps) * 32 * steps;
+    double cum = 0;
+    std::printf("hottest rows (share, cumulative):");
+    for (size_t i = 0; i < std::min<size_t>(hot.size(), 40); ++i) {
+        cum += hot[i].first / total;
+        if (i < 8 || i % 8 == 7) std::printf(" %zu:%.3f", i + 1, cum);
+    }
+    std::printf("\n");
+    auto score = [&](auto word_of) {
+        double wf = 0;
+        for (uint32_t w = 0; w < warps; ++w)
+            for (uint32_t k = 0; k < steps; ++k) {
+                std::set<uint32_t> words[32];
+                for (uint32_t l = 0; l < 32; ++l) {
+                    const uint32_t wd = word_of(S[w * 32 + l][k], B[w * 32 + l][k], l);
+                    words[wd & 31].insert(wd);
+                }
+                size_t m = 0;
+                for (auto& x : words) m = std::max(m, x.size());
+                wf += static_cast<double>(m);
+            }
+        return wf / (static_cast<double>(warps) * steps);
+    };
+    std::printf("current layout: %.3f wavefronts / warp step\n",
+                score([&](uint32_t s, uint8_t b, uint32_t) { return (rows_addr + s * t.row_bytes + 2 * col_of(b)) >> 2; }));
+    for (int i = 2; i < argc; ++i) {
+        const size_t H = static_cast<size_t>(std::atoi(argv[i]));
+        std::map<uint32_t, uint32_t> hidx;
+        for (size_t j = 0; j < std::min(H, hot.size()); ++j) hidx[hot[j].second] = static_cast<uint32_t>(j);
+        const uint32_t hot_base = 0x20000;   // lane-replicated rows: word (h * cols + col) * 32 + lane
+        const uint32_t cw = (t.range_k + 2) / 2;
+        double share = 0;
+        for (size_t j = 0; j < std::min(H, hot.size()); ++j) share += hot[j].first / total;
+        std::printf("hot %3zu (%.3f of steps, %6.1f KB replicated): %.3f wavefronts\n", H, share,
+                    H * cw * 128 / 1024.0, score([&](uint32_t s, uint8_t b, uint32_t l) {
+                        auto it = hidx.find(s);
+                        if (it != hidx.end()) return hot_base + (it->second * cw + col_of(b) / 2) * 32 + l;
+                        return (rows_addr + s * t.row_bytes + 2 * col_of(b)) >> 2;
+                    }));
+    }
+    return 0;
+}
