@@ -59,6 +59,7 @@ struct Args {
     uint32_t stage_addr[kMaxSlots];
     uint32_t start, skip, void_row, tail_delta, term_acc;
     uint32_t delim;
+    uint32_t delim4, delim_hi4;                 // RES: the delimiter in every byte; its bit 7 in every byte
     uint32_t row_bytes, cmap_addr, acc_shift;   // class layouts
     uint32_t rows_addr, range_x, range_k;       // range-clamped columns
     uint32_t range_x4;                          // range_x in every byte (XOR a whole word)
@@ -417,6 +418,30 @@ __device__ void range_direct(const Args& a, uint64_t c0, uint64_t c1, uint64_t r
     if constexpr (RES) lc.close(a.rcount + range);
 }
 
+// RES: a stage column that holds several line ends, walked again from its
+// entry row in byte order. Returns the owned lines' results (x, in order from
+// bit 0), their number (y bits 0-7) and the ownership after the column (y bit
+// 8); in registers, so the caller's LineCursor stays out of local memory.
+template <class C, int L>
+__device__ __noinline__ uint2 res_rewalk(const Args& a, uint32_t s, uint32_t stage, uint32_t r, bool own, bool live) {
+    uint32_t bits = 0, n = 0;
+    for (int g = 0; g < C::slice / 16; ++g) {
+        const uint4 v = lds128(stage + r * C::slice + (granule<C::slice>(r, g) << 4));
+        for (int w = 0; w < 4; ++w) {
+            const uint32_t x = word_of(v, w);
+            for (int k = 0; k < 4; ++k) {
+                const uint32_t b = (x >> (8 * k)) & 0xFFu;
+                s = step_b<L>(a, s, b);
+                if (b == a.delim) {
+                    if (own) bits |= counted<L>(a, s) << n++;
+                    own = live;
+                }
+            }
+        }
+    }
+    return make_uint2(bits, n | (own ? 256u : 0u));
+}
+
 template <class C, int L, bool RES>
 __global__ void __launch_bounds__(C::warps * 32, 1) k_lines_tma(const __grid_constant__ Args a,
                                                              const __grid_constant__ CUtensorMap map) {
@@ -493,15 +518,24 @@ __global__ void __launch_bounds__(C::warps * 32, 1) k_lines_tma(const __grid_con
             lc[j] = cursor_of(a, RES && valid[j] ? row : 0, valid[j] && s[j] == a.start, valid[j]);
         }
         uint32_t last[C::chains] = {};
+        // RES: accepted line ends per chain; a 32-byte column holding one line
+        // end gives that line's result as the difference across the column
+        uint32_t cj[C::chains];
+#pragma unroll
+        for (int j = 0; j < C::chains; ++j) cj[j] = 0;
         for (uint32_t col = 0; col < ncol; ++col) {
             const uint32_t st = col % C::stages;
             mbar_wait(bar0 + st * 8, (phase >> st) & 1u);
             phase ^= 1u << st;
-            // RES: per chain, bit i of dl / cl = byte i of the current 32 bytes is a
-            // delimiter / ends an accepted line; lines are recorded once per 32 bytes.
-            uint32_t dl[C::chains], cl[C::chains];
+            // RES: per chain, the column's delimiters as one bit each (byte 4w+k of
+            // the column at bit 8k+w: the order does not matter, only the count)
+            uint32_t dl[C::chains], s_in[C::chains], c_in[C::chains];
 #pragma unroll
-            for (int j = 0; j < C::chains; ++j) dl[j] = cl[j] = 0;
+            for (int j = 0; j < C::chains; ++j) {
+                dl[j] = 0;
+                s_in[j] = s[j];
+                c_in[j] = cj[j];
+            }
 #pragma unroll
             for (int g = 0; g < C::slice / 16; ++g) {
                 uint4 v[C::chains];
@@ -515,42 +549,42 @@ __global__ void __launch_bounds__(C::warps * 32, 1) k_lines_tma(const __grid_con
                     uint32_t wx[C::chains];   // range layout: the word XORed once, not each byte
 #pragma unroll
                     for (int j = 0; j < C::chains; ++j) wx[j] = L == 2 ? word_of(v[j], w) ^ a.range_x4 : 0u;
-                    const int sh = 16 * (g & 1) + 4 * w;   // bit of byte 0 of this word
 #pragma unroll
                     for (int k = 0; k < 4; ++k)
 #pragma unroll
                         for (int j = 0; j < C::chains; ++j) {
                             s[j] = L == 2 ? step_rx(a, s[j], wx[j], k) : step<L, true>(a, s[j], word_of(v[j], w), k);
-                            const uint32_t c = counted<L>(a, s[j]);
-                            cnt += c;
-                            if constexpr (RES) cl[j] |= c << (sh + k);
+                            if constexpr (RES) cj[j] += counted<L>(a, s[j]);
+                            else cnt += counted<L>(a, s[j]);
                         }
                     if constexpr (RES) {
 #pragma unroll
                         for (int j = 0; j < C::chains; ++j) {
-                            // 0xFF per delimiter byte -> one bit per byte (the 4 bits sum without carries)
-                            const uint32_t m = __vcmpeq4(word_of(v[j], w), a.delim * 0x01010101u) & 0x08040201u;
-                            dl[j] |= ((m * 0x01010101u) >> 24) << sh;
-                        }
-                    }
-                }
-                if constexpr (RES) {
-                    if ((g & 1) || g + 1 == C::slice / 16) {
-#pragma unroll
-                        for (int j = 0; j < C::chains; ++j) {
-                            uint32_t dm = dl[j];
-                            while (dm) {   // the lines that ended in these 32 bytes, in byte order
-                                const uint32_t i = __ffs(dm) - 1;
-                                if (lc[j].own) lc[j].push((cl[j] >> i) & 1u);
-                                lc[j].own = lc[j].live;
-                                dm &= dm - 1;
-                            }
-                            dl[j] = cl[j] = 0;
+                            // bit 7 of each byte: byte == delimiter (exact, no borrow between bytes)
+                            const uint32_t x = word_of(v[j], w);
+                            const uint32_t y = ((x ^ a.delim4) & 0x7F7F7F7Fu) + 0x7F7F7F7Fu;
+                            const uint32_t z = ~(y | (x ^ a.delim_hi4)) & 0x80808080u;
+                            dl[j] += z >> (7 - (4 * (g & 1) + w));
                         }
                     }
                 }
 #pragma unroll
                 for (int j = 0; j < C::chains; ++j) last[j] = v[j].w >> 24;
+            }
+            if constexpr (RES) {
+                static_assert(C::slice == 32, "RES records one 32-byte column at a time");
+#pragma unroll
+                for (int j = 0; j < C::chains; ++j) {
+                    const uint32_t nd = __popc(dl[j]);
+                    if (nd == 1) {
+                        if (lc[j].own) lc[j].push(cj[j] - c_in[j]);
+                        lc[j].own = lc[j].live;
+                    } else if (nd > 1) {   // several line ends: walk the column again, in byte order
+                        const uint2 rw = res_rewalk<C, L>(a, s_in[j], stage[st], j * 32 + lane, lc[j].own, lc[j].live);
+                        for (uint32_t i = 0; i < (rw.y & 0xFFu); ++i) lc[j].push((rw.x >> i) & 1u);
+                        lc[j].own = (rw.y >> 8) & 1u;
+                    }
+                }
             }
             __syncwarp();
             if (lane == 0 && col + C::stages < ncol) {
@@ -558,6 +592,10 @@ __global__ void __launch_bounds__(C::warps * 32, 1) k_lines_tma(const __grid_con
                 tma_issue<C::stage_bytes>(&map, stage[st], bar0 + st * 8, static_cast<int32_t>((col + C::stages) * C::slice),
                                           static_cast<int32_t>(row0));
             }
+        }
+        if constexpr (RES) {
+#pragma unroll
+            for (int j = 0; j < C::chains; ++j) cnt += cj[j];
         }
         {
             bool live[C::chains];
@@ -625,20 +663,33 @@ CUtensorMapSwizzle swizzle_of(int slice) {
 }
 
 // Per-line results (RES), second pass: range r's owned lines start at
-// line base[r] (exclusive scan of the counts); one warp per range writes
-// them from its result bits, coalesced.
+// line base[r] (exclusive scan of the counts). A warp takes 32 ranges: lane
+// j loads range j's count, base and first two result words (coalesced, all
+// independent), then the warp writes each range's bytes in turn, 32
+// consecutive bytes per store.
 __global__ void __launch_bounds__(256) k_lt_scatter(const uint32_t* __restrict__ rbits, uint32_t rwords,
                                                     const unsigned long long* __restrict__ count,
                                                     const unsigned long long* __restrict__ base, uint64_t nranges,
                                                     uint8_t* __restrict__ results) {
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t nwarps = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5);
-    for (uint64_t r = static_cast<uint64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); r < nranges;
-         r += nwarps) {
-        const uint32_t n = static_cast<uint32_t>(count[r]);
-        const uint64_t b = base[r];
+    for (uint64_t r0 = (static_cast<uint64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; r0 < nranges;
+         r0 += nwarps * 32) {
+        const uint64_t r = r0 + lane;
+        const bool in = r < nranges;
+        const uint32_t n = in ? static_cast<uint32_t>(count[r]) : 0u;
+        const uint64_t b = in ? base[r] : 0;
         const uint32_t* bits = rbits + r * rwords;
-        for (uint32_t i = lane; i < n; i += 32) results[b + i] = static_cast<uint8_t>((__ldg(bits + (i >> 5)) >> (i & 31)) & 1u);
+        const uint32_t w0 = n ? __ldg(bits) : 0u, w1 = n > 32 ? __ldg(bits + 1) : 0u;
+        for (int j = 0; j < 32; ++j) {
+            const uint32_t nj = __shfl_sync(0xFFFFFFFFu, n, j);
+            const uint64_t bj = __shfl_sync(0xFFFFFFFFu, b, j);
+            const uint32_t x0 = __shfl_sync(0xFFFFFFFFu, w0, j), x1 = __shfl_sync(0xFFFFFFFFu, w1, j);
+            for (uint32_t i = lane; i < nj; i += 32) {
+                const uint32_t w = i < 32 ? x0 : i < 64 ? x1 : __ldg(rbits + (r0 + j) * rwords + (i >> 5));
+                results[bj + i] = static_cast<uint8_t>((w >> (i & 31)) & 1u);
+            }
+        }
     }
 }
 
@@ -746,6 +797,8 @@ cudaError_t launch(const LtTable& t, const uint8_t* text, uint64_t len, uint8_t 
     a.tail_delta = t.tail_delta;
     a.term_acc = t.term_acc;
     a.delim = delim;
+    a.delim4 = delim * 0x01010101u;
+    a.delim_hi4 = a.delim4 & 0x80808080u;
     a.row_bytes = t.row_bytes;
     a.cmap_addr = t.cmap_addr;
     a.acc_shift = t.acc_shift;
@@ -793,7 +846,7 @@ cudaError_t launch(const LtTable& t, const uint8_t* text, uint64_t len, uint8_t 
     size_t temp_bytes = res_temp_bytes(nr);
     e = cub::DeviceScan::ExclusiveSum(temp, temp_bytes, a.rcount, base, static_cast<int64_t>(nr), st);
     if (e != cudaSuccess) return e;
-    const uint64_t want2 = (nr + 7) / 8, cap2 = static_cast<uint64_t>(device_sm_count(dev)) * 16;
+    const uint64_t want2 = (nr + 255) / 256, cap2 = static_cast<uint64_t>(device_sm_count(dev)) * 8;
     k_lt_scatter<<<static_cast<unsigned>(want2 < cap2 ? want2 : cap2), 256, 0, st>>>(a.rbits, a.rwords, a.rcount, base, nr,
                                                                                    results);
     return cudaGetLastError();
