@@ -663,31 +663,44 @@ CUtensorMapSwizzle swizzle_of(int slice) {
 }
 
 // Per-line results (RES), second pass: range r's owned lines start at
-// line base[r] (exclusive scan of the counts). A warp takes 32 ranges: lane
-// j loads range j's count, base and first two result words (coalesced, all
-// independent), then the warp writes each range's bytes in turn, 32
-// consecutive bytes per store.
+// line base[r] (exclusive scan of the counts). A warp takes units of 16
+// ranges: lane j loads range j's count, base and first two result words
+// (coalesced, independent), then the warp writes each range's bytes in turn,
+// up to 32 consecutive bytes per store. The grid is one wave of warps that
+// stride over the units (small units: no half-empty second wave). (A
+// decoupled look-back scan fused in here measured slower: ~9.5k warps start
+// together, so most look back hundreds of units before an inclusive prefix.)
+constexpr uint32_t kScatterUnit = 16;
+
 __global__ void __launch_bounds__(256) k_lt_scatter(const uint32_t* __restrict__ rbits, uint32_t rwords,
                                                     const unsigned long long* __restrict__ count,
                                                     const unsigned long long* __restrict__ base, uint64_t nranges,
                                                     uint8_t* __restrict__ results) {
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t nwarps = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5);
-    for (uint64_t r0 = (static_cast<uint64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; r0 < nranges;
-         r0 += nwarps * 32) {
+    for (uint64_t r0 = (static_cast<uint64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5)) * kScatterUnit;
+         r0 < nranges; r0 += nwarps * kScatterUnit) {
         const uint64_t r = r0 + lane;
-        const bool in = r < nranges;
+        const bool in = lane < kScatterUnit && r < nranges;
         const uint32_t n = in ? static_cast<uint32_t>(count[r]) : 0u;
-        const uint64_t b = in ? base[r] : 0;
+        const uint64_t b0 = base[r0];
+        const uint32_t rel = in ? static_cast<uint32_t>(base[r] - b0) : 0u;   // a unit's lines are < 2^32
         const uint32_t* bits = rbits + r * rwords;
         const uint32_t w0 = n ? __ldg(bits) : 0u, w1 = n > 32 ? __ldg(bits + 1) : 0u;
-        for (int j = 0; j < 32; ++j) {
+        uint8_t* out = results + b0;
+#pragma unroll 4
+        for (uint32_t j = 0; j < kScatterUnit; ++j) {
             const uint32_t nj = __shfl_sync(0xFFFFFFFFu, n, j);
-            const uint64_t bj = __shfl_sync(0xFFFFFFFFu, b, j);
-            const uint32_t x0 = __shfl_sync(0xFFFFFFFFu, w0, j), x1 = __shfl_sync(0xFFFFFFFFu, w1, j);
-            for (uint32_t i = lane; i < nj; i += 32) {
-                const uint32_t w = i < 32 ? x0 : i < 64 ? x1 : __ldg(rbits + (r0 + j) * rwords + (i >> 5));
-                results[bj + i] = static_cast<uint8_t>((w >> (i & 31)) & 1u);
+            if (nj == 0) continue;
+            const uint32_t bj = __shfl_sync(0xFFFFFFFFu, rel, j);
+            const uint32_t x0 = __shfl_sync(0xFFFFFFFFu, w0, j);
+            if (lane < nj) out[bj + lane] = static_cast<uint8_t>((x0 >> lane) & 1u);
+            if (nj > 32) {   // long lines are rare: the rest of the range
+                const uint32_t x1 = __shfl_sync(0xFFFFFFFFu, w1, j);
+                for (uint32_t i = 32 + lane; i < nj; i += 32) {
+                    const uint32_t w = i < 64 ? x1 : __ldg(rbits + (r0 + j) * rwords + (i >> 5));
+                    out[bj + i] = static_cast<uint8_t>((w >> (i & 31)) & 1u);
+                }
             }
         }
     }
@@ -846,7 +859,7 @@ cudaError_t launch(const LtTable& t, const uint8_t* text, uint64_t len, uint8_t 
     size_t temp_bytes = res_temp_bytes(nr);
     e = cub::DeviceScan::ExclusiveSum(temp, temp_bytes, a.rcount, base, static_cast<int64_t>(nr), st);
     if (e != cudaSuccess) return e;
-    const uint64_t want2 = (nr + 255) / 256, cap2 = static_cast<uint64_t>(device_sm_count(dev)) * 8;
+    const uint64_t want2 = (nr + 8 * kScatterUnit - 1) / (8 * kScatterUnit), cap2 = static_cast<uint64_t>(device_sm_count(dev)) * 8;
     k_lt_scatter<<<static_cast<unsigned>(want2 < cap2 ? want2 : cap2), 256, 0, st>>>(a.rbits, a.rwords, a.rcount, base, nr,
                                                                                    results);
     return cudaGetLastError();
