@@ -119,6 +119,7 @@ struct Args {
     unsigned int* seam;    // cooperative launch: tiles + 1 arrival counters (zero when idle; see seam_arrive)
     uint32_t entry;        // table state the string starts in (the start state unless chained)
     uint32_t* exit_state;  // nullable: table state after the string
+    uint32_t fn_states;    // packed layout: > 0 = transfer-function mode with this many states (LtTable::fn_states)
 };
 
 // Packed layout (L == 3): the table word of byte b holds next*5 at bit
@@ -366,6 +367,141 @@ __device__ __forceinline__ void seam_arrive(const Args& a, uint64_t t, uint64_t 
         atomicMax(a.bad_inv, ~static_cast<unsigned long long>(j));
 }
 
+// Transfer-function mode (packed tables, LtTable::fn_states): every lane
+// walks its ranges from all S states at once on the TMA ring (S funnel shifts
+// per byte instead of one, no entry guess) and stores each range's function
+// in g[range]; fn_finish composes them in range order.
+template <class C, int S>
+__device__ void fn_tiles(const Args& a, const CUtensorMap* map, uint32_t warp, uint32_t lane, uint32_t bar0,
+                         uint32_t tbar) {
+    uint32_t phase = 0;
+    const uint32_t ncol = a.chunk / C::slice;
+    const uint32_t* stage = a.stage_addr + warp * C::stages;
+    const uint32_t lb = lane_base();
+    for (uint64_t tile = static_cast<uint64_t>(warp) * gridDim.x + blockIdx.x; tile < a.tiles;
+         tile += static_cast<uint64_t>(gridDim.x) * C::warps) {
+        const uint64_t row0 = tile * C::rows;
+        if (lane == 0) {
+            const uint32_t pro = ncol < C::stages ? ncol : C::stages;
+            for (uint32_t st = 0; st < pro; ++st)
+                tma::issue<C::stage_bytes>(map, stage[st], bar0 + st * 8, static_cast<int32_t>(st * C::slice),
+                                           static_cast<int32_t>(row0));
+        }
+        tma::mbar_wait(tbar, 0);
+        uint32_t f[C::chains][S];
+#pragma unroll
+        for (int j = 0; j < C::chains; ++j)
+#pragma unroll
+            for (int i = 0; i < S; ++i) f[j][i] = 5u * i;
+        for (uint32_t col = 0; col < ncol; ++col) {
+            const uint32_t st = col % C::stages;
+            tma::mbar_wait(bar0 + st * 8, (phase >> st) & 1u);
+            phase ^= 1u << st;
+#pragma unroll
+            for (int g = 0; g < static_cast<int>(C::slice / 16); ++g) {
+                uint4 v[C::chains];
+#pragma unroll
+                for (int j = 0; j < C::chains; ++j) {
+                    const uint32_t r = j * 32 + lane;
+                    v[j] = tma::lds128(stage[st] + r * C::slice + (tma::granule<C::slice>(r, g) << 4));
+                }
+#pragma unroll
+                for (int w = 0; w < 4; ++w)
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+#pragma unroll
+                        for (int j = 0; j < C::chains; ++j) {
+                            const uint32_t t = tma::lds32(__dp4a(tma::word_of(v[j], w), 128u << (8 * k), lb));
+#pragma unroll
+                            for (int i = 0; i < S; ++i) f[j][i] = shr_wrap(t, f[j][i]);
+                        }
+            }
+            __syncwarp();
+            if (lane == 0 && col + C::stages < ncol) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                tma::issue<C::stage_bytes>(map, stage[st], bar0 + st * 8, static_cast<int32_t>((col + C::stages) * C::slice),
+                                           static_cast<int32_t>(row0));
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < C::chains; ++j) {
+            const uint64_t row = row0 + j * 32 + lane;
+            if (row >= a.rows) continue;
+            uint32_t fn = kFnIdentity;   // states >= S keep identity fields (never reached)
+#pragma unroll
+            for (int i = 0; i < S; ++i) fn = (fn & ~(31u << (5 * i))) | ((f[j][i] & 31u) << (5 * i));
+            a.g[row] = fn;
+        }
+    }
+}
+
+template <class C, bool COOP>
+__device__ void fn_mode(const Args& a, const CUtensorMap* map, uint8_t* sm, uint32_t warp, uint32_t lane, uint32_t bar0,
+                        uint32_t tbar) {
+    if (blockIdx.x == 0 && threadIdx.x == 0 && a.nranges > a.rows) {   // the remainder range, direct loads
+        tma::mbar_wait(tbar, 0);
+        a.g[a.rows] = walk_fn(a, a.rows * a.chunk, a.len);
+    }
+    switch (a.fn_states) {
+    case 1: fn_tiles<C, 1>(a, map, warp, lane, bar0, tbar); break;
+    case 2: fn_tiles<C, 2>(a, map, warp, lane, bar0, tbar); break;
+    case 3: fn_tiles<C, 3>(a, map, warp, lane, bar0, tbar); break;
+    case 4: fn_tiles<C, 4>(a, map, warp, lane, bar0, tbar); break;
+    case 5: fn_tiles<C, 5>(a, map, warp, lane, bar0, tbar); break;
+    default: fn_tiles<C, 6>(a, map, warp, lane, bar0, tbar); break;
+    }
+    tma::mbar_wait(tbar, 0);   // no CTA leaves with its table copy in flight
+    auto answer = [&](uint32_t x) {
+        *a.accept = static_cast<int32_t>((a.acc_mask >> (x / 5u)) & 1u);
+        if (a.repairs) *a.repairs = 0;
+        if (a.exit_state) *a.exit_state = x;
+    };
+    if constexpr (!COOP) {
+        // small inputs: the last CTA to finish composes the functions in order
+        uint32_t* last = reinterpret_cast<uint32_t*>(sm + (a.bar_addr + C::warps * C::stages * 8 - kLtSmemBase));
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) *last = atomicAdd(a.ticket, 1u) == gridDim.x - 1;
+        __syncthreads();
+        if (!*last || threadIdx.x != 0) return;
+        __threadfence();
+        uint32_t x = a.entry;
+        for (uint64_t j = 0; j < a.nranges; ++j) x = shr_wrap(*reinterpret_cast<volatile uint32_t*>(a.g + j), x) & 31u;
+        answer(x);
+        *a.ticket = 0;
+        return;
+    } else {
+        cg::grid_group grid = cg::this_grid();
+        grid.sync();
+        // threads own contiguous runs; warp, block, grid reductions keep the order;
+        // block composites go to mid[] (g holds the range functions still being read)
+        const uint64_t nthreads = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+        const uint64_t gtid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+        const uint64_t per_t = (a.nranges + nthreads - 1) / nthreads;
+        uint32_t f = kFnIdentity;
+        for (uint64_t j = gtid * per_t; j < min((gtid + 1) * per_t, a.nranges); ++j) f = fn_then(f, a.g[j]);
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const uint32_t g = __shfl_down_sync(0xFFFFFFFFu, f, off);
+            if (lane + off < 32) f = fn_then(f, g);
+        }
+        uint32_t* wf = reinterpret_cast<uint32_t*>(sm + (a.bar_addr + C::warps * C::stages * 8 + 16 - kLtSmemBase));
+        if (lane == 0) wf[warp] = f;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint32_t b = kFnIdentity;
+            for (uint32_t w = 0; w < C::warps; ++w) b = fn_then(b, wf[w]);
+            a.mid[blockIdx.x] = b;
+        }
+        grid.sync();
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            uint32_t x = a.entry;
+            for (uint32_t b = 0; b < gridDim.x; ++b) x = shr_wrap(a.mid[b], x) & 31u;
+            answer(x);
+        }
+    }
+}
+
 template <class C, int L, bool COOP>
 __global__ void __launch_bounds__(C::warps * 32, 1) k_chunk_tma(const __grid_constant__ Args a,
                                                            const __grid_constant__ CUtensorMap map) {
@@ -384,6 +520,12 @@ __global__ void __launch_bounds__(C::warps * 32, 1) k_chunk_tma(const __grid_con
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
+    if constexpr (L == 3) {
+        if (a.fn_states) {
+            fn_mode<C, COOP>(a, &map, sm, warp, lane, bar0, tbar);
+            return;
+        }
+    }
     // the table copy is waited for where it is first used: after each warp has
     // issued its first ring stages, so the two transfers overlap
     const uint32_t per = (a.chunk + kMidT - 1) / kMidT;   // checkpoints per range (the last may be partial)
@@ -714,6 +856,7 @@ cudaError_t launch_chunked_tma(const LtTable& t, const void* d_img, const uint8_
     a.range_x = t.range_x;
     a.range_k = t.range_k;
     a.acc_mask = t.acc_mask;
+    a.fn_states = t.packed ? t.fn_states : 0u;
     if (t.packed)
         return with_shape(t, chunk, [&](auto c) {
             using C = decltype(c);

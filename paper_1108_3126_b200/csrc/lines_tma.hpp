@@ -36,6 +36,11 @@ struct LtTable {
     // (word for byte b, lane l at 0x400 + 128 b + 4 l); states are 5*state, acc_mask bit i = accept(i)
     bool packed = false;
     uint32_t acc_mask = 0;
+    // packed chunk tables: states of the automaton when a byte permutes two or
+    // more of them (input runs of it never synchronise a lookback guess, e.g.
+    // (aaa)* over a's): the engine then computes every range's transfer
+    // function directly instead of guessing entries first; 0 = guess
+    uint32_t fn_states = 0;
     std::vector<uint8_t> lo, hi;     // images of [lo_addr, +lo) main rows and [hi_addr, +hi) upper rows
     uint32_t lo_addr = 0, hi_addr = 0;
     uint32_t lo_bytes = 0, hi_bytes = 0;

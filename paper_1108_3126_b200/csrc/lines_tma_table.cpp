@@ -533,6 +533,22 @@ LtTable make_chunk_tma_table(const Program& p, const Dfa& d, const std::vector<d
         }
         for (uint32_t s = 0; s < S; ++s) t.acc_mask |= static_cast<uint32_t>(d.accept[s] != 0) << s;
         t.start = 5u * static_cast<uint32_t>(d.start);
+        // a byte class whose step has a cycle of length >= 2 (a permutation of
+        // some states): runs of it keep every lookback guess ambiguous
+        bool cycles = false;
+        for (int32_t c = 0; c < d.n_classes && !cycles; ++c)
+            for (uint32_t s0 = 0; s0 < S && !cycles; ++s0) {
+                uint32_t x = s0;
+                for (uint32_t k = 1; k <= S; ++k) {
+                    x = next(x, static_cast<uint32_t>(c));
+                    if (x == s0) {
+                        cycles = k >= 2;
+                        break;
+                    }
+                }
+            }
+        if (const char* e = rxg::option("RXG_CHUNK_FN")) cycles = std::atoi(e) != 0;   // force on / off (tests, A/B)
+        t.fn_states = cycles ? S : 0u;
     } else if (S <= kLtChunkDirectMaxStates) {
         // direct: rows of 256 four-byte columns at chosen bank offsets
         // direct: rows of 256 four-byte columns at chosen bank offsets; a row's

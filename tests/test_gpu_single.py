@@ -310,3 +310,48 @@ def test_chunked_nonsynchronizing_by_transfer_functions(n):
     m.match_one_ex(d, acc, "chunked", nbytes=n)
     torch.cuda.synchronize()
     assert not bool(acc.item())
+
+
+@pytest.mark.parametrize("force", ["1", "0"])
+def test_chunked_transfer_function_mode(force):
+    """Packed tables: the transfer-function mode (every range walked from all
+    of its S states on the TMA ring, functions composed in range order) chosen
+    for automata with a permuting byte ((aaa)*), forced on here for patterns
+    of 1-6 states and forced off for (aaa)* (guess, then the fallback pass).
+    Small (last-CTA) and large (cooperative) launches, chained entry/exit
+    states; against the sequential walk and the oracle."""
+    rng = np.random.default_rng(31)
+    rx.set_option("RXG_CHUNK_FN", force)
+    try:
+        for p in ["(aaa)*", "(aa)*", "(a|b)*abb", "((a|b)(a|b))*", "(ab|ba)*a", "a*b*a*b*", "a*", "(a|b)*(aa|bb)"]:
+            m = rx.Matcher(p)
+            o = O(p)
+            for n in (0, 1, 100, 4097, 300_001, (5 << 20) + 3, (40 << 20) + 1):
+                w = (np.full(n, 97, np.uint8) if p in ("(aaa)*", "(aa)*", "a*")
+                     else rng.choice([97, 98], size=n).astype(np.uint8))
+                if n and p in ("(aaa)*", "(aa)*") and rng.integers(0, 2):
+                    w[int(rng.integers(0, n))] = 98
+                d = torch.zeros(n + 64, dtype=torch.uint8, device="cuda")
+                if n:
+                    d[:n].copy_(torch.from_numpy(w))
+                acc = torch.zeros(1, dtype=torch.int32, device="cuda")
+                ref = torch.zeros(1, dtype=torch.int32, device="cuda")
+                m.match_one_ex(d, acc, "chunked", nbytes=n)
+                m.match_one_ex(d, ref, "dfa_seq", nbytes=n)
+                torch.cuda.synchronize()
+                assert bool(acc.item()) == bool(ref.item()), (p, n, force)
+                if n <= 300_001:
+                    assert bool(acc.item()) == o.accepts(w.tobytes()), (p, n, force)
+            # chained pieces: the exit state of one call is the entry of the next
+            w = np.full((3 << 20) + 2, 97, np.uint8) if p in ("(aaa)*", "(aa)*") else rng.choice([97, 98], size=(3 << 20) + 2).astype(np.uint8)
+            d = torch.from_numpy(w).cuda()
+            acc = torch.zeros(1, dtype=torch.int32, device="cuda")
+            ex = torch.zeros(1, dtype=torch.int32, device="cuda")
+            cut = len(w) // 3
+            m.match_one_ex(d[:cut], acc, "chunked", nbytes=cut, d_exit_state=ex)
+            torch.cuda.synchronize()
+            m.match_one_ex(d[cut:], acc, "chunked", nbytes=len(w) - cut, flags=1, entry_state=int(ex.item()))
+            torch.cuda.synchronize()
+            assert bool(acc.item()) == o.accepts(w.tobytes()), (p, "chained", force)
+    finally:
+        rx.set_option("RXG_CHUNK_FN", None)
