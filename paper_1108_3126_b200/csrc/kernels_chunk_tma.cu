@@ -520,12 +520,6 @@ __global__ void __launch_bounds__(C::warps * 32, 1) k_chunk_tma(const __grid_con
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    if constexpr (L == 3) {
-        if (a.fn_states) {
-            fn_mode<C, COOP>(a, &map, sm, warp, lane, bar0, tbar);
-            return;
-        }
-    }
     // the table copy is waited for where it is first used: after each warp has
     // issued its first ring stages, so the two transfers overlap
     const uint32_t per = (a.chunk + kMidT - 1) / kMidT;   // checkpoints per range (the last may be partial)
@@ -762,6 +756,29 @@ __global__ void __launch_bounds__(C::warps * 32, 1) k_chunk_tma(const __grid_con
 
 uint32_t align_up(uint32_t x, uint32_t a) { return (x + a - 1) / a * a; }
 
+// Transfer-function mode as its own kernel (packed tables with
+// LtTable::fn_states): the guessing kernel above keeps its registers.
+template <class C, bool COOP>
+__global__ void __launch_bounds__(C::warps * 32, 1) k_chunk_fn(const __grid_constant__ Args a,
+                                                          const __grid_constant__ CUtensorMap map) {
+    extern __shared__ __align__(1024) uint8_t sm[];
+    if (static_cast<uint32_t>(__cvta_generic_to_shared(sm)) != kLtSmemBase) __trap();
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t bar0 = a.bar_addr + warp * C::stages * 8;
+    const uint32_t tbar = a.bar_addr + C::warps * C::stages * 8 + 8;
+    if (threadIdx.x == 0) {
+        tma::mbar_init(tbar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        tma::bulk_load(kLtSmemBase, a.img, a.img_words * 16u, tbar);
+    }
+    if (lane == 0) {
+        for (int st = 0; st < C::stages; ++st) tma::mbar_init(bar0 + st * 8, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    fn_mode<C, COOP>(a, &map, sm, warp, lane, bar0, tbar);
+}
+
 template <class C, int L>
 cudaError_t run(const LtTable& t, Args& a, int device, cudaStream_t st) {
     // stage ring after the table image, mbarriers after the ring
@@ -777,6 +794,9 @@ cudaError_t run(const LtTable& t, Args& a, int device, cudaStream_t st) {
     // grid syncs cost more than the in-order repair can
     const bool coop = a.len >= (4ull << 20) && a.seam;
     auto* kern = coop ? k_chunk_tma<C, L, true> : k_chunk_tma<C, L, false>;
+    if constexpr (L == 3) {
+        if (a.fn_states) kern = coop ? k_chunk_fn<C, true> : k_chunk_fn<C, false>;
+    }
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     int sms = 148;
