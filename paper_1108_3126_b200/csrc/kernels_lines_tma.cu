@@ -71,8 +71,9 @@ struct Args {
     // per-line results (RES), in one pass: every range records the results of
     // the lines it owns as range-local bits plus its line count; a scan of
     // the counts and a scatter kernel place them (no delimiter pre-pass)
-    uint32_t* rbits;                            // rwords words per range
+    uint32_t* rbits;                            // rwords words per range, transposed: word k of range r at k * nranges + r
     uint32_t rwords;
+    uint64_t nranges;
     unsigned long long* rcount;                 // owned lines per range
 };
 
@@ -83,13 +84,15 @@ struct LineCursor {
     uint32_t lj;     // owned lines recorded so far
     uint32_t bits;   // the current word of results
     uint32_t* out;   // the range's next result word
+    uint64_t stride; // words between a range's consecutive result words (the range count)
     bool own;
     bool live;       // false for lanes past the last range (they read zero fill)
 
     __device__ __forceinline__ void push(uint32_t v) {
         bits |= v << (lj & 31);
         if ((++lj & 31) == 0) {
-            *out++ = bits;
+            *out = bits;
+            out += stride;
             bits = 0;
         }
     }
@@ -100,7 +103,7 @@ struct LineCursor {
 };
 
 __device__ __forceinline__ LineCursor cursor_of(const Args& a, uint64_t range, bool own, bool live) {
-    return LineCursor{0u, 0u, a.rbits ? a.rbits + range * a.rwords : nullptr, own, live};
+    return LineCursor{0u, 0u, a.rbits ? a.rbits + range : nullptr, a.nranges, own, live};
 }
 
 // Kernel shape: warps per CTA, ranges per lane, bytes per range per stage, ring depth.
@@ -685,8 +688,8 @@ __global__ void __launch_bounds__(256) k_lt_scatter(const uint32_t* __restrict__
         const uint32_t n = in ? static_cast<uint32_t>(count[r]) : 0u;
         const uint64_t b0 = base[r0];
         const uint32_t rel = in ? static_cast<uint32_t>(base[r] - b0) : 0u;   // a unit's lines are < 2^32
-        const uint32_t* bits = rbits + r * rwords;
-        const uint32_t w0 = n ? __ldg(bits) : 0u, w1 = n > 32 ? __ldg(bits + 1) : 0u;
+        // transposed result words: the units' first words are contiguous (coalesced)
+        const uint32_t w0 = n ? __ldg(rbits + r) : 0u, w1 = n > 32 ? __ldg(rbits + nranges + r) : 0u;
         uint8_t* out = results + b0;
 #pragma unroll 4
         for (uint32_t j = 0; j < kScatterUnit; ++j) {
@@ -698,7 +701,7 @@ __global__ void __launch_bounds__(256) k_lt_scatter(const uint32_t* __restrict__
             if (nj > 32) {   // long lines are rare: the rest of the range
                 const uint32_t x1 = __shfl_sync(0xFFFFFFFFu, w1, j);
                 for (uint32_t i = 32 + lane; i < nj; i += 32) {
-                    const uint32_t w = i < 64 ? x1 : __ldg(rbits + (r0 + j) * rwords + (i >> 5));
+                    const uint32_t w = i < 64 ? x1 : __ldg(rbits + (i >> 5) * nranges + r0 + j);
                     out[bj + i] = static_cast<uint8_t>((w >> (i & 31)) & 1u);
                 }
             }
@@ -752,7 +755,7 @@ RangeSplit split_ranges(uint64_t len, uint32_t chunk) {
     return r;
 }
 
-// RES scratch: [counts | bases | scan temp | result bits (rwords per range)].
+// RES scratch: [counts | bases | scan temp | result bits (rwords per range, transposed)].
 uint32_t res_words(uint32_t chunk, uint32_t rem_piece) {
     return ((chunk > rem_piece ? chunk : rem_piece) + 1 + 31) / 32;
 }
@@ -791,6 +794,7 @@ cudaError_t launch(const LtTable& t, const uint8_t* text, uint64_t len, uint8_t 
     void* temp = nullptr;
     if constexpr (RES) {
         a.rwords = res_words(chunk, rs.rem_piece);
+        a.nranges = nr;
         if (!scratch || scratch_bytes < res_scratch_bytes(nr, a.rwords)) return cudaErrorInvalidValue;
         a.rcount = static_cast<unsigned long long*>(scratch);
         base = a.rcount + nr;
