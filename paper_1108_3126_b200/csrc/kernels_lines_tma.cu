@@ -563,11 +563,13 @@ __global__ void __launch_bounds__(C::warps * 32, 1) k_lines_tma(const __grid_con
                     if constexpr (RES) {
 #pragma unroll
                         for (int j = 0; j < C::chains; ++j) {
-                            // bit 7 of each byte: byte == delimiter (exact, no borrow between bytes)
-                            const uint32_t x = word_of(v[j], w);
-                            const uint32_t y = ((x ^ a.delim4) & 0x7F7F7F7Fu) + 0x7F7F7F7Fu;
-                            const uint32_t z = ~(y | (x ^ a.delim_hi4)) & 0x80808080u;
-                            dl[j] += z >> (7 - (4 * (g & 1) + w));
+                            // bit 7 of each byte: byte == delimiter, by the has-zero test on
+                            // x ^ delim (3 ops). A borrow can flag extra bytes, but only in a word
+                            // that holds a delimiter: a column with one line end never reads as
+                            // none or as one, only as several (the exact re-walk below)
+                            const uint32_t u = word_of(v[j], w) ^ a.delim4;
+                            const uint32_t z = (u - 0x01010101u) & ~u & 0x80808080u;
+                            dl[j] |= z >> (7 - (4 * (g & 1) + w));
                         }
                     }
                 }
