@@ -1,6 +1,6 @@
 // K2 for fixed-stride batches on the TMA data path (config (b): 1M strings
 // of 32 bytes). Each lane walks whole strings (three per lane: 96 strings per
-// warp tile); the tiles of a warp stream through a 3-stage shared-memory ring
+// warp tile); the tiles of a warp stream through a 2-stage shared-memory ring
 // that runs across tiles, so the next tile is in flight while the current one
 // is walked (the LDG variant, k_fixed_abs, waits for each pass's loads).
 //   stride 32 ("packed"): the buffer is viewed as [n/4][128 B], a tile is 24
@@ -19,7 +19,7 @@ namespace rxg {
 
 namespace {
 
-constexpr int kFW = 16, kFC = 3, kFRows = 32 * kFC, kFSt = 3;
+constexpr int kFW = 24, kFC = 3, kFRows = 32 * kFC, kFSt = 2;   // (tools/ab_fixed.py: 16x3x3 15.4 us, 24x3x2 14.4, 16x4x2 15.3, 32x2x2 15.4, 16x2x4 16.4, 24x2x3 15.4 on (b), L2 flushed)
 constexpr uint32_t kFSlice = 32, kFStageBytes = kFRows * kFSlice;
 constexpr uint32_t kFBase = 0x400;   // the table image's absolute entries assume this window
 
