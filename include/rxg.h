@@ -397,6 +397,12 @@ int rxg_match_many(int device, const char* patterns, int32_t n_patterns, const u
 int rxg_shard_bounds(const uint8_t* text, uint64_t len, int32_t delimiter, uint32_t stride,
                      int ndev, uint64_t* offsets);
 
+/* Strings in a host buffer as the batch calls split it (delimiter 0-255:
+ * delimiters plus an unterminated last string, std::getline semantics;
+ * delimiter < 0: len / stride): the size of a per-string results buffer.
+ * Host only, counted on a few host threads. */
+int rxg_count_strings(const uint8_t* text, uint64_t len, int32_t delimiter, uint32_t stride, uint64_t* n);
+
 /* Number of kernels the last matching call on this thread launched. */
 int rxg_last_launch_count(void);
 

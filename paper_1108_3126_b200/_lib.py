@@ -106,6 +106,7 @@ _SIG = {
     "rxg_match_one_multi": (C.c_int, [C.POINTER(C.c_int), C.c_int, C.c_char_p, C.c_size_t, _P, C.c_uint64,
                                       C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
     "rxg_shard_bounds": (C.c_int, [_P, C.c_uint64, C.c_int32, C.c_uint32, C.c_int, C.POINTER(C.c_uint64)]),
+    "rxg_count_strings": (C.c_int, [_P, C.c_uint64, C.c_int32, C.c_uint32, C.POINTER(C.c_uint64)]),
     "rxg_last_launch_count": (C.c_int, []),
     "rxg_set_option": (C.c_int, [C.c_char_p, C.c_char_p]),
     "rxg_match_one_stats": (C.c_int, [_P, _P, C.c_uint64, C.POINTER(C.c_int32), C.POINTER(rxg_match_stats)]),
@@ -125,7 +126,7 @@ _SIG = {
 
 OPTION_NAMES = ("RXG_NO_TMA", "RXG_NO_LT", "RXG_NO_FIXED_TMA", "RXG_LINE_CHUNK", "RXG_LT_SHAPE", "RXG_CHUNK_SHAPE",
                 "RXG_TMA_PROMO", "RXG_SKIP_SHARE", "RXG_COL_BYTES", "RXG_NO_ROW_PAIRS", "RXG_FORCE_CLASS",
-                "RXG_NO_RANGE_LAYOUT", "RXG_NO_PACKED", "RXG_CHUNK_FN")
+                "RXG_NO_RANGE_LAYOUT", "RXG_NO_PACKED", "RXG_CHUNK_FN", "RXG_COPY_THREADS")
 
 _lib = None
 

@@ -405,6 +405,18 @@ int line_table(rxg_heap* h, int delim, TableSlot** out, std::shared_ptr<const Lt
     return RXG_OK;
 }
 
+// Host threads filling pinned staging from pageable input: half the cores,
+// 2-16 (config (c), 1 GB pageable, tools/copy_threads.py: 4 threads 28.7 GB/s,
+// 8 31.8, 12 43.6, 16 42.4, 24 43.2); RXG_COPY_THREADS overrides for A/B.
+unsigned copy_threads() {
+    if (const char* e = rxg::option("RXG_COPY_THREADS")) {
+        const unsigned v = static_cast<unsigned>(std::atoi(e));
+        if (v >= 1 && v <= 64) return v;
+    }
+    const unsigned hc = std::thread::hardware_concurrency();
+    return std::min(16u, std::max(2u, hc / 2));
+}
+
 uint32_t env_chunk() {
     const char* e = rxg::option("RXG_LINE_CHUNK");   // tuning override (bytes per range)
     return e ? static_cast<uint32_t>(std::strtoul(e, nullptr, 10)) : 0u;
@@ -1189,8 +1201,7 @@ int stage_pageable_aware(rxg_heap* h, uint8_t* dst, const uint8_t* src, uint64_t
         h->pin_bytes = piece;
     }
     if (!h->copier) {
-        const unsigned hc = std::thread::hardware_concurrency();
-        h->copier = std::make_unique<HostCopyPool>(std::min(8u, std::max(2u, hc / 2)));
+        h->copier = std::make_unique<HostCopyPool>(copy_threads());
     }
     cudaEvent_t done[2];
     for (auto& e : done) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
@@ -1353,8 +1364,7 @@ int host_batch(rxg_heap* h, const uint8_t* text, uint64_t len, int32_t delimiter
     // download into pageable memory.
     const bool pool_count = results && delimiter >= 0 && len >= (1u << 20);
     if ((pageable || pool_count) && !h->copier) {
-        const unsigned hc = std::thread::hardware_concurrency();
-        h->copier = std::make_unique<HostCopyPool>(std::min(8u, std::max(2u, hc / 2)));
+        h->copier = std::make_unique<HostCopyPool>(copy_threads());
     }
     cudaEvent_t copied[2], consumed[2], landed[2];
     for (int i = 0; i < 2; ++i) {
@@ -1725,6 +1735,33 @@ int rxg_shard_bounds(const uint8_t* text, uint64_t len, int32_t delimiter, uint3
         offsets[k] = std::max(cut, offsets[k - 1]);
     }
     offsets[ndev] = len;
+    return RXG_OK;
+}
+
+int rxg_count_strings(const uint8_t* text, uint64_t len, int32_t delimiter, uint32_t stride, uint64_t* n) {
+    if (!n || (!text && len) || delimiter > 255) return fail(RXG_EINVAL, "bad arguments");
+    if (delimiter < 0) {
+        if (stride == 0 || len % stride) return fail(RXG_EINVAL, "fixed stride must divide the buffer length");
+        *n = len / stride;
+        return RXG_OK;
+    }
+    // delimiters counted on a few host threads (the per-string results a
+    // caller sizes before a host-buffer call), plus an unterminated last string
+    const unsigned T = len < (8u << 20) ? 1u : std::min(16u, std::max(1u, std::thread::hardware_concurrency() / 2));
+    std::vector<uint64_t> part(T, 0);
+    std::vector<std::thread> ts;
+    const uint64_t per = (len + T - 1) / T;
+    for (unsigned k = 0; k < T; ++k) {
+        const uint64_t lo = std::min(len, per * k), hi = std::min(len, lo + per);
+        auto run = [&, k, lo, hi] { part[k] = count_byte(text + lo, hi - lo, static_cast<uint8_t>(delimiter)); };
+        if (T == 1) run();
+        else ts.emplace_back(run);
+    }
+    for (auto& t : ts) t.join();
+    uint64_t c = 0;
+    for (uint64_t x : part) c += x;
+    if (len && text[len - 1] != static_cast<uint8_t>(delimiter)) ++c;
+    *n = c;
     return RXG_OK;
 }
 
