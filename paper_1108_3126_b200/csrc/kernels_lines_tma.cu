@@ -677,7 +677,7 @@ CUtensorMapSwizzle swizzle_of(int slice) {
 // together, so most look back hundreds of units before an inclusive prefix.)
 constexpr uint32_t kScatterUnit = 16;
 
-__global__ void __launch_bounds__(256) k_lt_scatter(const uint32_t* __restrict__ rbits, uint32_t rwords,
+__global__ void __launch_bounds__(256) k_lt_scatter(const uint32_t* __restrict__ rbits,
                                                     const unsigned long long* __restrict__ count,
                                                     const unsigned long long* __restrict__ base, uint64_t nranges,
                                                     uint8_t* __restrict__ results) {
@@ -866,7 +866,7 @@ cudaError_t launch(const LtTable& t, const uint8_t* text, uint64_t len, uint8_t 
     e = cub::DeviceScan::ExclusiveSum(temp, temp_bytes, a.rcount, base, static_cast<int64_t>(nr), st);
     if (e != cudaSuccess) return e;
     const uint64_t want2 = (nr + 8 * kScatterUnit - 1) / (8 * kScatterUnit), cap2 = static_cast<uint64_t>(device_sm_count(dev)) * 8;
-    k_lt_scatter<<<static_cast<unsigned>(want2 < cap2 ? want2 : cap2), 256, 0, st>>>(a.rbits, a.rwords, a.rcount, base, nr,
+    k_lt_scatter<<<static_cast<unsigned>(want2 < cap2 ? want2 : cap2), 256, 0, st>>>(a.rbits, a.rcount, base, nr,
                                                                                    results);
     return cudaGetLastError();
 }
