@@ -1,29 +1,35 @@
-// K2 (lines), TMA-staged variant for memoized step tables that fit the
-// raw-byte u16 layout (DFA <= ~56 states, e.g. config (c)).
+// K2 (lines), TMA-staged: the memoized lockstep step over lines of one
+// buffer, count of accepted lines and (RES) one result byte per line.
 //
-// Data path per warp: the warp owns 64 consecutive equal byte ranges
-// ("rows" of a 2-D view [rows][chunk] of the input) — two per lane. A TMA
-// tensor map streams 32-byte column slices of those 64 rows into a 3-stage
-// shared-memory ring (SWIZZLE_32B, so the per-lane 16-byte reads of 8
-// consecutive rows hit 8 distinct bank groups). One elected lane arms the
-// stage mbarrier and issues the copy; all lanes wait on its phase. 24 warps
-// per CTA, one CTA per SM (the table plus ring use ~188 KB of shared memory).
+// Data path per warp: the warp owns 32 * K consecutive equal byte ranges
+// ("rows" of a 2-D view [rows][chunk] of the input), K per lane. A TMA
+// tensor map streams 32-byte column slices of those rows into a shared-memory
+// ring (SWIZZLE_32B, so the per-lane 16-byte reads of 8 consecutive rows hit
+// 8 distinct bank groups). One elected lane arms the stage mbarrier and
+// issues the copy; all lanes wait on its phase. Shapes (warps x K x stages)
+// per table layout are listed above launch_any; one CTA per SM.
 //
-// Step per input byte (the memoized lockstep macro step, see tables.hpp):
-//     a = IDP.4A(word, 4<<8k, s)   extract byte k, scale by the 4-byte column stride, add row
+// Step per input byte, direct layout (the memoized lockstep macro step, see
+// tables.hpp and lines_tma_table.cpp):
+//     a = IDP.4A(word, c<<8k, s)   extract byte k, scale by the column stride c, add the row
 //     s = LDS.U16 [a]              s and the entries are absolute shared addresses
-//     n += hi32(s * 2^17)          START_A (the accepted-line-end row) is the only
+//     n += s >> 15 (LEA.HI)        START_A (the accepted-line-end row) is the only
 //                                  row at >= 0x8000 the main loop can enter
-// Columns are 4 B apart, so the bytes of one row map to banks (row + b) mod 32
-// (' ' and 'a' no longer collide); rows are 1060 B apart (265 words = 9 mod
-// 32), so lanes in different states reading the same byte land in
-// different banks.
+// Class layouts (larger DFAs) index rows by state and columns by byte class
+// (a class map) or by min(b ^ x, k) (range-clamped columns).
 //
 // Line ownership (every line matched exactly once): a range owns the lines
 // starting in it after its first byte, plus the line starting right after
 // it when its last byte is the delimiter; it enters in SKIP (range 0 in the
 // start state) and finishes its last line through the tail copy of the
-// table with direct global loads (see range_direct).
+// table with direct global loads (finish_lines, range_direct).
+//
+// Per-line results (RES) in one pass: the byte loop is the count walk; each
+// 4-byte word adds a has-zero delimiter mask, and per 32-byte stage column a
+// chain with one line end records that line's result as the column's count
+// difference (several: the column is walked again from its entry row). A
+// range's owned results go out as range-local bits and a count; a cub scan
+// of the counts and k_lt_scatter place them.
 #include <cub/device/device_scan.cuh>
 #include <cuda.h>
 #include <cudaTypedefs.h>

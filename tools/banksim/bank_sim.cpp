@@ -5,6 +5,7 @@
 //
 //   bank_sim CONFIG [HOT...]   (CONFIG a-e; HOT: hot-row counts to model)
 #include <algorithm>
+#include <array>
 #include <cstdio>
 #include <cstdlib>
 #include <map>
@@ -85,6 +86,55 @@ int main(int argc, char** argv) {
     };
     std::printf("current layout: %.3f wavefronts / warp step\n",
                 score([&](uint32_t s, uint8_t b, uint32_t) { return (rows_addr + s * t.row_bytes + 2 * col_of(b)) >> 2; }));
+    // Local search on the row numbering (the builder's greedy placement is the
+    // start): swap two main rows when the pairwise same-bank mass
+    // sum_{s != s'} P(s, c) P(s', c') [bank(s, c) == bank(s', c')] drops.
+    {
+        const uint32_t rbw = t.row_bytes / 4, base = rows_addr / 4;
+        const uint32_t nmain = static_cast<uint32_t>(d.n_states) + 2;
+        std::vector<std::array<double, 32>> Hs(nmain);   // word-offset histogram per current row (offset 0 row)
+        for (auto& h : Hs) h.fill(0.0);
+        for (uint32_t w = 0; w < warps * 32; ++w)
+            for (uint32_t k = 0; k < steps; ++k) {
+                const uint32_t s = S[w][k];
+                if (s < nmain) Hs[s][(col_of(B[w][k]) / 2) & 31u] += 1.0 / total;
+            }
+        std::vector<uint32_t> row(nmain);
+        for (uint32_t r = 0; r < nmain; ++r) row[r] = r;
+        auto off = [&](uint32_t r) { return (base + r * rbw) & 31u; };
+        auto pair_cost = [&](uint32_t a, uint32_t oa, uint32_t b, uint32_t ob) {
+            double c = 0;
+            for (uint32_t k = 0; k < 32; ++k) c += Hs[a][k] * Hs[b][(k + oa + 64 - ob) & 31u];
+            return c;
+        };
+        auto cost_of = [&](uint32_t a, uint32_t oa, uint32_t skip) {   // row a at offset oa against all others
+            double c = 0;
+            for (uint32_t b = 0; b < nmain; ++b)
+                if (b != a && b != skip) c += pair_cost(a, oa, b, off(row[b]));
+            return c;
+        };
+        for (int pass = 0; pass < 4; ++pass) {
+            int swaps = 0;
+            for (uint32_t a = 0; a < nmain; ++a)
+                for (uint32_t b = a + 1; b < nmain; ++b) {
+                    const uint32_t oa = off(row[a]), ob = off(row[b]);
+                    if (oa == ob) continue;
+                    const double now = cost_of(a, oa, b) + cost_of(b, ob, a);
+                    const double sw = cost_of(a, ob, b) + cost_of(b, oa, a);
+                    if (sw < now - 1e-12) {
+                        std::swap(row[a], row[b]);
+                        ++swaps;
+                    }
+                }
+            std::printf("local search pass %d: %d swaps\n", pass, swaps);
+            if (!swaps) break;
+        }
+        std::printf("renumbered layout: %.3f wavefronts / warp step\n",
+                    score([&](uint32_t s, uint8_t b, uint32_t) {
+                        const uint32_t r = s < nmain ? row[s] : s;
+                        return (rows_addr + r * t.row_bytes + 2 * col_of(b)) >> 2;
+                    }));
+    }
     for (int i = 2; i < argc; ++i) {
         const size_t H = static_cast<size_t>(std::atoi(argv[i]));
         std::map<uint32_t, uint32_t> hidx;
