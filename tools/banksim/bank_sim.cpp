@@ -135,6 +135,22 @@ int main(int argc, char** argv) {
                         return (rows_addr + r * t.row_bytes + 2 * col_of(b)) >> 2;
                     }));
     }
+    // Paired rows: two states share each column word (u16 halves), rows of
+    // (k + 1) words at an odd stride; states paired in hotness order.
+    {
+        std::map<uint32_t, uint32_t> pair_of;
+        uint32_t np = 0;
+        for (size_t j = 0; j < hot.size(); ++j) pair_of[hot[j].second] = static_cast<uint32_t>(j / 2);
+        np = static_cast<uint32_t>((hot.size() + 1) / 2);
+        uint32_t pw = t.range_k + 1;
+        if ((pw & 1u) == 0) ++pw;
+        std::printf("paired rows (%u pairs, %u words each): %.3f wavefronts / warp step\n", np, pw,
+                    score([&](uint32_t s, uint8_t b, uint32_t) {
+                        auto it = pair_of.find(s);
+                        const uint32_t pr = it != pair_of.end() ? it->second : np + s;
+                        return 0x1000u + pr * pw + col_of(b);
+                    }));
+    }
     for (int i = 2; i < argc; ++i) {
         const size_t H = static_cast<size_t>(std::atoi(argv[i]));
         std::map<uint32_t, uint32_t> hidx;
