@@ -135,6 +135,36 @@ int main(int argc, char** argv) {
                         return (rows_addr + r * t.row_bytes + 2 * col_of(b)) >> 2;
                     }));
     }
+    // Absorbing hot state: lanes in a state whose every non-delimiter byte
+    // leads back to itself skip the table load (predicated off). (Config (d)'s
+    // accepting state is absorbing only over the pattern's alphabet: bytes of
+    // class 0 lead to the dead state, so an exact skip also needs a per-word
+    // alphabet test; the two compares alone measured +2% on (d).)
+    {
+        const uint32_t h0 = hot[0].second;
+        bool absorbing = true;
+        for (int b = 0; b < 256 && absorbing; ++b)
+            if (b != '\n' && lt_step(t, h0, static_cast<uint8_t>(b)) != h0) absorbing = false;
+        std::printf("hottest row %u (share %.3f) absorbing: %d\n", h0, hot[0].first / total, absorbing);
+        if (absorbing) {
+            double wf = 0;
+            for (uint32_t w = 0; w < warps; ++w)
+                for (uint32_t k = 0; k < steps; ++k) {
+                    std::set<uint32_t> words[32];
+                    for (uint32_t l = 0; l < 32; ++l) {
+                        const uint32_t s0 = S[w * 32 + l][k];
+                        const uint8_t b = B[w * 32 + l][k];
+                        if (s0 == h0 && b != '\n') continue;
+                        const uint32_t wd = (rows_addr + s0 * t.row_bytes + 2 * col_of(b)) >> 2;
+                        words[wd & 31].insert(wd);
+                    }
+                    size_t m = 0;
+                    for (auto& x : words) m = std::max(m, x.size());
+                    wf += static_cast<double>(m);
+                }
+            std::printf("absorbing row skipped: %.3f wavefronts / warp step\n", wf / (static_cast<double>(warps) * steps));
+        }
+    }
     // Paired rows: two states share each column word (u16 halves), rows of
     // (k + 1) words at an odd stride; states paired in hotness order.
     {
