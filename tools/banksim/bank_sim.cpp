@@ -165,6 +165,31 @@ int main(int argc, char** argv) {
             std::printf("absorbing row skipped: %.3f wavefronts / warp step\n", wf / (static_cast<double>(warps) * steps));
         }
     }
+    // Hot rows lane-replicated over a compact column set (the columns with a
+    // sampled share >= 0.5% in the hot rows), the rest through the cold rows.
+    for (size_t H : {8u, 16u, 24u, 32u}) {
+        std::map<uint32_t, uint32_t> hidx;
+        for (size_t j = 0; j < std::min(H, hot.size()); ++j) hidx[hot[j].second] = static_cast<uint32_t>(j);
+        std::map<uint32_t, double> colw;
+        double hs = 0;
+        for (uint32_t w = 0; w < warps * 32; ++w)
+            for (uint32_t k = 0; k < steps; ++k)
+                if (hidx.count(S[w][k])) {
+                    colw[col_of(B[w][k])] += 1;
+                    hs += 1;
+                }
+        std::map<uint32_t, uint32_t> cidx;
+        for (auto& kv : colw)
+            if (kv.second >= 0.005 * hs) cidx[kv.first] = static_cast<uint32_t>(cidx.size());
+        const uint32_t cw = static_cast<uint32_t>((cidx.size() + 1) / 2);
+        std::printf("hot %2zu compact cols %zu (%u words): %.1f KB, %.3f wavefronts\n", H, cidx.size(), cw, H * cw * 128 / 1024.0,
+                    score([&](uint32_t s0, uint8_t b, uint32_t l) {
+                        auto it = hidx.find(s0);
+                        auto ic = cidx.find(col_of(b));
+                        if (it != hidx.end() && ic != cidx.end()) return 0x20000u + (it->second * cw + ic->second / 2) * 32 + l;
+                        return (rows_addr + s0 * t.row_bytes + 2 * col_of(b)) >> 2;
+                    }));
+    }
     // Paired rows: two states share each column word (u16 halves), rows of
     // (k + 1) words at an odd stride; states paired in hotness order.
     {
