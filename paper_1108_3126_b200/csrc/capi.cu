@@ -537,7 +537,7 @@ int batch_device(rxg_heap* h, const uint8_t* d_text, uint64_t len, int32_t delim
                                                                chunk, d_count, d_results, scratch, sb, cs, st);
                 cudaFreeAsync(scratch, st);
                 if (e != cudaSuccess) return cuda_fail(e, "launch_lines_tma_results");
-                ls.kernels = 3;
+                ls.kernels = 2;   // the walk and the scatter
             } else {
                 RXG_CUDA(zero_count_now());
             }

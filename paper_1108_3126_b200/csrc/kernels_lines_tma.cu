@@ -30,7 +30,6 @@
 // difference (several: the column is walked again from its entry row). A
 // range's owned results go out as range-local bits and a count; a cub scan
 // of the counts and k_lt_scatter place them.
-#include <cub/device/device_scan.cuh>
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -81,6 +80,7 @@ struct Args {
     uint32_t rwords;
     uint64_t nranges;
     unsigned long long* rcount;                 // owned lines per range
+    uint32_t* tsum;                             // owned lines per warp tile (+ one for the remainder pieces)
 };
 
 // Per-line results bookkeeping of one range (RES): the results of the lines
@@ -389,7 +389,7 @@ __device__ void finish_lines(const Args& a, uint32_t (&s)[K], uint64_t (&pos)[K]
 //
 // A range processed entirely with direct loads (the remainder pieces).
 template <int L, bool RES>
-__device__ void range_direct(const Args& a, uint64_t c0, uint64_t c1, uint64_t range, uint32_t& cnt) {
+__device__ uint32_t range_direct(const Args& a, uint64_t c0, uint64_t c1, uint64_t range, uint32_t& cnt) {
     uint32_t s = c0 == 0 ? a.start : a.skip;
     LineCursor lc = cursor_of(a, range, s == a.start, true);
     uint32_t last = 0;
@@ -425,6 +425,7 @@ __device__ void range_direct(const Args& a, uint64_t c0, uint64_t c1, uint64_t r
         if constexpr (RES) lc.push(ok);
     }
     if constexpr (RES) lc.close(a.rcount + range);
+    return RES ? lc.lj : 0u;   // owned lines (RES)
 }
 
 // RES: a stage column that holds several line ends, walked again from its
@@ -495,10 +496,18 @@ __global__ void __launch_bounds__(C::warps * 32, 1) k_lines_tma(const __grid_con
     if (blockIdx.x == 0 && warp == 0 && a.rem_pieces) {
         mbar_wait(tbar, 0);
         const uint64_t r0 = a.rows * a.chunk;
+        uint32_t own = 0;
         for (uint32_t p = lane; p < a.rem_pieces; p += 32) {
             const uint64_t c0 = r0 + static_cast<uint64_t>(p) * a.rem_piece;
-            range_direct<L, RES>(a, c0, min(c0 + a.rem_piece, a.len), a.rows + p, cnt);
+            own += range_direct<L, RES>(a, c0, min(c0 + a.rem_piece, a.len), a.rows + p, cnt);
         }
+        if constexpr (RES) {   // the remainder pieces are the scatter's last unit
+            own = __reduce_add_sync(0xFFFFFFFFu, own);
+            if (lane == 0) a.tsum[a.tiles] = own;
+        }
+    }
+    if constexpr (RES) {
+        if (blockIdx.x == 0 && threadIdx.x == 0 && !a.rem_pieces) a.tsum[a.tiles] = 0;
     }
 
     uint32_t phase = 0;   // bit st = parity of stage st's next completion
@@ -628,6 +637,13 @@ __global__ void __launch_bounds__(C::warps * 32, 1) k_lines_tma(const __grid_con
                     if (valid[j]) lc[j].close(a.rcount + row0 + j * 32 + lane);
                 }
             }
+            if constexpr (RES) {   // the tile's owned lines: the scatter places tiles from these
+                uint32_t own = 0;
+#pragma unroll
+                for (int j = 0; j < C::chains; ++j) own += valid[j] ? lc[j].lj : 0u;
+                own = __reduce_add_sync(0xFFFFFFFFu, own);
+                if (lane == 0) a.tsum[tile] = own;
+            }
         }
     }
     cnt = __reduce_add_sync(0xFFFFFFFFu, cnt);
@@ -673,34 +689,55 @@ CUtensorMapSwizzle swizzle_of(int slice) {
     }
 }
 
-// Per-line results (RES), second pass: range r's owned lines start at
-// line base[r] (exclusive scan of the counts). A warp takes units of 16
-// ranges: lane j loads range j's count, base and first two result words
-// (coalesced, independent), then the warp writes each range's bytes in turn,
-// up to 32 consecutive bytes per store. The grid is one wave of warps that
-// stride over the units (small units: no half-empty second wave). (A
-// decoupled look-back scan fused in here measured slower: ~9.5k warps start
-// together, so most look back hundreds of units before an inclusive prefix.)
-constexpr uint32_t kScatterUnit = 16;
-
+// Per-line results (RES), second pass, one launch: a warp takes one walk
+// tile (its R consecutive ranges; the last unit is the remainder pieces).
+// The tile's first line is the sum of the owned-line totals of the tiles
+// before it: each block sums the totals before its first tile (a few
+// thousand u32 values, cached), each warp adds those of the block's earlier
+// tiles. Within the tile, 32 ranges at a time: lane j holds range j's count
+// and first two result words (coalesced: the words are transposed), a warp
+// scan gives the ranges' offsets, and the warp writes each range's bytes,
+// up to 32 consecutive bytes per store. (A decoupled look-back over all
+// ranges measured slower: ~9.5k warps start together and look back far.)
 __global__ void __launch_bounds__(256) k_lt_scatter(const uint32_t* __restrict__ rbits,
                                                     const unsigned long long* __restrict__ count,
-                                                    const unsigned long long* __restrict__ base, uint64_t nranges,
-                                                    uint8_t* __restrict__ results) {
-    const uint32_t lane = threadIdx.x & 31;
-    const uint64_t nwarps = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5);
-    for (uint64_t r0 = (static_cast<uint64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5)) * kScatterUnit;
-         r0 < nranges; r0 += nwarps * kScatterUnit) {
+                                                    const uint32_t* __restrict__ tsum, uint64_t nunits, uint32_t R,
+                                                    uint64_t rows, uint64_t nranges, uint8_t* __restrict__ results) {
+    __shared__ unsigned long long part[8];
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint64_t u0 = static_cast<uint64_t>(blockIdx.x) * 8;
+    unsigned long long acc = 0;
+    for (uint64_t i = threadIdx.x; i < u0; i += blockDim.x) acc += tsum[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xFFFFFFFFu, acc, o);
+    if (lane == 0) part[warp] = acc;
+    __syncthreads();
+    const uint64_t u = u0 + warp;
+    if (u >= nunits) return;
+    unsigned long long prefix = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) prefix += part[w];
+    prefix += __reduce_add_sync(0xFFFFFFFFu, lane < warp ? tsum[u0 + lane] : 0u);
+    const bool pieces = u + 1 == nunits;
+    const uint64_t rb = pieces ? rows : u * R;
+    const uint64_t re = pieces ? nranges : min(rb + R, rows);
+    uint8_t* out = results + prefix;
+    uint32_t run = 0;   // lines of this tile placed so far
+    for (uint64_t r0 = rb; r0 < re; r0 += 32) {
         const uint64_t r = r0 + lane;
-        const bool in = lane < kScatterUnit && r < nranges;
+        const bool in = r < re;
         const uint32_t n = in ? static_cast<uint32_t>(count[r]) : 0u;
-        const uint64_t b0 = base[r0];
-        const uint32_t rel = in ? static_cast<uint32_t>(base[r] - b0) : 0u;   // a unit's lines are < 2^32
-        // transposed result words: the units' first words are contiguous (coalesced)
         const uint32_t w0 = n ? __ldg(rbits + r) : 0u, w1 = n > 32 ? __ldg(rbits + nranges + r) : 0u;
-        uint8_t* out = results + b0;
+        uint32_t incl = n;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+            if (lane >= static_cast<uint32_t>(o)) incl += y;
+        }
+        const uint32_t rel = run + incl - n;
+        run += __shfl_sync(0xFFFFFFFFu, incl, 31);
 #pragma unroll 4
-        for (uint32_t j = 0; j < kScatterUnit; ++j) {
+        for (uint32_t j = 0; j < 32; ++j) {
             const uint32_t nj = __shfl_sync(0xFFFFFFFFu, n, j);
             if (nj == 0) continue;
             const uint32_t bj = __shfl_sync(0xFFFFFFFFu, rel, j);
@@ -768,15 +805,12 @@ uint32_t res_words(uint32_t chunk, uint32_t rem_piece) {
     return ((chunk > rem_piece ? chunk : rem_piece) + 1 + 31) / 32;
 }
 
-size_t res_temp_bytes(uint64_t nranges) {
-    size_t temp = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, temp, static_cast<unsigned long long*>(nullptr),
-                                  static_cast<unsigned long long*>(nullptr), static_cast<int64_t>(nranges));
-    return (temp + 255) & ~size_t(255);
-}
+// RES scratch: [owned lines per range (u64) | per-tile totals (u32; tiles <= ranges / 32,
+// + the remainder unit) | result bits (rwords per range, transposed)].
+size_t res_tsum_bytes(uint64_t nranges) { return ((nranges / 32 + 2) * sizeof(uint32_t) + 255) & ~size_t(255); }
 
 size_t res_scratch_bytes(uint64_t nranges, uint32_t rwords) {
-    return 2 * nranges * sizeof(unsigned long long) + res_temp_bytes(nranges) + nranges * rwords * 4ull + 256;
+    return nranges * sizeof(unsigned long long) + res_tsum_bytes(nranges) + nranges * rwords * 4ull + 256;
 }
 
 template <class C, int L, bool RES>
@@ -798,16 +832,13 @@ cudaError_t launch(const LtTable& t, const uint8_t* text, uint64_t len, uint8_t 
     a.rem_piece = rs.rem_piece;
     a.rem_pieces = rs.rem_pieces;
     const uint64_t nr = rs.rows + rs.rem_pieces;
-    unsigned long long* base = nullptr;
-    void* temp = nullptr;
     if constexpr (RES) {
         a.rwords = res_words(chunk, rs.rem_piece);
         a.nranges = nr;
         if (!scratch || scratch_bytes < res_scratch_bytes(nr, a.rwords)) return cudaErrorInvalidValue;
         a.rcount = static_cast<unsigned long long*>(scratch);
-        base = a.rcount + nr;
-        temp = base + nr;
-        a.rbits = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(temp) + res_temp_bytes(nr));
+        a.tsum = reinterpret_cast<uint32_t*>(a.rcount + nr);
+        a.rbits = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(a.tsum) + res_tsum_bytes(nr));
     }
     a.img_lo = static_cast<const uint4*>(t.d_lo);
     a.lo_addr = t.lo_addr;
@@ -867,13 +898,11 @@ cudaError_t launch(const LtTable& t, const uint8_t* text, uint64_t len, uint8_t 
     k_lines_tma<C, L, RES><<<grid, C::warps * 32, smem, st>>>(a, map);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess || !RES) return e;
-    // per-line results: place each range's owned lines (scan of the counts, then scatter)
-    size_t temp_bytes = res_temp_bytes(nr);
-    e = cub::DeviceScan::ExclusiveSum(temp, temp_bytes, a.rcount, base, static_cast<int64_t>(nr), st);
-    if (e != cudaSuccess) return e;
-    const uint64_t want2 = (nr + 8 * kScatterUnit - 1) / (8 * kScatterUnit), cap2 = static_cast<uint64_t>(device_sm_count(dev)) * 8;
-    k_lt_scatter<<<static_cast<unsigned>(want2 < cap2 ? want2 : cap2), 256, 0, st>>>(a.rbits, a.rcount, base, nr,
-                                                                                   results);
+    // per-line results: place each tile's owned lines (tile totals summed in the scatter)
+    const uint64_t nunits = a.tiles + 1;
+    k_lt_scatter<<<static_cast<unsigned>((nunits + 7) / 8), 256, 0, st>>>(a.rbits, a.rcount, a.tsum, nunits,
+                                                                          static_cast<uint32_t>(C::rows), a.rows, nr,
+                                                                          results);
     return cudaGetLastError();
 }
 
