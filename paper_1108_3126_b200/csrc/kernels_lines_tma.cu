@@ -28,8 +28,9 @@
 // 4-byte word adds a has-zero delimiter mask, and per 32-byte stage column a
 // chain with one line end records that line's result as the column's count
 // difference (several: the column is walked again from its entry row). A
-// range's owned results go out as range-local bits and a count; a cub scan
-// of the counts and k_lt_scatter place them.
+// range's owned results go out as range-local bits and a count, each warp
+// tile's total as well; k_lt_scatter places them (one tile per warp, its
+// base summed from the totals before it).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
