@@ -705,6 +705,7 @@ __global__ void __launch_bounds__(256) k_lt_scatter(const uint32_t* __restrict__
                                                     const uint32_t* __restrict__ tsum, uint64_t nunits, uint32_t R,
                                                     uint64_t rows, uint64_t nranges, uint8_t* __restrict__ results) {
     __shared__ unsigned long long part[8];
+    __shared__ uint32_t wbits[8][66];   // per warp: a group's results as bits (32 ranges x <= 64 lines, + slack)
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint64_t u0 = static_cast<uint64_t>(blockIdx.x) * 8;
     unsigned long long acc = 0;
@@ -724,6 +725,7 @@ __global__ void __launch_bounds__(256) k_lt_scatter(const uint32_t* __restrict__
     const uint64_t re = pieces ? nranges : min(rb + R, rows);
     uint8_t* out = results + prefix;
     uint32_t run = 0;   // lines of this tile placed so far
+    uint32_t* bitbuf = wbits[warp];
     for (uint64_t r0 = rb; r0 < re; r0 += 32) {
         const uint64_t r = r0 + lane;
         const bool in = r < re;
@@ -735,20 +737,68 @@ __global__ void __launch_bounds__(256) k_lt_scatter(const uint32_t* __restrict__
             const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
             if (lane >= static_cast<uint32_t>(o)) incl += y;
         }
-        const uint32_t rel = run + incl - n;
-        run += __shfl_sync(0xFFFFFFFFu, incl, 31);
+        const uint32_t rel = incl - n;   // within this group of 32 ranges
+        const uint32_t total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+        uint8_t* gout = out + run;
+        run += total;
+        if (total == 0) continue;
+        if (!__any_sync(0xFFFFFFFFu, n > 64)) {
+            // the group's results as one bit array (at most 32 * 64 bits), then
+            // 16 bytes per lane store: 16 bits spread to bytes, aligned 16-byte
+            // stores inside, byte stores in the partial chunks at the edges
+            bitbuf[lane] = 0u;
+            bitbuf[lane + 32] = 0u;
+            if (lane < 2) bitbuf[lane + 64] = 0u;
+            __syncwarp();
+            if (n) {
+                const uint32_t k = rel >> 5, sh = rel & 31u;
+                atomicOr(bitbuf + k, w0 << sh);
+                if (sh) atomicOr(bitbuf + k + 1, w0 >> (32 - sh));
+                if (n > 32) {
+                    atomicOr(bitbuf + k + 1, w1 << sh);
+                    if (sh) atomicOr(bitbuf + k + 2, w1 >> (32 - sh));
+                }
+            }
+            __syncwarp();
+            const uintptr_t g0 = reinterpret_cast<uintptr_t>(gout), ga = g0 & ~uintptr_t(15);
+            const uint32_t nchunks = static_cast<uint32_t>((g0 + total - ga + 15) >> 4);
+            for (uint32_t c = lane; c < nchunks; c += 32) {
+                const uintptr_t cb = ga + 16u * c;   // chunk start (global address)
+                const int32_t b0 = static_cast<int32_t>(static_cast<intptr_t>(cb) - static_cast<intptr_t>(g0));   // bit of its first byte
+                if (b0 >= 0 && b0 + 16 <= static_cast<int32_t>(total)) {
+                    const uint32_t bw = static_cast<uint32_t>(b0) >> 5, bs = static_cast<uint32_t>(b0) & 31u;
+                    const uint32_t lo = bitbuf[bw], hi = bs + 16 > 32 ? bitbuf[bw + 1] : 0u;
+                    const uint32_t bits16 = __funnelshift_r(lo, hi, bs) & 0xFFFFu;
+                    uint4 v;
+                    v.x = ((bits16 & 0xFu) * 0x00204081u) & 0x01010101u;
+                    v.y = (((bits16 >> 4) & 0xFu) * 0x00204081u) & 0x01010101u;
+                    v.z = (((bits16 >> 8) & 0xFu) * 0x00204081u) & 0x01010101u;
+                    v.w = (((bits16 >> 12) & 0xFu) * 0x00204081u) & 0x01010101u;
+                    *reinterpret_cast<uint4*>(cb) = v;
+                } else {   // a partial chunk: only this group's bytes
+                    for (int32_t i = 0; i < 16; ++i) {
+                        const int32_t bi = b0 + i;
+                        if (bi < 0 || bi >= static_cast<int32_t>(total)) continue;
+                        reinterpret_cast<uint8_t*>(cb)[i] = static_cast<uint8_t>((bitbuf[bi >> 5] >> (bi & 31)) & 1u);
+                    }
+                }
+            }
+            __syncwarp();
+            continue;
+        }
+        // ranges with more than 64 lines (short lines): each range's bytes in turn
 #pragma unroll 4
         for (uint32_t j = 0; j < 32; ++j) {
             const uint32_t nj = __shfl_sync(0xFFFFFFFFu, n, j);
             if (nj == 0) continue;
             const uint32_t bj = __shfl_sync(0xFFFFFFFFu, rel, j);
             const uint32_t x0 = __shfl_sync(0xFFFFFFFFu, w0, j);
-            if (lane < nj) out[bj + lane] = static_cast<uint8_t>((x0 >> lane) & 1u);
-            if (nj > 32) {   // long lines are rare: the rest of the range
+            if (lane < nj) gout[bj + lane] = static_cast<uint8_t>((x0 >> lane) & 1u);
+            if (nj > 32) {
                 const uint32_t x1 = __shfl_sync(0xFFFFFFFFu, w1, j);
                 for (uint32_t i = 32 + lane; i < nj; i += 32) {
                     const uint32_t w = i < 64 ? x1 : __ldg(rbits + (i >> 5) * nranges + r0 + j);
-                    out[bj + i] = static_cast<uint8_t>((w >> (i & 31)) & 1u);
+                    gout[bj + i] = static_cast<uint8_t>((w >> (i & 31)) & 1u);
                 }
             }
         }
