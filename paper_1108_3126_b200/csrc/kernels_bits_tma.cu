@@ -94,14 +94,14 @@ BitsTables make_bits_tables(const Program& p, int32_t delim) {
     auto rg = [&](int32_t g, int32_t w) { return g < t.G ? rows[static_cast<size_t>(g) * WT + w] : 0u; };
     std::vector<uint32_t>& img = t.img;
     if (WT <= 4) {
-        // per byte: [M, D (2 on the delimiter, else 0), pad]; then T_g, R_g of the
+        // per byte: [M, D (1 on the delimiter, else 0), pad]; then T_g, R_g of the
         // groups >= 2 (broadcast rows); registers: SH, E0, T_0, R_0, T_1, R_1
         t.row_words = WT == 1 ? 2 : (WT + 1 + 3) / 4 * 4;
         img.assign(static_cast<size_t>(256) * t.row_words, 0u);
         for (int b = 0; b < 256; ++b) {
             uint32_t* r = &img[static_cast<size_t>(b) * t.row_words];
             for (int32_t w = 0; w < WT; ++w) r[w] = M[static_cast<size_t>(b) * WT + w];
-            r[WT] = b == delim ? 2u : 0u;
+            r[WT] = b == delim ? 1u : 0u;
         }
         t.xg_off = static_cast<uint32_t>(img.size()) * 4;
         for (int32_t g = 2; g < t.G; ++g) {
@@ -122,7 +122,7 @@ BitsTables make_bits_tables(const Program& p, int32_t delim) {
         for (int b = 0; b < 256; ++b) {
             uint32_t* r = &img[static_cast<size_t>(b) * t.row_words];
             for (int32_t w = 0; w < WT; ++w) r[w] = M[static_cast<size_t>(b) * WT + w];
-            r[WT] = b == delim ? 2u : 0u;
+            r[WT] = b == delim ? 1u : 0u;
         }
         t.xg_off = static_cast<uint32_t>(img.size()) * 4;
         img.insert(img.end(), SH.begin(), SH.end());
@@ -153,7 +153,6 @@ struct BArgs {
     uint32_t delim4;                  // delimiter in every byte
     int32_t n_groups;
     uint32_t two;         // the constant 2 (a register operand keeps IMAD on the FMA pipe)
-    uint32_t half;        // the constant 2^31 (D >> 1 as an IMAD.HI, not a shift on the ALU pipe)
     const uint4* img;
     uint32_t img_words;   // 16-byte units
     uint32_t tab;         // shared address of M
@@ -294,16 +293,15 @@ __device__ __forceinline__ void bstep_row(const BArgs& a, const Rows<WT, GR, REG
             }
         }
     }
-    // String end, all on the FMA pipe: D is 2 on the delimiter (else 0) and
-    // the delimiter's M row is empty, so nx is empty there. Count A (bit 31 of
-    // the last word) as hi32(E * D), restart as E0 * (D / 2) + nx. Lanes
-    // past the last range hold E0 = 0 in R (they never count).
+    // String end without a select: D is 1 on the delimiter (else 0) and the
+    // delimiter's M row is empty, so nx is empty there. Count A (bit 31 of the
+    // last word) as (E * D) >> 31 (IMAD, LEA.HI), restart as E0 * D + nx
+    // (IMAD). Lanes past the last range hold E0 = 0 in R (they never count).
     (void)cm;
     const uint32_t D = row[WT];
-    asm("mad.hi.u32 %0, %1, %2, %0;" : "+r"(cnt) : "r"(E[WT - 1]), "r"(D));   // one IMAD.HI, no IADD3
-    const uint32_t d1 = __umulhi(D, a.half);
+    cnt += (E[WT - 1] * D) >> 31;
 #pragma unroll
-    for (int w = 0; w < WT; ++w) E[w] = R.e0[w] * d1 + nx[w];
+    for (int w = 0; w < WT; ++w) E[w] = R.e0[w] * D + nx[w];
     m = D;
 }
 
@@ -357,14 +355,13 @@ __device__ __forceinline__ void bstep(const BArgs& a, const Rows<WT, GR, REG>& R
                 }
             }
         }
-        cnt += __umulhi(E[WT - 1] & cm, D);   // D: 2 on the delimiter, else 0
-        const uint32_t d1 = __umulhi(D, a.half);
+        cnt += ((E[WT - 1] & cm) * D) >> 31;   // D: 1 on the delimiter, else 0
 #pragma unroll
         for (int w4 = 0; w4 < WT / 4; ++w4) {
             uint32_t e0[4];
             R.get4(1, w4, e0);
 #pragma unroll
-            for (int j = 0; j < 4; ++j) E[w4 * 4 + j] = e0[j] * d1 + nx[w4 * 4 + j];   // nx is empty on the delimiter
+            for (int j = 0; j < 4; ++j) E[w4 * 4 + j] = e0[j] * D + nx[w4 * 4 + j];   // nx is empty on the delimiter
         }
         m = D;
     }
@@ -783,7 +780,6 @@ cudaError_t run(const BitsImage& b, const uint8_t* text, uint64_t len, int32_t d
     a.delim4 = FIXED ? 0u : static_cast<uint32_t>(delim) * 0x01010101u;
     a.n_groups = b.t.G;
     a.two = 2;
-    a.half = 0x80000000u;
     a.img = static_cast<const uint4*>(b.d_img);
     a.img_words = static_cast<uint32_t>(b.t.img.size() / 4);
     a.regs_g = b.d_regs;
