@@ -355,13 +355,20 @@ __device__ __forceinline__ void bstep(const BArgs& a, const Rows<WT, GR, REG>& R
                 }
             }
         }
-        cnt += ((E[WT - 1] & cm) * D) >> 31;   // D: 1 on the delimiter, else 0
+        // D: 1 on the delimiter, else 0. E0 is read only at a line end (rare):
+        // E0 at a delimiter (nx is empty there), nx otherwise
+        if (D) {
+            cnt += (E[WT - 1] & cm) >> 31;
 #pragma unroll
-        for (int w4 = 0; w4 < WT / 4; ++w4) {
-            uint32_t e0[4];
-            R.get4(1, w4, e0);
+            for (int w4 = 0; w4 < WT / 4; ++w4) {
+                uint32_t e0[4];
+                R.get4(1, w4, e0);
 #pragma unroll
-            for (int j = 0; j < 4; ++j) E[w4 * 4 + j] = e0[j] * D + nx[w4 * 4 + j];   // nx is empty on the delimiter
+                for (int j = 0; j < 4; ++j) E[w4 * 4 + j] = e0[j];
+            }
+        } else {
+#pragma unroll
+            for (int w = 0; w < WT; ++w) E[w] = nx[w];
         }
         m = D;
     }
