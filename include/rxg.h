@@ -411,7 +411,8 @@ int rxg_last_launch_count(void);
  * RXG_NO_TMA, RXG_NO_LT, RXG_NO_FIXED_TMA (generic kernels), RXG_LINE_CHUNK
  * (bytes per range), RXG_LT_SHAPE, RXG_CHUNK_SHAPE, RXG_TMA_PROMO,
  * RXG_SKIP_SHARE, RXG_COL_BYTES, RXG_NO_ROW_PAIRS, RXG_FORCE_CLASS,
- * RXG_NO_RANGE_LAYOUT, RXG_NO_PACKED, RXG_CHUNK_FN ("0"/"1": force the
+ * RXG_NO_RANGE_LAYOUT, RXG_NO_PACKED, RXG_NO_BITS_TMA (the bitset engine's
+ * generic kernel), RXG_CHUNK_FN ("0"/"1": force the
  * chunk engine's transfer-function mode off/on for packed tables; by default
  * it is on for automata with a byte that permutes states), RXG_COPY_THREADS
  * (host threads filling pinned staging from pageable input). The library

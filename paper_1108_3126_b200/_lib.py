@@ -126,7 +126,7 @@ _SIG = {
 
 OPTION_NAMES = ("RXG_NO_TMA", "RXG_NO_LT", "RXG_NO_FIXED_TMA", "RXG_LINE_CHUNK", "RXG_LT_SHAPE", "RXG_CHUNK_SHAPE",
                 "RXG_TMA_PROMO", "RXG_SKIP_SHARE", "RXG_COL_BYTES", "RXG_NO_ROW_PAIRS", "RXG_FORCE_CLASS",
-                "RXG_NO_RANGE_LAYOUT", "RXG_NO_PACKED", "RXG_CHUNK_FN", "RXG_COPY_THREADS")
+                "RXG_NO_RANGE_LAYOUT", "RXG_NO_PACKED", "RXG_CHUNK_FN", "RXG_COPY_THREADS", "RXG_NO_BITS_TMA")
 
 _lib = None
 
