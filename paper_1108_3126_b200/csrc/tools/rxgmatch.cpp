@@ -183,7 +183,8 @@ int main(int argc, char** argv) {
         return kError;
     }
     // The device context and tables are built on a second thread while the
-    // input is read (CUDA initialisation is ~0.5 s of the end-to-end time).
+    // input is read (creating a CUDA context takes 1-3 s on these boxes, most of
+    // the end-to-end time; tools/cuda_init_probe.cpp).
     rxg_heap* h = nullptr;
     int made = RXG_OK;
     std::string made_err;
