@@ -310,3 +310,37 @@ def test_short_lines_results_every_offset(key, chunk):
         assert c == want_c and np.array_equal(r, want_r)
     finally:
         rx.set_option("RXG_LINE_CHUNK", None)
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_per_line_results_tma_vs_generic_random_mixes(seed):
+    """Per-line results of the TMA line kernel (range-local bits, per-tile
+    totals, the bit-array scatter with 16-byte stores) against the generic
+    kernel (RXG_NO_LT), on buffers mixing empty, short and long lines, at
+    sizes that leave ragged remainders and groups with > 64 lines per range."""
+    import torch
+
+    rng = np.random.default_rng(seed)
+    pat = "(a|b)*a(a|b)"
+    m = rx.Matcher(pat, device=0)
+    for size in (1, 31, 4097, 65_537, 1 << 20, (3 << 20) + 5, (24 << 20) + 11):
+        mode = rng.integers(0, 3)
+        if mode == 0:      # short lines (many lines per range: the per-range fallback)
+            w = rng.choice(np.frombuffer(b"ab\n", np.uint8), size=size, p=[0.3, 0.3, 0.4])
+        elif mode == 1:    # ~100-byte lines
+            w = rng.choice(np.frombuffer(b"ab\n", np.uint8), size=size, p=[0.495, 0.495, 0.01])
+        else:              # long lines with bursts of empty ones
+            w = rng.choice(np.frombuffer(b"ab\n", np.uint8), size=size, p=[0.4985, 0.4985, 0.003])
+            k = int(rng.integers(0, max(1, size - 200)))
+            w[k:k + 150] = 10
+        w = np.ascontiguousarray(w.astype(np.uint8))
+        c1, r1 = m.match_batch(w, 10, results=True)
+        rx.set_option("RXG_NO_LT", 1)
+        try:
+            m2 = rx.Matcher(pat, device=0)
+            c2, r2 = m2.match_batch(w, 10, results=True)
+        finally:
+            rx.set_option("RXG_NO_LT", None)
+        assert c1 == c2 == int(r1.sum()), (seed, size, mode)
+        assert np.array_equal(r1, r2), (seed, size, mode, int(np.argmax(r1 != r2)))
+        torch.cuda.synchronize()
