@@ -322,7 +322,7 @@ struct PernodeArgs {
     uint32_t lookback;         // bytes walked from E0 before a segment to guess its entry set
     uint32_t* entry;           // n_segs x W: the entry set each segment last walked from
     uint32_t* exits;           // 2 x n_segs x W: exit sets (double-buffered across repair rounds)
-    unsigned int* changed;     // 2 counters (zero when idle)
+    unsigned int* changed;     // 3 rotating round counters (zero when idle)
 };
 
 // One lockstep step of the warp-wide bitset. DENSE: <= 32 residual rows,
@@ -529,10 +529,17 @@ __global__ void __launch_bounds__(32) k_pernode(const __grid_constant__ PernodeA
         cg::grid_group grid = cg::this_grid();
         __threadfence();
         grid.sync();
+        // Round r counts its re-walked segments in changed[r % 3]; every block
+        // reads that counter after the round's grid sync. Block 0 zeroes the
+        // next round's counter during round r: its last use (round r - 2) was
+        // read by every block before they passed round r - 1's sync. (With
+        // two counters the reset raced with slow readers of the current one:
+        // a block could see 0 and leave while the others waited at the next
+        // sync.)
         for (int r = 0;; ++r) {
             const uint32_t* prev = a.exits + static_cast<size_t>(r & 1) * a.n_segs * sw;
             uint32_t* next = a.exits + static_cast<size_t>((r + 1) & 1) * a.n_segs * sw;
-            if (s == 0 && lane == 0) a.changed[(r + 1) & 1] = 0;
+            if (s == 0 && lane == 0) a.changed[(r + 1) % 3] = 0;
             bool diff = false;
             if (s > 0)
                 for (int w = lane; w < W; w += 32) diff |= __ldcg(prev + (s - 1) * sw + w) != __ldcg(a.entry + s * sw + w);
@@ -541,13 +548,13 @@ __global__ void __launch_bounds__(32) k_pernode(const __grid_constant__ PernodeA
                 put(a.entry + s * sw);
                 walk(lo, hi);
                 put(next + s * sw);
-                if (lane == 0) atomicAdd(&a.changed[r & 1], 1u);
+                if (lane == 0) atomicAdd(&a.changed[r % 3], 1u);
             } else {
                 for (int w = lane; w < W; w += 32) next[s * sw + w] = __ldcg(prev + s * sw + w);
             }
             __threadfence();
             grid.sync();
-            if (*reinterpret_cast<volatile unsigned int*>(&a.changed[r & 1]) == 0) {
+            if (*reinterpret_cast<volatile unsigned int*>(&a.changed[r % 3]) == 0) {
                 if (s == a.n_segs - 1) {
                     get(next + s * sw);
                     uint32_t acc = 0;
@@ -557,7 +564,7 @@ __global__ void __launch_bounds__(32) k_pernode(const __grid_constant__ PernodeA
                     acc = __reduce_or_sync(0xFFFFFFFFu, acc);
                     if (lane == 0) {
                         *a.accept = static_cast<int32_t>(acc);
-                        a.changed[r & 1] = 0;
+                        a.changed[(r + 2) % 3] = 0;   // the previous round's (all blocks read it before this sync)
                     }
                 }
                 return;

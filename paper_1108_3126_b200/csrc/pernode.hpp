@@ -47,8 +47,8 @@ cudaError_t launch_par(const RoundsTables& t, long long* c, long long* n, uint32
                        uint32_t symbol, int32_t single, unsigned long long* launches, cudaStream_t st);
 
 // Segmented K1 (long strings across SMs): device scratch for up to
-// max_segs segments of W words (pernode_seg_scratch_bytes), changed = 2
-// zeroed counters (zero again when the launch completes).
+// max_segs segments of W words (pernode_seg_scratch_bytes), changed = 3
+// zeroed round counters (16 bytes; zero again when the launch completes).
 struct PernodeSegScratch {
     uint32_t* entry = nullptr;     // max_segs x W
     uint32_t* exits = nullptr;     // 2 x max_segs x W
